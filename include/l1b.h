@@ -1,0 +1,245 @@
+/*
+ * l1b.h -- C ABI of the B200-native l1-least-squares hot path
+ *          (min_x tau*||x||_1 + 1/2*||A x - b||^2, arXiv 1503.03520).
+ *
+ * Plain C: plain pointers, sizes and status codes; no torch or C++ types.
+ * Implemented by libl1b.so (paper_1503_03520_b200/lib/), CUDA sm_100a only --
+ * there is no CPU path behind any of these entry points.
+ *
+ * Each group below names the reference interface it replaces (paths relative
+ * to /root/reference/proj).  The reference's C++ API throws; this ABI returns
+ * a status code and keeps the exception text in l1b_last_error() (thread
+ * local), so a host shim can rethrow the same exception type with the same
+ * message:
+ *   L1B_EINVAL  -> std::invalid_argument   (linops.cpp:13-18, solvers.cpp:133-143)
+ *   L1B_ERUNTIME-> std::runtime_error      (solvers.cpp:36-40, 233, 244; linops.cpp:481)
+ *   L1B_ELOGIC  -> std::logic_error        (linops.cpp:418-420)
+ *   L1B_ECUDA / L1B_ENOMEM / L1B_ENCCL     -> device failures (no reference analogue)
+ *
+ * Ownership: every device buffer inside an l1b_problem belongs to the library;
+ * host buffers passed in are read during the call only; host output buffers
+ * belong to the caller.  Device-pointer arguments (d_*) must live on the
+ * problem's device; work is ordered on the problem's stream
+ * (l1b_problem_stream), calls that return host data synchronise it.
+ */
+#ifndef L1B_H
+#define L1B_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define L1B_ABI_VERSION 1
+
+enum l1b_status {
+  L1B_OK = 0,
+  L1B_EINVAL = 1,
+  L1B_ERUNTIME = 2,
+  L1B_ELOGIC = 3,
+  L1B_ECUDA = 4,
+  L1B_ENOMEM = 5,
+  L1B_EUNSUPPORTED = 6,
+  L1B_ENCCL = 7
+};
+
+int l1b_abi_version(void);
+const char* l1b_last_error(void);
+
+/* ------------------------------------------------------------------------ */
+/* Host-side generator primitives (bit-exact std::mt19937_64 streams).
+ * Replace: rng.hpp:19-45 (mix_seed, uniform_*), Permutation::realize
+ * (linops.cpp:224-239), Spectrum::realize (linops.cpp:320-336),
+ * uniform_sparse_solution (solution.cpp:47-75).                             */
+uint64_t l1b_mix_seed(uint64_t seed, uint64_t salt);
+int l1b_realize_permutation(uint64_t n, uint64_t seed, uint32_t* map_out);
+int l1b_realize_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
+                                 double* sigma_out);
+/* Returns s through *s_out; support (ascending) and values need capacity s. */
+int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
+                                uint32_t* support_out, double* values_out);
+
+/* ------------------------------------------------------------------------ */
+/* Problem = device-resident instance: operator (sweep description + CSR/CSC
+ * materialised on device) + b + tau + planted x*.
+ * Replaces: OperatorSpec (linops.hpp:159-206) + finalize (linops.cpp:394-416),
+ * ProblemInstance (instance.hpp:36-52), generate_instance (instance.cpp:53-89),
+ * build_instance (bench.cpp:253-316).                                         */
+typedef struct l1b_problem l1b_problem;
+
+typedef struct {
+  uint64_t m, n;
+  uint32_t n_right;            /* right stages, in OperatorSpec::right_stages order */
+  const int32_t* right_offset; /* 0 or 1 (paired stages only) */
+  const double* right_theta;
+  uint32_t n_left;
+  const int32_t* left_offset;
+  const double* left_theta;
+  const uint32_t* p1;          /* m-entry map (Pv)[i] = v[map[i]]; NULL = identity */
+  const uint32_t* p2;
+  const double* sigma;         /* n realised singular values, all > 0 */
+} l1b_operator_desc;
+
+enum { L1B_SPECTRUM_UNIFORM_Q = 0, L1B_SPECTRUM_ALTERNATING = 1, L1B_SPECTRUM_EXPLICIT = 2 };
+
+/* ExperimentConfig + InstanceJob for one job (bench.hpp:16-97). */
+typedef struct {
+  uint64_t n;
+  double m_ratio;            /* m = llround(m_ratio * n), >= 1 */
+  uint32_t stages;           /* right stages, offsets (stages-1-i)%2 */
+  uint32_t left_stages;
+  int permute;               /* seeded P1, P2 */
+  int spectrum_kind;
+  int q;                     /* uniform: draws in (0, 10^q], + shift */
+  double shift;
+  double odd_value, even_value;
+  const double* sigma_explicit; /* L1B_SPECTRUM_EXPLICIT: n values */
+  double gamma;              /* OsGen value bound */
+  uint64_t s_divisor;        /* s = max(1, n / s_divisor) */
+  double tau;
+  double theta;
+  uint64_t seed;             /* ExperimentConfig::seed */
+  uint64_t job_index;        /* job.seed = mix_seed(seed, job_index) (bench.cpp:237) */
+  double fill_bound;         /* FillPolicy::interior bound, 0.9 */
+} l1b_gen_desc;
+
+/* Shard = contiguous block of A's nonempty rows [row_begin, row_end) of a
+ * banded instance (identity P1/P2, no left stages: |col - row| <= #stages),
+ * holding the matching column block [row_begin, row_end) of A^T.  Local
+ * vectors carry `halo` = #stages entries on each side.  NULL shard = the whole
+ * operator on one device.  row_end == 0 selects the default even split of
+ * [0, n) for (rank, world).                                                  */
+typedef struct {
+  int rank, world;
+  uint64_t row_begin, row_end;
+} l1b_shard_desc;
+
+int l1b_generate(int device, const l1b_gen_desc* gen, const l1b_shard_desc* shard,
+                 l1b_problem** out);
+int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, const double* b_host,
+                       const uint32_t* xstar_support, const double* xstar_values, uint64_t s,
+                       l1b_problem** out);
+int l1b_problem_free(l1b_problem* p);
+
+typedef struct {
+  uint64_t m, n;
+  uint64_t m_active;      /* rows [m_active, m) of A are structurally empty */
+  uint64_t nnz;           /* nnz(A) (this shard) */
+  uint64_t s;             /* |supp x*| */
+  double tau, noise_norm, cert_kappa, gram_lmax, f_star;
+  uint64_t device_bytes;  /* HBM held by the problem */
+  uint64_t row_begin, row_end, col_begin, col_end; /* shard ranges */
+  int csr_lanes, csc_lanes; /* lanes per row / per column in the SpMV kernels */
+} l1b_problem_info;
+
+int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* out);
+int l1b_problem_get_b(const l1b_problem* p, double* b_host);          /* m */
+int l1b_problem_get_sigma(const l1b_problem* p, double* sigma_host);  /* n */
+int l1b_problem_get_xstar(const l1b_problem* p, uint32_t* support, double* values);
+void* l1b_problem_stream(const l1b_problem* p);  /* cudaStream_t */
+int l1b_problem_set_stream(l1b_problem* p, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Operator products on device vectors.
+ * Replace: LinearOperator::apply / apply_transpose (linops.hpp:139-155;
+ * OperatorSpec::apply linops.cpp:422-446, apply_transpose :448-473),
+ * apply_gram_inverse (:475-490), gram_diagonal (:533-558), row/column
+ * (:566-619) via the exported CSR/CSC.                                      */
+enum { L1B_PATH_SPARSE = 0, /* CSR (A) / CSC (A^T) SpMV kernels */
+       L1B_PATH_SWEEP = 1   /* matrix-free Givens stage sweeps, bit-exact vs the reference */ };
+
+int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y);
+int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x);
+int l1b_gram_inverse(l1b_problem* p, const double* d_v, double* d_out);
+int l1b_gram_diagonal(l1b_problem* p, double* d_out);
+/* host buffers: row_ptr[m+1] (rows >= m_active are empty), col[nnz], val[nnz] */
+int l1b_export_csr(const l1b_problem* p, uint64_t* row_ptr, uint32_t* col, double* val);
+int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, double* val);
+
+/* tau*||x||_1 + 1/2*||A x - b||^2 (solvers.cpp:145-151). */
+int l1b_objective(l1b_problem* p, const double* d_x, double* f_out);
+
+typedef struct {
+  double max_support_violation;
+  double max_offsupport_violation;
+  double threshold;
+  int pass;
+} l1b_cert;
+/* verify_optimality (instance.cpp:175-202) */
+int l1b_verify_optimality(l1b_problem* p, double tol, l1b_cert* out);
+
+/* ------------------------------------------------------------------------ */
+/* Solvers.  Replace run_solver / fista_run / ista_run / coordinate_descent_run
+ * / newton_cg_run (solvers.hpp:106-117); the block-PCDM solver is the C2
+ * mapping.                                                  */
+enum { L1B_ISTA = 0, L1B_FISTA = 1, L1B_CD = 2, L1B_NEWTON_CG = 3, L1B_PCDM = 4 };
+enum { L1B_TARGET_REACHED = 0, L1B_ITER_BUDGET = 1, L1B_TIME_BUDGET = 2 };
+
+/* SolverConfig (solvers.hpp:17-41) */
+typedef struct {
+  int solver;
+  uint64_t max_iters;
+  double max_seconds;
+  int has_target;
+  double target;
+  double mu, eta;
+  uint64_t pcg_max_iters, ls_max_backtracks;
+  double grad_tol_rel;
+  double l_fixed;      /* > 0 pins L; else L = sigma_max^2 (LPolicy::spectrum) */
+  uint64_t varpi;      /* cd: modelled processors */
+  uint64_t omega;      /* cd/pcdm: 0 = measure max row nnz */
+  uint64_t seed;
+  uint64_t block;      /* pcdm: coordinates per block */
+} l1b_solver_cfg;
+
+void l1b_solver_cfg_default(l1b_solver_cfg* cfg);
+
+/* TraceSample (solvers.hpp:45-52) */
+typedef struct {
+  uint64_t iter;
+  double elapsed_s;
+  double objective;
+  uint64_t nnz;
+  double matvecs;
+  uint64_t extra;
+} l1b_sample;
+
+/* SolverTrace scalars (solvers.hpp:54-66) */
+typedef struct {
+  int status;
+  int reached_target;
+  double final_objective;
+  double elapsed_s;
+  double total_matvecs;
+  uint64_t total_pcg_iterations;
+  uint64_t newton_steps;
+  double time_to_target;
+  double matvecs_to_target;
+  uint64_t n_samples;        /* samples produced (may exceed cap; first cap written) */
+  uint64_t iterations;       /* iterations / sweeps / Newton steps executed */
+} l1b_summary;
+
+int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+              l1b_summary* summary, double* x_host, double* d_x);
+
+/* Stepping session over the device-resident loop (bench / profiling):
+ * begin -> step(k) (asynchronous) -> ... -> end.  FISTA / ISTA only.        */
+typedef struct l1b_session l1b_session;
+int l1b_session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session** out);
+int l1b_session_step(l1b_session* s, uint64_t iters);
+/* Runs iters iterations with CUDA events around each kernel on the problem's
+ * stream; ms_out[k] = total milliseconds of kernel k over those iterations
+ * (k = 0: A^T r + prox/momentum, 1: A x - b + residual momentum).           */
+int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms);
+int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations);
+int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
+                    double* x_host);
+/* Kernel launches issued by the library since load (all entry points). */
+uint64_t l1b_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* L1B_H */

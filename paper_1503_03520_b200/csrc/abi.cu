@@ -1,0 +1,697 @@
+// abi.cu -- the C ABI of include/l1b.h: object lifetimes, the host half of the
+// generator (sequential std::mt19937_64 streams), operator materialisation and
+// the solver drivers that enqueue the device-resident loops.
+//
+// The host side only orchestrates: every arithmetic pass over an n- or
+// m-vector runs in the kernels of k_*.cu.  The only host arithmetic is the
+// RNG streams (inherently sequential: rng.hpp:14-56), cos/sin of the stage
+// angles (so they come from the same libm as the reference, linops.cpp:84-85)
+// and O(1) scalars.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/l1b.h"
+#include "common.cuh"
+#include "kernels.hpp"
+#include "guard.hpp"
+#include "solvers.hpp"
+
+namespace l1b {
+
+std::atomic<uint64_t> g_launch_count{0};
+
+std::string& last_error_slot() {
+  static thread_local std::string slot;
+  return slot;
+}
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  const std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                          std::to_string(line) + ")";
+  if (e == cudaErrorMemoryAllocation) throw OutOfMemory(msg);
+  throw CudaError(msg);
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    L1B_CUDA(cudaGetDevice(&dev));
+    L1B_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+int grid_for(uint64_t work, int threads, int max_blocks_per_sm) {
+  const uint64_t blocks = (work + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)max_blocks_per_sm * sm_count();
+  return (int)std::max<uint64_t>(1, std::min(blocks, cap));
+}
+
+// ---------------------------------------------------------------------------
+// host RNG helpers -- same streams as rng.hpp:14-56
+namespace hostrng {
+using Rng = std::mt19937_64;
+
+uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (salt + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+inline double unit(Rng& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
+inline double in(Rng& r, double lo, double hi) { return lo + (hi - lo) * unit(r); }
+inline uint64_t index(Rng& r, uint64_t n) {
+  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  uint64_t x;
+  do {
+    x = r();
+  } while (x >= lim);
+  return x % n;
+}
+
+void permutation(uint64_t n, uint64_t seed, uint32_t* map) {  // linops.cpp:224-234
+  for (uint64_t i = 0; i < n; ++i) map[i] = (uint32_t)i;
+  Rng r(seed);
+  for (uint64_t i = n; i > 1; --i) std::swap(map[i - 1], map[index(r, i)]);
+}
+
+void spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
+                      double* out) {  // linops.cpp:323-331
+  Rng r(seed);
+  for (uint64_t i = 0; i < n; ++i) {
+    double u;
+    do {
+      u = in(r, lo, hi);
+    } while (u <= lo);
+    out[i] = u + shift;
+  }
+}
+
+void sparse_solution(uint64_t n, uint64_t s, double gamma, Rng& r, std::vector<uint32_t>& sup,
+                     std::vector<double>& val) {  // solution.cpp:47-75
+  sup.clear();
+  val.clear();
+  if (s == 0) return;
+  std::unordered_set<uint64_t> chosen;
+  chosen.reserve(s * 2);
+  for (uint64_t j = n - s; j < n; ++j) {
+    const uint64_t t = index(r, j + 1);
+    if (!chosen.insert(t).second) chosen.insert(j);
+  }
+  sup.assign(chosen.begin(), chosen.end());
+  std::sort(sup.begin(), sup.end());
+  val.reserve(s);
+  for (uint64_t k = 0; k < s; ++k) {
+    double v;
+    do {
+      v = in(r, -gamma, gamma);
+    } while (v == 0.0);
+    val.push_back(v);
+  }
+}
+}  // namespace hostrng
+
+}  // namespace l1b
+
+// ===========================================================================
+using namespace l1b;
+
+namespace {
+
+template <class T>
+T* dev_alloc(size_t count, size_t* bytes_acc) {
+  T* p = nullptr;
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  L1B_CUDA(cudaMalloc(&p, bytes));
+  if (bytes_acc) *bytes_acc += bytes;
+  return p;
+}
+
+template <class T>
+T* upload(const T* host, size_t count, cudaStream_t st, size_t* bytes_acc) {
+  T* p = dev_alloc<T>(count, bytes_acc);
+  if (count) L1B_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return p;
+}
+
+uint64_t pow2_ceil_lanes(double mean) {
+  uint64_t g = 1;
+  while ((double)g < mean && g < 32) g <<= 1;
+  return g;
+}
+
+}  // namespace
+
+struct l1b_problem {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  uint64_t m = 0, n = 0;
+  double tau = 1.0;
+  std::vector<int32_t> r_off, l_off;
+  std::vector<double> r_theta, l_theta;
+  OpView view;
+  double* d_sigma = nullptr;
+  uint32_t *d_p1 = nullptr, *d_p2 = nullptr, *d_p1inv = nullptr, *d_p2inv = nullptr;
+  double* d_b = nullptr;
+  double* d_gram = nullptr;
+  std::vector<uint32_t> xs_sup;
+  std::vector<double> xs_val;
+  double noise_norm = 0.0, cert_kappa = 1.0, lmax = 0.0;
+  LinesOut csr, csc;
+  double tail_sq = 0.0;
+  size_t device_bytes = 0;
+  uint64_t row_begin = 0, row_end = 0;
+
+  ~l1b_problem() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv,
+                    (void*)d_b, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
+                    (void*)csc.idx, (void*)csc.val})
+      if (p) cudaFree(p);
+    if (stream && own_stream) cudaStreamDestroy(stream);
+  }
+
+  Csr rows() const {
+    Csr c;
+    c.lines = csr.lines;
+    c.nnz = csr.nnz;
+    c.ptr32 = csr.ptr32;
+    c.ptr = csr.ptr;
+    c.idx = csr.idx;
+    c.val = csr.val;
+    c.lanes = (int)pow2_ceil_lanes(csr.lines ? (double)csr.nnz / (double)csr.lines : 1.0);
+    return c;
+  }
+  Csr cols() const {
+    Csr c;
+    c.lines = csc.lines;
+    c.nnz = csc.nnz;
+    c.ptr32 = csc.ptr32;
+    c.ptr = csc.ptr;
+    c.idx = csc.idx;
+    c.val = csc.val;
+    c.lanes = (int)pow2_ceil_lanes(csc.lines ? (double)csc.nnz / (double)csc.lines : 1.0);
+    return c;
+  }
+};
+
+namespace {
+
+void fill_stage_tab(StageTab& tab, const std::vector<int32_t>& off, const std::vector<double>& th) {
+  if (off.size() > (size_t)kMaxStages)
+    throw Unsupported("at most " + std::to_string(kMaxStages) + " stages per side are supported");
+  tab.count = (int)off.size();
+  for (size_t k = 0; k < off.size(); ++k) {
+    tab.offset[k] = off[k];
+    tab.c[k] = std::cos(th[k]);
+    tab.s[k] = std::sin(th[k]);
+  }
+}
+
+std::vector<uint32_t> inverse_map(const uint32_t* map, uint64_t m) {
+  std::vector<uint32_t> inv(m);
+  std::vector<uint8_t> seen(m, 0);
+  for (uint64_t i = 0; i < m; ++i) {
+    if (map[i] >= m || seen[map[i]])
+      throw InvalidArgument("Permutation: mapping is not a bijection");
+    seen[map[i]] = 1;
+    inv[map[i]] = (uint32_t)i;
+  }
+  return inv;
+}
+
+// Validation of OperatorSpec::finalize (linops.cpp:394-416) + device upload
+// of the description.  sigma/p1/p2 are host arrays.
+void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
+                    std::vector<int32_t> r_off, std::vector<double> r_th,
+                    std::vector<int32_t> l_off, std::vector<double> l_th, const uint32_t* p1,
+                    const uint32_t* p2, const double* sigma) {
+  if (m == 0 || n == 0) throw InvalidArgument("OperatorSpec: dimensions must be positive");
+  if (m < n) throw InvalidArgument("OperatorSpec: requires m >= n");
+  if (m > (1ull << 32)) throw InvalidArgument("OperatorSpec: m above 2^32 exceeds uint32 indices");
+  for (int32_t o : r_off)
+    if (o != 0 && o != 1) throw InvalidArgument("RotationStage: offset must be 0 or 1");
+  for (int32_t o : l_off)
+    if (o != 0 && o != 1) throw InvalidArgument("RotationStage: offset must be 0 or 1");
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(sigma[i] > 0.0) || !std::isfinite(sigma[i]))
+      throw std::runtime_error("Spectrum: all singular values must be strictly positive");
+  p->device = device;
+  L1B_CUDA(cudaSetDevice(device));
+  L1B_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  p->m = m;
+  p->n = n;
+  p->r_off = std::move(r_off);
+  p->r_theta = std::move(r_th);
+  p->l_off = std::move(l_off);
+  p->l_theta = std::move(l_th);
+  fill_stage_tab(p->view.right, p->r_off, p->r_theta);
+  fill_stage_tab(p->view.left, p->l_off, p->l_theta);
+  cudaStream_t st = p->stream;
+  p->d_sigma = upload(sigma, n, st, &p->device_bytes);
+  if (p1) {
+    auto inv = inverse_map(p1, m);
+    p->d_p1 = upload(p1, m, st, &p->device_bytes);
+    p->d_p1inv = upload(inv.data(), m, st, &p->device_bytes);
+  }
+  if (p2) {
+    auto inv = inverse_map(p2, m);
+    p->d_p2 = upload(p2, m, st, &p->device_bytes);
+    p->d_p2inv = upload(inv.data(), m, st, &p->device_bytes);
+  }
+  p->view.m = m;
+  p->view.n = n;
+  p->view.sigma = p->d_sigma;
+  p->view.p1 = p->d_p1;
+  p->view.p2 = p->d_p2;
+  p->view.p1_inv = p->d_p1inv;
+  p->view.p2_inv = p->d_p2inv;
+  double smax = sigma[0], smin = sigma[0];
+  for (uint64_t i = 1; i < n; ++i) {
+    smax = std::max(smax, sigma[i]);
+    smin = std::min(smin, sigma[i]);
+  }
+  p->lmax = smax * smax;                                     // gram_lmax (linops.cpp:560-564)
+  p->cert_kappa = (smax / smin) * (smax / smin);             // solution.cpp:127-133
+  L1B_CUDA(cudaStreamSynchronize(st));
+}
+
+// CSR (rows, trailing empty rows trimmed) + CSC of A, and the constant
+// 1/2*||b_tail||^2 part of every objective.
+void materialise(l1b_problem* p) {
+  build_lines(p->view, true, 0, p->m, 0, true, p->stream, &p->csr);
+  p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
+  build_lines(p->view, false, 0, p->n, 0, false, p->stream, &p->csc);
+  p->device_bytes += (p->csc.lines + 1) * (p->csc.ptr32 ? 4 : 8) + p->csc.nnz * 12;
+  p->row_begin = 0;
+  p->row_end = p->csr.lines;
+  p->tail_sq = 0.0;
+  if (p->csr.lines < p->m) {
+    std::vector<double> tail(p->m - p->csr.lines);
+    L1B_CUDA(cudaMemcpyAsync(tail.data(), p->d_b + p->csr.lines, tail.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+    for (double v : tail) p->tail_sq += v * v;
+  }
+}
+
+void check_problem(const l1b_problem* p) {
+  if (!p) throw InvalidArgument("null problem");
+  L1B_CUDA(cudaSetDevice(p->device));
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int l1b_abi_version(void) { return L1B_ABI_VERSION; }
+const char* l1b_last_error(void) { return last_error_slot().c_str(); }
+uint64_t l1b_launch_count(void) { return g_launch_count.load(); }
+
+uint64_t l1b_mix_seed(uint64_t seed, uint64_t salt) { return hostrng::mix_seed(seed, salt); }
+
+int l1b_realize_permutation(uint64_t n, uint64_t seed, uint32_t* map_out) {
+  return guard([&] {
+    if (!map_out) throw InvalidArgument("null output");
+    hostrng::permutation(n, seed, map_out);
+  });
+}
+
+int l1b_realize_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
+                                 double* sigma_out) {
+  return guard([&] { hostrng::spectrum_uniform(n, lo, hi, shift, seed, sigma_out); });
+}
+
+int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
+                                uint32_t* support_out, double* values_out) {
+  return guard([&] {
+    if (s > n) throw InvalidArgument("uniform_sparse_solution: s must not exceed n");
+    if (!(gamma > 0.0)) throw InvalidArgument("uniform_sparse_solution: gamma must be positive");
+    hostrng::Rng r(rng_seed);
+    std::vector<uint32_t> sup;
+    std::vector<double> val;
+    hostrng::sparse_solution(n, s, gamma, r, sup, val);
+    std::copy(sup.begin(), sup.end(), support_out);
+    std::copy(val.begin(), val.end(), values_out);
+  });
+}
+
+// build_instance (bench.cpp:253-316) + generate_instance (instance.cpp:53-89).
+int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard, l1b_problem** out) {
+  return guard([&] {
+    if (!g || !out) throw InvalidArgument("null argument");
+    *out = nullptr;
+    if (shard && shard->world > 1)
+      throw Unsupported("l1b_generate: sharded problems are built by l1b_generate_shard");
+    if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
+    if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
+    if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
+    if (!(g->tau > 0.0)) throw InvalidArgument("generate_instance: tau must be positive");
+    if (!(g->fill_bound >= 0.0 && g->fill_bound < 1.0))
+      throw InvalidArgument("FillPolicy: interior bound must lie in [0, 1)");
+    const uint64_t n = g->n;
+    const uint64_t m = (uint64_t)std::llround(g->m_ratio * (double)n);
+    const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
+    std::vector<int32_t> r_off, l_off;
+    for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
+    for (uint32_t i = 0; i < g->left_stages; ++i)
+      l_off.push_back((int32_t)((g->left_stages - 1 - i) % 2));
+    std::vector<uint32_t> p1, p2;
+    if (g->permute) {
+      if (m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
+      p1.resize(m);
+      p2.resize(m);
+      hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data());
+      hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data());
+    }
+    std::vector<double> sigma(n);
+    if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+      hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
+                                hostrng::mix_seed(job_seed, 3), sigma.data());
+    } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+      for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+    } else if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT) {
+      if (!g->sigma_explicit) throw InvalidArgument("explicit spectrum without values");
+      std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+    } else {
+      throw InvalidArgument("unknown spectrum kind");
+    }
+    auto p = std::make_unique<l1b_problem>();
+    setup_operator(p.get(), device, m, n, r_off, std::vector<double>(g->stages, g->theta), l_off,
+                   std::vector<double>(g->left_stages, g->theta), g->permute ? p1.data() : nullptr,
+                   g->permute ? p2.data() : nullptr, sigma.data());
+    p->tau = g->tau;
+    // planted solution (Rng(mix_seed(job.seed, 4)), bench.cpp:281-301)
+    const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
+    {
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+      hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
+    }
+    // subgradient g (instance.cpp:28-42), Rng(mix_seed(job.seed, 5))
+    std::vector<double> gv(n);
+    {
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+      for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
+      for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+    }
+    cudaStream_t st = p->stream;
+    // device: w = G (S^T S)^-1 G^T g; e = tau A w; b = A x* + e (instance.cpp:64-79)
+    double *d_g = nullptr, *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;
+    uint32_t* d_sup = nullptr;
+    double* d_val = nullptr;
+    d_g = upload(gv.data(), n, st, nullptr);
+    L1B_CUDA(cudaMalloc(&d_e, m * sizeof(double)));
+    L1B_CUDA(cudaMalloc(&d_x, n * sizeof(double)));
+    L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
+    p->d_b = dev_alloc<double>(m, &p->device_bytes);
+    d_sup = upload(p->xs_sup.data(), s, st, nullptr);
+    d_val = upload(p->xs_val.data(), s, st, nullptr);
+    sweep_gram_inverse(p->view, d_g, d_g, st);
+    sweep_apply(p->view, d_g, d_e, st);
+    scatter_sparse(d_sup, d_val, s, d_x, n, st);
+    sweep_apply(p->view, d_x, p->d_b, st);
+    generator_combine(p->tau, d_e, p->d_b, m, d_ss, st);
+    double ss = 0.0;
+    L1B_CUDA(cudaMemcpyAsync(&ss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    p->noise_norm = std::sqrt(ss);
+    for (void* q : {(void*)d_g, (void*)d_e, (void*)d_x, (void*)d_ss, (void*)d_sup, (void*)d_val})
+      cudaFree(q);
+    materialise(p.get());
+    *out = p.release();
+  });
+}
+
+int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, const double* b_host,
+                       const uint32_t* xs_support, const double* xs_values, uint64_t s,
+                       l1b_problem** out) {
+  return guard([&] {
+    if (!op || !out || !b_host || !op->sigma) throw InvalidArgument("null argument");
+    *out = nullptr;
+    if (!(tau > 0.0)) throw InvalidArgument("generate_instance: tau must be positive");
+    auto p = std::make_unique<l1b_problem>();
+    std::vector<int32_t> ro(op->right_offset, op->right_offset + op->n_right);
+    std::vector<double> rt(op->right_theta, op->right_theta + op->n_right);
+    std::vector<int32_t> lo(op->left_offset, op->left_offset + op->n_left);
+    std::vector<double> lt(op->left_theta, op->left_theta + op->n_left);
+    setup_operator(p.get(), device, op->m, op->n, ro, rt, lo, lt, op->p1, op->p2, op->sigma);
+    p->tau = tau;
+    if (s) {
+      if (!xs_support || !xs_values) throw InvalidArgument("null x* arrays");
+      p->xs_sup.assign(xs_support, xs_support + s);
+      p->xs_val.assign(xs_values, xs_values + s);
+      for (uint64_t k = 0; k < s; ++k) {
+        if (p->xs_sup[k] >= op->n) throw InvalidArgument("SparseSolution: index out of range");
+        if (k && p->xs_sup[k] <= p->xs_sup[k - 1])
+          throw InvalidArgument("SparseSolution: support must be strictly increasing");
+        if (p->xs_val[k] == 0.0) throw InvalidArgument("SparseSolution: stored values must be nonzero");
+      }
+    }
+    p->d_b = upload(b_host, op->m, p->stream, &p->device_bytes);
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+    materialise(p.get());
+    *out = p.release();
+  });
+}
+
+int l1b_problem_free(l1b_problem* p) {
+  return guard([&] { delete p; });
+}
+
+int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
+  return guard([&] {
+    if (!p || !o) throw InvalidArgument("null argument");
+    o->m = p->m;
+    o->n = p->n;
+    o->m_active = p->csr.lines;
+    o->nnz = p->csr.nnz;
+    o->s = p->xs_sup.size();
+    o->tau = p->tau;
+    o->noise_norm = p->noise_norm;
+    o->cert_kappa = p->cert_kappa;
+    o->gram_lmax = p->lmax;
+    double l1 = 0.0;
+    for (double v : p->xs_val) l1 += std::abs(v);
+    o->f_star = p->tau * l1 + 0.5 * p->noise_norm * p->noise_norm;  // instance.cpp:49-51
+    o->device_bytes = p->device_bytes;
+    o->row_begin = p->row_begin;
+    o->row_end = p->row_end;
+    o->col_begin = 0;
+    o->col_end = p->n;
+    o->csr_lanes = p->rows().lanes;
+    o->csc_lanes = p->cols().lanes;
+  });
+}
+
+int l1b_problem_get_b(const l1b_problem* p, double* b) {
+  return guard([&] {
+    check_problem(p);
+    L1B_CUDA(cudaMemcpyAsync(b, p->d_b, p->m * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int l1b_problem_get_sigma(const l1b_problem* p, double* s) {
+  return guard([&] {
+    check_problem(p);
+    L1B_CUDA(cudaMemcpyAsync(s, p->d_sigma, p->n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int l1b_problem_get_xstar(const l1b_problem* p, uint32_t* support, double* values) {
+  return guard([&] {
+    if (!p) throw InvalidArgument("null problem");
+    std::copy(p->xs_sup.begin(), p->xs_sup.end(), support);
+    std::copy(p->xs_val.begin(), p->xs_val.end(), values);
+  });
+}
+
+void* l1b_problem_stream(const l1b_problem* p) { return p ? (void*)p->stream : nullptr; }
+
+int l1b_problem_set_stream(l1b_problem* p, void* stream) {
+  return guard([&] {
+    check_problem(p);
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+    if (p->own_stream) L1B_CUDA(cudaStreamDestroy(p->stream));
+    p->stream = (cudaStream_t)stream;
+    p->own_stream = false;
+  });
+}
+
+int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
+  return guard([&] {
+    check_problem(p);
+    if (path == L1B_PATH_SWEEP) {
+      sweep_apply(p->view, d_x, d_y, p->stream);
+    } else {
+      spmv(p->rows(), d_x, d_y, p->stream);
+      if (p->csr.lines < p->m)
+        L1B_CUDA(cudaMemsetAsync(d_y + p->csr.lines, 0, (p->m - p->csr.lines) * sizeof(double),
+                                 p->stream));
+    }
+  });
+}
+
+int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x) {
+  return guard([&] {
+    check_problem(p);
+    if (path == L1B_PATH_SWEEP)
+      sweep_apply_transpose(p->view, d_y, d_x, p->stream);
+    else
+      spmv(p->cols(), d_y, d_x, p->stream);
+  });
+}
+
+int l1b_gram_inverse(l1b_problem* p, const double* d_v, double* d_out) {
+  return guard([&] {
+    check_problem(p);
+    sweep_gram_inverse(p->view, d_v, d_out, p->stream);
+  });
+}
+
+namespace {
+const double* gram_diag_device(l1b_problem* p) {
+  if (!p->d_gram) {
+    p->d_gram = dev_alloc<double>(p->n, &p->device_bytes);
+    gram_diagonal(p->view, 0, p->n, p->d_gram, p->stream);
+  }
+  return p->d_gram;
+}
+}  // namespace
+
+int l1b_gram_diagonal(l1b_problem* p, double* d_out) {
+  return guard([&] {
+    check_problem(p);
+    const double* g = gram_diag_device(p);
+    L1B_CUDA(cudaMemcpyAsync(d_out, g, p->n * sizeof(double), cudaMemcpyDeviceToDevice, p->stream));
+  });
+}
+
+namespace {
+void export_lines(const l1b_problem* p, const LinesOut& L, uint64_t dim, uint64_t* ptr,
+                  uint32_t* idx, double* val) {
+  check_problem(p);
+  std::vector<uint32_t> p32;
+  if (L.ptr32) {
+    p32.resize(L.lines + 1);
+    L1B_CUDA(cudaMemcpyAsync(p32.data(), L.ptr, p32.size() * 4, cudaMemcpyDeviceToHost, p->stream));
+  } else {
+    L1B_CUDA(cudaMemcpyAsync(ptr, L.ptr, (L.lines + 1) * 8, cudaMemcpyDeviceToHost, p->stream));
+  }
+  if (L.nnz) {
+    L1B_CUDA(cudaMemcpyAsync(idx, L.idx, L.nnz * 4, cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaMemcpyAsync(val, L.val, L.nnz * 8, cudaMemcpyDeviceToHost, p->stream));
+  }
+  L1B_CUDA(cudaStreamSynchronize(p->stream));
+  if (L.ptr32)
+    for (uint64_t i = 0; i <= L.lines; ++i) ptr[i] = p32[i];
+  for (uint64_t i = L.lines + 1; i <= dim; ++i) ptr[i] = L.nnz;
+}
+}  // namespace
+
+int l1b_export_csr(const l1b_problem* p, uint64_t* row_ptr, uint32_t* col, double* val) {
+  return guard([&] { export_lines(p, p->csr, p->m, row_ptr, col, val); });
+}
+
+int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, double* val) {
+  return guard([&] { export_lines(p, p->csc, p->n, col_ptr, row, val); });
+}
+
+int l1b_objective(l1b_problem* p, const double* d_x, double* f_out) {
+  return guard([&] {
+    check_problem(p);
+    double* d_f = nullptr;
+    L1B_CUDA(cudaMallocAsync(&d_f, sizeof(double), p->stream));
+    objective(p->rows(), d_x, p->n, p->d_b, p->tau, p->tail_sq, d_f, p->stream);
+    L1B_CUDA(cudaMemcpyAsync(f_out, d_f, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaFreeAsync(d_f, p->stream));
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int l1b_verify_optimality(l1b_problem* p, double tol, l1b_cert* out) {
+  return guard([&] {
+    check_problem(p);
+    cudaStream_t st = p->stream;
+    double *xd = nullptr, *res = nullptr, *r = nullptr, *mx = nullptr;
+    L1B_CUDA(cudaMallocAsync(&xd, p->n * sizeof(double), st));
+    L1B_CUDA(cudaMallocAsync(&res, p->m * sizeof(double), st));
+    L1B_CUDA(cudaMallocAsync(&r, p->n * sizeof(double), st));
+    L1B_CUDA(cudaMallocAsync(&mx, 2 * sizeof(double), st));
+    uint32_t* d_sup = nullptr;
+    double* d_val = nullptr;
+    const uint64_t s = p->xs_sup.size();
+    L1B_CUDA(cudaMallocAsync(&d_sup, std::max<uint64_t>(s, 1) * 4, st));
+    L1B_CUDA(cudaMallocAsync(&d_val, std::max<uint64_t>(s, 1) * 8, st));
+    if (s) {
+      L1B_CUDA(cudaMemcpyAsync(d_sup, p->xs_sup.data(), s * 4, cudaMemcpyHostToDevice, st));
+      L1B_CUDA(cudaMemcpyAsync(d_val, p->xs_val.data(), s * 8, cudaMemcpyHostToDevice, st));
+    }
+    scatter_sparse(d_sup, d_val, s, xd, p->n, st);
+    sweep_apply(p->view, xd, res, st);        // instance.cpp:179
+    vec_sub(res, p->d_b, p->m, st);           // :180
+    sweep_apply_transpose(p->view, res, r, st);  // :182
+    certificate(r, xd, p->tau, p->n, mx, st);
+    double h[2];
+    L1B_CUDA(cudaMemcpyAsync(h, mx, sizeof(h), cudaMemcpyDeviceToHost, st));
+    for (void* q : {(void*)xd, (void*)res, (void*)r, (void*)mx, (void*)d_sup, (void*)d_val})
+      L1B_CUDA(cudaFreeAsync(q, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    out->max_support_violation = h[0];
+    out->max_offsupport_violation = h[1];
+    out->threshold = tol * p->tau;
+    out->pass = h[0] <= out->threshold && h[1] <= out->threshold;
+  });
+}
+
+void l1b_solver_cfg_default(l1b_solver_cfg* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->solver = L1B_FISTA;
+  c->max_iters = 100000;  // solvers.hpp:19-38
+  c->max_seconds = 600.0;
+  c->mu = 1e-5;
+  c->eta = 0.1;
+  c->pcg_max_iters = 1000;
+  c->ls_max_backtracks = 50;
+  c->grad_tol_rel = 1e-8;
+  c->varpi = 1;
+  c->block = 256;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// accessors used by the solver drivers (solvers.cu)
+namespace l1b {
+ProblemView problem_view(l1b_problem* p) {
+  ProblemView v;
+  v.device = p->device;
+  v.stream = p->stream;
+  v.m = p->m;
+  v.n = p->n;
+  v.tau = p->tau;
+  v.lmax = p->lmax;
+  v.tail_sq = p->tail_sq;
+  v.b = p->d_b;
+  v.A = p->rows();
+  v.At = p->cols();
+  v.op = &p->view;
+  v.gram = nullptr;
+  return v;
+}
+const double* problem_gram(l1b_problem* p) { return gram_diag_device(p); }
+}  // namespace l1b

@@ -1,0 +1,173 @@
+// common.cuh -- shared types, error handling and device helpers of libl1b.
+//
+// Layout in HBM:
+//   * A rows  : CSR over the active rows [0, m_act): ptr (u32 when nnz < 2^32,
+//               else u64), col u32, val f64 -- exactly OperatorSpec::row()'s
+//               entries (linops.cpp:597-619), ascending, exact zeros dropped.
+//   * A cols  : CSC (= CSR of A^T) over n columns, same widths, exactly
+//               OperatorSpec::column() (linops.cpp:566-595).
+//   * vectors : dense f64, n (x, y, ...) and m (b, residuals).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace l1b {
+
+// ---------------------------------------------------------------------------
+// errors: each maps to one l1b_status (include/l1b.h)
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct LogicError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct OutOfMemory : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define L1B_CUDA(call) ::l1b::cuda_check((call), #call, __FILE__, __LINE__)
+#define L1B_LAUNCHED() ::l1b::note_launch()
+
+extern std::atomic<uint64_t> g_launch_count;
+inline void note_launch() {
+  g_launch_count.fetch_add(1, std::memory_order_relaxed);
+  L1B_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// operator description as kernels see it
+constexpr int kMaxStages = 32;
+
+struct StageTab {
+  int count = 0;
+  int offset[kMaxStages];
+  double c[kMaxStages];  // cos(theta) from the host libm (linops.cpp:84-85)
+  double s[kMaxStages];
+};
+
+struct OpView {
+  uint64_t m = 0, n = 0;
+  const uint32_t* p1 = nullptr;      // map, null = identity
+  const uint32_t* p2 = nullptr;
+  const uint32_t* p1_inv = nullptr;
+  const uint32_t* p2_inv = nullptr;
+  const double* sigma = nullptr;
+  StageTab right, left;
+};
+
+// ---------------------------------------------------------------------------
+// launch geometry
+constexpr int kThreads = 256;
+int sm_count();
+int grid_for(uint64_t work_items, int threads = kThreads, int max_blocks_per_sm = 8);
+
+// ---------------------------------------------------------------------------
+// device helpers
+#ifdef __CUDACC__
+// rotate_pair (linops.cpp:20-30).  The library is compiled with --fmad=false,
+// so every product and sum rounds separately, as in the reference's x86-64
+// build: results are bit-identical for identical inputs.
+__device__ __forceinline__ void rotate_pair(double& vi, double& vj, double c, double s,
+                                            bool transposed) {
+  const double a = vi, b = vj;
+  if (transposed) {
+    vi = c * a + s * b;
+    vj = -s * a + c * b;
+  } else {
+    vi = c * a - s * b;
+    vj = s * a + c * b;
+  }
+}
+
+// soft_threshold (solvers.cpp:153-157)
+__device__ __forceinline__ double soft_threshold(double v, double t) {
+  if (v > t) return v - t;
+  if (v < -t) return v + t;
+  return 0.0;
+}
+
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Block-wide sum of NS doubles held per thread (result valid in thread 0).
+template <int NS>
+__device__ __forceinline__ void block_sum(double (&v)[NS]) {
+  __shared__ double red[NS][kThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) red[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      v[k] = lane < (int)(blockDim.x >> 5) ? red[k][lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    }
+  }
+  __syncthreads();
+}
+
+// Deterministic grid reduction: every block stores its NS partial sums, the
+// last block to arrive (ticket) folds all partials in a fixed order and
+// returns true in all of its threads with the totals in `tot` (thread 0 of
+// that block holds them; they are also broadcast through shared memory).
+template <int NS>
+__device__ __forceinline__ bool grid_sum(double (&v)[NS], double* partials, unsigned int* ticket,
+                                         double (&tot)[NS]) {
+  block_sum<NS>(v);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) partials[(size_t)blockIdx.x * NS + k] = v[k];
+    __threadfence();
+    const unsigned int t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+  for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) acc[k] += __ldcg(&partials[(size_t)b * NS + k]);
+  }
+  block_sum<NS>(acc);
+  __shared__ double bc[NS];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) bc[k] = acc[k];
+    *ticket = 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NS; ++k) tot[k] = bc[k];
+  return true;
+}
+#endif
+
+}  // namespace l1b

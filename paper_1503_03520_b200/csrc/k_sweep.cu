@@ -1,0 +1,214 @@
+// k_sweep.cu -- matrix-free products A = P1 Gtilde P2 Sigma G^T as Givens
+// stage sweeps on device, in the reference's operation order
+// (linops.cpp:422-490) and rounding (--fmad=false, host cos/sin), so the
+// generator's b, e and the certificate are bit-identical to the reference.
+// One thread per rotation pair; a stage is one launch (used by the generator
+// and the PATH_SWEEP products; the fused multi-stage kernel is the next step,
+// SURVEY.md 8(f)-1).
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace l1b {
+
+namespace {
+
+__global__ void stage_kernel(double* __restrict__ v, uint64_t dim, int off, double c, double s,
+                             bool transposed) {
+  const uint64_t npairs = dim > (uint64_t)off ? (dim - off) / 2 : 0;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < npairs;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = off + 2 * t;
+    double a = v[k], b = v[k + 1];
+    rotate_pair(a, b, c, s, transposed);
+    v[k] = a;
+    v[k + 1] = b;
+  }
+}
+
+// t[i] = j < n ? sigma[j] * v[j] : 0  with j = P2 map[i]   (linops.cpp:432-440)
+__global__ void sigma_fwd(const double* __restrict__ v, double* __restrict__ t,
+                          const double* __restrict__ sigma, const uint32_t* __restrict__ p2,
+                          uint64_t n, uint64_t m) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = p2 ? p2[i] : i;
+    t[i] = j < n ? sigma[j] * v[j] : 0.0;
+  }
+}
+
+// v[j] = sigma[j] * t[i] for j = P2 map[i] < n              (linops.cpp:459-467)
+__global__ void sigma_bwd(const double* __restrict__ t, double* __restrict__ v,
+                          const double* __restrict__ sigma, const uint32_t* __restrict__ p2,
+                          uint64_t n, uint64_t m) {
+  const uint64_t lim = p2 ? m : n;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lim;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = p2 ? p2[i] : i;
+    if (j < n) v[j] = sigma[j] * t[i];
+  }
+}
+
+__global__ void gather_kernel(const double* __restrict__ in, double* __restrict__ out,
+                              const uint32_t* __restrict__ map, uint64_t m) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[map[i]];
+}
+
+__global__ void scatter_kernel(const double* __restrict__ in, double* __restrict__ out,
+                               const uint32_t* __restrict__ map, uint64_t m) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[map[i]] = in[i];
+}
+
+__global__ void gram_scale(double* __restrict__ u, const double* __restrict__ sigma, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    u[i] /= sigma[i] * sigma[i];
+}
+
+__global__ void scatter_sparse_kernel(const uint32_t* sup, const double* val, uint64_t s,
+                                      double* dense) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < s;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    dense[sup[k]] = val[k];
+}
+
+__global__ void combine_kernel(double tau, double* __restrict__ e, double* __restrict__ b,
+                               uint64_t m, double* partials, unsigned int* ticket, double* out) {
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double ei = e[i] * tau;  // instance.cpp:70
+    e[i] = ei;
+    b[i] += ei;                    // instance.cpp:77
+    acc[0] += ei * ei;             // instance.cpp:78
+  }
+  double tot[1];
+  if (grid_sum<1>(acc, partials, ticket, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+__global__ void cert_kernel(const double* __restrict__ r, const double* __restrict__ xd,
+                            double tau, uint64_t n, unsigned long long* out2) {
+  double sup = 0.0, off = 0.0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double x = xd[i];
+    if (x != 0.0) {
+      const double sign = x > 0.0 ? 1.0 : -1.0;
+      sup = fmax(sup, fabs(r[i] + tau * sign));
+    } else {
+      off = fmax(off, fmax(fabs(r[i]) - tau, 0.0));
+    }
+  }
+  // non-negative doubles order like their bit patterns
+  atomicMax(&out2[0], (unsigned long long)__double_as_longlong(sup));
+  atomicMax(&out2[1], (unsigned long long)__double_as_longlong(off));
+}
+
+__global__ void sub_kernel(double* __restrict__ a, const double* __restrict__ b, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] -= b[i];
+}
+
+void run_stage(double* v, uint64_t dim, int off, double c, double s, bool tr, cudaStream_t st) {
+  const uint64_t npairs = dim > (uint64_t)off ? (dim - off) / 2 : 0;
+  if (!npairs) return;
+  stage_kernel<<<grid_for(npairs), kThreads, 0, st>>>(v, dim, off, c, s, tr);
+  L1B_LAUNCHED();
+}
+
+}  // namespace
+
+void sweep_apply(const OpView& op, const double* x, double* y, cudaStream_t st) {
+  double *v = nullptr, *t = nullptr;
+  L1B_CUDA(cudaMallocAsync(&v, op.n * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&t, op.m * sizeof(double), st));
+  L1B_CUDA(cudaMemcpyAsync(v, x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  for (int s = 0; s < op.right.count; ++s)
+    run_stage(v, op.n, op.right.offset[s], op.right.c[s], op.right.s[s], true, st);
+  sigma_fwd<<<grid_for(op.m), kThreads, 0, st>>>(v, t, op.sigma, op.p2, op.n, op.m);
+  L1B_LAUNCHED();
+  for (int s = op.left.count - 1; s >= 0; --s)
+    run_stage(t, op.m, op.left.offset[s], op.left.c[s], op.left.s[s], false, st);
+  if (op.p1) {
+    gather_kernel<<<grid_for(op.m), kThreads, 0, st>>>(t, y, op.p1, op.m);
+    L1B_LAUNCHED();
+  } else {
+    L1B_CUDA(cudaMemcpyAsync(y, t, op.m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  L1B_CUDA(cudaFreeAsync(v, st));
+  L1B_CUDA(cudaFreeAsync(t, st));
+}
+
+void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStream_t st) {
+  double *v = nullptr, *t = nullptr;
+  L1B_CUDA(cudaMallocAsync(&v, op.n * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&t, op.m * sizeof(double), st));
+  if (op.p1) {
+    scatter_kernel<<<grid_for(op.m), kThreads, 0, st>>>(y, t, op.p1, op.m);
+    L1B_LAUNCHED();
+  } else {
+    L1B_CUDA(cudaMemcpyAsync(t, y, op.m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  for (int s = 0; s < op.left.count; ++s)
+    run_stage(t, op.m, op.left.offset[s], op.left.c[s], op.left.s[s], true, st);
+  L1B_CUDA(cudaMemsetAsync(v, 0, op.n * sizeof(double), st));
+  sigma_bwd<<<grid_for(op.p2 ? op.m : op.n), kThreads, 0, st>>>(t, v, op.sigma, op.p2, op.n, op.m);
+  L1B_LAUNCHED();
+  for (int s = op.right.count - 1; s >= 0; --s)
+    run_stage(v, op.n, op.right.offset[s], op.right.c[s], op.right.s[s], false, st);
+  L1B_CUDA(cudaMemcpyAsync(x, v, op.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  L1B_CUDA(cudaFreeAsync(v, st));
+  L1B_CUDA(cudaFreeAsync(t, st));
+}
+
+void sweep_gram_inverse(const OpView& op, const double* vin, double* out, cudaStream_t st) {
+  if (out != vin)
+    L1B_CUDA(cudaMemcpyAsync(out, vin, op.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  for (int s = 0; s < op.right.count; ++s)
+    run_stage(out, op.n, op.right.offset[s], op.right.c[s], op.right.s[s], true, st);
+  gram_scale<<<grid_for(op.n), kThreads, 0, st>>>(out, op.sigma, op.n);
+  L1B_LAUNCHED();
+  for (int s = op.right.count - 1; s >= 0; --s)
+    run_stage(out, op.n, op.right.offset[s], op.right.c[s], op.right.s[s], false, st);
+}
+
+void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* dense, uint64_t n,
+                    cudaStream_t st) {
+  L1B_CUDA(cudaMemsetAsync(dense, 0, n * sizeof(double), st));
+  if (!s) return;
+  scatter_sparse_kernel<<<grid_for(s), kThreads, 0, st>>>(sup, val, s, dense);
+  L1B_LAUNCHED();
+}
+
+void generator_combine(double tau, double* e, double* b, uint64_t m, double* d_sum_sq,
+                       cudaStream_t st) {
+  const int grid = grid_for(m);
+  double* partials = nullptr;
+  unsigned int* ticket = nullptr;
+  L1B_CUDA(cudaMallocAsync(&partials, grid * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  L1B_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  combine_kernel<<<grid, kThreads, 0, st>>>(tau, e, b, m, partials, ticket, d_sum_sq);
+  L1B_LAUNCHED();
+  L1B_CUDA(cudaFreeAsync(partials, st));
+  L1B_CUDA(cudaFreeAsync(ticket, st));
+}
+
+void certificate(const double* r, const double* xd, double tau, uint64_t n, double* d_out2,
+                 cudaStream_t st) {
+  L1B_CUDA(cudaMemsetAsync(d_out2, 0, 2 * sizeof(double), st));
+  cert_kernel<<<grid_for(n), kThreads, 0, st>>>(r, xd, tau, n, (unsigned long long*)d_out2);
+  L1B_LAUNCHED();
+}
+
+void vec_sub(double* a, const double* b, uint64_t n, cudaStream_t st) {
+  if (!n) return;
+  sub_kernel<<<grid_for(n), kThreads, 0, st>>>(a, b, n);
+  L1B_LAUNCHED();
+}
+
+}  // namespace l1b

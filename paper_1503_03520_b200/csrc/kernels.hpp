@@ -1,0 +1,90 @@
+// kernels.hpp -- host-side launchers of the device kernels (one per .cu file).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace l1b {
+
+// ---- k_build.cu ----------------------------------------------------------
+struct LinesOut {
+  uint64_t lines = 0;    // lines kept (trailing empty lines trimmed when asked)
+  uint64_t nnz = 0;
+  uint32_t max_len = 0;
+  bool ptr32 = true;
+  void* ptr = nullptr;   // (lines + 1) x u32 or u64
+  uint32_t* idx = nullptr;
+  double* val = nullptr;
+};
+// Lines [first, first + nlines) of A (rows) or A^T (columns = CSC of A).
+// Indices are stored minus idx_base (wrapping), i.e. local to a window.
+void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, uint64_t idx_base,
+                 bool trim_tail, cudaStream_t st, LinesOut* out);
+void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, cudaStream_t st);
+
+// ---- k_sweep.cu (matrix-free, bit-exact vs linops.cpp) ---------------------
+void sweep_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
+void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStream_t st);
+void sweep_gram_inverse(const OpView& op, const double* v, double* out, cudaStream_t st);
+void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* dense, uint64_t n,
+                    cudaStream_t st);
+// b += tau * e-part: e *= tau; b += e; returns sum(e^2) through *sum_sq (device)
+void generator_combine(double tau, double* e, double* b, uint64_t m, double* d_sum_sq,
+                       cudaStream_t st);
+void vec_sub(double* a, const double* b, uint64_t n, cudaStream_t st);  // a -= b
+// max_S |r_i + tau sign(x_i)|, max_{S^c} (|r_i| - tau)_+  (instance.cpp:187-198)
+void certificate(const double* r, const double* xd, double tau, uint64_t n, double* d_out2,
+                 cudaStream_t st);
+
+// ---- k_spmv.cu -------------------------------------------------------------
+struct Csr {  // CSR of A (rows) or of A^T (= CSC of A)
+  uint64_t lines = 0;
+  uint64_t nnz = 0;
+  bool ptr32 = true;
+  const void* ptr = nullptr;
+  const uint32_t* idx = nullptr;
+  const double* val = nullptr;
+  int lanes = 8;
+};
+
+// y[0, lines) = M x
+void spmv(const Csr& M, const double* x, double* y, cudaStream_t st);
+// out = tau*||x||_1 + 0.5*(sum_{i<lines} (Mx - b)_i^2 + tail_sq) into *d_f
+void objective(const Csr& A, const double* x, uint64_t n, const double* b, double tau,
+               double tail_sq, double* d_f, cudaStream_t st);
+
+// FISTA / ISTA device loop state (solvers.cpp:277-382)
+struct FistaSample {
+  uint64_t iter;
+  double f;
+  double nnz;
+  uint64_t ts_ns;
+};
+struct FistaDev {
+  double t, lval, tau, f, nnz, target, tail_sq;
+  uint64_t k, max_iters, n_samples, cap, last_sampled, t0_ns, last_ts;
+  int stop, status, accel, has_target;
+  unsigned int ticket[4];
+  double scal[4];  // l1, nnz, mismatches, ||r||^2 of the last iteration
+};
+
+struct FistaBufs {
+  double *x, *y;          // n (own columns)
+  double *r_x, *r_y;      // rows (own rows)
+  const double* b;
+  FistaDev* st;
+  FistaSample* trace;
+  double* partials;       // grid_max * 4
+};
+
+int spmv_grid_max();
+void fista_init(const FistaBufs& fb, uint64_t m_rows, cudaStream_t st);
+// K1: x, y <- prox/momentum of A^T r_y      (CSC over n columns)
+void fista_k1(const Csr& At, const FistaBufs& fb, cudaStream_t st);
+// K2: r_x, r_y <- A x - b, residual momentum (CSR over active rows) + finalize
+void fista_k2(const Csr& A, const FistaBufs& fb, cudaStream_t st);
+
+}  // namespace l1b

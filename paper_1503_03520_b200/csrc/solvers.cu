@@ -1,0 +1,346 @@
+// solvers.cu -- host drivers of the device-resident solver loops.
+//
+// FISTA/ISTA (solvers.cpp:277-382): two fused kernels per iteration (k_spmv.cu)
+// and no host round trip: the stop decision (fixed point, target, iteration
+// budget, divergence) is taken on device and turns later launches into
+// no-ops, so the host enqueues chunks and only polls a pinned copy of the stop
+// flag between chunks (time budget = the reference's loop-head check at chunk
+// granularity).  Trace samples are stamped with %globaltimer on device.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "guard.hpp"
+#include "solvers.hpp"
+
+using namespace l1b;
+
+namespace l1b {
+void validate_cfg(const l1b_solver_cfg* c, uint64_t n);
+void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+              l1b_summary* summary, double* x_host, double* d_x);
+void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+                  l1b_summary* summary, double* x_host, double* d_x);
+}  // namespace l1b
+
+struct l1b_session {
+  l1b_problem* prob = nullptr;
+  ProblemView v;
+  l1b_solver_cfg cfg;
+  bool accel = true;
+  double *x = nullptr, *y = nullptr, *r_x = nullptr, *r_y = nullptr, *partials = nullptr;
+  FistaDev* st = nullptr;
+  FistaSample* trace = nullptr;
+  FistaDev* h_st = nullptr;  // pinned
+  uint64_t cap = 0;
+  uint64_t launched = 0;
+  std::chrono::steady_clock::time_point t0;
+  bool time_out = false;
+
+  FistaBufs bufs() const {
+    FistaBufs b;
+    b.x = x;
+    b.y = y;
+    b.r_x = r_x;
+    b.r_y = r_y;
+    b.b = v.b;
+    b.st = st;
+    b.trace = trace;
+    b.partials = partials;
+    return b;
+  }
+
+  ~l1b_session() {
+    cudaSetDevice(v.device);
+    if (v.stream) cudaStreamSynchronize(v.stream);
+    for (void* q : {(void*)x, (void*)r_x, (void*)partials, (void*)st, (void*)trace})
+      if (q) cudaFree(q);
+    if (accel) {
+      if (y) cudaFree(y);
+      if (r_y) cudaFree(r_y);
+    }
+    if (h_st) cudaFreeHost(h_st);
+  }
+};
+
+namespace {
+
+uint64_t sample_capacity(uint64_t max_iters) {
+  uint64_t c = std::min<uint64_t>(max_iters, 1000) + 2;
+  if (max_iters > 1000) c += (max_iters - 1000) / 10 + 1;
+  return std::min<uint64_t>(c, 1ull << 22);
+}
+
+void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
+  s->prob = p;
+  s->v = problem_view(p);
+  s->cfg = *cfg;
+  s->accel = cfg->solver == L1B_FISTA;
+  const ProblemView& v = s->v;
+  cudaStream_t st = v.stream;
+  L1B_CUDA(cudaMalloc(&s->x, v.n * sizeof(double)));
+  L1B_CUDA(cudaMalloc(&s->r_x, v.m * sizeof(double)));
+  if (s->accel) {
+    L1B_CUDA(cudaMalloc(&s->y, v.n * sizeof(double)));
+    L1B_CUDA(cudaMalloc(&s->r_y, v.m * sizeof(double)));
+  } else {
+    s->y = s->x;      // ISTA: base = x (solvers.cpp:317-318)
+    s->r_y = s->r_x;
+  }
+  L1B_CUDA(cudaMalloc(&s->partials, (size_t)spmv_grid_max() * 4 * sizeof(double)));
+  s->cap = sample_capacity(cfg->max_iters);
+  L1B_CUDA(cudaMalloc(&s->trace, s->cap * sizeof(FistaSample)));
+  L1B_CUDA(cudaMalloc(&s->st, sizeof(FistaDev)));
+  L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
+  L1B_CUDA(cudaMemsetAsync(s->x, 0, v.n * sizeof(double), st));
+  if (s->accel) L1B_CUDA(cudaMemsetAsync(s->y, 0, v.n * sizeof(double), st));
+  FistaDev h;
+  std::memset(&h, 0, sizeof(h));
+  h.t = 1.0;  // solvers.cpp:304
+  h.lval = cfg->l_fixed > 0.0 ? cfg->l_fixed : v.lmax;  // LipschitzState (:103-115)
+  h.tau = v.tau;
+  h.target = cfg->target;
+  h.has_target = cfg->has_target ? 1 : 0;
+  h.tail_sq = v.tail_sq;
+  h.max_iters = cfg->max_iters;
+  h.cap = s->cap;
+  h.accel = s->accel ? 1 : 0;
+  *s->h_st = h;
+  L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
+  s->t0 = std::chrono::steady_clock::now();
+  // residuals over all m rows: rows >= m_active keep r = -b for the whole run
+  fista_init(s->bufs(), v.m, st);
+}
+
+void session_step(l1b_session* s, uint64_t iters) {
+  const FistaBufs b = s->bufs();
+  for (uint64_t i = 0; i < iters; ++i) {
+    fista_k1(s->v.At, b, s->v.stream);
+    fista_k2(s->v.A, b, s->v.stream);
+  }
+  s->launched += iters;
+}
+
+void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* sum,
+                    double* x_host, double* d_x) {
+  cudaStream_t st = s->v.stream;
+  L1B_CUDA(cudaMemcpyAsync(s->h_st, s->st, sizeof(FistaDev), cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  const FistaDev h = *s->h_st;
+  const char* name = s->accel ? "fista" : "ista";
+  if (h.status < 0)
+    throw std::runtime_error(std::string(name) + ": objective diverged to a non-finite value");
+  int status = h.stop ? h.status : (s->time_out ? L1B_TIME_BUDGET : L1B_ITER_BUDGET);
+  const uint64_t kept = std::min<uint64_t>(h.n_samples, s->cap);
+  std::vector<FistaSample> tr(kept);
+  if (kept)
+    L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
+                             cudaMemcpyDeviceToHost, st));
+  if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, s->x, s->v.n * 8, cudaMemcpyDeviceToHost, st));
+  if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, s->x, s->v.n * 8, cudaMemcpyDeviceToDevice, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  // final sample when the last iteration was not sampled (solvers.cpp:379)
+  if (h.last_sampled != h.k) tr.push_back(FistaSample{h.k, h.f, h.nnz, h.last_ts});
+  std::memset(sum, 0, sizeof(*sum));
+  sum->status = status;
+  sum->time_to_target = INFINITY;
+  sum->matvecs_to_target = INFINITY;
+  sum->final_objective = NAN;
+  const uint64_t total = h.n_samples + (h.last_sampled != h.k ? 1 : 0);
+  for (size_t i = 0; i < tr.size(); ++i) {
+    l1b_sample o;
+    o.iter = tr[i].iter;
+    o.elapsed_s = (double)(tr[i].ts_ns - h.t0_ns) * 1e-9;
+    o.objective = tr[i].f;
+    o.nnz = (uint64_t)tr[i].nnz;
+    o.matvecs = 1.0 + 2.0 * (double)tr[i].iter;  // CountingOperator: 1 + 2 per iteration
+    o.extra = 0;
+    if (samples && i < cap) samples[i] = o;
+    sum->final_objective = o.objective;
+    if (!sum->reached_target && s->cfg.has_target && o.objective <= s->cfg.target) {
+      sum->reached_target = 1;  // Tracker::sample (solvers.cpp:61-69)
+      sum->time_to_target = o.elapsed_s;
+      sum->matvecs_to_target = o.matvecs;
+    }
+  }
+  sum->n_samples = total;
+  sum->iterations = h.k;
+  sum->elapsed_s = (double)(h.last_ts - h.t0_ns) * 1e-9;
+  sum->total_matvecs = 1.0 + 2.0 * (double)h.k;
+  if (status == L1B_TARGET_REACHED && !sum->reached_target) {  // Tracker::finish (:79-93)
+    sum->reached_target = 1;
+    sum->time_to_target = sum->elapsed_s;
+    sum->matvecs_to_target = sum->total_matvecs;
+  }
+}
+
+
+}  // namespace
+
+namespace l1b {
+
+void validate_cfg(const l1b_solver_cfg* c, uint64_t n) {  // SolverConfig::validate (solvers.cpp:133-143)
+  if (!c) throw InvalidArgument("null solver config");
+  if (c->solver < L1B_ISTA || c->solver > L1B_PCDM)
+    throw InvalidArgument("SolverConfig: unknown solver id");
+  if (!(c->mu > 0.0)) throw InvalidArgument("SolverConfig: mu must be positive");
+  if (!(c->eta > 0.0 && c->eta < 1.0)) throw InvalidArgument("SolverConfig: eta must lie in (0, 1)");
+  if (c->varpi < 1) throw InvalidArgument("SolverConfig: varpi must be at least 1");
+  if (c->omega && (c->omega < 1 || c->omega > n))
+    throw InvalidArgument("SolverConfig: omega must lie in [1, n]");
+  if (c->l_fixed < 0.0 || std::isnan(c->l_fixed))
+    throw InvalidArgument("SolverConfig: fixed L must be positive");
+  if (!(c->max_seconds > 0.0)) throw InvalidArgument("SolverConfig: max_seconds must be positive");
+}
+
+}  // namespace l1b
+
+extern "C" {
+
+int l1b_session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session** out) {
+  return guard([&] {
+    if (!p || !out) throw InvalidArgument("null argument");
+    *out = nullptr;
+    ProblemView v = problem_view(p);
+    validate_cfg(cfg, v.n);
+    if (cfg->solver != L1B_FISTA && cfg->solver != L1B_ISTA)
+      throw InvalidArgument("sessions drive FISTA / ISTA only");
+    L1B_CUDA(cudaSetDevice(v.device));
+    auto* s = new l1b_session();
+    try {
+      session_begin(p, cfg, s);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int l1b_session_step(l1b_session* s, uint64_t iters) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    session_step(s, iters);
+  });
+}
+
+int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms) {
+  return guard([&] {
+    if (!s || !ms_out || n_ms < 2) throw InvalidArgument("bad arguments");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    cudaStream_t st = s->v.stream;
+    std::vector<cudaEvent_t> ev(3 * iters);
+    for (auto& e : ev) L1B_CUDA(cudaEventCreate(&e));
+    const FistaBufs b = s->bufs();
+    for (uint64_t i = 0; i < iters; ++i) {
+      L1B_CUDA(cudaEventRecord(ev[3 * i], st));
+      fista_k1(s->v.At, b, st);
+      L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
+      fista_k2(s->v.A, b, st);
+      L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
+    }
+    s->launched += iters;
+    L1B_CUDA(cudaStreamSynchronize(st));
+    double k1 = 0.0, k2 = 0.0;
+    for (uint64_t i = 0; i < iters; ++i) {
+      float a = 0.f, c = 0.f;
+      L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+      L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));
+      k1 += a;
+      k2 += c;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    ms_out[0] = k1;
+    ms_out[1] = k2;
+  });
+}
+
+int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    L1B_CUDA(cudaMemcpyAsync(s->h_st, s->st, sizeof(FistaDev), cudaMemcpyDeviceToHost, s->v.stream));
+    L1B_CUDA(cudaStreamSynchronize(s->v.stream));
+    if (stopped) *stopped = s->h_st->stop;
+    if (iterations) *iterations = s->h_st->k;
+  });
+}
+
+int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
+                    double* x_host) {
+  const int rc = guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    l1b_summary tmp;
+    session_finish(s, samples, cap, summary ? summary : &tmp, x_host, nullptr);
+  });
+  delete s;
+  return rc;
+}
+
+int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+              l1b_summary* summary, double* x_host, double* d_x) {
+  return guard([&] {
+    if (!p || !summary) throw InvalidArgument("null argument");
+    ProblemView v = problem_view(p);
+    validate_cfg(cfg, v.n);
+    L1B_CUDA(cudaSetDevice(v.device));
+    if (cfg->solver == L1B_PCDM || cfg->solver == L1B_CD) {
+      run_pcdm(p, cfg, samples, cap, summary, x_host, d_x);
+      return;
+    }
+    if (cfg->solver == L1B_NEWTON_CG) {
+      run_newton_cg(p, cfg, samples, cap, summary, x_host, d_x);
+      return;
+    }
+    l1b_session s;
+    session_begin(p, cfg, &s);
+    cudaStream_t st = v.stream;
+    int* h_flags = nullptr;
+    L1B_CUDA(cudaMallocHost(&h_flags, 2 * sizeof(int)));
+    cudaEvent_t ev[2];
+    L1B_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    L1B_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    bool pending[2] = {false, false};
+    int slot = 0;
+    uint64_t chunk = 4;
+    try {
+      while (s.launched < cfg->max_iters) {
+        const uint64_t k = std::min<uint64_t>(chunk, cfg->max_iters - s.launched);
+        session_step(&s, k);
+        L1B_CUDA(cudaMemcpyAsync(&h_flags[slot], &s.st->stop, sizeof(int), cudaMemcpyDeviceToHost, st));
+        L1B_CUDA(cudaEventRecord(ev[slot], st));
+        pending[slot] = true;
+        slot ^= 1;
+        if (pending[slot]) {  // the previous chunk: one chunk of look-ahead stays queued
+          L1B_CUDA(cudaEventSynchronize(ev[slot]));
+          pending[slot] = false;
+          if (h_flags[slot]) break;
+        }
+        const double el =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - s.t0).count();
+        if (el > cfg->max_seconds) {
+          s.time_out = true;
+          break;
+        }
+        chunk = std::min<uint64_t>(chunk * 2, 64);
+      }
+      L1B_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
+      cudaFreeHost(h_flags);
+      throw;
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(h_flags);
+    session_finish(&s, samples, cap, summary, x_host, d_x);
+  });
+}
+
+}  // extern "C"

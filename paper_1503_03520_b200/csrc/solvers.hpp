@@ -1,0 +1,27 @@
+// solvers.hpp -- what the solver drivers see of a problem.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/l1b.h"
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace l1b {
+
+struct ProblemView {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t m = 0, n = 0;
+  double tau = 1.0, lmax = 0.0, tail_sq = 0.0;
+  const double* b = nullptr;  // m
+  Csr A;                      // CSR over active rows
+  Csr At;                     // CSC over n columns
+  const OpView* op = nullptr;
+  const double* gram = nullptr;
+};
+
+ProblemView problem_view(l1b_problem* p);
+const double* problem_gram(l1b_problem* p);  // lazily built diag(A^T A)
+
+}  // namespace l1b

@@ -1,0 +1,505 @@
+"""Python mirror of the reference's ``l1bench`` generator/solver API over the
+CUDA C ABI (include/l1b.h).
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/l1bench/*.hpp):
+
+==============================  ============================================
+reference (C++)                  here
+==============================  ============================================
+``ExperimentConfig`` + ``build_instance`` (bench.hpp:37-102)   :func:`build_instance`
+``ProblemInstance`` (instance.hpp:36-52)                         :class:`ProblemInstance`
+``OperatorSpec`` apply / apply_transpose / gram_diagonal (linops.hpp:139-206)  ``ProblemInstance.op``
+``verify_optimality`` (instance.hpp:74)                          :func:`verify_optimality`
+``SolverConfig`` / ``SolverTrace`` / ``StopReason`` (solvers.hpp:15-66)
+``run_solver`` / ``fista_run`` / ``ista_run`` / ``coordinate_descent_run`` / ``newton_cg_run``
+``objective`` (solvers.hpp:70)
+==============================  ============================================
+
+``std::invalid_argument`` surfaces as :class:`ValueError`, ``std::runtime_error``
+as :class:`RuntimeError`.  Device vectors are torch CUDA float64 tensors (torch
+is only the device-memory plumbing); everything else is numpy on the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+
+_u32p = C.POINTER(C.c_uint32)
+_f64p = C.POINTER(C.c_double)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def _lib():
+    return N.load()
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _dptr(t) -> int:
+    """Device pointer of a contiguous CUDA float64 torch tensor."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise ValueError("device vectors must be CUDA float64 torch tensors")
+    if not t.is_contiguous():
+        raise ValueError("device vectors must be contiguous")
+    return t.data_ptr()
+
+
+def mix_seed(seed: int, salt: int) -> int:
+    """splitmix64 finaliser of rng.hpp:19-24."""
+    return int(_lib().l1b_mix_seed(seed, salt))
+
+
+class StopReason(enum.IntEnum):  # solvers.hpp:24
+    target_reached = 0
+    iter_budget = 1
+    time_budget = 2
+
+    def __str__(self):  # to_string (solvers.cpp:124-131)
+        return {0: "target-reached", 1: "iter-budget", 2: "time-budget"}[int(self)]
+
+
+class LPolicy(enum.IntEnum):
+    spectrum = 0
+    backtracking = 1
+
+
+@dataclass
+class SolverConfig:  # solvers.hpp:17-41
+    id: str = "fista"
+    max_iters: int = 100000
+    max_seconds: float = 600.0
+    target_objective: Optional[float] = None
+    mu: float = 1e-5
+    eta: float = 0.1
+    pcg_max_iters: int = 1000
+    ls_max_backtracks: int = 50
+    grad_tol_rel: float = 1e-8
+    l_policy: LPolicy = LPolicy.spectrum
+    l_fixed: Optional[float] = None
+    varpi: int = 1
+    omega: Optional[int] = None
+    seed: int = 0
+    block: int = 256  # pcdm: coordinates per block
+
+    _IDS = {"ista": N.ISTA, "fista": N.FISTA, "cd": N.CD, "newton_cg": N.NEWTON_CG, "pcdm": N.PCDM}
+
+    def to_c(self) -> N.SolverCfg:
+        if self.id not in self._IDS:
+            raise ValueError(f"SolverConfig: unknown solver id '{self.id}'")
+        if self.l_policy == LPolicy.backtracking and self.l_fixed is None:
+            raise N.L1bUnsupported("LPolicy::backtracking is not built on device; use the spectrum policy")
+        c = N.SolverCfg()
+        _lib().l1b_solver_cfg_default(C.byref(c))
+        c.solver = self._IDS[self.id]
+        c.max_iters = int(self.max_iters)
+        c.max_seconds = float(self.max_seconds)
+        c.has_target = 0 if self.target_objective is None else 1
+        c.target = 0.0 if self.target_objective is None else float(self.target_objective)
+        c.mu, c.eta = float(self.mu), float(self.eta)
+        c.pcg_max_iters, c.ls_max_backtracks = int(self.pcg_max_iters), int(self.ls_max_backtracks)
+        c.grad_tol_rel = float(self.grad_tol_rel)
+        if self.l_fixed is not None and not (self.l_fixed > 0.0):
+            raise ValueError("SolverConfig: fixed L must be positive")
+        c.l_fixed = 0.0 if self.l_fixed is None else float(self.l_fixed)
+        c.varpi = int(self.varpi)
+        c.omega = 0 if self.omega is None else int(self.omega)
+        c.seed = int(self.seed)
+        c.block = int(self.block)
+        return c
+
+
+@dataclass
+class TraceSample:  # solvers.hpp:45-52
+    iter: int
+    elapsed_s: float
+    objective: float
+    nnz: int
+    matvecs: float
+    extra: int
+
+
+@dataclass
+class SolverTrace:  # solvers.hpp:54-66
+    solver: str
+    samples: list = field(default_factory=list)
+    status: StopReason = StopReason.iter_budget
+    reached_target: bool = False
+    final_objective: float = math.nan
+    elapsed_s: float = 0.0
+    total_matvecs: float = 0.0
+    total_pcg_iterations: int = 0
+    newton_steps: int = 0
+    time_to_target: float = math.inf
+    matvecs_to_target: float = math.inf
+    iterations: int = 0
+
+    def objectives(self) -> np.ndarray:
+        return np.array([s.objective for s in self.samples])
+
+    def iters(self) -> np.ndarray:
+        return np.array([s.iter for s in self.samples], dtype=np.int64)
+
+
+@dataclass
+class SparseSolution:  # solution.hpp:13-33
+    n: int
+    support: np.ndarray
+    values: np.ndarray
+
+    def nnz(self) -> int:
+        return len(self.support)
+
+    def dense(self) -> np.ndarray:
+        x = np.zeros(self.n)
+        x[self.support] = self.values
+        return x
+
+    def norm1(self) -> float:
+        return float(np.sum(np.abs(self.values)))
+
+
+@dataclass
+class CertificateReport:  # instance.hpp:58-63
+    max_support_violation: float
+    max_offsupport_violation: float
+    threshold: float
+    passed: bool
+
+
+class DeviceOperator:
+    """LinearOperator view of a problem's A on the GPU (linops.hpp:139-155).
+
+    ``path="sparse"`` runs the CSR/CSC SpMV kernels, ``path="sweep"`` the
+    matrix-free stage sweeps (bit-exact with OperatorSpec::apply)."""
+
+    def __init__(self, inst: "ProblemInstance"):
+        self._inst = inst
+
+    def rows(self) -> int:
+        return self._inst.m
+
+    def cols(self) -> int:
+        return self._inst.n
+
+    def _path(self, path):
+        return {"sparse": N.PATH_SPARSE, "sweep": N.PATH_SWEEP}[path]
+
+    def apply(self, x, out=None, path: str = "sparse"):
+        import torch
+
+        if x.shape != (self.cols(),):
+            raise ValueError(f"OperatorSpec::apply: expected length {self.cols()}, got {tuple(x.shape)}")
+        out = torch.empty(self.rows(), dtype=torch.float64, device=x.device) if out is None else out
+        N.check(_lib().l1b_apply(self._inst._h, self._path(path), _dptr(x), _dptr(out)))
+        return out
+
+    def apply_transpose(self, y, out=None, path: str = "sparse"):
+        import torch
+
+        if y.shape != (self.rows(),):
+            raise ValueError(f"OperatorSpec::apply_transpose: expected length {self.rows()}, got {tuple(y.shape)}")
+        out = torch.empty(self.cols(), dtype=torch.float64, device=y.device) if out is None else out
+        N.check(_lib().l1b_apply_transpose(self._inst._h, self._path(path), _dptr(y), _dptr(out)))
+        return out
+
+    def apply_gram_inverse(self, v, out=None):
+        import torch
+
+        out = torch.empty(self.cols(), dtype=torch.float64, device=v.device) if out is None else out
+        N.check(_lib().l1b_gram_inverse(self._inst._h, _dptr(v), _dptr(out)))
+        return out
+
+    def gram_diagonal(self, device="cuda"):
+        import torch
+
+        out = torch.empty(self.cols(), dtype=torch.float64, device=device)
+        N.check(_lib().l1b_gram_diagonal(self._inst._h, _dptr(out)))
+        return out
+
+    def gram_lmax(self) -> float:
+        return self._inst.info.gram_lmax
+
+    def csr(self):
+        """Rows of A exactly as OperatorSpec::row (linops.cpp:597-619)."""
+        info = self._inst.info
+        ptr = np.zeros(self.rows() + 1, dtype=np.uint64)
+        idx = np.empty(max(info.nnz, 1), dtype=np.uint32)
+        val = np.empty(max(info.nnz, 1))
+        N.check(_lib().l1b_export_csr(self._inst._h, _ptr(ptr, _u64p), _ptr(idx, _u32p), _ptr(val, _f64p)))
+        return ptr, idx[: info.nnz], val[: info.nnz]
+
+    def csc(self):
+        """Columns of A exactly as OperatorSpec::column (linops.cpp:566-595)."""
+        info = self._inst.info
+        ptr = np.zeros(self.cols() + 1, dtype=np.uint64)
+        idx = np.empty(max(info.nnz, 1), dtype=np.uint32)
+        val = np.empty(max(info.nnz, 1))
+        N.check(_lib().l1b_export_csc(self._inst._h, _ptr(ptr, _u64p), _ptr(idx, _u32p), _ptr(val, _f64p)))
+        return ptr, idx[: info.nnz], val[: info.nnz]
+
+
+class ProblemInstance:
+    """Device-resident instance (instance.hpp:36-52): operator + b + tau + x*."""
+
+    def __init__(self, handle):
+        self._h = handle
+        self.info = N.ProblemInfo()
+        N.check(_lib().l1b_problem_info_get(self._h, C.byref(self.info)))
+        self.op = DeviceOperator(self)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            try:
+                _lib().l1b_problem_free(h)
+            except Exception:
+                pass
+
+    # -- reference accessors --------------------------------------------------
+    @property
+    def m(self) -> int:
+        return int(self.info.m)
+
+    @property
+    def n(self) -> int:
+        return int(self.info.n)
+
+    def rows(self) -> int:
+        return self.m
+
+    def cols(self) -> int:
+        return self.n
+
+    @property
+    def tau(self) -> float:
+        return float(self.info.tau)
+
+    @property
+    def noise_norm(self) -> float:
+        return float(self.info.noise_norm)
+
+    @property
+    def cert_kappa(self) -> float:
+        return float(self.info.cert_kappa)
+
+    def objective_at_planted(self) -> float:  # instance.cpp:49-51
+        return float(self.info.f_star)
+
+    @property
+    def b(self) -> np.ndarray:
+        out = np.empty(self.m)
+        N.check(_lib().l1b_problem_get_b(self._h, _ptr(out, _f64p)))
+        return out
+
+    def sigma(self) -> np.ndarray:
+        out = np.empty(self.n)
+        N.check(_lib().l1b_problem_get_sigma(self._h, _ptr(out, _f64p)))
+        return out
+
+    @property
+    def x_star(self) -> SparseSolution:
+        s = int(self.info.s)
+        sup = np.empty(max(s, 1), dtype=np.uint32)
+        val = np.empty(max(s, 1))
+        N.check(_lib().l1b_problem_get_xstar(self._h, _ptr(sup, _u32p), _ptr(val, _f64p)))
+        return SparseSolution(self.n, sup[:s], val[:s])
+
+    @property
+    def stream(self) -> int:
+        return int(_lib().l1b_problem_stream(self._h) or 0)
+
+    def set_stream(self, stream_ptr: int):
+        N.check(_lib().l1b_problem_set_stream(self._h, stream_ptr))
+
+    # -- constructors ---------------------------------------------------------
+    @classmethod
+    def from_host(cls, m, n, right_stages, sigma, b, tau, x_support=(), x_values=(),
+                  left_stages=(), p1=None, p2=None, device: int = 0) -> "ProblemInstance":
+        """Upload an instance described on the host (e.g. one the reference
+        generated): stages as (offset, theta) pairs in OperatorSpec order."""
+        ro = np.array([s[0] for s in right_stages], dtype=np.int32)
+        rt = np.array([s[1] for s in right_stages], dtype=np.float64)
+        lo = np.array([s[0] for s in left_stages], dtype=np.int32)
+        lt = np.array([s[1] for s in left_stages], dtype=np.float64)
+        sig = np.ascontiguousarray(sigma, dtype=np.float64)
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        if sig.shape != (n,) or bb.shape != (m,):
+            raise ValueError("ProblemInstance.from_host: sigma / b size mismatch")
+        p1a = None if p1 is None else np.ascontiguousarray(p1, dtype=np.uint32)
+        p2a = None if p2 is None else np.ascontiguousarray(p2, dtype=np.uint32)
+        d = N.OperatorDesc(m, n, len(ro), _ptr(ro, C.POINTER(C.c_int32)), _ptr(rt, _f64p), len(lo),
+                           _ptr(lo, C.POINTER(C.c_int32)), _ptr(lt, _f64p), _ptr(p1a, _u32p),
+                           _ptr(p2a, _u32p), _ptr(sig, _f64p))
+        sup = np.ascontiguousarray(x_support, dtype=np.uint32)
+        val = np.ascontiguousarray(x_values, dtype=np.float64)
+        h = C.c_void_p()
+        N.check(_lib().l1b_problem_create(device, C.byref(d), float(tau), _ptr(bb, _f64p),
+                                          _ptr(sup, _u32p), _ptr(val, _f64p), len(sup), C.byref(h)))
+        return cls(h)
+
+
+def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: int = 0,
+                   permute: bool = False, q: Optional[int] = 1, shift: float = 0.1,
+                   alternating: Optional[tuple] = None, sigma: Optional[np.ndarray] = None,
+                   gamma: float = 10.0, s_divisor: int = 128, tau: float = 1.0,
+                   theta: float = 0.6283185307179586, seed: int = 1, job_index: int = 0,
+                   fill_bound: float = 0.9, device: int = 0) -> ProblemInstance:
+    """``build_instance(cfg, enumerate_jobs(cfg)[job_index])`` for a single-job
+    ExperimentConfig (bench.cpp:216-316), generated on the GPU.  ``sigma`` gives
+    an explicit spectrum (Spectrum::from_values), ``alternating=(odd, even)`` the
+    alternating one, otherwise uniform in (0, 10^q] + shift."""
+    sig = None
+    g = N.GenDesc()
+    g.n, g.m_ratio, g.stages, g.left_stages, g.permute = n, m_ratio, stages, left_stages, int(permute)
+    if sigma is not None:
+        sig = np.ascontiguousarray(sigma, dtype=np.float64)
+        if sig.shape != (n,):
+            raise ValueError("Spectrum: realized value count mismatch")
+        g.spectrum_kind, g.sigma_explicit = N.SPECTRUM_EXPLICIT, _ptr(sig, _f64p)
+    elif alternating is not None:
+        g.spectrum_kind, g.odd_value, g.even_value = N.SPECTRUM_ALTERNATING, *alternating
+    else:
+        g.spectrum_kind, g.q = N.SPECTRUM_UNIFORM_Q, int(q)
+    g.shift, g.gamma, g.s_divisor, g.tau, g.theta = shift, gamma, s_divisor, tau, theta
+    g.seed, g.job_index, g.fill_bound = seed, job_index, fill_bound
+    h = C.c_void_p()
+    N.check(_lib().l1b_generate(device, C.byref(g), None, C.byref(h)))
+    return ProblemInstance(h)
+
+
+def verify_optimality(inst: ProblemInstance, tol: float) -> CertificateReport:
+    c = N.Cert()
+    N.check(_lib().l1b_verify_optimality(inst._h, float(tol), C.byref(c)))
+    return CertificateReport(c.max_support_violation, c.max_offsupport_violation, c.threshold, bool(c.pass_))
+
+
+def objective(inst: ProblemInstance, x) -> float:
+    """tau*||x||_1 + 1/2*||A x - b||^2 for a device vector x (solvers.cpp:145-151)."""
+    f = C.c_double()
+    N.check(_lib().l1b_objective(inst._h, _dptr(x), C.byref(f)))
+    return float(f.value)
+
+
+def soft_threshold(v: float, t: float) -> float:  # solvers.cpp:153-157 (host scalar helper)
+    if v > t:
+        return v - t
+    if v < -t:
+        return v + t
+    return 0.0
+
+
+def cd_damping(omega: int, varpi: int, n: int) -> float:  # solvers.cpp:266-270
+    if n <= 1 or varpi <= 1:
+        return 1.0
+    return 1.0 + float(omega - 1) * float(varpi - 1) / float(n - 1)
+
+
+def _trace_from(name: str, samples, k: int, s: N.Summary) -> SolverTrace:
+    tr = SolverTrace(name)
+    tr.samples = [TraceSample(int(samples[i].iter), samples[i].elapsed_s, samples[i].objective,
+                              int(samples[i].nnz), samples[i].matvecs, int(samples[i].extra))
+                  for i in range(k)]
+    tr.status = StopReason(s.status)
+    tr.reached_target = bool(s.reached_target)
+    tr.final_objective = s.final_objective
+    tr.elapsed_s = s.elapsed_s
+    tr.total_matvecs = s.total_matvecs
+    tr.total_pcg_iterations = int(s.total_pcg_iterations)
+    tr.newton_steps = int(s.newton_steps)
+    tr.time_to_target = s.time_to_target
+    tr.matvecs_to_target = s.matvecs_to_target
+    tr.iterations = int(s.iterations)
+    return tr
+
+
+def run_solver(inst: ProblemInstance, cfg: SolverConfig, x_out: Optional[np.ndarray] = None,
+               cap: int = 1 << 20) -> SolverTrace:
+    """run_solver (solvers.cpp:574-581).  When ``x_out`` (float64[n]) is given
+    the final iterate is copied into it, like the reference's x_out pointer."""
+    c = cfg.to_c()
+    cap = max(1, min(cap, cfg.max_iters + 4 if cfg.max_iters < cap else cap))
+    samples = (N.Sample * cap)()
+    summ = N.Summary()
+    if x_out is not None:
+        if x_out.dtype != np.float64 or x_out.shape != (inst.n,) or not x_out.flags.c_contiguous:
+            raise ValueError("x_out must be a contiguous float64 array of length n")
+    N.check(_lib().l1b_solve(inst._h, C.byref(c), samples, cap, C.byref(summ), _ptr(x_out, _f64p), None))
+    name = {"cd": "cd", "newton_cg": "newton_cg", "fista": "fista", "ista": "ista", "pcdm": "pcdm"}[cfg.id]
+    return _trace_from(name, samples, min(int(summ.n_samples), cap), summ)
+
+
+def _with_id(cfg: SolverConfig, ident: str) -> SolverConfig:
+    from dataclasses import replace
+
+    return replace(cfg, id=ident)
+
+
+def fista_run(inst, cfg: SolverConfig, x_out=None) -> SolverTrace:
+    return run_solver(inst, _with_id(cfg, "fista"), x_out)
+
+
+def ista_run(inst, cfg: SolverConfig, x_out=None) -> SolverTrace:
+    return run_solver(inst, _with_id(cfg, "ista"), x_out)
+
+
+def coordinate_descent_run(inst, cfg: SolverConfig, x_out=None) -> SolverTrace:
+    return run_solver(inst, _with_id(cfg, "cd"), x_out)
+
+
+def newton_cg_run(inst, cfg: SolverConfig, x_out=None) -> SolverTrace:
+    return run_solver(inst, _with_id(cfg, "newton_cg"), x_out)
+
+
+def pcdm_run(inst, cfg: SolverConfig, x_out=None) -> SolverTrace:
+    return run_solver(inst, _with_id(cfg, "pcdm"), x_out)
+
+
+def known_solver(ident: str) -> bool:  # solvers.cpp:570-572 (+ pcdm)
+    return ident in SolverConfig._IDS
+
+
+class Session:
+    """Stepping handle over the device-resident FISTA/ISTA loop (bench.py)."""
+
+    def __init__(self, inst: ProblemInstance, cfg: SolverConfig):
+        self.inst = inst
+        c = cfg.to_c()
+        self._s = C.c_void_p()
+        N.check(_lib().l1b_session_begin(inst._h, C.byref(c), C.byref(self._s)))
+        self._name = cfg.id
+
+    def step(self, iters: int):
+        N.check(_lib().l1b_session_step(self._s, int(iters)))
+
+    def profile(self, iters: int):
+        ms = (C.c_double * 2)()
+        N.check(_lib().l1b_session_profile(self._s, int(iters), ms, 2))
+        return [ms[0], ms[1]]
+
+    def sync(self):
+        stopped, k = C.c_int(), C.c_uint64()
+        N.check(_lib().l1b_session_sync(self._s, C.byref(stopped), C.byref(k)))
+        return bool(stopped.value), int(k.value)
+
+    def end(self, x_out: Optional[np.ndarray] = None, cap: int = 1 << 16) -> SolverTrace:
+        samples = (N.Sample * cap)()
+        summ = N.Summary()
+        s, self._s = self._s, None
+        N.check(_lib().l1b_session_end(s, samples, cap, C.byref(summ), _ptr(x_out, _f64p)))
+        return _trace_from(self._name, samples, min(int(summ.n_samples), cap), summ)
+
+
+def launch_count() -> int:
+    return int(_lib().l1b_launch_count())

@@ -1,0 +1,82 @@
+"""CPU: the C-ABI library loads, exports every symbol include/l1b.h declares,
+and refuses to compute without a GPU (no silent CPU fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "l1b.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    names = set(re.findall(r"^[A-Za-z_][\w \*]*?\b(l1b_\w+)\s*\(", text, flags=re.M))
+    return sorted(names)
+
+
+def test_header_declares_abi():
+    names = declared_functions()
+    assert "l1b_solve" in names and "l1b_generate" in names and len(names) >= 25
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1503_03520_b200 import _native
+
+    lib = _native.load()
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    bound = {s[0] for s in _native.SIGNATURES}
+    assert set(declared_functions()) == bound
+
+
+def test_library_is_sm100a_only():
+    from paper_1503_03520_b200 import _native
+
+    data = open(_native.LIB_PATH, "rb").read()
+    assert b"sm_100a" in data
+
+
+def test_host_rng_primitives_match_oracle(oracle):
+    """The product's host RNG streams (std::mt19937_64) equal the oracle's."""
+    import numpy as np
+
+    from paper_1503_03520_b200 import _native as N
+
+    lib = N.load()
+    assert lib.l1b_mix_seed(3, 0) == oracle.mix_seed(3, 0)
+    mp = np.empty(1000, dtype=np.uint32)
+    N.check(lib.l1b_realize_permutation(1000, 77, mp.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    ref_map = np.empty(1000, dtype=np.uint32)
+    inv = np.empty(1000, dtype=np.uint32)
+    oracle.lib.lo_permutation_realize(1000, 77, ref_map.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                      inv.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+    np.testing.assert_array_equal(mp, ref_map)
+    sig = np.empty(500)
+    N.check(lib.l1b_realize_spectrum_uniform(500, 0.0, 10.0, 0.1, 9, sig.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    ref = np.empty(500)
+    oracle.lib.lo_spectrum_uniform(500, 0.0, 10.0, 0.1, 9, ref.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    np.testing.assert_array_equal(sig, ref)
+
+
+def test_compute_without_gpu_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    from paper_1503_03520_b200 import l1bench
+
+    with pytest.raises(Exception):
+        l1bench.build_instance(64, stages=1)
+
+
+def test_invalid_arguments_map_to_value_error():
+    from paper_1503_03520_b200 import l1bench
+
+    with pytest.raises(ValueError):
+        l1bench.SolverConfig(id="bogus").to_c()
+    with pytest.raises(ValueError):
+        l1bench.build_instance(1)  # ExperimentConfig: dimensions must be at least 2
