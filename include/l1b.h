@@ -131,7 +131,7 @@ typedef struct {
   double tau, noise_norm, cert_kappa, gram_lmax, f_star;
   uint64_t device_bytes;  /* HBM held by the problem */
   uint64_t row_begin, row_end, col_begin, col_end; /* shard ranges */
-  int csr_lanes, csc_lanes; /* lanes per row / per column in the SpMV kernels */
+  int csr_lanes, csc_lanes; /* lines per warp tile in the SpMV kernels */
 } l1b_problem_info;
 
 int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* out);

@@ -144,12 +144,6 @@ T* upload(const T* host, size_t count, cudaStream_t st, size_t* bytes_acc) {
   return p;
 }
 
-uint64_t pow2_ceil_lanes(double mean) {
-  uint64_t g = 1;
-  while ((double)g < mean && g < 32) g <<= 1;
-  return g;
-}
-
 }  // namespace
 
 struct l1b_problem {
@@ -191,7 +185,7 @@ struct l1b_problem {
     c.ptr = csr.ptr;
     c.idx = csr.idx;
     c.val = csr.val;
-    c.lanes = (int)pow2_ceil_lanes(csr.lines ? (double)csr.nnz / (double)csr.lines : 1.0);
+    c.lanes = 32;
     return c;
   }
   Csr cols() const {
@@ -202,7 +196,7 @@ struct l1b_problem {
     c.ptr = csc.ptr;
     c.idx = csc.idx;
     c.val = csc.val;
-    c.lanes = (int)pow2_ceil_lanes(csc.lines ? (double)csc.nnz / (double)csc.lines : 1.0);
+    c.lanes = 32;
     return c;
   }
 };

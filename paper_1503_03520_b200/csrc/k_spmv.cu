@@ -2,15 +2,12 @@
 // solver epilogues, and the FISTA/ISTA device loop (solvers.cpp:277-382).
 //
 // Kernel shape (HBM-bound, ~0.17 flop/B; no tensor cores -- not a dense
-// contraction): G lanes per line (G = next pow2 of the mean line length, 8 for
-// the 4-stage instances), a warp covers 32/G consecutive lines so the value and
-// index streams are read as contiguous 256 B / 128 B segments; partial
-// products are combined with a width-G shuffle tree.  The matrix streams are
-// loaded with the evict-first hint (ld.global.cs) so the gathered vector stays
-// L2-resident; the epilogue runs on the group leader and touches each vector
-// element exactly once.  Scalars (||x||_1, nnz, ||r||^2, ...) are reduced per
-// block and folded by the last block in a fixed order: results are
-// deterministic run to run.
+// contraction): one warp per tile of 32 consecutive lines (see spmv_kernel).
+// The matrix streams are loaded with the evict-first hint (ld.global.cs) so
+// the gathered vector stays L2-resident; each vector element of the epilogue
+// is touched exactly once, by a coalesced warp access.  Scalars (||x||_1,
+// nnz, ||r||^2, ...) are reduced per block and folded by the last block in a
+// fixed order: results are deterministic run to run.
 #include <cmath>
 
 #include "common.cuh"
@@ -20,13 +17,24 @@ namespace l1b {
 
 namespace {
 
-template <typename PtrT>
-__device__ __forceinline__ PtrT ld_ptr(const PtrT* p) {
-  return __ldg(p);
-}
+// The SpMV skeleton ("row tile per warp"): a warp owns 32 consecutive lines.
+//  1. lane l loads ptr[r0+l] and ptr[r0+l+1]: the tile's nonzeros are the
+//     contiguous range [ptr[r0], ptr[r0+32]);
+//  2. the warp streams that range with coalesced 8 B value / 4 B index loads
+//     (U = 8 independent loads per lane in flight, evict-first), gathers x and
+//     parks the products in shared memory (padded one slot per 16 to avoid
+//     bank conflicts for the 8-entry rows);
+//  3. lane l sums its own line's products in ascending index order (the
+//     reference's sequential dot order) and runs the epilogue for line r0+l,
+//     so every epilogue load/store is a coalesced 256 B warp access.
+// Tiles with more than kCap nonzeros are processed in kCap-sized chunks.
+// Epi provides: skip(), start(), line(i, value), finish().
+constexpr int kCapNnz = 256;
+constexpr int kUnroll = 8;
 
-// The SpMV skeleton.  Epi provides: skip(), line(i, value), finish().
-template <typename PtrT, int G, class Epi>
+__device__ __forceinline__ int pad(int off) { return off + (off >> 4); }
+
+template <typename PtrT, class Epi>
 __global__ void __launch_bounds__(kThreads) spmv_kernel(const PtrT* __restrict__ ptr,
                                                         const uint32_t* __restrict__ idx,
                                                         const double* __restrict__ val,
@@ -34,21 +42,44 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(const PtrT* __restrict__
                                                         uint64_t nlines, Epi epi) {
   if (epi.skip()) return;
   epi.start();
-  constexpr int LPW = 32 / G;
+  __shared__ double prod_all[kThreads / 32][kCapNnz + kCapNnz / 16];
   const int lane = threadIdx.x & 31;
-  const int sub = lane & (G - 1);
+  double* sp = prod_all[threadIdx.x >> 5];
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t base = warp * LPW; base < nlines; base += nwarps * LPW) {
-    const uint64_t line = base + (uint64_t)(lane / G);
+  for (uint64_t tile = warp; tile * 32 < nlines; tile += nwarps) {
+    const uint64_t line = tile * 32 + lane;
+    const bool live = line < nlines;
+    const PtrT my_s = __ldg(ptr + (live ? line : nlines));
+    const PtrT my_e = __ldg(ptr + (live ? line + 1 : nlines));
+    const PtrT rs = __shfl_sync(0xffffffffu, my_s, 0);
+    const PtrT re = __shfl_sync(0xffffffffu, my_e, 31);
     double sum = 0.0;
-    if (line < nlines) {
-      const PtrT s = ld_ptr(ptr + line), e = ld_ptr(ptr + line + 1);
-      for (PtrT p = s + sub; p < e; p += G) sum += __ldcs(val + p) * __ldg(x + __ldcs(idx + p));
-    }
+    for (PtrT chunk = rs; chunk < re; chunk += kCapNnz) {
+      const PtrT cend = min((PtrT)(chunk + kCapNnz), re);
+      for (PtrT q0 = chunk + lane; q0 < cend; q0 += 32 * kUnroll) {
+        uint32_t ii[kUnroll];
+        double vv[kUnroll];
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
-    if (sub == 0 && line < nlines) epi.line(line, sum);
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + 32 * u;
+          if (q < cend) {
+            ii[u] = __ldcs(idx + q);
+            vv[u] = __ldcs(val + q);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + 32 * u;
+          if (q < cend) sp[pad((int)(q - chunk))] = vv[u] * __ldg(x + ii[u]);
+        }
+      }
+      __syncwarp();
+      const PtrT a = max(my_s, chunk), e = min(my_e, cend);
+      for (PtrT q = a; q < e; ++q) sum += sp[pad((int)(q - chunk))];
+      __syncwarp();
+    }
+    if (live) epi.line(line, sum);
   }
   epi.finish();
 }
@@ -235,35 +266,21 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
 }
 
 // ---------------------------------------------------------------------------
-// dispatch over (pointer width, lanes)
-
-template <class Epi, typename PtrT, int G>
-void launch_g(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
-  static int grid_cap = 0;
-  if (!grid_cap) {
-    int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_kernel<PtrT, G, Epi>,
-                                                          kThreads, 0));
-    grid_cap = std::max(1, per_sm) * sm_count();
-  }
-  const uint64_t warps = (M.lines + (32 / G) - 1) / (32 / G);
-  const uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)grid_cap));
-  spmv_kernel<PtrT, G, Epi><<<grid, kThreads, 0, st>>>((const PtrT*)M.ptr, M.idx, M.val, x,
-                                                      M.lines, epi);
-  L1B_LAUNCHED();
-}
+// dispatch over the pointer width
 
 template <class Epi, typename PtrT>
 void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
-  switch (M.lanes) {
-    case 1: return launch_g<Epi, PtrT, 1>(M, x, epi, st);
-    case 2: return launch_g<Epi, PtrT, 2>(M, x, epi, st);
-    case 4: return launch_g<Epi, PtrT, 4>(M, x, epi, st);
-    case 8: return launch_g<Epi, PtrT, 8>(M, x, epi, st);
-    case 16: return launch_g<Epi, PtrT, 16>(M, x, epi, st);
-    default: return launch_g<Epi, PtrT, 32>(M, x, epi, st);
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_kernel<PtrT, Epi>, kThreads, 0));
+    grid_cap = std::max(1, per_sm) * sm_count();
   }
+  const uint64_t tiles = (M.lines + 31) / 32;
+  const uint64_t blocks = (tiles + (kThreads / 32) - 1) / (kThreads / 32);
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)grid_cap));
+  spmv_kernel<PtrT, Epi><<<grid, kThreads, 0, st>>>((const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi);
+  L1B_LAUNCHED();
 }
 
 template <class Epi>

@@ -47,7 +47,7 @@ struct Csr {  // CSR of A (rows) or of A^T (= CSC of A)
   const void* ptr = nullptr;
   const uint32_t* idx = nullptr;
   const double* val = nullptr;
-  int lanes = 8;
+  int lanes = 32;  // lines per warp tile
 };
 
 // y[0, lines) = M x

@@ -178,6 +178,33 @@ class CertificateReport:  # instance.hpp:58-63
     passed: bool
 
 
+def _ext_stream(inst):
+    import torch
+
+    if inst._ext is None:
+        inst._ext = torch.cuda.ExternalStream(inst.stream)
+    return inst._ext
+
+
+class _Ordered:
+    """Orders library work on the problem's stream after the caller's current
+    torch stream (inputs ready) and the caller's stream after it (outputs
+    ready) -- the C ABI only promises ordering on its own stream."""
+
+    def __init__(self, inst):
+        self.inst = inst
+
+    def __enter__(self):
+        import torch
+
+        _ext_stream(self.inst).wait_stream(torch.cuda.current_stream())
+
+    def __exit__(self, *a):
+        import torch
+
+        torch.cuda.current_stream().wait_stream(_ext_stream(self.inst))
+
+
 class DeviceOperator:
     """LinearOperator view of a problem's A on the GPU (linops.hpp:139-155).
 
@@ -202,7 +229,8 @@ class DeviceOperator:
         if x.shape != (self.cols(),):
             raise ValueError(f"OperatorSpec::apply: expected length {self.cols()}, got {tuple(x.shape)}")
         out = torch.empty(self.rows(), dtype=torch.float64, device=x.device) if out is None else out
-        N.check(_lib().l1b_apply(self._inst._h, self._path(path), _dptr(x), _dptr(out)))
+        with _Ordered(self._inst):
+            N.check(_lib().l1b_apply(self._inst._h, self._path(path), _dptr(x), _dptr(out)))
         return out
 
     def apply_transpose(self, y, out=None, path: str = "sparse"):
@@ -211,21 +239,24 @@ class DeviceOperator:
         if y.shape != (self.rows(),):
             raise ValueError(f"OperatorSpec::apply_transpose: expected length {self.rows()}, got {tuple(y.shape)}")
         out = torch.empty(self.cols(), dtype=torch.float64, device=y.device) if out is None else out
-        N.check(_lib().l1b_apply_transpose(self._inst._h, self._path(path), _dptr(y), _dptr(out)))
+        with _Ordered(self._inst):
+            N.check(_lib().l1b_apply_transpose(self._inst._h, self._path(path), _dptr(y), _dptr(out)))
         return out
 
     def apply_gram_inverse(self, v, out=None):
         import torch
 
         out = torch.empty(self.cols(), dtype=torch.float64, device=v.device) if out is None else out
-        N.check(_lib().l1b_gram_inverse(self._inst._h, _dptr(v), _dptr(out)))
+        with _Ordered(self._inst):
+            N.check(_lib().l1b_gram_inverse(self._inst._h, _dptr(v), _dptr(out)))
         return out
 
     def gram_diagonal(self, device="cuda"):
         import torch
 
         out = torch.empty(self.cols(), dtype=torch.float64, device=device)
-        N.check(_lib().l1b_gram_diagonal(self._inst._h, _dptr(out)))
+        with _Ordered(self._inst):
+            N.check(_lib().l1b_gram_diagonal(self._inst._h, _dptr(out)))
         return out
 
     def gram_lmax(self) -> float:
@@ -255,6 +286,7 @@ class ProblemInstance:
 
     def __init__(self, handle):
         self._h = handle
+        self._ext = None
         self.info = N.ProblemInfo()
         N.check(_lib().l1b_problem_info_get(self._h, C.byref(self.info)))
         self.op = DeviceOperator(self)
@@ -322,6 +354,7 @@ class ProblemInstance:
 
     def set_stream(self, stream_ptr: int):
         N.check(_lib().l1b_problem_set_stream(self._h, stream_ptr))
+        self._ext = None
 
     # -- constructors ---------------------------------------------------------
     @classmethod
@@ -388,7 +421,8 @@ def verify_optimality(inst: ProblemInstance, tol: float) -> CertificateReport:
 def objective(inst: ProblemInstance, x) -> float:
     """tau*||x||_1 + 1/2*||A x - b||^2 for a device vector x (solvers.cpp:145-151)."""
     f = C.c_double()
-    N.check(_lib().l1b_objective(inst._h, _dptr(x), C.byref(f)))
+    with _Ordered(inst):
+        N.check(_lib().l1b_objective(inst._h, _dptr(x), C.byref(f)))
     return float(f.value)
 
 

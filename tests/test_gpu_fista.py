@@ -47,7 +47,7 @@ def test_stop_rules():
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
-    inst = device_build("k4")
+    inst = device_build("odd")  # needs ~1400 iterations, no early fixed point
     # target already met at x0 -> no iteration (solvers.cpp:312)
     tr = l1bench.fista_run(inst, l1bench.SolverConfig(target_objective=1e300))
     assert tr.status == l1bench.StopReason.target_reached and tr.iterations == 0
