@@ -186,6 +186,7 @@ struct l1b_problem {
     c.idx = csr.idx;
     c.val = csr.val;
     c.lanes = 32;
+    c.tile_nnz_max = csr.tile_nnz_max;
     return c;
   }
   Csr cols() const {
@@ -197,6 +198,7 @@ struct l1b_problem {
     c.idx = csc.idx;
     c.val = csc.val;
     c.lanes = 32;
+    c.tile_nnz_max = csc.tile_nnz_max;
     return c;
   }
 };
@@ -685,6 +687,7 @@ ProblemView problem_view(l1b_problem* p) {
   v.At = p->cols();
   v.op = &p->view;
   v.gram = nullptr;
+  v.max_row_nnz = p->csr.max_len;
   return v;
 }
 const double* problem_gram(l1b_problem* p) { return gram_diag_device(p); }

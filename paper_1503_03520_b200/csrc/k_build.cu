@@ -186,6 +186,18 @@ __global__ void fill_lines(OpView op, bool rows, uint64_t first, uint64_t nlines
   }
 }
 
+__global__ void tile_max_kernel(const uint64_t* offs, uint64_t lines, uint64_t tile,
+                                unsigned long long* out) {
+  unsigned long long mx = 0;
+  const uint64_t ntiles = (lines + tile - 1) / tile;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = t * tile, b = min(a + tile, lines);
+    mx = max(mx, (unsigned long long)(offs[b] - offs[a]));
+  }
+  if (mx) atomicMax(out, mx);
+}
+
 __global__ void widen_u32(const uint32_t* in, uint64_t* out, uint64_t n) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
        t += (uint64_t)gridDim.x * blockDim.x)
@@ -299,10 +311,11 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
   }
   out->nnz = total;
   out->ptr32 = total < (1ull << 32);
+  // +16 B slack: the TMA stages copy 16-byte aligned supersets of each range
   const size_t ptr_bytes = (keep + 1) * (out->ptr32 ? 4 : 8);
-  if (cudaMalloc(&out->ptr, ptr_bytes) != cudaSuccess ||
-      cudaMalloc(&out->idx, std::max<uint64_t>(total, 1) * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMalloc(&out->val, std::max<uint64_t>(total, 1) * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&out->ptr, ptr_bytes + 16) != cudaSuccess ||
+      cudaMalloc(&out->idx, (total + 4) * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&out->val, (total + 2) * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     cudaFreeAsync(counts, st);
     cudaFreeAsync(offs, st);
@@ -321,10 +334,18 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
   } else {
     L1B_CUDA(cudaMemsetAsync(out->ptr, 0, ptr_bytes, st));
   }
+  // largest nonzero count of a 256-line tile (selects the TMA SpMV kernel)
+  L1B_CUDA(cudaMemsetAsync(scratch, 0, sizeof(Scratch), st));
+  if (keep > 0) {
+    tile_max_kernel<<<grid_for((keep + 255) / 256), kThreads, 0, st>>>(offs, keep, 256, &scratch->last);
+    L1B_LAUNCHED();
+  }
+  L1B_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(Scratch), cudaMemcpyDeviceToHost, st));
   L1B_CUDA(cudaFreeAsync(counts, st));
   L1B_CUDA(cudaFreeAsync(offs, st));
   L1B_CUDA(cudaFreeAsync(scratch, st));
   L1B_CUDA(cudaStreamSynchronize(st));
+  out->tile_nnz_max = h.last;
 }
 
 void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, cudaStream_t st) {

@@ -1,0 +1,510 @@
+// k_ncg.cu -- Newton-CG on the pseudo-Huber smoothed problem (pdNCG, C3):
+// newton_cg_run + pcg_solve (solvers.cpp:159-264, 487-568) on device.
+//
+// Per Newton step (host loop, one sync per step):
+//   grad kernel  (CSC):  grad = A^T r + tau x/sqrt(mu^2+x^2), d2psi, precond,
+//                        partials of ||x||_1, nnz, psi, ||grad||^2
+//   PCG (device loop, four kernels per iteration, no host round trip):
+//     Ka (CSR)  hav = A p
+//     Kb (CSC)  hp  = A^T hav + tau d2psi p, p.hp -> alpha / breakdown
+//     Kc        step += alpha p, r -= alpha hp, ||r||^2 and r.z partials ->
+//               best / convergence / beta
+//     Kd        best = step (if improved), p = z + beta p
+//   ad = A step (CSR), slope = grad.step, then Armijo backtracking with
+//   eight trial steps per pass (one fused reduction kernel for all eight).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "solvers.hpp"
+#include "spmv.cuh"
+
+namespace l1b {
+
+namespace {
+
+constexpr int kLs = 8;  // trial steps evaluated per line-search pass
+
+struct NcgDev {
+  double tau, mu;
+  // grad pass
+  double l1, nnz, psi, gg;
+  // PCG state (solvers.cpp:211-264)
+  double rz, php, alpha, beta, rn, best_norm, rhs_norm, eta, rr_pcg, rz_next;
+  uint64_t iterations, max_iters;
+  int done, converged, negcurv, error, improved, pad;
+  unsigned int ticket[4];
+  double ls[2 * kLs];  // psi(x + a s), ||r + a ad||^2 per trial
+  double slope;
+};
+
+// -- grad pass (solvers.cpp:522-529) ---------------------------------------
+struct EpiGrad {
+  const double* x;
+  const double* gram;
+  double* grad;
+  double* d2psi;
+  double* precond;
+  NcgDev* st;
+  double* partials;
+  double tau, mu;
+  double acc[4];  // ||x||_1, nnz(x), psi(x), ||grad||^2
+  static constexpr int kVec = 2;  // x, diag(A^T A) at the column
+  __host__ __device__ const double* vec(int v) const { return v == 0 ? x : gram; }
+  __device__ bool skip() const { return false; }
+  __device__ void start() {
+    tau = st->tau;
+    mu = st->mu;
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+  }
+  __device__ void line(uint64_t j, double g, const double* pv) {
+    const double xj = pv[0];
+    const double q = mu * mu + xj * xj;
+    const double root = sqrt(q);
+    const double gj = g + tau * xj / root;
+    const double d = mu * mu / (q * root);
+    grad[j] = gj;
+    d2psi[j] = d;
+    precond[j] = tau * d + pv[1];
+    acc[0] += fabs(xj);
+    acc[1] += xj != 0.0 ? 1.0 : 0.0;
+    acc[2] += root - mu;  // pseudo_huber term (solvers.cpp:162)
+    acc[3] += gj * gj;
+  }
+  __device__ void finish() {
+    double tot[4];
+    if (grid_sum<4>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) {
+      st->l1 = tot[0];
+      st->nnz = tot[1];
+      st->psi = tot[2];
+      st->gg = tot[3];
+    }
+  }
+};
+
+// -- PCG ----------------------------------------------------------------------
+// r = rhs = -grad, z = r / precond, p = z, step = best = 0, rz = r.z
+__global__ void pcg_init_kernel(const double* __restrict__ grad, const double* __restrict__ pre,
+                                double* r, double* p, double* step, double* best, uint64_t n,
+                                NcgDev* st, double* partials) {
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double ri = -grad[i];
+    const double zi = ri / pre[i];
+    r[i] = ri;
+    p[i] = zi;
+    step[i] = 0.0;
+    best[i] = 0.0;
+    acc[0] += ri * zi;
+  }
+  double tot[1];
+  if (grid_sum<1>(acc, partials, &st->ticket[1], tot) && threadIdx.x == 0) {
+    st->rz = tot[0];
+    st->iterations = 0;
+    st->best_norm = st->rhs_norm;
+    st->done = st->rhs_norm == 0.0 || st->max_iters == 0;
+    st->converged = st->rhs_norm == 0.0;
+    st->negcurv = 0;
+    st->error = 0;
+    st->improved = 0;
+  }
+}
+
+struct EpiHav {  // Ka: hav = A p
+  double* hav;
+  const NcgDev* st;
+  static constexpr int kVec = 0;
+  __host__ __device__ const double* vec(int) const { return nullptr; }
+  __device__ bool skip() const { return *(volatile const int*)&st->done; }
+  __device__ void start() {}
+  __device__ void line(uint64_t i, double s, const double*) { hav[i] = s; }
+  __device__ void finish() {}
+};
+
+struct EpiHp {  // Kb: hp = A^T hav + tau d2psi p  (solvers.cpp:537-541), p.hp
+  const double* p;
+  const double* d2psi;
+  double* hp;
+  NcgDev* st;
+  double* partials;
+  double tau;
+  double acc[1];
+  static constexpr int kVec = 2;  // p, d2psi at the column
+  __host__ __device__ const double* vec(int v) const { return v == 0 ? p : d2psi; }
+  __device__ bool skip() const { return *(volatile const int*)&st->done; }
+  __device__ void start() {
+    tau = st->tau;
+    acc[0] = 0.0;
+  }
+  __device__ void line(uint64_t j, double g, const double* pv) {
+    const double pj = pv[0];
+    const double h = g + tau * pv[1] * pj;
+    hp[j] = h;
+    acc[0] += pj * h;
+  }
+  __device__ void finish() {
+    double tot[1];
+    if (grid_sum<1>(acc, partials, &st->ticket[2], tot) && threadIdx.x == 0) {
+      const double php = tot[0];  // solvers.cpp:231-237
+      st->php = php;
+      if (!(php > 0.0)) {
+        if (!isfinite(php)) st->error = 1;
+        st->negcurv = 1;
+        st->done = 1;
+      } else {
+        st->alpha = st->rz / php;
+      }
+    }
+  }
+};
+
+// Kc: step += alpha p; r -= alpha hp (:238-241); ||r||, best, convergence;
+// r.z for the next direction (:255-258)
+__global__ void pcg_update_kernel(const double* __restrict__ p, const double* __restrict__ hp,
+                                  const double* __restrict__ pre, double* step, double* r,
+                                  uint64_t n, NcgDev* st, double* partials) {
+  if (*(volatile int*)&st->done) return;
+  const double alpha = st->alpha;
+  double acc[2] = {0.0, 0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    step[i] += alpha * p[i];
+    const double ri = r[i] - alpha * hp[i];
+    r[i] = ri;
+    acc[0] += ri * ri;
+    acc[1] += ri * (ri / pre[i]);
+  }
+  double tot[2];
+  if (grid_sum<2>(acc, partials, &st->ticket[3], tot) && threadIdx.x == 0) {
+    const double rn = sqrt(tot[0]);
+    st->iterations += 1;
+    st->rn = rn;
+    st->improved = 0;
+    if (!isfinite(rn)) {
+      st->error = 2;
+      st->done = 1;
+      return;
+    }
+    if (rn < st->best_norm) {
+      st->best_norm = rn;
+      st->improved = 1;
+    }
+    if (rn <= st->eta * st->rhs_norm) {
+      st->converged = 1;
+      st->done = 1;
+      return;
+    }
+    st->rz_next = tot[1];
+    st->beta = tot[1] / st->rz;
+    st->rz = tot[1];
+    if (st->iterations >= st->max_iters) st->done = 1;
+  }
+}
+
+// Kd: best = step when improved (:245-248); p = z + beta p (:259).  Safe to
+// re-run after the solve stopped: the copy is idempotent (step no longer
+// changes) and p only moves while !done; the last block clears `improved` so
+// trailing launches of a chunk return immediately.
+__global__ void pcg_direction_kernel(const double* __restrict__ r, const double* __restrict__ pre,
+                                     const double* __restrict__ step, double* p, double* best,
+                                     uint64_t n, NcgDev* st, unsigned int* ticket) {
+  const int improved = *(volatile int*)&st->improved;
+  const bool more = !*(volatile int*)&st->done;
+  if (!improved && !more) return;
+  const double beta = st->beta;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (improved) best[i] = step[i];
+    if (more) p[i] = r[i] / pre[i] + beta * p[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+      st->improved = 0;
+      *ticket = 0u;
+    }
+  }
+}
+
+// -- line search (solvers.cpp:551-560): eight trials per pass ---------------
+__global__ void ls_eval_kernel(const double* __restrict__ x, const double* __restrict__ s,
+                               const double* __restrict__ r, const double* __restrict__ ad,
+                               uint64_t n, uint64_t m_act, double alpha0, NcgDev* st,
+                               double* partials, unsigned int* ticket) {
+  double acc[2 * kLs];
+#pragma unroll
+  for (int k = 0; k < 2 * kLs; ++k) acc[k] = 0.0;
+  const double mu = st->mu;
+  const uint64_t lim = n > m_act ? n : m_act;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lim;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    double a = alpha0;
+    if (i < n) {
+      const double xi = x[i], si = s[i];
+#pragma unroll
+      for (int k = 0; k < kLs; ++k) {
+        const double xt = xi + a * si;  // x_trial (:554)
+        acc[k] += sqrt(mu * mu + xt * xt) - mu;
+        a *= 0.5;
+      }
+    }
+    a = alpha0;
+    if (i < m_act) {
+      const double ri = r[i], di = ad[i];
+#pragma unroll
+      for (int k = 0; k < kLs; ++k) {
+        const double rt = ri + a * di;  // r_trial (:555)
+        acc[kLs + k] += rt * rt;
+        a *= 0.5;
+      }
+    }
+  }
+  double tot[2 * kLs];
+  if (grid_sum<2 * kLs>(acc, partials, ticket, tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 2 * kLs; ++k) st->ls[k] = tot[k];
+  }
+}
+
+__global__ void ls_accept_kernel(double* x, const double* __restrict__ s, double* r,
+                                 const double* __restrict__ ad, uint64_t n, uint64_t m_act,
+                                 double alpha) {
+  const uint64_t lim = n > m_act ? n : m_act;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < lim;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i < n) x[i] = x[i] + alpha * s[i];
+    if (i < m_act) r[i] = r[i] + alpha * ad[i];
+  }
+}
+
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, uint64_t n,
+                           double* partials, unsigned int* ticket, double* out) {
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc[0] += a[i] * b[i];
+  double tot[1];
+  if (grid_sum<1>(acc, partials, ticket, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+__global__ void neg_residual_kernel(const double* __restrict__ b, double* r, uint64_t m) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    r[i] = 0.0 - b[i];
+}
+
+}  // namespace
+
+void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+                   l1b_summary* sum, double* x_host, double* d_x) {
+  const ProblemView v = problem_view(p);
+  const uint64_t n = v.n, m = v.m, ma = v.A.lines;
+  const double tau = v.tau, mu = cfg->mu;
+  cudaStream_t st = v.stream;
+  const double* gram = problem_gram(p);
+  std::vector<void*> bufs;
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
+    bufs.push_back((void*)*ptr);
+  };
+  double *x, *r, *grad, *d2psi, *pre, *ad, *hav, *rp, *pp, *hp, *step, *best, *partials, *scal;
+  unsigned int* tickets;
+  NcgDev* dst;
+  NcgDev* h = nullptr;
+  std::vector<l1b_sample> out;
+  auto fail = [&]() {
+    cudaStreamSynchronize(st);
+    for (void* q : bufs) cudaFree(q);
+    if (h) cudaFreeHost(h);
+  };
+  try {
+    alloc(&x, n * 8);
+    alloc(&r, m * 8);
+    alloc(&grad, n * 8);
+    alloc(&d2psi, n * 8);
+    alloc(&pre, n * 8);
+    alloc(&ad, m * 8);
+    alloc(&hav, m * 8);
+    alloc(&rp, n * 8);
+    alloc(&pp, n * 8);
+    alloc(&hp, n * 8);
+    alloc(&step, n * 8);
+    alloc(&best, n * 8);
+    alloc(&partials, (size_t)spmv_grid_max() * 2 * kLs * 8);
+    alloc(&scal, 8 * 8);
+    alloc(&tickets, 8 * 4);
+    alloc(&dst, sizeof(NcgDev));
+    L1B_CUDA(cudaMallocHost(&h, sizeof(NcgDev)));
+    L1B_CUDA(cudaMemsetAsync(tickets, 0, 8 * 4, st));
+    L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
+    L1B_CUDA(cudaMemsetAsync(ad, 0, m * 8, st));
+    std::memset(h, 0, sizeof(NcgDev));
+    h->tau = tau;
+    h->mu = mu;
+    h->eta = cfg->eta;
+    h->max_iters = cfg->pcg_max_iters;
+    L1B_CUDA(cudaMemcpyAsync(dst, h, sizeof(NcgDev), cudaMemcpyHostToDevice, st));
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] {
+      return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    uint64_t mv = 0;  // CountingOperator
+    // grad_tol = grad_tol_rel * max(1, ||A^T b||) (solvers.cpp:498-500)
+    spmv(v.At, v.b, grad, st);
+    ++mv;
+    dot_kernel<<<grid_for(n), kThreads, 0, st>>>(grad, grad, n, partials, tickets + 4, scal);
+    L1B_LAUNCHED();
+    double atb_sq = 0.0;
+    L1B_CUDA(cudaMemcpyAsync(&atb_sq, scal, 8, cudaMemcpyDeviceToHost, st));
+    // r = A*0 - b (:503-505)
+    neg_residual_kernel<<<grid_for(m), kThreads, 0, st>>>(v.b, r, m);
+    L1B_LAUNCHED();
+    ++mv;
+    dot_kernel<<<grid_for(ma), kThreads, 0, st>>>(r, r, ma, partials, tickets + 4, scal + 1);
+    L1B_LAUNCHED();
+    double rr = 0.0;
+    L1B_CUDA(cudaMemcpyAsync(&rr, scal + 1, 8, cudaMemcpyDeviceToHost, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    rr += v.tail_sq;
+    const double grad_tol = cfg->grad_tol_rel * std::max(1.0, std::sqrt(atb_sq));
+    int status = L1B_ITER_BUDGET;
+    uint64_t newton = 0, last_pcg = 0, total_pcg = 0;
+    bool reached = false;
+    double time_to = INFINITY, mv_to = INFINITY, f_last = NAN;
+    while (true) {
+      // grad pass: also yields ||x||_1, nnz, psi for f_true / f_smooth
+      launch(v.At, r, EpiGrad{x, gram, grad, d2psi, pre, dst, partials, 0, 0, {0, 0, 0, 0}}, st);
+      L1B_CUDA(cudaMemcpyAsync(h, dst, sizeof(NcgDev), cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+      ++mv;
+      const double f_true = tau * h->l1 + 0.5 * rr;  // :515
+      if (!std::isfinite(f_true))
+        throw std::runtime_error("newton_cg: objective diverged to a non-finite value");
+      l1b_sample smp{newton, elapsed(), f_true, (uint64_t)h->nnz, (double)(mv - 1), last_pcg};
+      out.push_back(smp);
+      f_last = f_true;
+      if (!reached && cfg->has_target && f_true <= cfg->target) {
+        reached = true;
+        time_to = smp.elapsed_s;
+        mv_to = smp.matvecs;
+      }
+      if (cfg->has_target && f_true <= cfg->target) {
+        status = L1B_TARGET_REACHED;
+        break;
+      }
+      const double f_smooth = tau * h->psi + 0.5 * rr;  // :521
+      if (std::sqrt(h->gg) <= grad_tol) {
+        status = L1B_TARGET_REACHED;
+        break;
+      }
+      if (newton >= cfg->max_iters) {
+        status = L1B_ITER_BUDGET;
+        break;
+      }
+      if (elapsed() > cfg->max_seconds) {
+        status = L1B_TIME_BUDGET;
+        break;
+      }
+      ++newton;
+      // ---- PCG (solvers.cpp:202-264) on device
+      h->rhs_norm = std::sqrt(h->gg);
+      L1B_CUDA(cudaMemcpyAsync(&dst->rhs_norm, &h->rhs_norm, 8, cudaMemcpyHostToDevice, st));
+      pcg_init_kernel<<<grid_for(n), kThreads, 0, st>>>(grad, pre, rp, pp, step, best, n, dst, partials);
+      L1B_LAUNCHED();
+      uint64_t launched = 0, chunk = 4;
+      while (launched < cfg->pcg_max_iters) {
+        const uint64_t k = std::min<uint64_t>(chunk, cfg->pcg_max_iters - launched);
+        for (uint64_t it = 0; it < k; ++it) {
+          launch(v.A, pp, EpiHav{hav, dst}, st);
+          launch(v.At, hav, EpiHp{pp, d2psi, hp, dst, partials, 0.0, {0.0}}, st);
+          pcg_update_kernel<<<grid_for(n), kThreads, 0, st>>>(pp, hp, pre, step, rp, n, dst, partials);
+          L1B_LAUNCHED();
+          pcg_direction_kernel<<<grid_for(n), kThreads, 0, st>>>(rp, pre, step, pp, best, n, dst, tickets + 6);
+          L1B_LAUNCHED();
+        }
+        launched += k;
+        L1B_CUDA(cudaMemcpyAsync(h, dst, sizeof(NcgDev), cudaMemcpyDeviceToHost, st));
+        L1B_CUDA(cudaStreamSynchronize(st));
+        if (h->done) break;
+        chunk = std::min<uint64_t>(chunk * 2, 64);
+      }
+      L1B_CUDA(cudaMemcpyAsync(h, dst, sizeof(NcgDev), cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+      if (h->error == 1) throw std::runtime_error("pcg_solve: breakdown, non-finite curvature");
+      if (h->error == 2) throw std::runtime_error("pcg_solve: breakdown, non-finite residual");
+      const uint64_t pcg_it = h->iterations;
+      mv += 2 * pcg_it;
+      last_pcg = pcg_it;
+      total_pcg += pcg_it;
+      // converged -> the current step; otherwise the best iterate (:250-263)
+      double* s = (h->converged && !h->negcurv) ? step : best;
+      if (h->rhs_norm == 0.0) s = step;
+      // ad = A s (:546), slope = grad.s (:547)
+      spmv(v.A, s, ad, st);
+      ++mv;
+      dot_kernel<<<grid_for(n), kThreads, 0, st>>>(grad, s, n, partials, tickets + 4, scal + 2);
+      L1B_LAUNCHED();
+      double slope = 0.0;
+      L1B_CUDA(cudaMemcpyAsync(&slope, scal + 2, 8, cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+      // Armijo backtracking (:551-560), the last trial accepted at the cap
+      double alpha = 1.0, alpha0 = 1.0, rr_acc = rr;
+      uint64_t bt = 0;
+      bool accepted = false;
+      while (!accepted) {
+        ls_eval_kernel<<<grid_for(std::max(n, ma)), kThreads, 0, st>>>(x, s, r, ad, n, ma, alpha0, dst,
+                                                                      partials, tickets + 5);
+        L1B_LAUNCHED();
+        L1B_CUDA(cudaMemcpyAsync(h, dst, sizeof(NcgDev), cudaMemcpyDeviceToHost, st));
+        L1B_CUDA(cudaStreamSynchronize(st));
+        for (int k = 0; k < kLs; ++k) {
+          const double rrt = h->ls[kLs + k] + v.tail_sq;
+          const double f_trial = tau * h->ls[k] + 0.5 * rrt;
+          if (f_trial <= f_smooth + 1e-4 * alpha * slope || bt >= cfg->ls_max_backtracks) {
+            accepted = true;
+            rr_acc = rrt;
+            break;
+          }
+          alpha *= 0.5;
+          ++bt;
+        }
+        alpha0 = alpha;
+      }
+      ls_accept_kernel<<<grid_for(std::max(n, ma)), kThreads, 0, st>>>(x, s, r, ad, n, ma, alpha);
+      L1B_LAUNCHED();
+      rr = rr_acc;
+    }
+    std::memset(sum, 0, sizeof(*sum));
+    for (size_t q = 0; q < out.size() && samples; ++q)
+      if (q < cap) samples[q] = out[q];
+    if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, x, n * 8, cudaMemcpyDeviceToHost, st));
+    if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, x, n * 8, cudaMemcpyDeviceToDevice, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    sum->status = status;
+    sum->reached_target = reached;
+    sum->time_to_target = time_to;
+    sum->matvecs_to_target = mv_to;
+    sum->final_objective = f_last;
+    sum->elapsed_s = elapsed();
+    sum->total_matvecs = (double)mv;
+    sum->total_pcg_iterations = total_pcg;
+    sum->newton_steps = newton;
+    sum->n_samples = out.size();
+    sum->iterations = newton;
+    if (status == L1B_TARGET_REACHED && !reached) {
+      sum->reached_target = 1;
+      sum->time_to_target = sum->elapsed_s;
+      sum->matvecs_to_target = sum->total_matvecs;
+    }
+  } catch (...) {
+    fail();
+    throw;
+  }
+  fail();
+}
+
+}  // namespace l1b

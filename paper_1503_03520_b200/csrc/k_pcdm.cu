@@ -1,0 +1,409 @@
+// k_pcdm.cu -- randomised (block) coordinate descent on device.
+//
+// L1B_PCDM: block PCDM, the C2 mapping of SURVEY.md 8(d): an epoch is
+//   floor(n/B) blocks of B distinct coordinates drawn from the
+//   uniform_index(rng, n) stream (duplicates inside a block redrawn); all B
+//   coordinates of a block take the CD model step of solvers.cpp:457-461
+//   against the same residual (one thread each, B "processors"), beta =
+//   cd_damping(omega, B, n); the block's residual update adds
+//   delta_c * A(rho, c) into r(rho) in ascending column order c.
+// L1B_CD: the reference's serial sampler (solvers.cpp:414-482) is the B = 1
+//   case with beta = cd_damping(omega, varpi, n); it replays the reference's
+//   updates bit for bit (same stream, same column values, same order).
+//
+// One CTA runs a whole epoch (the blocks are sequentially dependent; the
+// parallelism of PCDM is B).  Ownership of each touched residual row goes to
+// the smallest column of the block that touches it with a non-zero step, so
+// every row is updated by exactly one thread in a fixed order: no atomics,
+// deterministic.  After each epoch r = A x - b is refreshed with the CSR SpMV
+// (solvers.cpp:472-474) and f, the sample and the stop tests run on device.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "solvers.hpp"
+#include "spmv.cuh"
+
+namespace l1b {
+
+namespace {
+
+struct CdDev {
+  double tau, beta, target, tail_sq, f;
+  uint64_t epoch, max_epochs, n_samples, cap, t0_ns, last_ts;
+  int stop, status, has_target, pad;
+  unsigned int ticket[4];
+  double scal[4];  // rr, l1, nnz
+  unsigned long long applied, colops;  // of the running epoch
+};
+
+struct CdSample {
+  uint64_t epoch;
+  double f, nnz, applied, colops;
+  uint64_t ts;
+};
+
+template <typename CP, typename RP>
+__global__ void __launch_bounds__(1024) cd_epoch_kernel(
+    const uint32_t* __restrict__ coords, uint64_t nblocks, int B, const CP* __restrict__ cptr,
+    const uint32_t* __restrict__ crow, const double* __restrict__ cval,
+    const RP* __restrict__ rptr, const uint32_t* __restrict__ rcol,
+    const double* __restrict__ lips, double* x, double* r, uint32_t* stamp, double* delta,
+    uint32_t stamp_base, CdDev* st) {
+  if (*(volatile int*)&st->stop) return;
+  const double beta = st->beta, tau = st->tau;
+  const int t = threadIdx.x;
+  unsigned long long applied = 0, colops = 0;
+  for (uint64_t blk = 0; blk < nblocks; ++blk) {
+    const uint32_t sid = stamp_base + (uint32_t)blk + 1u;
+    uint32_t i = 0;
+    double d = 0.0;
+    if (t < B) {
+      i = coords[blk * (uint64_t)B + t];
+      const double li = lips[i];
+      if (li != 0.0) {  // zero columns are skipped (solvers.cpp:455)
+        double gi = 0.0;
+        for (CP p = cptr[i]; p < cptr[i + 1]; ++p) gi += cval[p] * r[crow[p]];
+        ++colops;
+        const double scale = beta * li;
+        const double xi = x[i];
+        const double xn = soft_threshold(xi - gi / scale, tau / scale);
+        d = xn - xi;
+        if (d != 0.0) {
+          x[i] = xn;
+          ++applied;
+          ++colops;
+        }
+      }
+      delta[i] = d;
+      stamp[i] = sid;
+    }
+    __syncthreads();
+    if (t < B && d != 0.0) {
+      for (CP p = cptr[i]; p < cptr[i + 1]; ++p) {
+        const uint32_t rho = crow[p];
+        // owner = smallest block column with a non-zero step touching rho
+        bool owner = true;
+        for (RP q = rptr[rho]; q < rptr[rho + 1]; ++q) {
+          const uint32_t c = rcol[q];
+          if (c >= i) break;
+          if (stamp[c] == sid && delta[c] != 0.0) {
+            owner = false;
+            break;
+          }
+        }
+        if (!owner) continue;
+        double acc = r[rho];
+        for (RP q = rptr[rho]; q < rptr[rho + 1]; ++q) {
+          const uint32_t c = rcol[q];
+          if (stamp[c] != sid) continue;
+          const double dc = delta[c];
+          if (dc == 0.0) continue;
+          double v = 0.0;  // A(rho, c) as stored in column c (solvers.cpp:465)
+          for (CP pc = cptr[c]; pc < cptr[c + 1]; ++pc)
+            if (crow[pc] == rho) {
+              v = cval[pc];
+              break;
+            }
+          acc += dc * v;
+        }
+        r[rho] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  // epoch counters
+  __shared__ unsigned long long s_app, s_col;
+  if (t == 0) s_app = s_col = 0;
+  __syncthreads();
+  atomicAdd(&s_app, applied);
+  atomicAdd(&s_col, colops);
+  __syncthreads();
+  if (t == 0) {
+    st->applied = s_app;
+    st->colops = s_col;
+  }
+}
+
+// r = A x - b over the active rows + ||r||^2 partials (refresh, :473-474)
+struct EpiRefresh {
+  const double* b;
+  double* r;
+  CdDev* st;
+  double* partials;
+  double acc[1];
+  static constexpr int kVec = 1;
+  __host__ __device__ const double* vec(int) const { return b; }
+  __device__ bool skip() const { return *(volatile const int*)&st->stop; }
+  __device__ void start() { acc[0] = 0.0; }
+  __device__ void line(uint64_t i, double s, const double* pv) {
+    const double v = s - pv[0];
+    r[i] = v;
+    acc[0] += v * v;
+  }
+  __device__ void finish() {
+    double tot[1];
+    if (grid_sum<1>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) st->scal[0] = tot[0];
+  }
+};
+
+__device__ void cd_record(CdDev* st, CdSample* trace, uint64_t e, double f, double nnz,
+                          double applied, double colops, uint64_t ts) {
+  if (st->n_samples < st->cap) trace[st->n_samples] = CdSample{e, f, nnz, applied, colops, ts};
+  st->n_samples++;
+}
+
+// ||x||_1, nnz(x) + finalisation of the epoch (solvers.cpp:475-477, 445-447)
+__global__ void cd_stats_kernel(const double* __restrict__ x, uint64_t n, CdDev* st,
+                                CdSample* trace, double* partials, int init) {
+  if (!init && *(volatile int*)&st->stop) return;
+  double acc[2] = {0.0, 0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    acc[0] += fabs(v);
+    acc[1] += v != 0.0 ? 1.0 : 0.0;
+  }
+  double tot[2];
+  if (grid_sum<2>(acc, partials, &st->ticket[1], tot) && threadIdx.x == 0) {
+    const double f = st->tau * tot[0] + 0.5 * (st->scal[0] + st->tail_sq);
+    const uint64_t ts = global_timer_ns();
+    if (init) {
+      st->t0_ns = ts;
+      st->epoch = 0;
+      cd_record(st, trace, 0, f, tot[1], 0.0, 0.0, ts);
+    } else {
+      st->epoch += 1;
+      cd_record(st, trace, st->epoch, f, tot[1], (double)st->applied, (double)st->colops, ts);
+    }
+    st->f = f;
+    st->last_ts = ts;
+    if (!isfinite(f)) {
+      st->stop = 1;
+      st->status = -1;
+    } else if (st->has_target && f <= st->target) {
+      st->stop = 1;
+      st->status = 0;
+    } else if (st->epoch >= st->max_epochs) {
+      st->stop = 1;
+      st->status = 1;
+    }
+  }
+}
+
+// r = A*0 - b over all m rows (solvers.cpp:436-437); ||r||^2 over the active
+// rows (the structurally empty tail keeps r = -b: tail_sq)
+__global__ void cd_init_residual(const double* __restrict__ b, double* r, uint64_t m,
+                                 uint64_t m_act, CdDev* st, double* partials) {
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = 0.0 - b[i];
+    r[i] = v;
+    if (i < m_act) acc[0] += v * v;
+  }
+  double tot[1];
+  if (grid_sum<1>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) st->scal[0] = tot[0];
+}
+
+template <typename CP, typename RP>
+void launch_epoch(const ProblemView& v, const uint32_t* coords, uint64_t nblocks, int B,
+                  const double* lips, double* x, double* r, uint32_t* stamp, double* delta,
+                  uint32_t stamp_base, CdDev* st) {
+  const int threads = std::min(1024, std::max(32, (B + 31) / 32 * 32));
+  cd_epoch_kernel<CP, RP><<<1, threads, 0, v.stream>>>(
+      coords, nblocks, B, (const CP*)v.At.ptr, v.At.idx, v.At.val, (const RP*)v.A.ptr, v.A.idx,
+      lips, x, r, stamp, delta, stamp_base, st);
+  L1B_LAUNCHED();
+}
+
+uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {  // rng.hpp:37-45
+  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  uint64_t x;
+  do {
+    x = g();
+  } while (x >= lim);
+  return x % n;
+}
+
+double cd_damping(uint64_t omega, uint64_t varpi, uint64_t n) {  // solvers.cpp:266-270
+  if (n <= 1 || varpi <= 1) return 1.0;
+  return 1.0 + static_cast<double>(omega - 1) * static_cast<double>(varpi - 1) /
+                   static_cast<double>(n - 1);
+}
+
+}  // namespace
+
+void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+              l1b_summary* sum, double* x_host, double* d_x) {
+  const ProblemView v = problem_view(p);
+  const bool serial = cfg->solver == L1B_CD;
+  const char* name = serial ? "cd" : "pcdm";
+  const uint64_t n = v.n;
+  if (v.m > (1ull << 32) || n > (1ull << 32)) throw Unsupported("cd: dimensions above 2^32");
+  const uint64_t B = serial ? 1 : std::min<uint64_t>(cfg->block ? cfg->block : 256, n);
+  if (B > 1024) throw Unsupported("pcdm: at most 1024 coordinates per block");
+  uint64_t omega = 1;
+  if (!serial || cfg->varpi > 1)  // solvers.cpp:424-427 (PCDM always models B processors)
+    omega = cfg->omega ? cfg->omega : std::min<uint64_t>(std::max<uint64_t>(1, v.max_row_nnz), n);
+  const double beta = serial ? cd_damping(omega, cfg->varpi, n) : cd_damping(omega, B, n);
+  const uint64_t per_epoch = serial ? n : n / B;  // blocks per epoch
+  const double* lips = problem_gram(p);
+  cudaStream_t st = v.stream;
+
+  double *x = nullptr, *r = nullptr, *delta = nullptr, *partials = nullptr;
+  uint32_t *stamp = nullptr, *d_coords = nullptr;
+  CdDev* dst = nullptr;
+  CdSample* trace = nullptr;
+  const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(16, (1ull << 26) / std::max<uint64_t>(1, per_epoch * B)));
+  const uint64_t tcap = std::min<uint64_t>(cfg->max_iters + 2, 1ull << 22);
+  std::vector<void*> bufs;
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
+    bufs.push_back((void*)*ptr);
+  };
+  uint32_t* h_coords = nullptr;
+  CdDev* h_st = nullptr;
+  try {
+    alloc(&x, n * 8);
+    alloc(&r, v.m * 8);
+    alloc(&delta, n * 8);
+    alloc(&stamp, n * 4);
+    alloc(&partials, (size_t)spmv_grid_max() * 4 * 8);
+    alloc(&d_coords, chunk * per_epoch * B * 4);
+    alloc(&dst, sizeof(CdDev));
+    alloc(&trace, tcap * sizeof(CdSample));
+    L1B_CUDA(cudaMallocHost(&h_coords, chunk * per_epoch * B * 4));
+    L1B_CUDA(cudaMallocHost(&h_st, sizeof(CdDev)));
+    L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
+    L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
+    CdDev h;
+    std::memset(&h, 0, sizeof(h));
+    h.tau = v.tau;
+    h.beta = beta;
+    h.target = cfg->target;
+    h.has_target = cfg->has_target ? 1 : 0;
+    h.tail_sq = v.tail_sq;
+    h.max_epochs = cfg->max_iters;
+    h.cap = tcap;
+    *h_st = h;
+    L1B_CUDA(cudaMemcpyAsync(dst, h_st, sizeof(CdDev), cudaMemcpyHostToDevice, st));
+    const auto t0 = std::chrono::steady_clock::now();
+    cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, v.A.lines, dst, partials);
+    L1B_LAUNCHED();
+    cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 1);
+    L1B_LAUNCHED();
+    std::mt19937_64 rng(cfg->seed);  // Rng rng = make_rng(cfg.seed) (solvers.cpp:430)
+    std::vector<uint64_t> seen(serial ? 0 : n, 0);
+    uint64_t draw_block = 0, launched = 0;
+    uint32_t stamp_base = 0;
+    bool time_out = false;
+    while (launched < cfg->max_iters) {
+      L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+      if (h_st->stop) break;
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
+        time_out = true;
+        break;
+      }
+      const uint64_t ep = std::min<uint64_t>(chunk, cfg->max_iters - launched);
+      // coordinate stream for `ep` epochs (host: mt19937_64 is sequential)
+      uint64_t k = 0;
+      for (uint64_t e = 0; e < ep; ++e)
+        for (uint64_t bl = 0; bl < per_epoch; ++bl) {
+          ++draw_block;
+          for (uint64_t t = 0; t < B; ++t) {
+            uint64_t i;
+            if (serial) {
+              i = uniform_index(rng, n);
+            } else {
+              do {
+                i = uniform_index(rng, n);
+              } while (seen[i] == draw_block);
+              seen[i] = draw_block;
+            }
+            h_coords[k++] = (uint32_t)i;
+          }
+        }
+      L1B_CUDA(cudaMemcpyAsync(d_coords, h_coords, k * 4, cudaMemcpyHostToDevice, st));
+      for (uint64_t e = 0; e < ep; ++e) {
+        const uint32_t* c = d_coords + e * per_epoch * B;
+        if (v.At.ptr32 && v.A.ptr32)
+          launch_epoch<uint32_t, uint32_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
+        else if (v.At.ptr32)
+          launch_epoch<uint32_t, uint64_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
+        else if (v.A.ptr32)
+          launch_epoch<uint64_t, uint32_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
+        else
+          launch_epoch<uint64_t, uint64_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
+        stamp_base += (uint32_t)per_epoch;
+        if (v.A.lines) launch(v.A, x, EpiRefresh{v.b, r, dst, partials, {0.0}}, st);
+        cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 0);
+        L1B_LAUNCHED();
+      }
+      launched += ep;
+    }
+    L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    const CdDev hs = *h_st;
+    if (hs.status < 0)
+      throw std::runtime_error(std::string(name) + ": objective diverged to a non-finite value");
+    const uint64_t kept = std::min<uint64_t>(hs.n_samples, tcap);
+    std::vector<CdSample> tr(kept);
+    if (kept) L1B_CUDA(cudaMemcpyAsync(tr.data(), trace, kept * sizeof(CdSample), cudaMemcpyDeviceToHost, st));
+    if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, x, n * 8, cudaMemcpyDeviceToHost, st));
+    if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, x, n * 8, cudaMemcpyDeviceToDevice, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    std::memset(sum, 0, sizeof(*sum));
+    sum->status = hs.stop ? hs.status : (time_out ? L1B_TIME_BUDGET : L1B_ITER_BUDGET);
+    sum->time_to_target = INFINITY;
+    sum->matvecs_to_target = INFINITY;
+    sum->final_objective = NAN;
+    uint64_t mvc = 1;   // CountingOperator::count_ (initial apply, :436)
+    double mvf = 0.0;   // CountingOperator::fractional_ (:470)
+    for (size_t q = 0; q < tr.size(); ++q) {
+      if (q > 0) {
+        mvf += tr[q].colops / static_cast<double>(n);
+        mvc += 1;  // refresh apply (:473)
+      }
+      l1b_sample o;
+      o.iter = tr[q].epoch;
+      o.elapsed_s = (double)(tr[q].ts - hs.t0_ns) * 1e-9;
+      o.objective = tr[q].f;
+      o.nnz = (uint64_t)tr[q].nnz;
+      o.matvecs = static_cast<double>(mvc) + mvf;
+      o.extra = (uint64_t)tr[q].applied;
+      if (samples && q < cap) samples[q] = o;
+      sum->final_objective = o.objective;
+      if (!sum->reached_target && cfg->has_target && o.objective <= cfg->target) {
+        sum->reached_target = 1;
+        sum->time_to_target = o.elapsed_s;
+        sum->matvecs_to_target = o.matvecs;
+      }
+    }
+    sum->n_samples = hs.n_samples;
+    sum->iterations = hs.epoch;
+    sum->elapsed_s = (double)(hs.last_ts - hs.t0_ns) * 1e-9;
+    sum->total_matvecs = static_cast<double>(mvc) + mvf;
+    if (sum->status == L1B_TARGET_REACHED && !sum->reached_target) {
+      sum->reached_target = 1;
+      sum->time_to_target = sum->elapsed_s;
+      sum->matvecs_to_target = sum->total_matvecs;
+    }
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    for (void* q : bufs) cudaFree(q);
+    if (h_coords) cudaFreeHost(h_coords);
+    if (h_st) cudaFreeHost(h_st);
+    throw;
+  }
+  cudaStreamSynchronize(st);
+  for (void* q : bufs) cudaFree(q);
+  cudaFreeHost(h_coords);
+  cudaFreeHost(h_st);
+}
+
+}  // namespace l1b

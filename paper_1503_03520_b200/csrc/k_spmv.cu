@@ -12,83 +12,19 @@
 
 #include "common.cuh"
 #include "kernels.hpp"
+#include "spmv.cuh"
 
 namespace l1b {
 
 namespace {
 
-// The SpMV skeleton ("row tile per warp"): a warp owns 32 consecutive lines.
-//  1. lane l loads ptr[r0+l] and ptr[r0+l+1]: the tile's nonzeros are the
-//     contiguous range [ptr[r0], ptr[r0+32]);
-//  2. the warp streams that range with coalesced 8 B value / 4 B index loads
-//     (U = 8 independent loads per lane in flight, evict-first), gathers x and
-//     parks the products in shared memory (padded one slot per 16 to avoid
-//     bank conflicts for the 8-entry rows);
-//  3. lane l sums its own line's products in ascending index order (the
-//     reference's sequential dot order) and runs the epilogue for line r0+l,
-//     so every epilogue load/store is a coalesced 256 B warp access.
-// Tiles with more than kCap nonzeros are processed in kCap-sized chunks.
-// Epi provides: skip(), start(), line(i, value), finish().
-constexpr int kCapNnz = 256;
-constexpr int kUnroll = 8;
-
-__device__ __forceinline__ int pad(int off) { return off + (off >> 4); }
-
-template <typename PtrT, class Epi>
-__global__ void __launch_bounds__(kThreads) spmv_kernel(const PtrT* __restrict__ ptr,
-                                                        const uint32_t* __restrict__ idx,
-                                                        const double* __restrict__ val,
-                                                        const double* __restrict__ x,
-                                                        uint64_t nlines, Epi epi) {
-  if (epi.skip()) return;
-  epi.start();
-  __shared__ double prod_all[kThreads / 32][kCapNnz + kCapNnz / 16];
-  const int lane = threadIdx.x & 31;
-  double* sp = prod_all[threadIdx.x >> 5];
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t tile = warp; tile * 32 < nlines; tile += nwarps) {
-    const uint64_t line = tile * 32 + lane;
-    const bool live = line < nlines;
-    const PtrT my_s = __ldg(ptr + (live ? line : nlines));
-    const PtrT my_e = __ldg(ptr + (live ? line + 1 : nlines));
-    const PtrT rs = __shfl_sync(0xffffffffu, my_s, 0);
-    const PtrT re = __shfl_sync(0xffffffffu, my_e, 31);
-    double sum = 0.0;
-    for (PtrT chunk = rs; chunk < re; chunk += kCapNnz) {
-      const PtrT cend = min((PtrT)(chunk + kCapNnz), re);
-      for (PtrT q0 = chunk + lane; q0 < cend; q0 += 32 * kUnroll) {
-        uint32_t ii[kUnroll];
-        double vv[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const PtrT q = q0 + 32 * u;
-          if (q < cend) {
-            ii[u] = __ldcs(idx + q);
-            vv[u] = __ldcs(val + q);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const PtrT q = q0 + 32 * u;
-          if (q < cend) sp[pad((int)(q - chunk))] = vv[u] * __ldg(x + ii[u]);
-        }
-      }
-      __syncwarp();
-      const PtrT a = max(my_s, chunk), e = min(my_e, cend);
-      for (PtrT q = a; q < e; ++q) sum += sp[pad((int)(q - chunk))];
-      __syncwarp();
-    }
-    if (live) epi.line(line, sum);
-  }
-  epi.finish();
-}
-
 struct EpiStore {
   double* y;
+  static constexpr int kVec = 0;
+  __host__ __device__ const double* vec(int) const { return nullptr; }
   __device__ bool skip() const { return false; }
   __device__ void start() {}
-  __device__ void line(uint64_t i, double s) { y[i] = s; }
+  __device__ void line(uint64_t i, double s, const double*) { y[i] = s; }
   __device__ void finish() {}
 };
 
@@ -99,10 +35,12 @@ struct EpiResidualSq {
   unsigned int* ticket;
   double* out;
   double acc[1];
+  static constexpr int kVec = 1;
+  __host__ __device__ const double* vec(int) const { return b; }
   __device__ bool skip() const { return false; }
   __device__ void start() { acc[0] = 0.0; }
-  __device__ void line(uint64_t i, double s) {
-    const double r = s - b[i];
+  __device__ void line(uint64_t, double s, const double* pv) {
+    const double r = s - pv[0];
     acc[0] += r * r;
   }
   __device__ void finish() {
@@ -129,6 +67,8 @@ struct EpiFistaX {
   double* partials;
   double inv_l, thr, beta;
   double acc[3];  // ||trial||_1, nnz(trial), #(trial != y)
+  static constexpr int kVec = 2;  // y, x at the column
+  __host__ __device__ const double* vec(int v) const { return v == 0 ? y : x; }
   __device__ bool skip() const { return *(volatile const int*)&st->stop; }
   __device__ void start() {
     double t_next;
@@ -137,9 +77,9 @@ struct EpiFistaX {
     thr = st->tau * inv_l;
     acc[0] = acc[1] = acc[2] = 0.0;
   }
-  __device__ void line(uint64_t j, double g) {
-    const double yo = y[j];
-    const double xo = x[j];
+  __device__ void line(uint64_t j, double g, const double* pv) {
+    const double yo = pv[0];
+    const double xo = pv[1];
     const double tr = soft_threshold(yo - inv_l * g, thr);
     acc[2] += tr != yo ? 1.0 : 0.0;
     y[j] = tr + beta * (tr - xo);
@@ -205,15 +145,17 @@ struct EpiFistaR {
   double* partials;
   double beta;
   double acc[1];
+  static constexpr int kVec = 2;  // b, r_x at the row
+  __host__ __device__ const double* vec(int v) const { return v == 0 ? b : r_x; }
   __device__ bool skip() const { return *(volatile const int*)&st->stop; }
   __device__ void start() {
     double t_next;
     fista_momentum(st, &t_next, &beta);
     acc[0] = 0.0;
   }
-  __device__ void line(uint64_t i, double s) {
-    const double rt = s - b[i];
-    const double rx = r_x[i];
+  __device__ void line(uint64_t i, double s, const double* pv) {
+    const double rt = s - pv[0];
+    const double rx = pv[1];
     r_y[i] = (1.0 + beta) * rt - beta * rx;
     r_x[i] = rt;
     acc[0] += rt * rt;
@@ -263,32 +205,6 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
       st->status = 1;
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// dispatch over the pointer width
-
-template <class Epi, typename PtrT>
-void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
-  static int grid_cap = 0;
-  if (!grid_cap) {
-    int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_kernel<PtrT, Epi>, kThreads, 0));
-    grid_cap = std::max(1, per_sm) * sm_count();
-  }
-  const uint64_t tiles = (M.lines + 31) / 32;
-  const uint64_t blocks = (tiles + (kThreads / 32) - 1) / (kThreads / 32);
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)grid_cap));
-  spmv_kernel<PtrT, Epi><<<grid, kThreads, 0, st>>>((const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi);
-  L1B_LAUNCHED();
-}
-
-template <class Epi>
-void launch(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
-  if (M.ptr32)
-    launch_p<Epi, uint32_t>(M, x, epi, st);
-  else
-    launch_p<Epi, uint64_t>(M, x, epi, st);
 }
 
 __global__ void l1_kernel(const double* __restrict__ x, uint64_t n, double* partials,

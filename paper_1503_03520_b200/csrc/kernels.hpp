@@ -14,8 +14,9 @@ struct LinesOut {
   uint64_t lines = 0;    // lines kept (trailing empty lines trimmed when asked)
   uint64_t nnz = 0;
   uint32_t max_len = 0;
+  uint64_t tile_nnz_max = 0;  // max nonzeros over 256-line tiles
   bool ptr32 = true;
-  void* ptr = nullptr;   // (lines + 1) x u32 or u64
+  void* ptr = nullptr;   // (lines + 1) x u32 or u64 (+16 B of slack for the bulk copies)
   uint32_t* idx = nullptr;
   double* val = nullptr;
 };
@@ -47,7 +48,8 @@ struct Csr {  // CSR of A (rows) or of A^T (= CSC of A)
   const void* ptr = nullptr;
   const uint32_t* idx = nullptr;
   const double* val = nullptr;
-  int lanes = 32;  // lines per warp tile
+  int lanes = 32;  // lines per warp tile (fallback kernel)
+  uint64_t tile_nnz_max = ~0ull;  // max nonzeros of a 256-line tile (TMA kernel when <= 2048)
 };
 
 // y[0, lines) = M x

@@ -19,6 +19,7 @@ struct ProblemView {
   Csr At;                     // CSC over n columns
   const OpView* op = nullptr;
   const double* gram = nullptr;
+  uint64_t max_row_nnz = 0;  // omega of solvers.cpp:401-410 (max nnz over rows)
 };
 
 ProblemView problem_view(l1b_problem* p);

@@ -1,0 +1,291 @@
+// spmv.cuh -- the fp64 CSR SpMV skeleton shared by every solver kernel
+// (k_spmv.cu FISTA, k_ncg.cu Newton-CG/PCG, k_pcdm.cu refresh): a template
+// over the pointer width and an epilogue functor, instantiated per TU.
+#pragma once
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace l1b {
+namespace spmv_detail {
+
+// Epilogue functors provide
+//   skip() / start() / finish()       (device; finish does the reductions),
+//   kVec, vec(v)                      the kVec n- or m-vectors the epilogue of
+//                                     line i reads at index i (staged in smem),
+//   line(i, value, pv)                pv[v] = vec(v)[i].
+
+// ---------------------------------------------------------------------------
+// Fallback skeleton ("row tile per warp") for operators whose 256-line tiles
+// exceed the TMA stage capacity: a warp owns 32 consecutive lines, streams
+// their contiguous nonzero range with coalesced loads, parks the products in
+// shared memory and lane l sums line r0+l in ascending index order.
+constexpr int kCapNnz = 256;
+constexpr int kUnroll = 8;
+
+__device__ __forceinline__ int pad(int off) { return off + (off >> 4); }
+
+template <class Epi>
+__device__ __forceinline__ void load_vecs(const Epi& epi, uint64_t line, double* pv) {
+#pragma unroll
+  for (int v = 0; v < Epi::kVec; ++v) pv[v] = epi.vec(v)[line];
+}
+
+template <typename PtrT, class Epi>
+__global__ void __launch_bounds__(kThreads) spmv_warp_kernel(const PtrT* __restrict__ ptr,
+                                                             const uint32_t* __restrict__ idx,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ x,
+                                                             uint64_t nlines, Epi epi) {
+  if (epi.skip()) return;
+  epi.start();
+  __shared__ double prod_all[kThreads / 32][kCapNnz + kCapNnz / 16];
+  const int lane = threadIdx.x & 31;
+  double* sp = prod_all[threadIdx.x >> 5];
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t tile = warp; tile * 32 < nlines; tile += nwarps) {
+    const uint64_t line = tile * 32 + lane;
+    const bool live = line < nlines;
+    const PtrT my_s = __ldg(ptr + (live ? line : nlines));
+    const PtrT my_e = __ldg(ptr + (live ? line + 1 : nlines));
+    const PtrT rs = __shfl_sync(0xffffffffu, my_s, 0);
+    const PtrT re = __shfl_sync(0xffffffffu, my_e, 31);
+    double pv[Epi::kVec > 0 ? Epi::kVec : 1];
+    if (live) load_vecs(epi, line, pv);
+    double sum = 0.0;
+    for (PtrT chunk = rs; chunk < re; chunk += kCapNnz) {
+      const PtrT cend = min((PtrT)(chunk + kCapNnz), re);
+      for (PtrT q0 = chunk + lane; q0 < cend; q0 += 32 * kUnroll) {
+        uint32_t ii[kUnroll];
+        double vv[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + 32 * u;
+          if (q < cend) {
+            ii[u] = __ldcs(idx + q);
+            vv[u] = __ldcs(val + q);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + 32 * u;
+          if (q < cend) sp[pad((int)(q - chunk))] = vv[u] * __ldg(x + ii[u]);
+        }
+      }
+      __syncwarp();
+      const PtrT a = max(my_s, chunk), e = min(my_e, cend);
+      for (PtrT q = a; q < e; ++q) sum += sp[pad((int)(q - chunk))];
+      __syncwarp();
+    }
+    if (live) epi.line(line, sum, pv);
+  }
+  epi.finish();
+}
+
+// ---------------------------------------------------------------------------
+// Main skeleton: TMA bulk-copy pipeline.  Persistent CTAs walk 256-line
+// tiles; one elected thread streams each tile's row pointers, values,
+// indices and epilogue vectors into a 3-stage shared-memory ring with
+// cp.async.bulk (UBLKCP, evict-first for the matrix streams) completing on an
+// mbarrier, two tiles ahead of the consumers.  The 256 threads then gather x
+// for the tile's nonzeros (8 independent gathers each, L1/L2 hits on the
+// band), park the products (padded against bank conflicts), and thread t sums
+// line r0+t in ascending index order and runs the epilogue on smem-staged
+// vectors.  Bytes in flight per SM ~ 2 CTAs x 2 stages x 30 KB, far above the
+// ~35 KB Little's law needs at HBM bandwidth.
+constexpr int kTileLines = 256;   // == kThreads
+constexpr int kTileNnz = 2048;    // nonzero capacity of one tile
+constexpr int kStages = 3;
+
+template <typename PtrT, int NV>
+struct TmaLayout {
+  static constexpr size_t r16(size_t b) { return (b + 15) / 16 * 16; }
+  static constexpr size_t vals_bytes = (kTileNnz + 2) * 8;
+  static constexpr size_t idx_bytes = (kTileNnz + 8) * 4;
+  static constexpr size_t ptr_bytes = r16((kTileLines + 1 + 16 / sizeof(PtrT)) * sizeof(PtrT));
+  static constexpr size_t vec_bytes = kTileLines * 8;
+  static constexpr size_t stage_bytes = vals_bytes + idx_bytes + ptr_bytes + NV * vec_bytes;
+  static constexpr size_t prod_off = kStages * stage_bytes;
+  static constexpr size_t prod_bytes = r16((kTileNnz + kTileNnz / 16 + 2) * 8);
+  static constexpr size_t bars_off = prod_off + prod_bytes;
+  static constexpr size_t total = bars_off + kStages * 8;
+};
+
+template <typename PtrT, class Epi>
+__global__ void __launch_bounds__(kThreads, 2) spmv_tma_kernel(const PtrT* __restrict__ ptr,
+                                                               const uint32_t* __restrict__ idx,
+                                                               const double* __restrict__ val,
+                                                               const double* __restrict__ x,
+                                                               uint64_t nlines, Epi epi,
+                                                               int vec_tma) {
+  if (epi.skip()) return;
+  epi.start();
+  using L = TmaLayout<PtrT, Epi::kVec>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
+  double* prod = reinterpret_cast<double*>(smem + L::prod_off);
+  const int t = threadIdx.x;
+  const uint64_t ntiles = (nlines + kTileLines - 1) / kTileLines;
+  const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr int E = 16 / sizeof(PtrT);
+
+  uint64_t pol = 0;
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    pol = l2_evict_first_policy();
+  }
+  __syncthreads();
+
+  // producer: stream tile #k of this CTA into its ring slot
+  auto issue = [&](uint64_t k, PtrT p0, PtrT p1) {
+    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+    const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
+    unsigned char* base = smem + (k % kStages) * L::stage_bytes;
+    double* s_val = reinterpret_cast<double*>(base);
+    uint32_t* s_idx = reinterpret_cast<uint32_t*>(base + L::vals_bytes);
+    PtrT* s_ptr = reinterpret_cast<PtrT*>(base + L::vals_bytes + L::idx_bytes);
+    double* s_vec = reinterpret_cast<double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
+    const uint32_t ptr_b = (uint32_t)(((nl + 1 + E - 1) / E) * 16);
+    const PtrT va = p0 & ~(PtrT)1, vb = (p1 + 1) & ~(PtrT)1;
+    const PtrT ia = p0 & ~(PtrT)3, ib = (p1 + 3) & ~(PtrT)3;
+    const uint32_t val_b = (uint32_t)(vb - va) * 8u, idx_b = (uint32_t)(ib - ia) * 4u;
+    const uint32_t nv = vec_tma ? (uint32_t)(nl & ~1ull) : 0u;
+    mbar_arrive_expect_tx(&bars[k % kStages], ptr_b + val_b + idx_b + Epi::kVec * nv * 8u);
+    bulk_g2s(s_ptr, ptr + r0, ptr_b, &bars[k % kStages]);
+    if (val_b) bulk_g2s_evict_first(s_val, val + va, val_b, &bars[k % kStages], pol);
+    if (idx_b) bulk_g2s_evict_first(s_idx, idx + ia, idx_b, &bars[k % kStages], pol);
+    if (nv) {
+#pragma unroll
+      for (int v = 0; v < Epi::kVec; ++v)
+        bulk_g2s(s_vec + v * kTileLines, epi.vec(v) + r0, nv * 8u, &bars[k % kStages]);
+    }
+  };
+  auto bounds = [&](uint64_t k, PtrT* p0, PtrT* p1) {
+    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+    const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
+    *p0 = __ldg(ptr + r0);
+    *p1 = __ldg(ptr + r0 + nl);
+  };
+
+  PtrT nx0 = 0, nx1 = 0;  // row-pointer bounds of the next tile to issue (prefetched)
+  if (t == 0) {
+    for (uint64_t k = 0; k + 1 < (uint64_t)kStages && k < mine; ++k) {
+      PtrT a, b;
+      bounds(k, &a, &b);
+      issue(k, a, b);
+    }
+    if (kStages - 1 < mine) bounds(kStages - 1, &nx0, &nx1);
+  }
+
+  for (uint64_t k = 0; k < mine; ++k) {
+    if (t == 0 && k + kStages - 1 < mine) {
+      fence_proxy_async();  // the slot was last read by generic loads in iteration k-1
+      issue(k + kStages - 1, nx0, nx1);
+      if (k + kStages < mine) bounds(k + kStages, &nx0, &nx1);
+    }
+    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+    const int nl = (int)min((uint64_t)kTileLines, nlines - r0);
+    unsigned char* base = smem + (k % kStages) * L::stage_bytes;
+    const double* s_val = reinterpret_cast<const double*>(base);
+    const uint32_t* s_idx = reinterpret_cast<const uint32_t*>(base + L::vals_bytes);
+    const PtrT* s_ptr = reinterpret_cast<const PtrT*>(base + L::vals_bytes + L::idx_bytes);
+    const double* s_vec =
+        reinterpret_cast<const double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
+    mbar_wait(&bars[k % kStages], (uint32_t)((k / kStages) & 1));
+    const PtrT p0 = s_ptr[0], p1 = s_ptr[nl];
+    const PtrT va = p0 & ~(PtrT)1, ia = p0 & ~(PtrT)3;
+    // products: 8 independent gathers per thread
+    for (PtrT q0 = p0 + t; q0 < p1; q0 += kThreads * kUnroll) {
+      double vv[kUnroll];
+      uint32_t ii[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const PtrT q = q0 + kThreads * u;
+        if (q < p1) {
+          vv[u] = s_val[q - va];
+          ii[u] = s_idx[q - ia];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const PtrT q = q0 + kThreads * u;
+        if (q < p1) prod[pad((int)(q - p0))] = vv[u] * __ldg(x + ii[u]);
+      }
+    }
+    __syncthreads();
+    if (t < nl) {
+      const PtrT a = s_ptr[t], e = s_ptr[t + 1];
+      double sum = 0.0;
+      for (PtrT q = a; q < e; ++q) sum += prod[pad((int)(q - p0))];
+      double pv[Epi::kVec > 0 ? Epi::kVec : 1];
+      if (vec_tma && t < (nl & ~1)) {
+#pragma unroll
+        for (int v = 0; v < Epi::kVec; ++v) pv[v] = s_vec[v * kTileLines + t];
+      } else {
+        load_vecs(epi, r0 + t, pv);
+      }
+      epi.line(r0 + t, sum, pv);
+    }
+    __syncthreads();
+  }
+  epi.finish();
+}
+
+// ---------------------------------------------------------------------------
+// dispatch over the pointer width
+
+template <class Epi, typename PtrT>
+inline void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
+  using L = TmaLayout<PtrT, Epi::kVec>;
+  if (M.tile_nnz_max <= (uint64_t)kTileNnz) {
+    static int grid_cap = 0;
+    if (!grid_cap) {
+      L1B_CUDA(cudaFuncSetAttribute(spmv_tma_kernel<PtrT, Epi>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::total));
+      int per_sm = 0;
+      L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_tma_kernel<PtrT, Epi>,
+                                                            kThreads, L::total));
+      grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    int vec_tma = 1;
+    for (int v = 0; v < Epi::kVec; ++v)
+      if (reinterpret_cast<uintptr_t>(epi.vec(v)) % 16) vec_tma = 0;
+    const uint64_t tiles = (M.lines + kTileLines - 1) / kTileLines;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
+    spmv_tma_kernel<PtrT, Epi><<<grid, kThreads, L::total, st>>>(
+        (const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi, vec_tma);
+    L1B_LAUNCHED();
+    return;
+  }
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_warp_kernel<PtrT, Epi>,
+                                                          kThreads, 0));
+    grid_cap = std::max(1, per_sm) * sm_count();
+  }
+  const uint64_t tiles = (M.lines + 31) / 32;
+  const uint64_t blocks = (tiles + (kThreads / 32) - 1) / (kThreads / 32);
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)grid_cap));
+  spmv_warp_kernel<PtrT, Epi><<<grid, kThreads, 0, st>>>((const PtrT*)M.ptr, M.idx, M.val, x,
+                                                         M.lines, epi);
+  L1B_LAUNCHED();
+}
+
+template <class Epi>
+inline void launch(const Csr& M, const double* x, const Epi& epi, cudaStream_t st) {
+  if (M.ptr32)
+    launch_p<Epi, uint32_t>(M, x, epi, st);
+  else
+    launch_p<Epi, uint64_t>(M, x, epi, st);
+}
+
+}  // namespace spmv_detail
+
+using spmv_detail::launch;
+
+}  // namespace l1b
