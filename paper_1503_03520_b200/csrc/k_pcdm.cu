@@ -15,8 +15,9 @@
 // parallelism of PCDM is B).  Ownership of each touched residual row goes to
 // the smallest column of the block that touches it with a non-zero step, so
 // every row is updated by exactly one thread in a fixed order: no atomics,
-// deterministic.  After each epoch r = A x - b is refreshed with the CSR SpMV
-// (solvers.cpp:472-474) and f, the sample and the stop tests run on device.
+// deterministic.  After each epoch r = A x - b is refreshed with the
+// matrix-free sweeps (solvers.cpp:472-474, bit-exact with OperatorSpec::apply)
+// and f, the sample and the stop tests run on device.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -25,7 +26,7 @@
 #include <vector>
 
 #include "solvers.hpp"
-#include "spmv.cuh"
+#include "kernels.hpp"
 
 namespace l1b {
 
@@ -128,27 +129,22 @@ __global__ void __launch_bounds__(1024) cd_epoch_kernel(
   }
 }
 
-// r = A x - b over the active rows + ||r||^2 partials (refresh, :473-474)
-struct EpiRefresh {
-  const double* b;
-  double* r;
-  CdDev* st;
-  double* partials;
-  double acc[1];
-  static constexpr int kVec = 1;
-  __host__ __device__ const double* vec(int) const { return b; }
-  __device__ bool skip() const { return *(volatile const int*)&st->stop; }
-  __device__ void start() { acc[0] = 0.0; }
-  __device__ void line(uint64_t i, double s, const double* pv) {
-    const double v = s - pv[0];
+// r -= b after the matrix-free refresh r = A x (solvers.cpp:473-474): the
+// sweep path is the reference's own OperatorSpec::apply, so the residual (and
+// hence every later coordinate decision) matches the reference bit for bit.
+__global__ void cd_refresh_finish(const double* __restrict__ b, double* r, uint64_t m, CdDev* st,
+                                  double* partials) {
+  if (*(volatile int*)&st->stop) return;
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = r[i] - b[i];
     r[i] = v;
     acc[0] += v * v;
   }
-  __device__ void finish() {
-    double tot[1];
-    if (grid_sum<1>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) st->scal[0] = tot[0];
-  }
-};
+  double tot[1];
+  if (grid_sum<1>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) st->scal[0] = tot[0];
+}
 
 __device__ void cd_record(CdDev* st, CdSample* trace, uint64_t e, double f, double nnz,
                           double applied, double colops, uint64_t ts) {
@@ -169,7 +165,7 @@ __global__ void cd_stats_kernel(const double* __restrict__ x, uint64_t n, CdDev*
   }
   double tot[2];
   if (grid_sum<2>(acc, partials, &st->ticket[1], tot) && threadIdx.x == 0) {
-    const double f = st->tau * tot[0] + 0.5 * (st->scal[0] + st->tail_sq);
+    const double f = st->tau * tot[0] + 0.5 * st->scal[0];
     const uint64_t ts = global_timer_ns();
     if (init) {
       st->t0_ns = ts;
@@ -194,16 +190,15 @@ __global__ void cd_stats_kernel(const double* __restrict__ x, uint64_t n, CdDev*
   }
 }
 
-// r = A*0 - b over all m rows (solvers.cpp:436-437); ||r||^2 over the active
-// rows (the structurally empty tail keeps r = -b: tail_sq)
+// r = A*0 - b over all m rows (solvers.cpp:436-437) and ||r||^2
 __global__ void cd_init_residual(const double* __restrict__ b, double* r, uint64_t m,
-                                 uint64_t m_act, CdDev* st, double* partials) {
+                                 CdDev* st, double* partials) {
   double acc[1] = {0.0};
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const double v = 0.0 - b[i];
     r[i] = v;
-    if (i < m_act) acc[0] += v * v;
+    acc[0] += v * v;
   }
   double tot[1];
   if (grid_sum<1>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) st->scal[0] = tot[0];
@@ -292,7 +287,7 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     *h_st = h;
     L1B_CUDA(cudaMemcpyAsync(dst, h_st, sizeof(CdDev), cudaMemcpyHostToDevice, st));
     const auto t0 = std::chrono::steady_clock::now();
-    cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, v.A.lines, dst, partials);
+    cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, dst, partials);
     L1B_LAUNCHED();
     cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 1);
     L1B_LAUNCHED();
@@ -340,7 +335,9 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
         else
           launch_epoch<uint64_t, uint64_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
         stamp_base += (uint32_t)per_epoch;
-        if (v.A.lines) launch(v.A, x, EpiRefresh{v.b, r, dst, partials, {0.0}}, st);
+        sweep_apply(*v.op, x, r, st);
+        cd_refresh_finish<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, dst, partials);
+        L1B_LAUNCHED();
         cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 0);
         L1B_LAUNCHED();
       }
