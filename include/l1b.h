@@ -132,6 +132,8 @@ typedef struct {
   uint64_t device_bytes;  /* HBM held by the problem */
   uint64_t row_begin, row_end, col_begin, col_end; /* shard ranges */
   int csr_lanes, csc_lanes; /* lines per warp tile in the SpMV kernels */
+  int world, rank;          /* shard of a row-block partition (1, 0 = whole) */
+  uint64_t halo;            /* x / r window overhang on each side (= #stages) */
 } l1b_problem_info;
 
 int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* out);
@@ -234,6 +236,24 @@ int l1b_session_step(l1b_session* s, uint64_t iters);
  * (k = 0: A^T r + prox/momentum, 1: A x - b + residual momentum).           */
 int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms);
 int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations);
+
+/* Row-block shards (world > 1): the caller drives each FISTA iteration and
+ * does the two halo exchanges and the 4-scalar all-reduce (NCCL through
+ * torch.distributed, see paper_1503_03520_b200/distributed.py):
+ *   begin -> [all-reduce scal, finalize] -> loop { exchange r_y halo; k1;
+ *   exchange x halo; k2; all-reduce scal; finalize }
+ * Windows: entry h + j of x_win / r_y_win is own column / row row_begin + j;
+ * entries [0, h) and [h + own, own + 2h) are the neighbours' boundary values. */
+typedef struct {
+  double* x_win;    /* own + 2*halo */
+  double* r_y_win;  /* own + 2*halo */
+  double* scal;     /* 4 doubles: ||x||_1, nnz(x), #(trial != y), ||r||^2 -- sum over ranks */
+  uint64_t own, halo;
+} l1b_shard_buffers;
+int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
+int l1b_session_k1(l1b_session* s);
+int l1b_session_k2(l1b_session* s);
+int l1b_session_finalize(l1b_session* s);
 int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
                     double* x_host);
 /* Kernel launches issued by the library since load (all entry points). */

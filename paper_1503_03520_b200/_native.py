@@ -48,7 +48,11 @@ class ProblemInfo(C.Structure):
                 ("tau", f64), ("noise_norm", f64), ("cert_kappa", f64), ("gram_lmax", f64),
                 ("f_star", f64), ("device_bytes", u64), ("row_begin", u64), ("row_end", u64),
                 ("col_begin", u64), ("col_end", u64), ("csr_lanes", C.c_int),
-                ("csc_lanes", C.c_int)]
+                ("csc_lanes", C.c_int), ("world", C.c_int), ("rank", C.c_int), ("halo", u64)]
+
+
+class ShardBuffers(C.Structure):
+    _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64)]
 
 
 class Cert(C.Structure):
@@ -109,6 +113,10 @@ SIGNATURES = [
     ("l1b_session_profile", C.c_int, [vp, u64, P(f64), C.c_int]),
     ("l1b_session_sync", C.c_int, [vp, P(C.c_int), P(u64)]),
     ("l1b_session_end", C.c_int, [vp, P(Sample), u64, P(Summary), P(f64)]),
+    ("l1b_session_buffers", C.c_int, [vp, P(ShardBuffers)]),
+    ("l1b_session_k1", C.c_int, [vp]),
+    ("l1b_session_k2", C.c_int, [vp]),
+    ("l1b_session_finalize", C.c_int, [vp]),
 ]
 
 

@@ -166,6 +166,9 @@ struct l1b_problem {
   double tail_sq = 0.0;
   size_t device_bytes = 0;
   uint64_t row_begin = 0, row_end = 0;
+  int world = 1, rank = 0;
+  uint64_t halo = 0;
+  uint64_t sig_begin = 0;  // shards: d_sigma holds sigma[sig_begin, ...)
 
   ~l1b_problem() {
     cudaSetDevice(device);
@@ -308,6 +311,11 @@ void check_problem(const l1b_problem* p) {
   L1B_CUDA(cudaSetDevice(p->device));
 }
 
+void check_whole(const l1b_problem* p) {
+  check_problem(p);
+  if (p->world > 1) throw Unsupported("operation needs the whole operator, not a row-block shard");
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -345,13 +353,153 @@ int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t r
   });
 }
 
+}  // extern "C"
+
+namespace {
+// Row-block shard of a banded instance (identity P1/P2, no left stages, so
+// |col - row| <= h = #stages and rows >= n are empty).  The host replays the
+// full sigma / g streams (sequential mt19937_64) but uploads only the window
+// [a - 3h, b + 3h); the device runs the generator's sweeps on that window
+// (k_sweep.cu window_stages), which reproduces the global b on the own rows
+// bit for bit, and materialises rows [a, b) (CSR, columns local to the x
+// window [a - h, b + h)) and columns [a, b) (CSC, rows local to the r window).
+void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
+                    l1b_problem** out) {
+  if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
+  if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
+  if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
+  if (!(g->tau > 0.0)) throw InvalidArgument("generate_instance: tau must be positive");
+  if (g->permute || g->left_stages)
+    throw Unsupported("row-block shards need a banded operator (no permutations, no left stages)");
+  if (sh->rank < 0 || sh->rank >= sh->world) throw InvalidArgument("shard: rank out of range");
+  const uint64_t n = g->n;
+  const uint64_t m = (uint64_t)std::llround(g->m_ratio * (double)n);
+  const uint64_t h = g->stages;
+  uint64_t a = sh->row_begin, b = sh->row_end;
+  if (b == 0) {
+    a = n * (uint64_t)sh->rank / (uint64_t)sh->world;
+    b = n * (uint64_t)(sh->rank + 1) / (uint64_t)sh->world;
+  }
+  if (!(a < b && b <= n)) throw InvalidArgument("shard: empty or out-of-range row block");
+  const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
+  // full spectrum (sigma_max / sigma_min are global), window of it uploaded
+  std::vector<double> sigma(n);
+  if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+    hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift, hostrng::mix_seed(job_seed, 3),
+                              sigma.data());
+  } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+    for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+  } else if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && g->sigma_explicit) {
+    std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+  } else {
+    throw InvalidArgument("unknown spectrum kind");
+  }
+  const uint64_t sa = a > 3 * h ? a - 3 * h : 0, sb = std::min(n, b + 3 * h);
+  auto p = std::make_unique<l1b_problem>();
+  std::vector<int32_t> r_off;
+  for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
+  // setup_operator validates / uploads the description; it needs the whole
+  // sigma only for the host-side checks, so give it the window afterwards.
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(sigma[i] > 0.0) || !std::isfinite(sigma[i]))
+      throw std::runtime_error("Spectrum: all singular values must be strictly positive");
+  p->device = device;
+  L1B_CUDA(cudaSetDevice(device));
+  L1B_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  cudaStream_t st = p->stream;
+  p->m = m;
+  p->n = n;
+  p->r_off = r_off;
+  p->r_theta.assign(g->stages, g->theta);
+  fill_stage_tab(p->view.right, p->r_off, p->r_theta);
+  fill_stage_tab(p->view.left, p->l_off, p->l_theta);
+  p->d_sigma = upload(sigma.data() + sa, sb - sa, st, &p->device_bytes);
+  p->sig_begin = sa;
+  p->view.m = m;
+  p->view.n = n;
+  p->view.sigma = p->d_sigma - sa;  // global indexing inside [sa, sb)
+  double smax = sigma[0], smin = sigma[0];
+  for (uint64_t i = 1; i < n; ++i) {
+    smax = std::max(smax, sigma[i]);
+    smin = std::min(smin, sigma[i]);
+  }
+  p->lmax = smax * smax;
+  p->cert_kappa = (smax / smin) * (smax / smin);
+  p->tau = g->tau;
+  p->world = sh->world;
+  p->rank = sh->rank;
+  p->row_begin = a;
+  p->row_end = b;
+  p->halo = h;
+  const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
+  {
+    hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+    hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
+  }
+  std::vector<double> gw(sb - sa), xw;
+  {
+    hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+    for (uint64_t i = 0; i < sb; ++i) {
+      const double v = hostrng::in(r, -g->fill_bound, g->fill_bound);
+      if (i >= sa) gw[i - sa] = v;
+    }
+    for (uint64_t k = 0; k < s; ++k) {
+      const uint64_t i = p->xs_sup[k];
+      if (i >= sa && i < sb) gw[i - sa] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+    }
+  }
+  const uint64_t va = a > h ? a - h : 0, vb = std::min(n, b + h), own = b - a;
+  xw.assign(vb - va, 0.0);
+  for (uint64_t k = 0; k < s; ++k) {
+    const uint64_t i = p->xs_sup[k];
+    if (i >= va && i < vb) xw[i - va] = p->xs_val[k];
+  }
+  // w = G (S^T S)^-1 G^T g on the window (valid on [a - h, b + h))
+  double* d_g = upload(gw.data(), gw.size(), st, nullptr);
+  window_stages(p->view.right, true, true, d_g, sa, sb, n, st);
+  window_scale_op(d_g, p->d_sigma, sb - sa, 0, 0.0, st);
+  window_stages(p->view.right, false, false, d_g, sa, sb, n, st);
+  // e_own = Sigma G^T w, b_own = Sigma G^T x* on [a, b)
+  double* d_v = nullptr;
+  double* d_x = upload(xw.data(), xw.size(), st, nullptr);
+  L1B_CUDA(cudaMalloc(&d_v, (vb - va) * sizeof(double)));
+  L1B_CUDA(cudaMemcpyAsync(d_v, d_g + (va - sa), (vb - va) * 8, cudaMemcpyDeviceToDevice, st));
+  window_stages(p->view.right, true, true, d_v, va, vb, n, st);
+  window_stages(p->view.right, true, true, d_x, va, vb, n, st);
+  window_scale_op(d_v + (a - va), p->d_sigma + (a - sa), own, 1, 0.0, st);
+  window_scale_op(d_x + (a - va), p->d_sigma + (a - sa), own, 1, 0.0, st);
+  p->d_b = dev_alloc<double>(own, &p->device_bytes);
+  L1B_CUDA(cudaMemcpyAsync(p->d_b, d_x + (a - va), own * 8, cudaMemcpyDeviceToDevice, st));
+  double* d_ss = nullptr;
+  L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
+  generator_combine(p->tau, d_v + (a - va), p->d_b, own, d_ss, st);  // e *= tau; b += e
+  double ss = 0.0;
+  L1B_CUDA(cudaMemcpyAsync(&ss, d_ss, 8, cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  p->noise_norm = std::sqrt(ss);  // this shard's part of ||e||
+  for (void* q : {(void*)d_g, (void*)d_v, (void*)d_x, (void*)d_ss}) cudaFree(q);
+  // rows / columns [a, b) with indices local to the windows starting at a - h
+  const uint64_t base = a - h;  // wraps for rank 0; stored indices stay >= 0
+  build_lines(p->view, true, a, own, base, false, st, &p->csr);
+  p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
+  build_lines(p->view, false, a, own, base, false, st, &p->csc);
+  p->device_bytes += (p->csc.lines + 1) * (p->csc.ptr32 ? 4 : 8) + p->csc.nnz * 12;
+  p->tail_sq = 0.0;  // rows >= n are structurally empty and b is exactly 0 there
+  *out = p.release();
+}
+}  // namespace
+
+extern "C" {
+
 // build_instance (bench.cpp:253-316) + generate_instance (instance.cpp:53-89).
 int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard, l1b_problem** out) {
   return guard([&] {
     if (!g || !out) throw InvalidArgument("null argument");
     *out = nullptr;
-    if (shard && shard->world > 1)
-      throw Unsupported("l1b_generate: sharded problems are built by l1b_generate_shard");
+    if (shard && shard->world > 1) {
+      generate_shard(device, g, shard, out);
+      return;
+    }
     if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
     if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
     if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
@@ -489,20 +637,29 @@ int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
     o->col_end = p->n;
     o->csr_lanes = p->rows().lanes;
     o->csc_lanes = p->cols().lanes;
+    o->world = p->world;
+    o->rank = p->rank;
+    o->halo = p->halo;
+    if (p->world > 1) {
+      o->m_active = p->row_end - p->row_begin;
+      o->col_begin = p->row_begin;
+      o->col_end = p->row_end;
+    }
   });
 }
 
 int l1b_problem_get_b(const l1b_problem* p, double* b) {
   return guard([&] {
     check_problem(p);
-    L1B_CUDA(cudaMemcpyAsync(b, p->d_b, p->m * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    const uint64_t rows = p->world > 1 ? p->row_end - p->row_begin : p->m;  // shards: own rows
+    L1B_CUDA(cudaMemcpyAsync(b, p->d_b, rows * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
   });
 }
 
 int l1b_problem_get_sigma(const l1b_problem* p, double* s) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     L1B_CUDA(cudaMemcpyAsync(s, p->d_sigma, p->n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
   });
@@ -530,7 +687,7 @@ int l1b_problem_set_stream(l1b_problem* p, void* stream) {
 
 int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     if (path == L1B_PATH_SWEEP) {
       sweep_apply(p->view, d_x, d_y, p->stream);
     } else {
@@ -544,7 +701,7 @@ int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
 
 int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     if (path == L1B_PATH_SWEEP)
       sweep_apply_transpose(p->view, d_y, d_x, p->stream);
     else
@@ -554,7 +711,7 @@ int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x
 
 int l1b_gram_inverse(l1b_problem* p, const double* d_v, double* d_out) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     sweep_gram_inverse(p->view, d_v, d_out, p->stream);
   });
 }
@@ -571,7 +728,7 @@ const double* gram_diag_device(l1b_problem* p) {
 
 int l1b_gram_diagonal(l1b_problem* p, double* d_out) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     const double* g = gram_diag_device(p);
     L1B_CUDA(cudaMemcpyAsync(d_out, g, p->n * sizeof(double), cudaMemcpyDeviceToDevice, p->stream));
   });
@@ -609,7 +766,7 @@ int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, doubl
 
 int l1b_objective(l1b_problem* p, const double* d_x, double* f_out) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     double* d_f = nullptr;
     L1B_CUDA(cudaMallocAsync(&d_f, sizeof(double), p->stream));
     objective(p->rows(), d_x, p->n, p->d_b, p->tau, p->tail_sq, d_f, p->stream);
@@ -621,7 +778,7 @@ int l1b_objective(l1b_problem* p, const double* d_x, double* f_out) {
 
 int l1b_verify_optimality(l1b_problem* p, double tol, l1b_cert* out) {
   return guard([&] {
-    check_problem(p);
+    check_whole(p);
     cudaStream_t st = p->stream;
     double *xd = nullptr, *res = nullptr, *r = nullptr, *mx = nullptr;
     L1B_CUDA(cudaMallocAsync(&xd, p->n * sizeof(double), st));
@@ -688,6 +845,11 @@ ProblemView problem_view(l1b_problem* p) {
   v.op = &p->view;
   v.gram = nullptr;
   v.max_row_nnz = p->csr.max_len;
+  v.world = p->world;
+  v.rank = p->rank;
+  v.row_begin = p->row_begin;
+  v.row_end = p->row_end;
+  v.halo = p->halo;
   return v;
 }
 const double* problem_gram(l1b_problem* p) { return gram_diag_device(p); }

@@ -164,13 +164,14 @@ struct EpiFistaR {
     double tot[1];
     if (grid_sum<1>(acc, partials, &st->ticket[1], tot) && threadIdx.x == 0) {
       st->scal[3] = tot[0];
-      fista_finalize(st, trace);
+      if (!st->defer) fista_finalize(st, trace);
     }
   }
 };
 
-// r_x = r_y = A*0 - b, f_0 (solvers.cpp:294-298, 301-302) and the loop-head
-// checks before the first iteration.
+__device__ void fista_init_finalize(FistaDev* st, FistaSample* trace);
+
+// r_x = r_y = A*0 - b and ||r||^2 (solvers.cpp:294-298, 301-302).
 __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, double* r_y,
                                   uint64_t m, FistaDev* st, FistaSample* trace,
                                   double* partials) {
@@ -184,7 +185,15 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
   }
   double tot[1];
   if (grid_sum<1>(acc, partials, &st->ticket[2], tot) && threadIdx.x == 0) {
-    const double f = st->tau * 0.0 + 0.5 * tot[0];
+    st->scal[3] = tot[0];
+    if (!st->defer) fista_init_finalize(st, trace);
+  }
+}
+
+// f_0, sample 0 and the loop-head checks before the first iteration
+__device__ void fista_init_finalize(FistaDev* st, FistaSample* trace) {
+  {
+    const double f = st->tau * 0.0 + 0.5 * (st->scal[3] + (st->defer ? st->tail_sq : 0.0));
     const uint64_t ts = global_timer_ns();
     st->t0_ns = ts;
     st->last_ts = ts;
@@ -194,6 +203,7 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
     if (st->cap > 0) trace[0] = FistaSample{0, f, 0.0, ts};
     st->n_samples = 1;
     st->last_sampled = 0;
+    st->initialized = 1;
     if (!isfinite(f)) {
       st->stop = 1;
       st->status = -1;
@@ -205,6 +215,14 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
       st->status = 1;
     }
   }
+}
+
+__global__ void fista_finalize_kernel(FistaDev* st, FistaSample* trace) {
+  if (st->stop) return;
+  if (!st->initialized)
+    fista_init_finalize(st, trace);
+  else
+    fista_finalize(st, trace);
 }
 
 __global__ void l1_kernel(const double* __restrict__ x, uint64_t n, double* partials,
@@ -256,12 +274,17 @@ void fista_init(const FistaBufs& fb, uint64_t m_rows, cudaStream_t st) {
 
 void fista_k1(const Csr& At, const FistaBufs& fb, cudaStream_t st) {
   EpiFistaX e{fb.x, fb.y, fb.st, fb.partials, 0.0, 0.0, 0.0, {0.0, 0.0, 0.0}};
-  launch(At, fb.r_y, e, st);
+  launch(At, fb.r_y_gather, e, st);
 }
 
 void fista_k2(const Csr& A, const FistaBufs& fb, cudaStream_t st) {
   EpiFistaR e{fb.b, fb.r_x, fb.r_y, fb.st, fb.trace, fb.partials, 0.0, {0.0}};
-  launch(A, fb.x, e, st);
+  launch(A, fb.x_gather, e, st);
+}
+
+void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st) {
+  fista_finalize_kernel<<<1, 1, 0, st>>>(fb.st, fb.trace);
+  L1B_LAUNCHED();
 }
 
 }  // namespace l1b

@@ -211,4 +211,55 @@ void vec_sub(double* a, const double* b, uint64_t n, cudaStream_t st) {
   L1B_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// Windowed sweeps for row-block shards: v holds global entries [ws, we); a
+// pair (k, k+1) of the global sweep is rotated iff both members lie in the
+// window (and k + 1 < dim), so every entry whose dependency cone stays inside
+// the window comes out bit-identical to the global sweep; the invalid margin
+// grows by one entry per stage at window edges that are not global edges.
+namespace {
+__global__ void stage_window_kernel(double* __restrict__ v, uint64_t ws, uint64_t we, uint64_t dim,
+                                    int off, double c, double s, bool transposed) {
+  const uint64_t first = ws > (uint64_t)off ? ws + ((ws - off) & 1) : (uint64_t)off;
+  const uint64_t last = min(we, dim);  // pairs need k + 1 < last
+  if (last < first + 2) return;
+  const uint64_t npairs = (last - first) / 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < npairs;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = first + 2 * t - ws;
+    double a = v[k], b = v[k + 1];
+    rotate_pair(a, b, c, s, transposed);
+    v[k] = a;
+    v[k + 1] = b;
+  }
+}
+
+__global__ void window_scale(double* __restrict__ v, const double* __restrict__ sig, uint64_t len,
+                             int mode, double tau) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (mode == 0) v[i] /= sig[i] * sig[i];      // (S^T S)^-1   (linops.cpp:485)
+    else if (mode == 1) v[i] = sig[i] * v[i];    // Sigma        (linops.cpp:433)
+    else v[i] = v[i] * tau;                      // e *= tau     (instance.cpp:70)
+  }
+}
+}  // namespace
+
+void window_stages(const StageTab& tab, bool forward, bool transposed, double* v, uint64_t ws,
+                   uint64_t we, uint64_t dim, cudaStream_t st) {
+  for (int q = 0; q < tab.count; ++q) {
+    const int s = forward ? q : tab.count - 1 - q;
+    stage_window_kernel<<<grid_for((we - ws) / 2 + 1), kThreads, 0, st>>>(
+        v, ws, we, dim, tab.offset[s], tab.c[s], tab.s[s], transposed);
+    L1B_LAUNCHED();
+  }
+}
+
+void window_scale_op(double* v, const double* sig, uint64_t len, int mode, double tau,
+                     cudaStream_t st) {
+  if (!len) return;
+  window_scale<<<grid_for(len), kThreads, 0, st>>>(v, sig, len, mode, tau);
+  L1B_LAUNCHED();
+}
+
 }  // namespace l1b

@@ -40,6 +40,13 @@ void vec_sub(double* a, const double* b, uint64_t n, cudaStream_t st);  // a -= 
 void certificate(const double* r, const double* xd, double tau, uint64_t n, double* d_out2,
                  cudaStream_t st);
 
+// windowed sweeps of a row-block shard (global entries [ws, we) of a dim-vector)
+void window_stages(const StageTab& tab, bool forward, bool transposed, double* v, uint64_t ws,
+                   uint64_t we, uint64_t dim, cudaStream_t st);
+// mode 0: v /= sig^2, 1: v = sig * v, 2: v *= tau
+void window_scale_op(double* v, const double* sig, uint64_t len, int mode, double tau,
+                     cudaStream_t st);
+
 // ---- k_spmv.cu -------------------------------------------------------------
 struct Csr {  // CSR of A (rows) or of A^T (= CSC of A)
   uint64_t lines = 0;
@@ -69,6 +76,8 @@ struct FistaDev {
   double t, lval, tau, f, nnz, target, tail_sq;
   uint64_t k, max_iters, n_samples, cap, last_sampled, t0_ns, last_ts;
   int stop, status, accel, has_target;
+  int defer;        // shards: K2 / init leave scal for the caller's all-reduce
+  int initialized;  // sample 0 written
   unsigned int ticket[4];
   double scal[4];  // l1, nnz, mismatches, ||r||^2 of the last iteration
 };
@@ -76,6 +85,8 @@ struct FistaDev {
 struct FistaBufs {
   double *x, *y;          // n (own columns)
   double *r_x, *r_y;      // rows (own rows)
+  const double* x_gather;    // vector K2 gathers (x, or the shard's x window)
+  const double* r_y_gather;  // vector K1 gathers (r_y, or the shard's r_y window)
   const double* b;
   FistaDev* st;
   FistaSample* trace;
@@ -88,5 +99,7 @@ void fista_init(const FistaBufs& fb, uint64_t m_rows, cudaStream_t st);
 void fista_k1(const Csr& At, const FistaBufs& fb, cudaStream_t st);
 // K2: r_x, r_y <- A x - b, residual momentum (CSR over active rows) + finalize
 void fista_k2(const Csr& A, const FistaBufs& fb, cudaStream_t st);
+// deferred finalisation (shards): after the caller summed st->scal across ranks
+void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 
 }  // namespace l1b

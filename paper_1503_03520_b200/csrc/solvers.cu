@@ -31,6 +31,9 @@ struct l1b_session {
   ProblemView v;
   l1b_solver_cfg cfg;
   bool accel = true;
+  bool shard = false;
+  uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
+  double *x_win = nullptr, *r_y_win = nullptr;  // shard windows (x, r_y point inside)
   double *x = nullptr, *y = nullptr, *r_x = nullptr, *r_y = nullptr, *partials = nullptr;
   FistaDev* st = nullptr;
   FistaSample* trace = nullptr;
@@ -47,6 +50,8 @@ struct l1b_session {
     b.r_x = r_x;
     b.r_y = r_y;
     b.b = v.b;
+    b.x_gather = shard ? x_win : x;
+    b.r_y_gather = shard ? r_y_win : r_y;
     b.st = st;
     b.trace = trace;
     b.partials = partials;
@@ -56,13 +61,15 @@ struct l1b_session {
   ~l1b_session() {
     cudaSetDevice(v.device);
     if (v.stream) cudaStreamSynchronize(v.stream);
-    for (void* q : {(void*)x, (void*)r_x, (void*)partials, (void*)st, (void*)trace})
-      if (q) cudaFree(q);
-    if (accel) {
-      if (y) cudaFree(y);
-      if (r_y) cudaFree(r_y);
-    }
+    for (void* q : allocs) cudaFree(q);
     if (h_st) cudaFreeHost(h_st);
+  }
+  std::vector<void*> allocs;
+  double* dalloc(uint64_t count) {
+    double* q = nullptr;
+    L1B_CUDA(cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(double)));
+    allocs.push_back(q);
+    return q;
   }
 };
 
@@ -81,22 +88,47 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->accel = cfg->solver == L1B_FISTA;
   const ProblemView& v = s->v;
   cudaStream_t st = v.stream;
-  L1B_CUDA(cudaMalloc(&s->x, v.n * sizeof(double)));
-  L1B_CUDA(cudaMalloc(&s->r_x, v.m * sizeof(double)));
-  if (s->accel) {
-    L1B_CUDA(cudaMalloc(&s->y, v.n * sizeof(double)));
-    L1B_CUDA(cudaMalloc(&s->r_y, v.m * sizeof(double)));
+  s->shard = v.world > 1;
+  if (s->shard) {
+    // windows: [halo | own | halo]; K1 writes own x, K2 gathers the x window,
+    // K2 writes own r_y, K1 gathers the r_y window
+    s->halo = v.halo;
+    s->nx = s->nr = v.row_end - v.row_begin;
+    s->x_win = s->dalloc(s->nx + 2 * s->halo);
+    s->r_y_win = s->dalloc(s->nr + 2 * s->halo);
+    L1B_CUDA(cudaMemsetAsync(s->x_win, 0, (s->nx + 2 * s->halo) * 8, st));
+    L1B_CUDA(cudaMemsetAsync(s->r_y_win, 0, (s->nr + 2 * s->halo) * 8, st));
+    s->x = s->x_win + s->halo;
+    s->r_y = s->r_y_win + s->halo;
+    if (s->accel) {
+      s->y = s->dalloc(s->nx);
+      s->r_x = s->dalloc(s->nr);
+    } else {
+      s->y = s->x;  // ISTA: base = x (solvers.cpp:317-318)
+      s->r_x = s->r_y;
+    }
   } else {
-    s->y = s->x;      // ISTA: base = x (solvers.cpp:317-318)
-    s->r_y = s->r_x;
+    s->nx = v.n;
+    s->nr = v.m;
+    s->x = s->dalloc(v.n);
+    s->r_x = s->dalloc(v.m);
+    if (s->accel) {
+      s->y = s->dalloc(v.n);
+      s->r_y = s->dalloc(v.m);
+    } else {
+      s->y = s->x;  // ISTA: base = x (solvers.cpp:317-318)
+      s->r_y = s->r_x;
+    }
   }
-  L1B_CUDA(cudaMalloc(&s->partials, (size_t)spmv_grid_max() * 4 * sizeof(double)));
+  s->partials = s->dalloc((uint64_t)spmv_grid_max() * 4);
   s->cap = sample_capacity(cfg->max_iters);
   L1B_CUDA(cudaMalloc(&s->trace, s->cap * sizeof(FistaSample)));
+  s->allocs.push_back(s->trace);
   L1B_CUDA(cudaMalloc(&s->st, sizeof(FistaDev)));
+  s->allocs.push_back(s->st);
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
-  L1B_CUDA(cudaMemsetAsync(s->x, 0, v.n * sizeof(double), st));
-  if (s->accel) L1B_CUDA(cudaMemsetAsync(s->y, 0, v.n * sizeof(double), st));
+  L1B_CUDA(cudaMemsetAsync(s->x, 0, s->nx * sizeof(double), st));
+  if (s->accel) L1B_CUDA(cudaMemsetAsync(s->y, 0, s->nx * sizeof(double), st));
   FistaDev h;
   std::memset(&h, 0, sizeof(h));
   h.t = 1.0;  // solvers.cpp:304
@@ -108,11 +140,12 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.max_iters = cfg->max_iters;
   h.cap = s->cap;
   h.accel = s->accel ? 1 : 0;
+  h.defer = s->shard ? 1 : 0;
   *s->h_st = h;
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
   s->t0 = std::chrono::steady_clock::now();
-  // residuals over all m rows: rows >= m_active keep r = -b for the whole run
-  fista_init(s->bufs(), v.m, st);
+  // residuals over all (own) rows: rows >= m_active keep r = -b for the whole run
+  fista_init(s->bufs(), s->nr, st);
 }
 
 void session_step(l1b_session* s, uint64_t iters) {
@@ -139,8 +172,8 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   if (kept)
     L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
                              cudaMemcpyDeviceToHost, st));
-  if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, s->x, s->v.n * 8, cudaMemcpyDeviceToHost, st));
-  if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, s->x, s->v.n * 8, cudaMemcpyDeviceToDevice, st));
+  if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, s->x, s->nx * 8, cudaMemcpyDeviceToHost, st));
+  if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, s->x, s->nx * 8, cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   // final sample when the last iteration was not sampled (solvers.cpp:379)
   if (h.last_sampled != h.k) tr.push_back(FistaSample{h.k, h.f, h.nnz, h.last_ts});
@@ -220,9 +253,47 @@ int l1b_session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session** o
   });
 }
 
+int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
+  return guard([&] {
+    if (!s || !out) throw InvalidArgument("null argument");
+    out->x_win = s->shard ? s->x_win : s->x;
+    out->r_y_win = s->shard ? s->r_y_win : s->r_y;
+    out->scal = &s->st->scal[0];
+    out->own = s->nx;
+    out->halo = s->halo;
+  });
+}
+
+int l1b_session_k1(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    fista_k1(s->v.At, s->bufs(), s->v.stream);
+  });
+}
+
+int l1b_session_k2(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    fista_k2(s->v.A, s->bufs(), s->v.stream);
+    s->launched += 1;
+  });
+}
+
+int l1b_session_finalize(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    if (!s->shard) throw LogicError("finalize is for row-block shards (single-device sessions finalise in K2)");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    fista_finalize_launch(s->bufs(), s->v.stream);
+  });
+}
+
 int l1b_session_step(l1b_session* s, uint64_t iters) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
+    if (s->shard) throw LogicError("shard sessions are stepped by the caller (k1 / k2 / finalize)");
     L1B_CUDA(cudaSetDevice(s->v.device));
     session_step(s, iters);
   });
@@ -231,6 +302,7 @@ int l1b_session_step(l1b_session* s, uint64_t iters) {
 int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms) {
   return guard([&] {
     if (!s || !ms_out || n_ms < 2) throw InvalidArgument("bad arguments");
+    if (s->shard) throw LogicError("profile drives single-device sessions");
     L1B_CUDA(cudaSetDevice(s->v.device));
     cudaStream_t st = s->v.stream;
     std::vector<cudaEvent_t> ev(3 * iters);
@@ -288,6 +360,8 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     if (!p || !summary) throw InvalidArgument("null argument");
     ProblemView v = problem_view(p);
     validate_cfg(cfg, v.n);
+    if (v.world > 1)
+      throw Unsupported("a row-block shard is solved by the distributed driver (l1b_session_k1/k2/finalize)");
     L1B_CUDA(cudaSetDevice(v.device));
     if (cfg->solver == L1B_PCDM || cfg->solver == L1B_CD) {
       run_pcdm(p, cfg, samples, cap, summary, x_host, d_x);

@@ -20,6 +20,10 @@ struct ProblemView {
   const OpView* op = nullptr;
   const double* gram = nullptr;
   uint64_t max_row_nnz = 0;  // omega of solvers.cpp:401-410 (max nnz over rows)
+  // row-block shard (world > 1): own rows == own columns [row_begin, row_end);
+  // A / At index x / r windows that start `halo` entries before row_begin
+  int world = 1, rank = 0;
+  uint64_t row_begin = 0, row_end = 0, halo = 0;
 };
 
 ProblemView problem_view(l1b_problem* p);

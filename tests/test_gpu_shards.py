@@ -1,0 +1,101 @@
+"""GPU: row-block shards (distributed.CudaShard) on ONE device.  The ranks are
+emulated sequentially in one process -- halo exchanges and the scalar
+all-reduce become tensor copies between the shards' buffers, no kernel ever
+waits on another -- and must reproduce the single-device FISTA run."""
+import math
+
+import numpy as np
+import pytest
+
+from gpu_util import need_cuda, rel_err
+
+pytestmark = pytest.mark.gpu
+
+KW = dict(n=4096, stages=4, q=1, s_divisor=100, seed=3, theta=2 * math.pi / 10)
+
+
+def _shards(world, iters):
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    cfg = l1bench.SolverConfig(max_iters=iters)
+    return [CudaShard(KW, r, world, 0, cfg) for r in range(world)]
+
+
+def _exchange(shards, name):
+    for g, s in enumerate(shards):
+        win, h, own = getattr(s, name), s.halo, s.own
+        if g > 0:
+            left = shards[g - 1]
+            win[0:h].copy_(getattr(left, name)[left.own:left.own + h])
+        if g < len(shards) - 1:
+            right = shards[g + 1]
+            win[own + h:own + 2 * h].copy_(getattr(right, name)[h:2 * h])
+
+
+def _allreduce(shards):
+    tot = sum(s.scal.clone() for s in shards)
+    for s in shards:
+        s.scal.copy_(tot)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shards_reproduce_single_device_fista(world):
+    torch = need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    iters = 60
+    inst = l1bench.build_instance(**KW)
+    x_ref = np.empty(inst.n)
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters), x_ref)
+    b_ref = inst.b
+    shards = _shards(world, iters)
+    for s in shards:  # the shard's own rows of b are the global b, bit for bit
+        a, e = s.inst.info.row_begin, s.inst.info.row_end
+        np.testing.assert_array_equal(s.inst.b[: e - a], b_ref[a:e])
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    _exchange(shards, "r_y_win")
+    for _ in range(iters):
+        for s in shards:
+            s.k1()
+        _exchange(shards, "x_win")
+        for s in shards:
+            s.k2()
+        _allreduce(shards)
+        for s in shards:
+            s.finalize()
+        _exchange(shards, "r_y_win")
+    torch.cuda.synchronize()
+    outs = [s.finish() for s in shards]
+    for t, _ in outs[1:]:
+        np.testing.assert_array_equal(t.objectives(), outs[0][0].objectives())
+    assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
+    x = np.concatenate([o[1] for o in outs])
+    assert rel_err(x, x_ref) < 1e-12
+    np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
+
+
+def test_shard_rows_match_global_rows():
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    inst = l1bench.build_instance(**KW)
+    gp, gi, gv = inst.op.csr()
+    for s in _shards(3, 5):
+        info = s.inst.info
+        a, e, h = int(info.row_begin), int(info.row_end), int(info.halo)
+        ptr = np.zeros(info.m + 1, dtype=np.uint64)
+        import ctypes as C
+
+        from paper_1503_03520_b200 import _native as N
+
+        idx = np.empty(info.nnz, dtype=np.uint32)
+        val = np.empty(info.nnz)
+        N.check(N.load().l1b_export_csr(s.inst._h, ptr.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                        idx.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                        val.ctypes.data_as(C.POINTER(C.c_double))))
+        lo, hi = int(gp[a]), int(gp[e])
+        np.testing.assert_array_equal(idx.astype(np.int64) + (a - h), gi[lo:hi].astype(np.int64))
+        np.testing.assert_array_equal(val, gv[lo:hi])
