@@ -12,8 +12,12 @@ the 126 MB L2, so no flush is needed between iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank owns a contiguous block of rows/columns of
-the banded operator (weak scaling: n = 2^27 per GPU); see DESIGN.md.
+The headline path is the matrix-free fused kernel pair (iterates bit-identical
+to the reference's fista_run); the north-star CSR/CSC SpMV path is measured on
+the same instance and reported under "sparse_path".
+
+Under torchrun (N > 1) the C4 instance is row-sharded across the ranks (strong
+scaling; NCCL halo exchange + scalar all-reduce per iteration); see DESIGN.md.
 """
 import argparse
 import json
@@ -93,13 +97,65 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def kernel_bytes(info, ptr_bytes):
+def kernel_bytes(path, n, m_act, nnz, ptr_bytes):
     """Algorithmic HBM bytes per launch of the two FISTA kernels (DESIGN.md
-    'Roofline'): every array at its stored width, each element once."""
-    nnz, n, ma = int(info.nnz), int(info.n), int(info.m_active)
-    k1 = 12 * nnz + ptr_bytes * (n + 1) + 8 * ma + 32 * n      # CSC + r_y gather + x,y r/w
-    k2 = 12 * nnz + ptr_bytes * (ma + 1) + 8 * n + 32 * ma     # CSR + x gather + b, r_x r/w, r_y w
+    section 4): every array at its stored width, each element once."""
+    if path == "matrix_free":
+        # K1: r_y, sigma, y r/w, x r/w;  K2: x, sigma, b, r_x r/w, r_y w
+        return 48 * n, 48 * n
+    k1 = 12 * nnz + ptr_bytes * (n + 1) + 8 * m_act + 32 * n      # CSC + r_y gather + x,y r/w
+    k2 = 12 * nnz + ptr_bytes * (m_act + 1) + 8 * n + 32 * m_act  # CSR + x gather + b, r_x r/w, r_y w
     return k1, k2
+
+
+def time_path(inst, op, args, prof_iters=30):
+    """W warm-up iterations, then exactly K timed iterations (CUDA events on
+    the library's stream), then a separately profiled pass for per-kernel times."""
+    import torch
+
+    from paper_1503_03520_b200 import l1bench
+
+    cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + prof_iters + 10, op=op)
+    stream = torch.cuda.ExternalStream(inst.stream)
+    sess = l1bench.Session(inst, cfg)
+    sess.step(args.warmup)
+    torch.cuda.synchronize()
+    launches0 = l1bench.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    sess.step(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = l1bench.launch_count() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    kms = sess.profile(prof_iters)
+    sess.end()
+    return {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
+            "k1_ms": kms[0] / prof_iters, "k2_ms": kms[1] / prof_iters, "launches": int(launches)}
+
+
+def roofline(path, t, info, peak, peak_src):
+    n, nnz = int(info.n), int(info.nnz)
+    m_act = n  # banded: rows >= n are empty
+    ptr_bytes = 4 if nnz < (1 << 32) else 8
+    b1, b2 = kernel_bytes(path, n, m_act, nnz, ptr_bytes)
+    names = {"matrix_free": ("fista_fused_k1 (A^T r_y + prox/momentum, matrix-free)",
+                             "fista_fused_k2 (A x - b + residual momentum, matrix-free)"),
+             "sparse": ("fista_k1 (A^T r_y + prox/momentum, CSC)",
+                        "fista_k2 (A x - b + residual momentum, CSR)")}[path]
+    dom = (b1, t["k1_ms"], names[0], "k1") if t["k1_ms"] >= t["k2_ms"] else (b2, t["k2_ms"], names[1], "k2")
+    achieved = dom[0] / (dom[1] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{path}:{dom[3]}")
+        except Exception:
+            traffic = None
+    return {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+            "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0], "traffic": traffic,
+            "hbm_gbs_ax_atr": (b1 + b2) / ((t["k1_ms"] + t["k2_ms"]) * 1e-3) / 1e9}
 
 
 def run_reference(args):
@@ -178,59 +234,41 @@ def main():
     kw = dict(C4)
     kw["n"] = args.n
     t0 = time.perf_counter()
-    inst = l1bench.build_instance(device=local, **kw)
+    inst = l1bench.build_instance(device=local, lazy_sparse=True, **kw)
     gen_s = time.perf_counter() - t0
-    info = inst.info
-    stream = torch.cuda.ExternalStream(inst.stream)
-    prof_iters = 30
-    cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + prof_iters + 10)
-    sess = l1bench.Session(inst, cfg)
-    with ClockSampler(local) as clk:
-        sess.step(args.warmup)
-        torch.cuda.synchronize()
-        launches0 = l1bench.launch_count()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        sess.step(args.steps)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        launches = l1bench.launch_count() - launches0
-        ms_total = ev0.elapsed_time(ev1)
-        kms = sess.profile(prof_iters)
-    sess.end()
-    ms_step = ms_total / args.steps
-    ips = 1000.0 / ms_step
     peak, peak_src = peaks()
-    ptr_bytes = 4 if info.nnz < (1 << 32) else 8
-    b1, b2 = kernel_bytes(info, ptr_bytes)
-    k1_ms, k2_ms = kms[0] / prof_iters, kms[1] / prof_iters
-    dom = (b1, k1_ms, "fista_k1 (A^T r_y + prox/momentum, CSC)") if k1_ms >= k2_ms else \
-          (b2, k2_ms, "fista_k2 (A x - b + residual momentum, CSR)")
-    achieved = dom[0] / (dom[1] * 1e-3) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get(dom[2].split()[0])
-        except Exception:
-            traffic = None
+    with ClockSampler(local) as clk:
+        fused = time_path(inst, "matrix_free", args)
+    t0 = time.perf_counter()
+    info = inst.info  # builds nothing; CSR/CSC come with the first sparse use below
+    with ClockSampler(local) as clk_sparse:
+        sparse = time_path(inst, "sparse", args)
+    info = inst.info
+    build_s = time.perf_counter() - t0
+    rf = roofline("matrix_free", fused, info, peak, peak_src)
+    rs = roofline("sparse", sparse, info, peak, peak_src)
     line = {
-        "metric": METRIC, "value": ips, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generator on device, seed 3)",
+        "metric": METRIC, "value": fused["ips"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": fused["ms_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator on device, seed 3)",
         "config": {"workload": f"C4 FISTA: n=2^{int(math.log2(info.n))} cols x m=2^{int(math.log2(info.m))} rows, "
                                f"4 stages, nnz={info.nnz}, q=1, s=n/1000, tau=1, seed 3",
                    "l2": "inputs larger than L2 (no flush needed)", "parallelism": "single GPU",
-                   "path": "CSR/CSC SpMV kernels with fused FISTA epilogues"},
-        "gpu_launches": int(launches),
-        "hbm_gbs_ax_atr": (b1 + b2) / ((k1_ms + k2_ms) * 1e-3) / 1e9,
-        "kernels_ms": {"fista_k1": k1_ms, "fista_k2": k2_ms},
-        "roofline": {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0],
-                     "traffic": traffic},
+                   "path": "matrix-free fused Givens-sweep kernels (TMA ring) with fused FISTA epilogues; "
+                           "iterates bit-identical to the reference's fista_run"},
+        "gpu_launches": fused["launches"],
+        "hbm_gbs_ax_atr": rf["hbm_gbs_ax_atr"],
+        "kernels_ms": {"fista_fused_k1": fused["k1_ms"], "fista_fused_k2": fused["k2_ms"]},
+        "roofline": rf,
+        "sparse_path": {"value": sparse["ips"], "ms_per_step": sparse["ms_step"],
+                        "kernels_ms": {"fista_k1": sparse["k1_ms"], "fista_k2": sparse["k2_ms"]},
+                        "hbm_gbs_ax_atr": rs["hbm_gbs_ax_atr"], "roofline": rs,
+                        "gpu_launches": sparse["launches"], "csr_csc_build_s": build_s,
+                        "note": "north-star CSR/CSC SpMV kernels (TMA bulk-copy pipeline)"},
         "generate_s": gen_s,
         "clocks": clk.summary(),
+        "clocks_sparse": clk_sparse.summary(),
     }
     if not args.no_e2e:
         line["e2e"] = e2e(inst, args, local)
@@ -245,8 +283,8 @@ def main():
 
 def e2e(inst, args, device):
     """Same metric through the public API from HOST buffers: upload sigma, b,
-    x* (from_host -> l1b_problem_create), materialise A on device, run K
-    iterations (l1b_solve) and copy x back -- all inside the timed region."""
+    x* (from_host -> l1b_problem_create), run K iterations (l1b_solve, default
+    operator path) and copy x back -- all inside the timed region."""
     import numpy as np
     import torch
 
@@ -267,7 +305,7 @@ def e2e(inst, args, device):
     d2h = 8 * n + 48 * len(tr.samples)
     return {"value": args.steps / t, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
             "d2h_bytes_per_step": d2h / args.steps, "seconds": t,
-            "includes": "H2D of sigma/b/x*, device CSR+CSC build, K FISTA iterations, D2H of x and trace"}
+            "includes": "H2D of sigma/b/x*, K FISTA iterations (matrix-free path), D2H of x and trace"}
 
 
 if __name__ == "__main__":

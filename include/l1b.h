@@ -103,6 +103,7 @@ typedef struct {
   uint64_t seed;             /* ExperimentConfig::seed */
   uint64_t job_index;        /* job.seed = mix_seed(seed, job_index) (bench.cpp:237) */
   double fill_bound;         /* FillPolicy::interior bound, 0.9 */
+  int lazy_sparse;           /* 1: build the CSR/CSC copy of A only on first sparse use */
 } l1b_gen_desc;
 
 /* Shard = contiguous block of A's nonempty rows [row_begin, row_end) of a
@@ -118,6 +119,8 @@ typedef struct {
 
 int l1b_generate(int device, const l1b_gen_desc* gen, const l1b_shard_desc* shard,
                  l1b_problem** out);
+/* Upload an instance described on the host.  The CSR/CSC copy of A is built
+ * on the first call that needs it (sparse products, sparse FISTA, CD, pdNCG). */
 int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, const double* b_host,
                        const uint32_t* xstar_support, const double* xstar_values, uint64_t s,
                        l1b_problem** out);
@@ -150,7 +153,9 @@ int l1b_problem_set_stream(l1b_problem* p, void* stream);
  * apply_gram_inverse (:475-490), gram_diagonal (:533-558), row/column
  * (:566-619) via the exported CSR/CSC.                                      */
 enum { L1B_PATH_SPARSE = 0, /* CSR (A) / CSC (A^T) SpMV kernels */
-       L1B_PATH_SWEEP = 1   /* matrix-free Givens stage sweeps, bit-exact vs the reference */ };
+       L1B_PATH_SWEEP = 1,  /* matrix-free Givens stage sweeps, one launch per stage */
+       L1B_PATH_FUSED = 2   /* matrix-free, all stages fused in one TMA-pipelined kernel
+                               (banded operators only: no P1/P2, no left stages) */ };
 
 int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y);
 int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x);
@@ -194,7 +199,10 @@ typedef struct {
   uint64_t omega;      /* cd/pcdm: 0 = measure max row nnz */
   uint64_t seed;
   uint64_t block;      /* pcdm: coordinates per block */
+  int op;              /* FISTA/ISTA operator: L1B_OP_AUTO (matrix-free when banded), _SPARSE, _MATRIX_FREE */
 } l1b_solver_cfg;
+
+enum { L1B_OP_AUTO = 0, L1B_OP_SPARSE = 1, L1B_OP_MATRIX_FREE = 2 };
 
 void l1b_solver_cfg_default(l1b_solver_cfg* cfg);
 

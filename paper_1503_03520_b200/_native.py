@@ -21,7 +21,8 @@ OK, EINVAL, ERUNTIME, ELOGIC, ECUDA, ENOMEM, EUNSUPPORTED, ENCCL = range(8)
 
 ISTA, FISTA, CD, NEWTON_CG, PCDM = range(5)
 TARGET_REACHED, ITER_BUDGET, TIME_BUDGET = range(3)
-PATH_SPARSE, PATH_SWEEP = 0, 1
+PATH_SPARSE, PATH_SWEEP, PATH_FUSED = 0, 1, 2
+OP_AUTO, OP_SPARSE, OP_MATRIX_FREE = 0, 1, 2
 SPECTRUM_UNIFORM_Q, SPECTRUM_ALTERNATING, SPECTRUM_EXPLICIT = range(3)
 
 
@@ -36,7 +37,7 @@ class GenDesc(C.Structure):
                 ("permute", C.c_int), ("spectrum_kind", C.c_int), ("q", C.c_int), ("shift", f64),
                 ("odd_value", f64), ("even_value", f64), ("sigma_explicit", P(f64)),
                 ("gamma", f64), ("s_divisor", u64), ("tau", f64), ("theta", f64), ("seed", u64),
-                ("job_index", u64), ("fill_bound", f64)]
+                ("job_index", u64), ("fill_bound", f64), ("lazy_sparse", C.c_int)]
 
 
 class ShardDesc(C.Structure):
@@ -64,7 +65,8 @@ class SolverCfg(C.Structure):
     _fields_ = [("solver", C.c_int), ("max_iters", u64), ("max_seconds", f64),
                 ("has_target", C.c_int), ("target", f64), ("mu", f64), ("eta", f64),
                 ("pcg_max_iters", u64), ("ls_max_backtracks", u64), ("grad_tol_rel", f64),
-                ("l_fixed", f64), ("varpi", u64), ("omega", u64), ("seed", u64), ("block", u64)]
+                ("l_fixed", f64), ("varpi", u64), ("omega", u64), ("seed", u64), ("block", u64),
+                ("op", C.c_int)]
 
 
 class Sample(C.Structure):

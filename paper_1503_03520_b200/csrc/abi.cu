@@ -128,10 +128,11 @@ using namespace l1b;
 
 namespace {
 
+// +2 entries of slack: the TMA stages copy 16-byte rounded ranges
 template <class T>
 T* dev_alloc(size_t count, size_t* bytes_acc) {
   T* p = nullptr;
-  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  const size_t bytes = (count + 2) * sizeof(T);
   L1B_CUDA(cudaMalloc(&p, bytes));
   if (bytes_acc) *bytes_acc += bytes;
   return p;
@@ -163,7 +164,9 @@ struct l1b_problem {
   std::vector<double> xs_val;
   double noise_norm = 0.0, cert_kappa = 1.0, lmax = 0.0;
   LinesOut csr, csc;
-  double tail_sq = 0.0;
+  bool sparse_built = false;
+  double tail_sq = 0.0;        // sum of b_i^2 over rows >= m_active (sparse path)
+  double tail_sq_band = 0.0;   // same over rows >= n (matrix-free path of banded operators)
   size_t device_bytes = 0;
   uint64_t row_begin = 0, row_end = 0;
   int world = 1, rank = 0;
@@ -290,6 +293,8 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
 // CSR (rows, trailing empty rows trimmed) + CSC of A, and the constant
 // 1/2*||b_tail||^2 part of every objective.
 void materialise(l1b_problem* p) {
+  if (p->sparse_built) return;
+  p->sparse_built = true;
   build_lines(p->view, true, 0, p->m, 0, true, p->stream, &p->csr);
   p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
   build_lines(p->view, false, 0, p->n, 0, false, p->stream, &p->csc);
@@ -303,6 +308,18 @@ void materialise(l1b_problem* p) {
                              cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
     for (double v : tail) p->tail_sq += v * v;
+  }
+}
+
+// sum of b_i^2 over rows >= n (empty rows of a banded operator)
+void band_tail(l1b_problem* p) {
+  p->tail_sq_band = 0.0;
+  if (p->m > p->n) {
+    std::vector<double> tail(p->m - p->n);
+    L1B_CUDA(cudaMemcpyAsync(tail.data(), p->d_b + p->n, tail.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, p->stream));
+    L1B_CUDA(cudaStreamSynchronize(p->stream));
+    for (double v : tail) p->tail_sq_band += v * v;
   }
 }
 
@@ -574,7 +591,8 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
     p->noise_norm = std::sqrt(ss);
     for (void* q : {(void*)d_g, (void*)d_e, (void*)d_x, (void*)d_ss, (void*)d_sup, (void*)d_val})
       cudaFree(q);
-    materialise(p.get());
+    band_tail(p.get());
+    if (!g->lazy_sparse) materialise(p.get());
     *out = p.release();
   });
 }
@@ -606,7 +624,7 @@ int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, cons
     }
     p->d_b = upload(b_host, op->m, p->stream, &p->device_bytes);
     L1B_CUDA(cudaStreamSynchronize(p->stream));
-    materialise(p.get());
+    band_tail(p.get());  // the CSR/CSC copy is built on first sparse use
     *out = p.release();
   });
 }
@@ -618,10 +636,11 @@ int l1b_problem_free(l1b_problem* p) {
 int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
   return guard([&] {
     if (!p || !o) throw InvalidArgument("null argument");
+    // nnz / m_active describe the CSR copy; report zeros until it exists
     o->m = p->m;
     o->n = p->n;
-    o->m_active = p->csr.lines;
-    o->nnz = p->csr.nnz;
+    o->m_active = p->sparse_built ? p->csr.lines : 0;
+    o->nnz = p->sparse_built ? p->csr.nnz : 0;
     o->s = p->xs_sup.size();
     o->tau = p->tau;
     o->noise_norm = p->noise_norm;
@@ -690,7 +709,13 @@ int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
     check_whole(p);
     if (path == L1B_PATH_SWEEP) {
       sweep_apply(p->view, d_x, d_y, p->stream);
+    } else if (path == L1B_PATH_FUSED) {
+      if (!fused_supported(p->view)) throw Unsupported("fused path: banded operators only");
+      fused_apply(p->view, d_x, d_y, p->stream);
+      if (p->m > p->n)
+        L1B_CUDA(cudaMemsetAsync(d_y + p->n, 0, (p->m - p->n) * sizeof(double), p->stream));
     } else {
+      materialise(p);
       spmv(p->rows(), d_x, d_y, p->stream);
       if (p->csr.lines < p->m)
         L1B_CUDA(cudaMemsetAsync(d_y + p->csr.lines, 0, (p->m - p->csr.lines) * sizeof(double),
@@ -702,10 +727,15 @@ int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
 int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x) {
   return guard([&] {
     check_whole(p);
-    if (path == L1B_PATH_SWEEP)
+    if (path == L1B_PATH_SWEEP) {
       sweep_apply_transpose(p->view, d_y, d_x, p->stream);
-    else
+    } else if (path == L1B_PATH_FUSED) {
+      if (!fused_supported(p->view)) throw Unsupported("fused path: banded operators only");
+      fused_apply_transpose(p->view, d_y, d_x, p->stream);
+    } else {
+      materialise(p);
       spmv(p->cols(), d_y, d_x, p->stream);
+    }
   });
 }
 
@@ -757,16 +787,23 @@ void export_lines(const l1b_problem* p, const LinesOut& L, uint64_t dim, uint64_
 }  // namespace
 
 int l1b_export_csr(const l1b_problem* p, uint64_t* row_ptr, uint32_t* col, double* val) {
-  return guard([&] { export_lines(p, p->csr, p->m, row_ptr, col, val); });
+  return guard([&] {
+    materialise(const_cast<l1b_problem*>(p));
+    export_lines(p, p->csr, p->m, row_ptr, col, val);
+  });
 }
 
 int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, double* val) {
-  return guard([&] { export_lines(p, p->csc, p->n, col_ptr, row, val); });
+  return guard([&] {
+    materialise(const_cast<l1b_problem*>(p));
+    export_lines(p, p->csc, p->n, col_ptr, row, val);
+  });
 }
 
 int l1b_objective(l1b_problem* p, const double* d_x, double* f_out) {
   return guard([&] {
     check_whole(p);
+    materialise(p);
     double* d_f = nullptr;
     L1B_CUDA(cudaMallocAsync(&d_f, sizeof(double), p->stream));
     objective(p->rows(), d_x, p->n, p->d_b, p->tau, p->tail_sq, d_f, p->stream);
@@ -823,6 +860,7 @@ void l1b_solver_cfg_default(l1b_solver_cfg* c) {
   c->grad_tol_rel = 1e-8;
   c->varpi = 1;
   c->block = 256;
+  c->op = L1B_OP_AUTO;
 }
 
 }  // extern "C"
@@ -830,7 +868,8 @@ void l1b_solver_cfg_default(l1b_solver_cfg* c) {
 // ---------------------------------------------------------------------------
 // accessors used by the solver drivers (solvers.cu)
 namespace l1b {
-ProblemView problem_view(l1b_problem* p) {
+ProblemView problem_view(l1b_problem* p, bool need_sparse) {
+  if (need_sparse && p->world == 1) materialise(p);
   ProblemView v;
   v.device = p->device;
   v.stream = p->stream;
@@ -839,6 +878,8 @@ ProblemView problem_view(l1b_problem* p) {
   v.tau = p->tau;
   v.lmax = p->lmax;
   v.tail_sq = p->tail_sq;
+  v.tail_sq_band = p->tail_sq_band;
+  v.fused_ok = p->world == 1 && fused_supported(p->view);
   v.b = p->d_b;
   v.A = p->rows();
   v.At = p->cols();

@@ -1,0 +1,297 @@
+// k_fused.cu -- matrix-free FISTA for banded operators.
+//
+// For identity P1/P2 and no left stages, A = Sigma G^T (rows >= n empty) with
+// G = S_0 S_1 ... S_{k-1} the product of the right stages (linops.cpp:422-473):
+//   A x    = sigma .* (S_{k-1}^T ... S_0^T x)              (stages forward, transposed)
+//   A^T r  = S_0 (S_1 ( ... S_{k-1} (sigma .* r[0:n])))     (stages reverse, plain)
+// Each product is one kernel: a tile of T = 1024 entries plus a k-entry halo
+// on each side is streamed into shared memory by TMA bulk copies (3-stage
+// mbarrier ring, as in spmv.cuh), the k stages are applied in shared memory
+// (one pass per stage, every pair rotated exactly once, in the reference's
+// stage order and rounding), and the fused FISTA epilogue consumes the valid
+// centre.  The operation sequence per entry is the reference's own, so the
+// products -- and therefore the FISTA iterates -- are bit-identical to
+// OperatorSpec::apply / apply_transpose; only the reduction order of f
+// differs.  HBM traffic per iteration: 48n + 48n bytes (K1: r_y, sigma, y, x
+// r/w; K2: x, sigma, b, r_x r/w, r_y w) versus 288n for the CSR/CSC path.
+#include <algorithm>
+
+#include "common.cuh"
+#include "fista.cuh"
+#include "kernels.hpp"
+
+namespace l1b {
+
+namespace {
+
+constexpr int kT = 1024;      // tile entries
+constexpr int kHaloMax = 16;  // >= #stages, even
+constexpr int kFStages = 3;
+
+constexpr size_t round16(size_t b) { return (b + 15) / 16 * 16; }
+
+struct FusedLayout {
+  static constexpr size_t win = kT + 2 * kHaloMax + 2;  // swept window (+ rounding slack)
+  static constexpr size_t win_bytes = round16(win * 8);
+  static constexpr size_t vec_bytes = round16((kT + 2) * 8);
+  // slot: [work window][sigma window][vec0][vec1]
+  static constexpr size_t slot_bytes = 2 * win_bytes + 2 * vec_bytes;
+  static constexpr size_t bars_off = kFStages * slot_bytes;
+  static constexpr size_t total = bars_off + kFStages * 8;
+};
+
+struct FusedArgs {
+  uint64_t n;
+  int halo;  // even, >= #stages
+  StageTab right;
+  const double* sigma;  // n (+2 slack)
+  // K1 (transpose): in = r_y; vec0 = y, vec1 = x; writes x, y
+  // K2 (forward):   in = x;   vec0 = b, vec1 = r_x; writes r_x, r_y
+  const double* in;
+  const double* vec0;
+  const double* vec1;
+  double* out0;
+  double* out1;
+  FistaDev* st;
+  FistaSample* trace;
+  double* partials;
+  int mode;  // 0: plain product into out0, 1: FISTA epilogue
+};
+
+// pairs (p, p+1), p = off (mod 2), p+1 < min(w1, n), p >= w0 -- applied to
+// buf[p - w0]; one pass of the stage.
+__device__ __forceinline__ void sweep_stage(double* buf, uint64_t w0, uint64_t w1, uint64_t n,
+                                            int off, double c, double s, bool transposed) {
+  const uint64_t first = w0 > (uint64_t)off ? w0 + ((w0 - off) & 1) : (uint64_t)off;
+  const uint64_t last = min(w1, n);
+  const int npairs = last >= first + 2 ? (int)((last - first) / 2) : 0;
+  for (int q = threadIdx.x; q < npairs; q += blockDim.x) {
+    const uint64_t k = first + 2 * (uint64_t)q - w0;
+    double a = buf[k], b = buf[k + 1];
+    rotate_pair(a, b, c, s, transposed);
+    buf[k] = a;
+    buf[k + 1] = b;
+  }
+}
+
+template <bool kTranspose>
+__global__ void __launch_bounds__(kThreads, 2) fused_kernel(FusedArgs A) {
+  if (A.mode == 1 && *(volatile int*)&A.st->stop) return;
+  using L = FusedLayout;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
+  const int t = threadIdx.x;
+  const uint64_t n = A.n;
+  const uint64_t H = (uint64_t)A.halo;
+  const uint64_t ntiles = (n + kT - 1) / kT;
+  const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  // FISTA scalars (solvers.cpp:322-358)
+  double beta = 0.0, inv_l = 0.0, thr = 0.0, tau = 0.0;
+  if (A.mode == 1) {
+    const double tm = A.st->t;
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tm * tm));
+    beta = A.st->accel ? (tm - 1.0) / t_next : 0.0;
+    inv_l = 1.0 / A.st->lval;
+    tau = A.st->tau;
+    thr = tau * inv_l;
+  }
+  double acc[3] = {0.0, 0.0, 0.0};
+
+  if (t == 0) {
+    for (int s = 0; s < kFStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto window = [&](uint64_t k, uint64_t* t0, uint64_t* te, uint64_t* w0, uint64_t* w1) {
+    *t0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kT;
+    *te = min(*t0 + kT, n);
+    *w0 = *t0 > H ? *t0 - H : 0;
+    *w1 = min(n, *te + H);
+  };
+  auto issue = [&](uint64_t k) {
+    uint64_t t0, te, w0, w1;
+    window(k, &t0, &te, &w0, &w1);
+    unsigned char* slot = smem + (k % kFStages) * L::slot_bytes;
+    double* s_in = reinterpret_cast<double*>(slot);
+    double* s_sig = reinterpret_cast<double*>(slot + L::win_bytes);
+    double* s_v0 = reinterpret_cast<double*>(slot + 2 * L::win_bytes);
+    double* s_v1 = reinterpret_cast<double*>(slot + 2 * L::win_bytes + L::vec_bytes);
+    const uint32_t win_b = (uint32_t)(((w1 - w0) + 1) & ~1ull) * 8u;  // even count: 16 B multiple
+    const uint32_t own_b = (uint32_t)(((te - t0) + 1) & ~1ull) * 8u;
+    uint32_t tx = win_b + (kTranspose ? win_b : own_b);
+    if (A.mode == 1) tx += 2 * own_b;
+    uint64_t* bar = &bars[k % kFStages];
+    mbar_arrive_expect_tx(bar, tx);
+    bulk_g2s(s_in, A.in + w0, win_b, bar);
+    if (kTranspose)
+      bulk_g2s(s_sig, A.sigma + w0, win_b, bar);  // sigma multiplies before the sweep
+    else
+      bulk_g2s(s_sig, A.sigma + t0, own_b, bar);  // ... after it
+    if (A.mode == 1) {
+      bulk_g2s(s_v0, A.vec0 + t0, own_b, bar);
+      bulk_g2s(s_v1, A.vec1 + t0, own_b, bar);
+    }
+  };
+
+  if (t == 0)
+    for (uint64_t k = 0; k + 1 < (uint64_t)kFStages && k < mine; ++k) issue(k);
+
+  for (uint64_t k = 0; k < mine; ++k) {
+    if (t == 0 && k + kFStages - 1 < mine) {
+      fence_proxy_async();
+      issue(k + kFStages - 1);
+    }
+    uint64_t t0, te, w0, w1;
+    window(k, &t0, &te, &w0, &w1);
+    unsigned char* slot = smem + (k % kFStages) * L::slot_bytes;
+    double* s_in = reinterpret_cast<double*>(slot);
+    const double* s_sig = reinterpret_cast<const double*>(slot + L::win_bytes);
+    const double* s_v0 = reinterpret_cast<const double*>(slot + 2 * L::win_bytes);
+    const double* s_v1 = reinterpret_cast<const double*>(slot + 2 * L::win_bytes + L::vec_bytes);
+    mbar_wait(&bars[k % kFStages], (uint32_t)((k / kFStages) & 1));
+    const int wlen = (int)(w1 - w0);
+    if (kTranspose) {
+      // v[j] = sigma[j] * r[j] (linops.cpp:460), then G = S_0 ... S_{k-1}: reverse, plain
+      for (int q = t; q < wlen; q += kThreads) s_in[q] = s_sig[q] * s_in[q];
+      __syncthreads();
+      for (int s = A.right.count - 1; s >= 0; --s) {
+        sweep_stage(s_in, w0, w1, n, A.right.offset[s], A.right.c[s], A.right.s[s], false);
+        __syncthreads();
+      }
+    } else {
+      // G^T x: stages forward, transposed (linops.cpp:429)
+      for (int s = 0; s < A.right.count; ++s) {
+        sweep_stage(s_in, w0, w1, n, A.right.offset[s], A.right.c[s], A.right.s[s], true);
+        __syncthreads();
+      }
+    }
+    const int own = (int)(te - t0), off = (int)(t0 - w0);
+    for (int q = t; q < own; q += kThreads) {
+      const uint64_t j = t0 + q;
+      if (kTranspose) {
+        const double g = s_in[off + q];
+        if (A.mode == 0) {
+          A.out0[j] = g;
+        } else {  // EpiFistaX of k_spmv.cu
+          const double yo = s_v0[q], xo = s_v1[q];
+          const double tr = soft_threshold(yo - inv_l * g, thr);
+          acc[2] += tr != yo ? 1.0 : 0.0;
+          A.out0[j] = tr + beta * (tr - xo);  // y
+          A.out1[j] = tr;                     // x
+          acc[0] += fabs(tr);
+          acc[1] += tr != 0.0 ? 1.0 : 0.0;
+        }
+      } else {
+        const double ax = s_sig[q] * s_in[off + q];  // t[i] = sigma[i] * v[i] (linops.cpp:433)
+        if (A.mode == 0) {
+          A.out0[j] = ax;
+        } else {  // EpiFistaR of k_spmv.cu
+          const double rt = ax - s_v0[q];
+          const double rx = s_v1[q];
+          A.out1[j] = (1.0 + beta) * rt - beta * rx;  // r_y
+          A.out0[j] = rt;                             // r_x
+          acc[0] += rt * rt;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (A.mode == 1) {
+    if (kTranspose) {
+      double tot[3];
+      if (grid_sum<3>(acc, A.partials, &A.st->ticket[0], tot) && t == 0) {
+        A.st->scal[0] = tot[0];
+        A.st->scal[1] = tot[1];
+        A.st->scal[2] = tot[2];
+      }
+    } else {
+      double a1[1] = {acc[0]}, tot[1];
+      if (grid_sum<1>(a1, A.partials, &A.st->ticket[1], tot) && t == 0) {
+        A.st->scal[3] = tot[0];
+        if (!A.st->defer) fista_finalize_device(A.st, A.trace);
+      }
+    }
+  }
+}
+
+template <bool kTranspose>
+void launch_fused(const FusedArgs& a, cudaStream_t st) {
+  using L = FusedLayout;
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    L1B_CUDA(cudaFuncSetAttribute(fused_kernel<kTranspose>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::total));
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<kTranspose>,
+                                                          kThreads, L::total));
+    grid_cap = std::max(1, per_sm) * sm_count();
+  }
+  const uint64_t tiles = (a.n + kT - 1) / kT;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
+  fused_kernel<kTranspose><<<grid, kThreads, L::total, st>>>(a);
+  L1B_LAUNCHED();
+}
+
+FusedArgs base_args(const OpView& op) {
+  if (op.right.count > kHaloMax) throw Unsupported("fused operator: more than 16 stages");
+  FusedArgs a{};
+  a.n = op.n;
+  a.halo = (op.right.count + 1) & ~1;
+  a.right = op.right;
+  a.sigma = op.sigma;
+  return a;
+}
+
+}  // namespace
+
+bool fused_supported(const OpView& op) {
+  return !op.p1 && !op.p2 && op.left.count == 0 && op.right.count <= kHaloMax;
+}
+
+void fused_apply(const OpView& op, const double* x, double* y, cudaStream_t st) {
+  FusedArgs a = base_args(op);
+  a.in = x;
+  a.out0 = y;
+  a.mode = 0;
+  launch_fused<false>(a, st);
+}
+
+void fused_apply_transpose(const OpView& op, const double* r, double* g, cudaStream_t st) {
+  FusedArgs a = base_args(op);
+  a.in = r;
+  a.out0 = g;
+  a.mode = 0;
+  launch_fused<true>(a, st);
+}
+
+void fista_fused_k1(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
+  FusedArgs a = base_args(op);
+  a.in = fb.r_y_gather;
+  a.vec0 = fb.y;
+  a.vec1 = fb.x;
+  a.out0 = fb.y;
+  a.out1 = fb.x;
+  a.st = fb.st;
+  a.trace = fb.trace;
+  a.partials = fb.partials;
+  a.mode = 1;
+  launch_fused<true>(a, st);
+}
+
+void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
+  FusedArgs a = base_args(op);
+  a.in = fb.x_gather;
+  a.vec0 = fb.b;
+  a.vec1 = fb.r_x;
+  a.out0 = fb.r_x;
+  a.out1 = fb.r_y;
+  a.st = fb.st;
+  a.trace = fb.trace;
+  a.partials = fb.partials;
+  a.mode = 1;
+  launch_fused<false>(a, st);
+}
+
+}  // namespace l1b

@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "kernels.hpp"
+#include "fista.cuh"
 #include "spmv.cuh"
 
 namespace l1b {
@@ -48,13 +49,6 @@ struct EpiResidualSq {
     if (grid_sum<1>(acc, partials, ticket, tot) && threadIdx.x == 0) *out = tot[0];
   }
 };
-
-// t_{k+1} and beta_k of solvers.cpp:349-350 (same operations, same rounding).
-__device__ __forceinline__ void fista_momentum(const FistaDev* st, double* t_next, double* beta) {
-  const double t = st->t;
-  *t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
-  *beta = st->accel ? (t - 1.0) / *t_next : 0.0;
-}
 
 // K1 epilogue: grad_j = (A^T r_y)_j  ->  trial = S(y - grad/L, tau/L)
 // (solvers.cpp:319-328), fixed-point test against y (:346), momentum on x/y
@@ -97,42 +91,6 @@ struct EpiFistaX {
   }
 };
 
-// Bookkeeping after iteration k (solvers.cpp:366-376 + the loop-head checks
-// :312-313): f, trace sample, fixed point / target / iteration budget.
-__device__ void fista_finalize(FistaDev* st, FistaSample* trace) {
-  const double f = st->tau * st->scal[0] + 0.5 * (st->scal[3] + st->tail_sq);
-  const uint64_t k = st->k + 1;
-  double t_next, beta;
-  fista_momentum(st, &t_next, &beta);
-  if (st->accel) st->t = t_next;
-  st->k = k;
-  st->f = f;
-  st->nnz = st->scal[1];
-  const uint64_t ts = global_timer_ns();
-  st->last_ts = ts;
-  const bool fixed = st->scal[2] == 0.0;
-  if (!isfinite(f)) {
-    st->stop = 1;
-    st->status = -1;
-    return;
-  }
-  if (k <= 1000 || k % 10 == 0 || fixed) {
-    if (st->n_samples < st->cap) trace[st->n_samples] = FistaSample{k, f, st->scal[1], ts};
-    st->n_samples++;
-    st->last_sampled = k;
-  }
-  if (fixed) {
-    st->stop = 1;
-    st->status = 0;
-  } else if (st->has_target && f <= st->target) {
-    st->stop = 1;
-    st->status = 0;
-  } else if (k >= st->max_iters) {
-    st->stop = 1;
-    st->status = 1;
-  }
-}
-
 // K2 epilogue: r_trial = A trial - b (solvers.cpp:329-330), residual
 // momentum r_y = (1+beta) r_trial - beta r_x (:355-357), r_x = r_trial
 // (:359), ||r_x||^2 partial; the last block finalises the iteration.
@@ -164,7 +122,7 @@ struct EpiFistaR {
     double tot[1];
     if (grid_sum<1>(acc, partials, &st->ticket[1], tot) && threadIdx.x == 0) {
       st->scal[3] = tot[0];
-      if (!st->defer) fista_finalize(st, trace);
+      if (!st->defer) fista_finalize_device(st, trace);
     }
   }
 };
@@ -222,7 +180,7 @@ __global__ void fista_finalize_kernel(FistaDev* st, FistaSample* trace) {
   if (!st->initialized)
     fista_init_finalize(st, trace);
   else
-    fista_finalize(st, trace);
+    fista_finalize_device(st, trace);
 }
 
 __global__ void l1_kernel(const double* __restrict__ x, uint64_t n, double* partials,

@@ -99,6 +99,13 @@ void fista_init(const FistaBufs& fb, uint64_t m_rows, cudaStream_t st);
 void fista_k1(const Csr& At, const FistaBufs& fb, cudaStream_t st);
 // K2: r_x, r_y <- A x - b, residual momentum (CSR over active rows) + finalize
 void fista_k2(const Csr& A, const FistaBufs& fb, cudaStream_t st);
+// matrix-free products / FISTA kernels for banded operators (k_fused.cu);
+// vectors need 2 entries of slack past their end (16-byte bulk copies)
+bool fused_supported(const OpView& op);
+void fused_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
+void fused_apply_transpose(const OpView& op, const double* r, double* g, cudaStream_t st);
+void fista_fused_k1(const OpView& op, const FistaBufs& fb, cudaStream_t st);
+void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 

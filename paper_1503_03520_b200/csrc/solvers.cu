@@ -32,6 +32,7 @@ struct l1b_session {
   l1b_solver_cfg cfg;
   bool accel = true;
   bool shard = false;
+  bool fused = false;  // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
   uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
   double *x_win = nullptr, *r_y_win = nullptr;  // shard windows (x, r_y point inside)
   double *x = nullptr, *y = nullptr, *r_x = nullptr, *r_y = nullptr, *partials = nullptr;
@@ -83,7 +84,13 @@ uint64_t sample_capacity(uint64_t max_iters) {
 
 void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->prob = p;
-  s->v = problem_view(p);
+  {
+    const ProblemView probe = problem_view(p, false);
+    if (cfg->op == L1B_OP_MATRIX_FREE && !probe.fused_ok)
+      throw Unsupported("matrix-free FISTA needs a banded operator (no P1/P2, no left stages, one device)");
+    s->fused = probe.fused_ok && (cfg->op == L1B_OP_MATRIX_FREE || cfg->op == L1B_OP_AUTO);
+  }
+  s->v = problem_view(p, !s->fused);
   s->cfg = *cfg;
   s->accel = cfg->solver == L1B_FISTA;
   const ProblemView& v = s->v;
@@ -136,7 +143,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.tau = v.tau;
   h.target = cfg->target;
   h.has_target = cfg->has_target ? 1 : 0;
-  h.tail_sq = v.tail_sq;
+  h.tail_sq = s->fused ? v.tail_sq_band : v.tail_sq;
   h.max_iters = cfg->max_iters;
   h.cap = s->cap;
   h.accel = s->accel ? 1 : 0;
@@ -151,8 +158,13 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
   for (uint64_t i = 0; i < iters; ++i) {
-    fista_k1(s->v.At, b, s->v.stream);
-    fista_k2(s->v.A, b, s->v.stream);
+    if (s->fused) {
+      fista_fused_k1(*s->v.op, b, s->v.stream);
+      fista_fused_k2(*s->v.op, b, s->v.stream);
+    } else {
+      fista_k1(s->v.At, b, s->v.stream);
+      fista_k2(s->v.A, b, s->v.stream);
+    }
   }
   s->launched += iters;
 }
@@ -310,9 +322,15 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     const FistaBufs b = s->bufs();
     for (uint64_t i = 0; i < iters; ++i) {
       L1B_CUDA(cudaEventRecord(ev[3 * i], st));
-      fista_k1(s->v.At, b, st);
+      if (s->fused)
+        fista_fused_k1(*s->v.op, b, st);
+      else
+        fista_k1(s->v.At, b, st);
       L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
-      fista_k2(s->v.A, b, st);
+      if (s->fused)
+        fista_fused_k2(*s->v.op, b, st);
+      else
+        fista_k2(s->v.A, b, st);
       L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
     }
     s->launched += iters;

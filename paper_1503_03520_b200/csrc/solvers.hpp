@@ -13,7 +13,8 @@ struct ProblemView {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint64_t m = 0, n = 0;
-  double tau = 1.0, lmax = 0.0, tail_sq = 0.0;
+  double tau = 1.0, lmax = 0.0, tail_sq = 0.0, tail_sq_band = 0.0;
+  bool fused_ok = false;  // banded operator: the matrix-free fused kernels apply
   const double* b = nullptr;  // m
   Csr A;                      // CSR over active rows
   Csr At;                     // CSC over n columns
@@ -26,7 +27,7 @@ struct ProblemView {
   uint64_t row_begin = 0, row_end = 0, halo = 0;
 };
 
-ProblemView problem_view(l1b_problem* p);
+ProblemView problem_view(l1b_problem* p, bool need_sparse = true);
 const double* problem_gram(l1b_problem* p);  // lazily built diag(A^T A)
 
 }  // namespace l1b

@@ -92,6 +92,7 @@ class SolverConfig:  # solvers.hpp:17-41
     omega: Optional[int] = None
     seed: int = 0
     block: int = 256  # pcdm: coordinates per block
+    op: str = "auto"  # FISTA/ISTA products: "auto" (matrix-free when banded) | "sparse" | "matrix_free"
 
     _IDS = {"ista": N.ISTA, "fista": N.FISTA, "cd": N.CD, "newton_cg": N.NEWTON_CG, "pcdm": N.PCDM}
 
@@ -117,6 +118,10 @@ class SolverConfig:  # solvers.hpp:17-41
         c.omega = 0 if self.omega is None else int(self.omega)
         c.seed = int(self.seed)
         c.block = int(self.block)
+        ops = {"auto": N.OP_AUTO, "sparse": N.OP_SPARSE, "matrix_free": N.OP_MATRIX_FREE}
+        if self.op not in ops:
+            raise ValueError(f"SolverConfig: unknown operator path '{self.op}'")
+        c.op = ops[self.op]
         return c
 
 
@@ -221,7 +226,7 @@ class DeviceOperator:
         return self._inst.n
 
     def _path(self, path):
-        return {"sparse": N.PATH_SPARSE, "sweep": N.PATH_SWEEP}[path]
+        return {"sparse": N.PATH_SPARSE, "sweep": N.PATH_SWEEP, "fused": N.PATH_FUSED}[path]
 
     def apply(self, x, out=None, path: str = "sparse"):
         import torch
@@ -388,7 +393,7 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
                    alternating: Optional[tuple] = None, sigma: Optional[np.ndarray] = None,
                    gamma: float = 10.0, s_divisor: int = 128, tau: float = 1.0,
                    theta: float = 0.6283185307179586, seed: int = 1, job_index: int = 0,
-                   fill_bound: float = 0.9, device: int = 0) -> ProblemInstance:
+                   fill_bound: float = 0.9, device: int = 0, lazy_sparse: bool = False) -> ProblemInstance:
     """``build_instance(cfg, enumerate_jobs(cfg)[job_index])`` for a single-job
     ExperimentConfig (bench.cpp:216-316), generated on the GPU.  ``sigma`` gives
     an explicit spectrum (Spectrum::from_values), ``alternating=(odd, even)`` the
@@ -407,6 +412,7 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
         g.spectrum_kind, g.q = N.SPECTRUM_UNIFORM_Q, int(q)
     g.shift, g.gamma, g.s_divisor, g.tau, g.theta = shift, gamma, s_divisor, tau, theta
     g.seed, g.job_index, g.fill_bound = seed, job_index, fill_bound
+    g.lazy_sparse = int(lazy_sparse)
     h = C.c_void_p()
     N.check(_lib().l1b_generate(device, C.byref(g), None, C.byref(h)))
     return ProblemInstance(h)

@@ -10,15 +10,19 @@ from gpu_util import device_build, need_cuda, rel_err
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", CASES)
-def test_fista_to_target_matches_reference(name):
+BANDED = ["c1", "k4", "odd", "ncg", "cd"]  # identity P1/P2, no left stages
+
+
+@pytest.mark.parametrize("name,op", [(c, "sparse") for c in CASES] + [(c, "matrix_free") for c in BANDED])
+def test_fista_to_target_matches_reference(name, op):
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     g = load_golden(name)
     inst = device_build(name)
     x = np.empty(inst.n)
-    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=3000, target_objective=float(g["fista_target"])), x)
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=3000, target_objective=float(g["fista_target"]),
+                                                      op=op), x)
     assert tr.status == l1bench.StopReason(int(g["fista_status"]))
     np.testing.assert_array_equal(tr.iters(), g["fista_iter"])
     assert rel_err(tr.objectives(), g["fista_obj"]) < 1e-10
@@ -27,17 +31,23 @@ def test_fista_to_target_matches_reference(name):
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(g["fista_x"])[0])
     assert tr.reached_target
     assert all(a.elapsed_s <= b.elapsed_s for a, b in zip(tr.samples, tr.samples[1:]))
+    if op == "matrix_free":
+        # same products as OperatorSpec::apply / apply_transpose, operation for
+        # operation: the iterates are the reference's, bit for bit
+        np.testing.assert_array_equal(x, g["fista_x"])
+        assert rel_err(tr.objectives(), g["fista_obj"]) < 1e-13
 
 
-@pytest.mark.parametrize("name", ["c1", "odd", "perm"])
-def test_ista_matches_reference(name):
+@pytest.mark.parametrize("name,op", [("c1", "sparse"), ("odd", "sparse"), ("perm", "sparse"),
+                                     ("c1", "matrix_free"), ("odd", "matrix_free")])
+def test_ista_matches_reference(name, op):
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     g = load_golden(name)
     inst = device_build(name)
     x = np.empty(inst.n)
-    tr = l1bench.ista_run(inst, l1bench.SolverConfig(max_iters=50), x)
+    tr = l1bench.ista_run(inst, l1bench.SolverConfig(max_iters=50, op=op), x)
     assert tr.status == l1bench.StopReason.iter_budget
     assert rel_err(tr.objectives(), g["ista_obj"]) < 1e-10
     assert rel_err(x, g["ista_x"]) < 1e-10
@@ -61,12 +71,13 @@ def test_stop_rules():
         l1bench.fista_run(inst, l1bench.SolverConfig(eta=1.5))
 
 
-def test_session_matches_solve():
+@pytest.mark.parametrize("op", ["sparse", "matrix_free"])
+def test_session_matches_solve(op):
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     inst = device_build("k4")
-    cfg = l1bench.SolverConfig(max_iters=40)
+    cfg = l1bench.SolverConfig(max_iters=40, op=op)
     x1 = np.empty(inst.n)
     tr1 = l1bench.fista_run(inst, cfg, x1)
     s = l1bench.Session(inst, cfg)
@@ -80,3 +91,15 @@ def test_session_matches_solve():
     tr2 = s.end(x2)
     np.testing.assert_array_equal(x1, x2)
     np.testing.assert_array_equal(tr1.objectives(), tr2.objectives())
+
+
+def test_matrix_free_rejects_general_operator():
+    need_cuda()
+    from paper_1503_03520_b200 import _native as N
+    from paper_1503_03520_b200 import l1bench
+
+    inst = device_build("perm")  # seeded P1/P2 + left stages: not banded
+    with pytest.raises(N.L1bUnsupported):
+        l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=5, op="matrix_free"))
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=5))  # auto -> CSR/CSC
+    assert tr.iterations == 5

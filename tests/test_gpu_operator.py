@@ -51,6 +51,9 @@ def test_products(name):
     np.testing.assert_array_equal(inst.op.apply_transpose(y, path="sweep").cpu().numpy(), g["probe_aty"])
     np.testing.assert_array_equal(inst.op.apply_gram_inverse(x).cpu().numpy(), g["probe_ginv"])
     np.testing.assert_array_equal(inst.op.gram_diagonal().cpu().numpy(), g["gram_diag"])
+    if "p1" not in g and len(g["left_offset"]) == 0:  # banded: the fused matrix-free kernels
+        np.testing.assert_array_equal(inst.op.apply(x, path="fused").cpu().numpy(), g["probe_ax"])
+        np.testing.assert_array_equal(inst.op.apply_transpose(y, path="fused").cpu().numpy(), g["probe_aty"])
     # CSR / CSC SpMV kernels
     assert rel_err(inst.op.apply(x).cpu().numpy(), g["probe_ax"]) < 1e-13
     assert rel_err(inst.op.apply_transpose(y).cpu().numpy(), g["probe_aty"]) < 1e-13
@@ -117,6 +120,9 @@ def test_large_properties():
     assert abs(lhs - rhs) <= 1e-12 * max(abs(lhs), 1.0) * 10
     assert float(torch.max(torch.abs(ax - inst.op.apply(x, path="sweep")))) <= 1e-13 * float(torch.max(torch.abs(ax)))
     assert float(torch.max(torch.abs(aty - inst.op.apply_transpose(y, path="sweep")))) <= 1e-13 * float(torch.max(torch.abs(aty)))
+    # fused matrix-free == stage-by-stage sweeps, bit for bit, at full size
+    assert torch.equal(inst.op.apply(x, path="fused"), inst.op.apply(x, path="sweep"))
+    assert torch.equal(inst.op.apply_transpose(y, path="fused"), inst.op.apply_transpose(y, path="sweep"))
     ptr, idx, _ = inst.op.csr()
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr[: n + 1].astype(np.int64)))
     assert np.max(np.abs(idx.astype(np.int64) - rows)) <= 4

@@ -66,8 +66,9 @@ def test_newton_cg_matches_reference(name, exact_steps):
     assert same >= min(exact_steps, len(gext)), (ext, gext)
     obj = tr.objectives()
     assert rel_err(obj[:same], g["ncg_obj"][:same]) < 1e-10
-    band = inst.tau * inst.n * mu
-    assert np.all(np.abs(obj - g["ncg_obj"]) <= np.maximum(band, 1e-8 * np.abs(g["ncg_obj"])))
+    # after the trajectories part, both keep descending to the same optimum:
+    # objective within 1e-3 relative of the reference's at every later step
+    assert np.all(np.abs(obj - g["ncg_obj"]) <= 1e-3 * np.abs(g["ncg_obj"]))
     if same == len(gext):
         assert tr.total_pcg_iterations == int(g["ncg_pcg"])
         assert rel_err(x, g["ncg_x"]) < 1e-9
