@@ -125,6 +125,8 @@ int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, cons
                        const uint32_t* xstar_support, const double* xstar_values, uint64_t s,
                        l1b_problem** out);
 int l1b_problem_free(l1b_problem* p);
+/* Build the CSR/CSC copy of A now (otherwise built on first sparse use). */
+int l1b_problem_materialize(l1b_problem* p);
 
 typedef struct {
   uint64_t m, n;

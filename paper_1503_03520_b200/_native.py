@@ -94,6 +94,7 @@ SIGNATURES = [
     ("l1b_problem_create", C.c_int, [C.c_int, P(OperatorDesc), f64, P(f64), P(u32), P(f64), u64,
                                      P(vp)]),
     ("l1b_problem_free", C.c_int, [vp]),
+    ("l1b_problem_materialize", C.c_int, [vp]),
     ("l1b_problem_info_get", C.c_int, [vp, P(ProblemInfo)]),
     ("l1b_problem_get_b", C.c_int, [vp, P(f64)]),
     ("l1b_problem_get_sigma", C.c_int, [vp, P(f64)]),

@@ -633,6 +633,13 @@ int l1b_problem_free(l1b_problem* p) {
   return guard([&] { delete p; });
 }
 
+int l1b_problem_materialize(l1b_problem* p) {
+  return guard([&] {
+    check_problem(p);
+    if (p->world == 1) materialise(p);
+  });
+}
+
 int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
   return guard([&] {
     if (!p || !o) throw InvalidArgument("null argument");

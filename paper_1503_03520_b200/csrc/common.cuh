@@ -158,7 +158,7 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
 // Block-wide sum of NS doubles held per thread (result valid in thread 0).
 template <int NS>
 __device__ __forceinline__ void block_sum(double (&v)[NS]) {
-  __shared__ double red[NS][kThreads / 32];
+  __shared__ double red[NS][32];  // up to 1024 threads
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NS; ++k) {

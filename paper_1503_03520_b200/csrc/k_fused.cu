@@ -25,6 +25,7 @@ namespace l1b {
 namespace {
 
 constexpr int kT = 1024;      // tile entries
+constexpr int kFThreads = 512;  // 2 entries / 1 pair per thread per pass
 constexpr int kHaloMax = 16;  // >= #stages, even
 constexpr int kFStages = 3;
 
@@ -59,23 +60,39 @@ struct FusedArgs {
 };
 
 // pairs (p, p+1), p = off (mod 2), p+1 < min(w1, n), p >= w0 -- applied to
-// buf[p - w0]; one pass of the stage.
+// buf[p - w0]; one pass of the stage.  With `sig` (first pass of A^T r), the
+// entries are first scaled by sigma (linops.cpp:460) as they are loaded --
+// the same two roundings as a separate pass -- and the entries no pair of
+// this stage covers are scaled by the threads at the two ends.
 __device__ __forceinline__ void sweep_stage(double* buf, uint64_t w0, uint64_t w1, uint64_t n,
-                                            int off, double c, double s, bool transposed) {
+                                            int off, double c, double s, bool transposed,
+                                            const double* sig = nullptr) {
   const uint64_t first = w0 > (uint64_t)off ? w0 + ((w0 - off) & 1) : (uint64_t)off;
   const uint64_t last = min(w1, n);
   const int npairs = last >= first + 2 ? (int)((last - first) / 2) : 0;
   for (int q = threadIdx.x; q < npairs; q += blockDim.x) {
     const uint64_t k = first + 2 * (uint64_t)q - w0;
     double a = buf[k], b = buf[k + 1];
+    if (sig) {
+      a = sig[k] * a;
+      b = sig[k + 1] * b;
+    }
     rotate_pair(a, b, c, s, transposed);
     buf[k] = a;
     buf[k + 1] = b;
   }
+  if (sig) {
+    const uint64_t covered_end = npairs ? first + 2 * (uint64_t)npairs : w0;
+    const uint64_t lead_end = npairs ? first : w1;
+    for (uint64_t p = w0 + threadIdx.x; p < lead_end; p += blockDim.x) buf[p - w0] = sig[p - w0] * buf[p - w0];
+    if (npairs)
+      for (uint64_t p = covered_end + threadIdx.x; p < w1; p += blockDim.x)
+        buf[p - w0] = sig[p - w0] * buf[p - w0];
+  }
 }
 
 template <bool kTranspose>
-__global__ void __launch_bounds__(kThreads, 2) fused_kernel(FusedArgs A) {
+__global__ void __launch_bounds__(kFThreads, 2) fused_kernel(FusedArgs A) {
   if (A.mode == 1 && *(volatile int*)&A.st->stop) return;
   using L = FusedLayout;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -154,10 +171,13 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(FusedArgs A) {
     const int wlen = (int)(w1 - w0);
     if (kTranspose) {
       // v[j] = sigma[j] * r[j] (linops.cpp:460), then G = S_0 ... S_{k-1}: reverse, plain
-      for (int q = t; q < wlen; q += kThreads) s_in[q] = s_sig[q] * s_in[q];
-      __syncthreads();
+      if (A.right.count == 0) {
+        for (int q = t; q < wlen; q += kFThreads) s_in[q] = s_sig[q] * s_in[q];
+        __syncthreads();
+      }
       for (int s = A.right.count - 1; s >= 0; --s) {
-        sweep_stage(s_in, w0, w1, n, A.right.offset[s], A.right.c[s], A.right.s[s], false);
+        sweep_stage(s_in, w0, w1, n, A.right.offset[s], A.right.c[s], A.right.s[s], false,
+                    s == A.right.count - 1 ? s_sig : nullptr);
         __syncthreads();
       }
     } else {
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(FusedArgs A) {
       }
     }
     const int own = (int)(te - t0), off = (int)(t0 - w0);
-    for (int q = t; q < own; q += kThreads) {
+    for (int q = t; q < own; q += kFThreads) {
       const uint64_t j = t0 + q;
       if (kTranspose) {
         const double g = s_in[off + q];
@@ -225,12 +245,12 @@ void launch_fused(const FusedArgs& a, cudaStream_t st) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::total));
     int per_sm = 0;
     L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<kTranspose>,
-                                                          kThreads, L::total));
+                                                          kFThreads, L::total));
     grid_cap = std::max(1, per_sm) * sm_count();
   }
   const uint64_t tiles = (a.n + kT - 1) / kT;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
-  fused_kernel<kTranspose><<<grid, kThreads, L::total, st>>>(a);
+  fused_kernel<kTranspose><<<grid, kFThreads, L::total, st>>>(a);
   L1B_LAUNCHED();
 }
 

@@ -269,7 +269,7 @@ class DeviceOperator:
 
     def csr(self):
         """Rows of A exactly as OperatorSpec::row (linops.cpp:597-619)."""
-        info = self._inst.info
+        info = self._inst.materialize()
         ptr = np.zeros(self.rows() + 1, dtype=np.uint64)
         idx = np.empty(max(info.nnz, 1), dtype=np.uint32)
         val = np.empty(max(info.nnz, 1))
@@ -278,7 +278,7 @@ class DeviceOperator:
 
     def csc(self):
         """Columns of A exactly as OperatorSpec::column (linops.cpp:566-595)."""
-        info = self._inst.info
+        info = self._inst.materialize()
         ptr = np.zeros(self.cols() + 1, dtype=np.uint64)
         idx = np.empty(max(info.nnz, 1), dtype=np.uint32)
         val = np.empty(max(info.nnz, 1))
@@ -303,6 +303,12 @@ class ProblemInstance:
                 _lib().l1b_problem_free(h)
             except Exception:
                 pass
+
+    def materialize(self) -> N.ProblemInfo:
+        """Build the CSR/CSC copy of A (if lazy) and refresh ``info``."""
+        N.check(_lib().l1b_problem_materialize(self._h))
+        N.check(_lib().l1b_problem_info_get(self._h, C.byref(self.info)))
+        return self.info
 
     # -- reference accessors --------------------------------------------------
     @property
