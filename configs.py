@@ -1,0 +1,145 @@
+#!/usr/bin/env python3
+"""Runs BASELINE.json's single-GPU configurations C1-C4 end to end on the GPU
+(the reference mapping of SURVEY.md 8(d) / DESIGN.md section 2) and, beside
+each, the reference's own CPU solver (oracle/_ref) on a bounded sample.
+Prints one JSON object per config; `--out FILE` also writes them as a list.
+
+  python configs.py [--only c1,c2,c3,c4] [--out profiles/r1_configs.json]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+THETA = 2 * math.pi / 10
+
+
+def log_sigma(n):
+    return [math.pow(10.0, float(i) / float(n - 1)) for i in range(n)]
+
+
+CONFIGS = {
+    "c1": dict(desc="FISTA, n=2^12 x m=2^13, log-spaced sigma (kappa=100), s=n/100, seed 0, to the 1e-8 gap",
+               gen=dict(n=1 << 12, stages=1, s_divisor=100, seed=0), sigma="log", solver="fista",
+               rel_gap=1e-8, max_iters=100000),
+    "c2": dict(desc="block PCDM (B=256), n=2^15 x m=2^16, q=1, s=n/100, seed 1, 100 epochs",
+               gen=dict(n=1 << 15, stages=1, q=1, s_divisor=100, seed=1), solver="pcdm",
+               max_iters=100, block=256, solver_seed=1),
+    "c3": dict(desc="pdNCG, n=2^19 x m=2^20, q=2, s=n/1000, seed 2, mu=1e-5 fixed, 30 Newton steps",
+               gen=dict(n=1 << 19, stages=1, q=2, s_divisor=1000, seed=2), solver="newton_cg",
+               max_iters=30),
+    "c4": dict(desc="FISTA, n=2^27 x m=2^28, 4 stages, q=1, s=n/1000, seed 3, 500 iterations",
+               gen=dict(n=1 << 27, stages=4, q=1, s_divisor=1000, seed=3), solver="fista",
+               max_iters=500),
+}
+
+# bounded CPU samples of the reference (oracle/_ref): (n, solver iterations)
+CPU_SAMPLE = {"c1": None, "c2": (1 << 15, 10), "c3": (1 << 19, 2), "c4": (1 << 20, 5)}
+
+
+def run_gpu(name, c):
+    import torch
+
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(c["gen"], theta=THETA)
+    if c.get("sigma") == "log":
+        kw["sigma"] = log_sigma(kw["n"])
+    t0 = time.perf_counter()
+    inst = l1bench.build_instance(lazy_sparse=(c["solver"] == "fista"), **kw)
+    gen_s = time.perf_counter() - t0
+    f_star = inst.objective_at_planted()
+    b = inst.b
+    f0 = 0.5 * float((b * b).sum())
+    target = None
+    if "rel_gap" in c:
+        target = f_star + c["rel_gap"] * max(f0 - f_star, 0.0)
+    cfg = l1bench.SolverConfig(id=c["solver"], max_iters=c["max_iters"], target_objective=target,
+                               block=c.get("block", 256), seed=c.get("solver_seed", 0),
+                               max_seconds=3600.0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr = l1bench.run_solver(inst, cfg)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"config": name, "desc": c["desc"], "n": inst.n, "m": inst.m, "generate_s": gen_s,
+           "solver": c["solver"], "status": str(tr.status), "iterations": tr.iterations,
+           "solve_wall_s": wall, "solve_device_s": tr.elapsed_s, "f_final": tr.final_objective,
+           "f_star": f_star, "rel_gap_final": (tr.final_objective - f_star) / max(f0 - f_star, 1e-300),
+           "matvecs": tr.total_matvecs}
+    if c["solver"] == "newton_cg":
+        out["pcg_iterations"] = tr.total_pcg_iterations
+        out["smoothing_band_tau_n_mu"] = inst.tau * inst.n * 1e-5
+    if target is not None:
+        out["target"] = target
+        out["time_to_target_s"] = tr.time_to_target
+    if tr.iterations:
+        out["iters_per_s"] = tr.iterations / max(tr.elapsed_s, 1e-12)
+    return out
+
+
+def run_cpu(name, c):
+    from pyoracle import REF_SO, Reference
+
+    if not os.path.exists(REF_SO):
+        return {"unavailable": "oracle/_ref/libl1ref.so not built"}
+    ref = Reference()
+    kw = dict(c["gen"], theta=THETA)
+    sample = CPU_SAMPLE[name]
+    iters = c["max_iters"]
+    if sample:
+        kw["n"], iters = sample
+    if c.get("sigma") == "log":
+        import numpy as np
+
+        kw["sigma"] = np.array(log_sigma(kw["n"]))
+    inst = ref.build_instance(**kw)
+    f0 = 0.5 * float((inst.b() ** 2).sum())
+    target = None
+    if "rel_gap" in c:
+        target = inst.f_star + c["rel_gap"] * max(f0 - inst.f_star, 0.0)
+    solver = "cd" if c["solver"] == "pcdm" else c["solver"]
+    t0 = time.perf_counter()
+    tr, _ = inst.solve(solver, max_iters=iters, target=target, varpi=c.get("block", 1),
+                       seed=c.get("solver_seed", 0))
+    wall = time.perf_counter() - t0
+    n_iter = int(tr["iter"][-1]) if len(tr["iter"]) else 0
+    out = {"kind": "reference", "cores": 1, "n": inst.n, "solver": solver, "iterations": n_iter,
+           "wall_s": wall, "f_final": tr["final_objective"],
+           "sample": "full run" if not sample else f"n={kw['n']}, {iters} iterations (bounded)"}
+    if n_iter:
+        out["iters_per_s"] = n_iter / max(tr["elapsed_s_total"], 1e-12)
+        if sample:
+            out["iters_per_s_scaled_to_config_n"] = out["iters_per_s"] * kw["n"] / c["gen"]["n"]
+    if target is not None:
+        out["time_to_target_s"] = float(tr["elapsed_s"][-1])
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c1,c2,c3,c4")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    res = []
+    for name in args.only.split(","):
+        c = CONFIGS[name]
+        r = run_gpu(name, c)
+        if not args.no_cpu:
+            r["cpu_reference"] = run_cpu(name, c)
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -295,6 +295,15 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
 void materialise(l1b_problem* p) {
   if (p->sparse_built) return;
   p->sparse_built = true;
+  if (p->world > 1) {  // row-block shard: rows / columns [a, b), window-local indices
+    const uint64_t a = p->row_begin, own = p->row_end - p->row_begin;
+    build_lines(p->view, true, a, own, a - p->halo, false, p->stream, &p->csr);
+    p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
+    build_lines(p->view, false, a, own, a - p->halo, false, p->stream, &p->csc);
+    p->device_bytes += (p->csc.lines + 1) * (p->csc.ptr32 ? 4 : 8) + p->csc.nnz * 12;
+    p->tail_sq = 0.0;  // rows >= n are structurally empty and b is exactly 0 there
+    return;
+  }
   build_lines(p->view, true, 0, p->m, 0, true, p->stream, &p->csr);
   p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
   build_lines(p->view, false, 0, p->n, 0, false, p->stream, &p->csc);
@@ -391,13 +400,18 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   if (sh->rank < 0 || sh->rank >= sh->world) throw InvalidArgument("shard: rank out of range");
   const uint64_t n = g->n;
   const uint64_t m = (uint64_t)std::llround(g->m_ratio * (double)n);
-  const uint64_t h = g->stages;
+  // window overhang: #stages rounded up to even (16-byte aligned bulk copies)
+  const uint64_t h = ((uint64_t)g->stages + 1) & ~1ull;
   uint64_t a = sh->row_begin, b = sh->row_end;
-  if (b == 0) {
-    a = n * (uint64_t)sh->rank / (uint64_t)sh->world;
-    b = n * (uint64_t)(sh->rank + 1) / (uint64_t)sh->world;
+  if (b == 0) {  // even split, boundaries on multiples of 16 (distributed.partition)
+    auto cut = [&](uint64_t g_) {
+      return g_ == (uint64_t)sh->world ? n : (n * g_ / (uint64_t)sh->world) / 16 * 16;
+    };
+    a = cut((uint64_t)sh->rank);
+    b = cut((uint64_t)sh->rank + 1);
   }
   if (!(a < b && b <= n)) throw InvalidArgument("shard: empty or out-of-range row block");
+  if (a % 2) throw InvalidArgument("shard: row_begin must be even");
   const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
   // full spectrum (sigma_max / sigma_min are global), window of it uploaded
   std::vector<double> sigma(n);
@@ -495,13 +509,9 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   L1B_CUDA(cudaStreamSynchronize(st));
   p->noise_norm = std::sqrt(ss);  // this shard's part of ||e||
   for (void* q : {(void*)d_g, (void*)d_v, (void*)d_x, (void*)d_ss}) cudaFree(q);
+  p->tail_sq = p->tail_sq_band = 0.0;  // rows >= n are empty and b is exactly 0 there
   // rows / columns [a, b) with indices local to the windows starting at a - h
-  const uint64_t base = a - h;  // wraps for rank 0; stored indices stay >= 0
-  build_lines(p->view, true, a, own, base, false, st, &p->csr);
-  p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
-  build_lines(p->view, false, a, own, base, false, st, &p->csc);
-  p->device_bytes += (p->csc.lines + 1) * (p->csc.ptr32 ? 4 : 8) + p->csc.nnz * 12;
-  p->tail_sq = 0.0;  // rows >= n are structurally empty and b is exactly 0 there
+  if (!g->lazy_sparse) materialise(p.get());
   *out = p.release();
 }
 }  // namespace
@@ -636,7 +646,7 @@ int l1b_problem_free(l1b_problem* p) {
 int l1b_problem_materialize(l1b_problem* p) {
   return guard([&] {
     check_problem(p);
-    if (p->world == 1) materialise(p);
+    materialise(p);
   });
 }
 
@@ -876,7 +886,7 @@ void l1b_solver_cfg_default(l1b_solver_cfg* c) {
 // accessors used by the solver drivers (solvers.cu)
 namespace l1b {
 ProblemView problem_view(l1b_problem* p, bool need_sparse) {
-  if (need_sparse && p->world == 1) materialise(p);
+  if (need_sparse) materialise(p);
   ProblemView v;
   v.device = p->device;
   v.stream = p->stream;
@@ -886,7 +896,7 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   v.lmax = p->lmax;
   v.tail_sq = p->tail_sq;
   v.tail_sq_band = p->tail_sq_band;
-  v.fused_ok = p->world == 1 && fused_supported(p->view);
+  v.fused_ok = fused_supported(p->view);
   v.b = p->d_b;
   v.A = p->rows();
   v.At = p->cols();

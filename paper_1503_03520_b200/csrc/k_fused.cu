@@ -25,7 +25,7 @@ namespace l1b {
 namespace {
 
 constexpr int kT = 1024;      // tile entries
-constexpr int kFThreads = 512;  // 2 entries / 1 pair per thread per pass
+constexpr int kFThreads = 256;
 constexpr int kHaloMax = 16;  // >= #stages, even
 constexpr int kFStages = 3;
 
@@ -43,11 +43,13 @@ struct FusedLayout {
 
 struct FusedArgs {
   uint64_t n;
+  uint64_t lo, hi;  // lines produced: global [lo, hi) (a shard's own range)
   int halo;  // even, >= #stages
   StageTab right;
   const double* sigma;  // n (+2 slack)
   // K1 (transpose): in = r_y; vec0 = y, vec1 = x; writes x, y
   // K2 (forward):   in = x;   vec0 = b, vec1 = r_x; writes r_x, r_y
+  // every pointer is indexed by GLOBAL entry (pre-offset by the caller)
   const double* in;
   const double* vec0;
   const double* vec1;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(FusedArgs A) {
   const int t = threadIdx.x;
   const uint64_t n = A.n;
   const uint64_t H = (uint64_t)A.halo;
-  const uint64_t ntiles = (n + kT - 1) / kT;
+  const uint64_t ntiles = (A.hi - A.lo + kT - 1) / kT;
   const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   // FISTA scalars (solvers.cpp:322-358)
@@ -122,8 +124,8 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(FusedArgs A) {
   __syncthreads();
 
   auto window = [&](uint64_t k, uint64_t* t0, uint64_t* te, uint64_t* w0, uint64_t* w1) {
-    *t0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kT;
-    *te = min(*t0 + kT, n);
+    *t0 = A.lo + (blockIdx.x + k * gridDim.x) * (uint64_t)kT;
+    *te = min(*t0 + kT, A.hi);
     *w0 = *t0 > H ? *t0 - H : 0;
     *w1 = min(n, *te + H);
   };
@@ -248,7 +250,7 @@ void launch_fused(const FusedArgs& a, cudaStream_t st) {
                                                           kFThreads, L::total));
     grid_cap = std::max(1, per_sm) * sm_count();
   }
-  const uint64_t tiles = (a.n + kT - 1) / kT;
+  const uint64_t tiles = (a.hi - a.lo + kT - 1) / kT;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
   fused_kernel<kTranspose><<<grid, kFThreads, L::total, st>>>(a);
   L1B_LAUNCHED();
@@ -258,6 +260,8 @@ FusedArgs base_args(const OpView& op) {
   if (op.right.count > kHaloMax) throw Unsupported("fused operator: more than 16 stages");
   FusedArgs a{};
   a.n = op.n;
+  a.lo = 0;
+  a.hi = op.n;
   a.halo = (op.right.count + 1) & ~1;
   a.right = op.right;
   a.sigma = op.sigma;
@@ -286,13 +290,22 @@ void fused_apply_transpose(const OpView& op, const double* r, double* g, cudaStr
   launch_fused<true>(a, st);
 }
 
+// global-index view of an own-range array that starts at global index `first`
+template <class T>
+T* at_global(T* p, int64_t first) {
+  return p - first;
+}
+
 void fista_fused_k1(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
   FusedArgs a = base_args(op);
-  a.in = fb.r_y_gather;
-  a.vec0 = fb.y;
-  a.vec1 = fb.x;
-  a.out0 = fb.y;
-  a.out1 = fb.x;
+  a.lo = fb.lo;
+  a.hi = fb.hi;
+  const int64_t lo = (int64_t)fb.lo;
+  a.in = at_global(fb.r_y_gather, fb.gather_base);
+  a.vec0 = at_global(fb.y, lo);
+  a.vec1 = at_global(fb.x, lo);
+  a.out0 = at_global(fb.y, lo);
+  a.out1 = at_global(fb.x, lo);
   a.st = fb.st;
   a.trace = fb.trace;
   a.partials = fb.partials;
@@ -302,11 +315,14 @@ void fista_fused_k1(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
 
 void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
   FusedArgs a = base_args(op);
-  a.in = fb.x_gather;
-  a.vec0 = fb.b;
-  a.vec1 = fb.r_x;
-  a.out0 = fb.r_x;
-  a.out1 = fb.r_y;
+  a.lo = fb.lo;
+  a.hi = fb.hi;
+  const int64_t lo = (int64_t)fb.lo;
+  a.in = at_global(fb.x_gather, fb.gather_base);
+  a.vec0 = at_global(fb.b, lo);
+  a.vec1 = at_global(fb.r_x, lo);
+  a.out0 = at_global(fb.r_x, lo);
+  a.out1 = at_global(fb.r_y, lo);
   a.st = fb.st;
   a.trace = fb.trace;
   a.partials = fb.partials;

@@ -87,6 +87,10 @@ struct FistaBufs {
   double *r_x, *r_y;      // rows (own rows)
   const double* x_gather;    // vector K2 gathers (x, or the shard's x window)
   const double* r_y_gather;  // vector K1 gathers (r_y, or the shard's r_y window)
+  // own range [lo, hi) of rows == columns in global indices; gather windows
+  // start at global index gather_base (0 on one device, a - halo on a shard)
+  uint64_t lo = 0, hi = 0;
+  int64_t gather_base = 0;
   const double* b;
   FistaDev* st;
   FistaSample* trace;

@@ -53,6 +53,9 @@ struct l1b_session {
     b.b = v.b;
     b.x_gather = shard ? x_win : x;
     b.r_y_gather = shard ? r_y_win : r_y;
+    b.lo = shard ? v.row_begin : 0;
+    b.hi = shard ? v.row_end : v.n;
+    b.gather_base = shard ? (int64_t)v.row_begin - (int64_t)v.halo : 0;
     b.st = st;
     b.trace = trace;
     b.partials = partials;

@@ -34,8 +34,11 @@ from . import _native as N
 
 def partition(n: int, world: int):
     """Even split of the n nonempty rows (= nnz-balanced: every row of a
-    banded instance holds 2*#stages entries except at the two ends)."""
-    return [(n * g // world, n * (g + 1) // world) for g in range(world)]
+    banded instance holds 2*#stages entries except at the two ends), with the
+    boundaries on multiples of 16 (16-byte aligned bulk copies); identical to
+    the default split of l1b_generate (abi.cu generate_shard)."""
+    cut = [n if g == world else (n * g // world) // 16 * 16 for g in range(world + 1)]
+    return [(cut[g], cut[g + 1]) for g in range(world)]
 
 
 class _CAI:
@@ -89,6 +92,7 @@ class CudaShard:
         g.s_divisor, g.tau = kw.get("s_divisor", 128), kw.get("tau", 1.0)
         g.theta, g.seed, g.job_index = kw.get("theta", 2 * math.pi / 10), kw.get("seed", 1), 0
         g.fill_bound = 0.9
+        g.lazy_sparse = 0 if getattr(cfg, "op", "auto") == "sparse" else 1
         sh = N.ShardDesc(rank, world, 0, 0)
         h = C.c_void_p()
         N.check(lib.l1b_generate(device, C.byref(g), C.byref(sh), C.byref(h)))

@@ -14,7 +14,7 @@ class CpuShard:
     def __init__(self, oracle, inst, rank, world, max_iters):
         self.rank, self.world = rank, world
         n = inst.n
-        h = len(inst.op.right_offset)
+        h = (len(inst.op.right_offset) + 1) & ~1  # window overhang: #stages rounded up to even
         a, b = partition(n, world)[rank]
         self.own, self.halo, self.a = b - a, h, a
         rp, ri, rv = oracle.csr(inst.op)

@@ -14,11 +14,11 @@ pytestmark = pytest.mark.gpu
 KW = dict(n=4096, stages=4, q=1, s_divisor=100, seed=3, theta=2 * math.pi / 10)
 
 
-def _shards(world, iters):
+def _shards(world, iters, op="auto"):
     from paper_1503_03520_b200 import l1bench
     from paper_1503_03520_b200.distributed import CudaShard
 
-    cfg = l1bench.SolverConfig(max_iters=iters)
+    cfg = l1bench.SolverConfig(max_iters=iters, op=op)
     return [CudaShard(KW, r, world, 0, cfg) for r in range(world)]
 
 
@@ -39,17 +39,17 @@ def _allreduce(shards):
         s.scal.copy_(tot)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_shards_reproduce_single_device_fista(world):
+@pytest.mark.parametrize("world,op", [(2, "sparse"), (3, "sparse"), (2, "matrix_free"), (3, "matrix_free")])
+def test_shards_reproduce_single_device_fista(world, op):
     torch = need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     iters = 60
     inst = l1bench.build_instance(**KW)
     x_ref = np.empty(inst.n)
-    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters), x_ref)
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, op=op), x_ref)
     b_ref = inst.b
-    shards = _shards(world, iters)
+    shards = _shards(world, iters, op)
     for s in shards:  # the shard's own rows of b are the global b, bit for bit
         a, e = s.inst.info.row_begin, s.inst.info.row_end
         np.testing.assert_array_equal(s.inst.b[: e - a], b_ref[a:e])
@@ -73,6 +73,8 @@ def test_shards_reproduce_single_device_fista(world):
         np.testing.assert_array_equal(t.objectives(), outs[0][0].objectives())
     assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
     x = np.concatenate([o[1] for o in outs])
+    if op == "matrix_free":  # same products entry by entry: sharding changes nothing
+        np.testing.assert_array_equal(x, x_ref)
     assert rel_err(x, x_ref) < 1e-12
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
 
@@ -83,7 +85,7 @@ def test_shard_rows_match_global_rows():
 
     inst = l1bench.build_instance(**KW)
     gp, gi, gv = inst.op.csr()
-    for s in _shards(3, 5):
+    for s in _shards(3, 5, "sparse"):
         info = s.inst.info
         a, e, h = int(info.row_begin), int(info.row_end), int(info.halo)
         ptr = np.zeros(info.m + 1, dtype=np.uint64)
