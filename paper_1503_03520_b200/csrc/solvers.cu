@@ -283,7 +283,10 @@ int l1b_session_k1(l1b_session* s) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
-    fista_k1(s->v.At, s->bufs(), s->v.stream);
+    if (s->fused)
+      fista_fused_k1(*s->v.op, s->bufs(), s->v.stream);
+    else
+      fista_k1(s->v.At, s->bufs(), s->v.stream);
   });
 }
 
@@ -291,7 +294,10 @@ int l1b_session_k2(l1b_session* s) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
-    fista_k2(s->v.A, s->bufs(), s->v.stream);
+    if (s->fused)
+      fista_fused_k2(*s->v.op, s->bufs(), s->v.stream);
+    else
+      fista_k2(s->v.A, s->bufs(), s->v.stream);
     s->launched += 1;
   });
 }
