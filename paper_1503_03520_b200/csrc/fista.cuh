@@ -21,6 +21,7 @@ __device__ inline void fista_finalize_device(FistaDev* st, FistaSample* trace) {
   const uint64_t k = st->k + 1;
   double t_next, beta;
   fista_momentum(st, &t_next, &beta);
+  st->beta_y = beta;  // y = trial + beta (trial - x)  (solvers.cpp:349-352)
   if (st->accel) st->t = t_next;
   st->k = k;
   st->f = f;

@@ -330,4 +330,198 @@ void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
   launch_fused<false>(a, st);
 }
 
+// ---------------------------------------------------------------------------
+// One kernel per FISTA iteration (banded operators, one device).
+//
+// Iteration k+1 needs only the last two iterates: y_k = x_k + beta (x_k -
+// x_{k-1}) and r_y = (1 + beta) r_k - beta r_{k-1} are formed on the fly
+// (solvers.cpp:349-357, same operations), so y and r_y are never stored and
+// x / r rotate through three buffers (a tile's halo reads of x_k, x_{k-1}
+// never meet another tile's writes of x_{k+1}).  Per tile [t0, te):
+//   r windows [t0-2H, te+2H):  u = sigma .* r_y ; g = G u        (A^T r_y)
+//   x windows [t0-H, te+H):    trial = S(y - g/L, tau/L); own -> x_{k+1}
+//   own rows:                  r_{k+1} = sigma .* (G^T trial) - b
+// HBM per iteration: x_k, x_{k-1}, r_k, r_{k-1}, sigma, b read + x_{k+1},
+// r_{k+1} written = 64n bytes (96n for the two-kernel pair, 288n for CSR/CSC).
+namespace {
+
+constexpr int kTI = 1024;     // tile entries
+constexpr int kIStages = 2;
+
+struct IterLayout {
+  static constexpr size_t rwin = kTI + 4 * kHaloMax + 2;
+  static constexpr size_t xwin = kTI + 2 * kHaloMax + 2;
+  static constexpr size_t rwin_b = round16(rwin * 8);
+  static constexpr size_t xwin_b = round16(xwin * 8);
+  static constexpr size_t own_b = round16((kTI + 2) * 8);
+  // slot: r_k | r_km1 | sigma (r window) | x_k | x_km1 (x window) | b (own)
+  static constexpr size_t off_rkm1 = rwin_b;
+  static constexpr size_t off_sig = 2 * rwin_b;
+  static constexpr size_t off_xk = 3 * rwin_b;
+  static constexpr size_t off_xkm1 = 3 * rwin_b + xwin_b;
+  static constexpr size_t off_b = 3 * rwin_b + 2 * xwin_b;
+  static constexpr size_t slot_bytes = off_b + own_b;
+  static constexpr size_t bars_off = kIStages * slot_bytes;
+  static constexpr size_t total = bars_off + kIStages * 8;
+};
+
+struct IterArgs {
+  uint64_t n;
+  int halo;
+  StageTab right;
+  const double* sigma;
+  IterBufs b;
+};
+
+__global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
+  FistaDev* st = A.b.st;
+  if (*(volatile int*)&st->stop) return;
+  using L = IterLayout;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
+  const int t = threadIdx.x;
+  const uint64_t n = A.n;
+  const uint64_t H = (uint64_t)A.halo;
+  const uint64_t ntiles = (n + kTI - 1) / kTI;
+  const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const double beta = st->beta_y;  // forms y_k, r_y from the last two iterates
+  const double inv_l = 1.0 / st->lval;
+  const double thr = st->tau * inv_l;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // ||x||_1, nnz, #(trial != y), ||r||^2
+
+  if (t == 0) {
+    for (int s = 0; s < kIStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  struct Win {
+    uint64_t t0, te, r0, r1, x0, x1;
+  };
+  auto window = [&](uint64_t k) {
+    Win w;
+    w.t0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTI;
+    w.te = min(w.t0 + kTI, n);
+    w.r0 = w.t0 > 2 * H ? w.t0 - 2 * H : 0;
+    w.r1 = min(n, w.te + 2 * H);
+    w.x0 = w.t0 > H ? w.t0 - H : 0;
+    w.x1 = min(n, w.te + H);
+    return w;
+  };
+  auto even_bytes = [](uint64_t len) { return (uint32_t)((len + 1) & ~1ull) * 8u; };
+  auto issue = [&](uint64_t k) {
+    const Win w = window(k);
+    unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
+    const uint32_t rb = even_bytes(w.r1 - w.r0), xb = even_bytes(w.x1 - w.x0),
+                   ob = even_bytes(w.te - w.t0);
+    uint64_t* bar = &bars[k % kIStages];
+    mbar_arrive_expect_tx(bar, 3 * rb + 2 * xb + ob);
+    bulk_g2s(slot, A.b.r_k + w.r0, rb, bar);
+    bulk_g2s(slot + L::off_rkm1, A.b.r_km1 + w.r0, rb, bar);
+    bulk_g2s(slot + L::off_sig, A.sigma + w.r0, rb, bar);
+    bulk_g2s(slot + L::off_xk, A.b.x_k + w.x0, xb, bar);
+    bulk_g2s(slot + L::off_xkm1, A.b.x_km1 + w.x0, xb, bar);
+    bulk_g2s(slot + L::off_b, A.b.b + w.t0, ob, bar);
+  };
+
+  if (t == 0)
+    for (uint64_t k = 0; k + 1 < (uint64_t)kIStages && k < mine; ++k) issue(k);
+
+  for (uint64_t k = 0; k < mine; ++k) {
+    if (t == 0 && k + kIStages - 1 < mine) {
+      fence_proxy_async();
+      issue(k + kIStages - 1);
+    }
+    const Win w = window(k);
+    unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
+    double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y -> g
+    const double* s_rm = reinterpret_cast<const double*>(slot + L::off_rkm1);
+    const double* s_sig = reinterpret_cast<const double*>(slot + L::off_sig);
+    double* s_x = reinterpret_cast<double*>(slot + L::off_xk);     // x_k -> y
+    double* s_tr = reinterpret_cast<double*>(slot + L::off_xkm1);  // x_{k-1} -> trial -> G^T trial
+    const double* s_b = reinterpret_cast<const double*>(slot + L::off_b);
+    mbar_wait(&bars[k % kIStages], (uint32_t)((k / kIStages) & 1));
+    const int rl = (int)(w.r1 - w.r0), xl = (int)(w.x1 - w.x0);
+    // 1. u = sigma .* r_y,  r_y = (1 + beta) r_k - beta r_{k-1}
+    for (int q = t; q < rl; q += kThreads) {
+      const double ry = (1.0 + beta) * s_r[q] - beta * s_rm[q];
+      s_r[q] = s_sig[q] * ry;
+    }
+    // 2. y = x_k + beta (x_k - x_{k-1}) on the x window
+    for (int q = t; q < xl; q += kThreads) {
+      const double xk = s_x[q];
+      s_x[q] = xk + beta * (xk - s_tr[q]);
+    }
+    __syncthreads();
+    // 3. g = G u: stages reverse, plain (linops.cpp:469-471)
+    for (int s = A.right.count - 1; s >= 0; --s) {
+      sweep_stage(s_r, w.r0, w.r1, n, A.right.offset[s], A.right.c[s], A.right.s[s], false);
+      __syncthreads();
+    }
+    // 4. trial = S(y - g/L, tau/L) on the x window (solvers.cpp:326-328)
+    const uint64_t xo = w.x0 - w.r0;
+    for (int q = t; q < xl; q += kThreads) {
+      const double y = s_x[q];
+      const double tr = soft_threshold(y - inv_l * s_r[xo + q], thr);
+      s_tr[q] = tr;
+      const uint64_t j = w.x0 + q;
+      if (j >= w.t0 && j < w.te) {
+        A.b.x_next[j] = tr;
+        acc[0] += fabs(tr);
+        acc[1] += tr != 0.0 ? 1.0 : 0.0;
+        acc[2] += tr != y ? 1.0 : 0.0;
+      }
+    }
+    __syncthreads();
+    // 5. G^T trial: stages forward, transposed (linops.cpp:429)
+    for (int s = 0; s < A.right.count; ++s) {
+      sweep_stage(s_tr, w.x0, w.x1, n, A.right.offset[s], A.right.c[s], A.right.s[s], true);
+      __syncthreads();
+    }
+    // 6. r_{k+1} = sigma .* (G^T trial) - b on the own rows (linops.cpp:433, solvers.cpp:330)
+    const int own = (int)(w.te - w.t0);
+    const uint64_t so = w.t0 - w.r0, to = w.t0 - w.x0;
+    for (int q = t; q < own; q += kThreads) {
+      const double rt = s_sig[so + q] * s_tr[to + q] - s_b[q];
+      A.b.r_next[w.t0 + q] = rt;
+      acc[3] += rt * rt;
+    }
+    __syncthreads();
+  }
+  double tot[4];
+  if (grid_sum<4>(acc, A.b.partials, &st->ticket[0], tot) && t == 0) {
+    st->scal[0] = tot[0];
+    st->scal[1] = tot[1];
+    st->scal[2] = tot[2];
+    st->scal[3] = tot[3];
+    fista_finalize_device(st, A.b.trace);
+  }
+}
+
+}  // namespace
+
+void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st) {
+  using L = IterLayout;
+  if (op.right.count > kHaloMax) throw Unsupported("fused operator: more than 16 stages");
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    L1B_CUDA(cudaFuncSetAttribute(fista_iter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L::total));
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_iter_kernel, kThreads,
+                                                          L::total));
+    grid_cap = std::max(1, per_sm) * sm_count();
+  }
+  IterArgs a;
+  a.n = op.n;
+  a.halo = (op.right.count + 1) & ~1;
+  a.right = op.right;
+  a.sigma = op.sigma;
+  a.b = ib;
+  const uint64_t tiles = (op.n + kTI - 1) / kTI;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
+  fista_iter_kernel<<<grid, kThreads, L::total, st>>>(a);
+  L1B_LAUNCHED();
+}
+
 }  // namespace l1b

@@ -151,7 +151,7 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
 // f_0, sample 0 and the loop-head checks before the first iteration
 __device__ void fista_init_finalize(FistaDev* st, FistaSample* trace) {
   {
-    const double f = st->tau * 0.0 + 0.5 * (st->scal[3] + (st->defer ? st->tail_sq : 0.0));
+    const double f = st->tau * 0.0 + 0.5 * (st->scal[3] + st->init_tail);
     const uint64_t ts = global_timer_ns();
     st->t0_ns = ts;
     st->last_ts = ts;

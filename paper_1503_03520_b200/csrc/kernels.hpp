@@ -74,6 +74,8 @@ struct FistaSample {
 };
 struct FistaDev {
   double t, lval, tau, f, nnz, target, tail_sq;
+  double init_tail;  // sum b_i^2 of the rows the init kernel does not cover
+  double beta_y;     // momentum that forms y / r_y from the last two iterates (single-kernel path)
   uint64_t k, max_iters, n_samples, cap, last_sampled, t0_ns, last_ts;
   int stop, status, accel, has_target;
   int defer;        // shards: K2 / init leave scal for the caller's all-reduce
@@ -110,6 +112,21 @@ void fused_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
 void fused_apply_transpose(const OpView& op, const double* r, double* g, cudaStream_t st);
 void fista_fused_k1(const OpView& op, const FistaBufs& fb, cudaStream_t st);
 void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st);
+// one kernel per FISTA iteration (k_fused.cu): x / r rotate through 3 buffers,
+// y and r_y are formed on the fly from the last two iterates
+struct IterBufs {
+  const double* x_k;    // x after iteration k (window reads)
+  const double* x_km1;  // x after iteration k-1
+  const double* r_k;    // r = A x - b after iteration k (rows [0, n))
+  const double* r_km1;
+  double* x_next;       // x after iteration k+1 (own writes)
+  double* r_next;
+  const double* b;
+  FistaDev* st;
+  FistaSample* trace;
+  double* partials;
+};
+void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 

@@ -32,7 +32,10 @@ struct l1b_session {
   l1b_solver_cfg cfg;
   bool accel = true;
   bool shard = false;
-  bool fused = false;  // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
+  bool fused = false;   // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
+  bool single = false;  // ... as one kernel per iteration (one device): x / r rotate
+  double* X[3] = {nullptr, nullptr, nullptr};
+  double* R[3] = {nullptr, nullptr, nullptr};
   uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
   double *x_win = nullptr, *r_y_win = nullptr;  // shard windows (x, r_y point inside)
   double *x = nullptr, *y = nullptr, *r_x = nullptr, *r_y = nullptr, *partials = nullptr;
@@ -43,6 +46,22 @@ struct l1b_session {
   uint64_t launched = 0;
   std::chrono::steady_clock::time_point t0;
   bool time_out = false;
+
+  // launch j computes iteration j+1 from x_j (X[j%3]) and x_{j-1} (X[(j+2)%3])
+  IterBufs iter_bufs(uint64_t j) const {
+    IterBufs ib;
+    ib.x_k = X[j % 3];
+    ib.x_km1 = X[(j + 2) % 3];
+    ib.r_k = R[j % 3];
+    ib.r_km1 = R[(j + 2) % 3];
+    ib.x_next = X[(j + 1) % 3];
+    ib.r_next = R[(j + 1) % 3];
+    ib.b = v.b;
+    ib.st = st;
+    ib.trace = trace;
+    ib.partials = partials;
+    return ib;
+  }
 
   FistaBufs bufs() const {
     FistaBufs b;
@@ -99,7 +118,22 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   const ProblemView& v = s->v;
   cudaStream_t st = v.stream;
   s->shard = v.world > 1;
-  if (s->shard) {
+  s->single = s->fused && !s->shard;
+  if (s->single) {
+    // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows;
+    // X[2] / R[2] stand for the iterate "before" the first one (x_{-1} = x_0)
+    s->nx = v.n;
+    s->nr = v.n;
+    for (int q = 0; q < 3; ++q) {
+      s->X[q] = s->dalloc(v.n);
+      s->R[q] = s->dalloc(v.n);
+      L1B_CUDA(cudaMemsetAsync(s->X[q], 0, v.n * 8, st));
+    }
+    s->x = s->X[0];
+    s->y = s->X[0];
+    s->r_x = s->R[0];
+    s->r_y = s->R[2];
+  } else if (s->shard) {
     // windows: [halo | own | halo]; K1 writes own x, K2 gathers the x window,
     // K2 writes own r_y, K1 gathers the r_y window
     s->halo = v.halo;
@@ -138,7 +172,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->allocs.push_back(s->st);
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
   L1B_CUDA(cudaMemsetAsync(s->x, 0, s->nx * sizeof(double), st));
-  if (s->accel) L1B_CUDA(cudaMemsetAsync(s->y, 0, s->nx * sizeof(double), st));
+  if (s->accel && !s->single) L1B_CUDA(cudaMemsetAsync(s->y, 0, s->nx * sizeof(double), st));
   FistaDev h;
   std::memset(&h, 0, sizeof(h));
   h.t = 1.0;  // solvers.cpp:304
@@ -151,17 +185,20 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.cap = s->cap;
   h.accel = s->accel ? 1 : 0;
   h.defer = s->shard ? 1 : 0;
+  h.init_tail = s->single ? v.tail_sq_band : 0.0;  // the init kernel covers rows [0, nr)
   *s->h_st = h;
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
   s->t0 = std::chrono::steady_clock::now();
   // residuals over all (own) rows: rows >= m_active keep r = -b for the whole run
-  fista_init(s->bufs(), s->nr, st);
+  fista_init(s->bufs(), s->nr, st);  // (single: writes r_0 into R[0] and R[2])
 }
 
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
   for (uint64_t i = 0; i < iters; ++i) {
-    if (s->fused) {
+    if (s->single) {
+      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), s->v.stream);
+    } else if (s->fused) {
       fista_fused_k1(*s->v.op, b, s->v.stream);
       fista_fused_k2(*s->v.op, b, s->v.stream);
     } else {
@@ -187,8 +224,9 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   if (kept)
     L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
                              cudaMemcpyDeviceToHost, st));
-  if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, s->x, s->nx * 8, cudaMemcpyDeviceToHost, st));
-  if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, s->x, s->nx * 8, cudaMemcpyDeviceToDevice, st));
+  const double* xf = s->single ? s->X[h.k % 3] : s->x;  // x after the last executed iteration
+  if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, xf, s->nx * 8, cudaMemcpyDeviceToHost, st));
+  if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, xf, s->nx * 8, cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   // final sample when the last iteration was not sampled (solvers.cpp:379)
   if (h.last_sampled != h.k) tr.push_back(FistaSample{h.k, h.f, h.nnz, h.last_ts});
@@ -331,15 +369,19 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     const FistaBufs b = s->bufs();
     for (uint64_t i = 0; i < iters; ++i) {
       L1B_CUDA(cudaEventRecord(ev[3 * i], st));
-      if (s->fused)
+      if (s->single)
+        fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), st);
+      else if (s->fused)
         fista_fused_k1(*s->v.op, b, st);
       else
         fista_k1(s->v.At, b, st);
       L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
-      if (s->fused)
+      if (s->single) {
+      } else if (s->fused) {
         fista_fused_k2(*s->v.op, b, st);
-      else
+      } else {
         fista_k2(s->v.A, b, st);
+      }
       L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
     }
     s->launched += iters;
