@@ -373,6 +373,46 @@ struct IterArgs {
   IterBufs b;
 };
 
+// All S stages of one product for two consecutive outputs [P, P+2), in
+// registers: the window [P-S, P+2+S) of the input is loaded (entries outside
+// [0, n) are never touched by a rotation), every pair of every stage that
+// lies inside the window is rotated, and the two centre entries -- whose
+// dependency cone fits the window -- come out exactly as in the reference's
+// full-vector sweeps.  No barrier between stages.
+template <int S>
+__device__ __forceinline__ void chain2(const double* win, int64_t g0, int64_t n,
+                                       const StageTab& tab, bool transposed, double& o0,
+                                       double& o1) {
+  constexpr int W = 2 * S + 2;
+  double v[W];
+  if ((S & 1) == 0) {  // window starts on an even smem index: 16-byte loads
+    const double2* w2 = reinterpret_cast<const double2*>(win);
+#pragma unroll
+    for (int q = 0; q < W / 2; ++q) {
+      const double2 d = w2[q];
+      v[2 * q] = d.x;
+      v[2 * q + 1] = d.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; ++q) v[q] = win[q];
+  }
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int s = transposed ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
+    const int64_t o = tab.offset[s];
+    const double c = tab.c[s], sn = tab.s[s];
+#pragma unroll
+    for (int l = 0; l + 1 < W; ++l) {
+      const int64_t p = g0 + l;
+      if (((p - o) & 1) == 0 && p >= o && p + 1 < n) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+    }
+  }
+  o0 = v[S];
+  o1 = v[S + 1];
+}
+
+template <int S>
 __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   FistaDev* st = A.b.st;
   if (*(volatile int*)&st->stop) return;
@@ -380,9 +420,9 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
   const int t = threadIdx.x;
-  const uint64_t n = A.n;
-  const uint64_t H = (uint64_t)A.halo;
-  const uint64_t ntiles = (n + kTI - 1) / kTI;
+  const int64_t n = (int64_t)A.n;
+  constexpr int64_t H = (S + 1) & ~1;  // window overhang (even)
+  const uint64_t ntiles = (A.n + kTI - 1) / kTI;
   const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const double beta = st->beta_y;  // forms y_k, r_y from the last two iterates
   const double inv_l = 1.0 / st->lval;
@@ -395,96 +435,99 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   }
   __syncthreads();
 
-  struct Win {
-    uint64_t t0, te, r0, r1, x0, x1;
-  };
-  auto window = [&](uint64_t k) {
-    Win w;
-    w.t0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTI;
-    w.te = min(w.t0 + kTI, n);
-    w.r0 = w.t0 > 2 * H ? w.t0 - 2 * H : 0;
-    w.r1 = min(n, w.te + 2 * H);
-    w.x0 = w.t0 > H ? w.t0 - H : 0;
-    w.x1 = min(n, w.te + H);
-    return w;
-  };
-  auto even_bytes = [](uint64_t len) { return (uint32_t)((len + 1) & ~1ull) * 8u; };
+  // tile [t0, te); r window [t0 - 2H, te + 2H) and x window [t0 - H, te + H),
+  // both kept on their unclipped grid in shared memory (entries outside
+  // [0, n) are zero-filled and never rotated)
+  auto tile0 = [&](uint64_t k) { return (int64_t)((blockIdx.x + k * gridDim.x) * (uint64_t)kTI); };
+  auto even_bytes = [](int64_t len) { return (uint32_t)((len + 1) & ~1ll) * 8u; };
   auto issue = [&](uint64_t k) {
-    const Win w = window(k);
+    const int64_t t0 = tile0(k), te = min(t0 + kTI, n);
+    const int64_t r0 = max(t0 - 2 * H, (int64_t)0), r1 = min(n, te + 2 * H);
+    const int64_t x0 = max(t0 - H, (int64_t)0), x1 = min(n, te + H);
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
-    const uint32_t rb = even_bytes(w.r1 - w.r0), xb = even_bytes(w.x1 - w.x0),
-                   ob = even_bytes(w.te - w.t0);
+    // smem index 0 <-> global t0 - 2H (r) / t0 - H (x)
+    const int64_t rs = r0 - (t0 - 2 * H), xs = x0 - (t0 - H);
+    const uint32_t rb = even_bytes(r1 - r0), xb = even_bytes(x1 - x0), ob = even_bytes(te - t0);
     uint64_t* bar = &bars[k % kIStages];
     mbar_arrive_expect_tx(bar, 3 * rb + 2 * xb + ob);
-    bulk_g2s(slot, A.b.r_k + w.r0, rb, bar);
-    bulk_g2s(slot + L::off_rkm1, A.b.r_km1 + w.r0, rb, bar);
-    bulk_g2s(slot + L::off_sig, A.sigma + w.r0, rb, bar);
-    bulk_g2s(slot + L::off_xk, A.b.x_k + w.x0, xb, bar);
-    bulk_g2s(slot + L::off_xkm1, A.b.x_km1 + w.x0, xb, bar);
-    bulk_g2s(slot + L::off_b, A.b.b + w.t0, ob, bar);
+    bulk_g2s(slot + rs * 8, A.b.r_k + r0, rb, bar);
+    bulk_g2s(slot + L::off_rkm1 + rs * 8, A.b.r_km1 + r0, rb, bar);
+    bulk_g2s(slot + L::off_sig + rs * 8, A.sigma + r0, rb, bar);
+    bulk_g2s(slot + L::off_xk + xs * 8, A.b.x_k + x0, xb, bar);
+    bulk_g2s(slot + L::off_xkm1 + xs * 8, A.b.x_km1 + x0, xb, bar);
+    bulk_g2s(slot + L::off_b, A.b.b + t0, ob, bar);
   };
 
-  if (t == 0)
+  // zero the out-of-range margins of both slots once (they are never written by TMA)
+  for (int q = t; q < (int)(kIStages * L::slot_bytes / 8); q += kThreads)
+    reinterpret_cast<double*>(smem)[q] = 0.0;
+  __syncthreads();
+  if (t == 0) {
+    fence_proxy_async();
     for (uint64_t k = 0; k + 1 < (uint64_t)kIStages && k < mine; ++k) issue(k);
+  }
 
   for (uint64_t k = 0; k < mine; ++k) {
     if (t == 0 && k + kIStages - 1 < mine) {
       fence_proxy_async();
       issue(k + kIStages - 1);
     }
-    const Win w = window(k);
+    const int64_t t0 = tile0(k), te = min(t0 + kTI, n);
+    const int64_t gr = t0 - 2 * H, gx = t0 - H;  // global index of smem entry 0
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
-    double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y -> g
+    double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y
     const double* s_rm = reinterpret_cast<const double*>(slot + L::off_rkm1);
     const double* s_sig = reinterpret_cast<const double*>(slot + L::off_sig);
     double* s_x = reinterpret_cast<double*>(slot + L::off_xk);     // x_k -> y
-    double* s_tr = reinterpret_cast<double*>(slot + L::off_xkm1);  // x_{k-1} -> trial -> G^T trial
+    double* s_tr = reinterpret_cast<double*>(slot + L::off_xkm1);  // x_{k-1} -> trial
     const double* s_b = reinterpret_cast<const double*>(slot + L::off_b);
     mbar_wait(&bars[k % kIStages], (uint32_t)((k / kIStages) & 1));
-    const int rl = (int)(w.r1 - w.r0), xl = (int)(w.x1 - w.x0);
-    // 1. u = sigma .* r_y,  r_y = (1 + beta) r_k - beta r_{k-1}
-    for (int q = t; q < rl; q += kThreads) {
+    const int rlen = (int)(te - t0 + 4 * H), xlen = (int)(te - t0 + 2 * H);
+    // 1. u = sigma .* r_y, r_y = (1 + beta) r_k - beta r_{k-1}; y = x_k + beta (x_k - x_{k-1})
+    for (int q = t; q < rlen; q += kThreads) {
       const double ry = (1.0 + beta) * s_r[q] - beta * s_rm[q];
       s_r[q] = s_sig[q] * ry;
     }
-    // 2. y = x_k + beta (x_k - x_{k-1}) on the x window
-    for (int q = t; q < xl; q += kThreads) {
+    for (int q = t; q < xlen; q += kThreads) {
       const double xk = s_x[q];
       s_x[q] = xk + beta * (xk - s_tr[q]);
     }
     __syncthreads();
-    // 3. g = G u: stages reverse, plain (linops.cpp:469-471)
-    for (int s = A.right.count - 1; s >= 0; --s) {
-      sweep_stage(s_r, w.r0, w.r1, n, A.right.offset[s], A.right.c[s], A.right.s[s], false);
-      __syncthreads();
-    }
-    // 4. trial = S(y - g/L, tau/L) on the x window (solvers.cpp:326-328)
-    const uint64_t xo = w.x0 - w.r0;
-    for (int q = t; q < xl; q += kThreads) {
-      const double y = s_x[q];
-      const double tr = soft_threshold(y - inv_l * s_r[xo + q], thr);
-      s_tr[q] = tr;
-      const uint64_t j = w.x0 + q;
-      if (j >= w.t0 && j < w.te) {
-        A.b.x_next[j] = tr;
-        acc[0] += fabs(tr);
-        acc[1] += tr != 0.0 ? 1.0 : 0.0;
-        acc[2] += tr != y ? 1.0 : 0.0;
+    // 2. g = G u on the x window (two entries per thread, stages in registers),
+    //    trial = S(y - g/L, tau/L); own entries -> x_{k+1}
+    for (int q = 2 * t; q < xlen; q += 2 * kThreads) {
+      double g0v, g1v;
+      chain2<S>(s_r + (q + H - S), gx + q - S, n, A.right, false, g0v, g1v);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int qq = q + e;
+        if (qq >= xlen) break;
+        const double y = s_x[qq];
+        const double tr = soft_threshold(y - inv_l * (e ? g1v : g0v), thr);
+        const int64_t j = gx + qq;
+        if (j >= t0 && j < te) {
+          A.b.x_next[j] = tr;
+          acc[0] += fabs(tr);
+          acc[1] += tr != 0.0 ? 1.0 : 0.0;
+          acc[2] += tr != y ? 1.0 : 0.0;
+        }
+        s_tr[qq] = (j >= 0 && j < n) ? tr : 0.0;
       }
     }
     __syncthreads();
-    // 5. G^T trial: stages forward, transposed (linops.cpp:429)
-    for (int s = 0; s < A.right.count; ++s) {
-      sweep_stage(s_tr, w.x0, w.x1, n, A.right.offset[s], A.right.c[s], A.right.s[s], true);
-      __syncthreads();
-    }
-    // 6. r_{k+1} = sigma .* (G^T trial) - b on the own rows (linops.cpp:433, solvers.cpp:330)
-    const int own = (int)(w.te - w.t0);
-    const uint64_t so = w.t0 - w.r0, to = w.t0 - w.x0;
-    for (int q = t; q < own; q += kThreads) {
-      const double rt = s_sig[so + q] * s_tr[to + q] - s_b[q];
-      A.b.r_next[w.t0 + q] = rt;
-      acc[3] += rt * rt;
+    // 3. r_{k+1} = sigma .* (G^T trial) - b on the own rows
+    const int own = (int)(te - t0);
+    for (int q = 2 * t; q < own; q += 2 * kThreads) {
+      double a0, a1;
+      chain2<S>(s_tr + (q + H - S), t0 + q - S, n, A.right, true, a0, a1);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int qq = q + e;
+        if (qq >= own) break;
+        const double rt = s_sig[2 * H + qq] * (e ? a1 : a0) - s_b[qq];
+        A.b.r_next[t0 + qq] = rt;
+        acc[3] += rt * rt;
+      }
     }
     __syncthreads();
   }
@@ -498,30 +541,44 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   }
 }
 
-}  // namespace
-
-void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st) {
+template <int S>
+void launch_iter(const IterArgs& a, cudaStream_t st) {
   using L = IterLayout;
-  if (op.right.count > kHaloMax) throw Unsupported("fused operator: more than 16 stages");
   static int grid_cap = 0;
   if (!grid_cap) {
-    L1B_CUDA(cudaFuncSetAttribute(fista_iter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    L1B_CUDA(cudaFuncSetAttribute(fista_iter_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)L::total));
     int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_iter_kernel, kThreads,
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_iter_kernel<S>, kThreads,
                                                           L::total));
     grid_cap = std::max(1, per_sm) * sm_count();
   }
+  const uint64_t tiles = (a.n + kTI - 1) / kTI;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
+  fista_iter_kernel<S><<<grid, kThreads, L::total, st>>>(a);
+  L1B_LAUNCHED();
+}
+
+}  // namespace
+
+bool fused_iter_supported(const OpView& op) {
+  return fused_supported(op) && op.right.count >= 1 && op.right.count <= 4;
+}
+
+void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st) {
   IterArgs a;
   a.n = op.n;
   a.halo = (op.right.count + 1) & ~1;
   a.right = op.right;
   a.sigma = op.sigma;
   a.b = ib;
-  const uint64_t tiles = (op.n + kTI - 1) / kTI;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
-  fista_iter_kernel<<<grid, kThreads, L::total, st>>>(a);
-  L1B_LAUNCHED();
+  switch (op.right.count) {
+    case 1: return launch_iter<1>(a, st);
+    case 2: return launch_iter<2>(a, st);
+    case 3: return launch_iter<3>(a, st);
+    case 4: return launch_iter<4>(a, st);
+    default: throw Unsupported("single-kernel FISTA: 1..4 stages");
+  }
 }
 
 }  // namespace l1b

@@ -126,6 +126,7 @@ struct IterBufs {
   FistaSample* trace;
   double* partials;
 };
+bool fused_iter_supported(const OpView& op);  // banded, 1..4 stages
 void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);

@@ -118,7 +118,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   const ProblemView& v = s->v;
   cudaStream_t st = v.stream;
   s->shard = v.world > 1;
-  s->single = s->fused && !s->shard;
+  s->single = s->fused && !s->shard && fused_iter_supported(*v.op);
   if (s->single) {
     // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows;
     // X[2] / R[2] stand for the iterate "before" the first one (x_{-1} = x_0)
