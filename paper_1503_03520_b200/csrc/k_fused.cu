@@ -373,17 +373,17 @@ struct IterArgs {
   IterBufs b;
 };
 
-// All S stages of one product for two consecutive outputs [P, P+2), in
-// registers: the window [P-S, P+2+S) of the input is loaded (entries outside
-// [0, n) are never touched by a rotation), every pair of every stage that
-// lies inside the window is rotated, and the two centre entries -- whose
-// dependency cone fits the window -- come out exactly as in the reference's
-// full-vector sweeps.  No barrier between stages.
-template <int S>
-__device__ __forceinline__ void chain2(const double* win, int64_t g0, int64_t n,
-                                       const StageTab& tab, bool transposed, double& o0,
-                                       double& o1) {
-  constexpr int W = 2 * S + 2;
+// All S stages of one product for NO consecutive outputs [P, P+NO), in
+// registers: the window [P-S, P+NO+S) of the input is loaded, every pair of
+// every stage that lies inside the window is rotated, and the NO centre
+// entries -- whose dependency cones fit the window -- come out exactly as in
+// the reference's full-vector sweeps.  No barrier between stages.  The pair
+// parity of a stage is warp-uniform (P is a multiple of NO for every thread),
+// so away from the global ends the pairs are a fixed unrolled set.
+template <int S, int NO>
+__device__ __forceinline__ void chain(const double* win, int64_t g0, int64_t n,
+                                      const StageTab& tab, bool transposed, double (&out)[NO]) {
+  constexpr int W = 2 * S + NO;
   double v[W];
   if ((S & 1) == 0) {  // window starts on an even smem index: 16-byte loads
     const double2* w2 = reinterpret_cast<const double2*>(win);
@@ -397,20 +397,34 @@ __device__ __forceinline__ void chain2(const double* win, int64_t g0, int64_t n,
 #pragma unroll
     for (int q = 0; q < W; ++q) v[q] = win[q];
   }
+  const bool interior = g0 >= 1 && g0 + W <= n;  // every pair start p >= 1 >= offset, p+1 < n
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int s = transposed ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
     const int64_t o = tab.offset[s];
     const double c = tab.c[s], sn = tab.s[s];
+    const int par = (int)((g0 - o) & 1);
+    if (interior) {
+      if (par == 0) {
 #pragma unroll
-    for (int l = 0; l + 1 < W; ++l) {
-      const int64_t p = g0 + l;
-      if (((p - o) & 1) == 0 && p >= o && p + 1 < n) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+        for (int l = 0; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+      } else {
+#pragma unroll
+        for (int l = 1; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l + 1 < W; ++l) {
+        const int64_t p = g0 + l;
+        if ((l & 1) == par && p >= o && p + 1 < n) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+      }
     }
   }
-  o0 = v[S];
-  o1 = v[S + 1];
+#pragma unroll
+  for (int e = 0; e < NO; ++e) out[e] = v[S + e];
 }
+
+constexpr int kNO = 4;  // outputs per thread and chain
 
 template <int S>
 __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
@@ -495,15 +509,15 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
     __syncthreads();
     // 2. g = G u on the x window (two entries per thread, stages in registers),
     //    trial = S(y - g/L, tau/L); own entries -> x_{k+1}
-    for (int q = 2 * t; q < xlen; q += 2 * kThreads) {
-      double g0v, g1v;
-      chain2<S>(s_r + (q + H - S), gx + q - S, n, A.right, false, g0v, g1v);
+    for (int q = kNO * t; q < xlen; q += kNO * kThreads) {
+      double g[kNO];
+      chain<S, kNO>(s_r + (q + H - S), gx + q - S, n, A.right, false, g);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
         if (qq >= xlen) break;
         const double y = s_x[qq];
-        const double tr = soft_threshold(y - inv_l * (e ? g1v : g0v), thr);
+        const double tr = soft_threshold(y - inv_l * g[e], thr);
         const int64_t j = gx + qq;
         if (j >= t0 && j < te) {
           A.b.x_next[j] = tr;
@@ -517,14 +531,14 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
     __syncthreads();
     // 3. r_{k+1} = sigma .* (G^T trial) - b on the own rows
     const int own = (int)(te - t0);
-    for (int q = 2 * t; q < own; q += 2 * kThreads) {
-      double a0, a1;
-      chain2<S>(s_tr + (q + H - S), t0 + q - S, n, A.right, true, a0, a1);
+    for (int q = kNO * t; q < own; q += kNO * kThreads) {
+      double av[kNO];
+      chain<S, kNO>(s_tr + (q + H - S), t0 + q - S, n, A.right, true, av);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
         if (qq >= own) break;
-        const double rt = s_sig[2 * H + qq] * (e ? a1 : a0) - s_b[qq];
+        const double rt = s_sig[2 * H + qq] * av[e] - s_b[qq];
         A.b.r_next[t0 + qq] = rt;
         acc[3] += rt * rt;
       }
