@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   const int t = threadIdx.x;
   const int64_t n = (int64_t)A.n;
   constexpr int64_t H = (S + 1) & ~1;  // window overhang (even)
-  const uint64_t ntiles = (A.n + kTI - 1) / kTI;
+  constexpr int64_t TT = kTI - 2 * H;    // tile: the x window is exactly kNO * kThreads entries
+  const uint64_t ntiles = (A.n + TT - 1) / TT;
   const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const double beta = st->beta_y;  // forms y_k, r_y from the last two iterates
   const double inv_l = 1.0 / st->lval;
@@ -452,10 +453,10 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   // tile [t0, te); r window [t0 - 2H, te + 2H) and x window [t0 - H, te + H),
   // both kept on their unclipped grid in shared memory (entries outside
   // [0, n) are zero-filled and never rotated)
-  auto tile0 = [&](uint64_t k) { return (int64_t)((blockIdx.x + k * gridDim.x) * (uint64_t)kTI); };
+  auto tile0 = [&](uint64_t k) { return (int64_t)((blockIdx.x + k * gridDim.x) * (uint64_t)TT); };
   auto even_bytes = [](int64_t len) { return (uint32_t)((len + 1) & ~1ll) * 8u; };
   auto issue = [&](uint64_t k) {
-    const int64_t t0 = tile0(k), te = min(t0 + kTI, n);
+    const int64_t t0 = tile0(k), te = min(t0 + TT, n);
     const int64_t r0 = max(t0 - 2 * H, (int64_t)0), r1 = min(n, te + 2 * H);
     const int64_t x0 = max(t0 - H, (int64_t)0), x1 = min(n, te + H);
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
       fence_proxy_async();
       issue(k + kIStages - 1);
     }
-    const int64_t t0 = tile0(k), te = min(t0 + kTI, n);
+    const int64_t t0 = tile0(k), te = min(t0 + TT, n);
     const int64_t gr = t0 - 2 * H, gx = t0 - H;  // global index of smem entry 0
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
     double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y
@@ -567,7 +568,8 @@ void launch_iter(const IterArgs& a, cudaStream_t st) {
                                                           L::total));
     grid_cap = std::max(1, per_sm) * sm_count();
   }
-  const uint64_t tiles = (a.n + kTI - 1) / kTI;
+  constexpr uint64_t TT = kTI - 2 * ((S + 1) & ~1);
+  const uint64_t tiles = (a.n + TT - 1) / TT;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
   fista_iter_kernel<S><<<grid, kThreads, L::total, st>>>(a);
   L1B_LAUNCHED();
