@@ -83,17 +83,20 @@ struct l1b_session {
 
   ~l1b_session() {
     cudaSetDevice(v.device);
+    for (void* q : allocs) cudaFreeAsync(q, v.stream);  // back to the stream-ordered pool
     if (v.stream) cudaStreamSynchronize(v.stream);
-    for (void* q : allocs) cudaFree(q);
     if (h_st) cudaFreeHost(h_st);
   }
   std::vector<void*> allocs;
-  double* dalloc(uint64_t count) {
-    double* q = nullptr;
-    L1B_CUDA(cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(double)));
+  // stream-ordered allocations from the device pool (kept cached between
+  // sessions, see keep_pool): a session costs no cudaMalloc after the first
+  void* valloc(size_t bytes) {
+    void* q = nullptr;
+    L1B_CUDA(cudaMallocAsync(&q, std::max<size_t>(bytes, 16), v.stream));
     allocs.push_back(q);
     return q;
   }
+  double* dalloc(uint64_t count) { return (double*)valloc((count + 2) * sizeof(double)); }
 };
 
 namespace {
@@ -104,7 +107,21 @@ uint64_t sample_capacity(uint64_t max_iters) {
   return std::min<uint64_t>(c, 1ull << 22);
 }
 
+// Keep freed pool memory cached on the device (release threshold = max), so
+// repeated solves on resident instances do not go back to the driver.
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
+  keep_pool(problem_view(p, false).device);
   s->prob = p;
   {
     const ProblemView probe = problem_view(p, false);
@@ -166,10 +183,8 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   }
   s->partials = s->dalloc((uint64_t)spmv_grid_max() * 4);
   s->cap = sample_capacity(cfg->max_iters);
-  L1B_CUDA(cudaMalloc(&s->trace, s->cap * sizeof(FistaSample)));
-  s->allocs.push_back(s->trace);
-  L1B_CUDA(cudaMalloc(&s->st, sizeof(FistaDev)));
-  s->allocs.push_back(s->st);
+  s->trace = (FistaSample*)s->valloc(s->cap * sizeof(FistaSample));
+  s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
   L1B_CUDA(cudaMemsetAsync(s->x, 0, s->nx * sizeof(double), st));
   if (s->accel && !s->single) L1B_CUDA(cudaMemsetAsync(s->y, 0, s->nx * sizeof(double), st));

@@ -475,7 +475,13 @@ def run_solver(inst: ProblemInstance, cfg: SolverConfig, x_out: Optional[np.ndar
     """run_solver (solvers.cpp:574-581).  When ``x_out`` (float64[n]) is given
     the final iterate is copied into it, like the reference's x_out pointer."""
     c = cfg.to_c()
-    cap = max(1, min(cap, cfg.max_iters + 4 if cfg.max_iters < cap else cap))
+    # trace capacity: every iteration up to 1000, then every 10th (solvers.cpp:368-371)
+    # for ista/fista; one sample per sweep / Newton step otherwise
+    if cfg.id in ("fista", "ista"):
+        need = min(cfg.max_iters, 1000) + max(0, cfg.max_iters - 1000) // 10 + 3
+    else:
+        need = cfg.max_iters + 2
+    cap = max(1, min(cap, need))
     samples = (N.Sample * cap)()
     summ = N.Summary()
     if x_out is not None:
