@@ -255,10 +255,19 @@ int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations);
  * Windows: entry h + j of x_win / r_y_win is own column / row row_begin + j;
  * entries [0, h) and [h + own, own + 2h) are the neighbours' boundary values. */
 typedef struct {
-  double* x_win;    /* own + 2*halo */
-  double* r_y_win;  /* own + 2*halo */
+  double* x_win;    /* own + 2*halo (two-kernel mode) */
+  double* r_y_win;  /* own + 2*halo (two-kernel mode) */
   double* scal;     /* 4 doubles: ||x||_1, nnz(x), #(trial != y), ||r||^2 -- sum over ranks */
   uint64_t own, halo;
+  /* single-kernel mode (matrix-free, 1..4 stages): l1b_session_k1 runs iteration
+   * j+1 from x_j = x_bufs[j%3], x_{j-1} = x_bufs[(j+2)%3] (same for r) into
+   * x_bufs[(j+1)%3] / r_bufs[(j+1)%3]; the caller then exchanges the halos of
+   * those two (x_halo / r_halo entries each side); l1b_session_k2 is a no-op.
+   * Before the first iteration r_bufs[0] and r_bufs[2] need their halos. */
+  int single;
+  double* x_bufs[3];  /* own + 2*x_halo */
+  double* r_bufs[3];  /* own + 2*r_halo */
+  uint64_t x_halo, r_halo;
 } l1b_shard_buffers;
 int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
 int l1b_session_k1(l1b_session* s);

@@ -53,7 +53,9 @@ class ProblemInfo(C.Structure):
 
 
 class ShardBuffers(C.Structure):
-    _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64)]
+    _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64),
+                ("single", C.c_int), ("x_bufs", vp * 3), ("r_bufs", vp * 3), ("x_halo", u64),
+                ("r_halo", u64)]
 
 
 class Cert(C.Structure):

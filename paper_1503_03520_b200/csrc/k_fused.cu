@@ -367,6 +367,7 @@ struct IterLayout {
 
 struct IterArgs {
   uint64_t n;
+  uint64_t lo, hi;  // own rows == columns [lo, hi) (a shard's block; [0, n) on one device)
   int halo;
   StageTab right;
   const double* sigma;
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   const int64_t n = (int64_t)A.n;
   constexpr int64_t H = (S + 1) & ~1;  // window overhang (even)
   constexpr int64_t TT = kTI - 2 * H;    // tile: the x window is exactly kNO * kThreads entries
-  const uint64_t ntiles = (A.n + TT - 1) / TT;
+  const uint64_t ntiles = (A.hi - A.lo + TT - 1) / TT;
   const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const double beta = st->beta_y;  // forms y_k, r_y from the last two iterates
   const double inv_l = 1.0 / st->lval;
@@ -453,10 +454,12 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   // tile [t0, te); r window [t0 - 2H, te + 2H) and x window [t0 - H, te + H),
   // both kept on their unclipped grid in shared memory (entries outside
   // [0, n) are zero-filled and never rotated)
-  auto tile0 = [&](uint64_t k) { return (int64_t)((blockIdx.x + k * gridDim.x) * (uint64_t)TT); };
+  auto tile0 = [&](uint64_t k) {
+    return (int64_t)(A.lo + (blockIdx.x + k * gridDim.x) * (uint64_t)TT);
+  };
   auto even_bytes = [](int64_t len) { return (uint32_t)((len + 1) & ~1ll) * 8u; };
   auto issue = [&](uint64_t k) {
-    const int64_t t0 = tile0(k), te = min(t0 + TT, n);
+    const int64_t t0 = tile0(k), te = min(t0 + TT, (int64_t)A.hi);
     const int64_t r0 = max(t0 - 2 * H, (int64_t)0), r1 = min(n, te + 2 * H);
     const int64_t x0 = max(t0 - H, (int64_t)0), x1 = min(n, te + H);
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
       fence_proxy_async();
       issue(k + kIStages - 1);
     }
-    const int64_t t0 = tile0(k), te = min(t0 + TT, n);
+    const int64_t t0 = tile0(k), te = min(t0 + TT, (int64_t)A.hi);
     const int64_t gr = t0 - 2 * H, gx = t0 - H;  // global index of smem entry 0
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
     double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
     st->scal[1] = tot[1];
     st->scal[2] = tot[2];
     st->scal[3] = tot[3];
-    fista_finalize_device(st, A.b.trace);
+    if (!st->defer) fista_finalize_device(st, A.b.trace);
   }
 }
 
@@ -569,7 +572,7 @@ void launch_iter(const IterArgs& a, cudaStream_t st) {
     grid_cap = std::max(1, per_sm) * sm_count();
   }
   constexpr uint64_t TT = kTI - 2 * ((S + 1) & ~1);
-  const uint64_t tiles = (a.n + TT - 1) / TT;
+  const uint64_t tiles = (a.hi - a.lo + TT - 1) / TT;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
   fista_iter_kernel<S><<<grid, kThreads, L::total, st>>>(a);
   L1B_LAUNCHED();
@@ -581,9 +584,12 @@ bool fused_iter_supported(const OpView& op) {
   return fused_supported(op) && op.right.count >= 1 && op.right.count <= 4;
 }
 
-void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st) {
+void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi,
+                      cudaStream_t st) {
   IterArgs a;
   a.n = op.n;
+  a.lo = lo;
+  a.hi = hi;
   a.halo = (op.right.count + 1) & ~1;
   a.right = op.right;
   a.sigma = op.sigma;

@@ -127,7 +127,10 @@ struct IterBufs {
   double* partials;
 };
 bool fused_iter_supported(const OpView& op);  // banded, 1..4 stages
-void fista_fused_iter(const OpView& op, const IterBufs& ib, cudaStream_t st);
+// lines [lo, hi) (a shard's own block, [0, n) on one device); every IterBufs
+// pointer is indexed by GLOBAL entry
+void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi,
+                      cudaStream_t st);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 

@@ -36,6 +36,7 @@ struct l1b_session {
   bool single = false;  // ... as one kernel per iteration (one device): x / r rotate
   double* X[3] = {nullptr, nullptr, nullptr};
   double* R[3] = {nullptr, nullptr, nullptr};
+  uint64_t xh = 0, rh = 0;  // single-kernel windows: x / r halo widths (shards: H / 2H)
   uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
   double *x_win = nullptr, *r_y_win = nullptr;  // shard windows (x, r_y point inside)
   double *x = nullptr, *y = nullptr, *r_x = nullptr, *r_y = nullptr, *partials = nullptr;
@@ -49,14 +50,18 @@ struct l1b_session {
 
   // launch j computes iteration j+1 from x_j (X[j%3]) and x_{j-1} (X[(j+2)%3])
   IterBufs iter_bufs(uint64_t j) const {
+    // global-index views: window entry xh + (g - lo) holds global entry g
+    const int64_t lo = shard ? (int64_t)v.row_begin : 0;
+    auto gx = [&](double* p) { return p + (int64_t)xh - lo; };
+    auto gr = [&](double* p) { return p + (int64_t)rh - lo; };
     IterBufs ib;
-    ib.x_k = X[j % 3];
-    ib.x_km1 = X[(j + 2) % 3];
-    ib.r_k = R[j % 3];
-    ib.r_km1 = R[(j + 2) % 3];
-    ib.x_next = X[(j + 1) % 3];
-    ib.r_next = R[(j + 1) % 3];
-    ib.b = v.b;
+    ib.x_k = gx(X[j % 3]);
+    ib.x_km1 = gx(X[(j + 2) % 3]);
+    ib.r_k = gr(R[j % 3]);
+    ib.r_km1 = gr(R[(j + 2) % 3]);
+    ib.x_next = gx(X[(j + 1) % 3]);
+    ib.r_next = gr(R[(j + 1) % 3]);
+    ib.b = v.b - lo;
     ib.st = st;
     ib.trace = trace;
     ib.partials = partials;
@@ -135,21 +140,26 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   const ProblemView& v = s->v;
   cudaStream_t st = v.stream;
   s->shard = v.world > 1;
-  s->single = s->fused && !s->shard && fused_iter_supported(*v.op);
+  s->single = s->fused && fused_iter_supported(*v.op);
   if (s->single) {
-    // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows;
+    // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows
+    // (a shard: its own rows plus halos of H for x and 2H for r);
     // X[2] / R[2] stand for the iterate "before" the first one (x_{-1} = x_0)
-    s->nx = v.n;
-    s->nr = v.n;
+    const uint64_t H = ((uint64_t)v.op->right.count + 1) & ~1ull;
+    s->nx = s->nr = s->shard ? v.row_end - v.row_begin : v.n;
+    s->xh = s->shard ? H : 0;
+    s->rh = s->shard ? 2 * H : 0;
+    s->halo = s->xh;
     for (int q = 0; q < 3; ++q) {
-      s->X[q] = s->dalloc(v.n);
-      s->R[q] = s->dalloc(v.n);
-      L1B_CUDA(cudaMemsetAsync(s->X[q], 0, v.n * 8, st));
+      s->X[q] = s->dalloc(s->nx + 2 * s->xh);
+      s->R[q] = s->dalloc(s->nr + 2 * s->rh);
+      L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
+      L1B_CUDA(cudaMemsetAsync(s->R[q], 0, (s->nr + 2 * s->rh) * 8, st));
     }
-    s->x = s->X[0];
-    s->y = s->X[0];
-    s->r_x = s->R[0];
-    s->r_y = s->R[2];
+    s->x = s->X[0] + s->xh;
+    s->y = s->x;
+    s->r_x = s->R[0] + s->rh;
+    s->r_y = s->R[2] + s->rh;
   } else if (s->shard) {
     // windows: [halo | own | halo]; K1 writes own x, K2 gathers the x window,
     // K2 writes own r_y, K1 gathers the r_y window
@@ -212,7 +222,7 @@ void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
   for (uint64_t i = 0; i < iters; ++i) {
     if (s->single) {
-      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), s->v.stream);
+      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), 0, s->v.n, s->v.stream);
     } else if (s->fused) {
       fista_fused_k1(*s->v.op, b, s->v.stream);
       fista_fused_k2(*s->v.op, b, s->v.stream);
@@ -239,7 +249,7 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   if (kept)
     L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
                              cudaMemcpyDeviceToHost, st));
-  const double* xf = s->single ? s->X[h.k % 3] : s->x;  // x after the last executed iteration
+  const double* xf = s->single ? s->X[h.k % 3] + s->xh : s->x;  // x after the last executed iteration
   if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, xf, s->nx * 8, cudaMemcpyDeviceToHost, st));
   if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, xf, s->nx * 8, cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaStreamSynchronize(st));
@@ -329,6 +339,13 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->scal = &s->st->scal[0];
     out->own = s->nx;
     out->halo = s->halo;
+    out->single = s->single ? 1 : 0;
+    for (int q = 0; q < 3; ++q) {
+      out->x_bufs[q] = s->X[q];
+      out->r_bufs[q] = s->R[q];
+    }
+    out->x_halo = s->xh;
+    out->r_halo = s->rh;
   });
 }
 
@@ -336,10 +353,15 @@ int l1b_session_k1(l1b_session* s) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
-    if (s->fused)
+    if (s->single) {  // the whole iteration; k2 is then a no-op
+      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched), s->v.row_begin, s->v.row_end,
+                       s->v.stream);
+      s->launched += 1;
+    } else if (s->fused) {
       fista_fused_k1(*s->v.op, s->bufs(), s->v.stream);
-    else
+    } else {
       fista_k1(s->v.At, s->bufs(), s->v.stream);
+    }
   });
 }
 
@@ -347,6 +369,7 @@ int l1b_session_k2(l1b_session* s) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
+    if (s->single) return;
     if (s->fused)
       fista_fused_k2(*s->v.op, s->bufs(), s->v.stream);
     else
@@ -385,7 +408,7 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     for (uint64_t i = 0; i < iters; ++i) {
       L1B_CUDA(cudaEventRecord(ev[3 * i], st));
       if (s->single)
-        fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), st);
+        fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), 0, s->v.n, st);
       else if (s->fused)
         fista_fused_k1(*s->v.op, b, st);
       else

@@ -2,13 +2,20 @@
 
 Every config's operator is banded (identity P1/P2, no left stages:
 |col - row| <= h = #stages), so rank g owns rows [a_g, b_g) of A *and* the
-same range of columns.  Per iteration (solvers.cpp:311-377):
+same range of columns.  Per iteration (solvers.cpp:311-377), single-kernel
+mode (matrix-free, the default):
+
+    one kernel: x_{k+1}, r_{k+1} from x_k, x_{k-1}, r_k, r_{k-1}  (own block)
+    exchange the halos of x_{k+1} (H entries) and r_{k+1} (2H entries)
+    all-reduce 4 scalars (||x||_1, nnz, #(trial != y), ||r||^2) -> finalise
+
+and in two-kernel mode (CSR/CSC, or matrix-free with > 4 stages):
 
     exchange r_y halo  ->  K1: x, y <- prox/momentum(A^T r_y)   (own columns)
     exchange x halo    ->  K2: r_x, r_y <- A x - b, momentum    (own rows)
-    all-reduce 4 scalars (||x||_1, nnz, #(trial != y), ||r||^2) -> finalise
+    all-reduce 4 scalars -> finalise
 
-The halo exchanges move h = 4 doubles to each neighbour: they are the
+The halo exchanges move a few doubles to each neighbour: they are the
 "all-reduce of the partial A^T r" of the north star carried out in its exact
 sparse form -- the partial A^T r of rank g is nonzero only on columns
 [a_g - h, b_g + h), so only the boundary rows of r travel.  Collectives are
@@ -58,19 +65,28 @@ def device_view(ptr: int, n: int, device):
 def halo_exchange(win, own: int, h: int, rank: int, world: int, group=None):
     """win = [left halo | own | right halo]; send the own boundary entries to
     the neighbours and receive theirs into the halo slots."""
+    halo_exchange_many([(win, h)], own, rank, world, group)
+
+
+def halo_exchange_many(wins, own: int, rank: int, world: int, group=None):
+    """Several [halo | own | halo] windows (window, halo width) in one batch."""
     import torch.distributed as dist
 
-    if world == 1 or h == 0:
+    if world == 1:
         return
     ops = []
-    if rank > 0:
-        ops.append(dist.P2POp(dist.isend, win[h:2 * h], rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, win[0:h], rank - 1, group))
-    if rank < world - 1:
-        ops.append(dist.P2POp(dist.isend, win[own:own + h], rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, win[own + h:own + 2 * h], rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+    for win, h in wins:
+        if h == 0:
+            continue
+        if rank > 0:
+            ops.append(dist.P2POp(dist.isend, win[h:2 * h], rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, win[0:h], rank - 1, group))
+        if rank < world - 1:
+            ops.append(dist.P2POp(dist.isend, win[own:own + h], rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, win[own + h:own + 2 * h], rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
 
 
 class CudaShard:
@@ -104,13 +120,30 @@ class CudaShard:
         N.check(lib.l1b_session_buffers(self.sess._s, C.byref(b)))
         self.own, self.halo = int(b.own), int(b.halo)
         dev = torch.device("cuda", device)
-        self.x_win = device_view(b.x_win, self.own + 2 * self.halo, dev)
-        self.r_y_win = device_view(b.r_y_win, self.own + 2 * self.halo, dev)
+        self.single = bool(b.single)
+        self.j = 0  # iterations launched (single mode: buffer rotation)
+        if self.single:
+            self.x_halo, self.r_halo = int(b.x_halo), int(b.r_halo)
+            self.x_bufs = [device_view(b.x_bufs[q], self.own + 2 * self.x_halo, dev) for q in range(3)]
+            self.r_bufs = [device_view(b.r_bufs[q], self.own + 2 * self.r_halo, dev) for q in range(3)]
+        else:
+            self.x_win = device_view(b.x_win, self.own + 2 * self.halo, dev)
+            self.r_y_win = device_view(b.r_y_win, self.own + 2 * self.halo, dev)
         self.scal = device_view(b.scal, 4, dev)
         self._lib = lib
 
+    # single-kernel mode: windows to exchange after iteration j / before the first
+    def next_halos(self):
+        q = self.j % 3
+        return [(self.x_bufs[q], self.x_halo), (self.r_bufs[q], self.r_halo)]
+
+    def initial_halos(self):
+        return [(self.r_bufs[0], self.r_halo), (self.r_bufs[2], self.r_halo)]
+
     def k1(self):
         N.check(self._lib.l1b_session_k1(self.sess._s))
+        if self.single:
+            self.j += 1
 
     def k2(self):
         N.check(self._lib.l1b_session_k2(self.sess._s))
@@ -133,10 +166,7 @@ def fista_distributed(be, iterations: int, group=None, poll_every: int = 0):
     budget).  Returns the backend's (trace, own x)."""
     import torch.distributed as dist
 
-    rank, world = be.rank, be.world
-    dist.all_reduce(be.scal, group=group)  # ||b_own||^2 -> f_0
-    be.finalize()
-    halo_exchange(be.r_y_win, be.own, be.halo, rank, world, group)
+    start(be, group)
     for it in range(iterations):
         fista_iteration(be, group)
         if poll_every and (it + 1) % poll_every == 0 and be.stopped()[0]:
@@ -144,9 +174,27 @@ def fista_distributed(be, iterations: int, group=None, poll_every: int = 0):
     return be.finish()
 
 
+def start(be, group=None):
+    """f_0 from the all-reduced ||b_own||^2, then the initial halos."""
+    import torch.distributed as dist
+
+    dist.all_reduce(be.scal, group=group)
+    be.finalize()
+    if be.single:
+        halo_exchange_many(be.initial_halos(), be.own, be.rank, be.world, group)
+    else:
+        halo_exchange(be.r_y_win, be.own, be.halo, be.rank, be.world, group)
+
+
 def fista_iteration(be, group=None):
     import torch.distributed as dist
 
+    if be.single:
+        be.k1()  # the whole iteration
+        halo_exchange_many(be.next_halos(), be.own, be.rank, be.world, group)
+        dist.all_reduce(be.scal, group=group)
+        be.finalize()
+        return
     be.k1()
     halo_exchange(be.x_win, be.own, be.halo, be.rank, be.world, group)
     be.k2()
@@ -175,9 +223,7 @@ def bench_main(args, world: int, rank: int, local: int):
     cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + 10)
     be = CudaShard(kw, rank, world, local, cfg)
     gen_s = time.perf_counter() - t0
-    dist.all_reduce(be.scal)
-    be.finalize()
-    halo_exchange(be.r_y_win, be.own, be.halo, rank, world)
+    start(be)
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             fista_iteration(be)

@@ -12,7 +12,7 @@ from paper_1503_03520_b200.distributed import partition
 
 class CpuShard:
     def __init__(self, oracle, inst, rank, world, max_iters):
-        self.rank, self.world = rank, world
+        self.rank, self.world, self.single = rank, world, False
         n = inst.n
         h = (len(inst.op.right_offset) + 1) & ~1  # window overhang: #stages rounded up to even
         a, b = partition(n, world)[rank]
@@ -103,3 +103,110 @@ class CpuShard:
 
     def finish(self):
         return self.samples, self.x_win.numpy()[self.halo:self.halo + self.own].copy()
+
+
+class CpuShardSingle:
+    """Single-kernel mode stand-in (k_fused.cu fista_iter_kernel): x / r rotate
+    through three halo windows; y and r_y are formed from the last two
+    iterates; after each iteration the caller exchanges the halos of the new
+    x (H) and r (2H) windows."""
+
+    def __init__(self, oracle, inst, rank, world, max_iters):
+        self.rank, self.world, self.single = rank, world, True
+        n = inst.n
+        H = (len(inst.op.right_offset) + 1) & ~1
+        a, b = partition(n, world)[rank]
+        self.n, self.a, self.b_, self.own = n, a, b, b - a
+        self.x_halo, self.r_halo = H, 2 * H
+        rp, ri, rv = oracle.csr(inst.op)
+        cp, ci, cv = oracle.csc(inst.op)
+        # columns of the x window [a - H, b + H) with rows local to the r window [a - 2H, ...)
+        self.cols = {}
+        for j in range(max(0, a - H), min(n, b + H)):
+            self.cols[j] = (ci[cp[j]:cp[j + 1]].astype(np.int64) - (a - 2 * H), cv[cp[j]:cp[j + 1]])
+        self.rows = [(ri[rp[i]:rp[i + 1]].astype(np.int64) - (a - H), rv[rp[i]:rp[i + 1]]) for i in range(a, b)]
+        self.x_bufs = [torch.zeros(self.own + 2 * H, dtype=torch.float64) for _ in range(3)]
+        self.r_bufs = [torch.zeros(self.own + 4 * H, dtype=torch.float64) for _ in range(3)]
+        self.b = inst.b[a:b].copy()
+        r0 = 0.0 - self.b
+        for q in (0, 2):
+            self.r_bufs[q][2 * H:2 * H + self.own] = torch.from_numpy(r0.copy())
+        self.scal = torch.zeros(4, dtype=torch.float64)
+        self.scal[3] = float(np.sum(r0 * r0))
+        self.tau, self.L = inst.tau, oracle.gram_lmax(inst.op)
+        self.t, self.beta_y, self.k, self.j = 1.0, 0.0, 0, 0
+        self.stop, self.init = False, False
+        self.max_iters = max_iters
+        self.samples = []
+
+    def next_halos(self):
+        q = self.j % 3
+        return [(self.x_bufs[q], self.x_halo), (self.r_bufs[q], self.r_halo)]
+
+    def initial_halos(self):
+        return [(self.r_bufs[0], self.r_halo), (self.r_bufs[2], self.r_halo)]
+
+    def k1(self):
+        j, self.j = self.j, self.j + 1
+        if self.stop:
+            return
+        H, a, n, beta = self.x_halo, self.a, self.n, self.beta_y
+        xk, xkm1 = self.x_bufs[j % 3].numpy(), self.x_bufs[(j + 2) % 3].numpy()
+        rk, rkm1 = self.r_bufs[j % 3].numpy(), self.r_bufs[(j + 2) % 3].numpy()
+        xn, rn = self.x_bufs[(j + 1) % 3].numpy(), self.r_bufs[(j + 1) % 3].numpy()
+        ry = (1.0 + beta) * rk - beta * rkm1
+        inv_l = 1.0 / self.L
+        thr = self.tau * inv_l
+        trial = np.zeros(self.own + 2 * H)
+        l1 = nnz = mism = 0.0
+        for jj, (idx, val) in self.cols.items():
+            g = 0.0
+            for q in range(len(idx)):
+                g += val[q] * ry[idx[q]]
+            lx = jj - (a - H)
+            y = xk[lx] + beta * (xk[lx] - xkm1[lx])
+            v = y - inv_l * g
+            tr = v - thr if v > thr else (v + thr if v < -thr else 0.0)
+            trial[lx] = tr
+            if a <= jj < self.b_:
+                xn[lx] = tr
+                l1 += abs(tr)
+                nnz += tr != 0.0
+                mism += tr != y
+        rr = 0.0
+        for i, (idx, val) in enumerate(self.rows):
+            s = 0.0
+            for q in range(len(idx)):
+                s += val[q] * trial[idx[q]]
+            rt = s - self.b[i]
+            rn[2 * H + i] = rt
+            rr += rt * rt
+        self.scal[0], self.scal[1], self.scal[2], self.scal[3] = l1, nnz, mism, rr
+
+    def k2(self):
+        pass
+
+    def finalize(self):
+        if self.stop:
+            return
+        sc = self.scal.numpy()
+        if not self.init:
+            self.init = True
+            self.samples.append((0, 0.5 * sc[3]))
+            self.stop = self.max_iters == 0
+            return
+        f = self.tau * sc[0] + 0.5 * sc[3]
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * self.t * self.t))
+        self.beta_y = (self.t - 1.0) / t_next
+        self.t = t_next
+        self.k += 1
+        self.samples.append((self.k, f))
+        if sc[2] == 0.0 or self.k >= self.max_iters:
+            self.stop = True
+
+    def stopped(self):
+        return self.stop, self.k
+
+    def finish(self):
+        q = self.k % 3
+        return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()

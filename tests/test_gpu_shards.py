@@ -33,6 +33,19 @@ def _exchange(shards, name):
             win[own + h:own + 2 * h].copy_(getattr(right, name)[h:2 * h])
 
 
+def _exchange_many(shards, getter):
+    lists = [getter(s) for s in shards]
+    for g, s in enumerate(shards):
+        for w, (win, h) in enumerate(lists[g]):
+            own = s.own
+            if g > 0:
+                lwin, _ = lists[g - 1][w]
+                win[0:h].copy_(lwin[shards[g - 1].own:shards[g - 1].own + h])
+            if g < len(shards) - 1:
+                rwin, _ = lists[g + 1][w]
+                win[own + h:own + 2 * h].copy_(rwin[h:2 * h])
+
+
 def _allreduce(shards):
     tot = sum(s.scal.clone() for s in shards)
     for s in shards:
@@ -56,8 +69,21 @@ def test_shards_reproduce_single_device_fista(world, op):
     _allreduce(shards)
     for s in shards:
         s.finalize()
-    _exchange(shards, "r_y_win")
+    single = shards[0].single
+    assert single == (op == "matrix_free")
+    if single:
+        _exchange_many(shards, lambda s: s.initial_halos())
+    else:
+        _exchange(shards, "r_y_win")
     for _ in range(iters):
+        if single:  # one kernel per iteration, then the halos of x_{k+1} / r_{k+1}
+            for s in shards:
+                s.k1()
+            _exchange_many(shards, lambda s: s.next_halos())
+            _allreduce(shards)
+            for s in shards:
+                s.finalize()
+            continue
         for s in shards:
             s.k1()
         _exchange(shards, "x_win")
