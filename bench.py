@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--n", type=int, default=C4["n"], help="columns per GPU (default C4: 2^27)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the row-sharded NCCL driver even with one rank (plumbing check)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -223,7 +225,7 @@ def main():
 
     import torch
 
-    if world > 1:
+    if world > 1 or args.force_dist:
         from paper_1503_03520_b200 import distributed
 
         return distributed.bench_main(args, world, rank, local)

@@ -170,6 +170,7 @@ struct l1b_problem {
   size_t device_bytes = 0;
   uint64_t row_begin = 0, row_end = 0;
   int world = 1, rank = 0;
+  bool sharded = false;  // a row-block shard (l1b_generate with a shard descriptor)
   uint64_t halo = 0;
   uint64_t sig_begin = 0;  // shards: d_sigma holds sigma[sig_begin, ...)
 
@@ -295,7 +296,7 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
 void materialise(l1b_problem* p) {
   if (p->sparse_built) return;
   p->sparse_built = true;
-  if (p->world > 1) {  // row-block shard: rows / columns [a, b), window-local indices
+  if (p->sharded) {  // row-block shard: rows / columns [a, b), window-local indices
     const uint64_t a = p->row_begin, own = p->row_end - p->row_begin;
     build_lines(p->view, true, a, own, a - p->halo, false, p->stream, &p->csr);
     p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
@@ -339,7 +340,7 @@ void check_problem(const l1b_problem* p) {
 
 void check_whole(const l1b_problem* p) {
   check_problem(p);
-  if (p->world > 1) throw Unsupported("operation needs the whole operator, not a row-block shard");
+  if (p->sharded) throw Unsupported("operation needs the whole operator, not a row-block shard");
 }
 
 }  // namespace
@@ -458,6 +459,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   p->cert_kappa = (smax / smin) * (smax / smin);
   p->tau = g->tau;
   p->world = sh->world;
+  p->sharded = true;
   p->rank = sh->rank;
   p->row_begin = a;
   p->row_end = b;
@@ -523,7 +525,7 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
   return guard([&] {
     if (!g || !out) throw InvalidArgument("null argument");
     *out = nullptr;
-    if (shard && shard->world > 1) {
+    if (shard) {  // row-block shard (world >= 1)
       generate_shard(device, g, shard, out);
       return;
     }
@@ -676,7 +678,7 @@ int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
     o->world = p->world;
     o->rank = p->rank;
     o->halo = p->halo;
-    if (p->world > 1) {
+    if (p->sharded) {
       o->m_active = p->row_end - p->row_begin;
       o->col_begin = p->row_begin;
       o->col_end = p->row_end;
@@ -687,7 +689,7 @@ int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
 int l1b_problem_get_b(const l1b_problem* p, double* b) {
   return guard([&] {
     check_problem(p);
-    const uint64_t rows = p->world > 1 ? p->row_end - p->row_begin : p->m;  // shards: own rows
+    const uint64_t rows = p->sharded ? p->row_end - p->row_begin : p->m;  // shards: own rows
     L1B_CUDA(cudaMemcpyAsync(b, p->d_b, rows * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
   });
@@ -904,6 +906,7 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   v.gram = nullptr;
   v.max_row_nnz = p->csr.max_len;
   v.world = p->world;
+  v.shard = p->sharded;
   v.rank = p->rank;
   v.row_begin = p->row_begin;
   v.row_end = p->row_end;

@@ -139,7 +139,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->accel = cfg->solver == L1B_FISTA;
   const ProblemView& v = s->v;
   cudaStream_t st = v.stream;
-  s->shard = v.world > 1;
+  s->shard = v.shard;
   s->single = s->fused && fused_iter_supported(*v.op);
   if (s->single) {
     // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows
@@ -467,7 +467,7 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     if (!p || !summary) throw InvalidArgument("null argument");
     ProblemView v = problem_view(p);
     validate_cfg(cfg, v.n);
-    if (v.world > 1)
+    if (v.shard)
       throw Unsupported("a row-block shard is solved by the distributed driver (l1b_session_k1/k2/finalize)");
     L1B_CUDA(cudaSetDevice(v.device));
     if (cfg->solver == L1B_PCDM || cfg->solver == L1B_CD) {

@@ -24,6 +24,7 @@ struct ProblemView {
   // row-block shard (world > 1): own rows == own columns [row_begin, row_end);
   // A / At index x / r windows that start `halo` entries before row_begin
   int world = 1, rank = 0;
+  bool shard = false;
   uint64_t row_begin = 0, row_end = 0, halo = 0;
 };
 

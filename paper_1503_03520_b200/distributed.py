@@ -214,6 +214,10 @@ def bench_main(args, world: int, rank: int, local: int):
     from . import l1bench
 
     torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from bench import C4, METRIC, UNIT, ClockSampler, peaks  # noqa: E402
 
