@@ -259,8 +259,11 @@ def bench_main(args, world: int, rank: int, local: int):
             "config": {"workload": f"C4 FISTA n=2^{int(math.log2(info.n))} row-sharded over {world} GPUs "
                                    f"({be.own} rows/columns per GPU, halo {be.halo})",
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "parallelism": f"row-block shards x{world}: NCCL P2P halo (2 x {be.halo} doubles "
-                                      f"per neighbour per iteration) + 4-double all-reduce"},
+                       "parallelism": (f"row-block shards x{world}: one matrix-free kernel per iteration, "
+                                       f"NCCL P2P halo of x ({be.x_halo}) and r ({be.r_halo}) doubles per "
+                                       f"neighbour + 4-double all-reduce" if be.single else
+                                       f"row-block shards x{world}: NCCL P2P halo (2 x {be.halo} doubles "
+                                       f"per neighbour per iteration) + 4-double all-reduce")},
             "gpu_launches": int(launches), "iterations_done": int(k), "generate_s": gen_s,
             "clocks": clk.summary(),
         }
