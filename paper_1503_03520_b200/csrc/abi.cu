@@ -248,9 +248,6 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
     if (o != 0 && o != 1) throw InvalidArgument("RotationStage: offset must be 0 or 1");
   for (int32_t o : l_off)
     if (o != 0 && o != 1) throw InvalidArgument("RotationStage: offset must be 0 or 1");
-  for (uint64_t i = 0; i < n; ++i)
-    if (!(sigma[i] > 0.0) || !std::isfinite(sigma[i]))
-      throw std::runtime_error("Spectrum: all singular values must be strictly positive");
   p->device = device;
   L1B_CUDA(cudaSetDevice(device));
   L1B_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
@@ -281,11 +278,11 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
   p->view.p2 = p->d_p2;
   p->view.p1_inv = p->d_p1inv;
   p->view.p2_inv = p->d_p2inv;
-  double smax = sigma[0], smin = sigma[0];
-  for (uint64_t i = 1; i < n; ++i) {
-    smax = std::max(smax, sigma[i]);
-    smin = std::min(smin, sigma[i]);
-  }
+  // Spectrum::validate (linops.cpp:359-365) and sigma_max / sigma_min, on device
+  double smin = 0.0, smax = 0.0;
+  bool ok = false;
+  device_min_finite(p->d_sigma, n, &smin, &smax, &ok, st);
+  if (!ok) throw std::runtime_error("Spectrum: all singular values must be strictly positive");
   p->lmax = smax * smax;                                     // gram_lmax (linops.cpp:560-564)
   p->cert_kappa = (smax / smin) * (smax / smin);             // solution.cpp:127-133
   L1B_CUDA(cudaStreamSynchronize(st));
@@ -321,16 +318,10 @@ void materialise(l1b_problem* p) {
   }
 }
 
-// sum of b_i^2 over rows >= n (empty rows of a banded operator)
+// sum of b_i^2 over rows >= n (empty rows of a banded operator), on device
 void band_tail(l1b_problem* p) {
   p->tail_sq_band = 0.0;
-  if (p->m > p->n) {
-    std::vector<double> tail(p->m - p->n);
-    L1B_CUDA(cudaMemcpyAsync(tail.data(), p->d_b + p->n, tail.size() * sizeof(double),
-                             cudaMemcpyDeviceToHost, p->stream));
-    L1B_CUDA(cudaStreamSynchronize(p->stream));
-    for (double v : tail) p->tail_sq_band += v * v;
-  }
+  if (p->m > p->n) p->tail_sq_band = device_sum_sq(p->d_b + p->n, p->m - p->n, p->stream);
 }
 
 void check_problem(const l1b_problem* p) {

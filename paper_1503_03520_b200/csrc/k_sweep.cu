@@ -5,6 +5,8 @@
 // One thread per rotation pair; a stage is one launch (used by the generator
 // and the PATH_SWEEP products; the fused multi-stage kernel is the next step,
 // SURVEY.md 8(f)-1).
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -260,6 +262,74 @@ void window_scale_op(double* v, const double* sig, uint64_t len, int mode, doubl
   if (!len) return;
   window_scale<<<grid_for(len), kThreads, 0, st>>>(v, sig, len, mode, tau);
   L1B_LAUNCHED();
+}
+
+namespace {
+__global__ void sum_sq_kernel(const double* __restrict__ v, uint64_t n, double* partials,
+                              unsigned int* ticket, double* out) {
+  double acc[1] = {0.0};
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc[0] += v[i] * v[i];
+  double tot[1];
+  if (grid_sum<1>(acc, partials, ticket, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+__global__ void minmax_kernel(const double* __restrict__ v, uint64_t n, unsigned long long* out) {
+  // out[0] = min over bits of positive doubles, out[1] = max, out[2] = #(non-finite or <= 0)
+  unsigned long long mn = ~0ull, mx = 0ull, bad = 0ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double x = v[i];
+    if (!(x > 0.0) || !isfinite(x)) {
+      ++bad;
+      continue;
+    }
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    mn = b < mn ? b : mn;
+    mx = b > mx ? b : mx;
+  }
+  atomicMin(&out[0], mn);
+  atomicMax(&out[1], mx);
+  if (bad) atomicAdd(&out[2], bad);
+}
+}  // namespace
+
+double device_sum_sq(const double* v, uint64_t n, cudaStream_t st) {
+  const int grid = grid_for(n);
+  double* scratch = nullptr;
+  unsigned int* ticket = nullptr;
+  L1B_CUDA(cudaMallocAsync(&scratch, (grid + 1) * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  L1B_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  sum_sq_kernel<<<grid, kThreads, 0, st>>>(v, n, scratch + 1, ticket, scratch);
+  L1B_LAUNCHED();
+  double h = 0.0;
+  L1B_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaFreeAsync(scratch, st));
+  L1B_CUDA(cudaFreeAsync(ticket, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+void device_min_finite(const double* v, uint64_t n, double* vmin, double* vmax, bool* finite,
+                       cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  L1B_CUDA(cudaMallocAsync(&d, 3 * sizeof(unsigned long long), st));
+  const unsigned long long init[3] = {~0ull, 0ull, 0ull};
+  L1B_CUDA(cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  minmax_kernel<<<grid_for(n), kThreads, 0, st>>>(v, n, d);
+  L1B_LAUNCHED();
+  unsigned long long h[3];
+  L1B_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaFreeAsync(d, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  *finite = h[2] == 0;
+  double a, b;
+  std::memcpy(&a, &h[0], 8);
+  std::memcpy(&b, &h[1], 8);
+  *vmin = a;
+  *vmax = b;
 }
 
 }  // namespace l1b

@@ -36,6 +36,10 @@ void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* 
 void generator_combine(double tau, double* e, double* b, uint64_t m, double* d_sum_sq,
                        cudaStream_t st);
 void vec_sub(double* a, const double* b, uint64_t n, cudaStream_t st);  // a -= b
+double device_sum_sq(const double* v, uint64_t n, cudaStream_t st);      // sum v_i^2 (syncs)
+// min over i of sigma_i and a flag for any non-finite entry (syncs)
+void device_min_finite(const double* v, uint64_t n, double* vmin, double* vmax, bool* finite,
+                       cudaStream_t st);
 // max_S |r_i + tau sign(x_i)|, max_{S^c} (|r_i| - tau)_+  (instance.cpp:187-198)
 void certificate(const double* r, const double* xd, double tau, uint64_t n, double* d_out2,
                  cudaStream_t st);

@@ -315,7 +315,7 @@ int l1b_session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session** o
   return guard([&] {
     if (!p || !out) throw InvalidArgument("null argument");
     *out = nullptr;
-    ProblemView v = problem_view(p);
+    ProblemView v = problem_view(p, false);
     validate_cfg(cfg, v.n);
     if (cfg->solver != L1B_FISTA && cfg->solver != L1B_ISTA)
       throw InvalidArgument("sessions drive FISTA / ISTA only");
@@ -465,7 +465,7 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
               l1b_summary* summary, double* x_host, double* d_x) {
   return guard([&] {
     if (!p || !summary) throw InvalidArgument("null argument");
-    ProblemView v = problem_view(p);
+    ProblemView v = problem_view(p, false);
     validate_cfg(cfg, v.n);
     if (v.shard)
       throw Unsupported("a row-block shard is solved by the distributed driver (l1b_session_k1/k2/finalize)");
