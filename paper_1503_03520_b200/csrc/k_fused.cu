@@ -381,22 +381,46 @@ struct IterArgs {
 // the reference's full-vector sweeps.  No barrier between stages.  The pair
 // parity of a stage is warp-uniform (P is a multiple of NO for every thread),
 // so away from the global ends the pairs are a fixed unrolled set.
-template <int S, int NO>
-__device__ __forceinline__ void chain(const double* win, int64_t g0, int64_t n,
-                                      const StageTab& tab, bool transposed, double (&out)[NO]) {
+// window loader: plain copy of one smem window
+struct LoadPlain {
+  const double* w;
+  __device__ __forceinline__ double operator()(int q) const { return w[q]; }
+  __device__ __forceinline__ double2 pair(int q) const {
+    return reinterpret_cast<const double2*>(w)[q];
+  }
+};
+// u = sigma .* ((1 + beta) r_k - beta r_{k-1}), formed while loading (solvers.cpp:356, linops.cpp:460)
+struct LoadRy {
+  const double* rk;
+  const double* rkm1;
+  const double* sig;
+  double beta;
+  __device__ __forceinline__ double operator()(int q) const {
+    return sig[q] * ((1.0 + beta) * rk[q] - beta * rkm1[q]);
+  }
+  __device__ __forceinline__ double2 pair(int q) const {
+    const double2 a = reinterpret_cast<const double2*>(rk)[q];
+    const double2 b = reinterpret_cast<const double2*>(rkm1)[q];
+    const double2 s = reinterpret_cast<const double2*>(sig)[q];
+    return make_double2(s.x * ((1.0 + beta) * a.x - beta * b.x), s.y * ((1.0 + beta) * a.y - beta * b.y));
+  }
+};
+
+template <int S, int NO, class Load>
+__device__ __forceinline__ void chain(const Load& ld, int64_t g0, int64_t n, const StageTab& tab,
+                                      bool transposed, double (&out)[NO]) {
   constexpr int W = 2 * S + NO;
   double v[W];
   if ((S & 1) == 0) {  // window starts on an even smem index: 16-byte loads
-    const double2* w2 = reinterpret_cast<const double2*>(win);
 #pragma unroll
     for (int q = 0; q < W / 2; ++q) {
-      const double2 d = w2[q];
+      const double2 d = ld.pair(q);
       v[2 * q] = d.x;
       v[2 * q + 1] = d.y;
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < W; ++q) v[q] = win[q];
+    for (int q = 0; q < W; ++q) v[q] = ld(q);
   }
   const bool interior = g0 >= 1 && g0 + W <= n;  // every pair start p >= 1 >= offset, p+1 < n
 #pragma unroll
@@ -500,27 +524,20 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
     double* s_tr = reinterpret_cast<double*>(slot + L::off_xkm1);  // x_{k-1} -> trial
     const double* s_b = reinterpret_cast<const double*>(slot + L::off_b);
     mbar_wait(&bars[k % kIStages], (uint32_t)((k / kIStages) & 1));
-    const int rlen = (int)(te - t0 + 4 * H), xlen = (int)(te - t0 + 2 * H);
-    // 1. u = sigma .* r_y, r_y = (1 + beta) r_k - beta r_{k-1}; y = x_k + beta (x_k - x_{k-1})
-    for (int q = t; q < rlen; q += kThreads) {
-      const double ry = (1.0 + beta) * s_r[q] - beta * s_rm[q];
-      s_r[q] = s_sig[q] * ry;
-    }
-    for (int q = t; q < xlen; q += kThreads) {
-      const double xk = s_x[q];
-      s_x[q] = xk + beta * (xk - s_tr[q]);
-    }
-    __syncthreads();
-    // 2. g = G u on the x window (two entries per thread, stages in registers),
-    //    trial = S(y - g/L, tau/L); own entries -> x_{k+1}
+    const int xlen = (int)(te - t0 + 2 * H);
+    // 1. g = G u on the x window, u = sigma .* r_y formed while loading the
+    //    chain windows (kNO entries per thread, all stages in registers);
+    //    y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1}
     for (int q = kNO * t; q < xlen; q += kNO * kThreads) {
-      double g[kNO];
-      chain<S, kNO>(s_r + (q + H - S), gx + q - S, n, A.right, false, g);
+      double g[kNO], trv[kNO];
+      const int w0 = q + H - S;
+      chain<S, kNO>(LoadRy{s_r + w0, s_rm + w0, s_sig + w0, beta}, gx + q - S, n, A.right, false, g);
 #pragma unroll
       for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
         if (qq >= xlen) break;
-        const double y = s_x[qq];
+        const double xk = s_x[qq];
+        const double y = xk + beta * (xk - s_tr[qq]);
         const double tr = soft_threshold(y - inv_l * g[e], thr);
         const int64_t j = gx + qq;
         if (j >= t0 && j < te) {
@@ -529,15 +546,20 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
           acc[1] += tr != 0.0 ? 1.0 : 0.0;
           acc[2] += tr != y ? 1.0 : 0.0;
         }
-        s_tr[qq] = (j >= 0 && j < n) ? tr : 0.0;
+        trv[e] = (j >= 0 && j < n) ? tr : 0.0;
       }
+      // x_{k-1} (read above for y) -> trial, after every thread has read its y
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < kNO; ++e)
+        if (q + e < xlen) s_tr[q + e] = trv[e];
     }
     __syncthreads();
     // 3. r_{k+1} = sigma .* (G^T trial) - b on the own rows
     const int own = (int)(te - t0);
     for (int q = kNO * t; q < own; q += kNO * kThreads) {
       double av[kNO];
-      chain<S, kNO>(s_tr + (q + H - S), t0 + q - S, n, A.right, true, av);
+      chain<S, kNO>(LoadPlain{s_tr + (q + H - S)}, t0 + q - S, n, A.right, true, av);
 #pragma unroll
       for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
