@@ -548,8 +548,7 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
         }
         trv[e] = (j >= 0 && j < n) ? tr : 0.0;
       }
-      // x_{k-1} (read above for y) -> trial, after every thread has read its y
-      __syncwarp();
+      // x_{k-1} (read above for y) -> trial: each thread rewrites only its own kNO entries
 #pragma unroll
       for (int e = 0; e < kNO; ++e)
         if (q + e < xlen) s_tr[q + e] = trv[e];
