@@ -15,6 +15,7 @@
 // differs.  HBM traffic per iteration: 48n + 48n bytes (K1: r_y, sigma, y, x
 // r/w; K2: x, sigma, b, r_x r/w, r_y w) versus 288n for the CSR/CSC path.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fista.cuh"
@@ -346,9 +347,8 @@ void fista_fused_k2(const OpView& op, const FistaBufs& fb, cudaStream_t st) {
 namespace {
 
 constexpr int kTI = 1024;     // tile entries
-constexpr int kIStages = 2;
-
-struct IterLayout {
+template <int kIStages>
+struct IterLayoutT {
   static constexpr size_t rwin = kTI + 4 * kHaloMax + 2;
   static constexpr size_t xwin = kTI + 2 * kHaloMax + 2;
   static constexpr size_t rwin_b = round16(rwin * 8);
@@ -451,11 +451,11 @@ __device__ __forceinline__ void chain(const Load& ld, int64_t g0, int64_t n, con
 
 constexpr int kNO = 4;  // outputs per thread and chain
 
-template <int S>
-__global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
+template <int S, int kIStages, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterArgs A) {
   FistaDev* st = A.b.st;
   if (*(volatile int*)&st->stop) return;
-  using L = IterLayout;
+  using L = IterLayoutT<kIStages>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
   const int t = threadIdx.x;
@@ -580,23 +580,44 @@ __global__ void __launch_bounds__(kThreads, 2) fista_iter_kernel(IterArgs A) {
   }
 }
 
-template <int S>
-void launch_iter(const IterArgs& a, cudaStream_t st) {
-  using L = IterLayout;
+template <int S, int ST, int MB>
+void launch_iter_v(const IterArgs& a, cudaStream_t st) {
+  using L = IterLayoutT<ST>;
   static int grid_cap = 0;
   if (!grid_cap) {
-    L1B_CUDA(cudaFuncSetAttribute(fista_iter_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L::total));
+    L1B_CUDA(cudaFuncSetAttribute(fista_iter_kernel<S, ST, MB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::total));
     int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_iter_kernel<S>, kThreads,
-                                                          L::total));
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_iter_kernel<S, ST, MB>,
+                                                          kThreads, L::total));
     grid_cap = std::max(1, per_sm) * sm_count();
   }
   constexpr uint64_t TT = kTI - 2 * ((S + 1) & ~1);
   const uint64_t tiles = (a.hi - a.lo + TT - 1) / TT;
   const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
-  fista_iter_kernel<S><<<grid, kThreads, L::total, st>>>(a);
+  fista_iter_kernel<S, ST, MB><<<grid, kThreads, L::total, st>>>(a);
   L1B_LAUNCHED();
+}
+
+// pipeline depth x min CTAs/SM; L1B_ITER_VARIANT overrides the default (tuning runs)
+int iter_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("L1B_ITER_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int S>
+void launch_iter(const IterArgs& a, cudaStream_t st) {
+  switch (iter_variant()) {
+    case 1: return launch_iter_v<S, 1, 4>(a, st);
+    case 2: return launch_iter_v<S, 1, 3>(a, st);
+    case 3: return launch_iter_v<S, 3, 1>(a, st);
+    case 4: return launch_iter_v<S, 1, 2>(a, st);
+    default: return launch_iter_v<S, 2, 2>(a, st);
+  }
 }
 
 }  // namespace
