@@ -406,9 +406,9 @@ struct LoadRy {
   }
 };
 
-template <int S, int NO, class Load>
+template <int S, int NO, bool TR, bool INTERIOR, class Load>
 __device__ __forceinline__ void chain(const Load& ld, int64_t g0, int64_t n, const StageTab& tab,
-                                      bool transposed, double (&out)[NO]) {
+                                      double (&out)[NO]) {
   constexpr int W = 2 * S + NO;
   double v[W];
   if ((S & 1) == 0) {  // window starts on an even smem index: 16-byte loads
@@ -422,26 +422,26 @@ __device__ __forceinline__ void chain(const Load& ld, int64_t g0, int64_t n, con
 #pragma unroll
     for (int q = 0; q < W; ++q) v[q] = ld(q);
   }
-  const bool interior = g0 >= 1 && g0 + W <= n;  // every pair start p >= 1 >= offset, p+1 < n
 #pragma unroll
   for (int k = 0; k < S; ++k) {
-    const int s = transposed ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
-    const int64_t o = tab.offset[s];
+    const int s = TR ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
+    const int o = tab.offset[s];
     const double c = tab.c[s], sn = tab.s[s];
-    const int par = (int)((g0 - o) & 1);
-    if (interior) {
+    // g0 has the parity of S (tiles start on even entries, chains on multiples of NO)
+    const int par = (S + o) & 1;
+    if (INTERIOR) {  // tile away from both ends: every pair start p >= 1 >= offset, p+1 < n
       if (par == 0) {
 #pragma unroll
-        for (int l = 0; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+        for (int l = 0; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, TR);
       } else {
 #pragma unroll
-        for (int l = 1; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+        for (int l = 1; l + 1 < W; l += 2) rotate_pair(v[l], v[l + 1], c, sn, TR);
       }
     } else {
 #pragma unroll
       for (int l = 0; l + 1 < W; ++l) {
         const int64_t p = g0 + l;
-        if ((l & 1) == par && p >= o && p + 1 < n) rotate_pair(v[l], v[l + 1], c, sn, transposed);
+        if ((l & 1) == par && p >= o && p + 1 < n) rotate_pair(v[l], v[l + 1], c, sn, TR);
       }
     }
   }
@@ -525,13 +525,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
     const double* s_b = reinterpret_cast<const double*>(slot + L::off_b);
     mbar_wait(&bars[k % kIStages], (uint32_t)((k / kIStages) & 1));
     const int xlen = (int)(te - t0 + 2 * H);
+    const bool interior = t0 - 2 * H >= 1 && te + 2 * H <= n;  // tile-uniform
     // 1. g = G u on the x window, u = sigma .* r_y formed while loading the
     //    chain windows (kNO entries per thread, all stages in registers);
     //    y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1}
     for (int q = kNO * t; q < xlen; q += kNO * kThreads) {
       double g[kNO], trv[kNO];
       const int w0 = q + H - S;
-      chain<S, kNO>(LoadRy{s_r + w0, s_rm + w0, s_sig + w0, beta}, gx + q - S, n, A.right, false, g);
+      const LoadRy ld{s_r + w0, s_rm + w0, s_sig + w0, beta};
+      if (interior)
+        chain<S, kNO, false, true>(ld, gx + q - S, n, A.right, g);
+      else
+        chain<S, kNO, false, false>(ld, gx + q - S, n, A.right, g);
 #pragma unroll
       for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
@@ -558,7 +563,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
     const int own = (int)(te - t0);
     for (int q = kNO * t; q < own; q += kNO * kThreads) {
       double av[kNO];
-      chain<S, kNO>(LoadPlain{s_tr + (q + H - S)}, t0 + q - S, n, A.right, true, av);
+      const LoadPlain ld{s_tr + (q + H - S)};
+      if (interior)
+        chain<S, kNO, true, true>(ld, t0 + q - S, n, A.right, av);
+      else
+        chain<S, kNO, true, false>(ld, t0 + q - S, n, A.right, av);
 #pragma unroll
       for (int e = 0; e < kNO; ++e) {
         const int qq = q + e;
