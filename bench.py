@@ -109,9 +109,10 @@ def kernel_bytes(path, n, m_act, nnz, ptr_bytes):
     return k1, k2
 
 
-def time_path(inst, op, args, prof_iters=30):
+def time_path(inst, op, args, prof_iters=400):
     """W warm-up iterations, then exactly K timed iterations (CUDA events on
-    the library's stream), then a separately profiled pass for per-kernel times."""
+    the library's stream), then a separately profiled pass for per-kernel times
+    (long enough for several nvidia-smi clock samples under load)."""
     import torch
 
     from paper_1503_03520_b200 import l1bench
@@ -244,7 +245,7 @@ def main():
     t0 = time.perf_counter()
     info = inst.info  # builds nothing; CSR/CSC come with the first sparse use below
     with ClockSampler(local) as clk_sparse:
-        sparse = time_path(inst, "sparse", args)
+        sparse = time_path(inst, "sparse", args, prof_iters=120)
     info = inst.materialize()  # refreshed: nnz of the CSR/CSC copy
     build_s = time.perf_counter() - t0
     rf = roofline("matrix_free", fused, info, peak, peak_src)
