@@ -14,6 +14,7 @@
 #include <memory>
 #include <random>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -533,25 +534,38 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
     for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
     for (uint32_t i = 0; i < g->left_stages; ++i)
       l_off.push_back((int32_t)((g->left_stages - 1 - i) % 2));
+    // The four seeded streams (P1, P2, sigma, the subgradient fill) are
+    // independent mt19937_64 sequences: realise them on four host threads.
     std::vector<uint32_t> p1, p2;
-    if (g->permute) {
-      if (m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
-      p1.resize(m);
-      p2.resize(m);
-      hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data());
-      hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data());
-    }
-    std::vector<double> sigma(n);
-    if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
-      hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
-                                hostrng::mix_seed(job_seed, 3), sigma.data());
-    } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
-      for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
-    } else if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT) {
-      if (!g->sigma_explicit) throw InvalidArgument("explicit spectrum without values");
-      std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
-    } else {
+    std::vector<double> sigma(n), gv(n);
+    if (g->permute && m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
+    if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && !g->sigma_explicit)
+      throw InvalidArgument("explicit spectrum without values");
+    if (g->spectrum_kind < L1B_SPECTRUM_UNIFORM_Q || g->spectrum_kind > L1B_SPECTRUM_EXPLICIT)
       throw InvalidArgument("unknown spectrum kind");
+    {
+      std::vector<std::thread> pool;
+      if (g->permute) {
+        p1.resize(m);
+        p2.resize(m);
+        pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
+        pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
+      }
+      pool.emplace_back([&] {
+        if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+          hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
+                                    hostrng::mix_seed(job_seed, 3), sigma.data());
+        } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+          for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+        } else {
+          std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+        }
+      });
+      pool.emplace_back([&] {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
+        hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+        for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
+      });
+      for (auto& th : pool) th.join();
     }
     auto p = std::make_unique<l1b_problem>();
     setup_operator(p.get(), device, m, n, r_off, std::vector<double>(g->stages, g->theta), l_off,
@@ -564,13 +578,8 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
       hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
       hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
     }
-    // subgradient g (instance.cpp:28-42), Rng(mix_seed(job.seed, 5))
-    std::vector<double> gv(n);
-    {
-      hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
-      for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
-      for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
-    }
+    // subgradient g: signs on the support (instance.cpp:36-40)
+    for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
     cudaStream_t st = p->stream;
     // device: w = G (S^T S)^-1 G^T g; e = tau A w; b = A x* + e (instance.cpp:64-79)
     double *d_g = nullptr, *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;

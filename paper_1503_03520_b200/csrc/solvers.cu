@@ -491,6 +491,13 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     uint64_t chunk = 4;
     try {
       while (s.launched < cfg->max_iters) {
+        // loop-head time check (solvers.cpp:314), at chunk granularity
+        const double el =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - s.t0).count();
+        if (el > cfg->max_seconds) {
+          s.time_out = true;
+          break;
+        }
         const uint64_t k = std::min<uint64_t>(chunk, cfg->max_iters - s.launched);
         session_step(&s, k);
         L1B_CUDA(cudaMemcpyAsync(&h_flags[slot], &s.st->stop, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -501,12 +508,6 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
           L1B_CUDA(cudaEventSynchronize(ev[slot]));
           pending[slot] = false;
           if (h_flags[slot]) break;
-        }
-        const double el =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - s.t0).count();
-        if (el > cfg->max_seconds) {
-          s.time_out = true;
-          break;
         }
         chunk = std::min<uint64_t>(chunk * 2, 64);
       }
