@@ -25,13 +25,17 @@ def test_tiny_instances_all_solvers(oracle, n, stages, m_ratio):
         np.testing.assert_array_equal(got, want)
     for got, want in zip(inst.op.csc(), oracle.csc(oi.op)):
         np.testing.assert_array_equal(got, want)
+    otr, ox = oracle.fista(oi, max_iters=60)
     for op in ("sparse", "matrix_free"):
         x = np.empty(n)
         tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=60, op=op), x)
-        otr, ox = oracle.fista(oi, max_iters=60)
-        assert rel_err(tr.objectives(), otr["objective"]) < 1e-10
+        f, fo = tr.objectives(), otr["objective"]
+        if op == "matrix_free":  # the reference's own products: same trajectory, same stop
+            np.testing.assert_array_equal(x, ox)
+            assert len(f) == len(fo) and tr.status == l1bench.StopReason(otr["status"])
+        k = min(len(f), len(fo))  # CSR/CSC rounding can move an exact fixed point by an iteration
+        assert rel_err(f[:k], fo[:k]) < 1e-10
         assert rel_err(x, ox) < 1e-10
-        assert tr.status == l1bench.StopReason(otr["status"])
     x = np.empty(n)
     tr = l1bench.coordinate_descent_run(inst, l1bench.SolverConfig(max_iters=5, varpi=2, seed=4), x)
     otr, ox = oracle.cd(oi, max_iters=5, varpi=2, seed=4)
