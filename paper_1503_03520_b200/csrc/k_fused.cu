@@ -389,23 +389,6 @@ struct LoadPlain {
     return reinterpret_cast<const double2*>(w)[q];
   }
 };
-// u = sigma .* ((1 + beta) r_k - beta r_{k-1}), formed while loading (solvers.cpp:356, linops.cpp:460)
-struct LoadRy {
-  const double* rk;
-  const double* rkm1;
-  const double* sig;
-  double beta;
-  __device__ __forceinline__ double operator()(int q) const {
-    return sig[q] * ((1.0 + beta) * rk[q] - beta * rkm1[q]);
-  }
-  __device__ __forceinline__ double2 pair(int q) const {
-    const double2 a = reinterpret_cast<const double2*>(rk)[q];
-    const double2 b = reinterpret_cast<const double2*>(rkm1)[q];
-    const double2 s = reinterpret_cast<const double2*>(sig)[q];
-    return make_double2(s.x * ((1.0 + beta) * a.x - beta * b.x), s.y * ((1.0 + beta) * a.y - beta * b.y));
-  }
-};
-
 template <int S, int NO, bool TR, bool INTERIOR, class Load>
 __device__ __forceinline__ void chain(const Load& ld, int64_t g0, int64_t n, const StageTab& tab,
                                       double (&out)[NO]) {
@@ -524,39 +507,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
     double* s_tr = reinterpret_cast<double*>(slot + L::off_xkm1);  // x_{k-1} -> trial
     const double* s_b = reinterpret_cast<const double*>(slot + L::off_b);
     mbar_wait(&bars[k % kIStages], (uint32_t)((k / kIStages) & 1));
-    const int xlen = (int)(te - t0 + 2 * H);
+    const int rlen = (int)(te - t0 + 4 * H), xlen = (int)(te - t0 + 2 * H);
     const bool interior = t0 - 2 * H >= 1 && te + 2 * H <= n;  // tile-uniform
-    // 1. g = G u on the x window, u = sigma .* r_y formed while loading the
-    //    chain windows (kNO entries per thread, all stages in registers);
-    //    y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1}
+    // Shared-memory traffic is the limiter here: per-element work runs with
+    // consecutive threads on consecutive entries (2 wavefronts per warp
+    // access); only the register chains read per-thread windows.
+    // 0. u = sigma .* r_y, r_y = (1 + beta) r_k - beta r_{k-1}   (in place of r_k)
+    for (int q = t; q < rlen; q += kThreads) s_r[q] = s_sig[q] * ((1.0 + beta) * s_r[q] - beta * s_rm[q]);
+    __syncthreads();
+    // 1. g = G u on the x window: kNO entries per thread, all stages in registers;
+    //    g parked in the (now free) r_{k-1} buffer at x-window positions
+    double* s_g = const_cast<double*>(s_rm);
     for (int q = kNO * t; q < xlen; q += kNO * kThreads) {
-      double g[kNO], trv[kNO];
-      const int w0 = q + H - S;
-      const LoadRy ld{s_r + w0, s_rm + w0, s_sig + w0, beta};
+      double g[kNO];
+      const LoadPlain ld{s_r + (q + H - S)};
       if (interior)
         chain<S, kNO, false, true>(ld, gx + q - S, n, A.right, g);
       else
         chain<S, kNO, false, false>(ld, gx + q - S, n, A.right, g);
-#pragma unroll
-      for (int e = 0; e < kNO; ++e) {
-        const int qq = q + e;
-        if (qq >= xlen) break;
-        const double xk = s_x[qq];
-        const double y = xk + beta * (xk - s_tr[qq]);
-        const double tr = soft_threshold(y - inv_l * g[e], thr);
-        const int64_t j = gx + qq;
-        if (j >= t0 && j < te) {
-          A.b.x_next[j] = tr;
-          acc[0] += fabs(tr);
-          acc[1] += tr != 0.0 ? 1.0 : 0.0;
-          acc[2] += tr != y ? 1.0 : 0.0;
-        }
-        trv[e] = (j >= 0 && j < n) ? tr : 0.0;
+      reinterpret_cast<double2*>(s_g + q)[0] = make_double2(g[0], g[1]);
+      reinterpret_cast<double2*>(s_g + q)[1] = make_double2(g[2], g[3]);
+    }
+    __syncthreads();
+    // 2. y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1}
+    for (int q = t; q < xlen; q += kThreads) {
+      const double xk = s_x[q];
+      const double y = xk + beta * (xk - s_tr[q]);
+      const double tr = soft_threshold(y - inv_l * s_g[q], thr);
+      const int64_t j = gx + q;
+      if (j >= t0 && j < te) {
+        A.b.x_next[j] = tr;
+        acc[0] += fabs(tr);
+        acc[1] += tr != 0.0 ? 1.0 : 0.0;
+        acc[2] += tr != y ? 1.0 : 0.0;
       }
-      // x_{k-1} (read above for y) -> trial: each thread rewrites only its own kNO entries
-#pragma unroll
-      for (int e = 0; e < kNO; ++e)
-        if (q + e < xlen) s_tr[q + e] = trv[e];
+      s_tr[q] = (j >= 0 && j < n) ? tr : 0.0;
     }
     __syncthreads();
     // 3. r_{k+1} = sigma .* (G^T trial) - b on the own rows
@@ -568,13 +553,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
         chain<S, kNO, true, true>(ld, t0 + q - S, n, A.right, av);
       else
         chain<S, kNO, true, false>(ld, t0 + q - S, n, A.right, av);
+      const double2 sg0 = reinterpret_cast<const double2*>(s_sig + 2 * H + q)[0];
+      const double2 sg1 = reinterpret_cast<const double2*>(s_sig + 2 * H + q)[1];
+      const double2 b0 = reinterpret_cast<const double2*>(s_b + q)[0];
+      const double2 b1 = reinterpret_cast<const double2*>(s_b + q)[1];
+      const double rt[kNO] = {sg0.x * av[0] - b0.x, sg0.y * av[1] - b0.y, sg1.x * av[2] - b1.x,
+                              sg1.y * av[3] - b1.y};
+      if (q + kNO <= own) {
+        double2* dst = reinterpret_cast<double2*>(A.b.r_next + t0 + q);
+        dst[0] = make_double2(rt[0], rt[1]);
+        dst[1] = make_double2(rt[2], rt[3]);
 #pragma unroll
-      for (int e = 0; e < kNO; ++e) {
-        const int qq = q + e;
-        if (qq >= own) break;
-        const double rt = s_sig[2 * H + qq] * av[e] - s_b[qq];
-        A.b.r_next[t0 + qq] = rt;
-        acc[3] += rt * rt;
+        for (int e = 0; e < kNO; ++e) acc[3] += rt[e] * rt[e];
+      } else {
+        for (int e = 0; e < own - q; ++e) {
+          A.b.r_next[t0 + q + e] = rt[e];
+          acc[3] += rt[e] * rt[e];
+        }
       }
     }
     __syncthreads();
