@@ -14,28 +14,21 @@ __device__ __forceinline__ void fista_momentum(const FistaDev* st, double* t_nex
   *beta = st->accel ? (t - 1.0) / *t_next : 0.0;
 }
 
-// Bookkeeping after iteration k (solvers.cpp:366-376 + the loop-head checks
-// :312-313): f, trace sample, fixed point / target / iteration budget.
-__device__ inline void fista_finalize_device(FistaDev* st, FistaSample* trace) {
-  const double f = st->tau * st->scal[0] + 0.5 * (st->scal[3] + st->tail_sq);
-  const uint64_t k = st->k + 1;
-  double t_next, beta;
-  fista_momentum(st, &t_next, &beta);
-  st->beta_y = beta;  // y = trial + beta (trial - x)  (solvers.cpp:349-352)
-  if (st->accel) st->t = t_next;
+// Iteration k's record and stop checks (solvers.cpp:366-376 + the loop-head
+// checks :312-313): f, trace sample, fixed point / target / iteration budget.
+__device__ inline void fista_record(FistaDev* st, FistaSample* trace, uint64_t k, double f,
+                                    double nnz, bool fixed, uint64_t ts) {
   st->k = k;
   st->f = f;
-  st->nnz = st->scal[1];
-  const uint64_t ts = global_timer_ns();
+  st->nnz = nnz;
   st->last_ts = ts;
-  const bool fixed = st->scal[2] == 0.0;
   if (!isfinite(f)) {
     st->stop = 1;
     st->status = -1;
     return;
   }
   if (k <= 1000 || k % 10 == 0 || fixed) {
-    if (st->n_samples < st->cap) trace[st->n_samples] = FistaSample{k, f, st->scal[1], ts};
+    if (st->n_samples < st->cap) trace[st->n_samples] = FistaSample{k, f, nnz, ts};
     st->n_samples++;
     st->last_sampled = k;
   }
@@ -49,6 +42,41 @@ __device__ inline void fista_finalize_device(FistaDev* st, FistaSample* trace) {
     st->stop = 1;
     st->status = 1;
   }
+}
+
+// Bookkeeping after iteration k (scal = l1, nnz, mismatches, ||r||^2 of x_k)
+__device__ inline void fista_finalize_device(FistaDev* st, FistaSample* trace) {
+  const double f = st->tau * st->scal[0] + 0.5 * (st->scal[3] + st->tail_sq);
+  double t_next, beta;
+  fista_momentum(st, &t_next, &beta);
+  st->beta_y = beta;  // y = trial + beta (trial - x)  (solvers.cpp:349-352)
+  if (st->accel) st->t = t_next;
+  fista_record(st, trace, st->k + 1, f, st->scal[1], st->scal[2] == 0.0, global_timer_ns());
+}
+
+// Lagged bookkeeping after kernel j of the recomputing path: scal = l1, nnz,
+// mismatches of x_{j+1} and ||r_j||^2.  Iteration j is recorded first (its l1 /
+// nnz / mismatches were stashed by kernel j-1), then -- unless that stopped
+// the loop, or this is the flush after the last kernel -- the momentum for
+// kernel j+1 (it depends on t only) and x_{j+1}'s sums are stashed.  Same
+// values and order of checks as fista_finalize_device, one kernel later.
+__device__ inline void fista_finalize_lagged(FistaDev* st, FistaSample* trace, bool flush) {
+  if (st->pend_valid) {
+    const double f = st->tau * st->pend[0] + 0.5 * (st->scal[3] + st->tail_sq);
+    st->pend_valid = 0;
+    fista_record(st, trace, st->k + 1, f, st->pend[1], st->pend[2] == 0.0, st->pend_ts);
+    if (st->stop) return;
+  }
+  if (flush) return;
+  double t_next, beta;
+  fista_momentum(st, &t_next, &beta);
+  st->beta_y = beta;
+  if (st->accel) st->t = t_next;
+  st->pend[0] = st->scal[0];
+  st->pend[1] = st->scal[1];
+  st->pend[2] = st->scal[2];
+  st->pend_ts = global_timer_ns();
+  st->pend_valid = 1;
 }
 
 }  // namespace l1b

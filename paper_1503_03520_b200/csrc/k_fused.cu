@@ -351,8 +351,9 @@ template <int kIStages>
 struct IterLayoutT {
   static constexpr size_t rwin = kTI + 4 * kHaloMax + 2;
   static constexpr size_t xwin = kTI + 2 * kHaloMax + 2;
-  static constexpr size_t rwin_b = round16(rwin * 8);
-  static constexpr size_t xwin_b = round16(xwin * 8);
+  // whole 128-byte rows: the chain inputs are stored swizzled within rows
+  static constexpr size_t rwin_b = (rwin * 8 + 127) / 128 * 128;
+  static constexpr size_t xwin_b = (xwin * 8 + 127) / 128 * 128;
   static constexpr size_t own_b = round16((kTI + 2) * 8);
   // slot: r_k | r_km1 | sigma (r window) | x_k | x_km1 (x window) | b (own)
   static constexpr size_t off_rkm1 = rwin_b;
@@ -381,12 +382,18 @@ struct IterArgs {
 // the reference's full-vector sweeps.  No barrier between stages.  The pair
 // parity of a stage is warp-uniform (P is a multiple of NO for every thread),
 // so away from the global ends the pairs are a fixed unrolled set.
-// window loader: plain copy of one smem window
-struct LoadPlain {
+// Chain inputs (u, trial) are written by lane-contiguous passes into a
+// swizzled layout: 16-byte chunk c of each 128-byte row r sits at c ^ (r & 7),
+// so that the chains' per-thread windows (lane stride 32 bytes) hit all 32
+// banks in every 16-byte load instead of half of them.
+__device__ __forceinline__ int swz_chunk(int c) { return (c & ~7) | ((c ^ (c >> 3)) & 7); }
+__device__ __forceinline__ int swz(int e) { return (swz_chunk(e >> 1) << 1) | (e & 1); }
+struct LoadSwz {
   const double* w;
-  __device__ __forceinline__ double operator()(int q) const { return w[q]; }
-  __device__ __forceinline__ double2 pair(int q) const {
-    return reinterpret_cast<const double2*>(w)[q];
+  int e0;  // logical index of window entry 0
+  __device__ __forceinline__ double operator()(int q) const { return w[swz(e0 + q)]; }
+  __device__ __forceinline__ double2 pair(int q) const {  // e0 even
+    return reinterpret_cast<const double2*>(w)[swz_chunk((e0 >> 1) + q)];
   }
 };
 template <int S, int NO, bool TR, bool INTERIOR, class Load>
@@ -512,43 +519,57 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
     // Shared-memory traffic is the limiter here: per-element work runs with
     // consecutive threads on consecutive entries (2 wavefronts per warp
     // access); only the register chains read per-thread windows.
-    // 0. u = sigma .* r_y, r_y = (1 + beta) r_k - beta r_{k-1}   (in place of r_k)
-    for (int q = t; q < rlen; q += kThreads) s_r[q] = s_sig[q] * ((1.0 + beta) * s_r[q] - beta * s_rm[q]);
+    // 0. u = sigma .* r_y, r_y = (1 + beta) r_k - beta r_{k-1}: in place of r_k,
+    //    swizzled (rows lie inside one warp's 32 entries: read all, then write)
+    for (int q0 = 0; q0 < rlen; q0 += kThreads) {
+      const int q = q0 + t;
+      double u = 0.0;
+      if (q < rlen) u = s_sig[q] * ((1.0 + beta) * s_r[q] - beta * s_rm[q]);
+      __syncwarp();
+      if (q < rlen) s_r[swz(q)] = u;
+    }
     __syncthreads();
     // 1. g = G u on the x window: kNO entries per thread, all stages in registers;
-    //    g parked in the (now free) r_{k-1} buffer at x-window positions
+    //    g parked (swizzled) in the now free r_{k-1} buffer at x-window positions
     double* s_g = const_cast<double*>(s_rm);
     for (int q = kNO * t; q < xlen; q += kNO * kThreads) {
       double g[kNO];
-      const LoadPlain ld{s_r + (q + H - S)};
+      const LoadSwz ld{s_r, q + (int)H - S};
       if (interior)
         chain<S, kNO, false, true>(ld, gx + q - S, n, A.right, g);
       else
         chain<S, kNO, false, false>(ld, gx + q - S, n, A.right, g);
-      reinterpret_cast<double2*>(s_g + q)[0] = make_double2(g[0], g[1]);
-      reinterpret_cast<double2*>(s_g + q)[1] = make_double2(g[2], g[3]);
+      reinterpret_cast<double2*>(s_g)[swz_chunk(q >> 1)] = make_double2(g[0], g[1]);
+      reinterpret_cast<double2*>(s_g)[swz_chunk((q >> 1) + 1)] = make_double2(g[2], g[3]);
     }
     __syncthreads();
-    // 2. y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1}
-    for (int q = t; q < xlen; q += kThreads) {
-      const double xk = s_x[q];
-      const double y = xk + beta * (xk - s_tr[q]);
-      const double tr = soft_threshold(y - inv_l * s_g[q], thr);
-      const int64_t j = gx + q;
-      if (j >= t0 && j < te) {
-        A.b.x_next[j] = tr;
-        acc[0] += fabs(tr);
-        acc[1] += tr != 0.0 ? 1.0 : 0.0;
-        acc[2] += tr != y ? 1.0 : 0.0;
+    // 2. y = x_k + beta (x_k - x_{k-1}); trial = S(y - g/L, tau/L); own -> x_{k+1};
+    //    trial in place of x_{k-1}, swizzled
+    for (int q0 = 0; q0 < xlen; q0 += kThreads) {
+      const int q = q0 + t;
+      double tr = 0.0;
+      if (q < xlen) {
+        const double xk = s_x[q];
+        const double y = xk + beta * (xk - s_tr[q]);
+        tr = soft_threshold(y - inv_l * s_g[swz(q)], thr);
+        const int64_t j = gx + q;
+        if (j >= t0 && j < te) {
+          A.b.x_next[j] = tr;
+          acc[0] += fabs(tr);
+          acc[1] += tr != 0.0 ? 1.0 : 0.0;
+          acc[2] += tr != y ? 1.0 : 0.0;
+        }
+        if (j < 0 || j >= n) tr = 0.0;
       }
-      s_tr[q] = (j >= 0 && j < n) ? tr : 0.0;
+      __syncwarp();
+      if (q < xlen) s_tr[swz(q)] = tr;
     }
     __syncthreads();
     // 3. r_{k+1} = sigma .* (G^T trial) - b on the own rows
     const int own = (int)(te - t0);
     for (int q = kNO * t; q < own; q += kNO * kThreads) {
       double av[kNO];
-      const LoadPlain ld{s_tr + (q + H - S)};
+      const LoadSwz ld{s_tr, q + (int)H - S};
       if (interior)
         chain<S, kNO, true, true>(ld, t0 + q - S, n, A.right, av);
       else
@@ -566,10 +587,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
 #pragma unroll
         for (int e = 0; e < kNO; ++e) acc[3] += rt[e] * rt[e];
       } else {
-        for (int e = 0; e < own - q; ++e) {
-          A.b.r_next[t0 + q + e] = rt[e];
-          acc[3] += rt[e] * rt[e];
-        }
+#pragma unroll
+        for (int e = 0; e < kNO; ++e)
+          if (e < own - q) {
+            A.b.r_next[t0 + q + e] = rt[e];
+            acc[3] += rt[e] * rt[e];
+          }
       }
     }
     __syncthreads();

@@ -137,7 +137,7 @@ __global__ void fista_init_kernel(const double* __restrict__ b, double* r_x, dou
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const double r = 0.0 - b[i];
-    r_x[i] = r;
+    if (r_x) r_x[i] = r;  // null: the recomputing kernel keeps no residual vectors
     if (r_y != r_x) r_y[i] = r;
     acc[0] += r * r;
   }

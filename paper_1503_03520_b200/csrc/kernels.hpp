@@ -86,6 +86,11 @@ struct FistaDev {
   int initialized;  // sample 0 written
   unsigned int ticket[4];
   double scal[4];  // l1, nnz, mismatches, ||r||^2 of the last iteration
+  // lagged objective (recomputing kernel): kernel j sums ||r_j||^2 while it
+  // produces x_{j+1}; x_{j+1}'s l1 / nnz / mismatches wait here for kernel j+1
+  double pend[3];
+  uint64_t pend_ts;
+  int pend_valid;
 };
 
 struct FistaBufs {
@@ -135,6 +140,14 @@ bool fused_iter_supported(const OpView& op);  // banded, 1..4 stages
 // pointer is indexed by GLOBAL entry
 void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi,
                       cudaStream_t st);
+// the same iteration with r_k, r_{k-1} recomputed from x_k, x_{k-1} (k_iter_rc.cu):
+// reads x_k, x_km1, sigma, b, writes x_next (32-byte aligned, lo % 4 == 0);
+// r_* of ib unused.  A shard's x windows need fista_rc_halo(stages) entries.
+// The objective lags one kernel (fista_finalize_lagged); flush = true records
+// the last iterate's (x_k of ib) after the loop.
+void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
+                   bool flush = false);
+int fista_rc_halo(int stages);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -34,6 +36,7 @@ struct l1b_session {
   bool shard = false;
   bool fused = false;   // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
   bool single = false;  // ... as one kernel per iteration (one device): x / r rotate
+  bool recompute = false;  // ... with r_k, r_{k-1} rebuilt from x (k_iter_rc.cu): no R buffers
   double* X[3] = {nullptr, nullptr, nullptr};
   double* R[3] = {nullptr, nullptr, nullptr};
   uint64_t xh = 0, rh = 0;  // single-kernel windows: x / r halo widths (shards: H / 2H)
@@ -57,15 +60,24 @@ struct l1b_session {
     IterBufs ib;
     ib.x_k = gx(X[j % 3]);
     ib.x_km1 = gx(X[(j + 2) % 3]);
-    ib.r_k = gr(R[j % 3]);
-    ib.r_km1 = gr(R[(j + 2) % 3]);
+    ib.r_k = recompute ? nullptr : gr(R[j % 3]);
+    ib.r_km1 = recompute ? nullptr : gr(R[(j + 2) % 3]);
     ib.x_next = gx(X[(j + 1) % 3]);
-    ib.r_next = gr(R[(j + 1) % 3]);
+    ib.r_next = recompute ? nullptr : gr(R[(j + 1) % 3]);
     ib.b = v.b - lo;
     ib.st = st;
     ib.trace = trace;
     ib.partials = partials;
     return ib;
+  }
+
+  // launch j of the single-kernel loop (iteration j + 1)
+  void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
+    const uint64_t lo = shard ? v.row_begin : 0, hi = shard ? v.row_end : v.n;
+    if (recompute)
+      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush);
+    else
+      fista_fused_iter(*v.op, iter_bufs(j), lo, hi, stream);
   }
 
   FistaBufs bufs() const {
@@ -141,6 +153,13 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   cudaStream_t st = v.stream;
   s->shard = v.shard;
   s->single = s->fused && fused_iter_supported(*v.op);
+  {
+    // recomputing kernel: one device, 32-byte aligned sigma / b (256-bit loads);
+    // L1B_ITER_RC=0 selects the stored-residual kernel (comparison runs)
+    const char* e = getenv("L1B_ITER_RC");
+    const bool aligned = ((uintptr_t)v.op->sigma % 32 == 0) && ((uintptr_t)v.b % 32 == 0);
+    s->recompute = s->single && !s->shard && aligned && !(e && e[0] == '0');
+  }
   if (s->single) {
     // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows
     // (a shard: its own rows plus halos of H for x and 2H for r);
@@ -152,14 +171,15 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     s->halo = s->xh;
     for (int q = 0; q < 3; ++q) {
       s->X[q] = s->dalloc(s->nx + 2 * s->xh);
-      s->R[q] = s->dalloc(s->nr + 2 * s->rh);
       L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
+      if (s->recompute) continue;
+      s->R[q] = s->dalloc(s->nr + 2 * s->rh);
       L1B_CUDA(cudaMemsetAsync(s->R[q], 0, (s->nr + 2 * s->rh) * 8, st));
     }
     s->x = s->X[0] + s->xh;
     s->y = s->x;
-    s->r_x = s->R[0] + s->rh;
-    s->r_y = s->R[2] + s->rh;
+    s->r_x = s->recompute ? nullptr : s->R[0] + s->rh;  // null: init only sums ||b||^2
+    s->r_y = s->recompute ? nullptr : s->R[2] + s->rh;
   } else if (s->shard) {
     // windows: [halo | own | halo]; K1 writes own x, K2 gathers the x window,
     // K2 writes own r_y, K1 gathers the r_y window
@@ -222,7 +242,7 @@ void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
   for (uint64_t i = 0; i < iters; ++i) {
     if (s->single) {
-      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), 0, s->v.n, s->v.stream);
+      s->iterate(s->launched + i, s->v.stream);
     } else if (s->fused) {
       fista_fused_k1(*s->v.op, b, s->v.stream);
       fista_fused_k2(*s->v.op, b, s->v.stream);
@@ -237,6 +257,8 @@ void session_step(l1b_session* s, uint64_t iters) {
 void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* sum,
                     double* x_host, double* d_x) {
   cudaStream_t st = s->v.stream;
+  // the recomputing kernel records each iterate one kernel late: record the last one
+  if (s->recompute) s->iterate(s->launched, st, true);
   L1B_CUDA(cudaMemcpyAsync(s->h_st, s->st, sizeof(FistaDev), cudaMemcpyDeviceToHost, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   const FistaDev h = *s->h_st;
@@ -354,8 +376,7 @@ int l1b_session_k1(l1b_session* s) {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
     if (s->single) {  // the whole iteration; k2 is then a no-op
-      fista_fused_iter(*s->v.op, s->iter_bufs(s->launched), s->v.row_begin, s->v.row_end,
-                       s->v.stream);
+      s->iterate(s->launched, s->v.stream);
       s->launched += 1;
     } else if (s->fused) {
       fista_fused_k1(*s->v.op, s->bufs(), s->v.stream);
@@ -408,7 +429,7 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     for (uint64_t i = 0; i < iters; ++i) {
       L1B_CUDA(cudaEventRecord(ev[3 * i], st));
       if (s->single)
-        fista_fused_iter(*s->v.op, s->iter_bufs(s->launched + i), 0, s->v.n, st);
+        s->iterate(s->launched + i, st);
       else if (s->fused)
         fista_fused_k1(*s->v.op, b, st);
       else
