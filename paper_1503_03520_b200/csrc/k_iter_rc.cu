@@ -93,20 +93,6 @@ __device__ __forceinline__ void load_seg(const RcArgs& A, int64_t e, bool full, 
   }
 }
 
-// the same group from a TMA-filled shared-memory slot [x_k | x_km1 | sigma | b]
-__device__ __forceinline__ void load_seg_smem(const double* slot, int lane, Seg& s) {
-  const double2* p = reinterpret_cast<const double2*>(slot) + 2 * lane;
-  double2 a, b;
-  a = p[0], b = p[1];
-  s.xk[0] = a.x, s.xk[1] = a.y, s.xk[2] = b.x, s.xk[3] = b.y;
-  a = p[kWin / 2], b = p[kWin / 2 + 1];
-  s.xm[0] = a.x, s.xm[1] = a.y, s.xm[2] = b.x, s.xm[3] = b.y;
-  a = p[kWin], b = p[kWin + 1];
-  s.sg[0] = a.x, s.sg[1] = a.y, s.sg[2] = b.x, s.sg[3] = b.y;
-  a = p[3 * kWin / 2], b = p[3 * kWin / 2 + 1];
-  s.bb[0] = a.x, s.bb[1] = a.y, s.bb[2] = b.x, s.bb[3] = b.y;
-}
-
 // All S stages on the warp's window; v holds entries [e0, e0+4) (e0 = 0 mod 4).
 // Stage pairs (p, p+1), p = offset (mod 2), p >= offset, p + 1 < n
 // (linops.cpp:46-60); INTERIOR: the window is away from both ends, every pair
@@ -156,18 +142,33 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
   }
 }
 
-// FLUSH: only ||r_k||^2 of the own rows (the objective of the last iterate)
-template <int S, bool INTERIOR, bool FLUSH>
+// Per-thread sums over the segments a thread sees
+struct Acc {
+  double l1 = 0.0, rr = 0.0;  // ||x_{k+1}||_1, ||r_k||^2 (own entries)
+  unsigned nz = 0, mism = 0;  // nnz(x_{k+1}), #(trial != y)
+};
+
+// One segment.  FAST: the window is away from both ends of [0, n) and of the
+// shard's x windows and the segment owns OWN full entries, so every pair
+// exists and a lane's four entries are either all own (lane_own) or all halo.
+// FLUSH: only ||r_k||^2 of the own rows (the objective of the last iterate).
+template <int S, bool FAST, bool FLUSH>
 __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w0, int lane,
-                                        double beta, double inv_l, double thr, double (&acc)[4]) {
+                                        bool lane_own, double beta, double inv_l, double thr,
+                                        Acc& acc) {
   using G = RcGeom<S>;
   const int64_t n = A.n;
   const int64_t e0 = w0 + 4 * lane;
-  // own entries of this segment: [w0 + H3, min(w0 + H3 + OWN, hi))
-  const int64_t own_lo = w0 + G::H3, own_hi = min(own_lo + G::OWN, A.hi);
   bool mine[4];
+  if (FAST) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) mine[i] = e0 + i >= own_lo && e0 + i < own_hi;
+    for (int i = 0; i < 4; ++i) mine[i] = lane_own;
+  } else {
+    // own entries of this segment: [w0 + H3, min(w0 + H3 + OWN, hi))
+    const int64_t own_lo = w0 + G::H3, own_hi = min(own_lo + G::OWN, A.hi);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mine[i] = e0 + i >= own_lo && e0 + i < own_hi;
+  }
   constexpr int K = FLUSH ? 1 : 2;
   double t[K][4];  // G^T x_k and G^T x_{k-1}, side by side (independent chains)
 #pragma unroll
@@ -175,34 +176,35 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
     t[0][i] = d.xk[i];
     if (!FLUSH) t[K - 1][i] = d.xm[i];
   }
-  wchain<S, true, INTERIOR, K>(t, e0, n, A.right);
-  double g[1][4];
+  wchain<S, true, FAST, K>(t, e0, n, A.right);
+  double g[1][4], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const double rk = d.sg[i] * t[0][i] - d.bb[i];
-    if (mine[i]) acc[3] += rk * rk;  // ||r_k||^2: x_k's objective, recorded one kernel late
+    if (mine[i]) rr += rk * rk;  // ||r_k||^2: x_k's objective, recorded one kernel late
     if (!FLUSH) {
       const double rm = d.sg[i] * t[K - 1][i] - d.bb[i];
       g[0][i] = d.sg[i] * ((1.0 + beta) * rk - beta * rm);
     }
   }
+  acc.rr += rr;
   if (FLUSH) return;
-  wchain<S, false, INTERIOR, 1>(g, e0, n, A.right);
-  double tr[4];
-  unsigned nz = 0, mism = 0;
+  wchain<S, false, FAST, 1>(g, e0, n, A.right);
+  double tr[4], l1 = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const double y = d.xk[i] + beta * (d.xk[i] - d.xm[i]);
     tr[i] = soft_threshold(y - inv_l * g[0][i], thr);
     if (mine[i]) {
-      acc[0] += fabs(tr[i]);
-      nz += tr[i] != 0.0;
-      mism += tr[i] != y;
+      l1 += fabs(tr[i]);
+      acc.nz += tr[i] != 0.0;
+      acc.mism += tr[i] != y;
     }
   }
-  acc[1] += (double)nz;
-  acc[2] += (double)mism;
-  if (mine[0] && mine[3]) {
+  acc.l1 += l1;
+  if (FAST) {
+    if (lane_own) st4(A.b.x_next + e0, tr);
+  } else if (mine[0] && mine[3]) {
     st4(A.b.x_next + e0, tr);
   } else {
 #pragma unroll
@@ -211,7 +213,9 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
   }
 }
 
-template <int S, int MB, int PF, int kD = 2, bool FLUSH = false>
+// Warps stream segments q = warp_id, warp_id + #warps, ...; the next segment's
+// loads are issued before the current one computes.
+template <int S, int MB, bool FLUSH = false>
 __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   using G = RcGeom<S>;
   FistaDev* st = A.b.st;
@@ -220,98 +224,43 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   const double inv_l = 1.0 / st->lval;
   const double thr = st->tau * inv_l;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool lane_own = 4 * lane >= G::H3 && 4 * lane < G::H3 + G::OWN;
   const int64_t n = A.n, lo = A.lo, hi = A.hi;
   // loads stay inside [0, n) and inside the x windows [lo - H3, hi + H3)
   const int64_t lim_lo = max((int64_t)0, lo - G::H3), lim_hi = min(n, hi + G::H3);
   const int64_t nseg = (hi - lo + G::OWN - 1) / G::OWN;
   // segments of one block are consecutive (their halos meet in L1/L2)
   const int64_t stride = (int64_t)gridDim.x * kRcWarps;
-  int64_t sgi = (int64_t)blockIdx.x * kRcWarps + warp;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // ||x||_1, nnz, #(trial != y), ||r||^2
+  Acc acc;
 
   auto w0_of = [&](int64_t q) { return lo + q * G::OWN - G::H3; };
   auto full_of = [&](int64_t w0) { return w0 >= lim_lo && w0 + kWin <= lim_hi; };
-  Seg cur, nxt;
-  if (PF == 4) {
-    // per-warp ring of kD slots, each one segment of the four inputs (4 KiB),
-    // filled by bulk copies (lane 0) kD - 1 segments ahead of the compute
-    extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int kSlot = 4 * kWin * 8;
-    unsigned char* ring = smem + (size_t)warp * kD * kSlot;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kRcWarps * kD * kSlot) + warp * kD;
-    if (lane == 0) {
-      for (int q = 0; q < kD; ++q) mbar_init(&bars[q], 1);
-      fence_mbar_init();
-    }
-    __syncwarp();
-    auto issue = [&](int64_t q, int slot) {  // lane 0
-      const int64_t w = w0_of(q);
-      if (q >= nseg || !full_of(w)) return;
-      unsigned char* d = ring + slot * kSlot;
-      mbar_arrive_expect_tx(&bars[slot], kSlot);
-      bulk_g2s(d, A.b.x_k + w, kWin * 8, &bars[slot]);
-      bulk_g2s(d + kWin * 8, A.b.x_km1 + w, kWin * 8, &bars[slot]);
-      bulk_g2s(d + 2 * kWin * 8, A.sigma + w, kWin * 8, &bars[slot]);
-      bulk_g2s(d + 3 * kWin * 8, A.b.b + w, kWin * 8, &bars[slot]);
-    };
-    if (lane == 0)
-      for (int q = 0; q < kD - 1; ++q) issue(sgi + q * stride, q);
-    uint32_t phase = 0;  // bit q: parity of slot q's next completion
-    int slot = 0;
-    for (int64_t i = 0; sgi < nseg; sgi += stride, ++i) {
-      const int64_t w0 = w0_of(sgi);
-      if (lane == 0) issue(sgi + (kD - 1) * stride, (slot + kD - 1) % kD);
-      const bool full = full_of(w0);
-      if (full) {
-        mbar_wait(&bars[slot], (phase >> slot) & 1);
-        phase ^= 1u << slot;
-        load_seg_smem(reinterpret_cast<const double*>(ring + slot * kSlot), lane, cur);
-      } else {
-        load_seg(A, w0 + 4 * lane, false, lim_lo, lim_hi, cur);
-      }
-      const bool interior = full && w0 >= 2 && w0 + kWin < n;
-      if (interior)
-        segment<S, true, FLUSH>(A, cur, w0, lane, beta, inv_l, thr, acc);
-      else
-        segment<S, false, FLUSH>(A, cur, w0, lane, beta, inv_l, thr, acc);
-      __syncwarp();  // the slot's reads are done before it is refilled
-      if (lane == 0) fence_proxy_async();
-      slot = (slot + 1) % kD;
-    }
-  } else {
-    if (sgi < nseg) {
-      const int64_t w0 = w0_of(sgi);
-      load_seg(A, w0 + 4 * lane, full_of(w0), lim_lo, lim_hi, cur);
-    }
-    for (; sgi < nseg; sgi += stride) {
-      const int64_t w0 = w0_of(sgi);
-      if (PF != 1) {
-        if (sgi != (int64_t)blockIdx.x * kRcWarps + warp)
-          load_seg(A, w0 + 4 * lane, full_of(w0), lim_lo, lim_hi, cur);
-        if (PF >= 2 && lane < 4) {  // bulk L2 prefetch of a later segment (no registers held)
-          const int64_t q = sgi + (PF - 1) * stride;
-          if (q < nseg && full_of(w0_of(q))) {
-            const double* base = lane == 0 ? A.b.x_k : lane == 1 ? A.b.x_km1 : lane == 2 ? A.sigma : A.b.b;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + w0_of(q)),
-                         "r"(kWin * 8)
-                         : "memory");
-          }
-        }
-      } else if (sgi + stride < nseg) {  // next segment's loads in flight during this one
-        const int64_t w1 = w0_of(sgi + stride);
-        load_seg(A, w1 + 4 * lane, full_of(w1), lim_lo, lim_hi, nxt);
-      }
-      // every pair touching the window exists: p >= w0 - 1 >= 1 >= offset, p + 1 <= w0 + kWin < n
-      const bool interior = full_of(w0) && w0 >= 2 && w0 + kWin < n;
-      if (interior)
-        segment<S, true, FLUSH>(A, cur, w0, lane, beta, inv_l, thr, acc);
-      else
-        segment<S, false, FLUSH>(A, cur, w0, lane, beta, inv_l, thr, acc);
-      if (PF == 1) cur = nxt;
-    }
+  auto load = [&](int64_t q, Seg& d) {
+    const int64_t w0 = w0_of(q);
+    load_seg(A, w0 + 4 * lane, full_of(w0), lim_lo, lim_hi, d);
+  };
+  auto run = [&](int64_t q, const Seg& d) {
+    const int64_t w0 = w0_of(q);
+    // every pair touching the window exists (p >= w0 - 1 >= 1 >= offset,
+    // p + 1 <= w0 + kWin < n) and the OWN entries are all inside [lo, hi)
+    const bool fast = full_of(w0) && w0 >= 2 && w0 + kWin < n && w0 + G::H3 + G::OWN <= hi;
+    if (fast)
+      segment<S, true, FLUSH>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+    else
+      segment<S, false, FLUSH>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+  };
+  Seg sa, sb;
+  int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
+  if (q < nseg) load(q, sa);
+  // (a two-way unrolled ping-pong without the copy measured slower: code size)
+  for (; q < nseg; q += stride) {
+    if (q + stride < nseg) load(q + stride, sb);
+    run(q, sa);
+    sa = sb;
   }
+  double sums[4] = {acc.l1, (double)acc.nz, (double)acc.mism, acc.rr};
   double tot[4];
-  if (grid_sum<4>(acc, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
+  if (grid_sum<4>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
     st->scal[0] = tot[0];
     st->scal[1] = tot[1];
     st->scal[2] = tot[2];
@@ -320,28 +269,24 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   }
 }
 
-template <int S, int MB, int PF, int kD = 2, bool FLUSH = false>
+template <int S, int MB, bool FLUSH = false>
 void launch_rc_v(const RcArgs& a, cudaStream_t st) {
   using G = RcGeom<S>;
   static int grid_cap = 0;
-  const size_t smem = PF == 4 ? (size_t)kRcWarps * kD * (4 * kWin * 8 + 8) : 0;
   if (!grid_cap) {
-    if (smem)
-      L1B_CUDA(cudaFuncSetAttribute(fista_rc_kernel<S, MB, PF, kD, FLUSH>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_rc_kernel<S, MB, PF, kD, FLUSH>,
-                                                          kRcThreads, smem));
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_rc_kernel<S, MB, FLUSH>,
+                                                          kRcThreads, 0));
     grid_cap = std::min(std::max(1, per_sm) * sm_count(), spmv_grid_max());
   }
   const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
   const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc_kernel<S, MB, PF, kD, FLUSH><<<grid, kRcThreads, smem, st>>>(a);
+  fista_rc_kernel<S, MB, FLUSH><<<grid, kRcThreads, 0, st>>>(a);
   L1B_LAUNCHED();
 }
 
-// min CTAs/SM x register prefetch of the next segment; L1B_RC_VARIANT picks (tuning runs)
+// min CTAs/SM; L1B_RC_VARIANT picks (tuning runs)
 int rc_variant() {
   static int v = -1;
   if (v < 0) {
@@ -354,20 +299,14 @@ int rc_variant() {
 template <int S>
 void launch_rc(const RcArgs& a, cudaStream_t st) {
   switch (rc_variant()) {
-    case 1: return launch_rc_v<S, 3, 0>(a, st);
-    case 2: return launch_rc_v<S, 3, 2>(a, st);
-    case 3: return launch_rc_v<S, 3, 3>(a, st);
-    case 4: return launch_rc_v<S, 2, 2>(a, st);
-    case 5: return launch_rc_v<S, 3, 4, 2>(a, st);
-    case 6: return launch_rc_v<S, 2, 4, 3>(a, st);
-    case 7: return launch_rc_v<S, 2, 4, 2>(a, st);
-    default: return launch_rc_v<S, 2, 1>(a, st);
+    case 1: return launch_rc_v<S, 1>(a, st);
+    default: return launch_rc_v<S, 2>(a, st);
   }
 }
 
 template <int S>
 void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
-  launch_rc_v<S, 2, 0, 2, true>(a, st);
+  launch_rc_v<S, 2, true>(a, st);
 }
 
 }  // namespace
