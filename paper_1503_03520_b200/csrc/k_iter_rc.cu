@@ -15,10 +15,13 @@
 //     rotates (v1, v2) in the lane and the pairs straddling lanes through one
 //     shuffle each way -- every rotation is done exactly once, no redundant
 //     cone work;
-//   * per iteration the chain runs four times (r_k, r_{k-1}, g = G u,
-//     r_{k+1}); each run invalidates S entries at both window ends, so the
-//     window carries a halo of H3 >= 3S entries per side and owns the middle
-//     128 - 2 H3 (104 for 3-4 stages);
+//   * per iteration the chain runs three times (r_k and r_{k-1} side by side,
+//     then g = G u); each of the two runs in series invalidates S entries at
+//     both window ends, so the window carries a halo of H3 >= 2S entries per
+//     side and owns the middle 128 - 2 H3 (112 for 3-4 stages);
+//   * ||r_{k+1}||^2 is not formed here: the next kernel sums ||r_k||^2 from the
+//     r_k it rebuilds anyway, and the objective is recorded one kernel late
+//     (fista_finalize_lagged; a flush launch records the last iterate);
 //   * no shared memory and no block barriers in the loop: warps stream their
 //     segments independently, with the next segment's loads in flight while
 //     the current one computes.
@@ -29,8 +32,7 @@
 //   u       = sigma .* ((1 + beta) r_k - beta r_{k-1})        (r_y, then A^T's sigma)
 //   g       = G u                                              (A^T r_y)
 //   y       = x_k + beta (x_k - x_{k-1});  trial = S(y - g/L, tau/L)   (:325-336)
-//   own:      x_{k+1} = trial; ||x||_1, nnz, #(trial != y)
-//   r_{k+1} = sigma .* (G^T trial) - b  -> ||r_{k+1}||^2 on the own rows
+//   own:      x_{k+1} = trial; ||x_{k+1}||_1, nnz, #(trial != y); ||r_k||^2
 #include "common.cuh"
 #include "fista.cuh"
 #include "kernels.hpp"
@@ -47,7 +49,9 @@ constexpr unsigned kFull = 0xffffffffu;
 
 template <int S>
 struct RcGeom {
-  static constexpr int H3 = (3 * S + 3) / 4 * 4;  // halo: >= 3S, 32-byte aligned
+  // halo: two chains in series (r = sigma G^T x - b, then g = G u) each spoil S
+  // entries per window end; 32-byte aligned
+  static constexpr int H3 = (2 * S + 3) / 4 * 4;
   static constexpr int OWN = kWin - 2 * H3;
 };
 
