@@ -263,13 +263,22 @@ typedef struct {
    * j+1 from x_j = x_bufs[j%3], x_{j-1} = x_bufs[(j+2)%3] (same for r) into
    * x_bufs[(j+1)%3] / r_bufs[(j+1)%3]; the caller then exchanges the halos of
    * those two (x_halo / r_halo entries each side); l1b_session_k2 is a no-op.
-   * Before the first iteration r_bufs[0] and r_bufs[2] need their halos. */
+   * Before the first iteration r_bufs[0] and r_bufs[2] need their halos.
+   * lagged = 1 (recomputing kernel, k_iter_rc.cu): no residual buffers
+   * (r_bufs null, r_halo 0), only the x halos travel; scal carries ||r_j||^2
+   * of the iterate the kernel started from, so each iteration is recorded by
+   * the NEXT finalize; after the loop: l1b_session_flush, all-reduce scal,
+   * l1b_session_finalize records the last iterate. */
   int single;
   double* x_bufs[3];  /* own + 2*x_halo */
   double* r_bufs[3];  /* own + 2*r_halo */
   uint64_t x_halo, r_halo;
+  int lagged;
 } l1b_shard_buffers;
 int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
+/* Lagged shard sessions: sums ||r||^2 of the last iterate into scal (a no-op
+ * for other sessions; single-device sessions flush inside l1b_session_end). */
+int l1b_session_flush(l1b_session* s);
 int l1b_session_k1(l1b_session* s);
 int l1b_session_k2(l1b_session* s);
 int l1b_session_finalize(l1b_session* s);

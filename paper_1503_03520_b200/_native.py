@@ -55,7 +55,7 @@ class ProblemInfo(C.Structure):
 class ShardBuffers(C.Structure):
     _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64),
                 ("single", C.c_int), ("x_bufs", vp * 3), ("r_bufs", vp * 3), ("x_halo", u64),
-                ("r_halo", u64)]
+                ("r_halo", u64), ("lagged", C.c_int)]
 
 
 class Cert(C.Structure):
@@ -122,6 +122,7 @@ SIGNATURES = [
     ("l1b_session_k1", C.c_int, [vp]),
     ("l1b_session_k2", C.c_int, [vp]),
     ("l1b_session_finalize", C.c_int, [vp]),
+    ("l1b_session_flush", C.c_int, [vp]),
 ]
 
 

@@ -174,12 +174,16 @@ struct l1b_problem {
   bool sharded = false;  // a row-block shard (l1b_generate with a shard descriptor)
   uint64_t halo = 0;
   uint64_t sig_begin = 0;  // shards: d_sigma holds sigma[sig_begin, ...)
+  // shards: b on [b_win_lo, b_win_hi) = own rows +- the recomputing kernel's
+  // halo (it rebuilds r on the rows around its own block)
+  double* d_b_win = nullptr;
+  uint64_t b_win_lo = 0, b_win_hi = 0;
 
   ~l1b_problem() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv,
-                    (void*)d_b, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
+                    (void*)d_b, (void*)d_b_win, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
                     (void*)csc.idx, (void*)csc.val})
       if (p) cudaFree(p);
     if (stream && own_stream) cudaStreamDestroy(stream);
@@ -418,7 +422,11 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   } else {
     throw InvalidArgument("unknown spectrum kind");
   }
-  const uint64_t sa = a > 3 * h ? a - 3 * h : 0, sb = std::min(n, b + 3 * h);
+  // b is also built on bh rows around the block for the recomputing FISTA
+  // kernel (k_iter_rc.cu); sigma / x / w windows widen by the same amount
+  const uint64_t bh = g->stages >= 1 && g->stages <= 4 ? (uint64_t)fista_rc_halo((int)g->stages) : 0;
+  const uint64_t sa = a > bh + 3 * h ? (a - bh - 3 * h) & ~3ull : 0;  // 32-byte aligned view
+  const uint64_t sb = std::min(n, b + bh + 3 * h);
   auto p = std::make_unique<l1b_problem>();
   std::vector<int32_t> r_off;
   for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
@@ -473,7 +481,8 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
       if (i >= sa && i < sb) gw[i - sa] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
     }
   }
-  const uint64_t va = a > h ? a - h : 0, vb = std::min(n, b + h), own = b - a;
+  const uint64_t va = a > bh + h ? a - bh - h : 0, vb = std::min(n, b + bh + h), own = b - a;
+  const uint64_t wa = a > bh ? a - bh : 0, wb = std::min(n, b + bh);  // b window
   xw.assign(vb - va, 0.0);
   for (uint64_t k = 0; k < s; ++k) {
     const uint64_t i = p->xs_sup[k];
@@ -491,12 +500,24 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   L1B_CUDA(cudaMemcpyAsync(d_v, d_g + (va - sa), (vb - va) * 8, cudaMemcpyDeviceToDevice, st));
   window_stages(p->view.right, true, true, d_v, va, vb, n, st);
   window_stages(p->view.right, true, true, d_x, va, vb, n, st);
-  window_scale_op(d_v + (a - va), p->d_sigma + (a - sa), own, 1, 0.0, st);
-  window_scale_op(d_x + (a - va), p->d_sigma + (a - sa), own, 1, 0.0, st);
+  window_scale_op(d_v + (wa - va), p->d_sigma + (wa - sa), wb - wa, 1, 0.0, st);
+  window_scale_op(d_x + (wa - va), p->d_sigma + (wa - sa), wb - wa, 1, 0.0, st);
   p->d_b = dev_alloc<double>(own, &p->device_bytes);
   L1B_CUDA(cudaMemcpyAsync(p->d_b, d_x + (a - va), own * 8, cudaMemcpyDeviceToDevice, st));
   double* d_ss = nullptr;
   L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
+  if (bh) {  // the same b = A x* + tau e, element for element, on the window
+    double* d_e = nullptr;
+    L1B_CUDA(cudaMalloc(&d_e, (wb - wa) * sizeof(double)));
+    L1B_CUDA(cudaMemcpyAsync(d_e, d_v + (wa - va), (wb - wa) * 8, cudaMemcpyDeviceToDevice, st));
+    p->d_b_win = dev_alloc<double>(wb - wa, &p->device_bytes);
+    L1B_CUDA(cudaMemcpyAsync(p->d_b_win, d_x + (wa - va), (wb - wa) * 8, cudaMemcpyDeviceToDevice, st));
+    generator_combine(p->tau, d_e, p->d_b_win, wb - wa, d_ss, st);
+    p->b_win_lo = wa;
+    p->b_win_hi = wb;
+    L1B_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_e);
+  }
   generator_combine(p->tau, d_v + (a - va), p->d_b, own, d_ss, st);  // e *= tau; b += e
   double ss = 0.0;
   L1B_CUDA(cudaMemcpyAsync(&ss, d_ss, 8, cudaMemcpyDeviceToHost, st));
@@ -911,6 +932,11 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   v.row_begin = p->row_begin;
   v.row_end = p->row_end;
   v.halo = p->halo;
+  if (p->d_b_win) {
+    v.b_win = p->d_b_win - p->b_win_lo;
+    v.b_win_lo = p->b_win_lo;
+    v.b_win_hi = p->b_win_hi;
+  }
   return v;
 }
 const double* problem_gram(l1b_problem* p) { return gram_diag_device(p); }

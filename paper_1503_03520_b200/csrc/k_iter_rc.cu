@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
     st->scal[1] = tot[1];
     st->scal[2] = tot[2];
     st->scal[3] = tot[3];
-    fista_finalize_lagged(st, A.b.trace, FLUSH);
+    if (FLUSH) st->flushing = 1;
+    if (!st->defer) fista_finalize_lagged(st, A.b.trace, FLUSH);  // shards: after the all-reduce
   }
 }
 

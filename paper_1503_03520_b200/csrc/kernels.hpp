@@ -91,6 +91,8 @@ struct FistaDev {
   double pend[3];
   uint64_t pend_ts;
   int pend_valid;
+  int lagged;    // the recomputing kernel: fista_finalize_lagged
+  int flushing;  // set by its flush launch (deferred finalize records, then stops stashing)
 };
 
 struct FistaBufs {

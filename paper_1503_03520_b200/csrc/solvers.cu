@@ -64,7 +64,7 @@ struct l1b_session {
     ib.r_km1 = recompute ? nullptr : gr(R[(j + 2) % 3]);
     ib.x_next = gx(X[(j + 1) % 3]);
     ib.r_next = recompute ? nullptr : gr(R[(j + 1) % 3]);
-    ib.b = v.b - lo;
+    ib.b = recompute && shard ? v.b_win : v.b - lo;
     ib.st = st;
     ib.trace = trace;
     ib.partials = partials;
@@ -156,9 +156,19 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   {
     // recomputing kernel: one device, 32-byte aligned sigma / b (256-bit loads);
     // L1B_ITER_RC=0 selects the stored-residual kernel (comparison runs)
+    // (shards: b on the rows around the block, blocks on multiples of 4 and at
+    // least one halo wide -- the exchange only reaches the next rank)
     const char* e = getenv("L1B_ITER_RC");
-    const bool aligned = ((uintptr_t)v.op->sigma % 32 == 0) && ((uintptr_t)v.b % 32 == 0);
-    s->recompute = s->single && !s->shard && aligned && !(e && e[0] == '0');
+    bool ok = s->single && !(e && e[0] == '0') && (uintptr_t)v.op->sigma % 32 == 0;
+    if (ok && s->shard) {
+      const uint64_t H3 = (uint64_t)fista_rc_halo(v.op->right.count);
+      ok = v.b_win && (uintptr_t)v.b_win % 32 == 0 && v.row_begin % 4 == 0 &&
+           v.row_end - v.row_begin >= H3 && v.b_win_lo <= (v.row_begin > H3 ? v.row_begin - H3 : 0) &&
+           v.b_win_hi >= std::min(v.n, v.row_end + H3);
+    } else if (ok) {
+      ok = (uintptr_t)v.b % 32 == 0;
+    }
+    s->recompute = ok;
   }
   if (s->single) {
     // x_k, x_{k-1}, x_{k+1} and r_k, r_{k-1}, r_{k+1} over the n active rows
@@ -166,8 +176,8 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     // X[2] / R[2] stand for the iterate "before" the first one (x_{-1} = x_0)
     const uint64_t H = ((uint64_t)v.op->right.count + 1) & ~1ull;
     s->nx = s->nr = s->shard ? v.row_end - v.row_begin : v.n;
-    s->xh = s->shard ? H : 0;
-    s->rh = s->shard ? 2 * H : 0;
+    s->xh = s->shard ? (s->recompute ? (uint64_t)fista_rc_halo(v.op->right.count) : H) : 0;
+    s->rh = s->shard && !s->recompute ? 2 * H : 0;
     s->halo = s->xh;
     for (int q = 0; q < 3; ++q) {
       s->X[q] = s->dalloc(s->nx + 2 * s->xh);
@@ -231,6 +241,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.accel = s->accel ? 1 : 0;
   h.defer = s->shard ? 1 : 0;
   h.init_tail = s->single ? v.tail_sq_band : 0.0;  // the init kernel covers rows [0, nr)
+  h.lagged = s->recompute ? 1 : 0;
   *s->h_st = h;
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
   s->t0 = std::chrono::steady_clock::now();
@@ -258,7 +269,7 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
                     double* x_host, double* d_x) {
   cudaStream_t st = s->v.stream;
   // the recomputing kernel records each iterate one kernel late: record the last one
-  if (s->recompute) s->iterate(s->launched, st, true);
+  if (s->recompute && !s->shard) s->iterate(s->launched, st, true);  // shards: l1b_session_flush
   L1B_CUDA(cudaMemcpyAsync(s->h_st, s->st, sizeof(FistaDev), cudaMemcpyDeviceToHost, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   const FistaDev h = *s->h_st;
@@ -368,6 +379,16 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     }
     out->x_halo = s->xh;
     out->r_halo = s->rh;
+    out->lagged = s->recompute ? 1 : 0;
+  });
+}
+
+int l1b_session_flush(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    if (!s->recompute || !s->shard) return;  // single device: inside l1b_session_end
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    s->iterate(s->launched, s->v.stream, true);
   });
 }
 

@@ -26,6 +26,9 @@ struct ProblemView {
   int world = 1, rank = 0;
   bool shard = false;
   uint64_t row_begin = 0, row_end = 0, halo = 0;
+  // shards: b by global row index, valid on [b_win_lo, b_win_hi) (null if absent)
+  const double* b_win = nullptr;
+  uint64_t b_win_lo = 0, b_win_hi = 0;
 };
 
 ProblemView problem_view(l1b_problem* p, bool need_sparse = true);

@@ -3,7 +3,16 @@
 Every config's operator is banded (identity P1/P2, no left stages:
 |col - row| <= h = #stages), so rank g owns rows [a_g, b_g) of A *and* the
 same range of columns.  Per iteration (solvers.cpp:311-377), single-kernel
-mode (matrix-free, the default):
+mode with recomputed residuals (matrix-free, 1..4 stages, the default):
+
+    one kernel: x_{k+1} from x_k, x_{k-1} (r_k, r_{k-1} rebuilt on the rows
+                around the block from a b window generated with the shard)
+    exchange the halos of x_{k+1} (H3 = 2h rounded up to 4 entries)
+    all-reduce 4 scalars (||x_{k+1}||_1, nnz, #(trial != y), ||r_k||^2) ->
+    finalise (iteration k's objective: recorded one kernel late, plus a
+    flush after the loop)
+
+stored-residual single-kernel mode (L1B_ITER_RC=0):
 
     one kernel: x_{k+1}, r_{k+1} from x_k, x_{k-1}, r_k, r_{k-1}  (own block)
     exchange the halos of x_{k+1} (H entries) and r_{k+1} (2H entries)
@@ -122,10 +131,13 @@ class CudaShard:
         dev = torch.device("cuda", device)
         self.single = bool(b.single)
         self.j = 0  # iterations launched (single mode: buffer rotation)
+        self.lagged = bool(b.lagged)
         if self.single:
             self.x_halo, self.r_halo = int(b.x_halo), int(b.r_halo)
             self.x_bufs = [device_view(b.x_bufs[q], self.own + 2 * self.x_halo, dev) for q in range(3)]
-            self.r_bufs = [device_view(b.r_bufs[q], self.own + 2 * self.r_halo, dev) for q in range(3)]
+            self.r_bufs = None
+            if self.r_halo:  # stored-residual kernel; the recomputing one keeps no r
+                self.r_bufs = [device_view(b.r_bufs[q], self.own + 2 * self.r_halo, dev) for q in range(3)]
         else:
             self.x_win = device_view(b.x_win, self.own + 2 * self.halo, dev)
             self.r_y_win = device_view(b.r_y_win, self.own + 2 * self.halo, dev)
@@ -135,10 +147,13 @@ class CudaShard:
     # single-kernel mode: windows to exchange after iteration j / before the first
     def next_halos(self):
         q = self.j % 3
-        return [(self.x_bufs[q], self.x_halo), (self.r_bufs[q], self.r_halo)]
+        return [(self.x_bufs[q], self.x_halo)] + ([(self.r_bufs[q], self.r_halo)] if self.r_bufs else [])
 
     def initial_halos(self):
-        return [(self.r_bufs[0], self.r_halo), (self.r_bufs[2], self.r_halo)]
+        return [(self.r_bufs[0], self.r_halo), (self.r_bufs[2], self.r_halo)] if self.r_bufs else []
+
+    def flush(self):
+        N.check(self._lib.l1b_session_flush(self.sess._s))
 
     def k1(self):
         N.check(self._lib.l1b_session_k1(self.sess._s))
@@ -171,7 +186,19 @@ def fista_distributed(be, iterations: int, group=None, poll_every: int = 0):
         fista_iteration(be, group)
         if poll_every and (it + 1) % poll_every == 0 and be.stopped()[0]:
             break
+    finish_lagged(be, group)
     return be.finish()
+
+
+def finish_lagged(be, group=None):
+    """Recomputing kernel: each iterate's objective is recorded by the finalize
+    after the NEXT kernel; the flush launch sums ||r||^2 of the last one."""
+    import torch.distributed as dist
+
+    if getattr(be, "lagged", False):
+        be.flush()
+        dist.all_reduce(be.scal, group=group)
+        be.finalize()
 
 
 def start(be, group=None):
@@ -246,6 +273,7 @@ def bench_main(args, world: int, rank: int, local: int):
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_total = float(ms.item())
+    finish_lagged(be)
     stopped, k = be.stopped()
     tr, _ = be.finish()
     if rank == 0:
@@ -259,7 +287,10 @@ def bench_main(args, world: int, rank: int, local: int):
             "config": {"workload": f"C4 FISTA n=2^{int(math.log2(info.n))} row-sharded over {world} GPUs "
                                    f"({be.own} rows/columns per GPU, halo {be.halo})",
                        "l2": "inputs larger than L2 (no flush needed)",
-                       "parallelism": (f"row-block shards x{world}: one matrix-free kernel per iteration, "
+                       "parallelism": (f"row-block shards x{world}: one matrix-free kernel per iteration "
+                                       f"(residuals recomputed), NCCL P2P halo of x ({be.x_halo} doubles per "
+                                       f"neighbour) + 4-double all-reduce" if be.single and be.lagged else
+                                       f"row-block shards x{world}: one matrix-free kernel per iteration, "
                                        f"NCCL P2P halo of x ({be.x_halo}) and r ({be.r_halo}) doubles per "
                                        f"neighbour + 4-double all-reduce" if be.single else
                                        f"row-block shards x{world}: NCCL P2P halo (2 x {be.halo} doubles "

@@ -210,3 +210,116 @@ class CpuShardSingle:
     def finish(self):
         q = self.k % 3
         return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()
+
+
+class CpuShardRc:
+    """Recomputing-kernel stand-in (k_iter_rc.cu fista_rc_kernel): only x
+    travels (three windows with halo H3 = 2S rounded up to 4); r_k, r_{k-1}
+    are rebuilt from x_k, x_{k-1} on the rows around the block (b window);
+    scal[3] is ||r_k||^2 of the iterate the kernel started from, so the
+    objective of iteration j is recorded by the finalize after kernel j
+    (fista_finalize_lagged) and a flush records the last one."""
+
+    def __init__(self, oracle, inst, rank, world, max_iters):
+        self.rank, self.world, self.single, self.lagged = rank, world, True, True
+        n = inst.n
+        S = len(inst.op.right_offset)
+        H3 = (2 * S + 3) // 4 * 4
+        a, b = partition(n, world)[rank]
+        self.n, self.a, self.b_, self.own, self.S = n, a, b, b - a, S
+        self.x_halo, self.r_halo = H3, 0
+        rp, ri, rv = oracle.csr(inst.op)
+        cp, ci, cv = oracle.csc(inst.op)
+        base = a - H3  # window-local index of global entry g: g - base
+        # rows [a - S, b + S) over the x window; columns [a, b) over those rows
+        self.rlo, self.rhi = max(0, a - S), min(n, b + S)
+        self.rows = {i: (ri[rp[i]:rp[i + 1]].astype(np.int64) - base, rv[rp[i]:rp[i + 1]])
+                     for i in range(self.rlo, self.rhi)}
+        self.cols = [(ci[cp[j]:cp[j + 1]].astype(np.int64), cv[cp[j]:cp[j + 1]]) for j in range(a, b)]
+        self.bwin = {i: inst.b[i] for i in range(self.rlo, self.rhi)}
+        self.x_bufs = [torch.zeros(self.own + 2 * H3, dtype=torch.float64) for _ in range(3)]
+        self.r_bufs = None
+        self.scal = torch.zeros(4, dtype=torch.float64)
+        self.scal[3] = float(sum((0.0 - inst.b[i]) ** 2 for i in range(a, b)))
+        self.tau, self.L = inst.tau, oracle.gram_lmax(inst.op)
+        self.t, self.beta_y, self.k, self.j = 1.0, 0.0, 0, 0
+        self.stop, self.init, self.pend, self.flushing = False, False, None, False
+        self.max_iters = max_iters
+        self.samples = []
+
+    def next_halos(self):
+        return [(self.x_bufs[self.j % 3], self.x_halo)]
+
+    def initial_halos(self):
+        return []
+
+    def _r(self, x):
+        return {i: sum(v * x[q] for q, v in zip(*self.rows[i])) - self.bwin[i] for i in self.rows}
+
+    def k1(self, flush=False):
+        j = self.j
+        if not flush:
+            self.j += 1
+        if self.stop:
+            return
+        H, a, beta = self.x_halo, self.a, self.beta_y
+        xk, xkm1 = self.x_bufs[j % 3].numpy(), self.x_bufs[(j + 2) % 3].numpy()
+        rk = self._r(xk)
+        rr = sum(rk[i] ** 2 for i in range(a, self.b_))
+        if flush:
+            self.flushing = True
+            self.scal[0], self.scal[1], self.scal[2], self.scal[3] = 0.0, 0.0, 0.0, rr
+            return
+        rkm1 = self._r(xkm1)
+        xn = self.x_bufs[(j + 1) % 3].numpy()
+        inv_l = 1.0 / self.L
+        thr = self.tau * inv_l
+        l1 = nnz = mism = 0.0
+        for jj, (idx, val) in zip(range(a, self.b_), self.cols):
+            g = sum(v * ((1.0 + beta) * rk[i] - beta * rkm1[i]) for i, v in zip(idx, val))
+            lx = jj - (a - H)
+            y = xk[lx] + beta * (xk[lx] - xkm1[lx])
+            v = y - inv_l * g
+            tr = v - thr if v > thr else (v + thr if v < -thr else 0.0)
+            xn[lx] = tr
+            l1 += abs(tr)
+            nnz += tr != 0.0
+            mism += tr != y
+        self.scal[0], self.scal[1], self.scal[2], self.scal[3] = l1, nnz, mism, rr
+
+    def k2(self):
+        pass
+
+    def flush(self):
+        self.k1(flush=True)
+
+    def finalize(self):
+        if self.stop:
+            return
+        sc = self.scal.numpy().copy()
+        if not self.init:
+            self.init = True
+            self.samples.append((0, 0.5 * sc[3]))
+            self.stop = self.max_iters == 0
+            return
+        if self.pend is not None:
+            l1, _, mism = self.pend
+            self.pend = None
+            self.k += 1
+            self.samples.append((self.k, self.tau * l1 + 0.5 * sc[3]))
+            if mism == 0.0 or self.k >= self.max_iters:
+                self.stop = True
+                return
+        if self.flushing:
+            return
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * self.t * self.t))
+        self.beta_y = (self.t - 1.0) / t_next
+        self.t = t_next
+        self.pend = (sc[0], sc[1], sc[2])
+
+    def stopped(self):
+        return self.stop, self.k
+
+    def finish(self):
+        q = self.k % 3
+        return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()

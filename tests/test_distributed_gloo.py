@@ -29,14 +29,15 @@ def _worker(rank, world, port, out_dir, single):
     sys.path.insert(0, os.path.join(HERE, ".."))
     import torch.distributed as dist
 
-    from dist_cpu_backend import CpuShard, CpuShardSingle
+    from dist_cpu_backend import CpuShard, CpuShardRc, CpuShardSingle
     from paper_1503_03520_b200.distributed import fista_distributed
     from pyoracle import Oracle
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     oracle = Oracle()
     inst = oracle.build_instance(**KW)
-    be = (CpuShardSingle if single else CpuShard)(oracle, inst, rank, world, ITERS)
+    cls = {"two": CpuShard, "single": CpuShardSingle, "rc": CpuShardRc}[single]
+    be = cls(oracle, inst, rank, world, ITERS)
     samples, x_own = fista_distributed(be, ITERS + 5)
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), f=np.array([s[1] for s in samples]),
              it=np.array([s[0] for s in samples]), x=x_own)
@@ -44,7 +45,8 @@ def _worker(rank, world, port, out_dir, single):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,single", [(2, False), (3, False), (2, True), (3, True)])
+@pytest.mark.parametrize("world,single", [(2, "two"), (3, "two"), (2, "single"), (3, "single"),
+                                          (2, "rc"), (3, "rc")])
 def test_sharded_fista_matches_single_process(tmp_path, oracle, world, single):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), single), nprocs=world, join=True)
     inst = oracle.build_instance(**KW)

@@ -14,12 +14,18 @@ pytestmark = pytest.mark.gpu
 KW = dict(n=4096, stages=4, q=1, s_divisor=100, seed=3, theta=2 * math.pi / 10)
 
 
-def _shards(world, iters, op="auto"):
+def _shards(world, iters, op="auto", stored=False):
+    import os
+
     from paper_1503_03520_b200 import l1bench
     from paper_1503_03520_b200.distributed import CudaShard
 
     cfg = l1bench.SolverConfig(max_iters=iters, op=op)
-    return [CudaShard(KW, r, world, 0, cfg) for r in range(world)]
+    os.environ["L1B_ITER_RC"] = "0" if stored else "1"  # read at session begin
+    try:
+        return [CudaShard(KW, r, world, 0, cfg) for r in range(world)]
+    finally:
+        del os.environ["L1B_ITER_RC"]
 
 
 def _exchange(shards, name):
@@ -52,17 +58,21 @@ def _allreduce(shards):
         s.scal.copy_(tot)
 
 
-@pytest.mark.parametrize("world,op", [(2, "sparse"), (3, "sparse"), (2, "matrix_free"), (3, "matrix_free")])
+@pytest.mark.parametrize("world,op", [(2, "sparse"), (3, "sparse"), (2, "matrix_free"), (3, "matrix_free"),
+                                     (4, "matrix_free"), (2, "stored"), (3, "stored")])
 def test_shards_reproduce_single_device_fista(world, op):
     torch = need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     iters = 60
+    stored = op == "stored"  # stored-residual single kernel (L1B_ITER_RC=0)
+    op = "matrix_free" if stored else op
     inst = l1bench.build_instance(**KW)
     x_ref = np.empty(inst.n)
     tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, op=op), x_ref)
     b_ref = inst.b
-    shards = _shards(world, iters, op)
+    shards = _shards(world, iters, op, stored)
+    assert shards[0].lagged == (op == "matrix_free" and not stored)
     for s in shards:  # the shard's own rows of b are the global b, bit for bit
         a, e = s.inst.info.row_begin, s.inst.info.row_end
         np.testing.assert_array_equal(s.inst.b[: e - a], b_ref[a:e])
@@ -93,6 +103,12 @@ def test_shards_reproduce_single_device_fista(world, op):
         for s in shards:
             s.finalize()
         _exchange(shards, "r_y_win")
+    if shards[0].lagged:  # the last iterate's objective: flush, all-reduce, finalize
+        for s in shards:
+            s.flush()
+        _allreduce(shards)
+        for s in shards:
+            s.finalize()
     torch.cuda.synchronize()
     outs = [s.finish() for s in shards]
     for t, _ in outs[1:]:
