@@ -102,7 +102,9 @@ __device__ __forceinline__ void load_seg(const RcArgs& A, int64_t e, bool full, 
 // (linops.cpp:46-60); INTERIOR: the window is away from both ends, every pair
 // exists.  Entries within S of a window end come out wrong (their partners
 // live outside the window) and are never used.
-template <int S, bool TR, bool INTERIOR, int K>
+// PAR >= 0: bit s is the parity of stage s's offset, fixed at compile time
+// (the generator's alternating offsets); PAR < 0: read from the table.
+template <int S, bool TR, bool INTERIOR, int K, int PAR>
 __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
                                        const StageTab& tab) {
 #pragma unroll
@@ -110,7 +112,8 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
     const int s = TR ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
     const int o = tab.offset[s];
     const double c = tab.c[s], sn = tab.s[s];
-    if ((o & 1) == 0) {
+    const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
+    if (par == 0) {
       const bool p0 = INTERIOR || (e0 >= o && e0 + 1 < n);
       const bool p2 = INTERIOR || (e0 + 2 >= o && e0 + 3 < n);
 #pragma unroll
@@ -152,11 +155,17 @@ struct Acc {
   unsigned nz = 0, mism = 0;  // nnz(x_{k+1}), #(trial != y)
 };
 
+// soft_threshold (solvers.cpp:153-157) with selects instead of branches (same values)
+__device__ __forceinline__ double shrink(double v, double t) {
+  const double a = v - t, c = v + t;
+  return v > t ? a : (v < -t ? c : 0.0);
+}
+
 // One segment.  FAST: the window is away from both ends of [0, n) and of the
 // shard's x windows and the segment owns OWN full entries, so every pair
 // exists and a lane's four entries are either all own (lane_own) or all halo.
 // FLUSH: only ||r_k||^2 of the own rows (the objective of the last iterate).
-template <int S, bool FAST, bool FLUSH>
+template <int S, bool FAST, bool FLUSH, int PAR>
 __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w0, int lane,
                                         bool lane_own, double beta, double inv_l, double thr,
                                         Acc& acc) {
@@ -180,7 +189,7 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
     t[0][i] = d.xk[i];
     if (!FLUSH) t[K - 1][i] = d.xm[i];
   }
-  wchain<S, true, FAST, K>(t, e0, n, A.right);
+  wchain<S, true, FAST, K, PAR>(t, e0, n, A.right);
   double g[1][4], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -193,17 +202,15 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
   }
   acc.rr += rr;
   if (FLUSH) return;
-  wchain<S, false, FAST, 1>(g, e0, n, A.right);
+  wchain<S, false, FAST, 1, PAR>(g, e0, n, A.right);
   double tr[4], l1 = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const double y = d.xk[i] + beta * (d.xk[i] - d.xm[i]);
-    tr[i] = soft_threshold(y - inv_l * g[0][i], thr);
-    if (mine[i]) {
-      l1 += fabs(tr[i]);
-      acc.nz += tr[i] != 0.0;
-      acc.mism += tr[i] != y;
-    }
+    tr[i] = shrink(y - inv_l * g[0][i], thr);
+    l1 += mine[i] ? fabs(tr[i]) : 0.0;
+    acc.nz += (unsigned)(mine[i] & (tr[i] != 0.0));
+    acc.mism += (unsigned)(mine[i] & (tr[i] != y));
   }
   acc.l1 += l1;
   if (FAST) {
@@ -219,7 +226,7 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
 
 // Warps stream segments q = warp_id, warp_id + #warps, ...; the next segment's
 // loads are issued before the current one computes.
-template <int S, int MB, bool FLUSH = false>
+template <int S, int MB, bool FLUSH = false, int PAR = -1>
 __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   using G = RcGeom<S>;
   FistaDev* st = A.b.st;
@@ -243,15 +250,19 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
     const int64_t w0 = w0_of(q);
     load_seg(A, w0 + 4 * lane, full_of(w0), lim_lo, lim_hi, d);
   };
+  // fast segments q in [q_lo, q_hi): the window lies inside the loadable range
+  // and [2, n - 1) -- every pair touching it exists (p >= w0 - 1 >= 1 >= offset,
+  // p + 1 <= w0 + kWin < n) -- and all OWN entries are inside [lo, hi)
+  const int64_t base = lo - G::H3;  // w0 of segment 0
+  const int64_t w_min = max((int64_t)2, lim_lo), w_max = min(lim_hi, n - 1) - kWin;
+  const int64_t q_lo = w_min <= base ? 0 : (w_min - base + G::OWN - 1) / G::OWN;
+  const int64_t q_hi = w_max < base ? 0 : min((w_max - base) / G::OWN + 1, (hi - lo) / G::OWN);
   auto run = [&](int64_t q, const Seg& d) {
     const int64_t w0 = w0_of(q);
-    // every pair touching the window exists (p >= w0 - 1 >= 1 >= offset,
-    // p + 1 <= w0 + kWin < n) and the OWN entries are all inside [lo, hi)
-    const bool fast = full_of(w0) && w0 >= 2 && w0 + kWin < n && w0 + G::H3 + G::OWN <= hi;
-    if (fast)
-      segment<S, true, FLUSH>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+    if (q >= q_lo && q < q_hi)
+      segment<S, true, FLUSH, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
     else
-      segment<S, false, FLUSH>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+      segment<S, false, FLUSH, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
   };
   Seg sa, sb;
   int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
@@ -274,20 +285,20 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   }
 }
 
-template <int S, int MB, bool FLUSH = false>
+template <int S, int MB, bool FLUSH = false, int PAR = -1>
 void launch_rc_v(const RcArgs& a, cudaStream_t st) {
   using G = RcGeom<S>;
   static int grid_cap = 0;
   if (!grid_cap) {
     int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_rc_kernel<S, MB, FLUSH>,
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_rc_kernel<S, MB, FLUSH, PAR>,
                                                           kRcThreads, 0));
     grid_cap = std::min(std::max(1, per_sm) * sm_count(), spmv_grid_max());
   }
   const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
   const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc_kernel<S, MB, FLUSH><<<grid, kRcThreads, 0, st>>>(a);
+  fista_rc_kernel<S, MB, FLUSH, PAR><<<grid, kRcThreads, 0, st>>>(a);
   L1B_LAUNCHED();
 }
 
@@ -301,17 +312,32 @@ int rc_variant() {
   return v;
 }
 
+// offsets (S-1-s) % 2, the generator's alternating stages (bench.cpp:270)
+template <int S>
+constexpr int canon_par() {
+  int m = 0;
+  for (int s = 0; s < S; ++s) m |= ((S - 1 - s) & 1) << s;
+  return m;
+}
+template <int S>
+bool is_canon(const StageTab& t) {
+  for (int s = 0; s < S; ++s)
+    if ((t.offset[s] & 1) != ((S - 1 - s) & 1)) return false;
+  return true;
+}
+
 template <int S>
 void launch_rc(const RcArgs& a, cudaStream_t st) {
+  const bool canon = is_canon<S>(a.right);
   switch (rc_variant()) {
-    case 1: return launch_rc_v<S, 1>(a, st);
-    default: return launch_rc_v<S, 2>(a, st);
+    case 1: return canon ? launch_rc_v<S, 1, false, canon_par<S>()>(a, st) : launch_rc_v<S, 1>(a, st);
+    default: return canon ? launch_rc_v<S, 2, false, canon_par<S>()>(a, st) : launch_rc_v<S, 2>(a, st);
   }
 }
 
 template <int S>
 void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
-  launch_rc_v<S, 2, true>(a, st);
+  launch_rc_v<S, 2, true>(a, st);  // once per solve: the generic stage table
 }
 
 }  // namespace
