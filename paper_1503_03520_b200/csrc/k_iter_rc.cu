@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   Seg sa, sb;
   int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
   if (q < nseg) load(q, sa);
-  // (a two-way unrolled ping-pong without the copy measured slower: code size)
+  // (measured slower: a two-way unrolled ping-pong without the copy -- code
+  // size; an extra L2 bulk prefetch of the segment after next)
   for (; q < nseg; q += stride) {
     if (q + stride < nseg) load(q + stride, sb);
     run(q, sa);
