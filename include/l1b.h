@@ -274,11 +274,24 @@ typedef struct {
   double* r_bufs[3];  /* own + 2*r_halo */
   uint64_t x_halo, r_halo;
   int lagged;
+  /* general = 1: a shard of a non-banded (permuted / left-stage) operator
+   * (l1b_generate with permute or left stages): rows of A split, x split by
+   * columns.  Per iteration: k1 writes this rank's partial A^T r_y to g_full
+   * (n_pad entries); the caller reduce-scatters g_full (rank r keeps entries
+   * [r*n_pad/world, ...)); l1b_session_prox updates the own slice of x_full
+   * (col_begin, col_count entries); the caller all-gathers x_full; k2; the
+   * caller all-reduces scal; finalize.                                      */
+  int general;
+  double* g_full;
+  double* x_full;
+  uint64_t n_pad, col_begin, col_count;
 } l1b_shard_buffers;
 int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
 /* Lagged shard sessions: sums ||r||^2 of the last iterate into scal (a no-op
  * for other sessions; single-device sessions flush inside l1b_session_end). */
 int l1b_session_flush(l1b_session* s);
+/* General shards: prox / momentum on the own columns from the reduced g.     */
+int l1b_session_prox(l1b_session* s);
 int l1b_session_k1(l1b_session* s);
 int l1b_session_k2(l1b_session* s);
 int l1b_session_finalize(l1b_session* s);

@@ -55,7 +55,8 @@ class ProblemInfo(C.Structure):
 class ShardBuffers(C.Structure):
     _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64),
                 ("single", C.c_int), ("x_bufs", vp * 3), ("r_bufs", vp * 3), ("x_halo", u64),
-                ("r_halo", u64), ("lagged", C.c_int)]
+                ("r_halo", u64), ("lagged", C.c_int), ("general", C.c_int), ("g_full", vp),
+                ("x_full", vp), ("n_pad", u64), ("col_begin", u64), ("col_count", u64)]
 
 
 class Cert(C.Structure):
@@ -123,6 +124,7 @@ SIGNATURES = [
     ("l1b_session_k2", C.c_int, [vp]),
     ("l1b_session_finalize", C.c_int, [vp]),
     ("l1b_session_flush", C.c_int, [vp]),
+    ("l1b_session_prox", C.c_int, [vp]),
 ]
 
 

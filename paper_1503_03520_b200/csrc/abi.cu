@@ -178,6 +178,10 @@ struct l1b_problem {
   // halo (it rebuilds r on the rows around its own block)
   double* d_b_win = nullptr;
   uint64_t b_win_lo = 0, b_win_hi = 0;
+  // general (non-banded) shard: rows [row_begin, row_end) of A, x sliced by
+  // columns [col_begin, col_end) of width col_slice (the last slice padded)
+  bool general = false;
+  uint64_t col_begin = 0, col_end = 0, col_slice = 0;
 
   ~l1b_problem() {
     cudaSetDevice(device);
@@ -298,6 +302,15 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
 void materialise(l1b_problem* p) {
   if (p->sparse_built) return;
   p->sparse_built = true;
+  if (p->general) {  // general shard: CSR rows [a, b) (global columns), CSC of that block
+    const uint64_t a = p->row_begin, own = p->row_end - p->row_begin;
+    build_lines(p->view, true, a, own, 0, false, p->stream, &p->csr);
+    p->device_bytes += (p->csr.lines + 1) * (p->csr.ptr32 ? 4 : 8) + p->csr.nnz * 12;
+    build_lines(p->view, false, 0, p->n, a, false, p->stream, &p->csc, a, p->row_end);
+    p->device_bytes += (p->csc.lines + 1) * (p->csc.ptr32 ? 4 : 8) + p->csc.nnz * 12;
+    p->tail_sq = 0.0;  // every row belongs to some block
+    return;
+  }
   if (p->sharded) {  // row-block shard: rows / columns [a, b), window-local indices
     const uint64_t a = p->row_begin, own = p->row_end - p->row_begin;
     build_lines(p->view, true, a, own, a - p->halo, false, p->stream, &p->csr);
@@ -529,6 +542,129 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   if (!g->lazy_sparse) materialise(p.get());
   *out = p.release();
 }
+
+// build_instance (bench.cpp:253-316) + generate_instance (instance.cpp:53-89)
+// of the whole problem on one device (the CSR/CSC copy stays lazy)
+std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
+  if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
+  if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
+  if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
+  if (!(g->tau > 0.0)) throw InvalidArgument("generate_instance: tau must be positive");
+  if (!(g->fill_bound >= 0.0 && g->fill_bound < 1.0))
+    throw InvalidArgument("FillPolicy: interior bound must lie in [0, 1)");
+  const uint64_t n = g->n;
+  const uint64_t m = (uint64_t)std::llround(g->m_ratio * (double)n);
+  const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
+  std::vector<int32_t> r_off, l_off;
+  for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
+  for (uint32_t i = 0; i < g->left_stages; ++i)
+    l_off.push_back((int32_t)((g->left_stages - 1 - i) % 2));
+  // The four seeded streams (P1, P2, sigma, the subgradient fill) are
+  // independent mt19937_64 sequences: realise them on four host threads.
+  std::vector<uint32_t> p1, p2;
+  std::vector<double> sigma(n), gv(n);
+  if (g->permute && m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
+  if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && !g->sigma_explicit)
+    throw InvalidArgument("explicit spectrum without values");
+  if (g->spectrum_kind < L1B_SPECTRUM_UNIFORM_Q || g->spectrum_kind > L1B_SPECTRUM_EXPLICIT)
+    throw InvalidArgument("unknown spectrum kind");
+  {
+    std::vector<std::thread> pool;
+    if (g->permute) {
+      p1.resize(m);
+      p2.resize(m);
+      pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
+      pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
+    }
+    pool.emplace_back([&] {
+      if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+        hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
+                                  hostrng::mix_seed(job_seed, 3), sigma.data());
+      } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+        for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+      } else {
+        std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+      }
+    });
+    pool.emplace_back([&] {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+      for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
+    });
+    for (auto& th : pool) th.join();
+  }
+  auto p = std::make_unique<l1b_problem>();
+  setup_operator(p.get(), device, m, n, r_off, std::vector<double>(g->stages, g->theta), l_off,
+                 std::vector<double>(g->left_stages, g->theta), g->permute ? p1.data() : nullptr,
+                 g->permute ? p2.data() : nullptr, sigma.data());
+  p->tau = g->tau;
+  // planted solution (Rng(mix_seed(job.seed, 4)), bench.cpp:281-301)
+  const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
+  {
+    hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+    hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
+  }
+  // subgradient g: signs on the support (instance.cpp:36-40)
+  for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+  cudaStream_t st = p->stream;
+  // device: w = G (S^T S)^-1 G^T g; e = tau A w; b = A x* + e (instance.cpp:64-79)
+  double *d_g = nullptr, *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;
+  uint32_t* d_sup = nullptr;
+  double* d_val = nullptr;
+  d_g = upload(gv.data(), n, st, nullptr);
+  L1B_CUDA(cudaMalloc(&d_e, m * sizeof(double)));
+  L1B_CUDA(cudaMalloc(&d_x, n * sizeof(double)));
+  L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
+  p->d_b = dev_alloc<double>(m, &p->device_bytes);
+  d_sup = upload(p->xs_sup.data(), s, st, nullptr);
+  d_val = upload(p->xs_val.data(), s, st, nullptr);
+  sweep_gram_inverse(p->view, d_g, d_g, st);
+  sweep_apply(p->view, d_g, d_e, st);
+  scatter_sparse(d_sup, d_val, s, d_x, n, st);
+  sweep_apply(p->view, d_x, p->d_b, st);
+  generator_combine(p->tau, d_e, p->d_b, m, d_ss, st);
+  double ss = 0.0;
+  L1B_CUDA(cudaMemcpyAsync(&ss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  p->noise_norm = std::sqrt(ss);
+  for (void* q : {(void*)d_g, (void*)d_e, (void*)d_x, (void*)d_ss, (void*)d_sup, (void*)d_val})
+    cudaFree(q);
+  band_tail(p.get());
+  return p;
+}
+
+// A general (permuted / left-stage) operator split over `world` devices: every
+// device generates the whole instance (operator description, b, x*), then
+// keeps rows [a, b) of A as CSR (global columns) and the CSC of that row block
+// (local rows); x is sliced by columns for the reduce-scatter / all-gather
+// FISTA of distributed.py.  Row and column cuts on multiples of 16.
+void generate_general_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
+                            l1b_problem** out) {
+  if (sh->rank < 0 || sh->rank >= sh->world) throw InvalidArgument("shard: rank out of range");
+  auto p = generate_whole(device, g);
+  const uint64_t m = p->m, n = p->n, W = (uint64_t)sh->world, r = (uint64_t)sh->rank;
+  uint64_t a = sh->row_begin, b = sh->row_end;
+  if (b == 0) {
+    auto cut = [&](uint64_t q) { return q == W ? m : (m * q / W) / 16 * 16; };
+    a = cut(r);
+    b = cut(r + 1);
+  }
+  if (!(a < b && b <= m)) throw InvalidArgument("shard: empty or out-of-range row block");
+  const uint64_t cs = ((n + W - 1) / W + 15) / 16 * 16;
+  p->sharded = true;
+  p->general = true;
+  p->world = sh->world;
+  p->rank = sh->rank;
+  p->row_begin = a;
+  p->row_end = b;
+  p->col_slice = cs;
+  p->col_begin = std::min(n, r * cs);
+  p->col_end = std::min(n, (r + 1) * cs);
+  p->halo = 0;
+  p->tail_sq = p->tail_sq_band = 0.0;
+  materialise(p.get());
+  *out = p.release();
+}
+
 }  // namespace
 
 extern "C" {
@@ -538,93 +674,15 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
   return guard([&] {
     if (!g || !out) throw InvalidArgument("null argument");
     *out = nullptr;
-    if (shard) {  // row-block shard (world >= 1)
+    if (shard && (g->permute || g->left_stages)) {  // general row-block shard
+      generate_general_shard(device, g, shard, out);
+      return;
+    }
+    if (shard) {  // banded row-block shard (world >= 1)
       generate_shard(device, g, shard, out);
       return;
     }
-    if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
-    if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
-    if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
-    if (!(g->tau > 0.0)) throw InvalidArgument("generate_instance: tau must be positive");
-    if (!(g->fill_bound >= 0.0 && g->fill_bound < 1.0))
-      throw InvalidArgument("FillPolicy: interior bound must lie in [0, 1)");
-    const uint64_t n = g->n;
-    const uint64_t m = (uint64_t)std::llround(g->m_ratio * (double)n);
-    const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
-    std::vector<int32_t> r_off, l_off;
-    for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
-    for (uint32_t i = 0; i < g->left_stages; ++i)
-      l_off.push_back((int32_t)((g->left_stages - 1 - i) % 2));
-    // The four seeded streams (P1, P2, sigma, the subgradient fill) are
-    // independent mt19937_64 sequences: realise them on four host threads.
-    std::vector<uint32_t> p1, p2;
-    std::vector<double> sigma(n), gv(n);
-    if (g->permute && m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
-    if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && !g->sigma_explicit)
-      throw InvalidArgument("explicit spectrum without values");
-    if (g->spectrum_kind < L1B_SPECTRUM_UNIFORM_Q || g->spectrum_kind > L1B_SPECTRUM_EXPLICIT)
-      throw InvalidArgument("unknown spectrum kind");
-    {
-      std::vector<std::thread> pool;
-      if (g->permute) {
-        p1.resize(m);
-        p2.resize(m);
-        pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
-        pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
-      }
-      pool.emplace_back([&] {
-        if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
-          hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
-                                    hostrng::mix_seed(job_seed, 3), sigma.data());
-        } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
-          for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
-        } else {
-          std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
-        }
-      });
-      pool.emplace_back([&] {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
-        hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
-        for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
-      });
-      for (auto& th : pool) th.join();
-    }
-    auto p = std::make_unique<l1b_problem>();
-    setup_operator(p.get(), device, m, n, r_off, std::vector<double>(g->stages, g->theta), l_off,
-                   std::vector<double>(g->left_stages, g->theta), g->permute ? p1.data() : nullptr,
-                   g->permute ? p2.data() : nullptr, sigma.data());
-    p->tau = g->tau;
-    // planted solution (Rng(mix_seed(job.seed, 4)), bench.cpp:281-301)
-    const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
-    {
-      hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
-      hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
-    }
-    // subgradient g: signs on the support (instance.cpp:36-40)
-    for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
-    cudaStream_t st = p->stream;
-    // device: w = G (S^T S)^-1 G^T g; e = tau A w; b = A x* + e (instance.cpp:64-79)
-    double *d_g = nullptr, *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;
-    uint32_t* d_sup = nullptr;
-    double* d_val = nullptr;
-    d_g = upload(gv.data(), n, st, nullptr);
-    L1B_CUDA(cudaMalloc(&d_e, m * sizeof(double)));
-    L1B_CUDA(cudaMalloc(&d_x, n * sizeof(double)));
-    L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
-    p->d_b = dev_alloc<double>(m, &p->device_bytes);
-    d_sup = upload(p->xs_sup.data(), s, st, nullptr);
-    d_val = upload(p->xs_val.data(), s, st, nullptr);
-    sweep_gram_inverse(p->view, d_g, d_g, st);
-    sweep_apply(p->view, d_g, d_e, st);
-    scatter_sparse(d_sup, d_val, s, d_x, n, st);
-    sweep_apply(p->view, d_x, p->d_b, st);
-    generator_combine(p->tau, d_e, p->d_b, m, d_ss, st);
-    double ss = 0.0;
-    L1B_CUDA(cudaMemcpyAsync(&ss, d_ss, sizeof(double), cudaMemcpyDeviceToHost, st));
-    L1B_CUDA(cudaStreamSynchronize(st));
-    p->noise_norm = std::sqrt(ss);
-    for (void* q : {(void*)d_g, (void*)d_e, (void*)d_x, (void*)d_ss, (void*)d_sup, (void*)d_val})
-      cudaFree(q);
-    band_tail(p.get());
+    auto p = generate_whole(device, g);
     if (!g->lazy_sparse) materialise(p.get());
     *out = p.release();
   });
@@ -701,8 +759,8 @@ int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* o) {
     o->halo = p->halo;
     if (p->sharded) {
       o->m_active = p->row_end - p->row_begin;
-      o->col_begin = p->row_begin;
-      o->col_end = p->row_end;
+      o->col_begin = p->general ? p->col_begin : p->row_begin;
+      o->col_end = p->general ? p->col_end : p->row_end;
     }
   });
 }
@@ -711,7 +769,8 @@ int l1b_problem_get_b(const l1b_problem* p, double* b) {
   return guard([&] {
     check_problem(p);
     const uint64_t rows = p->sharded ? p->row_end - p->row_begin : p->m;  // shards: own rows
-    L1B_CUDA(cudaMemcpyAsync(b, p->d_b, rows * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    const double* src = p->general ? p->d_b + p->row_begin : p->d_b;  // general: whole b kept
+    L1B_CUDA(cudaMemcpyAsync(b, src, rows * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
   });
 }
@@ -932,6 +991,10 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   v.row_begin = p->row_begin;
   v.row_end = p->row_end;
   v.halo = p->halo;
+  v.general = p->general;
+  v.col_begin = p->col_begin;
+  v.col_end = p->col_end;
+  v.col_slice = p->col_slice;
   if (p->d_b_win) {
     v.b_win = p->d_b_win - p->b_win_lo;
     v.b_win_lo = p->b_win_lo;

@@ -137,9 +137,12 @@ __device__ __forceinline__ const Line* run_line(const OpView& op, bool rows, uin
   return a;
 }
 
+// keep_lo / keep_hi: only entries whose index (row of a column, column of a
+// row) lies in [keep_lo, keep_hi) -- a general row-block shard's CSC
 __global__ void count_lines(OpView op, bool rows, uint64_t first, uint64_t nlines,
                             uint32_t* counts, unsigned long long* last_nonempty,
-                            unsigned int* max_len, int* overflow) {
+                            unsigned int* max_len, int* overflow, uint64_t keep_lo,
+                            uint64_t keep_hi) {
   Line l0, l1;
   unsigned long long last = 0;
   unsigned int mx = 0;
@@ -153,7 +156,8 @@ __global__ void count_lines(OpView op, bool rows, uint64_t first, uint64_t nline
       continue;
     }
     unsigned int c = 0;
-    for (int e = 0; e < r->cnt; ++e) c += r->val[e] != 0.0;
+    for (int e = 0; e < r->cnt; ++e)
+      c += r->val[e] != 0.0 && r->idx[e] >= keep_lo && r->idx[e] < keep_hi;
     counts[t] = c;
     if (c) {
       last = t + 1;
@@ -167,7 +171,7 @@ __global__ void count_lines(OpView op, bool rows, uint64_t first, uint64_t nline
 template <typename PtrT>
 __global__ void fill_lines(OpView op, bool rows, uint64_t first, uint64_t nlines,
                            const uint64_t* offs, PtrT* ptr, uint32_t* idx, double* val,
-                           uint64_t idx_base) {
+                           uint64_t idx_base, uint64_t keep_lo, uint64_t keep_hi) {
   Line l0, l1;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nlines;
        t += (uint64_t)gridDim.x * blockDim.x) {
@@ -178,7 +182,7 @@ __global__ void fill_lines(OpView op, bool rows, uint64_t first, uint64_t nlines
     if (t + 1 == nlines) ptr[nlines] = (PtrT)offs[nlines];
     if (!ok) continue;
     for (int e = 0; e < r->cnt; ++e) {
-      if (r->val[e] != 0.0) {
+      if (r->val[e] != 0.0 && r->idx[e] >= keep_lo && r->idx[e] < keep_hi) {
         idx[o] = (uint32_t)(r->idx[e] - idx_base);
         val[o++] = r->val[e];
       }
@@ -264,7 +268,8 @@ __global__ void gram_diag_kernel(OpView op, uint64_t first, uint64_t ncols, doub
 // ---------------------------------------------------------------------------
 
 void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, uint64_t idx_base,
-                 bool trim_tail, cudaStream_t st, LinesOut* out) {
+                 bool trim_tail, cudaStream_t st, LinesOut* out, uint64_t keep_lo,
+                 uint64_t keep_hi) {
   if (nlines == 0) throw InvalidArgument("build_lines: empty range");
   uint32_t* counts = nullptr;
   uint64_t* offs = nullptr;
@@ -279,7 +284,7 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
   L1B_CUDA(cudaMemsetAsync(scratch, 0, sizeof(Scratch), st));
   const int grid = grid_for(nlines, 128, 8);
   count_lines<<<grid, 128, 0, st>>>(op, rows, first, nlines, counts, &scratch->last,
-                                    &scratch->max_len, &scratch->overflow);
+                                    &scratch->max_len, &scratch->overflow, keep_lo, keep_hi);
   L1B_LAUNCHED();
   Scratch h;
   L1B_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(Scratch), cudaMemcpyDeviceToHost, st));
@@ -326,10 +331,10 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
   if (keep > 0) {
     if (out->ptr32)
       fill_lines<uint32_t><<<grid, 128, 0, st>>>(op, rows, first, keep, offs, (uint32_t*)out->ptr,
-                                                 out->idx, out->val, idx_base);
+                                                 out->idx, out->val, idx_base, keep_lo, keep_hi);
     else
       fill_lines<uint64_t><<<grid, 128, 0, st>>>(op, rows, first, keep, offs, (uint64_t*)out->ptr,
-                                                 out->idx, out->val, idx_base);
+                                                 out->idx, out->val, idx_base, keep_lo, keep_hi);
     L1B_LAUNCHED();
   } else {
     L1B_CUDA(cudaMemsetAsync(out->ptr, 0, ptr_bytes, st));

@@ -242,6 +242,42 @@ void fista_k2(const Csr& A, const FistaBufs& fb, cudaStream_t st) {
   launch(A, fb.x_gather, e, st);
 }
 
+// General shards: the prox / momentum half of K1 on the own column slice, once
+// the partial A^T r_y of every rank has been reduce-scattered into g (same
+// operations as EpiFistaX::line, solvers.cpp:325-352).
+__global__ void fista_prox_kernel(const double* __restrict__ g, double* x, double* y, uint64_t cols,
+                                  FistaDev* st, double* partials) {
+  if (*(volatile const int*)&st->stop) return;
+  double t_next, beta;
+  fista_momentum(st, &t_next, &beta);
+  const double inv_l = 1.0 / st->lval;
+  const double thr = st->tau * inv_l;
+  double acc[3] = {0.0, 0.0, 0.0};  // ||trial||_1, nnz(trial), #(trial != y)
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < cols;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double yo = y[j], xo = x[j];
+    const double tr = soft_threshold(yo - inv_l * g[j], thr);
+    acc[2] += tr != yo ? 1.0 : 0.0;
+    y[j] = tr + beta * (tr - xo);
+    x[j] = tr;
+    acc[0] += fabs(tr);
+    acc[1] += tr != 0.0 ? 1.0 : 0.0;
+  }
+  double tot[3];
+  if (grid_sum<3>(acc, partials, &st->ticket[0], tot) && threadIdx.x == 0) {
+    st->scal[0] = tot[0];
+    st->scal[1] = tot[1];
+    st->scal[2] = tot[2];
+  }
+}
+
+void fista_prox(const double* g, double* x, double* y, uint64_t cols, FistaDev* st,
+                double* partials, cudaStream_t stream) {
+  fista_prox_kernel<<<grid_for(std::max<uint64_t>(cols, 1)), kThreads, 0, stream>>>(g, x, y, cols, st,
+                                                                                  partials);
+  L1B_LAUNCHED();
+}
+
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st) {
   fista_finalize_kernel<<<1, 1, 0, st>>>(fb.st, fb.trace);
   L1B_LAUNCHED();

@@ -21,9 +21,11 @@ struct LinesOut {
   double* val = nullptr;
 };
 // Lines [first, first + nlines) of A (rows) or A^T (columns = CSC of A).
-// Indices are stored minus idx_base (wrapping), i.e. local to a window.
+// Indices are stored minus idx_base (wrapping), i.e. local to a window; only
+// entries with index in [keep_lo, keep_hi) are kept (a general shard's CSC).
 void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, uint64_t idx_base,
-                 bool trim_tail, cudaStream_t st, LinesOut* out);
+                 bool trim_tail, cudaStream_t st, LinesOut* out, uint64_t keep_lo = 0,
+                 uint64_t keep_hi = ~0ull);
 void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, cudaStream_t st);
 
 // ---- k_sweep.cu (matrix-free, bit-exact vs linops.cpp) ---------------------
@@ -150,6 +152,9 @@ void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
                    bool flush = false);
 int fista_rc_halo(int stages);
+// general shards: prox / momentum on the own column slice from the reduced g
+void fista_prox(const double* g, double* x, double* y, uint64_t cols, FistaDev* st,
+                double* partials, cudaStream_t stream);
 // deferred finalisation (shards): after the caller summed st->scal across ranks
 void fista_finalize_launch(const FistaBufs& fb, cudaStream_t st);
 

@@ -37,6 +37,9 @@ struct l1b_session {
   bool fused = false;   // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
   bool single = false;  // ... as one kernel per iteration (one device): x / r rotate
   bool recompute = false;  // ... with r_k, r_{k-1} rebuilt from x (k_iter_rc.cu): no R buffers
+  bool general = false;    // general row-block shard: reduce-scatter g, all-gather x (distributed.py)
+  double *g_full = nullptr, *x_full = nullptr;  // n_pad = world * col_slice entries each
+  uint64_t n_pad = 0, col_off = 0;              // own slice: [col_off, col_off + nx)
   double* X[3] = {nullptr, nullptr, nullptr};
   double* R[3] = {nullptr, nullptr, nullptr};
   uint64_t xh = 0, rh = 0;  // single-kernel windows: x / r halo widths (shards: H / 2H)
@@ -86,8 +89,8 @@ struct l1b_session {
     b.y = y;
     b.r_x = r_x;
     b.r_y = r_y;
-    b.b = v.b;
-    b.x_gather = shard ? x_win : x;
+    b.b = general ? v.b + v.row_begin : v.b;
+    b.x_gather = general ? x_full : shard ? x_win : x;
     b.r_y_gather = shard ? r_y_win : r_y;
     b.lo = shard ? v.row_begin : 0;
     b.hi = shard ? v.row_end : v.n;
@@ -190,6 +193,30 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     s->y = s->x;
     s->r_x = s->recompute ? nullptr : s->R[0] + s->rh;  // null: init only sums ||b||^2
     s->r_y = s->recompute ? nullptr : s->R[2] + s->rh;
+  } else if (v.general) {
+    // general shard: K1a writes the partial A^T r_y over all columns into
+    // g_full; the caller reduce-scatters it (rank r's slice = entries
+    // [r*cs, (r+1)*cs)); the prox updates the own slice of x_full, which the
+    // caller all-gathers before K2 (CSR rows with global columns)
+    s->general = true;
+    const uint64_t cs = v.col_slice;
+    s->n_pad = (uint64_t)v.world * cs;
+    s->col_off = (uint64_t)v.rank * cs;
+    s->nx = v.col_end - v.col_begin;
+    s->nr = v.row_end - v.row_begin;
+    s->g_full = s->dalloc(s->n_pad);
+    s->x_full = s->dalloc(s->n_pad);
+    L1B_CUDA(cudaMemsetAsync(s->g_full, 0, s->n_pad * 8, st));
+    L1B_CUDA(cudaMemsetAsync(s->x_full, 0, s->n_pad * 8, st));
+    s->x = s->x_full + s->col_off;
+    s->r_y = s->dalloc(s->nr);
+    if (s->accel) {
+      s->y = s->dalloc(cs);
+      s->r_x = s->dalloc(s->nr);
+    } else {
+      s->y = s->x;  // ISTA: base = x (solvers.cpp:317-318)
+      s->r_x = s->r_y;
+    }
   } else if (s->shard) {
     // windows: [halo | own | halo]; K1 writes own x, K2 gathers the x window,
     // K2 writes own r_y, K1 gathers the r_y window
@@ -380,6 +407,21 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->x_halo = s->xh;
     out->r_halo = s->rh;
     out->lagged = s->recompute ? 1 : 0;
+    out->general = s->general ? 1 : 0;
+    out->g_full = s->g_full;
+    out->x_full = s->x_full;
+    out->n_pad = s->n_pad;
+    out->col_begin = s->col_off;
+    out->col_count = s->general ? s->nx : 0;
+  });
+}
+
+int l1b_session_prox(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    if (!s->general) throw LogicError("prox is the middle step of general-shard sessions");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    fista_prox(s->g_full + s->col_off, s->x, s->y, s->nx, s->st, s->partials, s->v.stream);
   });
 }
 
@@ -399,6 +441,8 @@ int l1b_session_k1(l1b_session* s) {
     if (s->single) {  // the whole iteration; k2 is then a no-op
       s->iterate(s->launched, s->v.stream);
       s->launched += 1;
+    } else if (s->general) {  // partial A^T r_y of the own rows, all n columns
+      spmv(s->v.At, s->r_y, s->g_full, s->v.stream);
     } else if (s->fused) {
       fista_fused_k1(*s->v.op, s->bufs(), s->v.stream);
     } else {

@@ -29,6 +29,10 @@ struct ProblemView {
   // shards: b by global row index, valid on [b_win_lo, b_win_hi) (null if absent)
   const double* b_win = nullptr;
   uint64_t b_win_lo = 0, b_win_hi = 0;
+  // general (non-banded) shard: A's rows [row_begin, row_end) as CSR with global
+  // columns + the CSC of that block (local rows); x sliced by columns
+  bool general = false;
+  uint64_t col_begin = 0, col_end = 0, col_slice = 0;
 };
 
 ProblemView problem_view(l1b_problem* p, bool need_sparse = true);

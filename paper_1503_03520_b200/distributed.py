@@ -24,6 +24,14 @@ and in two-kernel mode (CSR/CSC, or matrix-free with > 4 stages):
     exchange x halo    ->  K2: r_x, r_y <- A x - b, momentum    (own rows)
     all-reduce 4 scalars -> finalise
 
+General operators (permuted rows / left stages, SURVEY 8(e) "keep the dense
+allreduce as the general path for permute=true"): rank g owns a row block of
+A (CSR, global columns) and the CSC of that block, x is split by columns:
+
+    K1a: partial A_g^T r_y over all n columns -> reduce-scatter (NCCL) ->
+    prox / momentum on the own column slice -> all-gather x (NCCL) ->
+    K2: r_x, r_y <- A_g x - b_g, momentum -> all-reduce 4 scalars -> finalise
+
 The halo exchanges move a few doubles to each neighbour: they are the
 "all-reduce of the partial A^T r" of the north star carried out in its exact
 sparse form -- the partial A^T r of rank g is nonzero only on columns
@@ -111,7 +119,7 @@ class CudaShard:
         g = N.GenDesc()
         kw = dict(gen_kwargs)
         g.n, g.m_ratio, g.stages = kw["n"], kw.get("m_ratio", 2.0), kw.get("stages", 1)
-        g.left_stages, g.permute = 0, 0
+        g.left_stages, g.permute = kw.get("left_stages", 0), int(kw.get("permute", False))
         g.spectrum_kind, g.q = N.SPECTRUM_UNIFORM_Q, kw.get("q", 1)
         g.shift, g.gamma = kw.get("shift", 0.1), kw.get("gamma", 10.0)
         g.s_divisor, g.tau = kw.get("s_divisor", 128), kw.get("tau", 1.0)
@@ -132,13 +140,19 @@ class CudaShard:
         self.single = bool(b.single)
         self.j = 0  # iterations launched (single mode: buffer rotation)
         self.lagged = bool(b.lagged)
+        self.general = bool(b.general)
+        if self.general:  # non-banded operator: g reduce-scattered, x all-gathered
+            self.n_pad = int(b.n_pad)
+            self.g_full = device_view(b.g_full, self.n_pad, dev)
+            self.x_full = device_view(b.x_full, self.n_pad, dev)
+            self.col_begin, self.col_count = int(b.col_begin), int(b.col_count)
         if self.single:
             self.x_halo, self.r_halo = int(b.x_halo), int(b.r_halo)
             self.x_bufs = [device_view(b.x_bufs[q], self.own + 2 * self.x_halo, dev) for q in range(3)]
             self.r_bufs = None
             if self.r_halo:  # stored-residual kernel; the recomputing one keeps no r
                 self.r_bufs = [device_view(b.r_bufs[q], self.own + 2 * self.r_halo, dev) for q in range(3)]
-        else:
+        elif not self.general:
             self.x_win = device_view(b.x_win, self.own + 2 * self.halo, dev)
             self.r_y_win = device_view(b.r_y_win, self.own + 2 * self.halo, dev)
         self.scal = device_view(b.scal, 4, dev)
@@ -154,6 +168,9 @@ class CudaShard:
 
     def flush(self):
         N.check(self._lib.l1b_session_flush(self.sess._s))
+
+    def prox(self):
+        N.check(self._lib.l1b_session_prox(self.sess._s))
 
     def k1(self):
         N.check(self._lib.l1b_session_k1(self.sess._s))
@@ -201,12 +218,42 @@ def finish_lagged(be, group=None):
         be.finalize()
 
 
+def reduce_scatter_slices(full, rank, world, group=None):
+    """Sum `full` over the ranks; rank r needs only slice r (n_pad / world
+    entries).  NCCL: in-place reduce-scatter; gloo (CPU tests): all-reduce."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return
+    cs = full.numel() // world
+    if dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(full[rank * cs:(rank + 1) * cs], full, group=group)
+    else:
+        dist.all_reduce(full, group=group)
+
+
+def all_gather_slices(full, rank, world, group=None):
+    """Every rank's slice r of `full` to all ranks (in place)."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return
+    cs = full.numel() // world
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, full[rank * cs:(rank + 1) * cs], group=group)
+    else:
+        mine = full[rank * cs:(rank + 1) * cs].clone()
+        dist.all_gather(list(full.split(cs)), mine, group=group)
+
+
 def start(be, group=None):
     """f_0 from the all-reduced ||b_own||^2, then the initial halos."""
     import torch.distributed as dist
 
     dist.all_reduce(be.scal, group=group)
     be.finalize()
+    if getattr(be, "general", False):
+        return
     if be.single:
         halo_exchange_many(be.initial_halos(), be.own, be.rank, be.world, group)
     else:
@@ -216,6 +263,17 @@ def start(be, group=None):
 def fista_iteration(be, group=None):
     import torch.distributed as dist
 
+    if getattr(be, "general", False):
+        # non-banded A: K1a partial A^T r_y over all columns -> reduce-scatter ->
+        # prox on the own columns -> all-gather x -> K2 on the own rows
+        be.k1()
+        reduce_scatter_slices(be.g_full, be.rank, be.world, group)
+        be.prox()
+        all_gather_slices(be.x_full, be.rank, be.world, group)
+        be.k2()
+        dist.all_reduce(be.scal, group=group)
+        be.finalize()
+        return
     if be.single:
         be.k1()  # the whole iteration
         halo_exchange_many(be.next_halos(), be.own, be.rank, be.world, group)

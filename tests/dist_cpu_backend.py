@@ -323,3 +323,118 @@ class CpuShardRc:
     def finish(self):
         q = self.k % 3
         return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()
+
+
+class CpuShardGeneral:
+    """General-operator stand-in (permuted rows): rows [a, b) of A (CSR, global
+    columns) and the CSC of that block; x split by columns in slices of cs
+    (n_pad = world * cs); the driver reduce-scatters g_full and all-gathers
+    x_full (distributed.reduce_scatter_slices / all_gather_slices)."""
+
+    def __init__(self, oracle, inst, rank, world, max_iters):
+        self.rank, self.world, self.single, self.lagged, self.general = rank, world, False, False, True
+        n, m = inst.n, len(inst.b)
+        cut = lambda q: m if q == world else (m * q // world) // 16 * 16  # noqa: E731
+        a, b = cut(rank), cut(rank + 1)
+        cs = ((n + world - 1) // world + 15) // 16 * 16
+        self.n, self.a, self.b_, self.cs = n, a, b, cs
+        self.n_pad = world * cs
+        self.col_begin = rank * cs
+        self.col_count = max(0, min(n, (rank + 1) * cs) - min(n, rank * cs))
+        rp, ri, rv = oracle.csr(inst.op)
+        cp, ci, cv = oracle.csc(inst.op)
+        nrow = len(rp) - 1
+        self.rows = [(ri[rp[i]:rp[i + 1]].astype(np.int64), rv[rp[i]:rp[i + 1]]) if i < nrow else
+                     (np.zeros(0, np.int64), np.zeros(0)) for i in range(a, b)]
+        self.cols = []
+        for j in range(n):
+            idx, val = ci[cp[j]:cp[j + 1]].astype(np.int64), cv[cp[j]:cp[j + 1]]
+            keep = (idx >= a) & (idx < b)
+            self.cols.append((idx[keep] - a, val[keep]))
+        self.g_full = torch.zeros(self.n_pad, dtype=torch.float64)
+        self.x_full = torch.zeros(self.n_pad, dtype=torch.float64)
+        self.y = np.zeros(cs)
+        self.bown = inst.b[a:b].copy()
+        self.r_x = 0.0 - self.bown
+        self.r_y = self.r_x.copy()
+        self.scal = torch.zeros(4, dtype=torch.float64)
+        self.scal[3] = float(np.sum(self.r_x * self.r_x))
+        self.tau, self.L = inst.tau, oracle.gram_lmax(inst.op)
+        self.t, self.k, self.stop, self.init = 1.0, 0, False, False
+        self.max_iters = max_iters
+        self.samples = []
+
+    def _beta(self):
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * self.t * self.t))
+        return t_next, (self.t - 1.0) / t_next
+
+    def k1(self):
+        if self.stop:
+            return
+        g = self.g_full.numpy()
+        g[:] = 0.0
+        for j, (idx, val) in enumerate(self.cols):
+            s = 0.0
+            for q in range(len(idx)):
+                s += val[q] * self.r_y[idx[q]]
+            g[j] = s
+
+    def prox(self):
+        if self.stop:
+            return
+        g, x = self.g_full.numpy(), self.x_full.numpy()
+        _, beta = self._beta()
+        inv_l = 1.0 / self.L
+        thr = self.tau * inv_l
+        l1 = nnz = mism = 0.0
+        for q in range(self.col_count):
+            j = self.col_begin + q
+            yo, xo = self.y[q], x[j]
+            v = yo - inv_l * g[j]
+            tr = v - thr if v > thr else (v + thr if v < -thr else 0.0)
+            mism += tr != yo
+            self.y[q] = tr + beta * (tr - xo)
+            x[j] = tr
+            l1 += abs(tr)
+            nnz += tr != 0.0
+        self.scal[0], self.scal[1], self.scal[2] = l1, nnz, mism
+
+    def k2(self):
+        if self.stop:
+            return
+        x = self.x_full.numpy()
+        _, beta = self._beta()
+        rr = 0.0
+        for i, (idx, val) in enumerate(self.rows):
+            s = 0.0
+            for q in range(len(idx)):
+                s += val[q] * x[idx[q]]
+            rt = s - self.bown[i]
+            self.r_y[i] = (1.0 + beta) * rt - beta * self.r_x[i]
+            self.r_x[i] = rt
+            rr += rt * rt
+        self.scal[3] = rr
+
+    def finalize(self):
+        if self.stop:
+            return
+        sc = self.scal.numpy()
+        if not self.init:
+            self.init = True
+            self.samples.append((0, 0.5 * sc[3]))
+            self.stop = self.max_iters == 0
+            return
+        f = self.tau * sc[0] + 0.5 * sc[3]
+        t_next, _ = self._beta()
+        self.t = t_next
+        self.k += 1
+        self.samples.append((self.k, f))
+        if sc[2] == 0.0 or self.k >= self.max_iters:
+            self.stop = True
+
+    def stopped(self):
+        return self.stop, self.k
+
+    def finish(self):
+        x = self.x_full.numpy()
+        return self.samples, x[self.col_begin:self.col_begin + self.col_count].copy()

@@ -13,6 +13,9 @@ import torch.multiprocessing as mp
 HERE = os.path.dirname(os.path.abspath(__file__))
 ITERS = 40
 KW = dict(n=96, stages=4, q=1, s_divisor=16, seed=3, theta=2 * math.pi / 10)
+# a permuted operator with left stages: not banded -> reduce-scatter / all-gather path
+KW_PERM = dict(n=80, stages=2, left_stages=1, permute=True, q=1, s_divisor=16, seed=5,
+               theta=2 * math.pi / 10)
 
 
 def _free_port():
@@ -29,14 +32,14 @@ def _worker(rank, world, port, out_dir, single):
     sys.path.insert(0, os.path.join(HERE, ".."))
     import torch.distributed as dist
 
-    from dist_cpu_backend import CpuShard, CpuShardRc, CpuShardSingle
+    from dist_cpu_backend import CpuShard, CpuShardGeneral, CpuShardRc, CpuShardSingle
     from paper_1503_03520_b200.distributed import fista_distributed
     from pyoracle import Oracle
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     oracle = Oracle()
-    inst = oracle.build_instance(**KW)
-    cls = {"two": CpuShard, "single": CpuShardSingle, "rc": CpuShardRc}[single]
+    inst = oracle.build_instance(**(KW_PERM if single == "general" else KW))
+    cls = {"two": CpuShard, "single": CpuShardSingle, "rc": CpuShardRc, "general": CpuShardGeneral}[single]
     be = cls(oracle, inst, rank, world, ITERS)
     samples, x_own = fista_distributed(be, ITERS + 5)
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), f=np.array([s[1] for s in samples]),
@@ -46,10 +49,10 @@ def _worker(rank, world, port, out_dir, single):
 
 
 @pytest.mark.parametrize("world,single", [(2, "two"), (3, "two"), (2, "single"), (3, "single"),
-                                          (2, "rc"), (3, "rc")])
+                                          (2, "rc"), (3, "rc"), (2, "general"), (3, "general")])
 def test_sharded_fista_matches_single_process(tmp_path, oracle, world, single):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), single), nprocs=world, join=True)
-    inst = oracle.build_instance(**KW)
+    inst = oracle.build_instance(**(KW_PERM if single == "general" else KW))
     tr, x_ref = oracle.fista(inst, max_iters=ITERS)
     parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     for p in parts[1:]:  # every rank saw the same all-reduced objective trace

@@ -143,3 +143,60 @@ def test_shard_rows_match_global_rows():
         lo, hi = int(gp[a]), int(gp[e])
         np.testing.assert_array_equal(idx.astype(np.int64) + (a - h), gi[lo:hi].astype(np.int64))
         np.testing.assert_array_equal(val, gv[lo:hi])
+
+
+KW_PERM = dict(n=4096, stages=2, left_stages=1, permute=True, q=1, s_divisor=100, seed=6,
+               theta=2 * math.pi / 10)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_general_shards_reproduce_single_device_fista(world):
+    """Permuted operator with a left stage (not banded): row blocks of A,
+    columns of x split; the reduce-scatter of g and the all-gather of x are
+    emulated by sums / copies between the shards' buffers."""
+    torch = need_cuda()
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    iters = 50
+    inst = l1bench.build_instance(**KW_PERM)
+    x_ref = np.empty(inst.n)
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, op="sparse"), x_ref)
+    cfg = l1bench.SolverConfig(max_iters=iters)
+    shards = [CudaShard(KW_PERM, r, world, 0, cfg) for r in range(world)]
+    assert all(s.general for s in shards)
+    b_ref = inst.b
+    for s in shards:  # the shard's rows of b are the global b, bit for bit
+        a, e = s.inst.info.row_begin, s.inst.info.row_end
+        np.testing.assert_array_equal(s.inst.b[: e - a], b_ref[a:e])
+    cs = shards[0].n_pad // world
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    for _ in range(iters):
+        for s in shards:
+            s.k1()
+        tot = sum(s.g_full.clone() for s in shards)  # reduce-scatter (every slice)
+        for s in shards:
+            s.g_full.copy_(tot)
+        for s in shards:
+            s.prox()
+        for src in shards:  # all-gather of the own slices
+            sl = src.x_full[src.rank * cs:(src.rank + 1) * cs]
+            for dst in shards:
+                if dst is not src:
+                    dst.x_full[src.rank * cs:(src.rank + 1) * cs].copy_(sl)
+        for s in shards:
+            s.k2()
+        _allreduce(shards)
+        for s in shards:
+            s.finalize()
+    torch.cuda.synchronize()
+    outs = [s.finish() for s in shards]
+    for t, _ in outs[1:]:
+        np.testing.assert_array_equal(t.objectives(), outs[0][0].objectives())
+    assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
+    x = np.concatenate([o[1] for o in outs])
+    assert x.shape == x_ref.shape
+    assert rel_err(x, x_ref) < 1e-12
+    np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
