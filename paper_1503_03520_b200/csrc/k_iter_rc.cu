@@ -37,6 +37,7 @@
 #include "fista.cuh"
 #include "kernels.hpp"
 
+#include <cooperative_groups.h>
 #include <cstdlib>
 
 namespace l1b {
@@ -67,6 +68,12 @@ __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                : "l"(p));
 }
+// x in the persistent kernel: written by other SMs between grid barriers -> L2 (.cg)
+__device__ __forceinline__ void ld4cg(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
 __device__ __forceinline__ void st4(double* p, const double (&v)[4]) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]),
                "d"(v[3])
@@ -77,20 +84,27 @@ struct Seg {
   double xk[4], xm[4], sg[4], bb[4];
 };
 
-// window group [e, e+4) of every input; entries outside [lim_lo, lim_hi) read 0
+// window group [e, e+4) of every input; entries outside [lim_lo, lim_hi) read 0.
+// COH: x is read through L2 (the persistent kernel rewrites it between barriers).
+template <bool COH = false>
 __device__ __forceinline__ void load_seg(const RcArgs& A, int64_t e, bool full, int64_t lim_lo,
                                          int64_t lim_hi, Seg& s) {
   if (full) {
-    ld4(A.b.x_k + e, s.xk);
-    ld4(A.b.x_km1 + e, s.xm);
+    if (COH) {
+      ld4cg(A.b.x_k + e, s.xk);
+      ld4cg(A.b.x_km1 + e, s.xm);
+    } else {
+      ld4(A.b.x_k + e, s.xk);
+      ld4(A.b.x_km1 + e, s.xm);
+    }
     ld4(A.sigma + e, s.sg);
     ld4(A.b.b + e, s.bb);
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const bool in = e + i >= lim_lo && e + i < lim_hi;
-      s.xk[i] = in ? A.b.x_k[e + i] : 0.0;
-      s.xm[i] = in ? A.b.x_km1[e + i] : 0.0;
+      s.xk[i] = in ? (COH ? __ldcg(A.b.x_k + e + i) : A.b.x_k[e + i]) : 0.0;
+      s.xm[i] = in ? (COH ? __ldcg(A.b.x_km1 + e + i) : A.b.x_km1[e + i]) : 0.0;
       s.sg[i] = in ? A.sigma[e + i] : 0.0;
       s.bb[i] = in ? A.b.b[e + i] : 0.0;
     }
@@ -286,16 +300,109 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   }
 }
 
+// Small instances (C1: n = 2^12, a few warps of work per iteration): the
+// per-kernel cost is launch + grid-reduction latency, not bandwidth.  One
+// cooperative launch then runs up to `iters` iterations back to back, with
+// two grid barriers per iteration (after the sums; after block 0 recorded the
+// iteration), the x buffers rotating as in the one-kernel-per-iteration loop.
+// Same segment code => same iterates.
+struct RcPArgs {
+  RcArgs a;          // a.b.x_* unused: X[] rotate
+  double* X[3];      // global-index views of the three x buffers
+  uint64_t j0, iters;
+};
+
+template <int S, int PAR>
+__global__ void __launch_bounds__(kRcThreads, 2) fista_rc_persistent(RcPArgs P) {
+  namespace cg = cooperative_groups;
+  using G = RcGeom<S>;
+  cg::grid_group grid = cg::this_grid();
+  RcArgs A = P.a;
+  FistaDev* st = A.b.st;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool lane_own = 4 * lane >= G::H3 && 4 * lane < G::H3 + G::OWN;
+  const int64_t n = A.n, lo = A.lo, hi = A.hi;
+  const int64_t lim_lo = max((int64_t)0, lo - G::H3), lim_hi = min(n, hi + G::H3);
+  const int64_t nseg = (hi - lo + G::OWN - 1) / G::OWN;
+  const int64_t stride = (int64_t)gridDim.x * kRcWarps;
+  const int64_t base = lo - G::H3;
+  const int64_t w_min = max((int64_t)2, lim_lo), w_max = min(lim_hi, n - 1) - kWin;
+  const int64_t q_lo = w_min <= base ? 0 : (w_min - base + G::OWN - 1) / G::OWN;
+  const int64_t q_hi = w_max < base ? 0 : min((w_max - base) / G::OWN + 1, (hi - lo) / G::OWN);
+  for (uint64_t it = 0; it < P.iters; ++it) {
+    if (*(volatile int*)&st->stop) break;  // uniform: read after the last barrier
+    const uint64_t j = P.j0 + it;
+    A.b.x_k = P.X[j % 3];
+    A.b.x_km1 = P.X[(j + 2) % 3];
+    A.b.x_next = P.X[(j + 1) % 3];
+    const double beta = __ldcg(&st->beta_y);
+    const double inv_l = 1.0 / __ldcg(&st->lval);
+    const double thr = __ldcg(&st->tau) * inv_l;
+    Acc acc;
+    for (int64_t q = (int64_t)blockIdx.x * kRcWarps + warp; q < nseg; q += stride) {
+      const int64_t w0 = base + q * G::OWN;
+      Seg d;
+      load_seg<true>(A, w0 + 4 * lane, w0 >= lim_lo && w0 + kWin <= lim_hi, lim_lo, lim_hi, d);
+      if (q >= q_lo && q < q_hi)
+        segment<S, true, false, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+      else
+        segment<S, false, false, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+    }
+    double sums[4] = {acc.l1, (double)acc.nz, (double)acc.mism, acc.rr};
+    block_sum<4>(sums);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) A.b.partials[(size_t)blockIdx.x * 4 + k] = sums[k];
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {  // fixed-order fold of the block partials, then the record
+      double tot[4] = {0.0, 0.0, 0.0, 0.0};
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) tot[k] += __ldcg(&A.b.partials[(size_t)b * 4 + k]);
+      }
+      block_sum<4>(tot);
+      if (threadIdx.x == 0) {
+        st->scal[0] = tot[0];
+        st->scal[1] = tot[1];
+        st->scal[2] = tot[2];
+        st->scal[3] = tot[3];
+        fista_finalize_lagged(st, A.b.trace, false);
+      }
+    }
+    grid.sync();
+  }
+}
+
+// co-resident CTAs of a kernel, once per process (the first query also loads
+// the kernel's module: fista_rc_prepare calls it before the timed loop)
+template <auto K>
+int grid_cap_of() {
+  static const int cap = [] {
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, kRcThreads, 0));
+    return std::min(std::max(1, per_sm) * sm_count(), spmv_grid_max());
+  }();
+  return cap;
+}
+
+template <int S, int PAR>
+void launch_rc_persistent(const RcPArgs& p, cudaStream_t st) {
+  const int grid_cap = grid_cap_of<fista_rc_persistent<S, PAR>>();
+  using G = RcGeom<S>;
+  const int64_t nseg = (p.a.hi - p.a.lo + G::OWN - 1) / G::OWN;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nseg + kRcWarps - 1) / kRcWarps, grid_cap));
+  RcPArgs a = p;
+  void* args[] = {&a};
+  L1B_CUDA(cudaLaunchCooperativeKernel((const void*)fista_rc_persistent<S, PAR>, dim3(grid),
+                                       dim3(kRcThreads), args, 0, st));
+  L1B_LAUNCHED();
+}
+
 template <int S, int MB, bool FLUSH = false, int PAR = -1>
 void launch_rc_v(const RcArgs& a, cudaStream_t st) {
   using G = RcGeom<S>;
-  static int grid_cap = 0;
-  if (!grid_cap) {
-    int per_sm = 0;
-    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_rc_kernel<S, MB, FLUSH, PAR>,
-                                                          kRcThreads, 0));
-    grid_cap = std::min(std::max(1, per_sm) * sm_count(), spmv_grid_max());
-  }
+  const int grid_cap = grid_cap_of<fista_rc_kernel<S, MB, FLUSH, PAR>>();
   const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
   const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
@@ -342,6 +449,50 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+template <int S>
+void prepare_s(const StageTab& t) {
+  if (is_canon<S>(t)) {
+    grid_cap_of<fista_rc_kernel<S, 2, false, canon_par<S>()>>();
+    grid_cap_of<fista_rc_persistent<S, canon_par<S>()>>();
+  } else {
+    grid_cap_of<fista_rc_kernel<S, 2, false, -1>>();
+    grid_cap_of<fista_rc_persistent<S, -1>>();
+  }
+  grid_cap_of<fista_rc_kernel<S, 2, true, -1>>();
+}
+
+void fista_rc_prepare(const OpView& op) {
+  switch (op.right.count) {
+    case 1: return prepare_s<1>(op.right);
+    case 2: return prepare_s<2>(op.right);
+    case 3: return prepare_s<3>(op.right);
+    case 4: return prepare_s<4>(op.right);
+    default: return;
+  }
+}
+
+void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[3], uint64_t j0,
+                   uint64_t iters, uint64_t lo, uint64_t hi, cudaStream_t st) {
+  if (lo % 4 != 0) throw std::invalid_argument("fista_rc_loop: block start must be a multiple of 4");
+  RcPArgs p;
+  p.a.n = (int64_t)op.n;
+  p.a.lo = (int64_t)lo;
+  p.a.hi = (int64_t)hi;
+  p.a.right = op.right;
+  p.a.sigma = op.sigma;
+  p.a.b = ib;
+  for (int q = 0; q < 3; ++q) p.X[q] = X[q];
+  p.j0 = j0;
+  p.iters = iters;
+  switch (op.right.count) {
+    case 1: return is_canon<1>(op.right) ? launch_rc_persistent<1, canon_par<1>()>(p, st) : launch_rc_persistent<1, -1>(p, st);
+    case 2: return is_canon<2>(op.right) ? launch_rc_persistent<2, canon_par<2>()>(p, st) : launch_rc_persistent<2, -1>(p, st);
+    case 3: return is_canon<3>(op.right) ? launch_rc_persistent<3, canon_par<3>()>(p, st) : launch_rc_persistent<3, -1>(p, st);
+    case 4: return is_canon<4>(op.right) ? launch_rc_persistent<4, canon_par<4>()>(p, st) : launch_rc_persistent<4, -1>(p, st);
+    default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
+  }
+}
 
 int fista_rc_halo(int stages) {
   switch (stages) {

@@ -152,6 +152,13 @@ void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
                    bool flush = false);
 int fista_rc_halo(int stages);
+// `iters` iterations j0, j0+1, ... of the same kernel in ONE cooperative launch
+// (grid barriers between iterations; x rotates through X[j % 3]) -- small
+// instances, where a launch per iteration costs more than the iteration.
+void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[3], uint64_t j0,
+                   uint64_t iters, uint64_t lo, uint64_t hi, cudaStream_t st);
+// loads the recomputing kernels and sizes their grids (outside the timed loop)
+void fista_rc_prepare(const OpView& op);
 // general shards: prox / momentum on the own column slice from the reduced g
 void fista_prox(const double* g, double* x, double* y, uint64_t cols, FistaDev* st,
                 double* partials, cudaStream_t stream);

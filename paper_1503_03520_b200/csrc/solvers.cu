@@ -270,14 +270,34 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.init_tail = s->single ? v.tail_sq_band : 0.0;  // the init kernel covers rows [0, nr)
   h.lagged = s->recompute ? 1 : 0;
   *s->h_st = h;
+  if (s->recompute) fista_rc_prepare(*v.op);  // module load + grid sizing before t0
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
   s->t0 = std::chrono::steady_clock::now();
   // residuals over all (own) rows: rows >= m_active keep r = -b for the whole run
   fista_init(s->bufs(), s->nr, st);  // (single: writes r_0 into R[0] and R[2])
 }
 
+// Small single-device instances run a whole chunk of iterations in one
+// cooperative launch (k_iter_rc.cu fista_rc_loop); L1B_PERSIST=0 disables.
+constexpr uint64_t kPersistMaxN = 1ull << 20;
+
+bool persist_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("L1B_PERSIST");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
+  if (s->recompute && !s->shard && s->v.n <= kPersistMaxN && iters > 1 && persist_enabled()) {
+    fista_rc_loop(*s->v.op, s->iter_bufs(s->launched), s->X, s->launched, iters, 0, s->v.n,
+                  s->v.stream);
+    s->launched += iters;
+    return;
+  }
   for (uint64_t i = 0; i < iters; ++i) {
     if (s->single) {
       s->iterate(s->launched + i, s->v.stream);
@@ -564,11 +584,18 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       run_newton_cg(p, cfg, samples, cap, summary, x_host, d_x);
       return;
     }
-    l1b_session s;
-    session_begin(p, cfg, &s);
-    cudaStream_t st = v.stream;
+    // host-side setup before session_begin: the device clock of the trace
+    // starts in its init kernel
     int* h_flags = nullptr;
     L1B_CUDA(cudaMallocHost(&h_flags, 2 * sizeof(int)));
+    l1b_session s;
+    try {
+      session_begin(p, cfg, &s);
+    } catch (...) {
+      cudaFreeHost(h_flags);
+      throw;
+    }
+    cudaStream_t st = v.stream;
     cudaEvent_t ev[2];
     L1B_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     L1B_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
