@@ -15,8 +15,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "solvers.hpp"
 #include "spmv.cuh"
@@ -230,6 +233,180 @@ __global__ void pcg_direction_kernel(const double* __restrict__ r, const double*
   }
 }
 
+// -- PCG in one cooperative launch (small / medium n) -------------------------
+// At C3 (n = 2^19) the four PCG kernels run 10-20 us each while the data of
+// an iteration (~40 MB) sits in L2: the iteration is latency-bound.  This
+// kernel runs the whole pcg_solve loop with four grid barriers per iteration;
+// every block folds the per-block partials itself (same order everywhere, so
+// all blocks take identical decisions) and block 0 writes the state back.
+// Per-element formulas and line sums (ascending, from 0.0) are those of
+// Ka..Kd; only the grouping of the three dot products differs.
+struct PcgArgs {
+  const void* a_ptr;
+  const uint32_t* a_idx;
+  const double* a_val;
+  uint64_t a_lines;
+  const void* t_ptr;
+  const uint32_t* t_idx;
+  const double* t_val;
+  uint64_t n;
+  const double *pre, *d2psi;
+  double *p, *hav, *hp, *r, *step, *best;
+  NcgDev* st;
+  double* partials;
+};
+
+template <int NS>
+__device__ __forceinline__ void fold_partials(const double* partials, double (&tot)[NS]) {
+#pragma unroll
+  for (int k = 0; k < NS; ++k) tot[k] = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) tot[k] += __ldcg(&partials[(size_t)b * NS + k]);
+  }
+  block_sum<NS>(tot);
+  __shared__ double bc[NS];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) bc[k] = tot[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NS; ++k) tot[k] = bc[k];
+  __syncthreads();
+}
+
+template <typename PtrT>
+__global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  NcgDev* st = P.st;
+  const PtrT* ap = static_cast<const PtrT*>(P.a_ptr);
+  const PtrT* tp = static_cast<const PtrT*>(P.t_ptr);
+  const uint64_t gsz = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const double tau = st->tau, eta = st->eta, rhs_norm = st->rhs_norm;
+  const uint64_t max_iters = st->max_iters;
+  double rz = st->rz, best_norm = st->best_norm, php = 0.0, alpha = 0.0, beta = 0.0, rn = 0.0;
+  int done = st->done, converged = st->converged, negcurv = 0, error = 0;
+  uint64_t it = 0;
+  while (!done) {
+    // Ka: hav = A p
+    for (uint64_t i = t0; i < P.a_lines; i += gsz) {
+      double sum = 0.0;
+      for (PtrT q = ap[i]; q < ap[i + 1]; ++q) sum += P.a_val[q] * __ldcg(P.p + P.a_idx[q]);
+      P.hav[i] = sum;
+    }
+    grid.sync();
+    // Kb: hp = A^T hav + tau d2psi p (solvers.cpp:537-541), p.hp
+    {
+      double acc[1] = {0.0};
+      for (uint64_t j = t0; j < P.n; j += gsz) {
+        double g = 0.0;
+        for (PtrT q = tp[j]; q < tp[j + 1]; ++q) g += P.t_val[q] * __ldcg(P.hav + P.t_idx[q]);
+        const double pj = __ldcg(P.p + j);
+        const double h = g + tau * P.d2psi[j] * pj;
+        P.hp[j] = h;
+        acc[0] += pj * h;
+      }
+      block_sum<1>(acc);
+      if (threadIdx.x == 0) P.partials[blockIdx.x] = acc[0];
+    }
+    grid.sync();
+    {
+      double tot[1];
+      fold_partials<1>(P.partials, tot);
+      php = tot[0];  // solvers.cpp:231-237
+    }
+    if (!(php > 0.0)) {
+      if (!isfinite(php)) error = 1;
+      negcurv = 1;
+      done = 1;
+      break;
+    }
+    alpha = rz / php;
+    grid.sync();  // partials are reused below
+    // Kc: step += alpha p; r -= alpha hp (:238-241); ||r||^2, r.z
+    {
+      double acc[2] = {0.0, 0.0};
+      for (uint64_t i = t0; i < P.n; i += gsz) {
+        P.step[i] += alpha * __ldcg(P.p + i);
+        const double ri = P.r[i] - alpha * __ldcg(P.hp + i);
+        P.r[i] = ri;
+        acc[0] += ri * ri;
+        acc[1] += ri * (ri / P.pre[i]);
+      }
+      block_sum<2>(acc);
+      if (threadIdx.x == 0) {
+        P.partials[(size_t)blockIdx.x * 2] = acc[0];
+        P.partials[(size_t)blockIdx.x * 2 + 1] = acc[1];
+      }
+    }
+    grid.sync();
+    double tot[2];
+    fold_partials<2>(P.partials, tot);
+    rn = sqrt(tot[0]);
+    ++it;
+    int improved = 0;
+    if (!isfinite(rn)) {
+      error = 2;
+      done = 1;
+      break;
+    }
+    if (rn < best_norm) {
+      best_norm = rn;
+      improved = 1;
+    }
+    if (rn <= eta * rhs_norm) {
+      converged = 1;
+      done = 1;
+    } else {
+      beta = tot[1] / rz;
+      rz = tot[1];
+      if (it >= max_iters) done = 1;
+    }
+    // Kd: best = step when improved (:245-248); p = z + beta p (:259)
+    for (uint64_t i = t0; i < P.n; i += gsz) {
+      if (improved) P.best[i] = P.step[i];
+      if (!done) P.p[i] = P.r[i] / P.pre[i] + beta * P.p[i];
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rz = rz;
+    st->php = php;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rn = rn;
+    st->best_norm = best_norm;
+    st->iterations = it;
+    st->done = 1;
+    st->converged = converged;
+    st->negcurv = negcurv;
+    st->error = error;
+    st->improved = 0;
+  }
+}
+
+// grid of the cooperative PCG loop (0: not applicable -> the four-kernel loop)
+template <typename PtrT>
+int pcg_loop_grid() {
+  static const int cap = [] {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_loop_kernel<PtrT>, kThreads, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    // all co-resident CTAs (measured at C3: 1/2/4/8 per SM -> 49/31/27/27 us per
+    // PCG iteration); L1B_PCG_BPS caps it for experiments
+    const char* e = getenv("L1B_PCG_BPS");
+    const int bps = e ? std::min(per_sm, std::max(1, atoi(e))) : per_sm;
+    return std::min(bps * sm_count(), spmv_grid_max());
+  }();
+  return cap;
+}
+
 // -- line search (solvers.cpp:551-560): eight trials per pass ---------------
 __global__ void ls_eval_kernel(const double* __restrict__ x, const double* __restrict__ s,
                                const double* __restrict__ r, const double* __restrict__ ad,
@@ -348,6 +525,13 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
     h->eta = cfg->eta;
     h->max_iters = cfg->pcg_max_iters;
     L1B_CUDA(cudaMemcpyAsync(dst, h, sizeof(NcgDev), cudaMemcpyHostToDevice, st));
+    // cooperative PCG loop for small / medium n (L1B_PERSIST=0: four kernels)
+    int coop_grid = 0;
+    {
+      const char* e = getenv("L1B_PERSIST");
+      if (!(e && e[0] == '0') && n <= (1ull << 21) && v.A.ptr32 == v.At.ptr32)
+        coop_grid = v.A.ptr32 ? pcg_loop_grid<uint32_t>() : pcg_loop_grid<uint64_t>();
+    }
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] {
       return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -416,6 +600,16 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
       pcg_init_kernel<<<grid_for(n), kThreads, 0, st>>>(grad, pre, rp, pp, step, best, n, dst, partials);
       L1B_LAUNCHED();
       uint64_t launched = 0, chunk = 4;
+      if (coop_grid > 0) {  // the whole solve in one cooperative launch
+        PcgArgs pa{v.A.ptr, v.A.idx, v.A.val, v.A.lines, v.At.ptr, v.At.idx, v.At.val, n,
+                   pre, d2psi, pp, hav, hp, rp, step, best, dst, partials};
+        void* args[] = {&pa};
+        const void* fn = v.A.ptr32 ? (const void*)pcg_loop_kernel<uint32_t>
+                                   : (const void*)pcg_loop_kernel<uint64_t>;
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(coop_grid), dim3(kThreads), args, 0, st));
+        L1B_LAUNCHED();
+        launched = cfg->pcg_max_iters;  // skip the four-kernel loop
+      }
       while (launched < cfg->pcg_max_iters) {
         const uint64_t k = std::min<uint64_t>(chunk, cfg->pcg_max_iters - launched);
         for (uint64_t it = 0; it < k; ++it) {
