@@ -260,18 +260,20 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
     bufs.push_back((void*)*ptr);
   };
-  uint32_t* h_coords = nullptr;
+  uint32_t* h_coords = nullptr;  // two chunk buffers: generate one while the other uploads
   CdDev* h_st = nullptr;
+  cudaEvent_t uploaded[2] = {nullptr, nullptr};
   try {
     alloc(&x, n * 8);
     alloc(&r, v.m * 8);
     alloc(&delta, n * 8);
     alloc(&stamp, n * 4);
     alloc(&partials, (size_t)spmv_grid_max() * 4 * 8);
-    alloc(&d_coords, chunk * per_epoch * B * 4);
+    alloc(&d_coords, 2 * chunk * per_epoch * B * 4);
     alloc(&dst, sizeof(CdDev));
     alloc(&trace, tcap * sizeof(CdSample));
-    L1B_CUDA(cudaMallocHost(&h_coords, chunk * per_epoch * B * 4));
+    L1B_CUDA(cudaMallocHost(&h_coords, 2 * chunk * per_epoch * B * 4));
+    for (auto& e : uploaded) L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     L1B_CUDA(cudaMallocHost(&h_st, sizeof(CdDev)));
     L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
     L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
@@ -296,16 +298,11 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     uint64_t draw_block = 0, launched = 0;
     uint32_t stamp_base = 0;
     bool time_out = false;
-    while (launched < cfg->max_iters) {
-      L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
-      L1B_CUDA(cudaStreamSynchronize(st));
-      if (h_st->stop) break;
-      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
-        time_out = true;
-        break;
-      }
-      const uint64_t ep = std::min<uint64_t>(chunk, cfg->max_iters - launched);
-      // coordinate stream for `ep` epochs (host: mt19937_64 is sequential)
+    // coordinate stream (host: mt19937_64 is sequential), one chunk of epochs
+    // at a time into buffer `slot`; the next chunk is drawn while the device
+    // runs this one, so the host RNG is off the critical path
+    auto draw = [&](uint64_t ep, int slot) {
+      uint32_t* out = h_coords + (uint64_t)slot * chunk * per_epoch * B;
       uint64_t k = 0;
       for (uint64_t e = 0; e < ep; ++e)
         for (uint64_t bl = 0; bl < per_epoch; ++bl) {
@@ -320,12 +317,25 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
               } while (seen[i] == draw_block);
               seen[i] = draw_block;
             }
-            h_coords[k++] = (uint32_t)i;
+            out[k++] = (uint32_t)i;
           }
         }
-      L1B_CUDA(cudaMemcpyAsync(d_coords, h_coords, k * 4, cudaMemcpyHostToDevice, st));
+      return k;
+    };
+    int slot = 0;
+    uint64_t ep = std::min<uint64_t>(chunk, cfg->max_iters);
+    uint64_t k = ep ? draw(ep, slot) : 0;
+    while (launched < cfg->max_iters) {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
+        time_out = true;
+        break;
+      }
+      L1B_CUDA(cudaMemcpyAsync(d_coords + (uint64_t)slot * chunk * per_epoch * B,
+                               h_coords + (uint64_t)slot * chunk * per_epoch * B, k * 4,
+                               cudaMemcpyHostToDevice, st));
+      L1B_CUDA(cudaEventRecord(uploaded[slot], st));
       for (uint64_t e = 0; e < ep; ++e) {
-        const uint32_t* c = d_coords + e * per_epoch * B;
+        const uint32_t* c = d_coords + (slot * chunk + e) * per_epoch * B;
         if (v.At.ptr32 && v.A.ptr32)
           launch_epoch<uint32_t, uint32_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
         else if (v.At.ptr32)
@@ -342,6 +352,18 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
         L1B_LAUNCHED();
       }
       launched += ep;
+      L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
+      // draw the next chunk while the device works (its buffer's last upload
+      // must have left the host first)
+      const uint64_t ep_next = std::min<uint64_t>(chunk, cfg->max_iters - launched);
+      slot ^= 1;
+      if (ep_next) {
+        L1B_CUDA(cudaEventSynchronize(uploaded[slot]));
+        k = draw(ep_next, slot);
+      }
+      L1B_CUDA(cudaStreamSynchronize(st));
+      if (h_st->stop) break;
+      ep = ep_next;
     }
     L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
     L1B_CUDA(cudaStreamSynchronize(st));
@@ -395,12 +417,15 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     for (void* q : bufs) cudaFree(q);
     if (h_coords) cudaFreeHost(h_coords);
     if (h_st) cudaFreeHost(h_st);
+    for (auto e : uploaded)
+      if (e) cudaEventDestroy(e);
     throw;
   }
   cudaStreamSynchronize(st);
   for (void* q : bufs) cudaFree(q);
   cudaFreeHost(h_coords);
   cudaFreeHost(h_st);
+  for (auto e : uploaded) cudaEventDestroy(e);
 }
 
 }  // namespace l1b
