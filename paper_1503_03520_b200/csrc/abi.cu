@@ -985,6 +985,7 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   v.op = &p->view;
   v.gram = nullptr;
   v.max_row_nnz = p->csr.max_len;
+  v.max_col_nnz = p->csc.max_len;
   v.world = p->world;
   v.shard = p->sharded;
   v.rank = p->rank;

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <vector>
@@ -129,6 +130,195 @@ __global__ void __launch_bounds__(1024) cd_epoch_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Planned epochs (columns of <= KC and rows of <= KR entries: k <= 2 stages,
+// C2).  The epoch kernel above walks the CSC / CSR and the stamp / delta
+// arrays through L2 for every block: ~8 dependent round trips per block.  The
+// static part of that walk (column entries, and for each touched row its
+// columns with A(rho, c) as stored in column c) only depends on the drawn
+// coordinates, so one parallel pass per chunk writes it as a per-slot record
+// (structure of arrays); the epoch kernel then prefetches the next block's
+// records, reads r and x once per block, and resolves "which block columns
+// moved" through a shared-memory hash of (column -> delta).  Same operations
+// in the same order as cd_epoch_kernel: identical iterates.
+struct Plan {
+  uint32_t* i;   // coordinate
+  double* l;     // L_i
+  uint32_t* nc;  // column length
+  uint32_t* row; // [KC][S] column rows (ascending)
+  double* val;   // [KC][S] column values
+  uint32_t* nr;  // [KC][S] row lengths
+  uint32_t* rc;  // [KC][KR][S] row columns (ascending)
+  double* rv;    // [KC][KR][S] A(row, col) as stored in the column
+  uint64_t S;    // slots (stride of the per-entry arrays)
+};
+
+template <int KC, int KR, typename CP, typename RP>
+__global__ void cd_plan_kernel(const uint32_t* __restrict__ coords, uint64_t count,
+                               const CP* __restrict__ cptr, const uint32_t* __restrict__ crow,
+                               const double* __restrict__ cval, const RP* __restrict__ rptr,
+                               const uint32_t* __restrict__ rcol, const double* __restrict__ lips,
+                               Plan P) {
+  const uint64_t S = P.S;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < count;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = coords[s];
+    P.i[s] = i;
+    P.l[s] = lips[i];
+    uint32_t e = 0;
+    for (CP p = cptr[i]; p < cptr[i + 1] && e < KC; ++p, ++e) {
+      const uint32_t rho = crow[p];
+      P.row[e * S + s] = rho;
+      P.val[e * S + s] = cval[p];
+      uint32_t f = 0;
+      for (RP q = rptr[rho]; q < rptr[rho + 1] && f < KR; ++q, ++f) {
+        const uint32_t c = rcol[q];
+        double v = 0.0;
+        for (CP pc = cptr[c]; pc < cptr[c + 1]; ++pc)
+          if (crow[pc] == rho) {
+            v = cval[pc];
+            break;
+          }
+        P.rc[((uint64_t)e * KR + f) * S + s] = c;
+        P.rv[((uint64_t)e * KR + f) * S + s] = v;
+      }
+      P.nr[e * S + s] = f;
+    }
+    P.nc[s] = e;
+  }
+}
+
+constexpr int kHash = 1024;  // >= 2 B: the planned path takes B <= 512
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t hslot(uint32_t c) { return (c * 2654435761u) >> 22; }  // 10 bits
+
+__device__ __forceinline__ void h_insert(uint32_t* keys, double* vals, uint32_t c, double d) {
+  uint32_t h = hslot(c);
+  while (atomicCAS(&keys[h], kEmpty, c) != kEmpty) h = (h + 1) & (kHash - 1);
+  vals[h] = d;
+}
+__device__ __forceinline__ double h_find(const uint32_t* keys, const double* vals, uint32_t c) {
+  uint32_t h = hslot(c);
+  for (;;) {
+    const uint32_t k = keys[h];
+    if (k == c) return vals[h];
+    if (k == kEmpty) return 0.0;
+    h = (h + 1) & (kHash - 1);
+  }
+}
+
+template <int KC, int KR>
+struct Rec {
+  uint32_t i, nc, row[KC], nr[KC], rc[KC][KR];
+  double l, val[KC], rv[KC][KR];
+};
+
+template <int KC, int KR>
+__device__ __forceinline__ void load_rec(const Plan& P, uint64_t s, Rec<KC, KR>& R) {
+  const uint64_t S = P.S;
+  R.i = P.i[s];
+  R.l = P.l[s];
+  R.nc = P.nc[s];
+#pragma unroll
+  for (int e = 0; e < KC; ++e) {
+    R.row[e] = P.row[e * S + s];
+    R.val[e] = P.val[e * S + s];
+    R.nr[e] = P.nr[e * S + s];
+#pragma unroll
+    for (int f = 0; f < KR; ++f) {
+      R.rc[e][f] = P.rc[((uint64_t)e * KR + f) * S + s];
+      R.rv[e][f] = P.rv[((uint64_t)e * KR + f) * S + s];
+    }
+  }
+}
+
+template <int KC, int KR>
+__global__ void __launch_bounds__(512) cd_epoch_plan_kernel(Plan P, uint64_t slot0, uint64_t nblocks,
+                                                             int B, double* x, double* r, CdDev* st) {
+  if (*(volatile int*)&st->stop) return;
+  __shared__ uint32_t keys[2][kHash];
+  __shared__ double vals[2][kHash];
+  const double beta = st->beta, tau = st->tau;
+  const int t = threadIdx.x;
+  for (int k = t; k < 2 * kHash; k += blockDim.x) (&keys[0][0])[k] = kEmpty;
+  unsigned long long applied = 0, colops = 0;
+  Rec<KC, KR> cur, nxt;
+  if (t < B && nblocks) load_rec(P, slot0 + t, cur);
+  __syncthreads();
+  for (uint64_t blk = 0; blk < nblocks; ++blk) {
+    const int T = (int)(blk & 1);
+    if (t < B && blk + 1 < nblocks) load_rec(P, slot0 + (blk + 1) * (uint64_t)B + t, nxt);
+    double d = 0.0, rval[KC];
+    if (t < B && cur.l != 0.0) {  // zero columns are skipped (solvers.cpp:455)
+      const uint32_t i = cur.i;
+#pragma unroll
+      for (int e = 0; e < KC; ++e) rval[e] = e < (int)cur.nc ? __ldcg(r + cur.row[e]) : 0.0;
+      const double xi = __ldcg(x + i);
+      double gi = 0.0;
+#pragma unroll
+      for (int e = 0; e < KC; ++e)
+        if (e < (int)cur.nc) gi += cur.val[e] * rval[e];
+      ++colops;
+      const double scale = beta * cur.l;
+      const double xn = soft_threshold(xi - gi / scale, tau / scale);
+      d = xn - xi;
+      if (d != 0.0) {
+        x[i] = xn;
+        ++applied;
+        ++colops;
+        h_insert(keys[T], vals[T], i, d);
+      }
+    }
+    __syncthreads();
+    if (d != 0.0) {
+      const uint32_t i = cur.i;
+#pragma unroll
+      for (int e = 0; e < KC; ++e) {
+        if (e >= (int)cur.nc) break;
+        // owner = smallest block column with a non-zero step touching the row
+        bool owner = true;
+#pragma unroll
+        for (int f = 0; f < KR; ++f) {
+          if (f >= (int)cur.nr[e]) break;
+          const uint32_t c = cur.rc[e][f];
+          if (c >= i) break;
+          if (h_find(keys[T], vals[T], c) != 0.0) {
+            owner = false;
+            break;
+          }
+        }
+        if (!owner) continue;
+        double acc = rval[e];
+#pragma unroll
+        for (int f = 0; f < KR; ++f) {
+          if (f >= (int)cur.nr[e]) break;
+          const uint32_t c = cur.rc[e][f];
+          const double dc = c == i ? d : h_find(keys[T], vals[T], c);
+          if (dc == 0.0) continue;
+          acc += dc * cur.rv[e][f];
+        }
+        r[cur.row[e]] = acc;
+      }
+    }
+    // the other table was last used by block blk - 1 (done) and is next used
+    // by block blk + 1 (after the barrier below)
+    for (int k = t; k < kHash; k += blockDim.x) keys[T ^ 1][k] = kEmpty;
+    __syncthreads();
+    if (t < B) cur = nxt;
+  }
+  __shared__ unsigned long long s_app, s_col;
+  if (t == 0) s_app = s_col = 0;
+  __syncthreads();
+  atomicAdd(&s_app, applied);
+  atomicAdd(&s_col, colops);
+  __syncthreads();
+  if (t == 0) {
+    st->applied = s_app;
+    st->colops = s_col;
+  }
+}
+
 // r -= b after the matrix-free refresh r = A x (solvers.cpp:473-474): the
 // sweep path is the reference's own OperatorSpec::apply, so the residual (and
 // hence every later coordinate decision) matches the reference bit for bit.
@@ -215,6 +405,29 @@ void launch_epoch(const ProblemView& v, const uint32_t* coords, uint64_t nblocks
   L1B_LAUNCHED();
 }
 
+template <int KC, int KR>
+void plan_and_run(const ProblemView& v, const uint32_t* coords, uint64_t count, const double* lips,
+                  Plan P, cudaStream_t st) {
+  const int grid = grid_for(count);
+  if (v.At.ptr32 && v.A.ptr32)
+    cd_plan_kernel<KC, KR, uint32_t, uint32_t><<<grid, kThreads, 0, st>>>(
+        coords, count, (const uint32_t*)v.At.ptr, v.At.idx, v.At.val, (const uint32_t*)v.A.ptr,
+        v.A.idx, lips, P);
+  else if (v.At.ptr32)
+    cd_plan_kernel<KC, KR, uint32_t, uint64_t><<<grid, kThreads, 0, st>>>(
+        coords, count, (const uint32_t*)v.At.ptr, v.At.idx, v.At.val, (const uint64_t*)v.A.ptr,
+        v.A.idx, lips, P);
+  else if (v.A.ptr32)
+    cd_plan_kernel<KC, KR, uint64_t, uint32_t><<<grid, kThreads, 0, st>>>(
+        coords, count, (const uint64_t*)v.At.ptr, v.At.idx, v.At.val, (const uint32_t*)v.A.ptr,
+        v.A.idx, lips, P);
+  else
+    cd_plan_kernel<KC, KR, uint64_t, uint64_t><<<grid, kThreads, 0, st>>>(
+        coords, count, (const uint64_t*)v.At.ptr, v.At.idx, v.At.val, (const uint64_t*)v.A.ptr,
+        v.A.idx, lips, P);
+  L1B_LAUNCHED();
+}
+
 uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {  // rng.hpp:37-45
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
   uint64_t x;
@@ -250,6 +463,14 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
   cudaStream_t st = v.stream;
 
   double *x = nullptr, *r = nullptr, *delta = nullptr, *partials = nullptr;
+  // planned epochs for short columns / rows (k <= 2 stages); L1B_PCDM_PLAN=0: off
+  int plan_k = 0;
+  {
+    const char* e = getenv("L1B_PCDM_PLAN");
+    if (!(e && e[0] == '0') && v.max_col_nnz <= 4 && v.max_row_nnz <= 4 && B <= 512)
+      plan_k = (v.max_col_nnz <= 2 && v.max_row_nnz <= 2) ? 2 : 4;
+  }
+  Plan plan{};
   uint32_t *stamp = nullptr, *d_coords = nullptr;
   CdDev* dst = nullptr;
   CdSample* trace = nullptr;
@@ -270,6 +491,18 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     alloc(&stamp, n * 4);
     alloc(&partials, (size_t)spmv_grid_max() * 4 * 8);
     alloc(&d_coords, 2 * chunk * per_epoch * B * 4);
+    if (plan_k) {
+      const uint64_t S = chunk * per_epoch * B, K = (uint64_t)plan_k;
+      plan.S = S;
+      alloc(&plan.i, S * 4);
+      alloc(&plan.l, S * 8);
+      alloc(&plan.nc, S * 4);
+      alloc(&plan.row, K * S * 4);
+      alloc(&plan.val, K * S * 8);
+      alloc(&plan.nr, K * S * 4);
+      alloc(&plan.rc, K * K * S * 4);
+      alloc(&plan.rv, K * K * S * 8);
+    }
     alloc(&dst, sizeof(CdDev));
     alloc(&trace, tcap * sizeof(CdSample));
     L1B_CUDA(cudaMallocHost(&h_coords, 2 * chunk * per_epoch * B * 4));
@@ -334,9 +567,22 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
                                h_coords + (uint64_t)slot * chunk * per_epoch * B, k * 4,
                                cudaMemcpyHostToDevice, st));
       L1B_CUDA(cudaEventRecord(uploaded[slot], st));
+      if (plan_k == 2)
+        plan_and_run<2, 2>(v, d_coords + (uint64_t)slot * chunk * per_epoch * B, k, lips, plan, st);
+      else if (plan_k == 4)
+        plan_and_run<4, 4>(v, d_coords + (uint64_t)slot * chunk * per_epoch * B, k, lips, plan, st);
       for (uint64_t e = 0; e < ep; ++e) {
         const uint32_t* c = d_coords + (slot * chunk + e) * per_epoch * B;
-        if (v.At.ptr32 && v.A.ptr32)
+        const int threads = std::min(1024, std::max(32, (int)(B + 31) / 32 * 32));
+        if (plan_k == 2) {
+          cd_epoch_plan_kernel<2, 2><<<1, threads, 0, st>>>(plan, e * per_epoch * B, per_epoch, (int)B,
+                                                            x, r, dst);
+          L1B_LAUNCHED();
+        } else if (plan_k == 4) {
+          cd_epoch_plan_kernel<4, 4><<<1, threads, 0, st>>>(plan, e * per_epoch * B, per_epoch, (int)B,
+                                                            x, r, dst);
+          L1B_LAUNCHED();
+        } else if (v.At.ptr32 && v.A.ptr32)
           launch_epoch<uint32_t, uint32_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);
         else if (v.At.ptr32)
           launch_epoch<uint32_t, uint64_t>(v, c, per_epoch, (int)B, lips, x, r, stamp, delta, stamp_base, dst);

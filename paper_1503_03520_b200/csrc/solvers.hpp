@@ -21,6 +21,7 @@ struct ProblemView {
   const OpView* op = nullptr;
   const double* gram = nullptr;
   uint64_t max_row_nnz = 0;  // omega of solvers.cpp:401-410 (max nnz over rows)
+  uint64_t max_col_nnz = 0;
   // row-block shard (world > 1): own rows == own columns [row_begin, row_end);
   // A / At index x / r windows that start `halo` entries before row_begin
   int world = 1, rank = 0;
