@@ -97,16 +97,25 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def kernel_bytes(path, n, m_act, nnz, ptr_bytes):
-    """Algorithmic HBM bytes per launch of the two FISTA kernels (DESIGN.md
-    section 4): every array at its stored width, each element once."""
+# matrix-free kernels by l1b_session_kernel_mode: (bytes per launch / n, iterations
+# per launch, name); every array at its stored width, each element once
+MF_KERNELS = {
+    4: (48, 2, "fista_rc2 (two FISTA iterations per launch, matrix-free, residuals recomputed): "
+               "x_k, x_{k-1}, sigma, b read, x_{k+1}, x_{k+2} written"),
+    3: (40, 1, "fista_rc (one FISTA iteration, matrix-free, residuals recomputed): x_k, x_{k-1}, "
+               "sigma, b read, x_{k+1} written"),
+    2: (64, 1, "fista_iter (one FISTA iteration, matrix-free, stored residuals)"),
+}
+
+
+def kernel_bytes(path, n, m_act, nnz, ptr_bytes, kmode=None):
+    """Algorithmic HBM bytes per launch of the FISTA kernels and iterations per launch."""
     if path == "matrix_free":
-        # one kernel per iteration, residuals recomputed from x (k_iter_rc.cu
-        # fista_rc_kernel): x_k, x_{k-1}, sigma, b read; x_{k+1} written
-        return 40 * n, 0
+        per_n, ipl, _ = MF_KERNELS[kmode]
+        return per_n * n, 0, ipl
     k1 = 12 * nnz + ptr_bytes * (n + 1) + 8 * m_act + 32 * n      # CSC + r_y gather + x,y r/w
     k2 = 12 * nnz + ptr_bytes * (m_act + 1) + 8 * n + 32 * m_act  # CSR + x gather + b, r_x r/w, r_y w
-    return k1, k2
+    return k1, k2, 1
 
 
 def time_path(inst, op, args, prof_iters=400):
@@ -131,20 +140,27 @@ def time_path(inst, op, args, prof_iters=400):
     launches = l1bench.launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     kms = sess.profile(prof_iters)
+    kmode = sess.kernel_mode()
     sess.end()
     return {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
-            "k1_ms": kms[0] / prof_iters, "k2_ms": kms[1] / prof_iters, "launches": int(launches)}
+            "k1_ms": kms[0] / prof_iters, "k2_ms": kms[1] / prof_iters, "launches": int(launches),
+            "kmode": kmode}
 
 
 def roofline(path, t, info, peak, peak_src):
     n, nnz = int(info.n), int(info.nnz)
     m_act = n  # banded: rows >= n are empty
     ptr_bytes = 4 if nnz < (1 << 32) else 8
-    b1, b2 = kernel_bytes(path, n, m_act, nnz, ptr_bytes)
-    names = {"matrix_free": ("fista_rc (whole FISTA iteration, matrix-free, residuals recomputed)", "-"),
-             "sparse": ("fista_k1 (A^T r_y + prox/momentum, CSC)",
-                        "fista_k2 (A x - b + residual momentum, CSR)")}[path]
-    dom = (b1, t["k1_ms"], names[0], "k1") if t["k1_ms"] >= t["k2_ms"] else (b2, t["k2_ms"], names[1], "k2")
+    b1, b2, ipl = kernel_bytes(path, n, m_act, nnz, ptr_bytes, t.get("kmode"))
+    if path == "matrix_free":
+        names = (MF_KERNELS[t["kmode"]][2], "-")
+        key1 = {4: "rc2", 3: "k1", 2: "stored"}[t["kmode"]]
+    else:
+        names = ("fista_k1 (A^T r_y + prox/momentum, CSC)", "fista_k2 (A x - b + residual momentum, CSR)")
+        key1 = "k1"
+    # per-launch time = per-iteration kernel time x iterations per launch
+    dom = ((b1, t["k1_ms"] * ipl, names[0], key1) if t["k1_ms"] >= t["k2_ms"] else
+           (b2, t["k2_ms"], names[1], "k2"))
     achieved = dom[0] / (dom[1] * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -155,8 +171,9 @@ def roofline(path, t, info, peak, peak_src):
             traffic = None
     return {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak,
             "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-            "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0], "traffic": traffic,
-                    "hbm_gbs_ax_atr": (b1 + b2) / ((t["k1_ms"] + t["k2_ms"]) * 1e-3) / 1e9}
+            "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0], "iterations_per_launch": ipl,
+            "launch_ms": dom[1], "traffic": traffic,
+            "hbm_gbs_ax_atr": (b1 + b2) / ((t["k1_ms"] * ipl + t["k2_ms"]) * 1e-3) / 1e9}
 
 
 def run_reference(args):
@@ -263,12 +280,14 @@ def main():
         "config": {"workload": f"C4 FISTA: n=2^{int(math.log2(info.n))} cols x m=2^{int(math.log2(info.m))} rows, "
                                f"4 stages, nnz={info.nnz}, q=1, s=n/1000, tau=1, seed 3",
                    "l2": "inputs larger than L2 (no flush needed)", "parallelism": "single GPU",
-                   "path": "one matrix-free kernel per FISTA iteration: r_k, r_{k-1} recomputed from "
-                           "x_k, x_{k-1} (Givens stages in registers + warp shuffles, 256-bit loads), "
-                           "40n bytes/iteration; iterates bit-identical to the reference's fista_run"},
+                   "path": ("matrix-free, residuals recomputed from x (Givens stages in registers + "
+                            "warp shuffles, 256-bit loads); " +
+                            ("two FISTA iterations per launch, 24n bytes/iteration" if fused["kmode"] == 4
+                             else "one FISTA iteration per launch") +
+                            "; iterates bit-identical to the reference's fista_run")},
         "gpu_launches": fused["launches"],
         "hbm_gbs_ax_atr": rf["hbm_gbs_ax_atr"],
-        "kernels_ms": {"fista_rc": fused["k1_ms"]},
+        "kernels_ms_per_iteration": {"matrix_free": fused["k1_ms"]},
         "roofline": rf,
         "sparse_path": {"value": sparse["ips"], "ms_per_step": sparse["ms_step"],
                         "kernels_ms": {"fista_k1": sparse["k1_ms"], "fista_k2": sparse["k2_ms"]},

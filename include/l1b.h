@@ -260,8 +260,8 @@ typedef struct {
   double* scal;     /* 4 doubles: ||x||_1, nnz(x), #(trial != y), ||r||^2 -- sum over ranks */
   uint64_t own, halo;
   /* single-kernel mode (matrix-free, 1..4 stages): l1b_session_k1 runs iteration
-   * j+1 from x_j = x_bufs[j%3], x_{j-1} = x_bufs[(j+2)%3] (same for r) into
-   * x_bufs[(j+1)%3] / r_bufs[(j+1)%3]; the caller then exchanges the halos of
+   * j+1 from x_j = x_bufs[j%P], x_{j-1} = x_bufs[(j+P-1)%P] (r: period 3) into
+   * x_bufs[(j+1)%P] / r_bufs[(j+1)%3], P = x_nbufs; the caller then exchanges the halos of
    * those two (x_halo / r_halo entries each side); l1b_session_k2 is a no-op.
    * Before the first iteration r_bufs[0] and r_bufs[2] need their halos.
    * lagged = 1 (recomputing kernel, k_iter_rc.cu): no residual buffers
@@ -270,10 +270,11 @@ typedef struct {
    * the NEXT finalize; after the loop: l1b_session_flush, all-reduce scal,
    * l1b_session_finalize records the last iterate. */
   int single;
-  double* x_bufs[3];  /* own + 2*x_halo */
+  double* x_bufs[4];  /* own + 2*x_halo; x_nbufs of them rotate (x_j = x_bufs[j % x_nbufs]) */
   double* r_bufs[3];  /* own + 2*r_halo */
   uint64_t x_halo, r_halo;
   int lagged;
+  int x_nbufs;      /* 3, or 4 when lagged */
   /* general = 1: a shard of a non-banded (permuted / left-stage) operator
    * (l1b_generate with permute or left stages): rows of A split, x split by
    * columns.  Per iteration: k1 writes this rank's partial A^T r_y to g_full
@@ -292,6 +293,19 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
 int l1b_session_flush(l1b_session* s);
 /* General shards: prox / momentum on the own columns from the reduced g.     */
 int l1b_session_prox(l1b_session* s);
+/* Which FISTA kernels a session runs (bench roofline bookkeeping):
+ * bytes per iteration 288n-class CSR/CSC pair, 96n matrix-free pair, 64n
+ * stored-residual single kernel, 40n recomputing kernel, 24n two-iteration
+ * recomputing kernel (one device), general-shard CSR/CSC.                   */
+enum {
+  L1B_KMODE_SPARSE = 0,
+  L1B_KMODE_MATRIX_FREE_PAIR = 1,
+  L1B_KMODE_STORED_RESIDUAL = 2,
+  L1B_KMODE_RECOMPUTE = 3,
+  L1B_KMODE_RECOMPUTE_TWO = 4,
+  L1B_KMODE_GENERAL_SHARD = 5
+};
+int l1b_session_kernel_mode(l1b_session* s, int* mode);
 int l1b_session_k1(l1b_session* s);
 int l1b_session_k2(l1b_session* s);
 int l1b_session_finalize(l1b_session* s);

@@ -52,10 +52,16 @@ class ProblemInfo(C.Structure):
                 ("csc_lanes", C.c_int), ("world", C.c_int), ("rank", C.c_int), ("halo", u64)]
 
 
+# l1b_session_kernel_mode (include/l1b.h)
+KMODE_SPARSE, KMODE_MATRIX_FREE_PAIR, KMODE_STORED_RESIDUAL = 0, 1, 2
+KMODE_RECOMPUTE, KMODE_RECOMPUTE_TWO, KMODE_GENERAL_SHARD = 3, 4, 5
+
+
 class ShardBuffers(C.Structure):
     _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64),
-                ("single", C.c_int), ("x_bufs", vp * 3), ("r_bufs", vp * 3), ("x_halo", u64),
-                ("r_halo", u64), ("lagged", C.c_int), ("general", C.c_int), ("g_full", vp),
+                ("single", C.c_int), ("x_bufs", vp * 4), ("r_bufs", vp * 3), ("x_halo", u64),
+                ("r_halo", u64), ("lagged", C.c_int), ("x_nbufs", C.c_int), ("general", C.c_int),
+                ("g_full", vp),
                 ("x_full", vp), ("n_pad", u64), ("col_begin", u64), ("col_count", u64)]
 
 
@@ -125,6 +131,7 @@ SIGNATURES = [
     ("l1b_session_finalize", C.c_int, [vp]),
     ("l1b_session_flush", C.c_int, [vp]),
     ("l1b_session_prox", C.c_int, [vp]),
+    ("l1b_session_kernel_mode", C.c_int, [vp, P(C.c_int)]),
 ]
 
 

@@ -79,4 +79,39 @@ __device__ inline void fista_finalize_lagged(FistaDev* st, FistaSample* trace, b
   st->pend_valid = 1;
 }
 
+// Lagged bookkeeping after a two-iteration kernel (iterations j+1, j+2 from
+// x_j, x_{j-1}): records iteration j (stashed sums + ||r_j||^2) and, unless
+// that stopped the loop, iteration j+1 (all its sums are in scal8); then the
+// momentum for the next kernel and x_{j+2}'s sums are stashed.  The kernel
+// itself used beta_y for x_{j+1} and the next step of the t-sequence for
+// x_{j+2}; both steps are committed here.  Same values and order of checks as
+// two fista_finalize_lagged calls.
+__device__ inline void fista_finalize_lagged2(FistaDev* st, FistaSample* trace) {
+  const double* q = st->scal8;
+  const uint64_t ts = global_timer_ns();
+  if (st->pend_valid) {
+    const double f = st->tau * st->pend[0] + 0.5 * (q[0] + st->tail_sq);
+    st->pend_valid = 0;
+    fista_record(st, trace, st->k + 1, f, st->pend[1], st->pend[2] == 0.0, st->pend_ts);
+    if (st->stop) return;
+  }
+  double t_next, beta;
+  fista_momentum(st, &t_next, &beta);  // the step the kernel used for x_{j+2}
+  st->beta_y = beta;
+  if (st->accel) st->t = t_next;
+  {
+    const double f = st->tau * q[1] + 0.5 * (q[4] + st->tail_sq);
+    fista_record(st, trace, st->k + 1, f, q[2], q[3] == 0.0, ts);
+    if (st->stop) return;
+  }
+  fista_momentum(st, &t_next, &beta);
+  st->beta_y = beta;
+  if (st->accel) st->t = t_next;
+  st->pend[0] = q[5];
+  st->pend[1] = q[6];
+  st->pend[2] = q[7];
+  st->pend_ts = ts;
+  st->pend_valid = 1;
+}
+
 }  // namespace l1b

@@ -95,6 +95,9 @@ struct FistaDev {
   int pend_valid;
   int lagged;    // the recomputing kernel: fista_finalize_lagged
   int flushing;  // set by its flush launch (deferred finalize records, then stops stashing)
+  // two-iteration kernel: ||r_k||^2, (l1, nnz, mism) of x_{k+1}, ||r_{k+1}||^2,
+  // (l1, nnz, mism) of x_{k+2}
+  double scal8[8];
 };
 
 struct FistaBufs {
@@ -155,8 +158,12 @@ int fista_rc_halo(int stages);
 // `iters` iterations j0, j0+1, ... of the same kernel in ONE cooperative launch
 // (grid barriers between iterations; x rotates through X[j % 3]) -- small
 // instances, where a launch per iteration costs more than the iteration.
-void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[3], uint64_t j0,
+void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uint64_t j0,
                    uint64_t iters, uint64_t lo, uint64_t hi, cudaStream_t st);
+// two iterations (x_{k+1} into ib.x_next, x_{k+2} into x_next2) in one kernel:
+// 24n bytes per iteration (k_iter_rc.cu fista_rc2_kernel); one device
+void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
+                    cudaStream_t st);
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op);
 // general shards: prox / momentum on the own column slice from the reduced g

@@ -40,7 +40,8 @@ struct l1b_session {
   bool general = false;    // general row-block shard: reduce-scatter g, all-gather x (distributed.py)
   double *g_full = nullptr, *x_full = nullptr;  // n_pad = world * col_slice entries each
   uint64_t n_pad = 0, col_off = 0;              // own slice: [col_off, col_off + nx)
-  double* X[3] = {nullptr, nullptr, nullptr};
+  double* X[4] = {nullptr, nullptr, nullptr, nullptr};
+  int nbuf = 3;  // x rotation period: 4 for the recomputing kernels (two-iteration launches)
   double* R[3] = {nullptr, nullptr, nullptr};
   uint64_t xh = 0, rh = 0;  // single-kernel windows: x / r halo widths (shards: H / 2H)
   uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
@@ -54,18 +55,19 @@ struct l1b_session {
   std::chrono::steady_clock::time_point t0;
   bool time_out = false;
 
-  // launch j computes iteration j+1 from x_j (X[j%3]) and x_{j-1} (X[(j+2)%3])
+  // launch j computes iteration j+1 from x_j (X[j%P]) and x_{j-1} (X[(j+P-1)%P]), P = nbuf
   IterBufs iter_bufs(uint64_t j) const {
     // global-index views: window entry xh + (g - lo) holds global entry g
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
     auto gx = [&](double* p) { return p + (int64_t)xh - lo; };
     auto gr = [&](double* p) { return p + (int64_t)rh - lo; };
     IterBufs ib;
-    ib.x_k = gx(X[j % 3]);
-    ib.x_km1 = gx(X[(j + 2) % 3]);
+    const uint64_t P = (uint64_t)nbuf;
+    ib.x_k = gx(X[j % P]);
+    ib.x_km1 = gx(X[(j + P - 1) % P]);
     ib.r_k = recompute ? nullptr : gr(R[j % 3]);
     ib.r_km1 = recompute ? nullptr : gr(R[(j + 2) % 3]);
-    ib.x_next = gx(X[(j + 1) % 3]);
+    ib.x_next = gx(X[(j + 1) % P]);
     ib.r_next = recompute ? nullptr : gr(R[(j + 1) % 3]);
     ib.b = recompute && shard ? v.b_win : v.b - lo;
     ib.st = st;
@@ -75,6 +77,13 @@ struct l1b_session {
   }
 
   // launch j of the single-kernel loop (iteration j + 1)
+  // launches j and j+1 as one two-iteration kernel (recomputing path, one device)
+  void iterate2(uint64_t j, cudaStream_t stream) const {
+    const int64_t lo = shard ? (int64_t)v.row_begin : 0;
+    fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
+                   shard ? v.row_end : v.n, stream);
+  }
+
   void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
     const uint64_t lo = shard ? v.row_begin : 0, hi = shard ? v.row_end : v.n;
     if (recompute)
@@ -182,7 +191,8 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     s->xh = s->shard ? (s->recompute ? (uint64_t)fista_rc_halo(v.op->right.count) : H) : 0;
     s->rh = s->shard && !s->recompute ? 2 * H : 0;
     s->halo = s->xh;
-    for (int q = 0; q < 3; ++q) {
+    s->nbuf = s->recompute ? 4 : 3;
+    for (int q = 0; q < s->nbuf; ++q) {
       s->X[q] = s->dalloc(s->nx + 2 * s->xh);
       L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
       if (s->recompute) continue;
@@ -290,11 +300,36 @@ bool persist_enabled() {
   return on != 0;
 }
 
+// Large single-device instances run two iterations per launch (24n instead
+// of 40n bytes per iteration); L1B_RC2=0 keeps one per launch.
+bool rc2_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("L1B_RC2");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
+// `iters` single-device recomputing iterations as two-iteration launches (+ one
+// single launch for an odd count); returns false when the session is not one
+bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
+  if (!(s->recompute && !s->shard && rc2_enabled())) return false;
+  uint64_t i = 0;
+  for (; i + 2 <= iters; i += 2) s->iterate2(s->launched + i, st);
+  if (i < iters) s->iterate(s->launched + i, st);
+  return true;
+}
+
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
   if (s->recompute && !s->shard && s->v.n <= kPersistMaxN && iters > 1 && persist_enabled()) {
     fista_rc_loop(*s->v.op, s->iter_bufs(s->launched), s->X, s->launched, iters, 0, s->v.n,
                   s->v.stream);
+    s->launched += iters;
+    return;
+  }
+  if (step_pairs(s, iters, s->v.stream)) {
     s->launched += iters;
     return;
   }
@@ -329,7 +364,7 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   if (kept)
     L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
                              cudaMemcpyDeviceToHost, st));
-  const double* xf = s->single ? s->X[h.k % 3] + s->xh : s->x;  // x after the last executed iteration
+  const double* xf = s->single ? s->X[h.k % (uint64_t)s->nbuf] + s->xh : s->x;  // x after the last executed iteration
   if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, xf, s->nx * 8, cudaMemcpyDeviceToHost, st));
   if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, xf, s->nx * 8, cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaStreamSynchronize(st));
@@ -420,10 +455,9 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->own = s->nx;
     out->halo = s->halo;
     out->single = s->single ? 1 : 0;
-    for (int q = 0; q < 3; ++q) {
-      out->x_bufs[q] = s->X[q];
-      out->r_bufs[q] = s->R[q];
-    }
+    for (int q = 0; q < 4; ++q) out->x_bufs[q] = s->X[q];
+    for (int q = 0; q < 3; ++q) out->r_bufs[q] = s->R[q];
+    out->x_nbufs = s->nbuf;
     out->x_halo = s->xh;
     out->r_halo = s->rh;
     out->lagged = s->recompute ? 1 : 0;
@@ -433,6 +467,17 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->n_pad = s->n_pad;
     out->col_begin = s->col_off;
     out->col_count = s->general ? s->nx : 0;
+  });
+}
+
+int l1b_session_kernel_mode(l1b_session* s, int* mode) {
+  return guard([&] {
+    if (!s || !mode) throw InvalidArgument("null argument");
+    *mode = s->general ? L1B_KMODE_GENERAL_SHARD
+            : !s->single ? (s->fused ? L1B_KMODE_MATRIX_FREE_PAIR : L1B_KMODE_SPARSE)
+            : !s->recompute ? L1B_KMODE_STORED_RESIDUAL
+            : (!s->shard && rc2_enabled()) ? L1B_KMODE_RECOMPUTE_TWO
+                                           : L1B_KMODE_RECOMPUTE;
   });
 }
 
@@ -511,6 +556,35 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     std::vector<cudaEvent_t> ev(3 * iters);
     for (auto& e : ev) L1B_CUDA(cudaEventCreate(&e));
     const FistaBufs b = s->bufs();
+    // two-iteration launches, timed each -- where session_step uses them too
+    // (small instances step through the cooperative loop: single iterations)
+    if (s->recompute && !s->shard && rc2_enabled() &&
+        !(s->v.n <= kPersistMaxN && persist_enabled())) {
+      uint64_t i = 0;
+      for (; i < iters; i += 2) {
+        L1B_CUDA(cudaEventRecord(ev[3 * i], st));
+        if (i + 2 <= iters)
+          s->iterate2(s->launched + i, st);
+        else
+          s->iterate(s->launched + i, st);
+        L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
+        L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
+      }
+      s->launched += iters;
+      L1B_CUDA(cudaStreamSynchronize(st));
+      double k1 = 0.0, k2 = 0.0;  // k2: the empty second slot, as in single-kernel mode
+      for (i = 0; i < iters; i += 2) {
+        float a = 0.f, c = 0.f;
+        L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+        L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));
+        k1 += a;
+        k2 += c;
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+      ms_out[0] = k1;
+      ms_out[1] = k2;
+      return;
+    }
     for (uint64_t i = 0; i < iters; ++i) {
       L1B_CUDA(cudaEventRecord(ev[3 * i], st));
       if (s->single)

@@ -148,7 +148,8 @@ class CudaShard:
             self.col_begin, self.col_count = int(b.col_begin), int(b.col_count)
         if self.single:
             self.x_halo, self.r_halo = int(b.x_halo), int(b.r_halo)
-            self.x_bufs = [device_view(b.x_bufs[q], self.own + 2 * self.x_halo, dev) for q in range(3)]
+            self.nbuf = int(b.x_nbufs)  # x_j lives in x_bufs[j % nbuf]
+            self.x_bufs = [device_view(b.x_bufs[q], self.own + 2 * self.x_halo, dev) for q in range(self.nbuf)]
             self.r_bufs = None
             if self.r_halo:  # stored-residual kernel; the recomputing one keeps no r
                 self.r_bufs = [device_view(b.r_bufs[q], self.own + 2 * self.r_halo, dev) for q in range(3)]
@@ -160,7 +161,7 @@ class CudaShard:
 
     # single-kernel mode: windows to exchange after iteration j / before the first
     def next_halos(self):
-        q = self.j % 3
+        q = self.j % self.nbuf
         return [(self.x_bufs[q], self.x_halo)] + ([(self.r_bufs[q], self.r_halo)] if self.r_bufs else [])
 
     def initial_halos(self):

@@ -540,6 +540,12 @@ class Session:
         N.check(_lib().l1b_session_profile(self._s, int(iters), ms, 2))
         return [ms[0], ms[1]]
 
+    def kernel_mode(self) -> int:
+        """N.KMODE_* of the FISTA kernels this session runs."""
+        m = C.c_int()
+        N.check(_lib().l1b_session_kernel_mode(self._s, C.byref(m)))
+        return int(m.value)
+
     def sync(self):
         stopped, k = C.c_int(), C.c_uint64()
         N.check(_lib().l1b_session_sync(self._s, C.byref(stopped), C.byref(k)))

@@ -17,19 +17,24 @@ pytestmark = pytest.mark.gpu
 TH = 2 * math.pi / 10
 
 
-def _solve(inst, iters, rc, **cfg):
+def _solve(inst, iters, rc, env=None, **cfg):
+    """rc: recomputing kernels (else the stored-residual one); env: extra
+    switches, e.g. L1B_PERSIST=0 (no cooperative loop: two-iteration launches
+    on any n) or L1B_RC2=0 (one iteration per launch)."""
     from paper_1503_03520_b200 import l1bench
 
-    old = os.environ.get("L1B_ITER_RC")
-    os.environ["L1B_ITER_RC"] = "1" if rc else "0"
+    env = dict(env or {}, L1B_ITER_RC="1" if rc else "0")
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         x = np.empty(inst.n)
         tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, op="matrix_free", **cfg), x)
     finally:
-        if old is None:
-            del os.environ["L1B_ITER_RC"]
-        else:
-            os.environ["L1B_ITER_RC"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
     return tr, x
 
 
@@ -96,3 +101,79 @@ def test_rc_session_stepping_matches_solve():
     np.testing.assert_array_equal(x, x2)
     assert tr2.iterations == 25
     assert rel_err(tr.objectives(), tr2.objectives()) == 0.0
+
+
+# (the switches are read once per process by the library, so each mode below
+# runs in a subprocess of its own)
+_MODES = {"loop": {}, "pairs": {"L1B_PERSIST": "0"}, "single": {"L1B_PERSIST": "0", "L1B_RC2": "0"}}
+
+
+def _mode_run(mode, kw, iters, target=None):
+    import json
+    import subprocess
+    import sys
+
+    code = (
+        "import json, sys, numpy as np; sys.path.insert(0, '.');"
+        "from paper_1503_03520_b200 import l1bench;"
+        f"inst = l1bench.build_instance(**{kw!r});"
+        "x = np.empty(inst.n);"
+        f"cfg = l1bench.SolverConfig(max_iters={iters}, op='matrix_free'"
+        + (f", target_objective={target!r}" if target is not None else "") + ");"
+        "tr = l1bench.fista_run(inst, cfg, x);"
+        "np.save(sys.argv[1], x);"
+        "print(json.dumps({'f': list(tr.objectives()), 'it': [int(s.iter) for s in tr.samples],"
+        " 'status': int(tr.status), 'k': int(tr.iterations)}))")
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "x.npy")
+        env = dict(os.environ, **_MODES[mode])
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        p = subprocess.run([sys.executable, "-c", code, out], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        return json.loads(p.stdout.strip().splitlines()[-1]), np.load(out)
+
+
+@pytest.mark.parametrize("n,stages", [(100003, 4), (30001, 3), (20005, 2), (7777, 1)])
+def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages):
+    """fista_rc2_kernel (two iterations per launch) vs one iteration per launch
+    and vs the oracle: identical x, objectives within 1e-12."""
+    need_cuda()
+    kw = dict(n=n, stages=stages, q=1, s_divisor=100, seed=5, theta=TH)
+    iters = 41  # odd: the last launch is a single iteration
+    tp, xp = _mode_run("pairs", kw, iters)
+    ts, xs = _mode_run("single", kw, iters)
+    np.testing.assert_array_equal(xp, xs)
+    assert tp["it"] == ts["it"] and tp["k"] == ts["k"] == iters
+    assert rel_err(tp["f"], ts["f"]) < 1e-13
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+    np.testing.assert_array_equal(xp, ox)
+    assert rel_err(tp["f"], otr["objective"]) < 1e-12
+
+
+def test_two_iteration_kernel_stops_like_the_reference(oracle):
+    need_cuda()
+    kw = dict(n=3001, stages=4, q=1, s_divisor=50, seed=9, theta=TH)
+    oi = oracle.build_instance(**kw)
+    otr, _ = oracle.fista(oi, max_iters=400)
+    f = otr["objective"]
+    for k in (37, 38):  # the stop lands on the first / second iteration of a launch
+        assert f[k] < f[:k].min()
+        target = float(f[k] + 0.25 * (f[:k].min() - f[k]))
+        tp, xp = _mode_run("pairs", kw, 400, target)
+        otr2, ox2 = oracle.fista(oi, max_iters=400, target=target)
+        assert tp["k"] == int(otr2["iter"][-1]) == k
+        np.testing.assert_array_equal(xp, ox2)
+
+
+@pytest.mark.parametrize("stages", [4, 2])
+def test_two_iteration_kernel_large_n(oracle, stages):
+    """Above the cooperative-loop size (n > 2^20): the default path."""
+    need_cuda()
+    kw = dict(n=(1 << 20) + 12345, stages=stages, q=1, s_divisor=1000, seed=3, theta=TH)
+    tp, xp = _mode_run("loop", kw, 12)
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=12)
+    np.testing.assert_array_equal(xp, ox)
+    assert rel_err(tp["f"], otr["objective"]) < 1e-12
