@@ -467,6 +467,258 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2_kernel(RcArgs A, Rc2
   }
 }
 
+// ---------------------------------------------------------------------------
+// The two-iteration kernel with V entries per lane (window 32 V): the halo
+// (>= 4S, a multiple of V) is a smaller share of a wider window -- fewer
+// rotations per own entry, more registers per thread.
+template <int S, bool TR, bool INTERIOR, int K, int PAR, int V>
+__device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n,
+                                        const StageTab& tab) {
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const int s = TR ? k : S - 1 - k;
+    const int o = tab.offset[s];
+    const double c = tab.c[s], sn = tab.s[s];
+    const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
+    if (par == 0) {
+#pragma unroll
+      for (int p = 0; p < V; p += 2) {
+        const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
+      }
+    } else {
+      double right[K], left[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        right[q] = __shfl_down_sync(kFull, v[q][0], 1);
+        left[q] = __shfl_up_sync(kFull, v[q][V - 1], 1);
+      }
+#pragma unroll
+      for (int p = 1; p + 1 < V; p += 2) {
+        const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
+      }
+      const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
+      const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        if (pr) {
+          double a = v[q][V - 1], b = right[q];
+          rotate_pair(a, b, c, sn, TR);
+          v[q][V - 1] = a;
+        }
+        if (pl) {
+          double a = left[q], b = v[q][0];
+          rotate_pair(a, b, c, sn, TR);
+          v[q][0] = b;
+        }
+      }
+    }
+  }
+}
+
+template <int S, int V>
+struct RcGeomV {
+  static constexpr int W = 32 * V;
+  static constexpr int H3 = (4 * S + V - 1) / V * V;
+  static constexpr int OWN = W - 2 * H3;
+};
+
+template <int V>
+struct SegV {
+  double xk[V], xm[V], sg[V], bb[V];
+};
+
+template <int V>
+__device__ __forceinline__ void ldv(const double* p, double (&v)[V]) {
+  if (V % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < V; j += 4) {
+      double t[4];
+      ld4(p + j, t);
+      v[j] = t[0], v[j + 1] = t[1], v[j + 2] = t[2], v[j + 3] = t[3];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; j += 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(p + j));
+      v[j] = t.x, v[j + 1] = t.y;
+    }
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void load_segv(const RcArgs& A, int64_t e, bool full, int64_t lim_lo,
+                                          int64_t lim_hi, SegV<V>& s) {
+  if (full) {
+    ldv<V>(A.b.x_k + e, s.xk);
+    ldv<V>(A.b.x_km1 + e, s.xm);
+    ldv<V>(A.sigma + e, s.sg);
+    ldv<V>(A.b.b + e, s.bb);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const bool in = e + i >= lim_lo && e + i < lim_hi;
+      s.xk[i] = in ? A.b.x_k[e + i] : 0.0;
+      s.xm[i] = in ? A.b.x_km1[e + i] : 0.0;
+      s.sg[i] = in ? A.sigma[e + i] : 0.0;
+      s.bb[i] = in ? A.b.b[e + i] : 0.0;
+    }
+  }
+}
+
+template <bool FAST, int V>
+__device__ __forceinline__ void store_ownv(double* dst, int64_t e0, const bool (&mine)[V],
+                                           bool lane_own, const double (&v)[V]) {
+  if (FAST) {
+    if (lane_own) {
+      if (V % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < V; j += 4) {
+          const double t[4] = {v[j], v[j + 1], v[j + 2], v[j + 3]};
+          st4(dst + e0 + j, t);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; j += 2)
+          *reinterpret_cast<double2*>(dst + e0 + j) = make_double2(v[j], v[j + 1]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (mine[i]) dst[e0 + i] = v[i];
+  }
+}
+
+template <int S, bool FAST, int PAR, int V>
+__device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, const SegV<V>& d,
+                                          int64_t w0, int lane, bool lane_own, double beta_a,
+                                          double beta_b, double inv_l, double thr, Acc2& acc) {
+  using G = RcGeomV<S, V>;
+  const int64_t n = A.n;
+  const int64_t e0 = w0 + V * lane;
+  bool mine[V];
+  if (FAST) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) mine[i] = lane_own;
+  } else {
+    const int64_t own_lo = w0 + G::H3, own_hi = min(own_lo + G::OWN, A.hi);
+#pragma unroll
+    for (int i = 0; i < V; ++i) mine[i] = e0 + i >= own_lo && e0 + i < own_hi;
+  }
+  double t[2][V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    t[0][i] = d.xk[i];
+    t[1][i] = d.xm[i];
+  }
+  wchainv<S, true, FAST, 2, PAR, V>(t, e0, n, A.right);
+  double rk[V], g[1][V], rr = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    rk[i] = d.sg[i] * t[0][i] - d.bb[i];
+    if (mine[i]) rr += rk[i] * rk[i];
+    const double rm = d.sg[i] * t[1][i] - d.bb[i];
+    g[0][i] = d.sg[i] * ((1.0 + beta_a) * rk[i] - beta_a * rm);
+  }
+  acc.rr0 += rr;
+  wchainv<S, false, FAST, 1, PAR, V>(g, e0, n, A.right);
+  double x1[1][V], l1 = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const double y = d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
+    double v = shrink(y - inv_l * g[0][i], thr);
+    l1 += mine[i] ? fabs(v) : 0.0;
+    acc.nza += (unsigned)(mine[i] & (v != 0.0));
+    acc.misa += (unsigned)(mine[i] & (v != y));
+    if (!FAST && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
+    x1[0][i] = v;
+  }
+  acc.l1a += l1;
+  store_ownv<FAST, V>(O.x1, e0, mine, lane_own, x1[0]);
+  double t1[1][V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) t1[0][i] = x1[0][i];
+  wchainv<S, true, FAST, 1, PAR, V>(t1, e0, n, A.right);
+  double rr1 = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const double r1 = d.sg[i] * t1[0][i] - d.bb[i];
+    if (mine[i]) rr1 += r1 * r1;
+    g[0][i] = d.sg[i] * ((1.0 + beta_b) * r1 - beta_b * rk[i]);
+  }
+  acc.rr1 += rr1;
+  wchainv<S, false, FAST, 1, PAR, V>(g, e0, n, A.right);
+  double x2[V], l1b = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const double y = x1[0][i] + beta_b * (x1[0][i] - d.xk[i]);
+    x2[i] = shrink(y - inv_l * g[0][i], thr);
+    l1b += mine[i] ? fabs(x2[i]) : 0.0;
+    acc.nzb += (unsigned)(mine[i] & (x2[i] != 0.0));
+    acc.misb += (unsigned)(mine[i] & (x2[i] != y));
+  }
+  acc.l1b += l1b;
+  store_ownv<FAST, V>(O.x2, e0, mine, lane_own, x2);
+}
+
+template <int S, int MB, int PAR, int V, bool PF>
+__global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc2Out O) {
+  using G = RcGeomV<S, V>;
+  FistaDev* st = A.b.st;
+  if (*(volatile int*)&st->stop) return;
+  const double beta_a = st->beta_y;
+  double t_next, beta_b;
+  fista_momentum(st, &t_next, &beta_b);
+  const double inv_l = 1.0 / st->lval;
+  const double thr = st->tau * inv_l;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool lane_own = V * lane >= G::H3 && V * lane < G::H3 + G::OWN;
+  const int64_t n = A.n, lo = A.lo, hi = A.hi;
+  const int64_t lim_lo = max((int64_t)0, lo - G::H3), lim_hi = min(n, hi + G::H3);
+  const int64_t nseg = (hi - lo + G::OWN - 1) / G::OWN;
+  const int64_t stride = (int64_t)gridDim.x * kRcWarps;
+  Acc2 acc;
+  auto w0_of = [&](int64_t q) { return lo + q * G::OWN - G::H3; };
+  auto full_of = [&](int64_t w0) { return w0 >= lim_lo && w0 + G::W <= lim_hi; };
+  const int64_t base = lo - G::H3;
+  const int64_t w_min = max((int64_t)2, lim_lo), w_max = min(lim_hi, n - 1) - G::W;
+  const int64_t q_lo = w_min <= base ? 0 : (w_min - base + G::OWN - 1) / G::OWN;
+  const int64_t q_hi = w_max < base ? 0 : min((w_max - base) / G::OWN + 1, (hi - lo) / G::OWN);
+  SegV<V> sa, sb;
+  int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
+  if (q < nseg) load_segv<V>(A, w0_of(q) + V * lane, full_of(w0_of(q)), lim_lo, lim_hi, sa);
+  for (; q < nseg; q += stride) {
+    if (PF && q + stride < nseg) {
+      const int64_t w1 = w0_of(q + stride);
+      load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sb);
+    }
+    if (q >= q_lo && q < q_hi)
+      segment2v<S, true, PAR, V>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
+    else
+      segment2v<S, false, PAR, V>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
+    if (PF) {
+      sa = sb;
+    } else if (q + stride < nseg) {
+      const int64_t w1 = w0_of(q + stride);
+      load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sa);
+    }
+  }
+  double sums[8] = {acc.rr0, acc.l1a, (double)acc.nza, (double)acc.misa,
+                    acc.rr1, acc.l1b, (double)acc.nzb, (double)acc.misb};
+  double tot[8];
+  if (grid_sum<8>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) st->scal8[k] = tot[k];
+    fista_finalize_lagged2(st, A.b.trace);
+  }
+}
+
 // Small instances (C1: n = 2^12, a few warps of work per iteration): the
 // per-kernel cost is launch + grid-reduction latency, not bandwidth.  One
 // cooperative launch then runs up to `iters` iterations back to back, with
@@ -577,8 +829,36 @@ void launch_rc_v(const RcArgs& a, cudaStream_t st) {
   L1B_LAUNCHED();
 }
 
+template <int S, int PAR, int MB, int V, bool PF>
+void launch_rc2v(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
+  using G = RcGeomV<S, V>;
+  const int grid_cap = grid_cap_of<fista_rc2v_kernel<S, MB, PAR, V, PF>>();
+  const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
+  const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
+  fista_rc2v_kernel<S, MB, PAR, V, PF><<<grid, kRcThreads, 0, st>>>(a, o);
+  L1B_LAUNCHED();
+}
+
+int rc2_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("L1B_RC2_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int S, int PAR>
 void launch_rc2(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
+  // measured at C4 (iter/s): V=8 + prefetch, 1 CTA/SM (255 registers) 1843;
+  // V=6 + prefetch 1682; V=8 without prefetch 1466; V=4 (fista_rc2_kernel) 1468
+  switch (rc2_variant()) {
+    case 1: break;  // V = 4: fista_rc2_kernel below
+    case 2: return launch_rc2v<S, PAR, 1, 6, true>(a, o, st);
+    case 3: return launch_rc2v<S, PAR, 1, 8, false>(a, o, st);
+    default: return launch_rc2v<S, PAR, 1, 8, true>(a, o, st);
+  }
   using G = RcGeom2<S>;
   const int grid_cap = grid_cap_of<fista_rc2_kernel<S, 2, PAR>>();
   const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
@@ -633,11 +913,11 @@ void prepare_s(const StageTab& t) {
   if (is_canon<S>(t)) {
     grid_cap_of<fista_rc_kernel<S, 2, false, canon_par<S>()>>();
     grid_cap_of<fista_rc_persistent<S, canon_par<S>()>>();
-    grid_cap_of<fista_rc2_kernel<S, 2, canon_par<S>()>>();
+    grid_cap_of<fista_rc2v_kernel<S, 1, canon_par<S>(), 8, true>>();
   } else {
     grid_cap_of<fista_rc_kernel<S, 2, false, -1>>();
     grid_cap_of<fista_rc_persistent<S, -1>>();
-    grid_cap_of<fista_rc2_kernel<S, 2, -1>>();
+    grid_cap_of<fista_rc2v_kernel<S, 1, -1, 8, true>>();
   }
   grid_cap_of<fista_rc_kernel<S, 2, true, -1>>();
 }
