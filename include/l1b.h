@@ -275,6 +275,11 @@ typedef struct {
   uint64_t x_halo, r_halo;
   int lagged;
   int x_nbufs;      /* 3, or 4 when lagged */
+  /* pairs = 1 (lagged, default): l1b_session_k1 runs TWO iterations j+1, j+2
+   * (x_bufs[(j+1)%4], x_bufs[(j+2)%4]; exchange both halos) and leaves 8 sums
+   * in scal8 (all-reduce those, then finalize); the flush still uses scal. */
+  int pairs;
+  double* scal8;
   /* general = 1: a shard of a non-banded (permuted / left-stage) operator
    * (l1b_generate with permute or left stages): rows of A split, x split by
    * columns.  Per iteration: k1 writes this rank's partial A^T r_y to g_full

@@ -60,7 +60,8 @@ KMODE_RECOMPUTE, KMODE_RECOMPUTE_TWO, KMODE_GENERAL_SHARD = 3, 4, 5
 class ShardBuffers(C.Structure):
     _fields_ = [("x_win", vp), ("r_y_win", vp), ("scal", vp), ("own", u64), ("halo", u64),
                 ("single", C.c_int), ("x_bufs", vp * 4), ("r_bufs", vp * 3), ("x_halo", u64),
-                ("r_halo", u64), ("lagged", C.c_int), ("x_nbufs", C.c_int), ("general", C.c_int),
+                ("r_halo", u64), ("lagged", C.c_int), ("x_nbufs", C.c_int), ("pairs", C.c_int),
+                ("scal8", vp), ("general", C.c_int),
                 ("g_full", vp),
                 ("x_full", vp), ("n_pad", u64), ("col_begin", u64), ("col_count", u64)]
 

@@ -437,7 +437,9 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   }
   // b is also built on bh rows around the block for the recomputing FISTA
   // kernel (k_iter_rc.cu); sigma / x / w windows widen by the same amount
-  const uint64_t bh = g->stages >= 1 && g->stages <= 4 ? (uint64_t)fista_rc_halo((int)g->stages) : 0;
+  const uint64_t bh = g->stages >= 1 && g->stages <= 4
+                          ? (uint64_t)std::max(fista_rc_halo((int)g->stages), fista_rc2_halo((int)g->stages))
+                          : 0;
   const uint64_t sa = a > bh + 3 * h ? (a - bh - 3 * h) & ~3ull : 0;  // 32-byte aligned view
   const uint64_t sb = std::min(n, b + bh + 3 * h);
   auto p = std::make_unique<l1b_problem>();

@@ -463,7 +463,10 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2_kernel(RcArgs A, Rc2
     st->scal8[5] = tot[5];
     st->scal8[6] = tot[6];
     st->scal8[7] = tot[7];
-    fista_finalize_lagged2(st, A.b.trace);
+    if (st->defer)
+      st->pair_pending = 1;  // shards: recorded by the finalize after the all-reduce
+    else
+      fista_finalize_lagged2(st, A.b.trace);
   }
 }
 
@@ -715,7 +718,10 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc
   if (grid_sum<8>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) st->scal8[k] = tot[k];
-    fista_finalize_lagged2(st, A.b.trace);
+    if (st->defer)
+      st->pair_pending = 1;  // shards: recorded by the finalize after the all-reduce
+    else
+      fista_finalize_lagged2(st, A.b.trace);
   }
 }
 
@@ -970,6 +976,16 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
     case 2: return is_canon<2>(op.right) ? launch_rc2<2, canon_par<2>()>(a, o, st) : launch_rc2<2, -1>(a, o, st);
     case 3: return is_canon<3>(op.right) ? launch_rc2<3, canon_par<3>()>(a, o, st) : launch_rc2<3, -1>(a, o, st);
     case 4: return is_canon<4>(op.right) ? launch_rc2<4, canon_par<4>()>(a, o, st) : launch_rc2<4, -1>(a, o, st);
+    default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
+  }
+}
+
+int fista_rc2_halo(int stages) {
+  switch (stages) {
+    case 1: return RcGeomV<1, 8>::H3;
+    case 2: return RcGeomV<2, 8>::H3;
+    case 3: return RcGeomV<3, 8>::H3;
+    case 4: return RcGeomV<4, 8>::H3;
     default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
   }
 }

@@ -179,7 +179,10 @@ __global__ void fista_finalize_kernel(FistaDev* st, FistaSample* trace) {
   if (st->stop) return;
   if (!st->initialized)
     fista_init_finalize(st, trace);
-  else if (st->lagged)
+  else if (st->pair_pending) {
+    st->pair_pending = 0;
+    fista_finalize_lagged2(st, trace);
+  } else if (st->lagged)
     fista_finalize_lagged(st, trace, st->flushing != 0);
   else
     fista_finalize_device(st, trace);

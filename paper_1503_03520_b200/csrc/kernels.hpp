@@ -98,6 +98,7 @@ struct FistaDev {
   // two-iteration kernel: ||r_k||^2, (l1, nnz, mism) of x_{k+1}, ||r_{k+1}||^2,
   // (l1, nnz, mism) of x_{k+2}
   double scal8[8];
+  int pair_pending;  // shards: the last kernel ran two iterations (finalize: lagged2)
 };
 
 struct FistaBufs {
@@ -155,6 +156,8 @@ void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
                    bool flush = false);
 int fista_rc_halo(int stages);
+// x-window halo of the two-iteration kernel (default 8-entries-per-lane variant)
+int fista_rc2_halo(int stages);
 // `iters` iterations j0, j0+1, ... of the same kernel in ONE cooperative launch
 // (grid barriers between iterations; x rotates through X[j % 3]) -- small
 // instances, where a launch per iteration costs more than the iteration.

@@ -37,6 +37,7 @@ struct l1b_session {
   bool fused = false;   // matrix-free fused kernels (k_fused.cu) instead of CSR/CSC
   bool single = false;  // ... as one kernel per iteration (one device): x / r rotate
   bool recompute = false;  // ... with r_k, r_{k-1} rebuilt from x (k_iter_rc.cu): no R buffers
+  bool pairs = false;      // ... shard k1 = two iterations (fista_rc_iter2), halos of two x buffers
   bool general = false;    // general row-block shard: reduce-scatter g, all-gather x (distributed.py)
   double *g_full = nullptr, *x_full = nullptr;  // n_pad = world * col_slice entries each
   uint64_t n_pad = 0, col_off = 0;              // own slice: [col_off, col_off + nx)
@@ -130,6 +131,8 @@ struct l1b_session {
 
 namespace {
 
+bool rc2_enabled();  // L1B_RC2 switch (below)
+
 uint64_t sample_capacity(uint64_t max_iters) {
   uint64_t c = std::min<uint64_t>(max_iters, 1000) + 2;
   if (max_iters > 1000) c += (max_iters - 1000) / 10 + 1;
@@ -173,7 +176,8 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     const char* e = getenv("L1B_ITER_RC");
     bool ok = s->single && !(e && e[0] == '0') && (uintptr_t)v.op->sigma % 32 == 0;
     if (ok && s->shard) {
-      const uint64_t H3 = (uint64_t)fista_rc_halo(v.op->right.count);
+      const uint64_t H3 = (uint64_t)std::max(fista_rc_halo(v.op->right.count),
+                                             fista_rc2_halo(v.op->right.count));
       ok = v.b_win && (uintptr_t)v.b_win % 32 == 0 && v.row_begin % 4 == 0 &&
            v.row_end - v.row_begin >= H3 && v.b_win_lo <= (v.row_begin > H3 ? v.row_begin - H3 : 0) &&
            v.b_win_hi >= std::min(v.n, v.row_end + H3);
@@ -188,7 +192,11 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     // X[2] / R[2] stand for the iterate "before" the first one (x_{-1} = x_0)
     const uint64_t H = ((uint64_t)v.op->right.count + 1) & ~1ull;
     s->nx = s->nr = s->shard ? v.row_end - v.row_begin : v.n;
-    s->xh = s->shard ? (s->recompute ? (uint64_t)fista_rc_halo(v.op->right.count) : H) : 0;
+    s->pairs = s->shard && s->recompute && rc2_enabled();
+    s->xh = s->shard ? (s->recompute ? (uint64_t)std::max(fista_rc_halo(v.op->right.count),
+                                                          fista_rc2_halo(v.op->right.count))
+                                     : H)
+                     : 0;
     s->rh = s->shard && !s->recompute ? 2 * H : 0;
     s->halo = s->xh;
     s->nbuf = s->recompute ? 4 : 3;
@@ -461,6 +469,8 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->x_halo = s->xh;
     out->r_halo = s->rh;
     out->lagged = s->recompute ? 1 : 0;
+    out->pairs = s->pairs ? 1 : 0;
+    out->scal8 = &s->st->scal8[0];
     out->general = s->general ? 1 : 0;
     out->g_full = s->g_full;
     out->x_full = s->x_full;
@@ -503,7 +513,10 @@ int l1b_session_k1(l1b_session* s) {
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     L1B_CUDA(cudaSetDevice(s->v.device));
-    if (s->single) {  // the whole iteration; k2 is then a no-op
+    if (s->single && s->pairs) {  // two iterations (the extra one past a stop is discarded)
+      s->iterate2(s->launched, s->v.stream);
+      s->launched += 2;
+    } else if (s->single) {  // the whole iteration; k2 is then a no-op
       s->iterate(s->launched, s->v.stream);
       s->launched += 1;
     } else if (s->general) {  // partial A^T r_y of the own rows, all n columns
