@@ -83,6 +83,9 @@ typedef struct {
 } l1b_operator_desc;
 
 enum { L1B_SPECTRUM_UNIFORM_Q = 0, L1B_SPECTRUM_ALTERNATING = 1, L1B_SPECTRUM_EXPLICIT = 2 };
+/* SolutionRule::Kind (bench.hpp:25-32): uniform_sparse_solution (OsGen), the
+ * spectral one (solution.cpp:77-113, OsGen3) or two values on a uniform support */
+enum { L1B_SOLUTION_UNIFORM = 0, L1B_SOLUTION_SPECTRAL = 1, L1B_SOLUTION_TWO_VALUE = 2 };
 
 /* ExperimentConfig + InstanceJob for one job (bench.hpp:16-97). */
 typedef struct {
@@ -104,6 +107,9 @@ typedef struct {
   uint64_t job_index;        /* job.seed = mix_seed(seed, job_index) (bench.cpp:237) */
   double fill_bound;         /* FillPolicy::interior bound, 0.9 */
   int lazy_sparse;           /* 1: build the CSR/CSC copy of A only on first sparse use */
+  int solution_kind;         /* L1B_SOLUTION_*; 0 = uniform (the default) */
+  double s1_fraction;        /* spectral: share of s kept from the small end (0.5) */
+  double value_a, value_b;   /* two_value: first half / rest of the support (-1e4, 0.1) */
 } l1b_gen_desc;
 
 /* Shard = contiguous block of A's nonempty rows [row_begin, row_end) of a

@@ -436,6 +436,8 @@ class Reference:
         L.ref_build_instance.argtypes = [u64, f64, u64, u64, C.c_int, C.c_int, f64, u64, f64, f64,
                                          f64, u64, P(f64)]
         L.ref_build_instance.restype = C.c_void_p
+        L.ref_build_instance2.argtypes = L.ref_build_instance.argtypes + [C.c_int, f64, f64, f64]
+        L.ref_build_instance2.restype = C.c_void_p
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_dims.argtypes = [C.c_void_p, P(u64), P(u64)]
         for fn in ("ref_tau", "ref_noise_norm", "ref_cert_kappa", "ref_f_star", "ref_gram_lmax"):
@@ -468,12 +470,16 @@ class Reference:
         L.ref_solve.argtypes = [C.c_void_p, P(RefCfg), P(RefSample), u64, P(u64), P(RefSummary),
                                 P(f64)]
 
+    SOLUTION_KINDS = {"uniform": 0, "spectral": 1, "two_value": 2}
+
     def build_instance(self, n, m_ratio=2.0, stages=1, left_stages=0, permute=False, q=1,
                        shift=0.1, s_divisor=128, gamma=10.0, tau=1.0, theta=2 * math.pi / 10,
-                       seed=1, sigma=None):
+                       seed=1, sigma=None, solution="uniform", s1_fraction=0.5, value_a=-1e4,
+                       value_b=1e-1):
         sig = None if sigma is None else np.ascontiguousarray(sigma, dtype=np.float64)
-        h = self.lib.ref_build_instance(n, m_ratio, stages, left_stages, int(permute), q, shift,
-                                        s_divisor, gamma, tau, theta, seed, _ptr(sig, f64))
+        h = self.lib.ref_build_instance2(n, m_ratio, stages, left_stages, int(permute), q, shift,
+                                         s_divisor, gamma, tau, theta, seed, _ptr(sig, f64),
+                                         self.SOLUTION_KINDS[solution], s1_fraction, value_a, value_b)
         if not h:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return RefInstance(self, h)

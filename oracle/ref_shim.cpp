@@ -89,12 +89,32 @@ const char* ref_last_error() { return g_err.c_str(); }
 // ExperimentConfig / enumerate_jobs / build_instance (bench.hpp:37-102).  With
 // sigma_explicit != nullptr the same assembly is done through the operator
 // API with Spectrum::from_values (SURVEY.md 8(d) C1 mapping).
+void* ref_build_instance2(uint64_t n, double m_ratio, uint64_t stages, uint64_t left_stages,
+                          int permute, int q, double shift, uint64_t s_divisor, double gamma,
+                          double tau, double theta, uint64_t seed, const double* sigma_explicit,
+                          int solution_kind, double s1_fraction, double value_a, double value_b);
+
 void* ref_build_instance(uint64_t n, double m_ratio, uint64_t stages, uint64_t left_stages,
                          int permute, int q, double shift, uint64_t s_divisor, double gamma,
                          double tau, double theta, uint64_t seed, const double* sigma_explicit) {
+  return ref_build_instance2(n, m_ratio, stages, left_stages, permute, q, shift, s_divisor, gamma,
+                             tau, theta, seed, sigma_explicit, 0, 0.5, -1e4, 1e-1);
+}
+
+// + SolutionRule (bench.hpp:25-32): kind 0 uniform, 1 spectral, 2 two_value
+void* ref_build_instance2(uint64_t n, double m_ratio, uint64_t stages, uint64_t left_stages,
+                          int permute, int q, double shift, uint64_t s_divisor, double gamma,
+                          double tau, double theta, uint64_t seed, const double* sigma_explicit,
+                          int solution_kind, double s1_fraction, double value_a, double value_b) {
   RefInst* out = nullptr;
   int rc = guarded([&] {
     ExperimentConfig cfg;
+    cfg.solution.kind = solution_kind == 1   ? SolutionRule::Kind::spectral
+                        : solution_kind == 2 ? SolutionRule::Kind::two_value
+                                             : SolutionRule::Kind::uniform;
+    cfg.solution.s1_fraction = s1_fraction;
+    cfg.solution.value_a = value_a;
+    cfg.solution.value_b = value_b;
     cfg.name = "ref";
     cfg.n_list = {static_cast<std::size_t>(n)};
     cfg.m_ratio = m_ratio;

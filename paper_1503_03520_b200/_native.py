@@ -24,6 +24,7 @@ TARGET_REACHED, ITER_BUDGET, TIME_BUDGET = range(3)
 PATH_SPARSE, PATH_SWEEP, PATH_FUSED = 0, 1, 2
 OP_AUTO, OP_SPARSE, OP_MATRIX_FREE = 0, 1, 2
 SPECTRUM_UNIFORM_Q, SPECTRUM_ALTERNATING, SPECTRUM_EXPLICIT = range(3)
+SOLUTION_UNIFORM, SOLUTION_SPECTRAL, SOLUTION_TWO_VALUE = range(3)
 
 
 class OperatorDesc(C.Structure):
@@ -37,7 +38,8 @@ class GenDesc(C.Structure):
                 ("permute", C.c_int), ("spectrum_kind", C.c_int), ("q", C.c_int), ("shift", f64),
                 ("odd_value", f64), ("even_value", f64), ("sigma_explicit", P(f64)),
                 ("gamma", f64), ("s_divisor", u64), ("tau", f64), ("theta", f64), ("seed", u64),
-                ("job_index", u64), ("fill_bound", f64), ("lazy_sparse", C.c_int)]
+                ("job_index", u64), ("fill_bound", f64), ("lazy_sparse", C.c_int),
+                ("solution_kind", C.c_int), ("s1_fraction", f64), ("value_a", f64), ("value_b", f64)]
 
 
 class ShardDesc(C.Structure):

@@ -399,6 +399,43 @@ namespace {
 // (k_sweep.cu window_stages), which reproduces the global b on the own rows
 // bit for bit, and materialises rows [a, b) (CSR, columns local to the x
 // window [a - h, b + h)) and columns [a, b) (CSC, rows local to the r window).
+// The planted solution of bench.cpp:281-301 by SolutionRule::Kind.  uniform:
+// uniform_sparse_solution(n, s, gamma) from Rng(mix_seed(job.seed, 4));
+// two_value: the same support with gamma 1, values value_a on the first half
+// and value_b on the rest; spectral: spectral_sparse_solution
+// (solution.cpp:77-113) -- xhat = G gamma (Sigma^T Sigma)^{-1} 1 (right factor
+// applied on the device with the reference's stage order), the s1 smallest and
+// s2 = s - s1 largest |xhat| among its nonzeros (stable order), ascending.
+void planted_solution(const l1b_gen_desc* g, uint64_t n, uint64_t job_seed, const double* sigma,
+                      l1b_problem* p) {
+  const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
+  switch (g->solution_kind) {
+    case L1B_SOLUTION_UNIFORM: {
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+      hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
+      return;
+    }
+    case L1B_SOLUTION_TWO_VALUE: {
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+      hostrng::sparse_solution(n, s, 1.0, r, p->xs_sup, p->xs_val);
+      const size_t half = p->xs_val.size() / 2;
+      for (size_t k = 0; k < p->xs_val.size(); ++k) p->xs_val[k] = k < half ? g->value_a : g->value_b;
+      return;
+    }
+    case L1B_SOLUTION_SPECTRAL: {
+      const uint64_t s1 = (uint64_t)std::llround(g->s1_fraction * (double)s);
+      if (s1 > s) throw InvalidArgument("spectral_sparse_solution: s1 + s2 must not exceed n");
+      if (!(g->gamma > 0.0)) throw InvalidArgument("spectral_sparse_solution: gamma must be positive");
+      std::vector<double> xhat(n);
+      for (uint64_t i = 0; i < n; ++i) xhat[i] = g->gamma / (sigma[i] * sigma[i]);
+      spectral_select(p->view, xhat.data(), n, s1, s - s1, p->stream, p->xs_sup, p->xs_val);
+      return;
+    }
+    default:
+      throw InvalidArgument("unknown solution kind");
+  }
+}
+
 void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
                     l1b_problem** out) {
   if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
@@ -479,11 +516,10 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   p->row_begin = a;
   p->row_end = b;
   p->halo = h;
-  const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
-  {
-    hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
-    hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
-  }
+  if (g->solution_kind == L1B_SOLUTION_SPECTRAL)
+    throw Unsupported("row-block shards: the spectral planted solution needs the whole operator");
+  planted_solution(g, n, job_seed, nullptr, p.get());
+  const uint64_t s = p->xs_sup.size();
   std::vector<double> gw(sb - sa), xw;
   {
     hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
@@ -599,12 +635,9 @@ std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
                  std::vector<double>(g->left_stages, g->theta), g->permute ? p1.data() : nullptr,
                  g->permute ? p2.data() : nullptr, sigma.data());
   p->tau = g->tau;
-  // planted solution (Rng(mix_seed(job.seed, 4)), bench.cpp:281-301)
-  const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
-  {
-    hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
-    hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
-  }
+  // planted solution (bench.cpp:281-301)
+  planted_solution(g, n, job_seed, sigma.data(), p.get());
+  const uint64_t s = p->xs_sup.size();
   // subgradient g: signs on the support (instance.cpp:36-40)
   for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
   cudaStream_t st = p->stream;

@@ -8,6 +8,11 @@
 #include <cstring>
 
 #include "common.cuh"
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
 #include "kernels.hpp"
 
 namespace l1b {
@@ -165,6 +170,100 @@ void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStr
   L1B_CUDA(cudaMemcpyAsync(x, v, op.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaFreeAsync(v, st));
   L1B_CUDA(cudaFreeAsync(t, st));
+}
+
+namespace {
+__global__ void abs_key_kernel(const double* __restrict__ x, uint64_t n, unsigned long long* key,
+                               uint32_t* idx, unsigned long long* zeros) {
+  unsigned long long z = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    // |x| ordered as its bit pattern (non-negative doubles); 0 and -0 -> 0
+    const unsigned long long k = (unsigned long long)__double_as_longlong(x[i]) & 0x7fffffffffffffffull;
+    key[i] = k;
+    idx[i] = (uint32_t)i;
+    z += k == 0;
+  }
+  if (z) atomicAdd(zeros, z);
+}
+__global__ void gather_vals(const double* __restrict__ x, const uint32_t* __restrict__ idx, uint64_t k,
+                            double* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = x[idx[i]];
+}
+}  // namespace
+
+void spectral_select(const OpView& op, const double* xhat_host, uint64_t n, uint64_t s1, uint64_t s2,
+                     cudaStream_t st, std::vector<uint32_t>& sup, std::vector<double>& val) {
+  double* x = nullptr;
+  unsigned long long *key = nullptr, *key2 = nullptr, *zeros = nullptr;
+  uint32_t *idx = nullptr, *idx2 = nullptr;
+  L1B_CUDA(cudaMallocAsync(&x, n * 8, st));
+  L1B_CUDA(cudaMallocAsync(&key, n * 8, st));
+  L1B_CUDA(cudaMallocAsync(&key2, n * 8, st));
+  L1B_CUDA(cudaMallocAsync(&idx, n * 4, st));
+  L1B_CUDA(cudaMallocAsync(&idx2, n * 4, st));
+  L1B_CUDA(cudaMallocAsync(&zeros, 8, st));
+  L1B_CUDA(cudaMemsetAsync(zeros, 0, 8, st));
+  L1B_CUDA(cudaMemcpyAsync(x, xhat_host, n * 8, cudaMemcpyHostToDevice, st));
+  // op.apply_right_factor(xhat, false): stages last to first (linops.cpp:492-502)
+  for (int s = op.right.count - 1; s >= 0; --s)
+    run_stage(x, op.n, op.right.offset[s], op.right.c[s], op.right.s[s], false, st);
+  abs_key_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, key, idx, zeros);
+  L1B_LAUNCHED();
+  // stable ascending |xhat| (std::stable_sort of solution.cpp:93-95): radix sort is stable
+  size_t tmp_bytes = 0;
+  L1B_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, idx, idx2, n, 0, 64, st));
+  void* tmp = nullptr;
+  L1B_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  L1B_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, idx, idx2, n, 0, 64, st));
+  L1B_LAUNCHED();
+  unsigned long long z = 0;
+  L1B_CUDA(cudaMemcpyAsync(&z, zeros, 8, cudaMemcpyDeviceToHost, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  const uint64_t nz = n - z;  // the nonzeros, in sorted order: idx2[z, n)
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [first, count) of idx2 kept
+  if (nz <= s1 + s2)
+    ranges.push_back({z, nz});
+  else
+    ranges = {{z, s1}, {n - s2, s2}};
+  uint64_t kept = 0;
+  for (auto& r : ranges) kept += r.second;
+  uint32_t* kidx = nullptr;
+  double* kval = nullptr;
+  L1B_CUDA(cudaMallocAsync(&kidx, std::max<uint64_t>(kept, 1) * 4, st));
+  L1B_CUDA(cudaMallocAsync(&kval, std::max<uint64_t>(kept, 1) * 8, st));
+  uint64_t o = 0;
+  for (auto& r : ranges) {
+    if (r.second)
+      L1B_CUDA(cudaMemcpyAsync(kidx + o, idx2 + r.first, r.second * 4, cudaMemcpyDeviceToDevice, st));
+    o += r.second;
+  }
+  if (kept) {
+    gather_vals<<<grid_for(kept), kThreads, 0, st>>>(x, kidx, kept, kval);
+    L1B_LAUNCHED();
+  }
+  std::vector<uint32_t> hi(kept);
+  std::vector<double> hv(kept);
+  if (kept) {
+    L1B_CUDA(cudaMemcpyAsync(hi.data(), kidx, kept * 4, cudaMemcpyDeviceToHost, st));
+    L1B_CUDA(cudaMemcpyAsync(hv.data(), kval, kept * 8, cudaMemcpyDeviceToHost, st));
+  }
+  L1B_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {(void*)x, (void*)key, (void*)key2, (void*)idx, (void*)idx2, (void*)zeros, tmp,
+                  (void*)kidx, (void*)kval})
+    cudaFreeAsync(q, st);
+  // ascending support (std::sort(keep), solution.cpp:104), values xhat[i]
+  std::vector<uint64_t> order(kept);
+  for (uint64_t k = 0; k < kept; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return hi[a] < hi[b]; });
+  sup.resize(kept);
+  val.resize(kept);
+  for (uint64_t k = 0; k < kept; ++k) {
+    sup[k] = hi[order[k]];
+    val[k] = hv[order[k]];
+  }
 }
 
 void sweep_gram_inverse(const OpView& op, const double* vin, double* out, cudaStream_t st) {

@@ -1,6 +1,8 @@
 // kernels.hpp -- host-side launchers of the device kernels (one per .cu file).
 #pragma once
 
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,6 +33,11 @@ void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, 
 // ---- k_sweep.cu (matrix-free, bit-exact vs linops.cpp) ---------------------
 void sweep_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
 void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStream_t st);
+// spectral_sparse_solution's selection (solution.cpp:77-113) given xhat =
+// gamma / sigma^2 on the host: right factor applied on the device, the s1
+// smallest and s2 largest |xhat| nonzeros (stable), ascending support
+void spectral_select(const OpView& op, const double* xhat_host, uint64_t n, uint64_t s1, uint64_t s2,
+                     cudaStream_t st, std::vector<uint32_t>& sup, std::vector<double>& val);
 void sweep_gram_inverse(const OpView& op, const double* v, double* out, cudaStream_t st);
 void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* dense, uint64_t n,
                     cudaStream_t st);

@@ -125,6 +125,10 @@ class CudaShard:
         g.s_divisor, g.tau = kw.get("s_divisor", 128), kw.get("tau", 1.0)
         g.theta, g.seed, g.job_index = kw.get("theta", 2 * math.pi / 10), kw.get("seed", 1), 0
         g.fill_bound = 0.9
+        g.solution_kind = {"uniform": N.SOLUTION_UNIFORM, "spectral": N.SOLUTION_SPECTRAL,
+                           "two_value": N.SOLUTION_TWO_VALUE}[kw.get("solution", "uniform")]
+        g.s1_fraction, g.value_a, g.value_b = (kw.get("s1_fraction", 0.5), kw.get("value_a", -1e4),
+                                               kw.get("value_b", 1e-1))
         g.lazy_sparse = 0 if getattr(cfg, "op", "auto") == "sparse" else 1
         sh = N.ShardDesc(rank, world, 0, 0)
         h = C.c_void_p()

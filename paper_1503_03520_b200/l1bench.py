@@ -399,11 +399,15 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
                    alternating: Optional[tuple] = None, sigma: Optional[np.ndarray] = None,
                    gamma: float = 10.0, s_divisor: int = 128, tau: float = 1.0,
                    theta: float = 0.6283185307179586, seed: int = 1, job_index: int = 0,
-                   fill_bound: float = 0.9, device: int = 0, lazy_sparse: bool = False) -> ProblemInstance:
+                   fill_bound: float = 0.9, device: int = 0, lazy_sparse: bool = False,
+                   solution: str = "uniform", s1_fraction: float = 0.5, value_a: float = -1e4,
+                   value_b: float = 1e-1) -> ProblemInstance:
     """``build_instance(cfg, enumerate_jobs(cfg)[job_index])`` for a single-job
     ExperimentConfig (bench.cpp:216-316), generated on the GPU.  ``sigma`` gives
     an explicit spectrum (Spectrum::from_values), ``alternating=(odd, even)`` the
-    alternating one, otherwise uniform in (0, 10^q] + shift."""
+    alternating one, otherwise uniform in (0, 10^q] + shift.  ``solution`` is the
+    SolutionRule kind (bench.hpp:25-32): "uniform" (default), "spectral"
+    (spectral_sparse_solution, s1_fraction) or "two_value" (value_a, value_b)."""
     sig = None
     g = N.GenDesc()
     g.n, g.m_ratio, g.stages, g.left_stages, g.permute = n, m_ratio, stages, left_stages, int(permute)
@@ -419,6 +423,10 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
     g.shift, g.gamma, g.s_divisor, g.tau, g.theta = shift, gamma, s_divisor, tau, theta
     g.seed, g.job_index, g.fill_bound = seed, job_index, fill_bound
     g.lazy_sparse = int(lazy_sparse)
+    kinds = {"uniform": N.SOLUTION_UNIFORM, "spectral": N.SOLUTION_SPECTRAL, "two_value": N.SOLUTION_TWO_VALUE}
+    if solution not in kinds:
+        raise ValueError(f"SolutionRule: unknown kind '{solution}'")
+    g.solution_kind, g.s1_fraction, g.value_a, g.value_b = kinds[solution], s1_fraction, value_a, value_b
     h = C.c_void_p()
     N.check(_lib().l1b_generate(device, C.byref(g), None, C.byref(h)))
     return ProblemInstance(h)
