@@ -151,6 +151,16 @@ int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* out);
 int l1b_problem_get_b(const l1b_problem* p, double* b_host);          /* m */
 int l1b_problem_get_sigma(const l1b_problem* p, double* sigma_host);  /* n */
 int l1b_problem_get_xstar(const l1b_problem* p, uint32_t* support, double* values);
+/* The operator description back (save_instance, serialize.cpp:148-163): stage
+ * offsets / angles of the right (right = 1) or left factor (count first, arrays
+ * may be NULL), and P1 (which = 1) / P2 (which = 2) as an m-entry map unless
+ * *is_identity.                                                             */
+int l1b_problem_get_stages(const l1b_problem* p, int right, uint32_t* count, int32_t* offsets,
+                           double* thetas);
+int l1b_problem_get_perm(const l1b_problem* p, int which, int* is_identity, uint32_t* map);
+/* Instance metadata carried by instance files (serialize.cpp:182-219):
+ * ||e|| (f* = tau ||x*||_1 + ||e||^2 / 2, instance.cpp:49-51) and cert_kappa. */
+int l1b_problem_set_meta(l1b_problem* p, double noise_norm, double cert_kappa);
 void* l1b_problem_stream(const l1b_problem* p);  /* cudaStream_t */
 int l1b_problem_set_stream(l1b_problem* p, void* stream);
 

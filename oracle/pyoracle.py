@@ -438,6 +438,10 @@ class Reference:
         L.ref_build_instance.restype = C.c_void_p
         L.ref_build_instance2.argtypes = L.ref_build_instance.argtypes + [C.c_int, f64, f64, f64]
         L.ref_build_instance2.restype = C.c_void_p
+        L.ref_save_instance.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_save_instance.restype = C.c_int
+        L.ref_load_instance.argtypes = [C.c_char_p]
+        L.ref_load_instance.restype = C.c_void_p
         L.ref_free.argtypes = [C.c_void_p]
         L.ref_dims.argtypes = [C.c_void_p, P(u64), P(u64)]
         for fn in ("ref_tau", "ref_noise_norm", "ref_cert_kappa", "ref_f_star", "ref_gram_lmax"):
@@ -480,6 +484,18 @@ class Reference:
         h = self.lib.ref_build_instance2(n, m_ratio, stages, left_stages, int(permute), q, shift,
                                          s_divisor, gamma, tau, theta, seed, _ptr(sig, f64),
                                          self.SOLUTION_KINDS[solution], s1_fraction, value_a, value_b)
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return RefInstance(self, h)
+
+    def save_instance(self, inst, path):
+        """the reference's save_instance (serialize.cpp:182-219)"""
+        if self.lib.ref_save_instance(inst.h, str(path).encode()) != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def load_instance(self, path):
+        """the reference's load_instance (serialize.cpp:221-281)"""
+        h = self.lib.ref_load_instance(str(path).encode())
         if not h:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return RefInstance(self, h)

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "l1bench/bench.hpp"
+#include "l1bench/serialize.hpp"
 #include "l1bench/instance.hpp"
 #include "l1bench/linops.hpp"
 #include "l1bench/solvers.hpp"
@@ -168,6 +169,20 @@ void* ref_build_instance2(uint64_t n, double m_ratio, uint64_t stages, uint64_t 
 }
 
 void ref_free(void* h) { delete static_cast<RefInst*>(h); }
+
+// serialize.cpp's own save_instance / load_instance (instance files)
+int ref_save_instance(void* h, const char* path) {
+  return guarded([&] { save_instance(static_cast<RefInst*>(h)->inst, path); });
+}
+void* ref_load_instance(const char* path) {
+  RefInst* out = nullptr;
+  const int rc = guarded([&] {
+    auto* ri = new RefInst();
+    ri->inst = load_instance(path);
+    out = ri;
+  });
+  return rc == 0 ? out : nullptr;
+}
 
 void ref_dims(void* h, uint64_t* m, uint64_t* n) {
   auto* ri = static_cast<RefInst*>(h);

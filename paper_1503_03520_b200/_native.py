@@ -110,6 +110,9 @@ SIGNATURES = [
     ("l1b_problem_info_get", C.c_int, [vp, P(ProblemInfo)]),
     ("l1b_problem_get_b", C.c_int, [vp, P(f64)]),
     ("l1b_problem_get_sigma", C.c_int, [vp, P(f64)]),
+    ("l1b_problem_set_meta", C.c_int, [vp, f64, f64]),
+    ("l1b_problem_get_stages", C.c_int, [vp, C.c_int, P(u32), P(C.c_int32), P(f64)]),
+    ("l1b_problem_get_perm", C.c_int, [vp, C.c_int, P(C.c_int), P(u32)]),
     ("l1b_problem_get_xstar", C.c_int, [vp, P(u32), P(f64)]),
     ("l1b_problem_stream", vp, [vp]),
     ("l1b_problem_set_stream", C.c_int, [vp, vp]),

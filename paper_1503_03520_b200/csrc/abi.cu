@@ -818,6 +818,38 @@ int l1b_problem_get_sigma(const l1b_problem* p, double* s) {
   });
 }
 
+int l1b_problem_set_meta(l1b_problem* p, double noise_norm, double cert_kappa) {
+  return guard([&] {
+    if (!p) throw InvalidArgument("null problem");
+    p->noise_norm = noise_norm;
+    p->cert_kappa = cert_kappa;
+  });
+}
+
+int l1b_problem_get_stages(const l1b_problem* p, int right, uint32_t* count, int32_t* offsets,
+                           double* thetas) {
+  return guard([&] {
+    if (!p || !count) throw InvalidArgument("null argument");
+    const auto& off = right ? p->r_off : p->l_off;
+    const auto& th = right ? p->r_theta : p->l_theta;
+    *count = (uint32_t)off.size();
+    if (offsets) std::copy(off.begin(), off.end(), offsets);
+    if (thetas) std::copy(th.begin(), th.end(), thetas);
+  });
+}
+
+int l1b_problem_get_perm(const l1b_problem* p, int which, int* is_identity, uint32_t* map) {
+  return guard([&] {
+    if (!p || !is_identity || (which != 1 && which != 2)) throw InvalidArgument("bad argument");
+    const uint32_t* d = which == 1 ? p->d_p1 : p->d_p2;
+    *is_identity = d ? 0 : 1;
+    if (d && map) {
+      L1B_CUDA(cudaMemcpyAsync(map, d, p->m * sizeof(uint32_t), cudaMemcpyDeviceToHost, p->stream));
+      L1B_CUDA(cudaStreamSynchronize(p->stream));
+    }
+  });
+}
+
 int l1b_problem_get_xstar(const l1b_problem* p, uint32_t* support, double* values) {
   return guard([&] {
     if (!p) throw InvalidArgument("null problem");

@@ -61,6 +61,20 @@ def mix_seed(seed: int, salt: int) -> int:
     return int(_lib().l1b_mix_seed(seed, salt))
 
 
+def realize_permutation(n: int, seed: int) -> np.ndarray:
+    """Permutation::random(n, seed).map() (linops.cpp:224-239)."""
+    out = np.empty(n, dtype=np.uint32)
+    N.check(_lib().l1b_realize_permutation(n, seed, _ptr(out, _u32p)))
+    return out
+
+
+def realize_spectrum_uniform(n: int, lo: float, hi: float, shift: float, seed: int) -> np.ndarray:
+    """Spectrum::uniform(n, lo, hi, shift, seed).values() (linops.cpp:320-336)."""
+    out = np.empty(n)
+    N.check(_lib().l1b_realize_spectrum_uniform(n, lo, hi, shift, seed, _ptr(out, _f64p)))
+    return out
+
+
 class StopReason(enum.IntEnum):  # solvers.hpp:24
     target_reached = 0
     iter_budget = 1
@@ -359,6 +373,24 @@ class ProblemInstance:
         N.check(_lib().l1b_problem_get_xstar(self._h, _ptr(sup, _u32p), _ptr(val, _f64p)))
         return SparseSolution(self.n, sup[:s], val[:s])
 
+    def stages(self, right: bool = True):
+        """[(offset, theta)] of the right (G) or left (G~) factor."""
+        cnt = C.c_uint32()
+        N.check(_lib().l1b_problem_get_stages(self._h, int(right), C.byref(cnt), None, None))
+        k = int(cnt.value)
+        off = np.empty(max(k, 1), dtype=np.int32)
+        th = np.empty(max(k, 1))
+        N.check(_lib().l1b_problem_get_stages(self._h, int(right), C.byref(cnt),
+                                               off.ctypes.data_as(C.POINTER(C.c_int32)), _ptr(th, _f64p)))
+        return [(int(off[i]), float(th[i])) for i in range(k)]
+
+    def perm(self, which: int) -> Optional[np.ndarray]:
+        """P1 (which=1) / P2 (which=2) as an m-entry map, None for the identity."""
+        ident = C.c_int()
+        out = np.empty(self.m, dtype=np.uint32)
+        N.check(_lib().l1b_problem_get_perm(self._h, which, C.byref(ident), _ptr(out, _u32p)))
+        return None if ident.value else out
+
     @property
     def stream(self) -> int:
         return int(_lib().l1b_problem_stream(self._h) or 0)
@@ -430,6 +462,109 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
     h = C.c_void_p()
     N.check(_lib().l1b_generate(device, C.byref(g), None, C.byref(h)))
     return ProblemInstance(h)
+
+
+# -- instance files and traces (serialize.cpp:182-294) --------------------------
+_L1I_MAGIC = b"L1BINST\x01"
+
+
+def save_instance(inst: ProblemInstance, path: str) -> None:
+    """save_instance (serialize.cpp:182-219): magic, u64 header length, the JSON
+    header (operator description, tau, ||e||, cert_kappa, |x*|), b as raw
+    little-endian doubles, then x* as (u64 index, double) pairs.  The spectrum
+    is written as its realised values (the reference's own reader takes them
+    back bit for bit)."""
+    import json
+    import struct
+
+    def perm_json(which):
+        mp = inst.perm(which)
+        return {"kind": "identity"} if mp is None else {"kind": "explicit", "map": mp.tolist()}
+
+    op = {"version": 1, "m": inst.m, "n": inst.n,
+          "spectrum": {"kind": "explicit", "values": inst.sigma().tolist()},
+          "right_stages": [{"kind": "paired", "offset": o, "theta": t} for o, t in inst.stages(True)],
+          "left_stages": [{"kind": "paired", "offset": o, "theta": t} for o, t in inst.stages(False)],
+          "p1": perm_json(1), "p2": perm_json(2)}
+    xs = inst.x_star
+    header = {"version": 1, "kind": "tall", "m": inst.m, "n": inst.n, "tau": inst.tau,
+              "noise_norm": inst.noise_norm, "cert_kappa": inst.cert_kappa, "x_nnz": len(xs.support),
+              "op": op}
+    head = json.dumps(header, separators=(",", ":")).encode()
+    with open(path, "wb") as f:
+        f.write(_L1I_MAGIC)
+        f.write(struct.pack("<Q", len(head)))
+        f.write(head)
+        f.write(np.ascontiguousarray(inst.b, dtype="<f8").tobytes())
+        rec = np.empty(len(xs.support), dtype=[("i", "<u8"), ("v", "<f8")])
+        rec["i"], rec["v"] = xs.support, xs.values
+        f.write(rec.tobytes())
+
+
+def load_instance(path: str, device: int = 0) -> ProblemInstance:
+    """load_instance (serialize.cpp:221-281) onto the device: tall instances
+    with paired stages; spectrum explicit / uniform (realised values, or the
+    seeded draws) / alternating; permutations identity / seeded / explicit."""
+    import json
+    import struct
+
+    with open(path, "rb") as f:
+        if f.read(8) != _L1I_MAGIC:
+            raise RuntimeError(f"load_instance: '{path}' is not an instance file")
+        (hl,) = struct.unpack("<Q", f.read(8))
+        header = json.loads(f.read(hl).decode())
+        if header.get("kind") != "tall":
+            raise N.L1bUnsupported("load_instance: wide (IGen2) instances are out of scope")
+        m, n = int(header["m"]), int(header["n"])
+        b = np.frombuffer(f.read(8 * m), dtype="<f8").astype(np.float64)
+        s = int(header["x_nnz"])
+        rec = np.frombuffer(f.read(16 * s), dtype=[("i", "<u8"), ("v", "<f8")])
+        if len(b) != m or len(rec) != s:
+            raise RuntimeError(f"load_instance: truncated file '{path}'")
+    op = header["op"]
+    sp = op["spectrum"]
+    if sp["kind"] == "explicit" or (sp["kind"] == "uniform" and "values" in sp):
+        sigma = np.asarray(sp["values"], dtype=np.float64)
+    elif sp["kind"] == "uniform":
+        sigma = realize_spectrum_uniform(n, sp["lo"], sp["hi"], sp["shift"], sp["seed"])
+    elif sp["kind"] == "alternating":
+        sigma = np.where(np.arange(n) % 2 == 0, float(sp["odd"]), float(sp["even"]))
+    else:
+        raise ValueError(f"spectrum_from_json: unknown spectrum kind '{sp['kind']}'")
+
+    def stages(lst):
+        out = []
+        for st in lst:
+            if st["kind"] != "paired":
+                raise N.L1bUnsupported("load_instance: explicit rotation lists are out of scope")
+            out.append((int(st["offset"]), float(st["theta"])))
+        return out
+
+    def perm(pj):
+        if pj["kind"] == "identity":
+            return None
+        if pj["kind"] == "seeded":
+            return realize_permutation(m, int(pj["seed"]))
+        if pj["kind"] == "explicit":
+            return np.asarray(pj["map"], dtype=np.uint32)
+        raise ValueError(f"perm_from_json: unknown permutation kind '{pj['kind']}'")
+
+    inst = ProblemInstance.from_host(m, n, stages(op["right_stages"]), sigma, b, float(header["tau"]),
+                                     rec["i"].astype(np.uint32), rec["v"].copy(),
+                                     left_stages=stages(op["left_stages"]), p1=perm(op["p1"]),
+                                     p2=perm(op["p2"]), device=device)
+    N.check(_lib().l1b_problem_set_meta(inst._h, float(header["noise_norm"]), float(header["cert_kappa"])))
+    N.check(_lib().l1b_problem_info_get(inst._h, C.byref(inst.info)))
+    return inst
+
+
+def write_trace_csv(trace: SolverTrace, path: str) -> None:
+    """write_trace_csv (serialize.cpp:283-294), same columns and formats."""
+    with open(path, "w") as f:
+        f.write("solver,iter,elapsed_s,objective,nnz_x,matvecs,extra\n")
+        for s in trace.samples:
+            f.write("%s,%d,%.6f,%.17g,%d,%.3f,%d\n" % (trace.solver, s.iter, s.elapsed_s, s.objective,
+                                                       s.nnz, s.matvecs, s.extra))
 
 
 def verify_optimality(inst: ProblemInstance, tol: float) -> CertificateReport:
