@@ -253,7 +253,8 @@ struct PcgArgs {
   const double *pre, *d2psi;
   double *p, *hav, *hp, *r, *step, *best;
   NcgDev* st;
-  double* partials;
+  double* partials;  // >= 6 x grid doubles
+  double* p2;        // second direction buffer (n)
 };
 
 template <int NS>
@@ -276,7 +277,34 @@ __device__ __forceinline__ void fold_partials(const double* partials, double (&t
   __syncthreads();
 }
 
-template <typename PtrT>
+// sum_q val[q] * f(idx[q]) over [q0, q1), ascending from 0.0 (the SpMV line
+// sum); K >= q1 - q0: all index / value loads are issued before the gathers
+template <int K, typename PtrT, class F>
+__device__ __forceinline__ double line_sum(PtrT q0, PtrT q1, const uint32_t* __restrict__ idx,
+                                           const double* __restrict__ val, F f) {
+  if (K == 0) {
+    double sum = 0.0;
+    for (PtrT q = q0; q < q1; ++q) sum += val[q] * f(idx[q]);
+    return sum;
+  }
+  uint32_t c[K > 0 ? K : 1];
+  double v[K > 0 ? K : 1], g[K > 0 ? K : 1];
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    const bool in = q0 + e < q1;
+    c[e] = in ? idx[q0 + e] : 0u;
+    v[e] = in ? val[q0 + e] : 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < K; ++e) g[e] = q0 + e < q1 ? f(c[e]) : 0.0;
+  double sum = 0.0;
+#pragma unroll
+  for (int e = 0; e < K; ++e)
+    if (q0 + e < q1) sum += v[e] * g[e];
+  return sum;
+}
+
+template <typename PtrT, int K = 0>
 __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -288,36 +316,58 @@ __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
   const double tau = st->tau, eta = st->eta, rhs_norm = st->rhs_norm;
   const uint64_t max_iters = st->max_iters;
   double rz = st->rz, best_norm = st->best_norm, php = 0.0, alpha = 0.0, beta = 0.0, rn = 0.0;
-  int done = st->done, converged = st->converged, negcurv = 0, error = 0;
+  int done = st->done, converged = st->converged, negcurv = 0, error = 0, improved = 0;
   uint64_t it = 0;
+  // p_k in pc; Kd of iteration k-1 (best copy, p_k = z + beta p_{k-1}) is folded
+  // into Ka of iteration k: A p_k gathers p_k = r/pre + beta p_{k-1} on the fly
+  // (the same operations as the stored p_k) while the owners write it to pn.
+  // Two partial buffers (p.hp / the r sums) so that one fold needs no barrier.
+  double* pc = P.p;
+  double* pn = P.p2;
+  double* part_b = P.partials;
+  double* part_c = P.partials + 4 * (size_t)gridDim.x;
+  bool first = true;
   while (!done) {
-    // Ka: hav = A p
-    for (uint64_t i = t0; i < P.a_lines; i += gsz) {
-      double sum = 0.0;
-      for (PtrT q = ap[i]; q < ap[i + 1]; ++q) sum += P.a_val[q] * __ldcg(P.p + P.a_idx[q]);
-      P.hav[i] = sum;
+    if (first) {  // Ka: hav = A p_0
+      for (uint64_t i = t0; i < P.a_lines; i += gsz)
+        P.hav[i] = line_sum<K>(ap[i], ap[i + 1], P.a_idx, P.a_val,
+                               [&](uint32_t c) { return __ldcg(pc + c); });
+    } else {  // Kd of the last iteration + Ka
+      for (uint64_t i = t0; i < P.n; i += gsz) {
+        if (improved) P.best[i] = P.step[i];  // (:245-248)
+        pn[i] = P.r[i] / P.pre[i] + beta * pc[i];  // p = z + beta p (:259)
+      }
+      for (uint64_t i = t0; i < P.a_lines; i += gsz)
+        P.hav[i] = line_sum<K>(ap[i], ap[i + 1], P.a_idx, P.a_val, [&](uint32_t c) {
+          return __ldcg(P.r + c) / P.pre[c] + beta * __ldcg(pc + c);
+        });
+      double* t = pc;
+      pc = pn;
+      pn = t;
     }
+    first = false;
     grid.sync();
     // Kb: hp = A^T hav + tau d2psi p (solvers.cpp:537-541), p.hp
     {
       double acc[1] = {0.0};
       for (uint64_t j = t0; j < P.n; j += gsz) {
-        double g = 0.0;
-        for (PtrT q = tp[j]; q < tp[j + 1]; ++q) g += P.t_val[q] * __ldcg(P.hav + P.t_idx[q]);
-        const double pj = __ldcg(P.p + j);
+        const double g = line_sum<K>(tp[j], tp[j + 1], P.t_idx, P.t_val,
+                                     [&](uint32_t c) { return __ldcg(P.hav + c); });
+        const double pj = pc[j];
         const double h = g + tau * P.d2psi[j] * pj;
         P.hp[j] = h;
         acc[0] += pj * h;
       }
       block_sum<1>(acc);
-      if (threadIdx.x == 0) P.partials[blockIdx.x] = acc[0];
+      if (threadIdx.x == 0) part_b[blockIdx.x] = acc[0];
     }
     grid.sync();
     {
       double tot[1];
-      fold_partials<1>(P.partials, tot);
+      fold_partials<1>(part_b, tot);
       php = tot[0];  // solvers.cpp:231-237
     }
+    improved = 0;
     if (!(php > 0.0)) {
       if (!isfinite(php)) error = 1;
       negcurv = 1;
@@ -325,29 +375,27 @@ __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
       break;
     }
     alpha = rz / php;
-    grid.sync();  // partials are reused below
     // Kc: step += alpha p; r -= alpha hp (:238-241); ||r||^2, r.z
     {
       double acc[2] = {0.0, 0.0};
       for (uint64_t i = t0; i < P.n; i += gsz) {
-        P.step[i] += alpha * __ldcg(P.p + i);
-        const double ri = P.r[i] - alpha * __ldcg(P.hp + i);
+        P.step[i] += alpha * pc[i];
+        const double ri = P.r[i] - alpha * P.hp[i];
         P.r[i] = ri;
         acc[0] += ri * ri;
         acc[1] += ri * (ri / P.pre[i]);
       }
       block_sum<2>(acc);
       if (threadIdx.x == 0) {
-        P.partials[(size_t)blockIdx.x * 2] = acc[0];
-        P.partials[(size_t)blockIdx.x * 2 + 1] = acc[1];
+        part_c[(size_t)blockIdx.x * 2] = acc[0];
+        part_c[(size_t)blockIdx.x * 2 + 1] = acc[1];
       }
     }
     grid.sync();
     double tot[2];
-    fold_partials<2>(P.partials, tot);
+    fold_partials<2>(part_c, tot);
     rn = sqrt(tot[0]);
     ++it;
-    int improved = 0;
     if (!isfinite(rn)) {
       error = 2;
       done = 1;
@@ -365,13 +413,10 @@ __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
       rz = tot[1];
       if (it >= max_iters) done = 1;
     }
-    // Kd: best = step when improved (:245-248); p = z + beta p (:259)
-    for (uint64_t i = t0; i < P.n; i += gsz) {
-      if (improved) P.best[i] = P.step[i];
-      if (!done) P.p[i] = P.r[i] / P.pre[i] + beta * P.p[i];
-    }
-    grid.sync();
   }
+  // Kd of the last iteration: the best-iterate copy only
+  if (improved)
+    for (uint64_t i = t0; i < P.n; i += gsz) P.best[i] = P.step[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->rz = rz;
     st->php = php;
@@ -389,11 +434,11 @@ __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
 }
 
 // grid of the cooperative PCG loop (0: not applicable -> the four-kernel loop)
-template <typename PtrT>
+template <typename PtrT, int K>
 int pcg_loop_grid() {
   static const int cap = [] {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_loop_kernel<PtrT>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_loop_kernel<PtrT, K>, kThreads, 0) !=
         cudaSuccess) {
       cudaGetLastError();
       return 0;
@@ -488,7 +533,7 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
     L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
     bufs.push_back((void*)*ptr);
   };
-  double *x, *r, *grad, *d2psi, *pre, *ad, *hav, *rp, *pp, *hp, *step, *best, *partials, *scal;
+  double *x, *r, *grad, *d2psi, *pre, *ad, *hav, *rp, *pp, *pp2, *hp, *step, *best, *partials, *scal;
   unsigned int* tickets;
   NcgDev* dst;
   NcgDev* h = nullptr;
@@ -508,6 +553,7 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
     alloc(&hav, m * 8);
     alloc(&rp, n * 8);
     alloc(&pp, n * 8);
+    alloc(&pp2, n * 8);
     alloc(&hp, n * 8);
     alloc(&step, n * 8);
     alloc(&best, n * 8);
@@ -526,11 +572,20 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
     h->max_iters = cfg->pcg_max_iters;
     L1B_CUDA(cudaMemcpyAsync(dst, h, sizeof(NcgDev), cudaMemcpyHostToDevice, st));
     // cooperative PCG loop for small / medium n (L1B_PERSIST=0: four kernels)
-    int coop_grid = 0;
+    int coop_grid = 0, pcg_k = 0;
     {
       const char* e = getenv("L1B_PERSIST");
-      if (!(e && e[0] == '0') && n <= (1ull << 21) && v.A.ptr32 == v.At.ptr32)
-        coop_grid = v.A.ptr32 ? pcg_loop_grid<uint32_t>() : pcg_loop_grid<uint64_t>();
+      if (!(e && e[0] == '0') && n <= (1ull << 21) && v.A.ptr32 == v.At.ptr32) {
+        // lines of <= 2 / 4 entries (1 / 2 stages): unrolled gathers
+        const uint64_t lmax = std::max<uint64_t>(v.max_row_nnz, v.max_col_nnz);
+        pcg_k = lmax <= 2 ? 2 : lmax <= 4 ? 4 : 0;
+        if (v.A.ptr32)
+          coop_grid = pcg_k == 2 ? pcg_loop_grid<uint32_t, 2>() : pcg_k == 4 ? pcg_loop_grid<uint32_t, 4>()
+                                                                            : pcg_loop_grid<uint32_t, 0>();
+        else
+          coop_grid = pcg_k == 2 ? pcg_loop_grid<uint64_t, 2>() : pcg_k == 4 ? pcg_loop_grid<uint64_t, 4>()
+                                                                            : pcg_loop_grid<uint64_t, 0>();
+      }
     }
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] {
@@ -602,10 +657,15 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
       uint64_t launched = 0, chunk = 4;
       if (coop_grid > 0) {  // the whole solve in one cooperative launch
         PcgArgs pa{v.A.ptr, v.A.idx, v.A.val, v.A.lines, v.At.ptr, v.At.idx, v.At.val, n,
-                   pre, d2psi, pp, hav, hp, rp, step, best, dst, partials};
+                   pre, d2psi, pp, hav, hp, rp, step, best, dst, partials, pp2};
         void* args[] = {&pa};
-        const void* fn = v.A.ptr32 ? (const void*)pcg_loop_kernel<uint32_t>
-                                   : (const void*)pcg_loop_kernel<uint64_t>;
+        const void* fn =
+            v.A.ptr32 ? (pcg_k == 2   ? (const void*)pcg_loop_kernel<uint32_t, 2>
+                         : pcg_k == 4 ? (const void*)pcg_loop_kernel<uint32_t, 4>
+                                      : (const void*)pcg_loop_kernel<uint32_t, 0>)
+                      : (pcg_k == 2   ? (const void*)pcg_loop_kernel<uint64_t, 2>
+                         : pcg_k == 4 ? (const void*)pcg_loop_kernel<uint64_t, 4>
+                                      : (const void*)pcg_loop_kernel<uint64_t, 0>);
         L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(coop_grid), dim3(kThreads), args, 0, st));
         L1B_LAUNCHED();
         launched = cfg->pcg_max_iters;  // skip the four-kernel loop
