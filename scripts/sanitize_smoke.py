@@ -13,6 +13,8 @@ from paper_1503_03520_b200 import l1bench  # noqa: E402
 
 TH = 2 * math.pi / 10
 for kw in [dict(n=1000, stages=4, q=1, s_divisor=50, seed=3), dict(n=101, stages=3, q=2, seed=11, s_divisor=10),
+           dict(n=777, stages=1, q=1, s_divisor=20, seed=5, solution="spectral"),
+           dict(n=515, stages=2, q=1, s_divisor=20, seed=6, solution="two_value"),
            dict(n=96, m_ratio=1.5, stages=3, left_stages=2, permute=True, q=1, seed=7, s_divisor=16)]:
     inst = l1bench.build_instance(theta=TH, **kw)
     banded = not kw.get("permute")
@@ -36,5 +38,7 @@ import test_gpu_shards as T  # noqa: E402
 T.KW = dict(n=4096, stages=4, q=1, s_divisor=100, seed=3, theta=TH)
 for op in ("matrix_free", "sparse"):
     T.test_shards_reproduce_single_device_fista(2, op)
+T.KW_PERM = dict(n=1024, stages=2, left_stages=1, permute=True, q=1, s_divisor=50, seed=6, theta=TH)
+T.test_general_shards_reproduce_single_device_fista(2)
 torch.cuda.synchronize()
 print("sanitize smoke done")
