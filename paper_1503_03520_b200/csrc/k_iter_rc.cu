@@ -33,6 +33,14 @@
 //   g       = G u                                              (A^T r_y)
 //   y       = x_k + beta (x_k - x_{k-1});  trial = S(y - g/L, tau/L)   (:325-336)
 //   own:      x_{k+1} = trial; ||x_{k+1}||_1, nnz, #(trial != y); ||r_k||^2
+//
+// Kernels in this file:
+//   fista_rc_kernel      one iteration per launch (shards with L1B_RC2=0, odd
+//                        remainders, the flush that records the last iterate)
+//   fista_rc2v_kernel    TWO iterations per launch, V entries per lane (the
+//                        default, V = 8: 24n bytes per iteration)
+//   fista_rc_persistent  up to a chunk of iterations in one cooperative
+//                        launch (small instances, n <= 2^20)
 #include "common.cuh"
 #include "fista.cuh"
 #include "kernels.hpp"
@@ -309,12 +317,6 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
 // (halo 16 for 3-4 stages, 96 own entries of 128); five chain runs per two
 // iterations.  Per entry the operations are those of segment(): identical
 // iterates.
-template <int S>
-struct RcGeom2 {
-  static constexpr int H3 = (4 * S + 3) / 4 * 4;
-  static constexpr int OWN = kWin - 2 * H3;
-};
-
 struct Acc2 {
   double rr0 = 0.0, l1a = 0.0, rr1 = 0.0, l1b = 0.0;  // ||r_k||^2, ||x_{k+1}||_1, ||r_{k+1}||^2, ||x_{k+2}||_1
   unsigned nza = 0, misa = 0, nzb = 0, misb = 0;
@@ -324,151 +326,6 @@ struct Rc2Out {
   double* x1;  // x_{k+1}
   double* x2;  // x_{k+2}
 };
-
-template <bool FAST>
-__device__ __forceinline__ void store_own(double* dst, int64_t e0, const bool (&mine)[4],
-                                          bool lane_own, const double (&v)[4]) {
-  if (FAST) {
-    if (lane_own) st4(dst + e0, v);
-  } else if (mine[0] && mine[3]) {
-    st4(dst + e0, v);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (mine[i]) dst[e0 + i] = v[i];
-  }
-}
-
-template <int S, bool FAST, int PAR>
-__device__ __forceinline__ void segment2(const RcArgs& A, const Rc2Out& O, const Seg& d, int64_t w0,
-                                         int lane, bool lane_own, double beta_a, double beta_b,
-                                         double inv_l, double thr, Acc2& acc) {
-  using G = RcGeom2<S>;
-  const int64_t n = A.n;
-  const int64_t e0 = w0 + 4 * lane;
-  bool mine[4];
-  if (FAST) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mine[i] = lane_own;
-  } else {
-    const int64_t own_lo = w0 + G::H3, own_hi = min(own_lo + G::OWN, A.hi);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mine[i] = e0 + i >= own_lo && e0 + i < own_hi;
-  }
-  // iteration k+1
-  double t[2][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    t[0][i] = d.xk[i];
-    t[1][i] = d.xm[i];
-  }
-  wchain<S, true, FAST, 2, PAR>(t, e0, n, A.right);
-  double rk[4], g[1][4], rr = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    rk[i] = d.sg[i] * t[0][i] - d.bb[i];
-    if (mine[i]) rr += rk[i] * rk[i];
-    const double rm = d.sg[i] * t[1][i] - d.bb[i];
-    g[0][i] = d.sg[i] * ((1.0 + beta_a) * rk[i] - beta_a * rm);
-  }
-  acc.rr0 += rr;
-  wchain<S, false, FAST, 1, PAR>(g, e0, n, A.right);
-  double x1[1][4], l1 = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double y = d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
-    double v = shrink(y - inv_l * g[0][i], thr);
-    l1 += mine[i] ? fabs(v) : 0.0;
-    acc.nza += (unsigned)(mine[i] & (v != 0.0));
-    acc.misa += (unsigned)(mine[i] & (v != y));
-    if (!FAST && (e0 + i < 0 || e0 + i >= n)) v = 0.0;  // outside [0, n): no entry
-    x1[0][i] = v;
-  }
-  acc.l1a += l1;
-  store_own<FAST>(O.x1, e0, mine, lane_own, x1[0]);
-  // iteration k+2: r_{k+1} from x_{k+1}; r_k reused
-  double t1[1][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) t1[0][i] = x1[0][i];
-  wchain<S, true, FAST, 1, PAR>(t1, e0, n, A.right);
-  double rr1 = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double r1 = d.sg[i] * t1[0][i] - d.bb[i];
-    if (mine[i]) rr1 += r1 * r1;
-    g[0][i] = d.sg[i] * ((1.0 + beta_b) * r1 - beta_b * rk[i]);
-  }
-  acc.rr1 += rr1;
-  wchain<S, false, FAST, 1, PAR>(g, e0, n, A.right);
-  double x2[4], l1b = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double y = x1[0][i] + beta_b * (x1[0][i] - d.xk[i]);
-    x2[i] = shrink(y - inv_l * g[0][i], thr);
-    l1b += mine[i] ? fabs(x2[i]) : 0.0;
-    acc.nzb += (unsigned)(mine[i] & (x2[i] != 0.0));
-    acc.misb += (unsigned)(mine[i] & (x2[i] != y));
-  }
-  acc.l1b += l1b;
-  store_own<FAST>(O.x2, e0, mine, lane_own, x2);
-}
-
-template <int S, int MB, int PAR>
-__global__ void __launch_bounds__(kRcThreads, MB) fista_rc2_kernel(RcArgs A, Rc2Out O) {
-  using G = RcGeom2<S>;
-  FistaDev* st = A.b.st;
-  if (*(volatile int*)&st->stop) return;
-  const double beta_a = st->beta_y;  // x_{k+1} (set by the last finalize)
-  double t_next, beta_b;             // x_{k+2}: the next step of the t-sequence
-  fista_momentum(st, &t_next, &beta_b);
-  const double inv_l = 1.0 / st->lval;
-  const double thr = st->tau * inv_l;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool lane_own = 4 * lane >= G::H3 && 4 * lane < G::H3 + G::OWN;
-  const int64_t n = A.n, lo = A.lo, hi = A.hi;
-  const int64_t lim_lo = max((int64_t)0, lo - G::H3), lim_hi = min(n, hi + G::H3);
-  const int64_t nseg = (hi - lo + G::OWN - 1) / G::OWN;
-  const int64_t stride = (int64_t)gridDim.x * kRcWarps;
-  Acc2 acc;
-  auto w0_of = [&](int64_t q) { return lo + q * G::OWN - G::H3; };
-  auto full_of = [&](int64_t w0) { return w0 >= lim_lo && w0 + kWin <= lim_hi; };
-  const int64_t base = lo - G::H3;
-  const int64_t w_min = max((int64_t)2, lim_lo), w_max = min(lim_hi, n - 1) - kWin;
-  const int64_t q_lo = w_min <= base ? 0 : (w_min - base + G::OWN - 1) / G::OWN;
-  const int64_t q_hi = w_max < base ? 0 : min((w_max - base) / G::OWN + 1, (hi - lo) / G::OWN);
-  Seg sa, sb;
-  int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
-  if (q < nseg) load_seg(A, w0_of(q) + 4 * lane, full_of(w0_of(q)), lim_lo, lim_hi, sa);
-  for (; q < nseg; q += stride) {
-    if (q + stride < nseg) {
-      const int64_t w1 = w0_of(q + stride);
-      load_seg(A, w1 + 4 * lane, full_of(w1), lim_lo, lim_hi, sb);
-    }
-    if (q >= q_lo && q < q_hi)
-      segment2<S, true, PAR>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
-    else
-      segment2<S, false, PAR>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
-    sa = sb;
-  }
-  double sums[8] = {acc.rr0, acc.l1a, (double)acc.nza, (double)acc.misa,
-                    acc.rr1, acc.l1b, (double)acc.nzb, (double)acc.misb};
-  double tot[8];
-  if (grid_sum<8>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
-    // scal8 = ||r_k||^2, l1 / nnz / mism of x_{k+1}, ||r_{k+1}||^2, l1 / nnz / mism of x_{k+2}
-    st->scal8[0] = tot[0];
-    st->scal8[1] = tot[1];
-    st->scal8[2] = tot[2];
-    st->scal8[3] = tot[3];
-    st->scal8[4] = tot[4];
-    st->scal8[5] = tot[5];
-    st->scal8[6] = tot[6];
-    st->scal8[7] = tot[7];
-    if (st->defer)
-      st->pair_pending = 1;  // shards: recorded by the finalize after the all-reduce
-    else
-      fista_finalize_lagged2(st, A.b.trace);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // The two-iteration kernel with V entries per lane (window 32 V): the halo
@@ -858,20 +715,13 @@ int rc2_variant() {
 template <int S, int PAR>
 void launch_rc2(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
   // measured at C4 (iter/s): V=8 + prefetch, 1 CTA/SM (255 registers) 1843;
-  // V=6 + prefetch 1682; V=8 without prefetch 1466; V=4 (fista_rc2_kernel) 1468
+  // V=6 + prefetch 1682; V=8 without prefetch 1466; V=4 + prefetch, 2 CTAs/SM 1468
   switch (rc2_variant()) {
-    case 1: break;  // V = 4: fista_rc2_kernel below
+    case 1: return launch_rc2v<S, PAR, 2, 4, true>(a, o, st);
     case 2: return launch_rc2v<S, PAR, 1, 6, true>(a, o, st);
     case 3: return launch_rc2v<S, PAR, 1, 8, false>(a, o, st);
     default: return launch_rc2v<S, PAR, 1, 8, true>(a, o, st);
   }
-  using G = RcGeom2<S>;
-  const int grid_cap = grid_cap_of<fista_rc2_kernel<S, 2, PAR>>();
-  const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
-  const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc2_kernel<S, 2, PAR><<<grid, kRcThreads, 0, st>>>(a, o);
-  L1B_LAUNCHED();
 }
 
 // min CTAs/SM; L1B_RC_VARIANT picks (tuning runs)
