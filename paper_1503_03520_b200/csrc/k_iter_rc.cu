@@ -187,7 +187,8 @@ __device__ __forceinline__ double shrink(double v, double t) {
 // shard's x windows and the segment owns OWN full entries, so every pair
 // exists and a lane's four entries are either all own (lane_own) or all halo.
 // FLUSH: only ||r_k||^2 of the own rows (the objective of the last iterate).
-template <int S, bool FAST, bool FLUSH, int PAR>
+// SMEM: x_next is shared memory (generic stores instead of 256-bit global ones).
+template <int S, bool FAST, bool FLUSH, int PAR, bool SMEM = false>
 __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w0, int lane,
                                         bool lane_own, double beta, double inv_l, double thr,
                                         Acc& acc) {
@@ -235,7 +236,11 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
     acc.mism += (unsigned)(mine[i] & (tr[i] != y));
   }
   acc.l1 += l1;
-  if (FAST) {
+  if (SMEM) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (mine[i]) A.b.x_next[e0 + i] = tr[i];
+  } else if (FAST) {
     if (lane_own) st4(A.b.x_next + e0, tr);
   } else if (mine[0] && mine[3]) {
     st4(A.b.x_next + e0, tr);
@@ -668,6 +673,119 @@ int grid_cap_of() {
   return cap;
 }
 
+// Small instances that fit in shared memory (C1: n = 2^12): ONE CTA of 32
+// warps runs the chunk with sigma, b and the four x buffers resident in shared
+// memory (zero-padded by H3 on both sides) and the FISTA state in a shared
+// copy of FistaDev: an iteration costs block barriers and shared-memory
+// traffic only.  Same segment code, same bookkeeping => the same iterates.
+constexpr int kSmallThreads = 512;
+
+template <int S>
+struct SmallGeom {
+  static constexpr int P = RcGeom<S>::H3;  // padding on both sides (entries)
+};
+
+__host__ __device__ inline uint64_t small_stride(uint64_t n, int pad) {
+  return (n + 2 * (uint64_t)pad + 3) / 4 * 4;
+}
+
+template <int S, int PAR>
+__global__ void __launch_bounds__(kSmallThreads, 1) fista_rc_small(RcPArgs P) {
+  using G = RcGeom<S>;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ FistaDev sst;
+  const RcArgs& A0 = P.a;
+  const int64_t n = A0.n;
+  const int pad = SmallGeom<S>::P;
+  const uint64_t N = small_stride((uint64_t)n, pad);
+  double* s_sig = sm;
+  double* s_b = sm + N;
+  double* s_x[4] = {sm + 2 * N, sm + 3 * N, sm + 4 * N, sm + 5 * N};
+  const int t = threadIdx.x;
+  if (t == 0) sst = *A0.b.st;
+  for (uint64_t q = t; q < N; q += blockDim.x) {
+    const int64_t g = (int64_t)q - pad;
+    const bool in = g >= 0 && g < n;
+    s_sig[q] = in ? A0.sigma[g] : 0.0;
+    s_b[q] = in ? A0.b.b[g] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s_x[k][q] = in ? P.X[k][g] : 0.0;
+  }
+  __syncthreads();
+  const int lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
+  const bool lane_own = 4 * lane >= G::H3 && 4 * lane < G::H3 + G::OWN;
+  const int64_t nseg = (n + G::OWN - 1) / G::OWN;
+  RcArgs A = A0;
+  A.lo = 0;
+  A.hi = n;
+  A.sigma = s_sig + pad;  // global-index views of the padded arrays
+  A.b.b = s_b + pad;
+  for (uint64_t it = 0; it < P.iters; ++it) {
+    if (sst.stop) break;  // uniform: read after the last barrier
+    const uint64_t j = P.j0 + it;
+    A.b.x_k = s_x[j % 4] + pad;
+    A.b.x_km1 = s_x[(j + 3) % 4] + pad;
+    A.b.x_next = s_x[(j + 1) % 4] + pad;
+    const double beta = sst.beta_y;
+    const double inv_l = 1.0 / sst.lval;
+    const double thr = sst.tau * inv_l;
+    Acc acc;
+    for (int64_t q = warp; q < nseg; q += nwarps) {
+      const int64_t w0 = q * G::OWN - G::H3;
+      const int64_t e = w0 + 4 * lane;  // window entries read from the padded arrays
+      Seg d;
+      const bool inpad = e >= -pad && e + 4 <= n + pad;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t g = e + i;
+        const bool ok = inpad || (g >= -pad && g < n + pad);
+        d.xk[i] = ok ? A.b.x_k[g] : 0.0;
+        d.xm[i] = ok ? A.b.x_km1[g] : 0.0;
+        d.sg[i] = ok ? A.sigma[g] : 0.0;
+        d.bb[i] = ok ? A.b.b[g] : 0.0;
+      }
+      const bool fast = w0 >= 2 && w0 + kWin < n && w0 + G::H3 + G::OWN <= n;
+      if (fast)
+        segment<S, true, false, PAR, true>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+      else
+        segment<S, false, false, PAR, true>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+    }
+    double sums[4] = {acc.l1, (double)acc.nz, (double)acc.mism, acc.rr};
+    block_sum<4>(sums);  // (ends with a barrier: every x_{k+1} entry is written)
+    if (t == 0) {
+      sst.scal[0] = sums[0];
+      sst.scal[1] = sums[1];
+      sst.scal[2] = sums[2];
+      sst.scal[3] = sums[3];
+      fista_finalize_lagged(&sst, A0.b.trace, false);
+    }
+    __syncthreads();
+  }
+  for (uint64_t q = t; q < (uint64_t)n; q += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) P.X[k][q] = s_x[k][q + pad];
+  }
+  if (t == 0) *A0.b.st = sst;
+}
+
+template <int S, int PAR>
+bool launch_rc_small(const RcPArgs& p, cudaStream_t st) {
+  const size_t bytes = 6 * small_stride(p.a.n, SmallGeom<S>::P) * sizeof(double);
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    max_dyn = std::max(0, optin - (int)sizeof(FistaDev) - 1024);
+    L1B_CUDA(cudaFuncSetAttribute(fista_rc_small<S, PAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_dyn));
+  }
+  if (bytes > (size_t)max_dyn) return false;
+  fista_rc_small<S, PAR><<<1, kSmallThreads, bytes, st>>>(p);
+  L1B_LAUNCHED();
+  return true;
+}
+
 template <int S, int PAR>
 void launch_rc_persistent(const RcPArgs& p, cudaStream_t st) {
   const int grid_cap = grid_cap_of<fista_rc_persistent<S, PAR>>();
@@ -788,6 +906,15 @@ void fista_rc_prepare(const OpView& op) {
   }
 }
 
+bool small_enabled() {  // L1B_SMALL=0: the cooperative multi-CTA loop for every size
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("L1B_SMALL");
+    on = !(e && e[0] == '0');
+  }
+  return on != 0;
+}
+
 void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uint64_t j0,
                    uint64_t iters, uint64_t lo, uint64_t hi, cudaStream_t st) {
   if (lo % 4 != 0) throw std::invalid_argument("fista_rc_loop: block start must be a multiple of 4");
@@ -801,6 +928,17 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
   for (int q = 0; q < 4; ++q) p.X[q] = X[q];
   p.j0 = j0;
   p.iters = iters;
+  if (lo == 0 && hi == op.n && small_enabled()) {  // one CTA, everything in shared memory
+    bool done = false;
+    switch (op.right.count) {
+      case 1: done = is_canon<1>(op.right) ? launch_rc_small<1, canon_par<1>()>(p, st) : launch_rc_small<1, -1>(p, st); break;
+      case 2: done = is_canon<2>(op.right) ? launch_rc_small<2, canon_par<2>()>(p, st) : launch_rc_small<2, -1>(p, st); break;
+      case 3: done = is_canon<3>(op.right) ? launch_rc_small<3, canon_par<3>()>(p, st) : launch_rc_small<3, -1>(p, st); break;
+      case 4: done = is_canon<4>(op.right) ? launch_rc_small<4, canon_par<4>()>(p, st) : launch_rc_small<4, -1>(p, st); break;
+      default: break;
+    }
+    if (done) return;
+  }
   switch (op.right.count) {
     case 1: return is_canon<1>(op.right) ? launch_rc_persistent<1, canon_par<1>()>(p, st) : launch_rc_persistent<1, -1>(p, st);
     case 2: return is_canon<2>(op.right) ? launch_rc_persistent<2, canon_par<2>()>(p, st) : launch_rc_persistent<2, -1>(p, st);

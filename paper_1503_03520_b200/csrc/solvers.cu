@@ -329,9 +329,16 @@ bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
   return true;
 }
 
+// small single-device recomputing sessions step through fista_rc_loop (one
+// launch per chunk; also for single iterations, so that every iteration of a
+// session reduces its sums in the same order)
+bool uses_loop(const l1b_session* s) {
+  return s->recompute && !s->shard && s->v.n <= kPersistMaxN && persist_enabled();
+}
+
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
-  if (s->recompute && !s->shard && s->v.n <= kPersistMaxN && iters > 1 && persist_enabled()) {
+  if (uses_loop(s)) {
     fista_rc_loop(*s->v.op, s->iter_bufs(s->launched), s->X, s->launched, iters, 0, s->v.n,
                   s->v.stream);
     s->launched += iters;
@@ -359,7 +366,15 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
                     double* x_host, double* d_x) {
   cudaStream_t st = s->v.stream;
   // the recomputing kernel records each iterate one kernel late: record the last one
-  if (s->recompute && !s->shard) s->iterate(s->launched, st, true);  // shards: l1b_session_flush
+  // (shards: l1b_session_flush).  Loop sessions record it with one more
+  // iteration of the loop kernel (its x is discarded), so that every record
+  // of a small instance reduces its sums the same way.
+  if (s->recompute && !s->shard) {
+    if (uses_loop(s))
+      fista_rc_loop(*s->v.op, s->iter_bufs(s->launched), s->X, s->launched, 1, 0, s->v.n, st);
+    else
+      s->iterate(s->launched, st, true);
+  }
   L1B_CUDA(cudaMemcpyAsync(s->h_st, s->st, sizeof(FistaDev), cudaMemcpyDeviceToHost, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   const FistaDev h = *s->h_st;
@@ -569,10 +584,30 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     std::vector<cudaEvent_t> ev(3 * iters);
     for (auto& e : ev) L1B_CUDA(cudaEventCreate(&e));
     const FistaBufs b = s->bufs();
+    if (uses_loop(s)) {  // one-iteration launches of the loop kernel, timed each
+      for (uint64_t i = 0; i < iters; ++i) {
+        L1B_CUDA(cudaEventRecord(ev[3 * i], st));
+        fista_rc_loop(*s->v.op, s->iter_bufs(s->launched + i), s->X, s->launched + i, 1, 0, s->v.n, st);
+        L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
+        L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
+      }
+      s->launched += iters;
+      L1B_CUDA(cudaStreamSynchronize(st));
+      double k1 = 0.0, k2 = 0.0;
+      for (uint64_t i = 0; i < iters; ++i) {
+        float a = 0.f, c = 0.f;
+        L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+        L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));
+        k1 += a;
+        k2 += c;
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+      ms_out[0] = k1;
+      ms_out[1] = k2;
+      return;
+    }
     // two-iteration launches, timed each -- where session_step uses them too
-    // (small instances step through the cooperative loop: single iterations)
-    if (s->recompute && !s->shard && rc2_enabled() &&
-        !(s->v.n <= kPersistMaxN && persist_enabled())) {
+    if (s->recompute && !s->shard && rc2_enabled()) {
       uint64_t i = 0;
       for (; i < iters; i += 2) {
         L1B_CUDA(cudaEventRecord(ev[3 * i], st));
