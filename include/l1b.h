@@ -312,6 +312,19 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out);
 /* Lagged shard sessions: sums ||r||^2 of the last iterate into scal (a no-op
  * for other sessions; single-device sessions flush inside l1b_session_end). */
 int l1b_session_flush(l1b_session* s);
+/* Peer halos (lagged shards): the kernels store the new x entries within
+ * x_halo of the block ends straight into the neighbours' x buffers (over
+ * NVLink for other devices), so the caller skips the halo exchange and keeps
+ * only the scalar all-reduce (whose completion orders the stores before the
+ * neighbours' next kernels).  attach_peers takes the neighbours' x_bufs
+ * (4 each, NULL for no neighbour) as pointers valid on this device (same
+ * device, or peer access enabled); the IPC pair exchanges them between
+ * processes (4 cudaIpcMemHandle_t = 4 x 64 bytes per session).               */
+int l1b_session_attach_peers(l1b_session* s, double* const* left_bufs, uint64_t left_row_begin,
+                             double* const* right_bufs, uint64_t right_row_begin);
+int l1b_session_export_x_ipc(l1b_session* s, void* handles);
+int l1b_session_attach_peers_ipc(l1b_session* s, const void* left_handles, uint64_t left_row_begin,
+                                 const void* right_handles, uint64_t right_row_begin);
 /* General shards: prox / momentum on the own columns from the reduced g.     */
 int l1b_session_prox(l1b_session* s);
 /* Which FISTA kernels a session runs (bench roofline bookkeeping):

@@ -137,6 +137,9 @@ SIGNATURES = [
     ("l1b_session_finalize", C.c_int, [vp]),
     ("l1b_session_flush", C.c_int, [vp]),
     ("l1b_session_prox", C.c_int, [vp]),
+    ("l1b_session_attach_peers", C.c_int, [vp, P(vp), u64, P(vp), u64]),
+    ("l1b_session_export_x_ipc", C.c_int, [vp, vp]),
+    ("l1b_session_attach_peers_ipc", C.c_int, [vp, vp, u64, vp, u64]),
     ("l1b_session_kernel_mode", C.c_int, [vp, P(C.c_int)]),
 ]
 

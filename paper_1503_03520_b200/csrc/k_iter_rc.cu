@@ -69,7 +69,29 @@ struct RcArgs {
   StageTab right;
   const double* sigma;  // global index
   IterBufs b;           // x_k, x_km1, x_next, b by global index (r_* unused)
+  // row-block shards with attached peers: the new x entries within ph of the
+  // block ends are also stored straight into the neighbours' x windows
+  // (global-index views; [0]: x_{k+1}, [1]: x_{k+2}) -- the halo exchange
+  // rides on the kernel's own stores over NVLink instead of NCCL send / recv
+  PeerViews peers;
 };
+
+template <int V>
+__device__ __forceinline__ void peer_store(const RcArgs& A, int which, int64_t e0,
+                                           const bool (&mine)[V], const double (&v)[V]) {
+  if (!A.peers.on) return;
+  const int64_t lo = A.lo, hi = A.hi, ph = A.peers.halo;
+  if (e0 >= lo + ph && e0 + V <= hi - ph) return;
+  double* l = A.peers.left[which];
+  double* r = A.peers.right[which];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int64_t g = e0 + i;
+    if (!mine[i]) continue;
+    if (l && g < lo + ph) l[g] = v[i];
+    if (r && g >= hi - ph) r[g] = v[i];
+  }
+}
 
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
   asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -236,6 +258,7 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
     acc.mism += (unsigned)(mine[i] & (tr[i] != y));
   }
   acc.l1 += l1;
+  if (!SMEM) peer_store<4>(A, 0, e0, mine, tr);
   if (SMEM) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -301,6 +324,7 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
     run(q, sa);
     sa = sb;
   }
+  if (A.peers.on) __threadfence_system();  // peer stores performed before the kernel ends
   double sums[4] = {acc.l1, (double)acc.nz, (double)acc.mism, acc.rr};
   double tot[4];
   if (grid_sum<4>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
@@ -506,6 +530,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
   }
   acc.l1a += l1;
   store_ownv<FAST, V>(O.x1, e0, mine, lane_own, x1[0]);
+  peer_store<V>(A, 0, e0, mine, x1[0]);
   double t1[1][V];
 #pragma unroll
   for (int i = 0; i < V; ++i) t1[0][i] = x1[0][i];
@@ -530,6 +555,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
   }
   acc.l1b += l1b;
   store_ownv<FAST, V>(O.x2, e0, mine, lane_own, x2);
+  peer_store<V>(A, 1, e0, mine, x2);
 }
 
 template <int S, int MB, int PAR, int V, bool PF>
@@ -574,6 +600,7 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc
       load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sa);
     }
   }
+  if (A.peers.on) __threadfence_system();  // peer stores performed before the kernel ends
   double sums[8] = {acc.rr0, acc.l1a, (double)acc.nza, (double)acc.misa,
                     acc.rr1, acc.l1b, (double)acc.nzb, (double)acc.misb};
   double tot[8];
@@ -949,7 +976,7 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 }
 
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
-                    cudaStream_t st) {
+                    cudaStream_t st, const PeerViews& peers) {
   if (lo % 4 != 0) throw std::invalid_argument("fista_rc_iter2: block start must be a multiple of 4");
   RcArgs a;
   a.n = (int64_t)op.n;
@@ -958,6 +985,7 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
   a.right = op.right;
   a.sigma = op.sigma;
   a.b = ib;
+  a.peers = peers;
   const Rc2Out o{ib.x_next, x_next2};
   switch (op.right.count) {
     case 1: return is_canon<1>(op.right) ? launch_rc2<1, canon_par<1>()>(a, o, st) : launch_rc2<1, -1>(a, o, st);
@@ -989,7 +1017,7 @@ int fista_rc_halo(int stages) {
 }
 
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi,
-                   cudaStream_t st, bool flush) {
+                   cudaStream_t st, bool flush, const PeerViews& peers) {
   if (lo % 4 != 0) throw std::invalid_argument("fista_rc_iter: block start must be a multiple of 4");
   RcArgs a;
   a.n = (int64_t)op.n;
@@ -998,6 +1026,7 @@ void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t h
   a.right = op.right;
   a.sigma = op.sigma;
   a.b = ib;
+  a.peers = peers;
   switch (op.right.count * 2 + (flush ? 1 : 0)) {
     case 2: return launch_rc<1>(a, st);
     case 3: return launch_rc_flush<1>(a, st);

@@ -158,10 +158,18 @@ void fista_fused_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_
 // the same iteration with r_k, r_{k-1} recomputed from x_k, x_{k-1} (k_iter_rc.cu):
 // reads x_k, x_km1, sigma, b, writes x_next (32-byte aligned, lo % 4 == 0);
 // r_* of ib unused.  A shard's x windows need fista_rc_halo(stages) entries.
+// Neighbour shards' x windows as global-index views (x_{k+1}, x_{k+2}), for
+// kernels that store the halo entries themselves (peer memory over NVLink).
+struct PeerViews {
+  int on = 0;
+  int64_t halo = 0;
+  double* left[2] = {nullptr, nullptr};
+  double* right[2] = {nullptr, nullptr};
+};
 // The objective lags one kernel (fista_finalize_lagged); flush = true records
 // the last iterate's (x_k of ib) after the loop.
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
-                   bool flush = false);
+                   bool flush = false, const PeerViews& peers = PeerViews());
 int fista_rc_halo(int stages);
 // x-window halo of the two-iteration kernel (default 8-entries-per-lane variant)
 int fista_rc2_halo(int stages);
@@ -173,7 +181,7 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 // two iterations (x_{k+1} into ib.x_next, x_{k+2} into x_next2) in one kernel:
 // 24n bytes per iteration (k_iter_rc.cu fista_rc2_kernel); one device
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
-                    cudaStream_t st);
+                    cudaStream_t st, const PeerViews& peers = PeerViews());
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op);
 // general shards: prox / momentum on the own column slice from the reduced g

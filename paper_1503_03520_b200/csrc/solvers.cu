@@ -79,16 +79,36 @@ struct l1b_session {
 
   // launch j of the single-kernel loop (iteration j + 1)
   // launches j and j+1 as one two-iteration kernel (recomputing path, one device)
+  // neighbours' x buffers (global-index views) when the halo travels by the
+  // kernels' own peer stores (l1b_session_attach_peers)
+  bool peers_on = false;
+  double* peer_left[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* peer_right[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<void*> ipc_opened;
+  std::vector<double*> x_raw;  // cudaMalloc'd x buffers (shards: exportable over IPC)
+
+  PeerViews peers(uint64_t j) const {  // x_{j+1}, x_{j+2} of the neighbours
+    PeerViews pv;
+    if (!peers_on) return pv;
+    pv.on = 1;
+    pv.halo = (int64_t)xh;
+    for (int w = 0; w < 2; ++w) {
+      pv.left[w] = peer_left[(j + 1 + w) % 4];
+      pv.right[w] = peer_right[(j + 1 + w) % 4];
+    }
+    return pv;
+  }
+
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
     fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
-                   shard ? v.row_end : v.n, stream);
+                   shard ? v.row_end : v.n, stream, peers(j));
   }
 
   void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
     const uint64_t lo = shard ? v.row_begin : 0, hi = shard ? v.row_end : v.n;
     if (recompute)
-      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush);
+      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush, flush ? PeerViews() : peers(j));
     else
       fista_fused_iter(*v.op, iter_bufs(j), lo, hi, stream);
   }
@@ -113,6 +133,9 @@ struct l1b_session {
 
   ~l1b_session() {
     cudaSetDevice(v.device);
+    if (v.stream) cudaStreamSynchronize(v.stream);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    for (double* q : x_raw) cudaFree(q);
     for (void* q : allocs) cudaFreeAsync(q, v.stream);  // back to the stream-ordered pool
     if (v.stream) cudaStreamSynchronize(v.stream);
     if (h_st) cudaFreeHost(h_st);
@@ -201,7 +224,14 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     s->halo = s->xh;
     s->nbuf = s->recompute ? 4 : 3;
     for (int q = 0; q < s->nbuf; ++q) {
-      s->X[q] = s->dalloc(s->nx + 2 * s->xh);
+      if (s->shard && s->recompute) {  // plain allocations: exportable to peer processes (IPC)
+        double* p = nullptr;
+        L1B_CUDA(cudaMalloc(&p, (s->nx + 2 * s->xh + 2) * sizeof(double)));
+        s->x_raw.push_back(p);
+        s->X[q] = p;
+      } else {
+        s->X[q] = s->dalloc(s->nx + 2 * s->xh);
+      }
       L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
       if (s->recompute) continue;
       s->R[q] = s->dalloc(s->nr + 2 * s->rh);
@@ -503,6 +533,61 @@ int l1b_session_kernel_mode(l1b_session* s, int* mode) {
             : !s->recompute ? L1B_KMODE_STORED_RESIDUAL
             : (!s->shard && rc2_enabled()) ? L1B_KMODE_RECOMPUTE_TWO
                                            : L1B_KMODE_RECOMPUTE;
+  });
+}
+
+namespace {
+void attach_side(l1b_session* s, double* const* bufs, uint64_t peer_lo, double** out) {
+  for (int q = 0; q < 4; ++q) out[q] = bufs ? bufs[q] + (int64_t)s->xh - (int64_t)peer_lo : nullptr;
+}
+void check_peer_session(const l1b_session* s) {
+  if (!s) throw InvalidArgument("null session");
+  if (!(s->shard && s->recompute && s->nbuf == 4))
+    throw LogicError("peer halos need a row-block shard session on the recomputing kernels");
+}
+}  // namespace
+
+int l1b_session_attach_peers(l1b_session* s, double* const* left_bufs, uint64_t left_row_begin,
+                             double* const* right_bufs, uint64_t right_row_begin) {
+  return guard([&] {
+    check_peer_session(s);
+    attach_side(s, left_bufs, left_row_begin, s->peer_left);
+    attach_side(s, right_bufs, right_row_begin, s->peer_right);
+    s->peers_on = left_bufs || right_bufs;
+  });
+}
+
+int l1b_session_export_x_ipc(l1b_session* s, void* handles) {
+  return guard([&] {
+    check_peer_session(s);
+    if (!handles) throw InvalidArgument("null output");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    for (int q = 0; q < 4; ++q)
+      L1B_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handles) + q, s->X[q]));
+  });
+}
+
+int l1b_session_attach_peers_ipc(l1b_session* s, const void* left_handles, uint64_t left_row_begin,
+                                 const void* right_handles, uint64_t right_row_begin) {
+  return guard([&] {
+    check_peer_session(s);
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    double* lb[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* rb[4] = {nullptr, nullptr, nullptr, nullptr};
+    auto open = [&](const void* h, double** out) {
+      for (int q = 0; q < 4; ++q) {
+        void* p = nullptr;
+        L1B_CUDA(cudaIpcOpenMemHandle(&p, reinterpret_cast<const cudaIpcMemHandle_t*>(h)[q],
+                                      cudaIpcMemLazyEnablePeerAccess));
+        s->ipc_opened.push_back(p);
+        out[q] = static_cast<double*>(p);
+      }
+    };
+    if (left_handles) open(left_handles, lb);
+    if (right_handles) open(right_handles, rb);
+    attach_side(s, left_handles ? lb : nullptr, left_row_begin, s->peer_left);
+    attach_side(s, right_handles ? rb : nullptr, right_row_begin, s->peer_right);
+    s->peers_on = left_handles || right_handles;
   });
 }
 

@@ -161,6 +161,9 @@ class CudaShard:
         elif not self.general:
             self.x_win = device_view(b.x_win, self.own + 2 * self.halo, dev)
             self.r_y_win = device_view(b.r_y_win, self.own + 2 * self.halo, dev)
+        self.x_raw = [int(b.x_bufs[q] or 0) for q in range(4)]
+        self.row_begin = int(self.inst.info.row_begin)
+        self.peer_halos = False  # True once the kernels store the halos into the neighbours
         self.scal = device_view(b.scal, 4, dev)
         self.scal8 = device_view(b.scal8, 8, dev) if self.pairs else None
         self.scal_now = self.scal  # the sums the last step left for the all-reduce
@@ -179,6 +182,34 @@ class CudaShard:
     def flush(self):
         N.check(self._lib.l1b_session_flush(self.sess._s))
         self.scal_now = self.scal
+
+    def attach_peers_direct(self, left=None, right=None):
+        """Neighbour shards of THIS process (emulated ranks on one device, or
+        several devices with peer access): their x buffers as peer targets."""
+        def arr(sh):
+            return (C.c_void_p * 4)(*sh.x_raw) if sh is not None else None
+        N.check(self._lib.l1b_session_attach_peers(
+            self.sess._s, arr(left), left.row_begin if left is not None else 0,
+            arr(right), right.row_begin if right is not None else 0))
+        self.peer_halos = left is not None or right is not None
+
+    def attach_peers_ipc(self, group=None):
+        """One process per GPU: exchange cudaIpc handles of the x buffers
+        (all_gather_object) and attach the rank - 1 / rank + 1 neighbours."""
+        import torch.distributed as dist
+
+        h = (C.c_char * 256)()
+        N.check(self._lib.l1b_session_export_x_ipc(self.sess._s, h))
+        mine = (bytes(h), self.row_begin)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        buf = lambda r: (C.c_char * 256).from_buffer_copy(allh[r][0])  # noqa: E731
+        left = buf(self.rank - 1) if self.rank > 0 else None
+        right = buf(self.rank + 1) if self.rank < self.world - 1 else None
+        N.check(self._lib.l1b_session_attach_peers_ipc(
+            self.sess._s, left, allh[self.rank - 1][1] if left is not None else 0,
+            right, allh[self.rank + 1][1] if right is not None else 0))
+        self.peer_halos = left is not None or right is not None
 
     def prox(self):
         N.check(self._lib.l1b_session_prox(self.sess._s))
@@ -219,6 +250,27 @@ def fista_distributed(be, iterations: int, group=None, poll_every: int = 0):
             break
     finish_lagged(be, group)
     return be.finish()
+
+
+def verify_peer_halos(be, group=None):
+    """After a run with peer halos: send the boundary entries of the two newest
+    x vectors the NCCL way into scratch copies and compare them with the halos
+    the neighbours' kernels stored.  Returns "ok" or the first mismatch."""
+    import torch
+    import torch.distributed as dist
+
+    bad = torch.zeros(1, dtype=torch.float64, device=be.scal.device)
+    for q in (be.j % be.nbuf, (be.j - 1) % be.nbuf):
+        win = be.x_bufs[q]
+        tmp = win.clone()
+        halo_exchange_many([(tmp, be.x_halo)], be.own, be.rank, be.world, group)
+        h, own = be.x_halo, be.own
+        if be.rank > 0:
+            bad += (tmp[:h] != win[:h]).sum()
+        if be.rank < be.world - 1:
+            bad += (tmp[own + h:own + 2 * h] != win[own + h:own + 2 * h]).sum()
+    dist.all_reduce(bad, group=group)
+    return "ok" if bad.item() == 0 else f"{int(bad.item())} halo entries differ"
 
 
 def finish_lagged(be, group=None):
@@ -292,7 +344,8 @@ def fista_iteration(be, group=None):
         return 1
     if be.single:
         be.k1()  # the whole iteration (two when be.pairs)
-        halo_exchange_many(be.next_halos(), be.own, be.rank, be.world, group)
+        if not getattr(be, "peer_halos", False):  # else the kernel stored them into the neighbours
+            halo_exchange_many(be.next_halos(), be.own, be.rank, be.world, group)
         dist.all_reduce(getattr(be, "scal_now", be.scal), group=group)
         be.finalize()
         return 2 if getattr(be, "pairs", False) else 1
@@ -329,6 +382,13 @@ def bench_main(args, world: int, rank: int, local: int):
     cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + 10)
     be = CudaShard(kw, rank, world, local, cfg)
     gen_s = time.perf_counter() - t0
+    peer = "off"
+    if world > 1 and be.single and be.lagged and os.environ.get("L1B_PEER_HALOS", "1") != "0":
+        try:  # halos by the kernels' own stores into the neighbours (cudaIpc, NVLink)
+            be.attach_peers_ipc()
+            peer = "on"
+        except Exception as e:  # reported; the NCCL send / recv exchange stays
+            peer = f"unavailable: {e}"
     start(be)
     with ClockSampler(local) as clk:
         done = 0
@@ -351,6 +411,7 @@ def bench_main(args, world: int, rank: int, local: int):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_total = float(ms.item())
     finish_lagged(be)
+    peer_check = verify_peer_halos(be) if be.peer_halos else None
     stopped, k = be.stopped()
     tr, _ = be.finish()
     if rank == 0:
@@ -378,6 +439,7 @@ def bench_main(args, world: int, rank: int, local: int):
                                        f"row-block shards x{world}: NCCL P2P halo (2 x {be.halo} doubles "
                                        f"per neighbour per iteration) + 4-double all-reduce")},
             "gpu_launches": int(launches), "iterations_done": int(k), "generate_s": gen_s,
+            "peer_halos": peer, "peer_halo_check": peer_check,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

@@ -201,3 +201,40 @@ def test_general_shards_reproduce_single_device_fista(world):
     assert x.shape == x_ref.shape
     assert rel_err(x, x_ref) < 1e-12
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_halos_reproduce_single_device_fista(world):
+    """The kernels store the halo entries straight into the neighbours' x
+    buffers (l1b_session_attach_peers; same device here, NVLink peers on a
+    box): no halo exchange at all, the scalar all-reduce orders the steps."""
+    torch = need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    iters = 40
+    inst = l1bench.build_instance(**KW)
+    x_ref = np.empty(inst.n)
+    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, op="matrix_free"), x_ref)
+    shards = _shards(world, iters, "matrix_free")
+    for g, s in enumerate(shards):
+        s.attach_peers_direct(shards[g - 1] if g > 0 else None, shards[g + 1] if g + 1 < world else None)
+        assert s.peer_halos
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    for _ in range(iters):
+        for s in shards:  # every rank's kernel of this step before any rank's next one
+            s.k1()
+        _allreduce(shards)
+        for s in shards:
+            s.finalize()
+    for s in shards:
+        s.flush()
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    torch.cuda.synchronize()
+    outs = [s.finish() for s in shards]
+    x = np.concatenate([o[1] for o in outs])
+    np.testing.assert_array_equal(x, x_ref)
+    assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
