@@ -263,13 +263,22 @@ int l1b_session_step(l1b_session* s, uint64_t iters);
 int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms);
 int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations);
 
-/* Row-block shards (world > 1): the caller drives each FISTA iteration and
- * does the two halo exchanges and the 4-scalar all-reduce (NCCL through
- * torch.distributed, see paper_1503_03520_b200/distributed.py):
- *   begin -> [all-reduce scal, finalize] -> loop { exchange r_y halo; k1;
- *   exchange x halo; k2; all-reduce scal; finalize }
- * Windows: entry h + j of x_win / r_y_win is own column / row row_begin + j;
- * entries [0, h) and [h + own, own + 2h) are the neighbours' boundary values. */
+/* Row-block shards (world >= 1): the caller drives the FISTA loop and does the
+ * exchanges and the scalar all-reduce (NCCL through torch.distributed, see
+ * paper_1503_03520_b200/distributed.py).  Which protocol a session follows is
+ * in l1b_shard_buffers:
+ *   matrix-free, recomputing kernels (lagged = 1, the default for 1..4 stages):
+ *     begin -> [all-reduce scal, finalize] -> loop { k1 (two iterations when
+ *     pairs); x halos (or peer stores); all-reduce scal8 / scal; finalize }
+ *     -> flush; all-reduce scal; finalize
+ *   stored residuals (single = 1, lagged = 0): loop { k1; x and r halos;
+ *     all-reduce scal; finalize }
+ *   CSR/CSC two-kernel mode: loop { r_y halo; k1; x halo; k2; all-reduce scal;
+ *     finalize }
+ *   general operators (general = 1): loop { k1; reduce-scatter g_full; prox;
+ *     all-gather x_full; k2; all-reduce scal; finalize }
+ * Windows: entry h + j of a window is own column / row row_begin + j; entries
+ * [0, h) and [h + own, own + 2h) are the neighbours' boundary values.       */
 typedef struct {
   double* x_win;    /* own + 2*halo (two-kernel mode) */
   double* r_y_win;  /* own + 2*halo (two-kernel mode) */
