@@ -40,7 +40,7 @@ CONFIGS = {
 }
 
 # bounded CPU samples of the reference (oracle/_ref): (n, solver iterations)
-CPU_SAMPLE = {"c1": None, "c2": (1 << 15, 10), "c3": (1 << 19, 2), "c4": (1 << 20, 5)}
+CPU_SAMPLE = {"c1": None, "c2": (1 << 15, 10), "c3": (1 << 19, 2), "c4": (1 << 24, 3)}
 
 
 def run_gpu(name, c):
