@@ -5,6 +5,15 @@ each, the reference's own CPU solver (oracle/_ref) on a bounded sample.
 Prints one JSON object per config; `--out FILE` also writes them as a list.
 
   python configs.py [--only c1,c2,c3,c4] [--out profiles/r1_configs.json]
+  python configs.py --only c5 [--c5-ranks 0,3,7] [--c5-iters 200]
+
+C5 (n = 2^32, 8 GPUs) cannot run whole on the single GPU available here: the
+c5 entry builds the row-block shard of each requested rank of the 8-way split
+(the generator draws sigma / the fill on the device with mt19937_64
+jump-ahead, so a rank never replays or stores the 2^32-entry streams) and times
+that rank's own launches (two-iteration kernel + finalise) on the one GPU.
+The halo stores and the 8-double all-reduce of the real 8-GPU run are not in
+these numbers (no neighbours exist), so the rate is a per-rank compute figure.
 """
 import argparse
 import json
@@ -122,14 +131,73 @@ def run_cpu(name, c):
     return out
 
 
+C5 = dict(n=1 << 32, stages=4, q=0, s_divisor=10000, seed=4, theta=THETA)
+
+
+def run_c5(ranks, iters, world=8):
+    """Per-rank shards of C5 on the one GPU (see the module docstring)."""
+    import gc
+
+    import torch
+
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    out = {"config": "c5", "desc": "FISTA, n=2^32 x m=2^33, 4 stages, q=0, s=n/10000, seed 4; "
+                                   f"rank shards of the {world}-way row split, one at a time on one GPU",
+           "world": world, "iterations_timed": iters, "ranks": []}
+    for r in ranks:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh = CudaShard(C5, r, world, 0, l1bench.SolverConfig(max_iters=iters + 8, op="matrix_free"))
+        torch.cuda.synchronize()
+        gen_s = time.perf_counter() - t0
+        assert sh.single and sh.pairs, "C5 shards run the two-iteration kernel"
+        sh.finalize()  # f_0 from this rank's ||b_own||^2 (no all-reduce: one rank here)
+        for _ in range(2):
+            sh.k1()
+            sh.finalize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(iters // 2):
+            sh.k1()
+            sh.finalize()
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / (iters // 2 * 2)
+        info = sh.inst.info
+        out["ranks"].append({"rank": r, "rows": [int(info.row_begin), int(info.row_end)],
+                             "generate_s": gen_s, "ms_per_iteration": ms,
+                             "device_gb": int(info.device_bytes) / 1e9,
+                             "gbs_algorithmic": 24 * sh.own / (ms * 1e-3) / 1e9})
+        print(json.dumps(out["ranks"][-1]), flush=True)
+        del sh
+        gc.collect()
+        torch.cuda.empty_cache()
+    worst = max(x["ms_per_iteration"] for x in out["ranks"])
+    out["max_rank_ms_per_iteration"] = worst
+    out["projected_iters_per_s_compute_only"] = 1000.0 / worst
+    out["note"] = ("per-rank device time of the rank's own launches; the 8-GPU run adds the halo "
+                   "stores to the neighbours and one 8-double all-reduce per two iterations")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="c1,c2,c3,c4")
+    ap.add_argument("--c5-ranks", default="0,3,7")
+    ap.add_argument("--c5-iters", type=int, default=200)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     res = []
     for name in args.only.split(","):
+        if name == "c5":
+            r = run_c5([int(x) for x in args.c5_ranks.split(",")], args.c5_iters)
+            print(json.dumps(r), flush=True)
+            res.append(r)
+            continue
         c = CONFIGS[name]
         r = run_gpu(name, c)
         if not args.no_cpu:

@@ -57,6 +57,22 @@ uint64_t l1b_mix_seed(uint64_t seed, uint64_t salt);
 int l1b_realize_permutation(uint64_t n, uint64_t seed, uint32_t* map_out);
 int l1b_realize_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
                                  double* sigma_out);
+/* Device realisation of the per-entry streams (Spectrum::uniform,
+ * linops.cpp:323-331, with spectrum = 1; the l1_subgradient fill,
+ * instance.cpp:33-35, with spectrum = 0): draws [0, count) of
+ * Rng(seed) as lo + (hi - lo) * uniform_unit (+ shift), cut into chunks
+ * started by mt19937_64 jump-ahead (k_rng.cu).  Draws [win_lo, win_hi) go to
+ * the device buffer d_out; vmin / vmax (host, optional) receive the min / max
+ * over all draws; *exact = 0 when a spectrum draw would have been rejected
+ * (the stream shifts: replay it with l1b_realize_spectrum_uniform).
+ * Chunks hold >= 2^min_log2_chunk draws (at most 4096 chunks). */
+int l1b_device_uniform_draws(int device, uint64_t seed, uint64_t count, double lo, double hi,
+                             int spectrum, double shift, uint64_t win_lo, uint64_t win_hi,
+                             uint32_t min_log2_chunk, double* d_out, double* vmin, double* vmax,
+                             int* exact);
+/* Host check of the jump polynomials: raw outputs 2^log2_jump ...
+ * 2^log2_jump + count - 1 of std::mt19937_64(seed), reached by jumping. */
+int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, uint64_t* out);
 /* Returns s through *s_out; support (ascending) and values need capacity s. */
 int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
                                 uint32_t* support_out, double* values_out);

@@ -249,7 +249,7 @@ std::vector<uint32_t> inverse_map(const uint32_t* map, uint64_t m) {
 void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
                     std::vector<int32_t> r_off, std::vector<double> r_th,
                     std::vector<int32_t> l_off, std::vector<double> l_th, const uint32_t* p1,
-                    const uint32_t* p2, const double* sigma) {
+                    const uint32_t* p2, const double* sigma, double* d_sigma_ready = nullptr) {
   if (m == 0 || n == 0) throw InvalidArgument("OperatorSpec: dimensions must be positive");
   if (m < n) throw InvalidArgument("OperatorSpec: requires m >= n");
   if (m > (1ull << 32)) throw InvalidArgument("OperatorSpec: m above 2^32 exceeds uint32 indices");
@@ -269,7 +269,12 @@ void setup_operator(l1b_problem* p, int device, uint64_t m, uint64_t n,
   fill_stage_tab(p->view.right, p->r_off, p->r_theta);
   fill_stage_tab(p->view.left, p->l_off, p->l_theta);
   cudaStream_t st = p->stream;
-  p->d_sigma = upload(sigma, n, st, &p->device_bytes);
+  if (d_sigma_ready) {  // drawn on the device (k_rng.cu)
+    p->d_sigma = d_sigma_ready;
+    p->device_bytes += (n + 2) * sizeof(double);
+  } else {
+    p->d_sigma = upload(sigma, n, st, &p->device_bytes);
+  }
   if (p1) {
     auto inv = inverse_map(p1, m);
     p->d_p1 = upload(p1, m, st, &p->device_bytes);
@@ -375,6 +380,29 @@ int l1b_realize_spectrum_uniform(uint64_t n, double lo, double hi, double shift,
   return guard([&] { hostrng::spectrum_uniform(n, lo, hi, shift, seed, sigma_out); });
 }
 
+int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, uint64_t* out) {
+  return guard([&] {
+    if (!out && count) throw InvalidArgument("null output");
+    if (log2_jump > 63) throw InvalidArgument("jump above 2^63");
+    host_draws_after_jump(seed, (int)log2_jump, count, out);
+  });
+}
+
+int l1b_device_uniform_draws(int device, uint64_t seed, uint64_t count, double lo, double hi,
+                             int spectrum, double shift, uint64_t win_lo, uint64_t win_hi,
+                             uint32_t min_log2_chunk, double* d_out, double* vmin, double* vmax,
+                             int* exact) {
+  return guard([&] {
+    if (win_hi > count || win_lo > win_hi) throw InvalidArgument("draw window out of range");
+    if (win_hi > win_lo && !d_out) throw InvalidArgument("null output");
+    if (min_log2_chunk > 40) throw InvalidArgument("chunk above 2^40 draws");
+    L1B_CUDA(cudaSetDevice(device));
+    const bool ok = device_uniform_draws(seed, count, lo, hi, spectrum != 0, shift, win_lo, win_hi, d_out,
+                                         vmin, vmax, 0, (int)min_log2_chunk);
+    if (exact) *exact = ok ? 1 : 0;
+  });
+}
+
 int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
                                 uint32_t* support_out, double* values_out) {
   return guard([&] {
@@ -392,6 +420,16 @@ int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t r
 }  // extern "C"
 
 namespace {
+// The per-entry streams (sigma, the subgradient fill) are drawn on the device
+// (k_rng.cu, mt19937_64 jump-ahead) for n >= 2^16; L1B_DEVICE_RNG=0 keeps the
+// sequential host replay, =1 uses the device for every n.
+bool device_rng_for(uint64_t n) {
+  const char* e = getenv("L1B_DEVICE_RNG");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return n >= (1ull << 16);
+}
+
 // Row-block shard of a banded instance (identity P1/P2, no left stages, so
 // |col - row| <= h = #stages and rows >= n are empty).  The host replays the
 // full sigma / g streams (sequential mt19937_64) but uploads only the window
@@ -460,18 +498,6 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   if (!(a < b && b <= n)) throw InvalidArgument("shard: empty or out-of-range row block");
   if (a % 2) throw InvalidArgument("shard: row_begin must be even");
   const uint64_t job_seed = hostrng::mix_seed(g->seed, g->job_index);
-  // full spectrum (sigma_max / sigma_min are global), window of it uploaded
-  std::vector<double> sigma(n);
-  if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
-    hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift, hostrng::mix_seed(job_seed, 3),
-                              sigma.data());
-  } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
-    for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
-  } else if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && g->sigma_explicit) {
-    std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
-  } else {
-    throw InvalidArgument("unknown spectrum kind");
-  }
   // b is also built on bh rows around the block for the recomputing FISTA
   // kernel (k_iter_rc.cu); sigma / x / w windows widen by the same amount
   const uint64_t bh = g->stages >= 1 && g->stages <= 4
@@ -479,34 +505,66 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
                           : 0;
   const uint64_t sa = a > bh + 3 * h ? (a - bh - 3 * h) & ~3ull : 0;  // 32-byte aligned view
   const uint64_t sb = std::min(n, b + bh + 3 * h);
+  if (g->spectrum_kind < L1B_SPECTRUM_UNIFORM_Q || g->spectrum_kind > L1B_SPECTRUM_EXPLICIT ||
+      (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && !g->sigma_explicit))
+    throw InvalidArgument("unknown spectrum kind");
   auto p = std::make_unique<l1b_problem>();
   std::vector<int32_t> r_off;
   for (uint32_t i = 0; i < g->stages; ++i) r_off.push_back((int32_t)((g->stages - 1 - i) % 2));
-  // setup_operator validates / uploads the description; it needs the whole
-  // sigma only for the host-side checks, so give it the window afterwards.
-  for (uint64_t i = 0; i < n; ++i)
-    if (!(sigma[i] > 0.0) || !std::isfinite(sigma[i]))
-      throw std::runtime_error("Spectrum: all singular values must be strictly positive");
   p->device = device;
   L1B_CUDA(cudaSetDevice(device));
   L1B_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   cudaStream_t st = p->stream;
+  // sigma: the window [sa, sb) is kept, sigma_max / sigma_min are global.  On
+  // the device the whole stream is drawn (chunks jump-started) and reduced
+  // without being stored; on the host (L1B_DEVICE_RNG=0, other spectra, or a
+  // rejected draw) the full stream is replayed.
+  const bool dev_rng = device_rng_for(n);
+  double smax = 0.0, smin = 0.0;
+  bool have_sigma = false;
+  if (dev_rng && g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+    p->d_sigma = dev_alloc<double>(sb - sa, &p->device_bytes);
+    have_sigma = device_uniform_draws(hostrng::mix_seed(job_seed, 3), n, 0.0, std::pow(10.0, g->q), true,
+                                      g->shift, sa, sb, p->d_sigma, &smin, &smax, 0);
+    if (!have_sigma) {
+      cudaFree(p->d_sigma);
+      p->d_sigma = nullptr;
+      p->device_bytes -= (sb - sa + 2) * sizeof(double);
+    } else if (!(smin > 0.0) || !std::isfinite(smax)) {
+      throw std::runtime_error("Spectrum: all singular values must be strictly positive");
+    }
+  }
+  if (!have_sigma) {
+    std::vector<double> sigma(n);
+    if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+      hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift, hostrng::mix_seed(job_seed, 3),
+                                sigma.data());
+    } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+      for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+    } else {
+      std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+    }
+    for (uint64_t i = 0; i < n; ++i)
+      if (!(sigma[i] > 0.0) || !std::isfinite(sigma[i]))
+        throw std::runtime_error("Spectrum: all singular values must be strictly positive");
+    p->d_sigma = upload(sigma.data() + sa, sb - sa, st, &p->device_bytes);
+    smax = smin = sigma[0];
+    for (uint64_t i = 1; i < n; ++i) {
+      smax = std::max(smax, sigma[i]);
+      smin = std::min(smin, sigma[i]);
+    }
+    L1B_CUDA(cudaStreamSynchronize(st));
+  }
   p->m = m;
   p->n = n;
   p->r_off = r_off;
   p->r_theta.assign(g->stages, g->theta);
   fill_stage_tab(p->view.right, p->r_off, p->r_theta);
   fill_stage_tab(p->view.left, p->l_off, p->l_theta);
-  p->d_sigma = upload(sigma.data() + sa, sb - sa, st, &p->device_bytes);
   p->sig_begin = sa;
   p->view.m = m;
   p->view.n = n;
   p->view.sigma = p->d_sigma - sa;  // global indexing inside [sa, sb)
-  double smax = sigma[0], smin = sigma[0];
-  for (uint64_t i = 1; i < n; ++i) {
-    smax = std::max(smax, sigma[i]);
-    smin = std::min(smin, sigma[i]);
-  }
   p->lmax = smax * smax;
   p->cert_kappa = (smax / smin) * (smax / smin);
   p->tau = g->tau;
@@ -520,16 +578,41 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
     throw Unsupported("row-block shards: the spectral planted solution needs the whole operator");
   planted_solution(g, n, job_seed, nullptr, p.get());
   const uint64_t s = p->xs_sup.size();
-  std::vector<double> gw(sb - sa), xw;
+  // the subgradient fill on the window (instance.cpp:33-40): draws [sa, sb) of
+  // Rng(mix_seed(job.seed, 5)) -- on the device only the chunks meeting the
+  // window run -- then the signs of x* on the support
+  std::vector<double> xw;
+  double* d_g = nullptr;
   {
-    hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
-    for (uint64_t i = 0; i < sb; ++i) {
-      const double v = hostrng::in(r, -g->fill_bound, g->fill_bound);
-      if (i >= sa) gw[i - sa] = v;
-    }
+    std::vector<uint32_t> wsup;
+    std::vector<double> wsg;
     for (uint64_t k = 0; k < s; ++k) {
       const uint64_t i = p->xs_sup[k];
-      if (i >= sa && i < sb) gw[i - sa] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+      if (i >= sa && i < sb) {
+        wsup.push_back((uint32_t)(i - sa));
+        wsg.push_back(p->xs_val[k] > 0.0 ? 1.0 : -1.0);
+      }
+    }
+    if (dev_rng) {
+      d_g = dev_alloc<double>(sb - sa, nullptr);
+      device_uniform_draws(hostrng::mix_seed(job_seed, 5), n, -g->fill_bound, g->fill_bound, false, 0.0, sa,
+                           sb, d_g, nullptr, nullptr, st);
+      uint32_t* d_ws = upload(wsup.data(), wsup.size(), st, nullptr);
+      double* d_wv = upload(wsg.data(), wsg.size(), st, nullptr);
+      scatter_values(d_ws, d_wv, wsup.size(), d_g, st);
+      L1B_CUDA(cudaStreamSynchronize(st));
+      cudaFree(d_ws);
+      cudaFree(d_wv);
+    } else {
+      std::vector<double> gw(sb - sa);
+      hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+      for (uint64_t i = 0; i < sb; ++i) {
+        const double v = hostrng::in(r, -g->fill_bound, g->fill_bound);
+        if (i >= sa) gw[i - sa] = v;
+      }
+      for (size_t k = 0; k < wsup.size(); ++k) gw[wsup[k]] = wsg[k];
+      d_g = upload(gw.data(), gw.size(), st, nullptr);
+      L1B_CUDA(cudaStreamSynchronize(st));
     }
   }
   const uint64_t va = a > bh + h ? a - bh - h : 0, vb = std::min(n, b + bh + h), own = b - a;
@@ -540,7 +623,6 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
     if (i >= va && i < vb) xw[i - va] = p->xs_val[k];
   }
   // w = G (S^T S)^-1 G^T g on the window (valid on [a - h, b + h))
-  double* d_g = upload(gw.data(), gw.size(), st, nullptr);
   window_stages(p->view.right, true, true, d_g, sa, sb, n, st);
   window_scale_op(d_g, p->d_sigma, sb - sa, 0, 0.0, st);
   window_stages(p->view.right, false, false, d_g, sa, sb, n, st);
@@ -598,14 +680,33 @@ std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
   for (uint32_t i = 0; i < g->left_stages; ++i)
     l_off.push_back((int32_t)((g->left_stages - 1 - i) % 2));
   // The four seeded streams (P1, P2, sigma, the subgradient fill) are
-  // independent mt19937_64 sequences: realise them on four host threads.
+  // independent mt19937_64 sequences: sigma and the fill are drawn on the
+  // device (jump-ahead chunks), the permutations (Fisher-Yates with rejection,
+  // inherently sequential) on host threads.
   std::vector<uint32_t> p1, p2;
-  std::vector<double> sigma(n), gv(n);
+  std::vector<double> sigma, gv;
   if (g->permute && m > (1ull << 32)) throw InvalidArgument("Permutation: m above 2^32");
   if (g->spectrum_kind == L1B_SPECTRUM_EXPLICIT && !g->sigma_explicit)
     throw InvalidArgument("explicit spectrum without values");
   if (g->spectrum_kind < L1B_SPECTRUM_UNIFORM_Q || g->spectrum_kind > L1B_SPECTRUM_EXPLICIT)
     throw InvalidArgument("unknown spectrum kind");
+  const bool dev_rng = device_rng_for(n);
+  L1B_CUDA(cudaSetDevice(device));
+  double* d_sig = nullptr;
+  if (dev_rng && g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+    L1B_CUDA(cudaMalloc(&d_sig, (n + 2) * sizeof(double)));
+    if (!device_uniform_draws(hostrng::mix_seed(job_seed, 3), n, 0.0, std::pow(10.0, g->q), true, g->shift,
+                              0, n, d_sig, nullptr, nullptr, 0)) {
+      cudaFree(d_sig);  // a rejected draw: replay the stream sequentially
+      d_sig = nullptr;
+    }
+  }
+  double* d_g = nullptr;
+  if (dev_rng) {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
+    L1B_CUDA(cudaMalloc(&d_g, (n + 2) * sizeof(double)));
+    device_uniform_draws(hostrng::mix_seed(job_seed, 5), n, -g->fill_bound, g->fill_bound, false, 0.0, 0, n,
+                         d_g, nullptr, nullptr, 0);
+  }
   {
     std::vector<std::thread> pool;
     if (g->permute) {
@@ -614,38 +715,59 @@ std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
       pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
       pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
     }
-    pool.emplace_back([&] {
-      if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
-        hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
-                                  hostrng::mix_seed(job_seed, 3), sigma.data());
-      } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
-        for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
-      } else {
-        std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
-      }
-    });
-    pool.emplace_back([&] {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
-      hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
-      for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
-    });
+    if (!d_sig) {
+      sigma.resize(n);
+      pool.emplace_back([&] {
+        if (g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
+          hostrng::spectrum_uniform(n, 0.0, std::pow(10.0, g->q), g->shift,
+                                    hostrng::mix_seed(job_seed, 3), sigma.data());
+        } else if (g->spectrum_kind == L1B_SPECTRUM_ALTERNATING) {
+          for (uint64_t i = 0; i < n; ++i) sigma[i] = (i % 2 == 0) ? g->odd_value : g->even_value;
+        } else {
+          std::copy(g->sigma_explicit, g->sigma_explicit + n, sigma.begin());
+        }
+      });
+    }
+    if (!d_g) {
+      gv.resize(n);
+      pool.emplace_back([&] {  // l1_subgradient draws (instance.cpp:33-35), Rng(mix_seed(job.seed, 5))
+        hostrng::Rng r(hostrng::mix_seed(job_seed, 5));
+        for (uint64_t i = 0; i < n; ++i) gv[i] = hostrng::in(r, -g->fill_bound, g->fill_bound);
+      });
+    }
     for (auto& th : pool) th.join();
   }
   auto p = std::make_unique<l1b_problem>();
   setup_operator(p.get(), device, m, n, r_off, std::vector<double>(g->stages, g->theta), l_off,
                  std::vector<double>(g->left_stages, g->theta), g->permute ? p1.data() : nullptr,
-                 g->permute ? p2.data() : nullptr, sigma.data());
+                 g->permute ? p2.data() : nullptr, d_sig ? nullptr : sigma.data(), d_sig);
   p->tau = g->tau;
+  if (d_sig && g->solution_kind == L1B_SOLUTION_SPECTRAL) {  // xhat needs sigma on the host
+    sigma.resize(n);
+    L1B_CUDA(cudaMemcpy(sigma.data(), d_sig, n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
   // planted solution (bench.cpp:281-301)
-  planted_solution(g, n, job_seed, sigma.data(), p.get());
+  planted_solution(g, n, job_seed, sigma.empty() ? nullptr : sigma.data(), p.get());
   const uint64_t s = p->xs_sup.size();
-  // subgradient g: signs on the support (instance.cpp:36-40)
-  for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
   cudaStream_t st = p->stream;
+  // subgradient g: signs on the support (instance.cpp:36-40)
+  if (d_g) {
+    std::vector<double> sg(s);
+    for (uint64_t k = 0; k < s; ++k) sg[k] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+    uint32_t* d_ssup = upload(p->xs_sup.data(), s, st, nullptr);
+    double* d_sg = upload(sg.data(), s, st, nullptr);
+    scatter_values(d_ssup, d_sg, s, d_g, st);
+    L1B_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_ssup);
+    cudaFree(d_sg);
+  } else {
+    for (uint64_t k = 0; k < s; ++k) gv[p->xs_sup[k]] = p->xs_val[k] > 0.0 ? 1.0 : -1.0;
+    d_g = upload(gv.data(), n, st, nullptr);
+  }
   // device: w = G (S^T S)^-1 G^T g; e = tau A w; b = A x* + e (instance.cpp:64-79)
-  double *d_g = nullptr, *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;
+  double *d_e = nullptr, *d_x = nullptr, *d_ss = nullptr;
   uint32_t* d_sup = nullptr;
   double* d_val = nullptr;
-  d_g = upload(gv.data(), n, st, nullptr);
   L1B_CUDA(cudaMalloc(&d_e, m * sizeof(double)));
   L1B_CUDA(cudaMalloc(&d_x, n * sizeof(double)));
   L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));

@@ -285,6 +285,13 @@ void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* 
   L1B_LAUNCHED();
 }
 
+void scatter_values(const uint32_t* sup, const double* val, uint64_t s, double* dense,
+                    cudaStream_t st) {
+  if (!s) return;
+  scatter_sparse_kernel<<<grid_for(s), kThreads, 0, st>>>(sup, val, s, dense);
+  L1B_LAUNCHED();
+}
+
 void generator_combine(double tau, double* e, double* b, uint64_t m, double* d_sum_sq,
                        cudaStream_t st) {
   const int grid = grid_for(m);

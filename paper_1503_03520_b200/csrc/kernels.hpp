@@ -30,6 +30,20 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
                  uint64_t keep_hi = ~0ull);
 void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, cudaStream_t st);
 
+// ---- k_rng.cu (std::mt19937_64 streams on the device, bit-exact) ----------
+// Draws [0, count) of Rng(seed) as uniform_in(lo, hi) (rng.hpp:44-47); with
+// `spectrum` the draws follow Spectrum::uniform (linops.cpp:323-331): + shift,
+// rejection of u <= lo.  Draws [wlo, whi) are stored to d_out[i - wlo]; when
+// vmin / vmax are given, the min / max over all draws (non-negative values).
+// Returns false when a draw would be rejected (the stream shifts; the caller
+// replays it sequentially).  Chunks hold >= 2^min_log2_chunk draws.  Syncs.
+bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, bool spectrum,
+                          double shift, uint64_t wlo, uint64_t whi, double* d_out, double* vmin,
+                          double* vmax, cudaStream_t st, int min_log2_chunk = 12);
+// host: raw 64-bit outputs 2^log2_jump .. 2^log2_jump + count - 1 of
+// std::mt19937_64(seed) through the jump polynomial (log2_jump < 0: no jump)
+void host_draws_after_jump(uint64_t seed, int log2_jump, uint64_t count, uint64_t* out);
+
 // ---- k_sweep.cu (matrix-free, bit-exact vs linops.cpp) ---------------------
 void sweep_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
 void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStream_t st);
@@ -40,6 +54,9 @@ void spectral_select(const OpView& op, const double* xhat_host, uint64_t n, uint
                      cudaStream_t st, std::vector<uint32_t>& sup, std::vector<double>& val);
 void sweep_gram_inverse(const OpView& op, const double* v, double* out, cudaStream_t st);
 void scatter_sparse(const uint32_t* sup, const double* val, uint64_t s, double* dense, uint64_t n,
+                    cudaStream_t st);
+// dense[sup[k]] = val[k] (no zero fill)
+void scatter_values(const uint32_t* sup, const double* val, uint64_t s, double* dense,
                     cudaStream_t st);
 // b += tau * e-part: e *= tau; b += e; returns sum(e^2) through *sum_sq (device)
 void generator_combine(double tau, double* e, double* b, uint64_t m, double* d_sum_sq,

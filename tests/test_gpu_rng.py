@@ -1,0 +1,130 @@
+"""GPU: std::mt19937_64 streams drawn on the device (k_rng.cu) -- chunks
+started by jump-ahead, a 16-ary jump tree -- bit-identical to the oracle's
+sequential streams (Spectrum::uniform, linops.cpp:323-331; the l1_subgradient
+fill, instance.cpp:33-35), and the generator built on them identical to the
+sequential host replay (L1B_DEVICE_RNG=0) and to the oracle."""
+import ctypes
+import math
+import os
+
+import numpy as np
+import pytest
+
+from gpu_util import need_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def _draws(seed, count, lo, hi, spectrum, shift, wlo, whi, min_log2_chunk):
+    torch = need_cuda()
+    from paper_1503_03520_b200 import _native as N
+
+    out = torch.empty(max(whi - wlo, 1), dtype=torch.float64, device="cuda")
+    vmin, vmax, exact = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    N.check(N.load().l1b_device_uniform_draws(0, seed, count, lo, hi, spectrum, shift, wlo, whi,
+                                              min_log2_chunk, ctypes.c_void_p(out.data_ptr()),
+                                              ctypes.byref(vmin), ctypes.byref(vmax), ctypes.byref(exact)))
+    torch.cuda.synchronize()
+    return out[: whi - wlo].cpu().numpy(), vmin.value, vmax.value, exact.value
+
+
+def _oracle_spectrum(oracle, n, hi, shift, seed):
+    out = np.empty(n)
+    oracle.lib.lo_spectrum_uniform(n, 0.0, hi, shift, seed, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+@pytest.mark.parametrize("count,wlo,whi,chunk", [
+    (3_000_001, 1_000_003, 2_500_017, 10),   # 2930 chunks: three jump levels
+    (200_000, 0, 200_000, 12),               # 49 chunks: two levels
+    (1000, 0, 1000, 12),                     # one chunk, no jump
+    (70_000, 69_990, 70_000, 8),             # window at the very end
+])
+def test_spectrum_stream_bit_exact(oracle, count, wlo, whi, chunk):
+    seed = oracle.mix_seed(oracle.mix_seed(3, 0), 3)
+    got, vmin, vmax, exact = _draws(seed, count, 0.0, 10.0, 1, 0.1, wlo, whi, chunk)
+    want = _oracle_spectrum(oracle, count, 10.0, 0.1, seed)
+    assert exact == 1
+    np.testing.assert_array_equal(got, want[wlo:whi])
+    assert vmin == want.min() and vmax == want.max()
+
+
+def test_fill_stream_bit_exact(oracle):
+    n = 300_007
+    seed = oracle.mix_seed(oracle.mix_seed(9, 0), 5)
+    got, _, _, _ = _draws(seed, n, -0.9, 0.9, 0, 0.0, 0, n, 6)  # 4096 chunks of 2^7
+    want = np.empty(n)
+    r = oracle.rng(seed)
+    oracle.lib.lo_l1_subgradient(ctypes.c_uint64(n), None, None, ctypes.c_uint64(0), ctypes.c_double(0.9),
+                                 ctypes.byref(r), want.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    np.testing.assert_array_equal(got, want)
+
+
+def test_c4_sized_spectrum_stream_matches_host_replay():
+    """n = 2^26 draws (default chunking: 4096 chunks of 2^14) against the
+    library's own sequential host stream."""
+    from paper_1503_03520_b200 import _native as N
+
+    n = 1 << 26
+    seed = N.load().l1b_mix_seed(N.load().l1b_mix_seed(3, 0), 3)
+    got, vmin, vmax, exact = _draws(seed, n, 0.0, 10.0, 1, 0.1, 0, n, 12)
+    want = np.empty(n)
+    N.check(N.load().l1b_realize_spectrum_uniform(n, 0.0, 10.0, 0.1, seed,
+                                                  want.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    assert exact == 1
+    np.testing.assert_array_equal(got, want)
+    assert vmin == want.min() and vmax == want.max()
+
+
+def _with_env(val, fn):
+    old = os.environ.get("L1B_DEVICE_RNG")
+    os.environ["L1B_DEVICE_RNG"] = val
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["L1B_DEVICE_RNG"]
+        else:
+            os.environ["L1B_DEVICE_RNG"] = old
+
+
+@pytest.mark.parametrize("kw", [
+    dict(n=4096, stages=4, q=1, s_divisor=100, seed=3),
+    dict(n=5000, stages=2, left_stages=1, permute=True, q=2, s_divisor=50, seed=6),
+    dict(n=4096, stages=1, q=1, s_divisor=100, seed=2, solution="spectral", s1_fraction=0.5),
+])
+def test_generator_device_rng_equals_host_and_oracle(oracle, kw):
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(kw, theta=2 * math.pi / 10)
+    dev = _with_env("1", lambda: l1bench.build_instance(**kw))
+    host = _with_env("0", lambda: l1bench.build_instance(**kw))
+    np.testing.assert_array_equal(dev.sigma(), host.sigma())
+    np.testing.assert_array_equal(dev.b, host.b)
+    np.testing.assert_array_equal(dev.x_star.support, host.x_star.support)
+    np.testing.assert_array_equal(dev.x_star.values, host.x_star.values)
+    assert dev.noise_norm == host.noise_norm
+    if kw.get("solution", "uniform") == "uniform":
+        okw = {k: v for k, v in kw.items() if k not in ("solution", "s1_fraction")}
+        oi = oracle.build_instance(**okw)
+        np.testing.assert_array_equal(dev.b, oi.b)
+
+
+def test_shards_device_rng_reproduce_global_instance():
+    """Row-block shards draw only their windows of the fill stream and reduce
+    sigma over the whole stream without storing it: same b rows as the whole
+    instance, same L."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    kw = dict(n=40000, stages=4, q=1, s_divisor=100, seed=3, theta=2 * math.pi / 10)
+    whole = _with_env("0", lambda: l1bench.build_instance(**kw))
+    cfg = l1bench.SolverConfig(max_iters=4)
+    shards = _with_env("1", lambda: [CudaShard(kw, r, 3, 0, cfg) for r in range(3)])
+    for s in shards:
+        a, e = s.inst.info.row_begin, s.inst.info.row_end
+        np.testing.assert_array_equal(s.inst.b[: e - a], whole.b[a:e])
+        assert s.inst.info.gram_lmax == whole.info.gram_lmax
+        assert s.inst.info.cert_kappa == whole.info.cert_kappa
