@@ -474,8 +474,25 @@ void planted_solution(const l1b_gen_desc* g, uint64_t n, uint64_t job_seed, cons
   }
 }
 
+// L1B_GEN_TRACE=1: phase times of the shard generator on stderr
+struct PhaseTrace {
+  bool on;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t0;
+  PhaseTrace() : on(getenv("L1B_GEN_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+  void operator()(const char* what) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[l1b gen] %-22s %8.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
                     l1b_problem** out) {
+  PhaseTrace mark;
   if (g->n < 2) throw InvalidArgument("ExperimentConfig: dimensions must be at least 2");
   if (!(g->m_ratio >= 1.0)) throw InvalidArgument("ExperimentConfig: m_ratio must be >= 1");
   if (g->s_divisor == 0) throw InvalidArgument("ExperimentConfig: s_divisor must be positive");
@@ -515,6 +532,8 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   L1B_CUDA(cudaSetDevice(device));
   L1B_CUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   cudaStream_t st = p->stream;
+  mark.st = st;
+  mark("setup");
   // sigma: the window [sa, sb) is kept, sigma_max / sigma_min are global.  On
   // the device the whole stream is drawn (chunks jump-started) and reduced
   // without being stored; on the host (L1B_DEVICE_RNG=0, other spectra, or a
@@ -576,12 +595,13 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   p->halo = h;
   if (g->solution_kind == L1B_SOLUTION_SPECTRAL)
     throw Unsupported("row-block shards: the spectral planted solution needs the whole operator");
+  mark("sigma");
   planted_solution(g, n, job_seed, nullptr, p.get());
+  mark("planted solution");
   const uint64_t s = p->xs_sup.size();
   // the subgradient fill on the window (instance.cpp:33-40): draws [sa, sb) of
   // Rng(mix_seed(job.seed, 5)) -- on the device only the chunks meeting the
   // window run -- then the signs of x* on the support
-  std::vector<double> xw;
   double* d_g = nullptr;
   {
     std::vector<uint32_t> wsup;
@@ -617,18 +637,32 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   }
   const uint64_t va = a > bh + h ? a - bh - h : 0, vb = std::min(n, b + bh + h), own = b - a;
   const uint64_t wa = a > bh ? a - bh : 0, wb = std::min(n, b + bh);  // b window
-  xw.assign(vb - va, 0.0);
+  // x* on the window [va, vb): zero, then its support scattered on the device
+  std::vector<uint32_t> xsup;
+  std::vector<double> xval;
   for (uint64_t k = 0; k < s; ++k) {
     const uint64_t i = p->xs_sup[k];
-    if (i >= va && i < vb) xw[i - va] = p->xs_val[k];
+    if (i >= va && i < vb) {
+      xsup.push_back((uint32_t)(i - va));
+      xval.push_back(p->xs_val[k]);
+    }
   }
+  mark("fill + x* window");
   // w = G (S^T S)^-1 G^T g on the window (valid on [a - h, b + h))
   window_stages(p->view.right, true, true, d_g, sa, sb, n, st);
   window_scale_op(d_g, p->d_sigma, sb - sa, 0, 0.0, st);
   window_stages(p->view.right, false, false, d_g, sa, sb, n, st);
   // e_own = Sigma G^T w, b_own = Sigma G^T x* on [a, b)
   double* d_v = nullptr;
-  double* d_x = upload(xw.data(), xw.size(), st, nullptr);
+  double* d_x = dev_alloc<double>(vb - va, nullptr);
+  {
+    uint32_t* d_xs = upload(xsup.data(), xsup.size(), st, nullptr);
+    double* d_xv = upload(xval.data(), xval.size(), st, nullptr);
+    scatter_sparse(d_xs, d_xv, xsup.size(), d_x, vb - va, st);
+    L1B_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_xs);
+    cudaFree(d_xv);
+  }
   L1B_CUDA(cudaMalloc(&d_v, (vb - va) * sizeof(double)));
   L1B_CUDA(cudaMemcpyAsync(d_v, d_g + (va - sa), (vb - va) * 8, cudaMemcpyDeviceToDevice, st));
   window_stages(p->view.right, true, true, d_v, va, vb, n, st);
@@ -658,8 +692,10 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   p->noise_norm = std::sqrt(ss);  // this shard's part of ||e||
   for (void* q : {(void*)d_g, (void*)d_v, (void*)d_x, (void*)d_ss}) cudaFree(q);
   p->tail_sq = p->tail_sq_band = 0.0;  // rows >= n are empty and b is exactly 0 there
+  mark("sweeps + b");
   // rows / columns [a, b) with indices local to the windows starting at a - h
   if (!g->lazy_sparse) materialise(p.get());
+  mark("materialise");
   *out = p.release();
 }
 
