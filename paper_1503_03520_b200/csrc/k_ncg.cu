@@ -433,6 +433,210 @@ __global__ void __launch_bounds__(kThreads) pcg_loop_kernel(PcgArgs P) {
   }
 }
 
+// -- PCG for one right stage (C1-C3's operators): pair-local products --------
+// With a single Givens stage, no left stages and identity permutations,
+// A p = Sigma G^T p (rows >= n empty) and A^T A p = G Sigma Sigma G^T p act on
+// disjoint pairs (a, a + 1), a = 2u - offset: the Hessian-vector product of a
+// pair needs only that pair.  Each thread owns P pairs for the whole solve and
+// keeps p, r, step and hp in registers; an iteration is the pair-local
+// hessvec (the reference's own sweep arithmetic: OperatorSpec::apply /
+// apply_transpose, linops.cpp:422-473) and two grid-wide sums (p.hp, then
+// ||r||^2 and r.z), i.e. two grid barriers instead of three, with no gathers.
+struct PcgPairArgs {
+  uint64_t n;
+  int off;
+  double c, s;
+  const double *sigma, *pre, *d2psi;
+  const double *p, *r;  // p_0, r_0 (pcg_init_kernel)
+  double *step, *best;
+  NcgDev* st;
+  double* partials;  // >= 3 x grid doubles
+};
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  NcgDev* st = A.st;
+  const int64_t n = (int64_t)A.n;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const double c = A.c, s = A.s;
+  const double tau = st->tau, eta = st->eta, rhs_norm = st->rhs_norm;
+  const uint64_t max_iters = st->max_iters;
+  double rz = st->rz, best_norm = st->best_norm, php = 0.0, alpha = 0.0, beta = 0.0, rn = 0.0;
+  int done = st->done, converged = st->converged, negcurv = 0, error = 0;
+  uint64_t it = 0;
+  double p[P][2], r[P][2], stp[P][2], hp[P][2];
+  int64_t a[P];
+  bool va[P], vb[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    a[k] = 2 * (int64_t)(g0 + (uint64_t)k * T) - A.off;
+    va[k] = a[k] >= 0 && a[k] < n;
+    vb[k] = a[k] + 1 >= 0 && a[k] + 1 < n;
+    p[k][0] = va[k] ? A.p[a[k]] : 0.0;
+    p[k][1] = vb[k] ? A.p[a[k] + 1] : 0.0;
+    r[k][0] = va[k] ? A.r[a[k]] : 0.0;
+    r[k][1] = vb[k] ? A.r[a[k] + 1] : 0.0;
+    stp[k][0] = stp[k][1] = 0.0;  // step_0 = 0 (pcg_init_kernel)
+  }
+  double* part_b = A.partials;
+  double* part_c = A.partials + (size_t)gridDim.x;
+  while (!done) {
+    // hessvec (solvers.cpp:536-540): hav = A p, hp = A^T hav + tau d2psi p; p.hp
+    double acc[1] = {0.0};
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const bool pair = va[k] && vb[k];
+      double v0 = p[k][0], v1 = p[k][1];
+      if (pair) rotate_pair(v0, v1, c, s, true);  // G^T p
+      const double s0 = va[k] ? __ldg(A.sigma + a[k]) : 0.0;
+      const double s1 = vb[k] ? __ldg(A.sigma + a[k] + 1) : 0.0;
+      double w0 = s0 * (s0 * v0), w1 = s1 * (s1 * v1);  // Sigma^T (Sigma G^T p)
+      if (pair) rotate_pair(w0, w1, c, s, false);      // G (...)
+      if (va[k]) {
+        hp[k][0] = w0 + tau * __ldg(A.d2psi + a[k]) * p[k][0];
+        acc[0] += p[k][0] * hp[k][0];
+      } else {
+        hp[k][0] = 0.0;
+      }
+      if (vb[k]) {
+        hp[k][1] = w1 + tau * __ldg(A.d2psi + a[k] + 1) * p[k][1];
+        acc[0] += p[k][1] * hp[k][1];
+      } else {
+        hp[k][1] = 0.0;
+      }
+    }
+    block_sum<1>(acc);
+    if (threadIdx.x == 0) part_b[blockIdx.x] = acc[0];
+    grid.sync();
+    {
+      double tot[1];
+      fold_partials<1>(part_b, tot);
+      php = tot[0];  // solvers.cpp:231-237
+    }
+    if (!(php > 0.0)) {
+      if (!isfinite(php)) error = 1;
+      negcurv = 1;
+      break;
+    }
+    alpha = rz / php;
+    // step += alpha p; r -= alpha hp (:238-241); ||r||^2, r.z with z = r / pre
+    double acc2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!(e == 0 ? va[k] : vb[k])) continue;
+        stp[k][e] += alpha * p[k][e];
+        const double ri = r[k][e] - alpha * hp[k][e];
+        r[k][e] = ri;
+        acc2[0] += ri * ri;
+        acc2[1] += ri * (ri / __ldg(A.pre + a[k] + e));
+      }
+    }
+    block_sum<2>(acc2);
+    if (threadIdx.x == 0) {
+      part_c[(size_t)blockIdx.x * 2] = acc2[0];
+      part_c[(size_t)blockIdx.x * 2 + 1] = acc2[1];
+    }
+    grid.sync();
+    double tot[2];
+    fold_partials<2>(part_c, tot);
+    rn = sqrt(tot[0]);
+    ++it;
+    if (!isfinite(rn)) {
+      error = 2;
+      break;
+    }
+    if (rn < best_norm) {  // best = step (:245-248)
+      best_norm = rn;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        if (va[k]) A.best[a[k]] = stp[k][0];
+        if (vb[k]) A.best[a[k] + 1] = stp[k][1];
+      }
+    }
+    if (rn <= eta * rhs_norm) {
+      converged = 1;
+      break;
+    }
+    beta = tot[1] / rz;  // (:255-259)
+    rz = tot[1];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (va[k]) p[k][0] = r[k][0] / __ldg(A.pre + a[k]) + beta * p[k][0];
+      if (vb[k]) p[k][1] = r[k][1] / __ldg(A.pre + a[k] + 1) + beta * p[k][1];
+    }
+    if (it >= max_iters) break;
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    if (va[k]) A.step[a[k]] = stp[k][0];
+    if (vb[k]) A.step[a[k] + 1] = stp[k][1];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rz = rz;
+    st->php = php;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rn = rn;
+    st->best_norm = best_norm;
+    st->iterations = it;
+    st->done = 1;
+    st->converged = converged;
+    st->negcurv = negcurv;
+    st->error = error;
+    st->improved = 0;
+  }
+}
+
+// pairs per thread and grid of the pair-local PCG loop for n entries (0: the
+// operator or n does not fit; L1B_PCG_PAIR=0 disables it)
+struct PairPlan {
+  int P = 0, grid = 0;
+};
+template <int P>
+int pair_capacity() {
+  static const int cap = [] {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_pair_kernel<P>, kThreads, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return per_sm * sm_count();
+  }();
+  return cap;
+}
+bool e_persist_on() {
+  const char* e = getenv("L1B_PERSIST");
+  return !(e && e[0] == '0');
+}
+PairPlan pcg_pair_plan(const ProblemView& v) {
+  PairPlan pl;
+  const char* e = getenv("L1B_PCG_PAIR");
+  if (e && e[0] == '0') return pl;
+  const OpView* op = v.op;
+  if (!op || v.shard || op->right.count != 1 || op->left.count != 0 || op->p1 || op->p2 || v.m < v.n)
+    return pl;
+  const uint64_t units = (v.n + 2) / 2;
+  auto try_p = [&](int P, int cap) {
+    const uint64_t per = (uint64_t)P * kThreads;
+    const uint64_t g = (units + per - 1) / per;
+    if (!pl.P && cap > 0 && g <= (uint64_t)cap) {
+      pl.P = P;
+      pl.grid = (int)g;
+    }
+  };
+  try_p(1, pair_capacity<1>());
+  try_p(2, pair_capacity<2>());
+  try_p(4, pair_capacity<4>());
+  try_p(8, pair_capacity<8>());
+  return pl;
+}
+
 // grid of the cooperative PCG loop (0: not applicable -> the four-kernel loop)
 template <typename PtrT, int K>
 int pcg_loop_grid() {
@@ -587,6 +791,7 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
                                                                             : pcg_loop_grid<uint64_t, 0>();
       }
     }
+    const PairPlan pair = (e_persist_on() ? pcg_pair_plan(v) : PairPlan{});
     const auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] {
       return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -655,7 +860,18 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
       pcg_init_kernel<<<grid_for(n), kThreads, 0, st>>>(grad, pre, rp, pp, step, best, n, dst, partials);
       L1B_LAUNCHED();
       uint64_t launched = 0, chunk = 4;
-      if (coop_grid > 0) {  // the whole solve in one cooperative launch
+      if (pair.P) {  // single stage: pair-local products, one cooperative launch
+        PcgPairArgs pa{n, v.op->right.offset[0], v.op->right.c[0], v.op->right.s[0], v.op->sigma, pre, d2psi,
+                       pp, rp, step, best, dst, partials};
+        void* args[] = {&pa};
+        const void* fn = pair.P == 1   ? (const void*)pcg_pair_kernel<1>
+                         : pair.P == 2 ? (const void*)pcg_pair_kernel<2>
+                         : pair.P == 4 ? (const void*)pcg_pair_kernel<4>
+                                       : (const void*)pcg_pair_kernel<8>;
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pair.grid), dim3(kThreads), args, 0, st));
+        L1B_LAUNCHED();
+        launched = cfg->pcg_max_iters;
+      } else if (coop_grid > 0) {  // the whole solve in one cooperative launch
         PcgArgs pa{v.A.ptr, v.A.idx, v.A.val, v.A.lines, v.At.ptr, v.At.idx, v.At.val, n,
                    pre, d2psi, pp, hav, hp, rp, step, best, dst, partials, pp2};
         void* args[] = {&pa};
