@@ -457,10 +457,17 @@ template <int P>
 __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+  // sigma, d2psi, precond of the thread's entries, constant during the solve:
+  // thread-private slots of shared memory ([k][e][thread]: conflict-free)
+  extern __shared__ double cst[];
+  double* c_sig = cst;
+  double* c_d2 = cst + 2 * P * kThreads;
+  double* c_pre = cst + 4 * P * kThreads;
   NcgDev* st = A.st;
   const int64_t n = (int64_t)A.n;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const int tid = threadIdx.x;
   const double c = A.c, s = A.s;
   const double tau = st->tau, eta = st->eta, rhs_norm = st->rhs_norm;
   const uint64_t max_iters = st->max_iters;
@@ -470,16 +477,23 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
   double p[P][2], r[P][2], stp[P][2], hp[P][2];
   int64_t a[P];
   bool va[P], vb[P];
+  auto slot = [&](int k, int e) { return (2 * k + e) * kThreads + tid; };
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     a[k] = 2 * (int64_t)(g0 + (uint64_t)k * T) - A.off;
     va[k] = a[k] >= 0 && a[k] < n;
     vb[k] = a[k] + 1 >= 0 && a[k] + 1 < n;
-    p[k][0] = va[k] ? A.p[a[k]] : 0.0;
-    p[k][1] = vb[k] ? A.p[a[k] + 1] : 0.0;
-    r[k][0] = va[k] ? A.r[a[k]] : 0.0;
-    r[k][1] = vb[k] ? A.r[a[k] + 1] : 0.0;
-    stp[k][0] = stp[k][1] = 0.0;  // step_0 = 0 (pcg_init_kernel)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const bool v = e == 0 ? va[k] : vb[k];
+      const int64_t i = a[k] + e;
+      p[k][e] = v ? A.p[i] : 0.0;
+      r[k][e] = v ? A.r[i] : 0.0;
+      stp[k][e] = 0.0;  // step_0 = 0 (pcg_init_kernel)
+      c_sig[slot(k, e)] = v ? A.sigma[i] : 0.0;
+      c_d2[slot(k, e)] = v ? A.d2psi[i] : 0.0;
+      c_pre[slot(k, e)] = v ? A.pre[i] : 1.0;
+    }
   }
   double* part_b = A.partials;
   double* part_c = A.partials + (size_t)gridDim.x;
@@ -491,25 +505,16 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
       const bool pair = va[k] && vb[k];
       double v0 = p[k][0], v1 = p[k][1];
       if (pair) rotate_pair(v0, v1, c, s, true);  // G^T p
-      const double s0 = va[k] ? __ldg(A.sigma + a[k]) : 0.0;
-      const double s1 = vb[k] ? __ldg(A.sigma + a[k] + 1) : 0.0;
+      const double s0 = c_sig[slot(k, 0)], s1 = c_sig[slot(k, 1)];
       double w0 = s0 * (s0 * v0), w1 = s1 * (s1 * v1);  // Sigma^T (Sigma G^T p)
       if (pair) rotate_pair(w0, w1, c, s, false);      // G (...)
-      if (va[k]) {
-        hp[k][0] = w0 + tau * __ldg(A.d2psi + a[k]) * p[k][0];
-        acc[0] += p[k][0] * hp[k][0];
-      } else {
-        hp[k][0] = 0.0;
-      }
-      if (vb[k]) {
-        hp[k][1] = w1 + tau * __ldg(A.d2psi + a[k] + 1) * p[k][1];
-        acc[0] += p[k][1] * hp[k][1];
-      } else {
-        hp[k][1] = 0.0;
-      }
+      hp[k][0] = w0 + tau * c_d2[slot(k, 0)] * p[k][0];
+      hp[k][1] = w1 + tau * c_d2[slot(k, 1)] * p[k][1];
+      if (va[k]) acc[0] += p[k][0] * hp[k][0];
+      if (vb[k]) acc[0] += p[k][1] * hp[k][1];
     }
     block_sum<1>(acc);
-    if (threadIdx.x == 0) part_b[blockIdx.x] = acc[0];
+    if (tid == 0) part_b[blockIdx.x] = acc[0];
     grid.sync();
     {
       double tot[1];
@@ -522,22 +527,26 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
       break;
     }
     alpha = rz / php;
-    // step += alpha p; r -= alpha hp (:238-241); ||r||^2, r.z with z = r / pre
+    // step += alpha p; r -= alpha hp (:238-241); ||r||^2 and r.z, z = r / pre
+    // kept for the direction update
     double acc2[2] = {0.0, 0.0};
+    double z[P][2];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        if (!(e == 0 ? va[k] : vb[k])) continue;
         stp[k][e] += alpha * p[k][e];
         const double ri = r[k][e] - alpha * hp[k][e];
         r[k][e] = ri;
-        acc2[0] += ri * ri;
-        acc2[1] += ri * (ri / __ldg(A.pre + a[k] + e));
+        z[k][e] = ri / c_pre[slot(k, e)];
+        if (e == 0 ? va[k] : vb[k]) {
+          acc2[0] += ri * ri;
+          acc2[1] += ri * z[k][e];
+        }
       }
     }
     block_sum<2>(acc2);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       part_c[(size_t)blockIdx.x * 2] = acc2[0];
       part_c[(size_t)blockIdx.x * 2 + 1] = acc2[1];
     }
@@ -566,8 +575,8 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
     rz = tot[1];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      if (va[k]) p[k][0] = r[k][0] / __ldg(A.pre + a[k]) + beta * p[k][0];
-      if (vb[k]) p[k][1] = r[k][1] / __ldg(A.pre + a[k] + 1) + beta * p[k][1];
+      p[k][0] = z[k][0] + beta * p[k][0];
+      p[k][1] = z[k][1] + beta * p[k][1];
     }
     if (it >= max_iters) break;
   }
@@ -576,7 +585,7 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
     if (va[k]) A.step[a[k]] = stp[k][0];
     if (vb[k]) A.step[a[k] + 1] = stp[k][1];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     st->rz = rz;
     st->php = php;
     st->alpha = alpha;
@@ -592,6 +601,11 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
   }
 }
 
+template <int P>
+constexpr int pair_smem() {
+  return 6 * P * kThreads * (int)sizeof(double);
+}
+
 // pairs per thread and grid of the pair-local PCG loop for n entries (0: the
 // operator or n does not fit; L1B_PCG_PAIR=0 disables it)
 struct PairPlan {
@@ -601,8 +615,10 @@ template <int P>
 int pair_capacity() {
   static const int cap = [] {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_pair_kernel<P>, kThreads, 0) !=
-        cudaSuccess) {
+    if (cudaFuncSetAttribute(pcg_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem<P>()) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_pair_kernel<P>, kThreads, pair_smem<P>()) !=
+            cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
@@ -868,7 +884,9 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
                          : pair.P == 2 ? (const void*)pcg_pair_kernel<2>
                          : pair.P == 4 ? (const void*)pcg_pair_kernel<4>
                                        : (const void*)pcg_pair_kernel<8>;
-        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pair.grid), dim3(kThreads), args, 0, st));
+        const int smem = pair.P == 1 ? pair_smem<1>() : pair.P == 2 ? pair_smem<2>() : pair.P == 4 ? pair_smem<4>()
+                                                                                         : pair_smem<8>();
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pair.grid), dim3(kThreads), args, smem, st));
         L1B_LAUNCHED();
         launched = cfg->pcg_max_iters;
       } else if (coop_grid > 0) {  // the whole solve in one cooperative launch
