@@ -177,3 +177,66 @@ def test_two_iteration_kernel_large_n(oracle, stages):
     otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=12)
     np.testing.assert_array_equal(xp, ox)
     assert rel_err(tp["f"], otr["objective"]) < 1e-12
+
+
+def _pair_instance(oracle, n, off, q, seed):
+    """Single-stage instance with the given stage offset, built by the oracle
+    (b = A x* + tau A (A^T A)^-1 g) and uploaded as-is."""
+    import ctypes as C
+
+    from pyoracle import Instance, _ptr
+
+    js = oracle.mix_seed(seed, 0)
+    op = oracle.spec(n, stages=1, q=q, job_seed=js)
+    op.right_offset = np.array([off], dtype=np.int32)
+    s = max(1, n // 50)
+    rng = oracle.rng(oracle.mix_seed(js, 4))
+    sup = np.empty(s, dtype=np.uint32)
+    vals = np.empty(s)
+    oracle.lib.lo_uniform_sparse_solution(n, s, 10.0, C.byref(rng), _ptr(sup, C.c_uint32), _ptr(vals, C.c_double))
+    gen = oracle.rng(oracle.mix_seed(js, 5))
+    b = np.empty(op.m)
+    st = op.c_struct()
+    noise = oracle.lib.lo_generate_instance(C.byref(st), 1.0, _ptr(sup, C.c_uint32), _ptr(vals, C.c_double), s,
+                                            0.9, C.byref(gen), _ptr(b, C.c_double))
+    return Instance(op, 1.0, b, sup, vals, float(noise), js)
+
+
+@pytest.mark.parametrize("n,off", [(4096, 0), (4095, 1), (2047, 0), (1000, 1), (513, 0), (6, 1), (3, 0)])
+def test_pair_small_kernel_bit_identical(oracle, n, off):
+    """The pair-local one-CTA kernel (single stage, n <= 4096) against the
+    oracle and the window kernel (L1B_PAIR_SMALL=0): identical iterates,
+    samples, stop."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    oi = _pair_instance(oracle, n, off, q=1, seed=n + off)
+    inst = l1bench.ProblemInstance.from_host(oi.m, n, [(off, TH)], oi.op.sigma, oi.b, 1.0, oi.support, oi.values)
+    iters = 300
+    tr, x = _solve(inst, iters, rc=True)
+    otr, ox = oracle.fista(oi, max_iters=iters)
+    np.testing.assert_array_equal(x, ox)
+    np.testing.assert_array_equal(tr.iters(), otr["iter"])
+    assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
+    tw, xw = _solve(inst, iters, rc=True, env={"L1B_PAIR_SMALL": "0"})
+    np.testing.assert_array_equal(x, xw)
+    np.testing.assert_array_equal(tr.iters(), tw.iters())
+    assert tr.status == tw.status
+    np.testing.assert_array_equal([s.nnz for s in tr.samples], [s.nnz for s in tw.samples])
+
+
+def test_pair_small_kernel_target_stop(oracle):
+    """C1-style run to a target objective: same stopping iteration as the oracle."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    oi = _pair_instance(oracle, 4096, 0, q=1, seed=77)
+    inst = l1bench.ProblemInstance.from_host(oi.m, 4096, [(0, TH)], oi.op.sigma, oi.b, 1.0, oi.support,
+                                             oi.values)
+    f0 = 0.5 * float((oi.b ** 2).sum())
+    target = oi.f_star() + 1e-8 * (f0 - oi.f_star())
+    tr, x = _solve(inst, 100000, rc=True, target_objective=target)
+    otr, ox = oracle.fista(oi, max_iters=100000, target=target)
+    assert tr.status == l1bench.StopReason.target_reached
+    np.testing.assert_array_equal(tr.iters(), otr["iter"])
+    np.testing.assert_array_equal(x, ox)
