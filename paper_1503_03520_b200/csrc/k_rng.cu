@@ -17,8 +17,9 @@
 //     on 2 x 19937 output bits (host, once per process).
 //   * W_{k+J} = sum_j p_j W_{k+j} for p(t) = t^J mod P: jumping is one
 //     generation of 19937 words plus, for each of the 312 state words, an XOR
-//     over the set coefficients -- the 312 words are independent, one thread
-//     each, the whole sequence in shared memory (158 KB).
+//     over the set coefficients -- the 312 words are independent; 3 x 312
+//     threads each take a third of the coefficients, the whole sequence in
+//     shared memory (158 KB).
 //   * Chunk starts are built by a 16-ary tree of jumps (t^(16^l J) mod P by
 //     repeated squaring on the host, cached): <= 3 levels x 15 sequential
 //     jumps for C <= 4096 chunks.
@@ -209,7 +210,9 @@ const Poly& pow2_poly(int e) {
 //
 // CTA b takes window starts[b] and writes `count` windows out[b*FAN + t]
 // (t < count, clipped at `total`): t = 0 is the start, t -> t+1 jumps by poly.
-constexpr int JUMP_THREADS = 320;
+constexpr int JUMP_THREADS = 1024;
+constexpr int JUMP_SLICES = 3;  // the coefficient words split over 3 x 312 threads
+constexpr int SLICE_WORDS = (PW + JUMP_SLICES - 1) / JUMP_SLICES;
 
 __global__ void __launch_bounds__(JUMP_THREADS) mt_jump_kernel(const uint64_t* __restrict__ starts,
                                                               const uint64_t* __restrict__ poly,
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(JUMP_THREADS) mt_jump_kernel(const uint64_t* _
   extern __shared__ uint64_t smem[];
   uint64_t* x = smem;          // SEQ words
   uint64_t* p = smem + SEQ;    // PW words
+  uint64_t* part = p + PW;     // JUMP_SLICES x NW partial sums
   const int tid = threadIdx.x;
   const uint64_t first = (uint64_t)blockIdx.x * FAN;
   for (int i = tid; i < NW; i += blockDim.x) x[i] = starts[(uint64_t)blockIdx.x * NW + i];
@@ -230,19 +234,28 @@ __global__ void __launch_bounds__(JUMP_THREADS) mt_jump_kernel(const uint64_t* _
         if (tid < MID && k < DEG) x[k + NW] = next_word(x[k], x[k + 1], x[k + MID]);
         __syncthreads();
       }
-      uint64_t acc = 0;
-      if (tid < NW) {
-        for (int w = 0; w < PW; ++w) {
+      // word k of the jumped window = XOR over set coefficients j of x[j + k]:
+      // thread (slice, k) takes the coefficient words of its slice
+      if (tid < JUMP_SLICES * NW) {
+        const int k = tid % NW, sl = tid / NW;
+        const int w1 = min(PW, (sl + 1) * SLICE_WORDS);
+        uint64_t acc = 0;
+        for (int w = sl * SLICE_WORDS; w < w1; ++w) {
           uint64_t bits = p[w];
           while (bits) {
             const int j = (w << 6) + __ffsll((long long)bits) - 1;
             bits &= bits - 1;
-            acc ^= x[j + tid];
+            acc ^= x[j + k];
           }
         }
+        part[sl * NW + k] = acc;
       }
       __syncthreads();
-      if (tid < NW) x[tid] = acc;
+      if (tid < NW) {
+        uint64_t acc = 0;
+        for (int sl = 0; sl < JUMP_SLICES; ++sl) acc ^= part[sl * NW + tid];
+        x[tid] = acc;
+      }
       __syncthreads();
     }
     for (int i = tid; i < NW; i += blockDim.x) out[(first + t) * NW + i] = x[i];
@@ -381,7 +394,7 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
       L1B_CUDA(cudaStreamSynchronize(st));
     }
   }
-  const int smem = (SEQ + PW) * 8;
+  const int smem = (SEQ + PW + JUMP_SLICES * NW) * 8;
   L1B_CUDA(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   uint64_t n_prev = 1;
   for (int l = 0; l < levels; ++l) {
