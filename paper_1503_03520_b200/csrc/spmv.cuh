@@ -98,7 +98,17 @@ __global__ void __launch_bounds__(kThreads) spmv_warp_kernel(const PtrT* __restr
 // ~35 KB Little's law needs at HBM bandwidth.
 constexpr int kTileLines = 256;   // == kThreads
 constexpr int kTileNnz = 2048;    // nonzero capacity of one tile
-constexpr int kStages = 3;
+#ifndef L1B_SPMV_STAGES
+#define L1B_SPMV_STAGES 3
+#endif
+#ifndef L1B_SPMV_VEC
+#define L1B_SPMV_VEC 1  // stage the epilogue vectors with TMA too
+#endif
+#ifndef L1B_SPMV_MINB
+#define L1B_SPMV_MINB 2  // CTAs per SM the register allocation targets
+#endif
+constexpr int kStages = L1B_SPMV_STAGES;
+constexpr int kVecTma = L1B_SPMV_VEC;
 
 template <typename PtrT, int NV>
 struct TmaLayout {
@@ -106,7 +116,7 @@ struct TmaLayout {
   static constexpr size_t vals_bytes = (kTileNnz + 2) * 8;
   static constexpr size_t idx_bytes = (kTileNnz + 8) * 4;
   static constexpr size_t ptr_bytes = r16((kTileLines + 1 + 16 / sizeof(PtrT)) * sizeof(PtrT));
-  static constexpr size_t vec_bytes = kTileLines * 8;
+  static constexpr size_t vec_bytes = kVecTma ? kTileLines * 8 : 0;
   static constexpr size_t stage_bytes = vals_bytes + idx_bytes + ptr_bytes + NV * vec_bytes;
   static constexpr size_t prod_off = kStages * stage_bytes;
   static constexpr size_t prod_bytes = r16((kTileNnz + kTileNnz / 16 + 2) * 8);
@@ -115,7 +125,7 @@ struct TmaLayout {
 };
 
 template <typename PtrT, class Epi>
-__global__ void __launch_bounds__(kThreads, 2) spmv_tma_kernel(const PtrT* __restrict__ ptr,
+__global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const PtrT* __restrict__ ptr,
                                                                const uint32_t* __restrict__ idx,
                                                                const double* __restrict__ val,
                                                                const double* __restrict__ x,
@@ -251,7 +261,7 @@ inline void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t
                                                             kThreads, L::total));
       grid_cap = std::max(1, per_sm) * sm_count();
     }
-    int vec_tma = 1;
+    int vec_tma = kVecTma;
     for (int v = 0; v < Epi::kVec; ++v)
       if (reinterpret_cast<uintptr_t>(epi.vec(v)) % 16) vec_tma = 0;
     const uint64_t tiles = (M.lines + kTileLines - 1) / kTileLines;
