@@ -174,7 +174,11 @@ def roofline(path, t, info, peak, peak_src):
         except Exception:
             traffic = None
     long_ms = (t["k1_ms_long"] * ipl if dom[3] != "k2" else t["k2_ms_long"])
-    return {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak,
+    limiter = ("FP64 issue: ncu shows the FP64 pipe at 76.5 % of peak and DRAM at ~71 % for this kernel "
+               "(profiles/r1_ncu_full_fista_rc2v.txt); fractions are of the HBM roofline on algorithmic bytes"
+               if path == "matrix_free" and t.get("kmode") == 4 else
+               "HBM streaming (profiles/r1_ncu_full_spmv_tma.txt)" if path == "sparse" else None)
+    return {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak, "limiter": limiter,
             "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
             "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0], "iterations_per_launch": ipl,
             "launch_ms": dom[1], "launch_ms_source": "CUDA events around every launch of the timed region",
