@@ -92,6 +92,8 @@ def _with_env(val, fn):
     dict(n=4096, stages=4, q=1, s_divisor=100, seed=3),
     dict(n=5000, stages=2, left_stages=1, permute=True, q=2, s_divisor=50, seed=6),
     dict(n=4096, stages=1, q=1, s_divisor=100, seed=2, solution="spectral", s1_fraction=0.5),
+    dict(n=3001, stages=3, alternating=(2.0, 0.5), s_divisor=30, seed=8),
+    dict(n=2048, stages=2, q=1, s_divisor=64, seed=9, solution="two_value"),
 ])
 def test_generator_device_rng_equals_host_and_oracle(oracle, kw):
     need_cuda()
@@ -105,10 +107,28 @@ def test_generator_device_rng_equals_host_and_oracle(oracle, kw):
     np.testing.assert_array_equal(dev.x_star.support, host.x_star.support)
     np.testing.assert_array_equal(dev.x_star.values, host.x_star.values)
     assert dev.noise_norm == host.noise_norm
-    if kw.get("solution", "uniform") == "uniform":
+    if kw.get("solution", "uniform") == "uniform" and "alternating" not in kw:
         okw = {k: v for k, v in kw.items() if k not in ("solution", "s1_fraction")}
         oi = oracle.build_instance(**okw)
         np.testing.assert_array_equal(dev.b, oi.b)
+
+
+def test_shard_device_rng_ragged_and_single_rank():
+    """A shard layout whose windows reach both stream ends (world 1) and an
+    uneven 5-way split of an n that is no multiple of the chunking."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    kw = dict(n=70001, stages=4, q=2, s_divisor=70, seed=12, theta=2 * math.pi / 10)
+    whole = _with_env("0", lambda: l1bench.build_instance(**kw))
+    cfg = l1bench.SolverConfig(max_iters=2)
+    for world in (1, 5):
+        shards = _with_env("1", lambda: [CudaShard(kw, r, world, 0, cfg) for r in range(world)])
+        for s in shards:
+            a, e = s.inst.info.row_begin, s.inst.info.row_end
+            np.testing.assert_array_equal(s.inst.b[: e - a], whole.b[a:e])
+            assert s.inst.info.gram_lmax == whole.info.gram_lmax
 
 
 def test_shards_device_rng_reproduce_global_instance():
