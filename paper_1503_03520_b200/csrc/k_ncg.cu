@@ -453,16 +453,16 @@ struct PcgPairArgs {
   double* partials;  // >= 3 x grid doubles
 };
 
-template <int P>
-__global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
+template <int P, int BT = kThreads>
+__global__ void __launch_bounds__(BT) pcg_pair_kernel(PcgPairArgs A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   // sigma, d2psi, precond of the thread's entries, constant during the solve:
   // thread-private slots of shared memory ([k][e][thread]: conflict-free)
   extern __shared__ double cst[];
   double* c_sig = cst;
-  double* c_d2 = cst + 2 * P * kThreads;
-  double* c_pre = cst + 4 * P * kThreads;
+  double* c_d2 = cst + 2 * P * BT;
+  double* c_pre = cst + 4 * P * BT;
   NcgDev* st = A.st;
   const int64_t n = (int64_t)A.n;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
   double p[P][2], r[P][2], stp[P][2], hp[P][2];
   int64_t a[P];
   bool va[P], vb[P];
-  auto slot = [&](int k, int e) { return (2 * k + e) * kThreads + tid; };
+  auto slot = [&](int k, int e) { return (2 * k + e) * BT + tid; };
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     a[k] = 2 * (int64_t)(g0 + (uint64_t)k * T) - A.off;
@@ -601,23 +601,23 @@ __global__ void __launch_bounds__(kThreads) pcg_pair_kernel(PcgPairArgs A) {
   }
 }
 
-template <int P>
+template <int P, int BT = kThreads>
 constexpr int pair_smem() {
-  return 6 * P * kThreads * (int)sizeof(double);
+  return 6 * P * BT * (int)sizeof(double);
 }
 
 // pairs per thread and grid of the pair-local PCG loop for n entries (0: the
 // operator or n does not fit; L1B_PCG_PAIR=0 disables it)
 struct PairPlan {
-  int P = 0, grid = 0;
+  int P = 0, grid = 0, bt = kThreads;
 };
-template <int P>
+template <int P, int BT = kThreads>
 int pair_capacity() {
   static const int cap = [] {
     int per_sm = 0;
-    if (cudaFuncSetAttribute(pcg_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem<P>()) !=
-            cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_pair_kernel<P>, kThreads, pair_smem<P>()) !=
+    if (cudaFuncSetAttribute(pcg_pair_kernel<P, BT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pair_smem<P, BT>()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_pair_kernel<P, BT>, BT, pair_smem<P, BT>()) !=
             cudaSuccess) {
       cudaGetLastError();
       return 0;
@@ -638,16 +638,22 @@ PairPlan pcg_pair_plan(const ProblemView& v) {
   if (!op || v.shard || op->right.count != 1 || op->left.count != 0 || op->p1 || op->p2 || v.m < v.n)
     return pl;
   const uint64_t units = (v.n + 2) / 2;
-  auto try_p = [&](int P, int cap) {
-    const uint64_t per = (uint64_t)P * kThreads;
+  auto try_p = [&](int P, int cap, int bt = kThreads) {
+    const uint64_t per = (uint64_t)P * bt;
     const uint64_t g = (units + per - 1) / per;
     if (!pl.P && cap > 0 && g <= (uint64_t)cap) {
       pl.P = P;
       pl.grid = (int)g;
+      pl.bt = bt;
     }
   };
+  // four pairs per thread: 512-thread CTAs (one per SM, fewer partials per
+  // barrier; C3 42.3 -> 39.7 ms) unless L1B_PCG_BT=256
+  const char* eb = getenv("L1B_PCG_BT");
+  const bool wide = !(eb && atoi(eb) == 256);
   try_p(1, pair_capacity<1>());
   try_p(2, pair_capacity<2>());
+  if (wide) try_p(4, pair_capacity<4, 512>(), 512);
   try_p(4, pair_capacity<4>());
   try_p(8, pair_capacity<8>());
   return pl;
@@ -880,13 +886,18 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
         PcgPairArgs pa{n, v.op->right.offset[0], v.op->right.c[0], v.op->right.s[0], v.op->sigma, pre, d2psi,
                        pp, rp, step, best, dst, partials};
         void* args[] = {&pa};
-        const void* fn = pair.P == 1   ? (const void*)pcg_pair_kernel<1>
-                         : pair.P == 2 ? (const void*)pcg_pair_kernel<2>
-                         : pair.P == 4 ? (const void*)pcg_pair_kernel<4>
-                                       : (const void*)pcg_pair_kernel<8>;
-        const int smem = pair.P == 1 ? pair_smem<1>() : pair.P == 2 ? pair_smem<2>() : pair.P == 4 ? pair_smem<4>()
-                                                                                         : pair_smem<8>();
-        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pair.grid), dim3(kThreads), args, smem, st));
+        const bool wide = pair.bt == 512;
+        const void* fn = wide            ? (const void*)pcg_pair_kernel<4, 512>
+                         : pair.P == 1   ? (const void*)pcg_pair_kernel<1>
+                         : pair.P == 2   ? (const void*)pcg_pair_kernel<2>
+                         : pair.P == 4   ? (const void*)pcg_pair_kernel<4>
+                                         : (const void*)pcg_pair_kernel<8>;
+        const int smem = wide            ? pair_smem<4, 512>()
+                         : pair.P == 1   ? pair_smem<1>()
+                         : pair.P == 2   ? pair_smem<2>()
+                         : pair.P == 4   ? pair_smem<4>()
+                                         : pair_smem<8>();
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(pair.grid), dim3(pair.bt), args, smem, st));
         L1B_LAUNCHED();
         launched = cfg->pcg_max_iters;
       } else if (coop_grid > 0) {  // the whole solve in one cooperative launch
