@@ -105,7 +105,9 @@ def test_rc_session_stepping_matches_solve():
 
 # (the switches are read once per process by the library, so each mode below
 # runs in a subprocess of its own)
-_MODES = {"loop": {}, "pairs": {"L1B_PERSIST": "0"}, "single": {"L1B_PERSIST": "0", "L1B_RC2": "0"}}
+_MODES = {"loop": {}, "pairs": {"L1B_PERSIST": "0"}, "single": {"L1B_PERSIST": "0", "L1B_RC2": "0"},
+          # two-iteration kernel shapes (L1B_RC2_VARIANT): 4 / 6 per lane, 8 without prefetch
+          **{f"pairs_v{v}": {"L1B_PERSIST": "0", "L1B_RC2_VARIANT": str(v)} for v in (1, 2, 3)}}
 
 
 def _mode_run(mode, kw, iters, target=None):
@@ -136,14 +138,15 @@ def _mode_run(mode, kw, iters, target=None):
         return json.loads(p.stdout.strip().splitlines()[-1]), np.load(out)
 
 
+@pytest.mark.parametrize("mode", ["pairs", "pairs_v1", "pairs_v2", "pairs_v3"])
 @pytest.mark.parametrize("n,stages", [(100003, 4), (30001, 3), (20005, 2), (7777, 1)])
-def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages):
-    """fista_rc2_kernel (two iterations per launch) vs one iteration per launch
-    and vs the oracle: identical x, objectives within 1e-12."""
+def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages, mode):
+    """fista_rc2_kernel (two iterations per launch, every kernel shape) vs one
+    iteration per launch and vs the oracle: identical x, objectives within 1e-12."""
     need_cuda()
     kw = dict(n=n, stages=stages, q=1, s_divisor=100, seed=5, theta=TH)
     iters = 41  # odd: the last launch is a single iteration
-    tp, xp = _mode_run("pairs", kw, iters)
+    tp, xp = _mode_run(mode, kw, iters)
     ts, xs = _mode_run("single", kw, iters)
     np.testing.assert_array_equal(xp, xs)
     assert tp["it"] == ts["it"] and tp["k"] == ts["k"] == iters
