@@ -237,6 +237,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sparse", action="store_true", help="skip the CSR/CSC leg (tuning runs)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C3 side line")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-sharded NCCL driver even with one rank (plumbing check)")
     args = ap.parse_args()
@@ -319,12 +320,36 @@ def main():
     if e2e_line is not None:
         line["e2e"] = e2e_line
     del inst
+    if not args.no_configs:
+        try:
+            line["other_configs"] = small_configs()
+        except Exception as e:  # reported, never silently substituted
+            line["other_configs"] = {"error": str(e)}
     if not args.no_cpu:
         try:
             line["cpu_baseline"] = run_reference(args, warmup=1, steps=8)
         except Exception as e:  # reported, never silently substituted
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line))
+
+
+def small_configs():
+    """BASELINE.json's single-GPU side configurations C1-C3 (configs.py, same
+    mapping): device time of the whole run / to the tolerance on this GPU.  The
+    reference's CPU times beside them are in profiles/r1_configs.json."""
+    import configs as C
+
+    out = {}
+    for name in ("c1", "c2", "c3"):
+        r = C.run_gpu(name, C.CONFIGS[name])
+        e = {"desc": r["desc"], "iterations": r["iterations"], "device_s": r["solve_device_s"],
+             "status": r["status"], "rel_gap_final": r["rel_gap_final"]}
+        if "time_to_target_s" in r:
+            e["time_to_tolerance_s"] = r["time_to_target_s"]
+        if "pcg_iterations" in r:
+            e["pcg_iterations"] = r["pcg_iterations"]
+        out[name] = e
+    return out
 
 
 def e2e(inst, args, device):
