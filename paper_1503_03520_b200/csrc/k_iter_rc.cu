@@ -378,11 +378,25 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
           if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
       }
     } else {
-      double right[K], left[K];
+      // the pair straddling lanes l, l+1 is rotated once, by lane l, which
+      // hands the right output back (one rotation fewer per lane and odd stage
+      // than rotating it on both sides)
+      double right[K], back[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) right[q] = __shfl_down_sync(kFull, v[q][0], 1);
+      const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
+      const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
-        right[q] = __shfl_down_sync(kFull, v[q][0], 1);
-        left[q] = __shfl_up_sync(kFull, v[q][V - 1], 1);
+        double a = v[q][V - 1], b = right[q];
+        if (pr) rotate_pair(a, b, c, sn, TR);
+        v[q][V - 1] = a;
+        back[q] = b;
+      }
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const double b = __shfl_up_sync(kFull, back[q], 1);
+        if (pl) v[q][0] = b;
       }
 #pragma unroll
       for (int p = 1; p + 1 < V; p += 2) {
@@ -390,21 +404,6 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
 #pragma unroll
         for (int q = 0; q < K; ++q)
           if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
-      }
-      const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
-      const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
-#pragma unroll
-      for (int q = 0; q < K; ++q) {
-        if (pr) {
-          double a = v[q][V - 1], b = right[q];
-          rotate_pair(a, b, c, sn, TR);
-          v[q][V - 1] = a;
-        }
-        if (pl) {
-          double a = left[q], b = v[q][0];
-          rotate_pair(a, b, c, sn, TR);
-          v[q][0] = b;
-        }
       }
     }
   }
