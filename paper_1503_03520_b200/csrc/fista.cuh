@@ -16,6 +16,7 @@ __device__ __forceinline__ void fista_momentum(const FistaDev* st, double* t_nex
 
 // Iteration k's record and stop checks (solvers.cpp:366-376 + the loop-head
 // checks :312-313): f, trace sample, fixed point / target / iteration budget.
+// trace == nullptr: the bookkeeping without the sample store (replicas).
 __device__ inline void fista_record(FistaDev* st, FistaSample* trace, uint64_t k, double f,
                                     double nnz, bool fixed, uint64_t ts) {
   st->k = k;
@@ -28,7 +29,7 @@ __device__ inline void fista_record(FistaDev* st, FistaSample* trace, uint64_t k
     return;
   }
   if (k <= 1000 || k % 10 == 0 || fixed) {
-    if (st->n_samples < st->cap) trace[st->n_samples] = FistaSample{k, f, nnz, ts};
+    if (trace && st->n_samples < st->cap) trace[st->n_samples] = FistaSample{k, f, nnz, ts};
     st->n_samples++;
     st->last_sampled = k;
   }

@@ -941,19 +941,22 @@ __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_small(RcPArgs Pa, 
 }
 
 // The same pair-local iteration on a cluster of kClusterCtas CTAs (one per SM):
-// FP64 work and the per-thread pair count shrink 8x, the reduction goes
-// through distributed shared memory -- every CTA stores its four block sums
-// into CTA 0, CTA 0 folds them in rank order, runs the lagged bookkeeping and
-// broadcasts (stop, beta) back -- two cluster barriers per iteration.
+// FP64 work and the per-thread pair count shrink 8x.  The reduction goes
+// through distributed shared memory with ONE cluster barrier per iteration:
+// every CTA stores its four block sums into every CTA (double-buffered by
+// iteration parity), and after the barrier each CTA folds the eight partials
+// in rank order and runs the lagged bookkeeping on its own copy of the FISTA
+// state -- identical inputs, identical decisions; only CTA 0 writes the trace
+// and the state back.
 constexpr int kClusterCtas = 8;
 
 template <int P>
 __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_cluster(RcPArgs Pa, int off) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ FistaDev sst;                  // meaningful in CTA 0
-  __shared__ double part[kClusterCtas][4];  // CTA 0: the block sums of every CTA
-  __shared__ double bc[2];                  // (stop, beta_y) broadcast by CTA 0
+  __shared__ FistaDev sst;                     // every CTA: its replica of the state
+  __shared__ double part[2][kClusterCtas][4];  // block sums of every CTA, by parity
+  __shared__ double bc[2];                     // (stop, beta_y) of the replica
   extern __shared__ double cs[];
   const RcArgs& A = Pa.a;
   const int64_t n = A.n;
@@ -964,9 +967,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_cluster(RcPArgs Pa
   double* c_b = cs + 2 * P * T;
   auto slot = [&](int k, int e) { return (2 * k + e) * T + t; };
   if (t == 0) {
-    if (rank == 0) sst = *A.b.st;
-    bc[0] = A.b.st->stop ? 1.0 : 0.0;
-    bc[1] = A.b.st->beta_y;
+    sst = *A.b.st;
+    bc[0] = sst.stop ? 1.0 : 0.0;
+    bc[1] = sst.beta_y;
   }
   const double inv_l = 1.0 / A.b.st->lval;
   const double thr = A.b.st->tau * inv_l;
@@ -996,11 +999,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_cluster(RcPArgs Pa
     pair_residual(xk[k][0], xk[k][1], pair, c, s, s0, s1, b0, b1, rk[k][0], rk[k][1]);
     pair_residual(xm[k][0], xm[k][1], pair, c, s, s0, s1, b0, b1, rm[k][0], rm[k][1]);
   }
-  double* part0 = cluster.map_shared_rank(&part[0][0], 0);
-  cluster.sync();
+  __syncthreads();
   uint64_t done = 0;
   for (; done < Pa.iters; ++done) {
-    if (bc[0] != 0.0) break;  // uniform over the cluster: written before the last barrier
+    if (bc[0] != 0.0) break;  // every replica took the same decision
     const double beta = bc[1];
     double l1 = 0.0, rr = 0.0;
     unsigned nz = 0, mism = 0;
@@ -1039,27 +1041,28 @@ __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_cluster(RcPArgs Pa
     }
     double sums[4] = {l1, (double)nz, (double)mism, rr};
     block_sum<4>(sums);
-    if (t == 0) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) part0[rank * 4 + q] = sums[q];
+    const int par = (int)(done & 1);
+    if (t < kClusterCtas) {  // thread r stores this CTA's sums into CTA r
+      double* dst = cluster.map_shared_rank(&part[par][rank][0], t);
+      // thread 0 holds the block sums; the others read them from shared memory
+      dst[0] = __shfl_sync(0xffu, sums[0], 0);
+      dst[1] = __shfl_sync(0xffu, sums[1], 0);
+      dst[2] = __shfl_sync(0xffu, sums[2], 0);
+      dst[3] = __shfl_sync(0xffu, sums[3], 0);
     }
     cluster.sync();
-    if (rank == 0 && t == 0) {
+    if (t == 0) {
       double tot[4] = {0.0, 0.0, 0.0, 0.0};
       for (int r = 0; r < kClusterCtas; ++r)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) tot[q] += part[r][q];
+        for (int q = 0; q < 4; ++q) tot[q] += part[par][r][q];
 #pragma unroll
       for (int q = 0; q < 4; ++q) sst.scal[q] = tot[q];
-      fista_finalize_lagged(&sst, A.b.trace, false);
-      const double st0 = sst.stop ? 1.0 : 0.0, bt = sst.beta_y;
-      for (int r = 0; r < kClusterCtas; ++r) {
-        double* rb = cluster.map_shared_rank(&bc[0], r);
-        rb[0] = st0;
-        rb[1] = bt;
-      }
+      fista_finalize_lagged(&sst, rank == 0 ? A.b.trace : nullptr, false);
+      bc[0] = sst.stop ? 1.0 : 0.0;
+      bc[1] = sst.beta_y;
     }
-    cluster.sync();
+    __syncthreads();
   }
   double* Xk = Pa.X[(j0 + done) % 4];
   double* Xm = Pa.X[(j0 + done + 3) % 4];
@@ -1074,6 +1077,8 @@ __global__ void __launch_bounds__(kPairThreads, 1) fista_pair_cluster(RcPArgs Pa
       Xm[a[k] + 1] = xm[k][1];
     }
   }
+  // no CTA may exit while others could still store into its shared memory
+  cluster.sync();
   if (rank == 0 && t == 0) *A.b.st = sst;
 }
 
