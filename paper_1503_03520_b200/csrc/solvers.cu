@@ -808,7 +808,9 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     L1B_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     bool pending[2] = {false, false};
     int slot = 0;
-    uint64_t chunk = 4;
+    // small instances run whole chunks in one launch (fista_rc_loop): start at
+    // the full chunk, each launch costs a reload of the instance
+    uint64_t chunk = uses_loop(&s) ? 64 : 4;
     try {
       while (s.launched < cfg->max_iters) {
         // loop-head time check (solvers.cpp:314), at chunk granularity
