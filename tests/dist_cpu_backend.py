@@ -325,6 +325,156 @@ class CpuShardRc:
         return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()
 
 
+class CpuShardRc2:
+    """Two-iterations-per-launch stand-in (k_iter_rc.cu fista_rc2v_kernel, the
+    default shard mode): x rotates through four windows with halo H = 4S; one
+    k1() rebuilds r_j, r_{j-1} on rows [a-3S, b+3S), forms x_{j+1} on columns
+    [a-2S, b+2S), r_{j+1} on rows [a-S, b+S) and x_{j+2} on the own columns,
+    and leaves the 8 sums of scal8 (||r_j||^2, l1 / nnz / mismatches of
+    x_{j+1}, ||r_{j+1}||^2, those of x_{j+2}) for the all-reduce; finalize
+    records two iterations (fista_finalize_lagged2); the flush records the
+    last iterate (fista_finalize_lagged)."""
+
+    def __init__(self, oracle, inst, rank, world, max_iters):
+        self.rank, self.world, self.single, self.lagged, self.pairs = rank, world, True, True, True
+        n = inst.n
+        S = len(inst.op.right_offset)
+        H = 4 * S
+        a, b = partition(n, world)[rank]
+        self.n, self.a, self.b_, self.own, self.S = n, a, b, b - a, S
+        self.x_halo, self.r_halo, self.nbuf = H, 0, 4
+        rp, ri, rv = oracle.csr(inst.op)
+        cp, ci, cv = oracle.csc(inst.op)
+        base = a - H  # window-local index of global entry g: g - base
+        self.base = base
+        self.rows = {i: (ri[rp[i]:rp[i + 1]].astype(np.int64) - base, rv[rp[i]:rp[i + 1]])
+                     for i in range(max(0, a - 3 * S), min(n, b + 3 * S))}
+        self.cols = {j: (ci[cp[j]:cp[j + 1]].astype(np.int64), cv[cp[j]:cp[j + 1]])
+                     for j in range(max(0, a - 2 * S), min(n, b + 2 * S))}
+        self.bwin = {i: inst.b[i] for i in self.rows}
+        self.x_bufs = [torch.zeros(self.own + 2 * H, dtype=torch.float64) for _ in range(4)]
+        self.r_bufs = None
+        self.scal = torch.zeros(4, dtype=torch.float64)
+        self.scal8 = torch.zeros(8, dtype=torch.float64)
+        self.scal[3] = float(sum((0.0 - inst.b[i]) ** 2 for i in range(a, b)))
+        self.scal_now = self.scal
+        self.tau, self.L = inst.tau, oracle.gram_lmax(inst.op)
+        self.t, self.beta_y, self.k, self.j = 1.0, 0.0, 0, 0
+        self.stop, self.init, self.pend, self.flushing = False, False, None, False
+        self.max_iters = max_iters
+        self.samples = []
+
+    def next_halos(self):  # x_{j-1} and x_j were both written
+        return [(self.x_bufs[(self.j - 1) % 4], self.x_halo), (self.x_bufs[self.j % 4], self.x_halo)]
+
+    def initial_halos(self):
+        return []
+
+    def _r(self, x, lo, hi):
+        return {i: sum(v * x[q] for q, v in zip(*self.rows[i])) - self.bwin[i]
+                for i in range(max(0, lo), min(self.n, hi))}
+
+    def _momentum(self):
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * self.t * self.t))
+        return t_next, (self.t - 1.0) / t_next
+
+    def _prox(self, xk, xm, r1, r0, beta, lo, hi, out):
+        """x_new on columns [lo, hi) from x_k, x_{k-1} (windows) and the
+        residuals r1 = r_k, r0 = r_{k-1}; returns the own-column sums."""
+        inv_l = 1.0 / self.L
+        thr = self.tau * inv_l
+        l1 = nnz = mism = 0.0
+        for jj in range(max(0, lo), min(self.n, hi)):
+            idx, val = self.cols[jj]
+            g = sum(v * ((1.0 + beta) * r1[i] - beta * r0[i]) for i, v in zip(idx, val))
+            lx = jj - self.base
+            y = xk[lx] + beta * (xk[lx] - xm[lx])
+            v = y - inv_l * g
+            tr = v - thr if v > thr else (v + thr if v < -thr else 0.0)
+            out[lx] = tr
+            if self.a <= jj < self.b_:
+                l1 += abs(tr)
+                nnz += tr != 0.0
+                mism += tr != y
+        return l1, nnz, mism
+
+    def k1(self):
+        j, S, a, b = self.j, self.S, self.a, self.b_
+        self.j += 2
+        self.scal_now = self.scal8
+        if self.stop:
+            return
+        xk, xm = self.x_bufs[j % 4].numpy(), self.x_bufs[(j + 3) % 4].numpy()
+        t_next, beta_b = self._momentum()
+        rk = self._r(xk, a - 3 * S, b + 3 * S)
+        rm = self._r(xm, a - 3 * S, b + 3 * S)
+        rr0 = sum(rk[i] ** 2 for i in range(a, b))
+        x1 = np.zeros_like(xk)
+        l1a, nza, misa = self._prox(xk, xm, rk, rm, self.beta_y, a - 2 * S, b + 2 * S, x1)
+        r1 = self._r(x1, a - S, b + S)
+        rr1 = sum(r1[i] ** 2 for i in range(a, b))
+        x2 = np.zeros_like(xk)
+        l1b, nzb, misb = self._prox(x1, xk, r1, rk, beta_b, a, b, x2)
+        H, own = self.x_halo, self.own
+        self.x_bufs[(j + 1) % 4].numpy()[H:H + own] = x1[H:H + own]
+        self.x_bufs[(j + 2) % 4].numpy()[H:H + own] = x2[H:H + own]
+        self.scal8[:] = torch.tensor([rr0, l1a, nza, misa, rr1, l1b, nzb, misb], dtype=torch.float64)
+
+    def k2(self):
+        pass
+
+    def flush(self):  # ||r||^2 of the newest iterate, recorded by a lagged finalize
+        self.scal_now = self.scal
+        if self.stop:
+            return
+        x = self.x_bufs[self.j % 4].numpy()
+        r = self._r(x, self.a, self.b_)
+        self.scal[0], self.scal[1], self.scal[2] = 0.0, 0.0, 0.0
+        self.scal[3] = sum(r[i] ** 2 for i in range(self.a, self.b_))
+        self.flushing = True
+
+    def _record(self, f, mism):
+        self.k += 1
+        self.samples.append((self.k, f))
+        if mism == 0.0 or self.k >= self.max_iters:
+            self.stop = True
+
+    def finalize(self):
+        if self.stop:
+            return
+        if not self.init:
+            self.init = True
+            self.samples.append((0, 0.5 * float(self.scal[3])))
+            self.stop = self.max_iters == 0
+            return
+        if self.flushing:  # fista_finalize_lagged(flush)
+            if self.pend is not None:
+                l1, _, mism = self.pend
+                self.pend = None
+                self._record(self.tau * l1 + 0.5 * float(self.scal[3]), mism)
+            return
+        q = self.scal8.numpy().copy()
+        if self.pend is not None:  # iteration j: stashed sums + ||r_j||^2
+            l1, _, mism = self.pend
+            self.pend = None
+            self._record(self.tau * l1 + 0.5 * q[0], mism)
+            if self.stop:
+                return
+        self.t, self.beta_y = self._momentum()  # the step the kernel used for x_{j+2}
+        self._record(self.tau * q[1] + 0.5 * q[4], q[3])  # iteration j+1
+        if self.stop:
+            return
+        self.t, self.beta_y = self._momentum()
+        self.pend = (q[5], q[6], q[7])
+
+    def stopped(self):
+        return self.stop, self.k
+
+    def finish(self):
+        q = self.k % 4
+        return self.samples, self.x_bufs[q].numpy()[self.x_halo:self.x_halo + self.own].copy()
+
+
 class CpuShardGeneral:
     """General-operator stand-in (permuted rows): rows [a, b) of A (CSR, global
     columns) and the CSC of that block; x split by columns in slices of cs

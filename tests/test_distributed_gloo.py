@@ -32,14 +32,15 @@ def _worker(rank, world, port, out_dir, single):
     sys.path.insert(0, os.path.join(HERE, ".."))
     import torch.distributed as dist
 
-    from dist_cpu_backend import CpuShard, CpuShardGeneral, CpuShardRc, CpuShardSingle
+    from dist_cpu_backend import CpuShard, CpuShardGeneral, CpuShardRc, CpuShardRc2, CpuShardSingle
     from paper_1503_03520_b200.distributed import fista_distributed
     from pyoracle import Oracle
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     oracle = Oracle()
     inst = oracle.build_instance(**(KW_PERM if single == "general" else KW))
-    cls = {"two": CpuShard, "single": CpuShardSingle, "rc": CpuShardRc, "general": CpuShardGeneral}[single]
+    cls = {"two": CpuShard, "single": CpuShardSingle, "rc": CpuShardRc, "rc2": CpuShardRc2,
+           "general": CpuShardGeneral}[single]
     be = cls(oracle, inst, rank, world, ITERS)
     samples, x_own = fista_distributed(be, ITERS + 5)
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), f=np.array([s[1] for s in samples]),
@@ -49,7 +50,8 @@ def _worker(rank, world, port, out_dir, single):
 
 
 @pytest.mark.parametrize("world,single", [(2, "two"), (3, "two"), (2, "single"), (3, "single"),
-                                          (2, "rc"), (3, "rc"), (2, "general"), (3, "general")])
+                                          (2, "rc"), (3, "rc"), (2, "rc2"), (3, "rc2"), (4, "rc2"),
+                                          (2, "general"), (3, "general")])
 def test_sharded_fista_matches_single_process(tmp_path, oracle, world, single):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), single), nprocs=world, join=True)
     inst = oracle.build_instance(**(KW_PERM if single == "general" else KW))
