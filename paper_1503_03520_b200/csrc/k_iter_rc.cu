@@ -12,9 +12,9 @@
 //   * a warp holds a window of 128 consecutive entries, 4 per lane (one
 //     256-bit load per array and lane, a warp load = 1 KiB contiguous);
 //   * a stage whose pairs start on even entries is lane-local; an odd stage
-//     rotates (v1, v2) in the lane and the pairs straddling lanes through one
-//     shuffle each way -- every rotation is done exactly once, no redundant
-//     cone work;
+//     rotates (v1, v2) in the lane, and the pair straddling lanes l, l+1 is
+//     rotated by lane l (neighbour's entry in by one shuffle, the right output
+//     back by another) -- every rotation is done exactly once;
 //   * per iteration the chain runs three times (r_k and r_{k-1} side by side,
 //     then g = G u); each of the two runs in series invalidates S entries at
 //     both window ends, so the window carries a halo of H3 >= 2S entries per
@@ -41,6 +41,10 @@
 //                        default, V = 8: 24n bytes per iteration)
 //   fista_rc_persistent  up to a chunk of iterations in one cooperative
 //                        launch (small instances, n <= 2^20)
+//   fista_pair_cluster / fista_pair_small
+//                        single-stage instances (n <= 16384 / 4096): pair-local
+//                        products, state in registers, an 8-CTA cluster or one
+//                        CTA for the whole chunk
 #include "common.cuh"
 #include "fista.cuh"
 #include "kernels.hpp"
@@ -166,29 +170,29 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
         if (p2) rotate_pair(v[q][2], v[q][3], c, sn, TR);
       }
     } else {
-      double right[K], left[K];
+      // the pair straddling lanes l, l+1 is rotated once, by lane l, which
+      // hands the right output back through a second shuffle
+      double right[K], back[K];
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
-        right[q] = __shfl_down_sync(kFull, v[q][0], 1);  // lane+1's first entry
-        left[q] = __shfl_up_sync(kFull, v[q][3], 1);     // lane-1's last entry
-      }
+      for (int q = 0; q < K; ++q) right[q] = __shfl_down_sync(kFull, v[q][0], 1);  // lane+1's first entry
       const bool p1 = INTERIOR || (e0 + 1 >= o && e0 + 2 < n);
       const bool p3 = INTERIOR || (e0 + 3 >= o && e0 + 4 < n);
       const bool pm = INTERIOR || (e0 - 1 >= o && e0 < n);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
-        if (p1) rotate_pair(v[q][1], v[q][2], c, sn, TR);
-        if (p3) {
-          double a = v[q][3], b = right[q];
-          rotate_pair(a, b, c, sn, TR);
-          v[q][3] = a;
-        }
-        if (pm) {
-          double a = left[q], b = v[q][0];
-          rotate_pair(a, b, c, sn, TR);
-          v[q][0] = b;
-        }
+        double a = v[q][3], b = right[q];
+        if (p3) rotate_pair(a, b, c, sn, TR);
+        v[q][3] = a;
+        back[q] = b;
       }
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        const double b = __shfl_up_sync(kFull, back[q], 1);  // lane-1's right output
+        if (pm) v[q][0] = b;
+      }
+#pragma unroll
+      for (int q = 0; q < K; ++q)
+        if (p1) rotate_pair(v[q][1], v[q][2], c, sn, TR);
     }
   }
 }
