@@ -74,8 +74,6 @@ void seed_window(uint64_t seed, uint64_t* w) {
 // host: characteristic polynomial and t^(2^e) mod P
 using Poly = std::vector<uint64_t>;  // bit i = coefficient of t^i
 
-inline int getbit(const Poly& a, uint64_t i) { return (int)((a[i >> 6] >> (i & 63)) & 1ull); }
-
 // Berlekamp-Massey over GF(2) on s_k = bit 0 of draw k (any nonzero linear
 // functional of the state has minimal polynomial P: P is primitive).
 Poly compute_charpoly() {
