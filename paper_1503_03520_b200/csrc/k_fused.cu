@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) fista_iter_kernel(IterAr
       issue(k + kIStages - 1);
     }
     const int64_t t0 = tile0(k), te = min(t0 + TT, (int64_t)A.hi);
-    const int64_t gr = t0 - 2 * H, gx = t0 - H;  // global index of smem entry 0
+    const int64_t gx = t0 - H;  // global index of x smem entry 0 (r windows start at t0 - 2H)
     unsigned char* slot = smem + (k % kIStages) * L::slot_bytes;
     double* s_r = reinterpret_cast<double*>(slot);  // r_k -> sigma .* r_y
     const double* s_rm = reinterpret_cast<const double*>(slot + L::off_rkm1);

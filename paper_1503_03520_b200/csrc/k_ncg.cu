@@ -282,26 +282,27 @@ __device__ __forceinline__ void fold_partials(const double* partials, double (&t
 template <int K, typename PtrT, class F>
 __device__ __forceinline__ double line_sum(PtrT q0, PtrT q1, const uint32_t* __restrict__ idx,
                                            const double* __restrict__ val, F f) {
-  if (K == 0) {
+  if constexpr (K == 0) {
     double sum = 0.0;
     for (PtrT q = q0; q < q1; ++q) sum += val[q] * f(idx[q]);
     return sum;
+  } else {
+    uint32_t c[K];
+    double v[K], g[K];
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const bool in = q0 + e < q1;
+      c[e] = in ? idx[q0 + e] : 0u;
+      v[e] = in ? val[q0 + e] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < K; ++e) g[e] = q0 + e < q1 ? f(c[e]) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int e = 0; e < K; ++e)
+      if (q0 + e < q1) sum += v[e] * g[e];
+    return sum;
   }
-  uint32_t c[K > 0 ? K : 1];
-  double v[K > 0 ? K : 1], g[K > 0 ? K : 1];
-#pragma unroll
-  for (int e = 0; e < K; ++e) {
-    const bool in = q0 + e < q1;
-    c[e] = in ? idx[q0 + e] : 0u;
-    v[e] = in ? val[q0 + e] : 0.0;
-  }
-#pragma unroll
-  for (int e = 0; e < K; ++e) g[e] = q0 + e < q1 ? f(c[e]) : 0.0;
-  double sum = 0.0;
-#pragma unroll
-  for (int e = 0; e < K; ++e)
-    if (q0 + e < q1) sum += v[e] * g[e];
-  return sum;
 }
 
 template <typename PtrT, int K = 0>
