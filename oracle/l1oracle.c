@@ -53,6 +53,17 @@ uint64_t lo_mix_seed(uint64_t seed, uint64_t salt) {
 /* rng.hpp:27-29 */
 double lo_uniform_unit(lo_rng* r) { return (double)(lo_rng_next(r) >> 11) * 0x1.0p-53; }
 
+/* rng.hpp:48-56: Box-Muller, u1 in (0, 1) */
+double lo_normal(lo_rng* r) {
+  double u1;
+  do {
+    u1 = lo_uniform_unit(r);
+  } while (u1 <= 0.0);
+  const double u2 = lo_uniform_unit(r);
+  const double two_pi = 6.283185307179586476925286766559;
+  return sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+}
+
 /* rng.hpp:32-34 */
 double lo_uniform_in(lo_rng* r, double lo, double hi) { return lo + (hi - lo) * lo_uniform_unit(r); }
 
@@ -601,13 +612,55 @@ static lo_summary tk_finish(tracker* tk, int status, double mv) {
 /* ------------------------------------------------------------------------ */
 /* FISTA / ISTA with the spectrum (or fixed) L (solvers.cpp:277-382)         */
 
+/* linops.cpp:757-778 */
+double lo_estimate_gram_lmax(const lo_op* A, uint64_t iters, uint64_t seed) {
+  const uint64_t n = A->n, m = A->m;
+  lo_rng rng;
+  lo_rng_seed(&rng, seed);
+  double* v = (double*)malloc(n * sizeof(double));
+  double* w = (double*)malloc(n * sizeof(double));
+  double* av = (double*)malloc(m * sizeof(double));
+  for (uint64_t i = 0; i < n; ++i) v[i] = lo_normal(&rng);
+  double lambda = 0.0;
+  for (uint64_t it = 0; it < iters; ++it) {
+    double norm = 0.0;
+    for (uint64_t i = 0; i < n; ++i) norm += v[i] * v[i];
+    norm = sqrt(norm);
+    if (norm == 0.0) break;
+    for (uint64_t i = 0; i < n; ++i) v[i] /= norm;
+    lo_apply(A, v, av);
+    lo_apply_transpose(A, av, w);
+    lambda = 0.0;
+    for (uint64_t i = 0; i < n; ++i) lambda += v[i] * w[i];
+    double* t = v;
+    v = w;
+    w = t;
+  }
+  free(v);
+  free(w);
+  free(av);
+  return lambda;
+}
+
 lo_summary lo_fista(const lo_op* A, double tau, const double* b, const lo_cfg* cfg,
                     lo_sample* samples, uint64_t cap, double* x_out) {
   const uint64_t n = A->n, m = A->m;
   tracker tk;
   tk_init(&tk, cfg, samples, cap);
   double mv = 0.0;
-  const double lval = cfg->l_fixed > 0.0 ? cfg->l_fixed : lo_gram_lmax(A);
+  /* LipschitzState (solvers.cpp:99-120) */
+  double lval;
+  int bt_on = 0;
+  if (cfg->l_fixed > 0.0) {
+    lval = cfg->l_fixed;
+  } else if (!cfg->backtracking) {
+    lval = lo_gram_lmax(A);
+  } else {
+    bt_on = 1;
+    const double est = lo_estimate_gram_lmax(A, 30, lo_mix_seed(cfg->seed, 0x4c6d6178ULL));
+    lval = est > 0.0 ? est : 1.0;
+  }
+  const double lcap = lval * 0x1p60;
   double* x = (double*)calloc(n, sizeof(double));
   double* y = (double*)calloc(n, sizeof(double));
   double* grad = (double*)malloc(n * sizeof(double));
@@ -633,11 +686,28 @@ lo_summary lo_fista(const lo_op* A, double tau, const double* b, const lo_cfg* c
     const double* r_base = acc ? r_y : r_x;
     lo_apply_transpose(A, r_base, grad);
     mv += 1;
-    const double inv_l = 1.0 / lval;
-    for (uint64_t i = 0; i < n; ++i) trial[i] = lo_soft_threshold(base[i] - inv_l * grad[i], tau * inv_l);
-    lo_apply(A, trial, r_trial);
-    mv += 1;
-    for (uint64_t i = 0; i < m; ++i) r_trial[i] -= b[i];
+    const double g_base = 0.5 * dot(r_base, r_base, m);
+    if (bt_on) lval = fmax(lval * 0.5, 1e-12);
+    uint64_t backtracks = 0;
+    for (;;) { /* solvers.cpp:325-343 */
+      const double inv_l = 1.0 / lval;
+      for (uint64_t i = 0; i < n; ++i) trial[i] = lo_soft_threshold(base[i] - inv_l * grad[i], tau * inv_l);
+      lo_apply(A, trial, r_trial);
+      mv += 1;
+      for (uint64_t i = 0; i < m; ++i) r_trial[i] -= b[i];
+      if (!bt_on) break;
+      const double lhs = 0.5 * dot(r_trial, r_trial, m);
+      double quad = g_base, step_sq = 0.0;
+      for (uint64_t i = 0; i < n; ++i) {
+        const double d = trial[i] - base[i];
+        quad += grad[i] * d;
+        step_sq += d * d;
+      }
+      quad += 0.5 * lval * step_sq;
+      if (lhs <= quad + 1e-12 * (fabs(lhs) + fabs(quad)) || lval >= lcap) break;
+      lval *= 2.0;
+      ++backtracks;
+    }
     int fixed_point = 1;
     for (uint64_t i = 0; i < n; ++i)
       if (trial[i] != base[i]) { fixed_point = 0; break; }
@@ -656,7 +726,7 @@ lo_summary lo_fista(const lo_op* A, double tau, const double* b, const lo_cfg* c
     f = tau * norm1(x, n) + 0.5 * dot(r_x, r_x, m);
     if (!isfinite(f)) { status = -1; break; }
     if (k <= 1000 || k % 10 == 0 || fixed_point) {
-      tk_sample(&tk, k, f, count_nnz(x, n), mv, 0);
+      tk_sample(&tk, k, f, count_nnz(x, n), mv, backtracks);
       last_sampled = k;
     }
     if (fixed_point) { status = 0; break; }

@@ -139,9 +139,14 @@ typedef struct {
   uint64_t seed;
   uint64_t block;      /* block PCDM block size */
   int accelerated;     /* fista (1) / ista (0) */
+  int backtracking;    /* LPolicy::backtracking (solvers.hpp:15, 31) */
 } lo_cfg;
 
-/* FISTA/ISTA with spectrum L (solvers.cpp:277-382). x_out[n] may be NULL. */
+/* estimate_gram_lmax (linops.cpp:757-778): power iteration from normal() draws */
+double lo_estimate_gram_lmax(const lo_op* A, uint64_t iters, uint64_t seed);
+double lo_normal(lo_rng* r); /* rng.hpp:48-56 */
+/* FISTA/ISTA (solvers.cpp:277-382) with LipschitzState (:99-120): spectrum L,
+ * l_fixed, or backtracking seeded by the power iteration. x_out[n] may be NULL. */
 lo_summary lo_fista(const lo_op* A, double tau, const double* b, const lo_cfg* cfg,
                     lo_sample* samples, uint64_t cap, double* x_out);
 /* Serial randomized CD (solvers.cpp:414-482); columns from a CSC.       */

@@ -66,6 +66,7 @@ class LoCfg(C.Structure):
         ("mu", f64), ("eta", f64), ("grad_tol_rel", f64),
         ("pcg_max_iters", u64), ("ls_max_backtracks", u64), ("l_fixed", f64),
         ("varpi", u64), ("omega", u64), ("seed", u64), ("block", u64), ("accelerated", C.c_int),
+        ("backtracking", C.c_int),
     ]
 
 
@@ -343,10 +344,10 @@ class Oracle:
     @staticmethod
     def cfg(max_iters=100000, target=None, mu=1e-5, eta=0.1, grad_tol_rel=1e-8,
             pcg_max_iters=1000, ls_max_backtracks=50, l_fixed=0.0, varpi=1, omega=0, seed=0,
-            block=256, accelerated=True) -> LoCfg:
+            block=256, accelerated=True, backtracking=False) -> LoCfg:
         return LoCfg(max_iters, 0 if target is None else 1, 0.0 if target is None else target,
                      mu, eta, grad_tol_rel, pcg_max_iters, ls_max_backtracks, l_fixed, varpi, omega,
-                     seed, block, 1 if accelerated else 0)
+                     seed, block, 1 if accelerated else 0, 1 if backtracking else 0)
 
     def _run(self, fn, inst: Instance, cfg: LoCfg, extra_args=(), cap=200000):
         st = inst.op.c_struct()
@@ -422,7 +423,8 @@ class RefCfg(C.Structure):
     _fields_ = [("id", C.c_char_p), ("max_iters", u64), ("max_seconds", f64),
                 ("has_target", C.c_int), ("target", f64), ("mu", f64), ("eta", f64),
                 ("grad_tol_rel", f64), ("pcg_max_iters", u64), ("ls_max_backtracks", u64),
-                ("l_fixed", f64), ("varpi", u64), ("omega", u64), ("seed", u64)]
+                ("l_fixed", f64), ("varpi", u64), ("omega", u64), ("seed", u64),
+                ("backtracking", C.c_int)]
 
 
 class Reference:
@@ -645,10 +647,10 @@ class RefInstance:
 
     def solve(self, solver="fista", max_iters=100000, max_seconds=1e9, target=None, mu=1e-5,
               eta=0.1, grad_tol_rel=1e-8, pcg_max_iters=1000, ls_max_backtracks=50, l_fixed=0.0,
-              varpi=1, omega=0, seed=0, cap=200000):
+              varpi=1, omega=0, seed=0, cap=200000, backtracking=False):
         cfg = RefCfg(solver.encode(), max_iters, max_seconds, 0 if target is None else 1,
                      0.0 if target is None else target, mu, eta, grad_tol_rel, pcg_max_iters,
-                     ls_max_backtracks, l_fixed, varpi, omega, seed)
+                     ls_max_backtracks, l_fixed, varpi, omega, seed, 1 if backtracking else 0)
         samples = (RefSample * cap)()
         ns = u64()
         summ = RefSummary()

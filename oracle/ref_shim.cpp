@@ -83,6 +83,7 @@ typedef struct {
   uint64_t varpi;
   uint64_t omega;  // 0: unset
   uint64_t seed;
+  int backtracking;  // LPolicy::backtracking
 } ref_cfg;
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -340,6 +341,7 @@ int ref_solve(void* h, const ref_cfg* c, ref_sample* samples, uint64_t cap, uint
     cfg.varpi = c->varpi;
     if (c->omega) cfg.omega = c->omega;
     cfg.seed = c->seed;
+    if (c->backtracking) cfg.l_policy = LPolicy::backtracking;
     std::vector<double> x;
     SolverTrace tr = run_solver(inst, cfg, &x);
     const std::size_t k = std::min<std::size_t>(cap, tr.samples.size());

@@ -186,3 +186,24 @@ def test_oracle_matches_live_reference(oracle, reference):
     rtr, rx = ri.solve("fista", max_iters=200)
     np.testing.assert_array_equal(tr["objective"], rtr["objective"])
     np.testing.assert_array_equal(x, rx)
+
+
+@pytest.mark.parametrize("kw,solver", [
+    (dict(n=512, stages=2, q=1, s_divisor=20, seed=4), "fista"),
+    (dict(n=1000, stages=1, q=2, s_divisor=50, seed=7), "ista"),
+    (dict(n=300, stages=3, left_stages=1, permute=True, q=1, s_divisor=10, seed=9), "fista"),
+])
+def test_oracle_backtracking_matches_reference(oracle, reference, kw, solver):
+    """LPolicy::backtracking (solvers.cpp:99-120, 325-343): power-iteration seed
+    (estimate_gram_lmax, linops.cpp:757-778, normal() draws), halving per
+    iteration, doubling until the quadratic bound holds -- bit for bit."""
+    import math
+
+    kw = dict(kw, theta=2 * math.pi / 10)
+    oi, ri = oracle.build_instance(**kw), reference.build_instance(**kw)
+    otr, ox = oracle.fista(oi, max_iters=200, backtracking=True, accelerated=solver == "fista", seed=11)
+    rtr, rx = ri.solve(solver, max_iters=200, backtracking=True, seed=11)
+    np.testing.assert_array_equal(ox, rx)
+    for key in ("objective", "extra", "matvecs", "iter"):
+        np.testing.assert_array_equal(otr[key], rtr[key])
+    assert otr["extra"].sum() > 0  # backtracks happened
