@@ -234,9 +234,13 @@ typedef struct {
   uint64_t seed;
   uint64_t block;      /* pcdm: coordinates per block */
   int op;              /* FISTA/ISTA operator: L1B_OP_AUTO (matrix-free when banded), _SPARSE, _MATRIX_FREE */
+  int l_policy;        /* LPolicy (solvers.hpp:15): L1B_L_SPECTRUM, or L1B_L_BACKTRACKING (FISTA / ISTA,
+                          unless l_fixed is set: power-iteration seed, halving / doubling; host-led,
+                          l1b_solve only) */
 } l1b_solver_cfg;
 
 enum { L1B_OP_AUTO = 0, L1B_OP_SPARSE = 1, L1B_OP_MATRIX_FREE = 2 };
+enum { L1B_L_SPECTRUM = 0, L1B_L_BACKTRACKING = 1 };
 
 void l1b_solver_cfg_default(l1b_solver_cfg* cfg);
 

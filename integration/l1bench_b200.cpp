@@ -80,8 +80,7 @@ SolverTrace run_solver(const ProblemInstance& inst, const SolverConfig& cfg,
   else if (cfg.id == "cd") c.solver = L1B_CD;
   else if (cfg.id == "newton_cg") c.solver = L1B_NEWTON_CG;
   else throw std::invalid_argument("run_solver: unknown solver id '" + cfg.id + "'");
-  if (cfg.l_policy == LPolicy::backtracking && !cfg.l_fixed)
-    throw std::invalid_argument("b200: LPolicy::backtracking is not supported");
+  c.l_policy = cfg.l_policy == LPolicy::backtracking ? L1B_L_BACKTRACKING : L1B_L_SPECTRUM;
   c.max_iters = cfg.max_iters;
   c.max_seconds = cfg.max_seconds;
   c.has_target = cfg.target_objective.has_value();
@@ -160,12 +159,16 @@ extern "C" int b200_dropin_compare(const char* solver, uint64_t n, uint32_t stag
     cfg.s_divisor = 100;
     cfg.seed = seed;
     SolverConfig sc;
-    sc.id = solver;
+    std::string id = solver;  // "<solver>_bt": the backtracking Lipschitz policy
+    const bool bt = id.size() > 3 && id.compare(id.size() - 3, 3, "_bt") == 0;
+    if (bt) id.resize(id.size() - 3);
+    sc.id = id;
+    if (bt) sc.l_policy = LPolicy::backtracking;
     sc.max_iters = iters;
     sc.varpi = 4;
     sc.seed = 5;
     cfg.solvers = {sc};
-    cfg.reference = solver;
+    cfg.reference = id;
     const ProblemInstance inst = build_instance(cfg, enumerate_jobs(cfg).at(0));
     std::vector<double> xr, xb;
     const SolverTrace tr = l1bench::run_solver(inst, sc, &xr);

@@ -26,6 +26,8 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
               l1b_summary* summary, double* x_host, double* d_x);
 void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
                   l1b_summary* summary, double* x_host, double* d_x);
+void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
+                            l1b_summary* summary, double* x_host, double* d_x);
 }  // namespace l1b
 
 struct l1b_session {
@@ -472,6 +474,8 @@ void validate_cfg(const l1b_solver_cfg* c, uint64_t n) {  // SolverConfig::valid
     throw InvalidArgument("SolverConfig: omega must lie in [1, n]");
   if (c->l_fixed < 0.0 || std::isnan(c->l_fixed))
     throw InvalidArgument("SolverConfig: fixed L must be positive");
+  if (c->l_policy != L1B_L_SPECTRUM && c->l_policy != L1B_L_BACKTRACKING)
+    throw InvalidArgument("SolverConfig: unknown Lipschitz policy");
   if (!(c->max_seconds > 0.0)) throw InvalidArgument("SolverConfig: max_seconds must be positive");
 }
 
@@ -487,6 +491,8 @@ int l1b_session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session** o
     validate_cfg(cfg, v.n);
     if (cfg->solver != L1B_FISTA && cfg->solver != L1B_ISTA)
       throw InvalidArgument("sessions drive FISTA / ISTA only");
+    if (cfg->l_policy == L1B_L_BACKTRACKING && !(cfg->l_fixed > 0.0))
+      throw Unsupported("sessions run a constant L (spectrum or l_fixed); LPolicy::backtracking runs in l1b_solve");
     L1B_CUDA(cudaSetDevice(v.device));
     auto* s = new l1b_session();
     try {
@@ -789,6 +795,10 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     }
     if (cfg->solver == L1B_NEWTON_CG) {
       run_newton_cg(p, cfg, samples, cap, summary, x_host, d_x);
+      return;
+    }
+    if (cfg->l_policy == L1B_L_BACKTRACKING && !(cfg->l_fixed > 0.0)) {  // LipschitzState (:103-119)
+      run_fista_backtracking(p, cfg, samples, cap, summary, x_host, d_x);
       return;
     }
     // host-side setup before session_begin: the device clock of the trace

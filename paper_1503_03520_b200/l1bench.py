@@ -113,8 +113,6 @@ class SolverConfig:  # solvers.hpp:17-41
     def to_c(self) -> N.SolverCfg:
         if self.id not in self._IDS:
             raise ValueError(f"SolverConfig: unknown solver id '{self.id}'")
-        if self.l_policy == LPolicy.backtracking and self.l_fixed is None:
-            raise N.L1bUnsupported("LPolicy::backtracking is not built on device; use the spectrum policy")
         c = N.SolverCfg()
         _lib().l1b_solver_cfg_default(C.byref(c))
         c.solver = self._IDS[self.id]
@@ -132,6 +130,7 @@ class SolverConfig:  # solvers.hpp:17-41
         c.omega = 0 if self.omega is None else int(self.omega)
         c.seed = int(self.seed)
         c.block = int(self.block)
+        c.l_policy = int(LPolicy(self.l_policy))
         ops = {"auto": N.OP_AUTO, "sparse": N.OP_SPARSE, "matrix_free": N.OP_MATRIX_FREE}
         if self.op not in ops:
             raise ValueError(f"SolverConfig: unknown operator path '{self.op}'")

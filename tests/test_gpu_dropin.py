@@ -17,6 +17,7 @@ SO = os.path.join(ROOT, "integration", "_build", "libl1bench_b200_dropin.so")
 
 
 @pytest.mark.parametrize("solver,iters,tol", [("fista", 200, 1e-10), ("ista", 100, 1e-10),
+                                              ("fista_bt", 150, 1e-10), ("ista_bt", 100, 1e-10),
                                               ("cd", 10, 1e-10), ("newton_cg", 2, 1e-9)])
 def test_dropin_matches_reference(solver, iters, tol):
     need_cuda()

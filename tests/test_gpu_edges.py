@@ -90,8 +90,8 @@ def test_bad_arguments():
         l1bench.build_instance(n=64, tau=0.0)
     with pytest.raises(ValueError):
         l1bench.build_instance(n=64, m_ratio=0.5)
-    with pytest.raises(N.L1bUnsupported):
-        l1bench.fista_run(inst, l1bench.SolverConfig(l_policy=l1bench.LPolicy.backtracking))
+    with pytest.raises(N.L1bUnsupported):  # sessions keep L constant
+        l1bench.Session(inst, l1bench.SolverConfig(l_policy=l1bench.LPolicy.backtracking))
     with pytest.raises(ValueError):  # bad spectrum in from_host (Spectrum::validate)
         l1bench.ProblemInstance.from_host(4, 2, [(0, 0.3)], [1.0, 2.0], np.zeros(4), -1.0)
     with pytest.raises(RuntimeError):
