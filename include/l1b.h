@@ -195,6 +195,9 @@ int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y);
 int l1b_apply_transpose(l1b_problem* p, int path, const double* d_y, double* d_x);
 int l1b_gram_inverse(l1b_problem* p, const double* d_v, double* d_out);
 int l1b_gram_diagonal(l1b_problem* p, double* d_out);
+/* estimate_gram_lmax (linops.hpp:283, linops.cpp:757-778): power iteration
+ * from normal() draws of Rng(seed), products by the matrix-free sweeps */
+int l1b_estimate_gram_lmax(l1b_problem* p, uint64_t iters, uint64_t seed, double* out);
 /* host buffers: row_ptr[m+1] (rows >= m_active are empty), col[nnz], val[nnz] */
 int l1b_export_csr(const l1b_problem* p, uint64_t* row_ptr, uint32_t* col, double* val);
 int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, double* val);

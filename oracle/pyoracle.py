@@ -167,6 +167,8 @@ class Oracle:
             getattr(L, fn).argtypes = [P(LoOp), P(f64), P(f64)]
         L.lo_gram_diagonal.argtypes = [P(LoOp), P(f64)]
         L.lo_gram_lmax.argtypes = [P(LoOp)]
+        L.lo_estimate_gram_lmax.argtypes = [P(LoOp), u64, u64]
+        L.lo_estimate_gram_lmax.restype = f64
         L.lo_gram_lmax.restype = f64
         L.lo_permutation_realize.argtypes = [u64, u64, P(u32), P(u32)]
         L.lo_spectrum_uniform.argtypes = [u64, f64, f64, f64, u64, P(f64)]

@@ -123,6 +123,7 @@ SIGNATURES = [
     ("l1b_apply_transpose", C.c_int, [vp, C.c_int, vp, vp]),
     ("l1b_gram_inverse", C.c_int, [vp, vp, vp]),
     ("l1b_gram_diagonal", C.c_int, [vp, vp]),
+    ("l1b_estimate_gram_lmax", C.c_int, [vp, u64, u64, P(f64)]),
     ("l1b_export_csr", C.c_int, [vp, P(u64), P(u32), P(f64)]),
     ("l1b_export_csc", C.c_int, [vp, P(u64), P(u32), P(f64)]),
     ("l1b_objective", C.c_int, [vp, vp, P(f64)]),

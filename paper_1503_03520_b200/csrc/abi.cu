@@ -1080,6 +1080,15 @@ const double* gram_diag_device(l1b_problem* p) {
 }
 }  // namespace
 
+int l1b_estimate_gram_lmax(l1b_problem* p, uint64_t iters, uint64_t seed, double* out) {
+  return guard([&] {
+    check_whole(p);
+    if (!out) throw InvalidArgument("null output");
+    L1B_CUDA(cudaSetDevice(p->device));
+    *out = estimate_gram_lmax_device(p->view, p->m, p->n, iters, seed, p->stream);
+  });
+}
+
 int l1b_gram_diagonal(l1b_problem* p, double* d_out) {
   return guard([&] {
     check_whole(p);

@@ -114,6 +114,48 @@ struct BtScratch {
 
 }  // namespace
 
+// estimate_gram_lmax (linops.cpp:757-778): v from normal() draws of Rng(seed)
+// (host, same libm), then `iters` rounds of v /= ||v||; w = A^T A v;
+// lambda = v.w; v <-> w, with the reference's matrix-free products
+double estimate_gram_lmax_device(const OpView& op, uint64_t m, uint64_t n, uint64_t iters, uint64_t seed,
+                                 cudaStream_t st) {
+  std::mt19937_64 rng(seed);
+  std::vector<double> hv(n);
+  for (auto& q : hv) q = normal_draw(rng);
+  double *v = nullptr, *w = nullptr, *av = nullptr, *scratch = nullptr;
+  unsigned int* ticket = nullptr;
+  const int grid = grid_for(n);
+  L1B_CUDA(cudaMallocAsync(&v, n * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&w, n * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&av, m * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&scratch, (grid + 1) * sizeof(double), st));
+  L1B_CUDA(cudaMallocAsync(&ticket, sizeof(unsigned int), st));
+  L1B_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned int), st));
+  L1B_CUDA(cudaMemcpyAsync(v, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  auto dot = [&](const double* a, const double* b) {
+    bt_dot_kernel<<<grid, kThreads, 0, st>>>(a, b, n, scratch + 1, ticket, scratch);
+    L1B_LAUNCHED();
+    double h = 0.0;
+    L1B_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
+    L1B_CUDA(cudaStreamSynchronize(st));
+    return h;
+  };
+  double lambda = 0.0;
+  for (uint64_t it = 0; it < iters; ++it) {
+    const double norm = std::sqrt(dot(v, v));
+    if (norm == 0.0) break;
+    bt_div_kernel<<<grid, kThreads, 0, st>>>(v, n, norm);
+    L1B_LAUNCHED();
+    sweep_apply(op, v, av, st);
+    sweep_apply_transpose(op, av, w, st);
+    lambda = dot(v, w);
+    std::swap(v, w);
+  }
+  for (void* q : {(void*)v, (void*)w, (void*)av, (void*)scratch, (void*)ticket}) L1B_CUDA(cudaFreeAsync(q, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  return lambda;
+}
+
 void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
                             l1b_summary* sum, double* x_host, double* d_x) {
   const ProblemView v = problem_view(p, false);
@@ -130,13 +172,12 @@ void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sampl
   };
   BtScratch S;
   S.grid = grid_for(std::max(n, m));
-  double *x, *y, *grad, *trial, *r_x, *r_y, *r_trial, *w;
+  double *x, *y, *grad, *trial, *r_x, *r_y, *r_trial;
   try {
     alloc(&x, n);
     alloc(&y, n);
     alloc(&grad, n);
     alloc(&trial, n);
-    alloc(&w, n);
     alloc(&r_x, m);
     alloc(&r_y, m);
     alloc(&r_trial, m);
@@ -166,23 +207,8 @@ void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sampl
       lval = cfg->l_fixed;
     } else {
       bt = true;
-      std::mt19937_64 rng(l1b_mix_seed(cfg->seed, 0x4c6d6178ULL));
-      std::vector<double> hv(n);
-      for (auto& q : hv) q = normal_draw(rng);
-      double* vv = grad;  // scratch: v and w of estimate_gram_lmax
-      L1B_CUDA(cudaMemcpyAsync(vv, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
-      double lambda = 0.0;
-      for (int it = 0; it < 30; ++it) {
-        const double norm = std::sqrt(dot(vv, vv, n));
-        if (norm == 0.0) break;
-        bt_div_kernel<<<grid_for(n), kThreads, 0, st>>>(vv, n, norm);
-        L1B_LAUNCHED();
-        sweep_apply(op, vv, r_trial, st);
-        sweep_apply_transpose(op, r_trial, w, st);
-        lambda = dot(vv, w, n);
-        std::swap(vv, w);
-      }
-      lval = lambda > 0.0 ? lambda : 1.0;
+      const double est = estimate_gram_lmax_device(op, v.m, v.n, 30, l1b_mix_seed(cfg->seed, 0x4c6d6178ULL), st);
+      lval = est > 0.0 ? est : 1.0;
     }
     const double lcap = lval * 0x1p60;
 

@@ -44,6 +44,11 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 // std::mt19937_64(seed) through the jump polynomial (log2_jump < 0: no jump)
 void host_draws_after_jump(uint64_t seed, int log2_jump, uint64_t count, uint64_t* out);
 
+// ---- k_bt.cu ----------------------------------------------------------------
+// estimate_gram_lmax (linops.cpp:757-778) with the matrix-free products (syncs)
+double estimate_gram_lmax_device(const OpView& op, uint64_t m, uint64_t n, uint64_t iters, uint64_t seed,
+                                 cudaStream_t st);
+
 // ---- k_sweep.cu (matrix-free, bit-exact vs linops.cpp) ---------------------
 void sweep_apply(const OpView& op, const double* x, double* y, cudaStream_t st);
 void sweep_apply_transpose(const OpView& op, const double* y, double* x, cudaStream_t st);

@@ -280,6 +280,12 @@ class DeviceOperator:
     def gram_lmax(self) -> float:
         return self._inst.info.gram_lmax
 
+    def estimate_gram_lmax(self, iters: int = 30, seed: int = 0) -> float:
+        """estimate_gram_lmax(op, iters, seed) (linops.hpp:283): power iteration."""
+        out = C.c_double()
+        N.check(_lib().l1b_estimate_gram_lmax(self._inst._h, int(iters), int(seed), C.byref(out)))
+        return float(out.value)
+
     def csr(self):
         """Rows of A exactly as OperatorSpec::row (linops.cpp:597-619)."""
         info = self._inst.materialize()

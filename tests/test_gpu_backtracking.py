@@ -57,3 +57,24 @@ def test_backtracking_target_and_fixed_L():
     a = l1bench.run_solver(inst, l1bench.SolverConfig(max_iters=50, l_fixed=L, l_policy=l1bench.LPolicy.backtracking))
     b = l1bench.run_solver(inst, l1bench.SolverConfig(max_iters=50, l_fixed=L))
     assert rel_err(a.objectives(), b.objectives()) < 1e-12
+
+
+@pytest.mark.parametrize("kw", [dict(n=700, stages=2, q=1, seed=4),
+                                dict(n=300, stages=3, left_stages=1, permute=True, q=2, seed=9)])
+def test_estimate_gram_lmax_matches_oracle(oracle, kw):
+    """estimate_gram_lmax (linops.cpp:757-778) on the device vs the oracle
+    (same normal() draws, same sweeps; the dot products are grid sums)."""
+    import ctypes as C
+
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(kw, theta=TH, s_divisor=20)
+    inst = l1bench.build_instance(**kw)
+    oi = oracle.build_instance(**kw)
+    st = oi.op.c_struct()
+    for iters, seed in ((30, 11), (5, 2)):
+        want = oracle.lib.lo_estimate_gram_lmax(C.byref(st), iters, seed)
+        got = inst.op.estimate_gram_lmax(iters, seed)
+        assert abs(got - want) <= 1e-12 * abs(want)
+        assert got <= inst.info.gram_lmax * (1 + 1e-12)
