@@ -26,6 +26,9 @@
 #include <random>
 #include <vector>
 
+#include <cooperative_groups.h>
+#include <cub/device/device_scan.cuh>
+
 #include "solvers.hpp"
 #include "kernels.hpp"
 
@@ -428,6 +431,353 @@ void plan_and_run(const ProblemView& v, const uint32_t* coords, uint64_t count, 
   L1B_LAUNCHED();
 }
 
+// ---------------------------------------------------------------------------
+// Pair-local epochs (one right stage, no left stages, identity permutations:
+// C2's operator).  Column i of A = Sigma G^T e_i touches only the rows of
+// i's rotation pair (a, a + 1), a = 2u - offset, and row a / a + 1 only the
+// columns of that pair: a block step of coordinate i reads and writes nothing
+// outside its pair.  An epoch therefore splits into independent per-pair
+// sequences -- for each block in draw order, the block's members of the pair
+// (one or both) take the step of cd_epoch_kernel against the pair's residual
+// rows as they stood at the block's start, then the rows get
+// r + sum_c delta_c A(rho, c) in ascending column order -- and so does the
+// refresh r = A x - b (the one-stage sweep of OperatorSpec::apply on the
+// pair).  One thread keeps its pair's x, r, sigma, b, L and column values in
+// registers for the whole launch; the only grid-wide step per epoch is the
+// objective (one grid barrier).  Identical operations to cd_epoch_kernel:
+// identical iterates.
+//
+// The block draws come from the device (mt_stream_indices) in four steps per
+// chunk of epochs:
+//   cd_prevd_kernel   distance from each stream position back to the
+//                     previous draw of the same coordinate (<= W) -- a draw
+//                     is redrawn iff that previous draw lies in its block;
+//   cd_cand_*         the positions with such a previous draw within W
+//                     (~ W/n of them), compacted in stream order; the host
+//                     walks them to the block starts (s_{b+1} = s_b + B +
+//                     #redrawn in the block: sequential, ~1 candidate per
+//                     block, tens of microseconds per 100 epochs at C2);
+//   cd_scatter_kernel each kept draw -> an event (block << 1 | member) in
+//                     its pair's bucket of the epoch;
+//   cd_pair_kernel    the epochs.
+constexpr uint16_t kPrevRej = 0xffff;
+constexpr int kEvCap = 16;  // events per pair and epoch (Poisson(2B/n * ...) tail: overflow -> direct path)
+
+__global__ void cd_prevd_kernel(const uint32_t* __restrict__ idx, uint64_t L, int W,
+                                uint16_t* __restrict__ prevd) {
+  extern __shared__ uint32_t tile[];  // [W + blockDim.x]
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x;
+  for (int k = threadIdx.x; k < W + (int)blockDim.x; k += blockDim.x) {
+    const int64_t q = (int64_t)t0 - W + k;
+    tile[k] = (q >= 0 && (uint64_t)q < L) ? idx[q] : 0xffffffffu;
+  }
+  __syncthreads();
+  const uint64_t q = t0 + threadIdx.x;
+  if (q >= L) return;
+  const uint32_t v = tile[W + threadIdx.x];
+  uint16_t d = 0;
+  if (v == 0xffffffffu) {
+    d = kPrevRej;
+  } else {
+    const int lim = (int)((uint64_t)W < q ? (uint64_t)W : q);
+    for (int k = 1; k <= lim; ++k)
+      if (tile[W + threadIdx.x - k] == v) {
+        d = (uint16_t)k;
+        break;
+      }
+  }
+  prevd[q] = d;
+}
+
+// Candidates: the positions whose previous draw of the same coordinate lies
+// within W (or that the reference redraws outright), in stream order, packed
+// (q << 16 | distance).  Tiles of kCandTile positions: count, scan, write.
+constexpr int kCandTile = 4096;
+constexpr int kCandPer = kCandTile / kThreads;
+
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t* total) {
+  __shared__ uint64_t warp_tot[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    uint64_t t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;  // inclusive
+  }
+  __syncthreads();
+  const uint64_t before = (w ? warp_tot[w - 1] : 0) + x - v;
+  *total = warp_tot[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(kThreads) cd_cand_count(const uint16_t* __restrict__ prevd, uint64_t L,
+                                                          uint32_t* tile_cnt) {
+  const uint64_t q0 = blockIdx.x * (uint64_t)kCandTile + (uint64_t)threadIdx.x * kCandPer;
+  uint32_t c = 0;
+  for (int k = 0; k < kCandPer; ++k) c += (q0 + k < L && prevd[q0 + k] != 0) ? 1u : 0u;
+  double v[1] = {(double)c};
+  block_sum<1>(v);
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = (uint32_t)v[0];
+}
+
+__global__ void __launch_bounds__(kThreads) cd_cand_write(const uint16_t* __restrict__ prevd, uint64_t L,
+                                                          const uint32_t* __restrict__ tile_off,
+                                                          uint64_t* __restrict__ cand) {
+  const uint64_t q0 = blockIdx.x * (uint64_t)kCandTile + (uint64_t)threadIdx.x * kCandPer;
+  uint32_t c = 0;
+  for (int k = 0; k < kCandPer; ++k) c += (q0 + k < L && prevd[q0 + k] != 0) ? 1u : 0u;
+  uint64_t tot;
+  uint64_t o = tile_off[blockIdx.x] + block_exclusive_scan(c, &tot);
+  for (int k = 0; k < kCandPer; ++k) {
+    const uint64_t q = q0 + k;
+    if (q < L) {
+      const uint16_t d = prevd[q];
+      if (d != 0) cand[o++] = (q << 16) | d;
+    }
+  }
+}
+
+__global__ void cd_scatter_kernel(const uint32_t* __restrict__ idx, const uint16_t* __restrict__ prevd,
+                                  const uint64_t* __restrict__ s, uint64_t nb, uint64_t per_epoch,
+                                  int off, uint64_t U, uint32_t* cnt, uint32_t* ev, int* flag) {
+  const uint64_t end = s[nb];
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < end;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint16_t d = prevd[q];
+    if (d == kPrevRej) continue;
+    uint64_t lo = 0, hi = nb;  // block b: s[b] <= q < s[b + 1]
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (s[mid] <= q) lo = mid;
+      else hi = mid;
+    }
+    if (d != 0 && (uint64_t)d <= q - s[lo]) continue;  // redrawn
+    const uint64_t e = lo / per_epoch, bl = lo % per_epoch;
+    const uint64_t i = idx[q] + (uint64_t)off;
+    const uint64_t u = i >> 1;
+    const uint32_t slot = atomicAdd(&cnt[e * U + u], 1u);
+    if (slot < (uint32_t)kEvCap) ev[(e * kEvCap + slot) * U + u] = (uint32_t)(bl << 1) | (uint32_t)(i & 1);
+    else atomicOr(flag, 4);
+  }
+}
+
+struct CdPairArgs {
+  uint64_t n, m, U;
+  int off, ptr32;
+  double c, s;
+  const double *sigma, *b, *lips;
+  const void* cptr;
+  const uint32_t* crow;
+  const double* cval;
+  double *x, *r;
+  const uint32_t *cnt, *ev;
+  uint64_t epochs;  // of this launch
+  CdDev* st;
+  CdSample* trace;
+  double* partials;  // 2 x grid x 5
+};
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  CdDev* st = A.st;
+  if (*(volatile int*)&st->stop) return;
+  const double beta = st->beta, tau = st->tau;
+  const uint64_t epoch0 = st->epoch, max_epochs = st->max_epochs;
+  const int has_target = st->has_target;
+  const double target = st->target;
+  const int64_t n = (int64_t)A.n;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const double c = A.c, s = A.s;
+  // per pair: members e = 0, 1 (coordinates a + e), column entries (row member, value)
+  double x[P][2], r[P][2], sig[P][2], bb[P][2], li[P][2], cv[P][2][2];
+  int cr[P][2][2], nc[P][2];
+  bool va[P][2];
+  int64_t a[P];
+  bool live[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const uint64_t u = g0 + (uint64_t)k * T;
+    live[k] = u < A.U;
+    a[k] = 2 * (int64_t)u - A.off;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t i = a[k] + e;
+      va[k][e] = live[k] && i >= 0 && i < n;
+      x[k][e] = va[k][e] ? A.x[i] : 0.0;
+      r[k][e] = va[k][e] ? A.r[i] : 0.0;
+      sig[k][e] = va[k][e] ? A.sigma[i] : 0.0;
+      bb[k][e] = va[k][e] ? A.b[i] : 0.0;
+      li[k][e] = va[k][e] ? A.lips[i] : 0.0;
+      nc[k][e] = 0;
+      cr[k][e][0] = cr[k][e][1] = 0;
+      cv[k][e][0] = cv[k][e][1] = 0.0;
+      if (va[k][e]) {
+        const uint64_t p0 = A.ptr32 ? ((const uint32_t*)A.cptr)[i] : ((const uint64_t*)A.cptr)[i];
+        const uint64_t p1 = A.ptr32 ? ((const uint32_t*)A.cptr)[i + 1] : ((const uint64_t*)A.cptr)[i + 1];
+        int q = 0;
+        for (uint64_t p = p0; p < p1 && q < 2; ++p, ++q) {
+          cr[k][e][q] = (int)((int64_t)A.crow[p] - a[k]);  // 0 or 1
+          cv[k][e][q] = A.cval[p];
+        }
+        nc[k][e] = q;
+      }
+    }
+  }
+  // rows [n, m) stay 0 - b (empty rows): their ||r||^2 share, once
+  double tail = 0.0;
+  for (uint64_t i = (uint64_t)n + g0; i < A.m; i += T) tail += A.r[i] * A.r[i];
+  uint64_t e_done = 0;
+  for (uint64_t ep = 0; ep < A.epochs; ++ep) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // ||x||_1, nnz, ||r||^2, applied, colops
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      if (!live[k]) continue;
+      const uint64_t u = g0 + (uint64_t)k * T;
+      const int cnt = min((int)A.cnt[ep * A.U + u], kEvCap);
+      uint32_t key[kEvCap];
+      for (int j = 0; j < cnt; ++j) {
+        const uint32_t v = A.ev[(ep * kEvCap + j) * A.U + u];
+        int q = j;  // insertion sort: ascending (block, member)
+        while (q > 0 && key[q - 1] > v) {
+          key[q] = key[q - 1];
+          --q;
+        }
+        key[q] = v;
+      }
+      int j = 0;
+      while (j < cnt) {
+        const uint32_t bl = key[j] >> 1;
+        bool in[2] = {false, false};
+        while (j < cnt && (key[j] >> 1) == bl) in[key[j++] & 1] = true;
+        const double r0 = r[k][0], r1 = r[k][1];  // the block's residual
+        double d[2] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (!in[e] || li[k][e] == 0.0) continue;  // zero columns are skipped (solvers.cpp:455)
+          double gi = 0.0;
+          for (int q = 0; q < nc[k][e]; ++q) gi += cv[k][e][q] * (cr[k][e][q] ? r1 : r0);
+          acc[4] += 1.0;
+          const double scale = beta * li[k][e];
+          const double xi = x[k][e];
+          const double xn = soft_threshold(xi - gi / scale, tau / scale);
+          d[e] = xn - xi;
+          if (d[e] != 0.0) {
+            x[k][e] = xn;
+            acc[3] += 1.0;
+            acc[4] += 1.0;
+          }
+        }
+        // rows: r + sum over the pair's columns (ascending) with a step of delta_c A(rho, c)
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          double v = f ? r1 : r0;
+          bool any = false;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (d[e] == 0.0) continue;
+            for (int q = 0; q < nc[k][e]; ++q)
+              if (cr[k][e][q] == f) {
+                v += d[e] * cv[k][e][q];
+                any = true;
+              }
+          }
+          if (any) r[k][f] = v;
+        }
+      }
+      // refresh r = A x - b on the pair's rows (solvers.cpp:472-474: apply, then - b)
+      double v0 = x[k][0], v1 = x[k][1];
+      if (va[k][0] && va[k][1]) rotate_pair(v0, v1, c, s, true);
+      const double y0 = sig[k][0] * v0, y1 = sig[k][1] * v1;
+      r[k][0] = y0 - bb[k][0];
+      r[k][1] = y1 - bb[k][1];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (!va[k][e]) continue;
+        acc[0] += fabs(x[k][e]);
+        acc[1] += x[k][e] != 0.0 ? 1.0 : 0.0;
+        acc[2] += r[k][e] * r[k][e];
+      }
+    }
+    acc[2] += tail;
+    block_sum<5>(acc);
+    double* part = A.partials + (size_t)(ep & 1) * gridDim.x * 5;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int q = 0; q < 5; ++q) part[(size_t)blockIdx.x * 5 + q] = acc[q];
+    }
+    grid.sync();
+    double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
+#pragma unroll
+      for (int w = 0; w < 5; ++w) tot[w] += __ldcg(&part[(size_t)q * 5 + w]);
+    }
+    block_sum<5>(tot);
+    __shared__ double bc[5];
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int w = 0; w < 5; ++w) bc[w] = tot[w];
+    }
+    __syncthreads();
+    const double f = tau * bc[0] + 0.5 * bc[2];
+    const uint64_t epoch = epoch0 + ep + 1;
+    const int stop = !isfinite(f) ? 2 : (has_target && f <= target) ? 1 : epoch >= max_epochs ? 3 : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // cd_stats_kernel's bookkeeping
+      const uint64_t ts = global_timer_ns();
+      st->epoch = epoch;
+      st->applied = (unsigned long long)bc[3];
+      st->colops = (unsigned long long)bc[4];
+      cd_record(st, A.trace, epoch, f, bc[1], bc[3], bc[4], ts);
+      st->f = f;
+      st->last_ts = ts;
+      if (stop) {
+        st->stop = 1;
+        st->status = stop == 2 ? -1 : stop == 1 ? 0 : 1;
+      }
+    }
+    ++e_done;
+    if (stop) break;
+  }
+  (void)e_done;
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (!va[k][e]) continue;
+      A.x[a[k] + e] = x[k][e];
+      A.r[a[k] + e] = r[k][e];
+    }
+  }
+}
+
+template <int P>
+int cd_pair_capacity() {
+  static const int cap = [] {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P>, kThreads, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return per_sm * sm_count();
+  }();
+  return cap;
+}
+
 uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {  // rng.hpp:37-45
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
   uint64_t x;
@@ -443,6 +793,201 @@ double cd_damping(uint64_t omega, uint64_t varpi, uint64_t n) {  // solvers.cpp:
                    static_cast<double>(n - 1);
 }
 
+
+// The pair-local path (see cd_pair_kernel): 1 = ran (state in x / r / dst),
+// 0 = not applicable, -1 = handed over mid-run (the caller restarts on the
+// direct path; only on an event-bucket or look-back overflow).
+int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uint64_t per_epoch,
+                const double* lips, double* x, double* r, CdDev* dst, CdSample* trace, CdDev* h_st,
+                std::chrono::steady_clock::time_point t0, uint64_t& launched, bool& time_out) {
+  const char* env = getenv("L1B_PCDM_PAIR");
+  if (env && env[0] == '0') return 0;
+  const OpView* op = v.op;
+  const uint64_t n = v.n;
+  if (!op || v.shard || op->right.count != 1 || op->left.count != 0 || op->p1 || op->p2 || v.m < n ||
+      v.max_col_nnz > 2 || v.max_row_nnz > 2 || n >= (1ull << 30) || n < 4 * B || !v.At.ptr || !v.b)
+    return 0;
+  const uint64_t U = (n + 2) / 2;
+  int P = 0, grid = 0;
+  const void* fn = nullptr;
+  auto try_p = [&](int p, int cap, const void* f) {
+    const uint64_t g = (U + (uint64_t)p * kThreads - 1) / ((uint64_t)p * kThreads);
+    if (!P && cap > 0 && g <= (uint64_t)cap) {
+      P = p;
+      grid = (int)g;
+      fn = f;
+    }
+  };
+  try_p(1, cd_pair_capacity<1>(), (const void*)cd_pair_kernel<1>);
+  try_p(2, cd_pair_capacity<2>(), (const void*)cd_pair_kernel<2>);
+  try_p(4, cd_pair_capacity<4>(), (const void*)cd_pair_kernel<4>);
+  if (!P) return 0;
+  cudaStream_t st = v.stream;
+  const uint64_t E_max = std::max<uint64_t>(1, std::min<uint64_t>(cfg->max_iters, (1ull << 22) / (per_epoch * B)));
+  auto margin = [&](uint64_t T) { return T * B / n + 4096; };  // ~2x the expected redraws (B / 2n per draw)
+  const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));
+  const int W = (int)(2 * B + 64);
+  std::vector<void*> bufs;
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
+    bufs.push_back((void*)*ptr);
+  };
+  int rc = 1;
+  int* h_flag = nullptr;
+  uint64_t* h_starts_pinned = nullptr;
+  try {
+    uint32_t* idx[2];
+    uint16_t* prevd;
+    uint64_t *sarr, *win;
+    uint32_t *cnt, *ev;
+    int* flag;
+    double* part;
+    uint32_t* tile_cnt;
+    uint64_t* cand;
+    void* scan_tmp;
+    size_t scan_bytes = 0;
+    std::vector<uint64_t> h_cand;
+    alloc(&idx[0], cap_raw * 4);
+    alloc(&idx[1], cap_raw * 4);
+    alloc(&prevd, cap_raw * 2);
+    alloc(&sarr, (E_max * per_epoch + 1) * 8);
+    alloc(&cnt, E_max * U * 4);
+    alloc(&ev, E_max * kEvCap * U * 4);
+    alloc(&win, 312 * 8);
+    alloc(&flag, 16);
+    alloc(&part, (size_t)2 * grid * 5 * 8);
+    const uint64_t max_tiles = (cap_raw + kCandTile - 1) / kCandTile;
+    alloc(&tile_cnt, (max_tiles + 1) * 4);
+    alloc(&cand, cap_raw * 8);
+    L1B_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tile_cnt, tile_cnt, (int)(max_tiles + 1), st));
+    alloc(&scan_tmp, scan_bytes);
+    L1B_CUDA(cudaMallocHost(&h_starts_pinned, (E_max * per_epoch + 1) * 8));
+    L1B_CUDA(cudaMallocHost(&h_flag, 16));
+    {
+      uint64_t w[312];
+      mt_seed_state(cfg->seed, w);  // Rng rng = make_rng(cfg.seed) (solvers.cpp:430)
+      L1B_CUDA(cudaMemcpyAsync(win, w, sizeof(w), cudaMemcpyHostToDevice, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+    }
+    CdPairArgs a;
+    a.n = n;
+    a.m = v.m;
+    a.U = U;
+    a.off = op->right.offset[0];
+    a.ptr32 = v.At.ptr32 ? 1 : 0;
+    a.c = op->right.c[0];
+    a.s = op->right.s[0];
+    a.sigma = op->sigma;
+    a.b = v.b;
+    a.lips = lips;
+    a.cptr = v.At.ptr;
+    a.crow = v.At.idx;
+    a.cval = v.At.val;
+    a.x = x;
+    a.r = r;
+    a.cnt = cnt;
+    a.ev = ev;
+    a.st = dst;
+    a.trace = trace;
+    a.partials = part;
+    int cur = 0;
+    uint64_t have = 0;  // drawn positions in idx[cur] (position 0 = the chunk's first draw)
+    while (launched < cfg->max_iters) {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
+        time_out = true;
+        break;
+      }
+      const uint64_t E = std::min<uint64_t>(E_max, cfg->max_iters - launched);
+      const uint64_t nb = E * per_epoch, T = nb * B;
+      uint64_t need = T + margin(T);
+      for (;;) {
+        if (need > cap_raw) throw Unsupported("pcdm pairs: stream buffer");
+        if (have < need) {
+          mt_stream_indices(win, need - have, n, idx[cur] + have, st);
+          have = need;
+        }
+        cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
+            idx[cur], have, W, prevd);
+        L1B_LAUNCHED();
+        const uint64_t tiles = (have + kCandTile - 1) / kCandTile;
+        cd_cand_count<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt);
+        L1B_LAUNCHED();
+        L1B_CUDA(cudaMemsetAsync(tile_cnt + tiles, 0, 4, st));
+        size_t tb = scan_bytes;
+        L1B_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, tb, tile_cnt, tile_cnt, (int)(tiles + 1), st));
+        cd_cand_write<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt, cand);
+        L1B_LAUNCHED();
+        uint32_t ncand = 0;
+        L1B_CUDA(cudaMemcpyAsync(h_flag, tile_cnt + tiles, 4, cudaMemcpyDeviceToHost, st));
+        L1B_CUDA(cudaStreamSynchronize(st));
+        ncand = (uint32_t)h_flag[0];
+        h_cand.resize(ncand);
+        if (ncand)
+          L1B_CUDA(cudaMemcpyAsync(h_cand.data(), cand, (size_t)ncand * 8, cudaMemcpyDeviceToHost, st));
+        L1B_CUDA(cudaStreamSynchronize(st));
+        // block starts: a draw is redrawn iff its previous draw lies inside its block
+        bool short_stream = false;
+        uint64_t sb = 0, j = 0;
+        for (uint64_t blk = 0; blk < nb; ++blk) {
+          h_starts_pinned[blk] = sb;
+          uint64_t e = sb + B;
+          while (j < ncand && (h_cand[j] >> 16) < e) {
+            const uint64_t q = h_cand[j] >> 16, d = h_cand[j] & 0xffff;
+            if (d == kPrevRej || q - d >= sb) ++e;
+            ++j;
+          }
+          if (e - sb > (uint64_t)W) throw Unsupported("pcdm pairs: block longer than the look-back");
+          if (e > have) {
+            short_stream = true;
+            break;
+          }
+          sb = e;
+        }
+        if (short_stream) {  // more redraws than the margin: draw further and walk again
+          need = have + have / 2;
+          continue;
+        }
+        h_starts_pinned[nb] = sb;
+        L1B_CUDA(cudaMemcpyAsync(sarr, h_starts_pinned, (nb + 1) * 8, cudaMemcpyHostToDevice, st));
+        break;
+      }
+      L1B_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+      L1B_CUDA(cudaMemsetAsync(cnt, 0, E * U * 4, st));
+      cd_scatter_kernel<<<grid_for(T), kThreads, 0, st>>>(idx[cur], prevd, sarr, nb, per_epoch, a.off, U, cnt,
+                                                        ev, flag);
+      L1B_LAUNCHED();
+      a.epochs = E;
+      void* args[] = {&a};
+      L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
+      L1B_LAUNCHED();
+      const uint64_t used = h_starts_pinned[nb];
+      L1B_CUDA(cudaMemcpyAsync(h_flag, flag, 4, cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaStreamSynchronize(st));
+      if (*h_flag & 4) throw Unsupported("pcdm pairs: event bucket");
+      // the draws past the chunk's last block open the next chunk
+      if (have > used)
+        L1B_CUDA(cudaMemcpyAsync(idx[cur ^ 1], idx[cur] + used, (have - used) * 4, cudaMemcpyDeviceToDevice, st));
+      have -= used;
+      cur ^= 1;
+      launched += E;
+      if (h_st->stop) break;
+    }
+  } catch (const Unsupported&) {
+    rc = -1;
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    for (void* q : bufs) cudaFree(q);
+    if (h_flag) cudaFreeHost(h_flag);
+    if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
+    throw;
+  }
+  cudaStreamSynchronize(st);
+  for (void* q : bufs) cudaFree(q);
+  if (h_flag) cudaFreeHost(h_flag);
+  if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
+  return rc;
+}
 }  // namespace
 
 void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
@@ -508,8 +1053,6 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     L1B_CUDA(cudaMallocHost(&h_coords, 2 * chunk * per_epoch * B * 4));
     for (auto& e : uploaded) L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     L1B_CUDA(cudaMallocHost(&h_st, sizeof(CdDev)));
-    L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
-    L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
     CdDev h;
     std::memset(&h, 0, sizeof(h));
     h.tau = v.tau;
@@ -519,18 +1062,33 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     h.tail_sq = v.tail_sq;
     h.max_epochs = cfg->max_iters;
     h.cap = tcap;
-    *h_st = h;
-    L1B_CUDA(cudaMemcpyAsync(dst, h_st, sizeof(CdDev), cudaMemcpyHostToDevice, st));
+    // x = 0, r = A 0 - b, the epoch-0 sample (also the restart of the direct
+    // path when the pair-local one hands over)
+    auto init_state = [&]() {
+      L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
+      L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
+      *h_st = h;
+      L1B_CUDA(cudaMemcpyAsync(dst, h_st, sizeof(CdDev), cudaMemcpyHostToDevice, st));
+      cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, dst, partials);
+      L1B_LAUNCHED();
+      cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 1);
+      L1B_LAUNCHED();
+    };
     const auto t0 = std::chrono::steady_clock::now();
-    cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, dst, partials);
-    L1B_LAUNCHED();
-    cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 1);
-    L1B_LAUNCHED();
+    init_state();
+    uint64_t launched = 0;
+    bool time_out = false;
+    const int pair_mode = pair_epochs(v, cfg, B, per_epoch, lips, x, r, dst, trace, h_st, t0, launched, time_out);
+    if (pair_mode < 0) {  // handed over (a bucket or the look-back overflowed): start again
+      L1B_CUDA(cudaStreamSynchronize(st));
+      launched = 0;
+      time_out = false;
+      init_state();
+    }
     std::mt19937_64 rng(cfg->seed);  // Rng rng = make_rng(cfg.seed) (solvers.cpp:430)
     std::vector<uint64_t> seen(serial ? 0 : n, 0);
-    uint64_t draw_block = 0, launched = 0;
+    uint64_t draw_block = 0;
     uint32_t stamp_base = 0;
-    bool time_out = false;
     // coordinate stream (host: mt19937_64 is sequential), one chunk of epochs
     // at a time into buffer `slot`; the next chunk is drawn while the device
     // runs this one, so the host RNG is off the critical path
@@ -556,9 +1114,9 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       return k;
     };
     int slot = 0;
-    uint64_t ep = std::min<uint64_t>(chunk, cfg->max_iters);
+    uint64_t ep = pair_mode > 0 ? 0 : std::min<uint64_t>(chunk, cfg->max_iters);
     uint64_t k = ep ? draw(ep, slot) : 0;
-    while (launched < cfg->max_iters) {
+    while (pair_mode <= 0 && launched < cfg->max_iters) {
       if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
         time_out = true;
         break;

@@ -330,6 +330,36 @@ __global__ void __launch_bounds__(DRAW_THREADS) mt_draw_kernel(const uint64_t* _
   if (rej) atomicOr(a.rejected, 1);
 }
 
+
+// ---------------------------------------------------------------------------
+// uniform_index (rng.hpp:37-45) over a continuing stream: one CTA runs the
+// recurrence from the saved window W_k (312 words in global memory), writes
+// out[q] = raw % n for draws k .. k + count - 1 (0xffffffff where
+// raw >= lim: the reference redraws; the consumer skips the position) and
+// saves W_{k+count}.  Sequential by nature: 156 independent words per step.
+constexpr int IDX_THREADS = 160;
+__global__ void __launch_bounds__(IDX_THREADS) mt_index_kernel(uint64_t* window, uint64_t count,
+                                                               uint64_t n, uint64_t lim,
+                                                               uint32_t* __restrict__ out) {
+  __shared__ uint64_t ring[1024];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NW; i += blockDim.x) ring[i] = window[i];
+  __syncthreads();
+  const bool pow2 = (n & (n - 1)) == 0;
+  for (uint64_t base = 0; base < count; base += MID) {
+    const uint64_t k = base + (uint64_t)tid;
+    if (tid < MID) {
+      const uint64_t w = next_word(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + MID) & 1023]);
+      ring[(k + NW) & 1023] = w;
+      if (k < count) {
+        const uint64_t raw = temper(w);
+        out[k] = raw >= lim ? 0xffffffffu : (uint32_t)(pow2 ? (raw & (n - 1)) : raw % n);
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < NW; i += blockDim.x) window[i] = ring[(count + i) & 1023];
+}
 }  // namespace mt
 
 // Host restatement of the jump (the device kernel's arithmetic, one thread):
@@ -451,6 +481,16 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
     if (vmax) *vmax = mx;
   }
   return true;
+}
+
+void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312); }
+
+void mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
+                       cudaStream_t st) {
+  if (count == 0) return;
+  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  mt::mt_index_kernel<<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
+  L1B_LAUNCHED();
 }
 
 }  // namespace l1b
