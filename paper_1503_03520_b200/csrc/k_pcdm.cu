@@ -590,10 +590,69 @@ struct CdPairArgs {
   double* partials;  // 2 x grid x 5
 };
 
-template <int P>
+// the objective of an epoch from the blocks' partials (fixed order: every
+// caller folds identically) and cd_stats_kernel's bookkeeping
+__device__ __forceinline__ void epoch_objective(const double* part, unsigned nblocks, double tau, double& f,
+                                                double& nnz, double& applied, double& colops) {
+  double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (unsigned q = threadIdx.x; q < nblocks; q += blockDim.x) {
+#pragma unroll
+    for (int w = 0; w < 5; ++w) tot[w] += __ldcg(&part[(size_t)q * 5 + w]);
+  }
+  block_sum<5>(tot);
+  __shared__ double bc[5];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < 5; ++w) bc[w] = tot[w];
+  }
+  __syncthreads();
+  f = tau * bc[0] + 0.5 * bc[2];
+  nnz = bc[1];
+  applied = bc[3];
+  colops = bc[4];
+  __syncthreads();
+}
+
+// stop: 0 = go on, 1 = target, 2 = non-finite, 3 = epoch budget
+__device__ __forceinline__ void epoch_record(CdDev* st, CdSample* trace, uint64_t epoch, double f, double nnz,
+                                             double applied, double colops, int stop) {
+  const uint64_t ts = global_timer_ns();
+  st->epoch = epoch;
+  st->applied = (unsigned long long)applied;
+  st->colops = (unsigned long long)colops;
+  cd_record(st, trace, epoch, f, nnz, applied, colops, ts);
+  st->f = f;
+  st->last_ts = ts;
+  if (stop) {
+    st->stop = 1;
+    st->status = stop == 2 ? -1 : stop == 1 ? 0 : 1;
+  }
+}
+
+// !SYNC launches: the samples of its epochs, in order (one CTA)
+__global__ void cd_pair_fold(const double* partials, unsigned nblocks, uint64_t epochs, CdDev* st,
+                             CdSample* trace) {
+  if (*(volatile int*)&st->stop) return;
+  const uint64_t epoch0 = st->epoch, max_epochs = st->max_epochs;
+  const double tau = st->tau;
+  for (uint64_t ep = 0; ep < epochs; ++ep) {
+    double f, nnz, applied, colops;
+    epoch_objective(partials + (size_t)ep * nblocks * 5, nblocks, tau, f, nnz, applied, colops);
+    const uint64_t epoch = epoch0 + ep + 1;
+    const int stop = !isfinite(f) ? 2 : epoch >= max_epochs ? 3 : 0;
+    if (threadIdx.x == 0) epoch_record(st, trace, epoch, f, nnz, applied, colops, stop);
+    if (stop) break;
+  }
+}
+
+// SYNC: a grid barrier per epoch, the objective and the stop test in the
+// kernel (runs with a target).  !SYNC: epochs back to back, each block's
+// partials kept per epoch; cd_pair_fold records the samples afterwards (no
+// target: only the epoch budget or a non-finite objective stops a run, and the
+// budget is the launch's epoch count).
+template <int P, bool SYNC>
 __global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
   namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   CdDev* st = A.st;
   if (*(volatile int*)&st->stop) return;
   const double beta = st->beta, tau = st->tau;
@@ -642,17 +701,40 @@ __global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
   // rows [n, m) stay 0 - b (empty rows): their ||r||^2 share, once
   double tail = 0.0;
   for (uint64_t i = (uint64_t)n + g0; i < A.m; i += T) tail += A.r[i] * A.r[i];
-  uint64_t e_done = 0;
+  // the bucket count and first kPre events of the next epoch are loaded one
+  // epoch ahead (independent of the running epoch)
+  constexpr int kPre = 4;
+  uint32_t pc[P], pk[P][kPre];
+  auto prefetch = [&](uint64_t ep) {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const uint64_t u = g0 + (uint64_t)k * T;
+      pc[k] = 0;
+      if (!live[k] || ep >= A.epochs) continue;
+      pc[k] = __ldcg(&A.cnt[ep * A.U + u]);
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) pk[k][j] = __ldcg(&A.ev[(ep * kEvCap + j) * A.U + u]);
+    }
+  };
+  prefetch(0);
   for (uint64_t ep = 0; ep < A.epochs; ++ep) {
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // ||x||_1, nnz, ||r||^2, applied, colops
+    uint32_t cur_c[P], cur_k[P][kPre];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      cur_c[k] = pc[k];
+#pragma unroll
+      for (int j = 0; j < kPre; ++j) cur_k[k][j] = pk[k][j];
+    }
+    prefetch(ep + 1);
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       if (!live[k]) continue;
       const uint64_t u = g0 + (uint64_t)k * T;
-      const int cnt = min((int)A.cnt[ep * A.U + u], kEvCap);
+      const int cnt = min((int)cur_c[k], kEvCap);
       uint32_t key[kEvCap];
       for (int j = 0; j < cnt; ++j) {
-        const uint32_t v = A.ev[(ep * kEvCap + j) * A.U + u];
+        const uint32_t v = j < kPre ? cur_k[k][j] : __ldcg(&A.ev[(ep * kEvCap + j) * A.U + u]);
         int q = j;  // insertion sort: ascending (block, member)
         while (q > 0 && key[q - 1] > v) {
           key[q] = key[q - 1];
@@ -716,44 +798,20 @@ __global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
     }
     acc[2] += tail;
     block_sum<5>(acc);
-    double* part = A.partials + (size_t)(ep & 1) * gridDim.x * 5;
+    double* part = A.partials + (size_t)(SYNC ? (ep & 1) : ep) * gridDim.x * 5;
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int q = 0; q < 5; ++q) part[(size_t)blockIdx.x * 5 + q] = acc[q];
     }
-    grid.sync();
-    double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (unsigned q = threadIdx.x; q < gridDim.x; q += blockDim.x) {
-#pragma unroll
-      for (int w = 0; w < 5; ++w) tot[w] += __ldcg(&part[(size_t)q * 5 + w]);
-    }
-    block_sum<5>(tot);
-    __shared__ double bc[5];
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int w = 0; w < 5; ++w) bc[w] = tot[w];
-    }
-    __syncthreads();
-    const double f = tau * bc[0] + 0.5 * bc[2];
+    if constexpr (!SYNC) continue;
+    cg::this_grid().sync();
+    double f, nnz, applied, colops;
+    epoch_objective(part, gridDim.x, tau, f, nnz, applied, colops);
     const uint64_t epoch = epoch0 + ep + 1;
     const int stop = !isfinite(f) ? 2 : (has_target && f <= target) ? 1 : epoch >= max_epochs ? 3 : 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // cd_stats_kernel's bookkeeping
-      const uint64_t ts = global_timer_ns();
-      st->epoch = epoch;
-      st->applied = (unsigned long long)bc[3];
-      st->colops = (unsigned long long)bc[4];
-      cd_record(st, A.trace, epoch, f, bc[1], bc[3], bc[4], ts);
-      st->f = f;
-      st->last_ts = ts;
-      if (stop) {
-        st->stop = 1;
-        st->status = stop == 2 ? -1 : stop == 1 ? 0 : 1;
-      }
-    }
-    ++e_done;
+    if (blockIdx.x == 0 && threadIdx.x == 0) epoch_record(st, A.trace, epoch, f, nnz, applied, colops, stop);
     if (stop) break;
   }
-  (void)e_done;
 #pragma unroll
   for (int k = 0; k < P; ++k) {
 #pragma unroll
@@ -768,12 +826,15 @@ __global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
 template <int P>
 int cd_pair_capacity() {
   static const int cap = [] {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P>, kThreads, 0) != cudaSuccess) {
+    int per_sm = 0, per_sm2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P, true>, kThreads, 0) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, cd_pair_kernel<P, false>, kThreads, 0) !=
+            cudaSuccess) {
       cudaGetLastError();
       return 0;
     }
-    return per_sm * sm_count();
+    return std::min(per_sm, per_sm2) * sm_count();
   }();
   return cap;
 }
@@ -797,9 +858,11 @@ double cd_damping(uint64_t omega, uint64_t varpi, uint64_t n) {  // solvers.cpp:
 // The pair-local path (see cd_pair_kernel): 1 = ran (state in x / r / dst),
 // 0 = not applicable, -1 = handed over mid-run (the caller restarts on the
 // direct path; only on an event-bucket or look-back overflow).
+template <typename Start>
 int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uint64_t per_epoch,
                 const double* lips, double* x, double* r, CdDev* dst, CdSample* trace, CdDev* h_st,
-                std::chrono::steady_clock::time_point t0, uint64_t& launched, bool& time_out) {
+                Start&& start, const std::chrono::steady_clock::time_point& t0, uint64_t& launched,
+                bool& time_out) {
   const char* env = getenv("L1B_PCDM_PAIR");
   if (env && env[0] == '0') return 0;
   const OpView* op = v.op;
@@ -818,15 +881,20 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       fn = f;
     }
   };
-  try_p(1, cd_pair_capacity<1>(), (const void*)cd_pair_kernel<1>);
-  try_p(2, cd_pair_capacity<2>(), (const void*)cd_pair_kernel<2>);
-  try_p(4, cd_pair_capacity<4>(), (const void*)cd_pair_kernel<4>);
+  // with a target the objective is tested every epoch inside the kernel (grid
+  // barrier); without one the epochs run back to back
+  const bool sync = cfg->has_target != 0;
+  try_p(1, cd_pair_capacity<1>(), sync ? (const void*)cd_pair_kernel<1, true> : (const void*)cd_pair_kernel<1, false>);
+  try_p(2, cd_pair_capacity<2>(), sync ? (const void*)cd_pair_kernel<2, true> : (const void*)cd_pair_kernel<2, false>);
+  try_p(4, cd_pair_capacity<4>(), sync ? (const void*)cd_pair_kernel<4, true> : (const void*)cd_pair_kernel<4, false>);
   if (!P) return 0;
   cudaStream_t st = v.stream;
   const uint64_t E_max = std::max<uint64_t>(1, std::min<uint64_t>(cfg->max_iters, (1ull << 22) / (per_epoch * B)));
   auto margin = [&](uint64_t T) { return T * B / n + 4096; };  // ~2x the expected redraws (B / 2n per draw)
   const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));
-  const int W = (int)(2 * B + 64);
+  // look-back: a block is B kept draws plus ~B^2 / 2n redraws; W bounds its
+  // length (a longer block hands the run to the direct path)
+  const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
   std::vector<void*> bufs;
   auto alloc = [&](auto** ptr, size_t bytes) {
     L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
@@ -847,18 +915,18 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     void* scan_tmp;
     size_t scan_bytes = 0;
     std::vector<uint64_t> h_cand;
-    alloc(&idx[0], cap_raw * 4);
-    alloc(&idx[1], cap_raw * 4);
-    alloc(&prevd, cap_raw * 2);
+    alloc(&idx[0], (cap_raw + 312) * 4);  // + one generator round of slack
+    alloc(&idx[1], (cap_raw + 312) * 4);
+    alloc(&prevd, (cap_raw + 312) * 2);
     alloc(&sarr, (E_max * per_epoch + 1) * 8);
     alloc(&cnt, E_max * U * 4);
     alloc(&ev, E_max * kEvCap * U * 4);
     alloc(&win, 312 * 8);
     alloc(&flag, 16);
-    alloc(&part, (size_t)2 * grid * 5 * 8);
-    const uint64_t max_tiles = (cap_raw + kCandTile - 1) / kCandTile;
+    alloc(&part, (size_t)(sync ? 2 : E_max) * grid * 5 * 8);
+    const uint64_t max_tiles = (cap_raw + 312 + kCandTile - 1) / kCandTile;
     alloc(&tile_cnt, (max_tiles + 1) * 4);
-    alloc(&cand, cap_raw * 8);
+    alloc(&cand, (cap_raw + 312) * 8);
     L1B_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tile_cnt, tile_cnt, (int)(max_tiles + 1), st));
     alloc(&scan_tmp, scan_bytes);
     L1B_CUDA(cudaMallocHost(&h_starts_pinned, (E_max * per_epoch + 1) * 8));
@@ -869,6 +937,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       L1B_CUDA(cudaMemcpyAsync(win, w, sizeof(w), cudaMemcpyHostToDevice, st));
       L1B_CUDA(cudaStreamSynchronize(st));
     }
+    start();  // x = 0, r = -b, epoch-0 sample: the solve's clock starts here
     CdPairArgs a;
     a.n = n;
     a.m = v.m;
@@ -902,10 +971,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       uint64_t need = T + margin(T);
       for (;;) {
         if (need > cap_raw) throw Unsupported("pcdm pairs: stream buffer");
-        if (have < need) {
-          mt_stream_indices(win, need - have, n, idx[cur] + have, st);
-          have = need;
-        }
+        if (have < need) have += mt_stream_indices(win, need - have, n, idx[cur] + have, st);
         cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
             idx[cur], have, W, prevd);
         L1B_LAUNCHED();
@@ -958,8 +1024,15 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       L1B_LAUNCHED();
       a.epochs = E;
       void* args[] = {&a};
-      L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
-      L1B_LAUNCHED();
+      if (sync) {
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
+        L1B_LAUNCHED();
+      } else {
+        L1B_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
+        L1B_LAUNCHED();
+        cd_pair_fold<<<1, kThreads, 0, st>>>(part, (unsigned)grid, E, dst, trace);
+        L1B_LAUNCHED();
+      }
       const uint64_t used = h_starts_pinned[nb];
       L1B_CUDA(cudaMemcpyAsync(h_flag, flag, 4, cudaMemcpyDeviceToHost, st));
       L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
@@ -1074,16 +1147,21 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       cd_stats_kernel<<<grid_for(n), kThreads, 0, st>>>(x, n, dst, trace, partials, 1);
       L1B_LAUNCHED();
     };
-    const auto t0 = std::chrono::steady_clock::now();
-    init_state();
+    auto t0 = std::chrono::steady_clock::now();
+    auto start = [&]() {
+      t0 = std::chrono::steady_clock::now();
+      init_state();
+    };
     uint64_t launched = 0;
     bool time_out = false;
-    const int pair_mode = pair_epochs(v, cfg, B, per_epoch, lips, x, r, dst, trace, h_st, t0, launched, time_out);
-    if (pair_mode < 0) {  // handed over (a bucket or the look-back overflowed): start again
+    // the pair-local path allocates its buffers, then calls start()
+    const int pair_mode = pair_epochs(v, cfg, B, per_epoch, lips, x, r, dst, trace, h_st, start, t0, launched,
+                                      time_out);
+    if (pair_mode <= 0) {  // not applicable, or handed over (a bucket / the look-back overflowed)
       L1B_CUDA(cudaStreamSynchronize(st));
       launched = 0;
       time_out = false;
-      init_state();
+      start();
     }
     std::mt19937_64 rng(cfg->seed);  // Rng rng = make_rng(cfg.seed) (solvers.cpp:430)
     std::vector<uint64_t> seen(serial ? 0 : n, 0);

@@ -31,6 +31,7 @@
 // The spectrum's rejection (u <= lo, i.e. a raw draw with (x >> 11) == 0,
 // probability 2^-53 per draw) would shift every later position: it is
 // detected and reported, and the caller falls back to the sequential stream.
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -332,34 +333,40 @@ __global__ void __launch_bounds__(DRAW_THREADS) mt_draw_kernel(const uint64_t* _
 
 
 // ---------------------------------------------------------------------------
-// uniform_index (rng.hpp:37-45) over a continuing stream: one CTA runs the
-// recurrence from the saved window W_k (312 words in global memory), writes
-// out[q] = raw % n for draws k .. k + count - 1 (0xffffffff where
-// raw >= lim: the reference redraws; the consumer skips the position) and
-// saves W_{k+count}.  Sequential by nature: 156 independent words per step.
-constexpr int IDX_THREADS = 160;
-__global__ void __launch_bounds__(IDX_THREADS) mt_index_kernel(uint64_t* window, uint64_t count,
-                                                               uint64_t n, uint64_t lim,
-                                                               uint32_t* __restrict__ out) {
+// uniform_index (rng.hpp:37-45) over a continuing stream, from the saved window
+// W_k (312 words in global memory) to W_{k+count}, count a multiple of 156:
+// out[q] = raw % n for draws k .. k + count - 1 (0xffffffff where raw >= lim:
+// the reference redraws, the consumer skips the position).
+//
+// The recurrence is sequential: 156 independent words per step, through a
+// 1024-word shared-memory ring, one block barrier per step.  Its critical path
+// is only next_word; tempering, the reduction and the store of step t's words
+// run in a second group of warps during step t + 1 (the ring keeps them).
+constexpr int IDX_THREADS = 320;  // 160 recurrence + 160 emitters
+template <bool POW2>
+__global__ void __launch_bounds__(IDX_THREADS) mt_index_kernel(uint64_t* window, uint64_t count, uint64_t n,
+                                                               uint64_t lim, uint32_t* __restrict__ out) {
   __shared__ uint64_t ring[1024];
   const int tid = threadIdx.x;
+  const bool gen = tid < 160;
+  const int e = tid - 160;  // emitter lane
   for (int i = tid; i < NW; i += blockDim.x) ring[i] = window[i];
   __syncthreads();
-  const bool pow2 = (n & (n - 1)) == 0;
-  for (uint64_t base = 0; base < count; base += MID) {
-    const uint64_t k = base + (uint64_t)tid;
-    if (tid < MID) {
-      const uint64_t w = next_word(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + MID) & 1023]);
-      ring[(k + NW) & 1023] = w;
-      if (k < count) {
-        const uint64_t raw = temper(w);
-        out[k] = raw >= lim ? 0xffffffffu : (uint32_t)(pow2 ? (raw & (n - 1)) : raw % n);
-      }
+  for (uint64_t base = 0; base <= count; base += MID) {
+    if (gen) {
+      const uint64_t k = base + (uint64_t)tid;
+      if (tid < MID && base < count)
+        ring[(k + NW) & 1023] = next_word(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + MID) & 1023]);
+    } else if (base > 0 && e < MID) {  // the previous step's words
+      const uint64_t k = base - MID + (uint64_t)e;
+      const uint64_t raw = temper(ring[(k + NW) & 1023]);
+      out[k] = raw >= lim ? 0xffffffffu : (uint32_t)(POW2 ? (raw & (n - 1)) : raw % n);
     }
     __syncthreads();
   }
   for (int i = tid; i < NW; i += blockDim.x) window[i] = ring[(count + i) & 1023];
 }
+
 }  // namespace mt
 
 // Host restatement of the jump (the device kernel's arithmetic, one thread):
@@ -485,12 +492,15 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 
 void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312); }
 
-void mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
-                       cudaStream_t st) {
-  if (count == 0) return;
+uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
+                           cudaStream_t st) {
+  count = (count + mt::MID - 1) / mt::MID * mt::MID;
+  if (count == 0) return 0;
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
-  mt::mt_index_kernel<<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
+  if ((n & (n - 1)) == 0) mt::mt_index_kernel<true><<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
+  else mt::mt_index_kernel<false><<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
   L1B_LAUNCHED();
+  return count;
 }
 
 }  // namespace l1b
