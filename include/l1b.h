@@ -70,6 +70,14 @@ int l1b_device_uniform_draws(int device, uint64_t seed, uint64_t count, double l
                              int spectrum, double shift, uint64_t win_lo, uint64_t win_hi,
                              uint32_t min_log2_chunk, double* d_out, double* vmin, double* vmax,
                              int* exact);
+/* Device coordinate stream of the pair-local CD / PCDM path (k_rng.cu
+ * mt_stream_indices): raw draws of Rng(seed) reduced like uniform_index(rng,
+ * n) (rng.hpp:37-45), 0xffffffff where the reference would redraw, into the
+ * device buffer d_out.  Drawn in npieces consecutive launches that continue the
+ * saved generator state; each piece is rounded up to a multiple of 312 draws
+ * (d_out needs room for them); *drawn receives the total.  n < 2^32. */
+int l1b_device_index_stream(int device, uint64_t seed, uint64_t n, const uint64_t* piece_counts,
+                            uint32_t npieces, uint32_t* d_out, uint64_t* drawn);
 /* Host check of the jump polynomials: raw outputs 2^log2_jump ...
  * 2^log2_jump + count - 1 of std::mt19937_64(seed), reached by jumping. */
 int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, uint64_t* out);

@@ -103,6 +103,7 @@ SIGNATURES = [
     ("l1b_realize_spectrum_uniform", C.c_int, [u64, f64, f64, f64, u64, P(f64)]),
     ("l1b_device_uniform_draws", C.c_int, [C.c_int, u64, u64, f64, f64, C.c_int, f64, u64, u64, u32,
                                            vp, P(f64), P(f64), P(C.c_int)]),
+    ("l1b_device_index_stream", C.c_int, [C.c_int, u64, u64, P(u64), u32, vp, P(u64)]),
     ("l1b_mt_draws_after_jump", C.c_int, [u64, u32, u64, P(u64)]),
     ("l1b_uniform_sparse_solution", C.c_int, [u64, u64, f64, u64, P(u32), P(f64)]),
     ("l1b_generate", C.c_int, [C.c_int, P(GenDesc), P(ShardDesc), P(vp)]),

@@ -403,6 +403,30 @@ int l1b_device_uniform_draws(int device, uint64_t seed, uint64_t count, double l
   });
 }
 
+int l1b_device_index_stream(int device, uint64_t seed, uint64_t n, const uint64_t* piece_counts,
+                            uint32_t npieces, uint32_t* d_out, uint64_t* drawn) {
+  return guard([&] {
+    if (n == 0 || n >= (1ull << 32)) throw InvalidArgument("index stream: n must lie in [1, 2^32)");
+    if (npieces && (!piece_counts || !d_out)) throw InvalidArgument("null argument");
+    L1B_CUDA(cudaSetDevice(device));
+    uint64_t w[312];
+    mt_seed_state(seed, w);
+    uint64_t* d_w = nullptr;
+    L1B_CUDA(cudaMalloc(&d_w, sizeof(w)));
+    uint64_t total = 0;
+    try {
+      L1B_CUDA(cudaMemcpy(d_w, w, sizeof(w), cudaMemcpyHostToDevice));
+      for (uint32_t k = 0; k < npieces; ++k) total += mt_stream_indices(d_w, piece_counts[k], n, d_out + total, 0);
+      L1B_CUDA(cudaStreamSynchronize(0));
+    } catch (...) {
+      cudaFree(d_w);
+      throw;
+    }
+    L1B_CUDA(cudaFree(d_w));
+    if (drawn) *drawn = total;
+  });
+}
+
 int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
                                 uint32_t* support_out, double* values_out) {
   return guard([&] {

@@ -334,37 +334,84 @@ __global__ void __launch_bounds__(DRAW_THREADS) mt_draw_kernel(const uint64_t* _
 
 // ---------------------------------------------------------------------------
 // uniform_index (rng.hpp:37-45) over a continuing stream, from the saved window
-// W_k (312 words in global memory) to W_{k+count}, count a multiple of 156:
+// W_k (312 words in global memory) to W_{k+count}, count a multiple of 312:
 // out[q] = raw % n for draws k .. k + count - 1 (0xffffffff where raw >= lim:
 // the reference redraws, the consumer skips the position).
 //
-// The recurrence is sequential: 156 independent words per step, through a
-// 1024-word shared-memory ring, one block barrier per step.  Its critical path
-// is only next_word; tempering, the reduction and the store of step t's words
-// run in a second group of warps during step t + 1 (the ring keeps them).
-constexpr int IDX_THREADS = 320;  // 160 recurrence + 160 emitters
-template <bool POW2>
-__global__ void __launch_bounds__(IDX_THREADS) mt_index_kernel(uint64_t* window, uint64_t count, uint64_t n,
-                                                               uint64_t lim, uint32_t* __restrict__ out) {
-  __shared__ uint64_t ring[1024];
+// The recurrence is sequential.  Column j (0..155) of step t is
+// y_j(t) = x[312 + 156 t + j] = next_word(A_j, N_j, B_j) with A_j = x[156 t + j]
+// (two steps back), B_j = x[156 t + 156 + j] (one step back), N_j = A_{j+1}
+// (j < 155) and N_155 = B_0.  Thread j keeps A_j, B_j in registers and
+// thread 0 also runs column 155 (its N is column 0's own B), so the only
+// values crossing threads are the neighbour's A and B, from two steps back:
+// a thread runs TWO steps between block barriers, reading the (A, B) its
+// neighbour published at the previous barrier.  The untempered words go to
+// global memory; mt_temper_kernel (all SMs) tempers and reduces them after.
+constexpr int IDX_THREADS = 160;
+__global__ void __launch_bounds__(IDX_THREADS) mt_words_kernel(uint64_t* window, uint64_t count,
+                                                               uint64_t* __restrict__ words) {
+  __shared__ uint64_t pub[2][2][MID];   // [buffer][A | B][column]
   const int tid = threadIdx.x;
-  const bool gen = tid < 160;
-  const int e = tid - 160;  // emitter lane
-  for (int i = tid; i < NW; i += blockDim.x) ring[i] = window[i];
+  const bool rec = tid < MID - 1;       // columns 0..154 (thread 0 also 155)
+  uint64_t A = 0, B = 0, A2 = 0, B2 = 0;  // A2 / B2: column 155 (thread 0)
+  if (rec) {
+    A = window[tid];
+    B = window[MID + tid];
+    pub[0][0][tid] = A;
+    pub[0][1][tid] = B;
+  }
+  if (tid == 0) {
+    A2 = window[MID - 1];
+    B2 = window[2 * MID - 1];
+    pub[0][0][MID - 1] = A2;
+    pub[0][1][MID - 1] = B2;
+  }
   __syncthreads();
-  for (uint64_t base = 0; base <= count; base += MID) {
-    if (gen) {
-      const uint64_t k = base + (uint64_t)tid;
-      if (tid < MID && base < count)
-        ring[(k + NW) & 1023] = next_word(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + MID) & 1023]);
-    } else if (base > 0 && e < MID) {  // the previous step's words
-      const uint64_t k = base - MID + (uint64_t)e;
-      const uint64_t raw = temper(ring[(k + NW) & 1023]);
-      out[k] = raw >= lim ? 0xffffffffu : (uint32_t)(POW2 ? (raw & (n - 1)) : raw % n);
+  int p = 0;
+  for (uint64_t base = 0; base < count; base += 2 * MID) {
+    if (rec) {
+      const uint64_t NA = pub[p][0][tid + 1], NB = pub[p][1][tid + 1];
+      const uint64_t ya = next_word(A, NA, B);   // step t
+      const uint64_t yb = next_word(B, NB, ya);  // step t + 1: A <- B, N <- neighbour's B, B <- ya
+      if (tid == 0) {
+        const uint64_t za = next_word(A2, B, B2);   // column 155, N = B_0(t)
+        const uint64_t zb = next_word(B2, ya, za);  // N = B_0(t + 1) = y_0(t)
+        A2 = za;
+        B2 = zb;
+        words[base + MID - 1] = za;
+        words[base + 2 * MID - 1] = zb;
+        pub[p ^ 1][0][MID - 1] = za;
+        pub[p ^ 1][1][MID - 1] = zb;
+      }
+      A = ya;
+      B = yb;
+      words[base + tid] = ya;
+      words[base + MID + tid] = yb;
+      pub[p ^ 1][0][tid] = ya;
+      pub[p ^ 1][1][tid] = yb;
     }
+    p ^= 1;
     __syncthreads();
   }
-  for (int i = tid; i < NW; i += blockDim.x) window[i] = ring[(count + i) & 1023];
+  if (rec) {
+    window[tid] = A;
+    window[MID + tid] = B;
+  }
+  if (tid == 0) {
+    window[MID - 1] = A2;
+    window[2 * MID - 1] = B2;
+  }
+}
+
+
+template <bool POW2>
+__global__ void mt_temper_kernel(const uint64_t* __restrict__ words, uint64_t count, uint64_t n, uint64_t lim,
+                                 uint32_t* __restrict__ out) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t raw = temper(words[k]);
+    out[k] = raw >= lim ? 0xffffffffu : (uint32_t)(POW2 ? (raw & (n - 1)) : raw % n);
+  }
 }
 
 }  // namespace mt
@@ -494,12 +541,18 @@ void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312);
 
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            cudaStream_t st) {
-  count = (count + mt::MID - 1) / mt::MID * mt::MID;
+  count = (count + 2 * mt::MID - 1) / (2 * mt::MID) * (2 * mt::MID);
   if (count == 0) return 0;
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
-  if ((n & (n - 1)) == 0) mt::mt_index_kernel<true><<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
-  else mt::mt_index_kernel<false><<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, n, lim, d_out);
+  uint64_t* words = nullptr;
+  L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
+  mt::mt_words_kernel<<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, words);
   L1B_LAUNCHED();
+  const int grid = grid_for(count);
+  if ((n & (n - 1)) == 0) mt::mt_temper_kernel<true><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
+  else mt::mt_temper_kernel<false><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
+  L1B_LAUNCHED();
+  L1B_CUDA(cudaFreeAsync(words, st));
   return count;
 }
 

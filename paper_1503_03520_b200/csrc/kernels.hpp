@@ -43,7 +43,7 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 // uniform_index(rng, n) draws (rng.hpp:37-45) continuing a device-resident
 // stream: d_window = the 312-word state (mt_seed_state, updated in place);
 // d_out[q] = index of draw q, 0xffffffff where the reference would redraw.
-// Draws count rounded up to a multiple of 156 (returned; d_out must hold them).
+// Draws count rounded up to a multiple of 312 (returned; d_out must hold them).
 void mt_seed_state(uint64_t seed, uint64_t* w312);
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            cudaStream_t st);

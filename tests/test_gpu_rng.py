@@ -148,3 +148,29 @@ def test_shards_device_rng_reproduce_global_instance():
         np.testing.assert_array_equal(s.inst.b[: e - a], whole.b[a:e])
         assert s.inst.info.gram_lmax == whole.info.gram_lmax
         assert s.inst.info.cert_kappa == whole.info.cert_kappa
+
+
+@pytest.mark.parametrize("n,pieces", [(32768, [100_000]), (1_000_003, [1, 311, 313, 40_000, 3]),
+                                      (4096, [312] * 7), ((1 << 31), [5000])])
+def test_coordinate_index_stream_bit_exact(oracle, n, pieces):
+    """The pair-local CD / PCDM coordinate stream (mt_stream_indices, continued
+    over several launches) against std::mt19937_64 reduced like uniform_index:
+    raw % n, the redraw marker where raw >= UINT64_MAX - UINT64_MAX % n."""
+    torch = need_cuda()
+    from paper_1503_03520_b200 import _native as N
+
+    seed = oracle.mix_seed(1, 7)
+    cap = sum(-(-max(p, 1) // 312) * 312 for p in pieces)
+    out = torch.empty(cap, dtype=torch.int32, device="cuda")
+    arr = (ctypes.c_uint64 * len(pieces))(*pieces)
+    drawn = ctypes.c_uint64()
+    N.check(N.load().l1b_device_index_stream(0, seed, n, arr, len(pieces), ctypes.c_void_p(out.data_ptr()),
+                                             ctypes.byref(drawn)))
+    torch.cuda.synchronize()
+    assert drawn.value == sum(-(-p // 312) * 312 for p in pieces)
+    got = out[: drawn.value].cpu().numpy().view(np.uint32)
+    r = oracle.rng(seed)
+    raw = np.array([oracle.lib.lo_rng_next(ctypes.byref(r)) for _ in range(drawn.value)], dtype=np.uint64)
+    lim = np.uint64((1 << 64) - 1 - ((1 << 64) - 1) % n)
+    want = np.where(raw >= lim, np.uint64(0xFFFFFFFF), raw % np.uint64(n)).astype(np.uint32)
+    np.testing.assert_array_equal(got, want)
