@@ -416,7 +416,7 @@ int l1b_device_index_stream(int device, uint64_t seed, uint64_t n, const uint64_
     uint64_t total = 0;
     try {
       L1B_CUDA(cudaMemcpy(d_w, w, sizeof(w), cudaMemcpyHostToDevice));
-      for (uint32_t k = 0; k < npieces; ++k) total += mt_stream_indices(d_w, piece_counts[k], n, d_out + total, 0);
+      for (uint32_t k = 0; k < npieces; ++k) total += mt_stream_indices(d_w, piece_counts[k], n, d_out + total, nullptr, 0);
       L1B_CUDA(cudaStreamSynchronize(0));
     } catch (...) {
       cudaFree(d_w);

@@ -745,13 +745,13 @@ __global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
       int j = 0;
       while (j < cnt) {
         const uint32_t bl = key[j] >> 1;
-        bool in[2] = {false, false};
-        while (j < cnt && (key[j] >> 1) == bl) in[key[j++] & 1] = true;
+        int in = 0;  // bit e: member e steps in this block
+        while (j < cnt && (key[j] >> 1) == bl) in |= 1 << (key[j++] & 1);
         const double r0 = r[k][0], r1 = r[k][1];  // the block's residual
         double d[2] = {0.0, 0.0};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (!in[e] || li[k][e] == 0.0) continue;  // zero columns are skipped (solvers.cpp:455)
+          if (!((in >> e) & 1) || li[k][e] == 0.0) continue;  // zero columns are skipped (solvers.cpp:455)
           double gi = 0.0;
           for (int q = 0; q < nc[k][e]; ++q) gi += cv[k][e][q] * (cr[k][e][q] ? r1 : r0);
           acc[4] += 1.0;
@@ -906,7 +906,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   try {
     uint32_t* idx[2];
     uint16_t* prevd;
-    uint64_t *sarr, *win;
+    uint64_t *sarr, *win, *words;
     uint32_t *cnt, *ev;
     int* flag;
     double* part;
@@ -922,6 +922,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     alloc(&cnt, E_max * U * 4);
     alloc(&ev, E_max * kEvCap * U * 4);
     alloc(&win, 312 * 8);
+    alloc(&words, (cap_raw + 312) * 8);
     alloc(&flag, 16);
     alloc(&part, (size_t)(sync ? 2 : E_max) * grid * 5 * 8);
     const uint64_t max_tiles = (cap_raw + 312 + kCandTile - 1) / kCandTile;
@@ -971,7 +972,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       uint64_t need = T + margin(T);
       for (;;) {
         if (need > cap_raw) throw Unsupported("pcdm pairs: stream buffer");
-        if (have < need) have += mt_stream_indices(win, need - have, n, idx[cur] + have, st);
+        if (have < need) have += mt_stream_indices(win, need - have, n, idx[cur] + have, words, st);
         cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
             idx[cur], have, W, prevd);
         L1B_LAUNCHED();

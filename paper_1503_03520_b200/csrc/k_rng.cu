@@ -540,19 +540,19 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312); }
 
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
-                           cudaStream_t st) {
+                           uint64_t* d_words, cudaStream_t st) {
   count = (count + 2 * mt::MID - 1) / (2 * mt::MID) * (2 * mt::MID);
   if (count == 0) return 0;
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
-  uint64_t* words = nullptr;
-  L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
+  uint64_t* words = d_words;
+  if (!words) L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
   mt::mt_words_kernel<<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, words);
   L1B_LAUNCHED();
   const int grid = grid_for(count);
   if ((n & (n - 1)) == 0) mt::mt_temper_kernel<true><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
   else mt::mt_temper_kernel<false><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
   L1B_LAUNCHED();
-  L1B_CUDA(cudaFreeAsync(words, st));
+  if (!d_words) L1B_CUDA(cudaFreeAsync(words, st));
   return count;
 }
 
