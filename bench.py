@@ -257,7 +257,7 @@ def main():
         cb = run_reference(args)
         line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference generator, seed 3)", "impl": "reference",
                 "config": {"workload": "C4 FISTA (bounded CPU sample, see cpu_baseline.sample)"},
                 "cpu_baseline": cb,
@@ -300,7 +300,7 @@ def main():
     line = {
         "metric": METRIC, "value": fused["ips"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": fused["ms_step"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator on device, seed 3)",
         "config": {"workload": f"C4 FISTA: n=2^{int(math.log2(info.n))} cols x m=2^{int(math.log2(info.m))} rows, "
                                f"4 stages, nnz={info.nnz}, q=1, s=n/1000, tau=1, seed 3",
