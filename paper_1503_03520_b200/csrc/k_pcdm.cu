@@ -889,9 +889,15 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   try_p(4, cd_pair_capacity<4>(), sync ? (const void*)cd_pair_kernel<4, true> : (const void*)cd_pair_kernel<4, false>);
   if (!P) return 0;
   cudaStream_t st = v.stream;
-  const uint64_t E_max = std::max<uint64_t>(1, std::min<uint64_t>(cfg->max_iters, (1ull << 22) / (per_epoch * B)));
+  // chunks of ~2^19 draws: the stream for the next chunk is drawn (side stream,
+  // one SM) while the current chunk's walk and epochs run
+  const uint64_t E_max = std::max<uint64_t>(1, std::min<uint64_t>(cfg->max_iters, (1ull << 19) / (per_epoch * B)));
   auto margin = [&](uint64_t T) { return T * B / n + 4096; };  // ~2x the expected redraws (B / 2n per draw)
-  const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));
+  const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));  // one chunk
+  const uint64_t G = cap_raw / 2;  // draws per generator launch
+  // stream buffer: the whole run when it fits in 2^25 draws, else rewound
+  const uint64_t run_draws = cfg->max_iters * per_epoch * B;
+  const uint64_t scap = std::min<uint64_t>(run_draws + margin(run_draws) + 2 * cap_raw, (1ull << 25) + 2 * cap_raw);
   // look-back: a block is B kept draws plus ~B^2 / 2n redraws; W bounds its
   // length (a longer block hands the run to the direct path)
   const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
@@ -903,8 +909,10 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   int rc = 1;
   int* h_flag = nullptr;
   uint64_t* h_starts_pinned = nullptr;
+  cudaStream_t gs = nullptr;  // generator stream
+  std::vector<cudaEvent_t> evs;
   try {
-    uint32_t* idx[2];
+    uint32_t* S[2] = {nullptr, nullptr};
     uint16_t* prevd;
     uint64_t *sarr, *win, *words;
     uint32_t *cnt, *ev;
@@ -915,14 +923,13 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     void* scan_tmp;
     size_t scan_bytes = 0;
     std::vector<uint64_t> h_cand;
-    alloc(&idx[0], (cap_raw + 312) * 4);  // + one generator round of slack
-    alloc(&idx[1], (cap_raw + 312) * 4);
+    alloc(&S[0], (scap + 312) * 4);  // + one generator round of slack
     alloc(&prevd, (cap_raw + 312) * 2);
     alloc(&sarr, (E_max * per_epoch + 1) * 8);
     alloc(&cnt, E_max * U * 4);
     alloc(&ev, E_max * kEvCap * U * 4);
     alloc(&win, 312 * 8);
-    alloc(&words, (cap_raw + 312) * 8);
+    alloc(&words, (G + 312) * 8);
     alloc(&flag, 16);
     alloc(&part, (size_t)(sync ? 2 : E_max) * grid * 5 * 8);
     const uint64_t max_tiles = (cap_raw + 312 + kCandTile - 1) / kCandTile;
@@ -932,13 +939,25 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     alloc(&scan_tmp, scan_bytes);
     L1B_CUDA(cudaMallocHost(&h_starts_pinned, (E_max * per_epoch + 1) * 8));
     L1B_CUDA(cudaMallocHost(&h_flag, 16));
+    L1B_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
     {
       uint64_t w[312];
       mt_seed_state(cfg->seed, w);  // Rng rng = make_rng(cfg.seed) (solvers.cpp:430)
       L1B_CUDA(cudaMemcpyAsync(win, w, sizeof(w), cudaMemcpyHostToDevice, st));
       L1B_CUDA(cudaStreamSynchronize(st));
     }
+    auto new_event = [&]() {
+      cudaEvent_t e;
+      L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+      return e;
+    };
     start();  // x = 0, r = -b, epoch-0 sample: the solve's clock starts here
+    {
+      cudaEvent_t e = new_event();
+      L1B_CUDA(cudaEventRecord(e, st));
+      L1B_CUDA(cudaStreamWaitEvent(gs, e, 0));
+    }
     CdPairArgs a;
     a.n = n;
     a.m = v.m;
@@ -960,8 +979,27 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     a.st = dst;
     a.trace = trace;
     a.partials = part;
+    // stream positions relative to S[cur]: [0, gen_end) drawn (or queued on
+    // gs), the chunk starts at pos; pieces = (end, event) of each launch
     int cur = 0;
-    uint64_t have = 0;  // drawn positions in idx[cur] (position 0 = the chunk's first draw)
+    uint64_t pos = 0, gen_end = 0;
+    std::vector<std::pair<uint64_t, cudaEvent_t>> pieces;
+    auto gen_to = [&](uint64_t upto) {
+      while (gen_end < upto && gen_end + G <= scap) {
+        gen_end += mt_stream_indices(win, G, n, S[cur] + gen_end, words, gs);
+        cudaEvent_t e = new_event();
+        L1B_CUDA(cudaEventRecord(e, gs));
+        pieces.emplace_back(gen_end, e);
+      }
+    };
+    auto wait_for = [&](uint64_t upto) {  // st waits until [0, upto) is drawn
+      for (auto& pc : pieces)
+        if (pc.first >= upto) {
+          L1B_CUDA(cudaStreamWaitEvent(st, pc.second, 0));
+          return;
+        }
+      throw Unsupported("pcdm pairs: stream buffer");
+    };
     while (launched < cfg->max_iters) {
       if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > cfg->max_seconds) {
         time_out = true;
@@ -970,11 +1008,27 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       const uint64_t E = std::min<uint64_t>(E_max, cfg->max_iters - launched);
       const uint64_t nb = E * per_epoch, T = nb * B;
       uint64_t need = T + margin(T);
+      if (pos + need + G > scap) {  // rewind: the undrawn tail moves to the front of the other buffer
+        L1B_CUDA(cudaStreamSynchronize(gs));
+        if (!S[cur ^ 1]) alloc(&S[cur ^ 1], (scap + 312) * 4);
+        L1B_CUDA(cudaMemcpyAsync(S[cur ^ 1], S[cur] + pos, (gen_end - pos) * 4, cudaMemcpyDeviceToDevice, st));
+        L1B_CUDA(cudaStreamSynchronize(st));
+        cur ^= 1;
+        gen_end -= pos;
+        pos = 0;
+        pieces.clear();
+        pieces.emplace_back(gen_end, new_event());
+        L1B_CUDA(cudaEventRecord(pieces.back().second, st));
+      }
+      uint32_t* idx = S[cur] + pos;
+      uint64_t have = 0;
       for (;;) {
-        if (need > cap_raw) throw Unsupported("pcdm pairs: stream buffer");
-        if (have < need) have += mt_stream_indices(win, need - have, n, idx[cur] + have, words, st);
+        if (need > cap_raw) throw Unsupported("pcdm pairs: chunk buffer");
+        gen_to(pos + need + G);  // this chunk's draws and one launch ahead
+        wait_for(pos + need);
+        have = need;
         cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
-            idx[cur], have, W, prevd);
+            idx, have, W, prevd);
         L1B_LAUNCHED();
         const uint64_t tiles = (have + kCandTile - 1) / kCandTile;
         cd_cand_count<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt);
@@ -1010,7 +1064,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
           }
           sb = e;
         }
-        if (short_stream) {  // more redraws than the margin: draw further and walk again
+        if (short_stream) {  // more redraws than the margin: wait for more draws and walk again
           need = have + have / 2;
           continue;
         }
@@ -1020,8 +1074,8 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       }
       L1B_CUDA(cudaMemsetAsync(flag, 0, 4, st));
       L1B_CUDA(cudaMemsetAsync(cnt, 0, E * U * 4, st));
-      cd_scatter_kernel<<<grid_for(T), kThreads, 0, st>>>(idx[cur], prevd, sarr, nb, per_epoch, a.off, U, cnt,
-                                                        ev, flag);
+      cd_scatter_kernel<<<grid_for(T), kThreads, 0, st>>>(idx, prevd, sarr, nb, per_epoch, a.off, U, cnt, ev,
+                                                        flag);
       L1B_LAUNCHED();
       a.epochs = E;
       void* args[] = {&a};
@@ -1039,11 +1093,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
       L1B_CUDA(cudaStreamSynchronize(st));
       if (*h_flag & 4) throw Unsupported("pcdm pairs: event bucket");
-      // the draws past the chunk's last block open the next chunk
-      if (have > used)
-        L1B_CUDA(cudaMemcpyAsync(idx[cur ^ 1], idx[cur] + used, (have - used) * 4, cudaMemcpyDeviceToDevice, st));
-      have -= used;
-      cur ^= 1;
+      pos += used;  // the draws past the chunk's last block open the next chunk
       launched += E;
       if (h_st->stop) break;
     }
@@ -1051,12 +1101,18 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     rc = -1;
   } catch (...) {
     cudaStreamSynchronize(st);
+    if (gs) cudaStreamSynchronize(gs);
+    if (gs) cudaStreamDestroy(gs);
+    for (auto e : evs) cudaEventDestroy(e);
     for (void* q : bufs) cudaFree(q);
     if (h_flag) cudaFreeHost(h_flag);
     if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
     throw;
   }
   cudaStreamSynchronize(st);
+  if (gs) cudaStreamSynchronize(gs);
+  if (gs) cudaStreamDestroy(gs);
+  for (auto e : evs) cudaEventDestroy(e);
   for (void* q : bufs) cudaFree(q);
   if (h_flag) cudaFreeHost(h_flag);
   if (h_starts_pinned) cudaFreeHost(h_starts_pinned);

@@ -35,7 +35,9 @@ def _run(inst, solver, pair, **cfg):
 
 @pytest.mark.parametrize("n,block,solver,epochs", [(4096, 256, "pcdm", 12), (3001, 512, "pcdm", 9),
                                                    (20000, 64, "pcdm", 7), (1000, 1, "cd", 6),
-                                                   (4097, 1, "cd", 3), (65536, 1024, "pcdm", 4)])
+                                                   (4097, 1, "cd", 3), (65536, 1024, "pcdm", 4),
+                                                   (8192, 256, "pcdm", 150),    # three chunks, drawn ahead
+                                                   (65536, 256, "pcdm", 520)])  # > 2^25 draws: a rewind
 def test_pair_epochs_match_direct_epochs(n, block, solver, epochs):
     need_cuda()
     from paper_1503_03520_b200 import l1bench
