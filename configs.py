@@ -92,6 +92,16 @@ def run_gpu(name, c):
         out["time_to_target_s"] = tr.time_to_target
     if tr.iterations:
         out["iters_per_s"] = tr.iterations / max(tr.elapsed_s, 1e-12)
+    if c["solver"] == "pcdm":
+        # the reference's own algorithm on the same instance: serial CD (solvers.cpp:414-482),
+        # bit-exact with the reference, same epoch budget -- the like-for-like rate beside cpu_reference
+        scfg = l1bench.SolverConfig(id="cd", max_iters=c["max_iters"], seed=c.get("solver_seed", 0),
+                                    max_seconds=3600.0)
+        l1bench.run_solver(inst, scfg)
+        trc = l1bench.run_solver(inst, scfg)
+        out["serial_cd"] = {"epochs": trc.iterations, "solve_device_s": trc.elapsed_s,
+                            "epochs_per_s": trc.iterations / max(trc.elapsed_s, 1e-12),
+                            "f_final": trc.final_objective}
     return out
 
 
