@@ -550,6 +550,11 @@ __global__ void __launch_bounds__(kThreads) cd_cand_write(const uint16_t* __rest
   }
 }
 
+__global__ void cd_iota_kernel(uint64_t* s, uint64_t count) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    s[i] = i;
+}
+
 __global__ void cd_scatter_kernel(const uint32_t* __restrict__ idx, const uint16_t* __restrict__ prevd,
                                   const uint64_t* __restrict__ s, uint64_t nb, uint64_t per_epoch,
                                   int off, uint64_t U, uint32_t* cnt, uint32_t* ev, int* flag) {
@@ -900,7 +905,10 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   const uint64_t scap = std::min<uint64_t>(run_draws + margin(run_draws) + 2 * cap_raw, (1ull << 25) + 2 * cap_raw);
   // look-back: a block is B kept draws plus ~B^2 / 2n redraws; W bounds its
   // length (a longer block hands the run to the direct path)
+  // (B = 1, serial CD: a block never redraws; no look-back, only rejected raw
+  // draws become candidates)
   const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
+  const int W_prev = B == 1 ? 0 : W;
   std::vector<void*> bufs;
   auto alloc = [&](auto** ptr, size_t bytes) {
     L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
@@ -1028,7 +1036,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
         wait_for(pos + need);
         have = need;
         cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
-            idx, have, W, prevd);
+            idx, have, W_prev, prevd);
         L1B_LAUNCHED();
         const uint64_t tiles = (have + kCandTile - 1) / kCandTile;
         cd_cand_count<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt);
@@ -1047,6 +1055,16 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
           L1B_CUDA(cudaMemcpyAsync(h_cand.data(), cand, (size_t)ncand * 8, cudaMemcpyDeviceToHost, st));
         L1B_CUDA(cudaStreamSynchronize(st));
         // block starts: a draw is redrawn iff its previous draw lies inside its block
+        if (B == 1 && ncand == 0) {  // serial CD without a rejected draw: block b starts at b
+          if (nb + 1 > have) {
+            need = have + have / 2;
+            continue;
+          }
+          cd_iota_kernel<<<grid_for(nb + 1), kThreads, 0, st>>>(sarr, nb + 1);
+          L1B_LAUNCHED();
+          h_starts_pinned[nb] = nb;
+          break;
+        }
         bool short_stream = false;
         uint64_t sb = 0, j = 0;
         for (uint64_t blk = 0; blk < nb; ++blk) {
