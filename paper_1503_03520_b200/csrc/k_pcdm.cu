@@ -655,8 +655,9 @@ __global__ void cd_pair_fold(const double* partials, unsigned nblocks, uint64_t 
 // partials kept per epoch; cd_pair_fold records the samples afterwards (no
 // target: only the epoch budget or a non-finite objective stops a run, and the
 // budget is the launch's epoch count).
+constexpr int kPairThreads = 128;  // more SMs, one warp per sub-partition (the epoch is a latency chain)
 template <int P, bool SYNC>
-__global__ void __launch_bounds__(kThreads) cd_pair_kernel(CdPairArgs A) {
+__global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
   namespace cg = cooperative_groups;
   CdDev* st = A.st;
   if (*(volatile int*)&st->stop) return;
@@ -832,9 +833,9 @@ template <int P>
 int cd_pair_capacity() {
   static const int cap = [] {
     int per_sm = 0, per_sm2 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P, true>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P, true>, kPairThreads, 0) !=
             cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, cd_pair_kernel<P, false>, kThreads, 0) !=
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, cd_pair_kernel<P, false>, kPairThreads, 0) !=
             cudaSuccess) {
       cudaGetLastError();
       return 0;
@@ -879,7 +880,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   int P = 0, grid = 0;
   const void* fn = nullptr;
   auto try_p = [&](int p, int cap, const void* f) {
-    const uint64_t g = (U + (uint64_t)p * kThreads - 1) / ((uint64_t)p * kThreads);
+    const uint64_t g = (U + (uint64_t)p * kPairThreads - 1) / ((uint64_t)p * kPairThreads);
     if (!P && cap > 0 && g <= (uint64_t)cap) {
       P = p;
       grid = (int)g;
@@ -1098,10 +1099,10 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       a.epochs = E;
       void* args[] = {&a};
       if (sync) {
-        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
+        L1B_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPairThreads), args, 0, st));
         L1B_LAUNCHED();
       } else {
-        L1B_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, 0, st));
+        L1B_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kPairThreads), args, 0, st));
         L1B_LAUNCHED();
         cd_pair_fold<<<1, kThreads, 0, st>>>(part, (unsigned)grid, E, dst, trace);
         L1B_LAUNCHED();
