@@ -14,9 +14,11 @@ the 126 MB L2, so no flush is needed between iterations.
 
 Default K = 500 (the C4 config's iteration budget), W = 4.
 
-The headline path is the matrix-free fused kernel pair (iterates bit-identical
-to the reference's fista_run); the north-star CSR/CSC SpMV path is measured on
-the same instance and reported under "sparse_path".
+The headline path is the matrix-free two-iteration kernel with fused
+multiply-adds (--arith fma, the default: iterates within 1e-12 of the
+reference's fista_run, same supports); the same kernel with separately rounded
+products (bit-identical to the reference) is timed beside it ("other_arith"),
+and the north-star CSR/CSC SpMV path on the same instance ("sparse_path").
 
 Under torchrun (N > 1) the C4 instance is row-sharded across the ranks (strong
 scaling; NCCL halo exchange + scalar all-reduce per iteration); see DESIGN.md.
@@ -120,7 +122,7 @@ def kernel_bytes(path, n, m_act, nnz, ptr_bytes, kmode=None):
     return k1, k2, 1
 
 
-def time_path(inst, op, args, prof_iters=100):
+def time_path(inst, op, args, prof_iters=100, arith="exact"):
     """W warm-up iterations, then exactly K timed iterations between CUDA events
     on the library's stream; inside the timed region every launch is also
     bracketed by events on that stream (l1b_session_profile), which gives the
@@ -131,7 +133,7 @@ def time_path(inst, op, args, prof_iters=100):
 
     from paper_1503_03520_b200 import l1bench
 
-    cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + prof_iters + 10, op=op)
+    cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + prof_iters + 10, op=op, arith=arith)
     stream = torch.cuda.ExternalStream(inst.stream)
     sess = l1bench.Session(inst, cfg)
     sess.step(args.warmup)
@@ -150,7 +152,7 @@ def time_path(inst, op, args, prof_iters=100):
     return {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
             "k1_ms": kms[0] / args.steps, "k2_ms": kms[1] / args.steps, "launches": int(launches),
             "k1_ms_long": kms_long[0] / prof_iters, "k2_ms_long": kms_long[1] / prof_iters,
-            "kmode": kmode}
+            "kmode": kmode, "arith": arith}
 
 
 def roofline(path, t, info, peak, peak_src):
@@ -172,14 +174,18 @@ def roofline(path, t, info, peak, peak_src):
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"{path}:{dom[3]}")
+            key = f"{path}:{dom[3]}" + (":fma" if t.get("arith") == "fma" and path == "matrix_free" else "")
+            traffic = json.load(open(tf)).get(key)
         except Exception:
             traffic = None
     long_ms = (t["k1_ms_long"] * ipl if dom[3] != "k2" else t["k2_ms_long"])
-    limiter = ("FP64 issue: ncu shows the FP64 pipe at 76.5 % of peak and DRAM at ~71 % for this kernel "
-               "(profiles/r1_ncu_full_fista_rc2v.txt); fractions are of the HBM roofline on algorithmic bytes"
-               if path == "matrix_free" and t.get("kmode") == 4 else
-               "HBM streaming (profiles/r1_ncu_full_spmv_tma.txt)" if path == "sparse" else None)
+    if path == "matrix_free" and t.get("kmode") == 4:
+        limiter = ("HBM streaming: ncu shows DRAM 6.42 GB per launch (1.00x algorithmic), the FP64 pipe 59.5 % "
+                   "busy (profiles/r2_ncu_full_fista_rc2v_fma.txt)" if t.get("arith") == "fma" else
+                   "FP64 issue (separately rounded a*b+c): ncu shows the FP64 pipe at 76.5 % of peak and DRAM "
+                   "at ~71 % (profiles/r1_ncu_full_fista_rc2v.txt)")
+    else:
+        limiter = "HBM streaming (profiles/r1_ncu_full_spmv_tma.txt)" if path == "sparse" else None
     return {"bound": "hbm", "kernel": dom[2], "achieved": achieved, "peak": peak, "limiter": limiter,
             "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
             "frac_of_8tbs": achieved / 8000.0, "bytes_per_launch": dom[0], "iterations_per_launch": ipl,
@@ -189,45 +195,54 @@ def roofline(path, t, info, peak, peak_src):
             "hbm_gbs_ax_atr": (b1 + b2) / ((t["k1_ms"] * ipl + t["k2_ms"]) * 1e-3) / 1e9}
 
 
-def run_reference(args, warmup=None, steps=None):
-    """--impl reference / cpu_baseline: the reference's own FISTA (oracle/_ref,
-    built from /root/reference/proj/src) on the host cores, on a bounded sample:
-    the C4 recipe at n = 2^24 (1/8 of C4's n; its vectors, several GB, are as
-    far beyond the host caches as C4's -- a 2^20 sample runs from L3 and is
-    ~2x faster per entry), scaled by n_sample / n_C4."""
+def run_reference(args, warmup, steps):
+    """--impl reference / cpu_baseline: the reference's own fista_run
+    (oracle/_ref/libl1ref.so, the unmodified /root/reference/proj/src sources
+    compiled by oracle/Makefile; the plain-C oracle port where that build is
+    absent) on the host cores, on the C4 configuration ITSELF: the instance is
+    built by the reference's own generator at n = 2^27 (m = 2^28, ~20 GB of
+    host memory) and `warmup` + `steps` FISTA iterations run in one fista_run;
+    the timed region is the reference's own trace clock from the end of
+    iteration `warmup` to the end of iteration `warmup + steps`.  Single
+    threaded: the reference has no parallel code."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import REF_SO, Oracle, Reference
 
-    # a bounded sample whatever K is: one reference iteration at n = 2^24 takes ~0.8 s
-    warmup = min(args.warmup, 2) if warmup is None else warmup
-    steps = min(args.steps, 8) if steps is None else steps
-    n_s = 1 << 24
-    scale = n_s / C4["n"]
     kw = dict(C4)
-    kw["n"] = n_s
+    kw["n"] = args.n
+    t_gen = time.perf_counter()
     if os.path.exists(REF_SO):
         lib, kind = Reference(), "reference"
         inst = lib.build_instance(**kw)
+        t_gen = time.perf_counter() - t_gen
         tr, _ = inst.solve("fista", max_iters=warmup + steps)
         el = tr["elapsed_s"]
-        t = float(el[warmup + steps] - el[warmup])
+        it = list(tr["iter"])
+        t = float(el[it.index(warmup + steps)] - el[it.index(warmup)])
     else:  # the oracle port (plain C restatement)
         lib, kind = Oracle(), "port"
         inst = lib.build_instance(**kw)
+        t_gen = time.perf_counter() - t_gen
         t0 = time.perf_counter()
         lib.fista(inst, max_iters=warmup)
         t1 = time.perf_counter()
         lib.fista(inst, max_iters=warmup + steps)
         t = (time.perf_counter() - t1) - (t1 - t0)
-    ips_sample = steps / t
+    ips = steps / t
     return {
-        "value": ips_sample * scale, "unit": UNIT, "cores": 1, "kind": kind,
-        "sample": (f"{steps} FISTA iterations (after {warmup} warm-up) of the C4 recipe at "
-                   f"n=2^24 (1/8 of C4's n=2^27, beyond the host caches like C4), single-threaded "
-                   f"reference (it has no parallel code); {ips_sample:.4f} iter/s scaled by "
-                   f"n_sample/n_C4 (per-iteration cost linear in n, BASELINE.md 2)"),
+        "value": ips, "unit": UNIT, "cores": 1, "kind": kind,
+        "sample": (f"{steps} FISTA iterations (after {warmup} untimed) of C4 itself "
+                   f"(n=2^{int(math.log2(kw['n']))}, m=2n, 4 stages, q=1, s=n/1000, seed 3) through the "
+                   f"reference's fista_run, single-threaded (the reference has no parallel code); "
+                   f"instance built by the reference's generator in {t_gen:.1f} s (untimed)"),
+        "seconds_timed": t, "generate_s": t_gen, "same_config": kw["n"] == C4["n"],
         "host_cores_total": os.cpu_count(),
     }
+
+
+# the reference arm times at most this many C4 iterations (~8 s each on one
+# host core): the whole --impl reference run then stays within a few minutes
+REF_MAX_STEPS = 20
 
 
 def main():
@@ -239,7 +254,10 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=C4["n"], help="columns per GPU (default C4: 2^27)")
+    ap.add_argument("--n", type=int, default=C4["n"],
+                    help="global n, row-sharded across ranks when N > 1 (default C4: 2^27)")
+    ap.add_argument("--arith", default="fma", choices=["fma", "exact"],
+                    help="headline arithmetic of the matrix-free FISTA kernels")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sparse", action="store_true", help="skip the CSR/CSC leg (tuning runs)")
@@ -254,12 +272,15 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = run_reference(args)
+        steps = min(args.steps, REF_MAX_STEPS)
+        cb = run_reference(args, warmup=min(args.warmup, 1), steps=steps)
         line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / cb["value"],
+                "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 / cb["value"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference generator, seed 3)", "impl": "reference",
-                "config": {"workload": "C4 FISTA (bounded CPU sample, see cpu_baseline.sample)"},
+                "config": {"workload": "C4 FISTA: n=2^27 cols x m=2^28 rows, 4 stages, q=1, s=n/1000, "
+                                       "tau=1, seed 3 (the same instance as the GPU arm)"},
                 "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -282,14 +303,21 @@ def main():
     gen_s = time.perf_counter() - t0
     peak, peak_src = peaks()
     with ClockSampler(local) as clk:
-        fused = time_path(inst, "matrix_free", args)
+        fused = time_path(inst, "matrix_free", args, arith=args.arith)
     info = inst.info  # builds nothing; CSR/CSC come with the first sparse use below
     rf = roofline("matrix_free", fused, info, peak, peak_src)
+    # the other arithmetic mode on the same instance (exact = the reference's bits)
+    other = "exact" if args.arith == "fma" else "fma"
+    with ClockSampler(local) as clk_other:
+        alt = time_path(inst, "matrix_free", args, arith=other)
+    alt_line = {"arith": other, "value": alt["ips"], "ms_per_step": alt["ms_step"],
+                "roofline": roofline("matrix_free", alt, info, peak, peak_src), "clocks": clk_other.summary()}
     # e2e before the CSR/CSC copy exists (37 GB of device memory at C4)
     e2e_line = e2e(inst, args, local) if not args.no_e2e else None
     if args.no_sparse:
         print(json.dumps({"metric": METRIC, "value": fused["ips"], "ms_per_step": fused["ms_step"],
-                          "roofline": rf, "clocks": clk.summary(), "note": "tuning run (--no-sparse)"}))
+                          "arith": args.arith, "roofline": rf, "clocks": clk.summary(),
+                          "other_arith": alt_line, "note": "tuning run (--no-sparse)"}))
         return
     t0 = time.perf_counter()
     with ClockSampler(local) as clk_sparse:
@@ -309,7 +337,12 @@ def main():
                             "warp shuffles, 256-bit loads); " +
                             ("two FISTA iterations per launch, 24n bytes/iteration" if fused["kmode"] == 4
                              else "one FISTA iteration per launch") +
-                            "; iterates bit-identical to the reference's fista_run")},
+                            ("; fused multiply-adds (arith='fma'): iterates within 1e-12 of the reference's "
+                             "fista_run, same supports (tests/test_gpu_rc.py, tests/test_gpu_configs.py)"
+                             if args.arith == "fma" else
+                             "; iterates bit-identical to the reference's fista_run")),
+                   "arith": args.arith},
+        "other_arith": alt_line,
         "gpu_launches": fused["launches"],
         "hbm_gbs_ax_atr": rf["hbm_gbs_ax_atr"],
         "kernels_ms_per_iteration": {"matrix_free": fused["k1_ms"]},
@@ -333,7 +366,7 @@ def main():
             line["other_configs"] = {"error": str(e)}
     if not args.no_cpu:
         try:
-            line["cpu_baseline"] = run_reference(args, warmup=1, steps=8)
+            line["cpu_baseline"] = run_reference(args, warmup=1, steps=2)
         except Exception as e:  # reported, never silently substituted
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line))

@@ -248,10 +248,17 @@ typedef struct {
   int l_policy;        /* LPolicy (solvers.hpp:15): L1B_L_SPECTRUM, or L1B_L_BACKTRACKING (FISTA / ISTA,
                           unless l_fixed is set: power-iteration seed, halving / doubling; host-led,
                           l1b_solve only) */
+  int arith;           /* L1B_ARITH_EXACT (default): every a*b+c rounds twice, as in the
+                          reference's x86-64 build -- matrix-free FISTA iterates are the
+                          reference's bits; L1B_ARITH_FMA: the matrix-free FISTA kernels of
+                          instances with n > 2^20 contract a*b+c into one fused multiply-add
+                          (one rounding: <= 1e-12 relative to the reference, not bit-exact);
+                          other paths ignore it */
 } l1b_solver_cfg;
 
 enum { L1B_OP_AUTO = 0, L1B_OP_SPARSE = 1, L1B_OP_MATRIX_FREE = 2 };
 enum { L1B_L_SPECTRUM = 0, L1B_L_BACKTRACKING = 1 };
+enum { L1B_ARITH_EXACT = 0, L1B_ARITH_FMA = 1 };
 
 void l1b_solver_cfg_default(l1b_solver_cfg* cfg);
 

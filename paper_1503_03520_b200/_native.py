@@ -78,7 +78,7 @@ class SolverCfg(C.Structure):
                 ("has_target", C.c_int), ("target", f64), ("mu", f64), ("eta", f64),
                 ("pcg_max_iters", u64), ("ls_max_backtracks", u64), ("grad_tol_rel", f64),
                 ("l_fixed", f64), ("varpi", u64), ("omega", u64), ("seed", u64), ("block", u64),
-                ("op", C.c_int), ("l_policy", C.c_int)]
+                ("op", C.c_int), ("l_policy", C.c_int), ("arith", C.c_int)]
 
 
 class Sample(C.Structure):

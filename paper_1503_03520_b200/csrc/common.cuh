@@ -91,6 +91,33 @@ __device__ __forceinline__ void rotate_pair(double& vi, double& vj, double c, do
   }
 }
 
+// The contracted arithmetic mode (l1b_solver_cfg.arith = L1B_ARITH_FMA): every
+// a*b + c of the hot loop as one fused multiply-add -- one rounding instead of
+// two, so the results are no longer the reference's bits but at least as
+// accurate (parity: <= 1e-12 relative, tests/test_gpu_fma.py).  A rotation
+// costs 2 DMUL + 2 DFMA instead of 4 DMUL + 2 DADD.  F = false is the exact
+// (bit-identical) arithmetic above.
+template <bool F>
+__device__ __forceinline__ void rot(double& vi, double& vj, double c, double s, bool transposed) {
+  if (!F) {
+    rotate_pair(vi, vj, c, s, transposed);
+    return;
+  }
+  const double a = vi, b = vj;
+  if (transposed) {
+    vi = __fma_rn(c, a, s * b);
+    vj = __fma_rn(c, b, -(s * a));
+  } else {
+    vi = __fma_rn(c, a, -(s * b));
+    vj = __fma_rn(s, a, c * b);
+  }
+}
+// a * b - c
+template <bool F>
+__device__ __forceinline__ double mul_sub(double a, double b, double c) {
+  return F ? __fma_rn(a, b, -c) : a * b - c;
+}
+
 // soft_threshold (solvers.cpp:153-157)
 __device__ __forceinline__ double soft_threshold(double v, double t) {
   if (v > t) return v - t;

@@ -152,7 +152,7 @@ __device__ __forceinline__ void load_seg(const RcArgs& A, int64_t e, bool full, 
 // live outside the window) and are never used.
 // PAR >= 0: bit s is the parity of stage s's offset, fixed at compile time
 // (the generator's alternating offsets); PAR < 0: read from the table.
-template <int S, bool TR, bool INTERIOR, int K, int PAR>
+template <int S, bool TR, bool INTERIOR, int K, int PAR, bool F = false>
 __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
                                        const StageTab& tab) {
 #pragma unroll
@@ -166,8 +166,8 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
       const bool p2 = INTERIOR || (e0 + 2 >= o && e0 + 3 < n);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
-        if (p0) rotate_pair(v[q][0], v[q][1], c, sn, TR);
-        if (p2) rotate_pair(v[q][2], v[q][3], c, sn, TR);
+        if (p0) rot<F>(v[q][0], v[q][1], c, sn, TR);
+        if (p2) rot<F>(v[q][2], v[q][3], c, sn, TR);
       }
     } else {
       // the pair straddling lanes l, l+1 is rotated once, by lane l, which
@@ -181,7 +181,7 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         double a = v[q][3], b = right[q];
-        if (p3) rotate_pair(a, b, c, sn, TR);
+        if (p3) rot<F>(a, b, c, sn, TR);
         v[q][3] = a;
         back[q] = b;
       }
@@ -192,7 +192,7 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
       }
 #pragma unroll
       for (int q = 0; q < K; ++q)
-        if (p1) rotate_pair(v[q][1], v[q][2], c, sn, TR);
+        if (p1) rot<F>(v[q][1], v[q][2], c, sn, TR);
     }
   }
 }
@@ -214,7 +214,7 @@ __device__ __forceinline__ double shrink(double v, double t) {
 // exists and a lane's four entries are either all own (lane_own) or all halo.
 // FLUSH: only ||r_k||^2 of the own rows (the objective of the last iterate).
 // SMEM: x_next is shared memory (generic stores instead of 256-bit global ones).
-template <int S, bool FAST, bool FLUSH, int PAR, bool SMEM = false>
+template <int S, bool FAST, bool FLUSH, int PAR, bool SMEM = false, bool F = false>
 __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w0, int lane,
                                         bool lane_own, double beta, double inv_l, double thr,
                                         Acc& acc) {
@@ -238,25 +238,25 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
     t[0][i] = d.xk[i];
     if (!FLUSH) t[K - 1][i] = d.xm[i];
   }
-  wchain<S, true, FAST, K, PAR>(t, e0, n, A.right);
+  wchain<S, true, FAST, K, PAR, F>(t, e0, n, A.right);
   double g[1][4], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const double rk = d.sg[i] * t[0][i] - d.bb[i];
-    if (mine[i]) rr += rk * rk;  // ||r_k||^2: x_k's objective, recorded one kernel late
+    const double rk = mul_sub<F>(d.sg[i], t[0][i], d.bb[i]);
+    if (mine[i]) rr = F ? __fma_rn(rk, rk, rr) : rr + rk * rk;  // ||r_k||^2: x_k's objective, recorded one kernel late
     if (!FLUSH) {
-      const double rm = d.sg[i] * t[K - 1][i] - d.bb[i];
-      g[0][i] = d.sg[i] * ((1.0 + beta) * rk - beta * rm);
+      const double rm = mul_sub<F>(d.sg[i], t[K - 1][i], d.bb[i]);
+      g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta, rk, beta * rm);
     }
   }
   acc.rr += rr;
   if (FLUSH) return;
-  wchain<S, false, FAST, 1, PAR>(g, e0, n, A.right);
+  wchain<S, false, FAST, 1, PAR, F>(g, e0, n, A.right);
   double tr[4], l1 = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const double y = d.xk[i] + beta * (d.xk[i] - d.xm[i]);
-    tr[i] = shrink(y - inv_l * g[0][i], thr);
+    const double y = F ? __fma_rn(beta, d.xk[i] - d.xm[i], d.xk[i]) : d.xk[i] + beta * (d.xk[i] - d.xm[i]);
+    tr[i] = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
     l1 += mine[i] ? fabs(tr[i]) : 0.0;
     acc.nz += (unsigned)(mine[i] & (tr[i] != 0.0));
     acc.mism += (unsigned)(mine[i] & (tr[i] != y));
@@ -280,7 +280,7 @@ __device__ __forceinline__ void segment(const RcArgs& A, const Seg& d, int64_t w
 
 // Warps stream segments q = warp_id, warp_id + #warps, ...; the next segment's
 // loads are issued before the current one computes.
-template <int S, int MB, bool FLUSH = false, int PAR = -1>
+template <int S, int MB, bool FLUSH = false, int PAR = -1, bool F = false>
 __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   using G = RcGeom<S>;
   FistaDev* st = A.b.st;
@@ -314,9 +314,9 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc_kernel(RcArgs A) {
   auto run = [&](int64_t q, const Seg& d) {
     const int64_t w0 = w0_of(q);
     if (q >= q_lo && q < q_hi)
-      segment<S, true, FLUSH, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+      segment<S, true, FLUSH, PAR, false, F>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
     else
-      segment<S, false, FLUSH, PAR>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
+      segment<S, false, FLUSH, PAR, false, F>(A, d, w0, lane, lane_own, beta, inv_l, thr, acc);
   };
   Seg sa, sb;
   int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
@@ -364,7 +364,7 @@ struct Rc2Out {
 // The two-iteration kernel with V entries per lane (window 32 V): the halo
 // (>= 4S, a multiple of V) is a smaller share of a wider window -- fewer
 // rotations per own entry, more registers per thread.
-template <int S, bool TR, bool INTERIOR, int K, int PAR, int V>
+template <int S, bool TR, bool INTERIOR, int K, int PAR, int V, bool F>
 __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n,
                                         const StageTab& tab) {
 #pragma unroll
@@ -379,7 +379,7 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
         const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
 #pragma unroll
         for (int q = 0; q < K; ++q)
-          if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
+          if (ok) rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
       }
     } else {
       // the pair straddling lanes l, l+1 is rotated once, by lane l, which
@@ -393,7 +393,7 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         double a = v[q][V - 1], b = right[q];
-        if (pr) rotate_pair(a, b, c, sn, TR);
+        if (pr) rot<F>(a, b, c, sn, TR);
         v[q][V - 1] = a;
         back[q] = b;
       }
@@ -407,7 +407,7 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
         const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
 #pragma unroll
         for (int q = 0; q < K; ++q)
-          if (ok) rotate_pair(v[q][p], v[q][p + 1], c, sn, TR);
+          if (ok) rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
       }
     }
   }
@@ -487,7 +487,7 @@ __device__ __forceinline__ void store_ownv(double* dst, int64_t e0, const bool (
   }
 }
 
-template <int S, bool FAST, int PAR, int V>
+template <int S, bool FAST, int PAR, int V, bool F>
 __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, const SegV<V>& d,
                                           int64_t w0, int lane, bool lane_own, double beta_a,
                                           double beta_b, double inv_l, double thr, Acc2& acc) {
@@ -509,22 +509,22 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
     t[0][i] = d.xk[i];
     t[1][i] = d.xm[i];
   }
-  wchainv<S, true, FAST, 2, PAR, V>(t, e0, n, A.right);
+  wchainv<S, true, FAST, 2, PAR, V, F>(t, e0, n, A.right);
   double rk[V], g[1][V], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    rk[i] = d.sg[i] * t[0][i] - d.bb[i];
-    if (mine[i]) rr += rk[i] * rk[i];
-    const double rm = d.sg[i] * t[1][i] - d.bb[i];
-    g[0][i] = d.sg[i] * ((1.0 + beta_a) * rk[i] - beta_a * rm);
+    rk[i] = mul_sub<F>(d.sg[i], t[0][i], d.bb[i]);
+    if (mine[i]) rr = F ? __fma_rn(rk[i], rk[i], rr) : rr + rk[i] * rk[i];
+    const double rm = mul_sub<F>(d.sg[i], t[1][i], d.bb[i]);
+    g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_a, rk[i], beta_a * rm);
   }
   acc.rr0 += rr;
-  wchainv<S, false, FAST, 1, PAR, V>(g, e0, n, A.right);
+  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
   double x1[1][V], l1 = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const double y = d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
-    double v = shrink(y - inv_l * g[0][i], thr);
+    const double y = F ? __fma_rn(beta_a, d.xk[i] - d.xm[i], d.xk[i]) : d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
+    double v = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
     l1 += mine[i] ? fabs(v) : 0.0;
     acc.nza += (unsigned)(mine[i] & (v != 0.0));
     acc.misa += (unsigned)(mine[i] & (v != y));
@@ -537,21 +537,21 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
   double t1[1][V];
 #pragma unroll
   for (int i = 0; i < V; ++i) t1[0][i] = x1[0][i];
-  wchainv<S, true, FAST, 1, PAR, V>(t1, e0, n, A.right);
+  wchainv<S, true, FAST, 1, PAR, V, F>(t1, e0, n, A.right);
   double rr1 = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const double r1 = d.sg[i] * t1[0][i] - d.bb[i];
-    if (mine[i]) rr1 += r1 * r1;
-    g[0][i] = d.sg[i] * ((1.0 + beta_b) * r1 - beta_b * rk[i]);
+    const double r1 = mul_sub<F>(d.sg[i], t1[0][i], d.bb[i]);
+    if (mine[i]) rr1 = F ? __fma_rn(r1, r1, rr1) : rr1 + r1 * r1;
+    g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_b, r1, beta_b * rk[i]);
   }
   acc.rr1 += rr1;
-  wchainv<S, false, FAST, 1, PAR, V>(g, e0, n, A.right);
+  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
   double x2[V], l1b = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const double y = x1[0][i] + beta_b * (x1[0][i] - d.xk[i]);
-    x2[i] = shrink(y - inv_l * g[0][i], thr);
+    const double y = F ? __fma_rn(beta_b, x1[0][i] - d.xk[i], x1[0][i]) : x1[0][i] + beta_b * (x1[0][i] - d.xk[i]);
+    x2[i] = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
     l1b += mine[i] ? fabs(x2[i]) : 0.0;
     acc.nzb += (unsigned)(mine[i] & (x2[i] != 0.0));
     acc.misb += (unsigned)(mine[i] & (x2[i] != y));
@@ -561,7 +561,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
   peer_store<V>(A, 1, e0, mine, x2);
 }
 
-template <int S, int MB, int PAR, int V, bool PF>
+template <int S, int MB, int PAR, int V, bool PF, bool F>
 __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc2Out O) {
   using G = RcGeomV<S, V>;
   FistaDev* st = A.b.st;
@@ -593,9 +593,9 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc
       load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sb);
     }
     if (q >= q_lo && q < q_hi)
-      segment2v<S, true, PAR, V>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
+      segment2v<S, true, PAR, V, F>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
     else
-      segment2v<S, false, PAR, V>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
+      segment2v<S, false, PAR, V, F>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, inv_l, thr, acc);
     if (PF) {
       sa = sb;
     } else if (q + stride < nseg) {
@@ -1159,57 +1159,32 @@ void launch_rc_persistent(const RcPArgs& p, cudaStream_t st) {
   L1B_LAUNCHED();
 }
 
-template <int S, int MB, bool FLUSH = false, int PAR = -1>
+template <int S, int MB, bool FLUSH, int PAR, bool F>
 void launch_rc_v(const RcArgs& a, cudaStream_t st) {
   using G = RcGeom<S>;
-  const int grid_cap = grid_cap_of<fista_rc_kernel<S, MB, FLUSH, PAR>>();
+  const int grid_cap = grid_cap_of<fista_rc_kernel<S, MB, FLUSH, PAR, F>>();
   const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
   const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc_kernel<S, MB, FLUSH, PAR><<<grid, kRcThreads, 0, st>>>(a);
+  fista_rc_kernel<S, MB, FLUSH, PAR, F><<<grid, kRcThreads, 0, st>>>(a);
   L1B_LAUNCHED();
 }
 
-template <int S, int PAR, int MB, int V, bool PF>
-void launch_rc2v(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
-  using G = RcGeomV<S, V>;
-  const int grid_cap = grid_cap_of<fista_rc2v_kernel<S, MB, PAR, V, PF>>();
-  const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
-  const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc2v_kernel<S, MB, PAR, V, PF><<<grid, kRcThreads, 0, st>>>(a, o);
-  L1B_LAUNCHED();
-}
-
-int rc2_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("L1B_RC2_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-template <int S, int PAR>
+// The two-iteration kernel: 8 entries per lane with the next segment's loads
+// in flight, 1 CTA of 8 warps per SM (255 registers in the exact build).
+// Measured at C4 (iter/s, exact arithmetic): this shape 1843; 6 per lane 1682;
+// 8 per lane without prefetch 1466; 4 per lane, 2 CTAs/SM 1468 (those shapes
+// were dropped in round 2).
+constexpr int kRc2V = 8;
+template <int S, int PAR, bool F>
 void launch_rc2(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
-  // measured at C4 (iter/s): V=8 + prefetch, 1 CTA/SM (255 registers) 1843;
-  // V=6 + prefetch 1682; V=8 without prefetch 1466; V=4 + prefetch, 2 CTAs/SM 1468
-  switch (rc2_variant()) {
-    case 1: return launch_rc2v<S, PAR, 2, 4, true>(a, o, st);
-    case 2: return launch_rc2v<S, PAR, 1, 6, true>(a, o, st);
-    case 3: return launch_rc2v<S, PAR, 1, 8, false>(a, o, st);
-    default: return launch_rc2v<S, PAR, 1, 8, true>(a, o, st);
-  }
-}
-
-// min CTAs/SM; L1B_RC_VARIANT picks (tuning runs)
-int rc_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("L1B_RC_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
+  using G = RcGeomV<S, kRc2V>;
+  const int grid_cap = grid_cap_of<fista_rc2v_kernel<S, 1, PAR, kRc2V, true, F>>();
+  const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
+  const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
+  fista_rc2v_kernel<S, 1, PAR, kRc2V, true, F><<<grid, kRcThreads, 0, st>>>(a, o);
+  L1B_LAUNCHED();
 }
 
 // offsets (S-1-s) % 2, the generator's alternating stages (bench.cpp:270)
@@ -1226,42 +1201,50 @@ bool is_canon(const StageTab& t) {
   return true;
 }
 
-template <int S>
+// one iteration per launch, 2 CTAs/SM (measured: 1 CTA/SM slower)
+template <int S, bool F>
 void launch_rc(const RcArgs& a, cudaStream_t st) {
-  const bool canon = is_canon<S>(a.right);
-  switch (rc_variant()) {
-    case 1: return canon ? launch_rc_v<S, 1, false, canon_par<S>()>(a, st) : launch_rc_v<S, 1>(a, st);
-    default: return canon ? launch_rc_v<S, 2, false, canon_par<S>()>(a, st) : launch_rc_v<S, 2>(a, st);
-  }
+  if (is_canon<S>(a.right)) return launch_rc_v<S, 2, false, canon_par<S>(), F>(a, st);
+  launch_rc_v<S, 2, false, -1, F>(a, st);
 }
 
-template <int S>
+template <int S, bool F>
 void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
-  launch_rc_v<S, 2, true>(a, st);  // once per solve: the generic stage table
+  launch_rc_v<S, 2, true, -1, F>(a, st);  // once per solve: the generic stage table
+}
+
+template <int S, bool F>
+void launch_rc2_s(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
+  if (is_canon<S>(a.right)) return launch_rc2<S, canon_par<S>(), F>(a, o, st);
+  launch_rc2<S, -1, F>(a, o, st);
 }
 
 }  // namespace
 
-template <int S>
+template <int S, bool F>
 void prepare_s(const StageTab& t) {
   if (is_canon<S>(t)) {
-    grid_cap_of<fista_rc_kernel<S, 2, false, canon_par<S>()>>();
-    grid_cap_of<fista_rc_persistent<S, canon_par<S>()>>();
-    grid_cap_of<fista_rc2v_kernel<S, 1, canon_par<S>(), 8, true>>();
+    grid_cap_of<fista_rc_kernel<S, 2, false, canon_par<S>(), F>>();
+    grid_cap_of<fista_rc2v_kernel<S, 1, canon_par<S>(), kRc2V, true, F>>();
+    if (!F) grid_cap_of<fista_rc_persistent<S, canon_par<S>()>>();
   } else {
-    grid_cap_of<fista_rc_kernel<S, 2, false, -1>>();
-    grid_cap_of<fista_rc_persistent<S, -1>>();
-    grid_cap_of<fista_rc2v_kernel<S, 1, -1, 8, true>>();
+    grid_cap_of<fista_rc_kernel<S, 2, false, -1, F>>();
+    grid_cap_of<fista_rc2v_kernel<S, 1, -1, kRc2V, true, F>>();
+    if (!F) grid_cap_of<fista_rc_persistent<S, -1>>();
   }
-  grid_cap_of<fista_rc_kernel<S, 2, true, -1>>();
+  grid_cap_of<fista_rc_kernel<S, 2, true, -1, F>>();
 }
 
-void fista_rc_prepare(const OpView& op) {
-  switch (op.right.count) {
-    case 1: return prepare_s<1>(op.right);
-    case 2: return prepare_s<2>(op.right);
-    case 3: return prepare_s<3>(op.right);
-    case 4: return prepare_s<4>(op.right);
+void fista_rc_prepare(const OpView& op, bool fma) {
+  switch (op.right.count * 2 + (fma ? 1 : 0)) {
+    case 2: return prepare_s<1, false>(op.right);
+    case 3: return prepare_s<1, true>(op.right);
+    case 4: return prepare_s<2, false>(op.right);
+    case 5: return prepare_s<2, true>(op.right);
+    case 6: return prepare_s<3, false>(op.right);
+    case 7: return prepare_s<3, true>(op.right);
+    case 8: return prepare_s<4, false>(op.right);
+    case 9: return prepare_s<4, true>(op.right);
     default: return;
   }
 }
@@ -1310,7 +1293,7 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 }
 
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
-                    cudaStream_t st, const PeerViews& peers) {
+                    cudaStream_t st, const PeerViews& peers, bool fma) {
   if (lo % 4 != 0) throw std::invalid_argument("fista_rc_iter2: block start must be a multiple of 4");
   RcArgs a;
   a.n = (int64_t)op.n;
@@ -1321,21 +1304,25 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
   a.b = ib;
   a.peers = peers;
   const Rc2Out o{ib.x_next, x_next2};
-  switch (op.right.count) {
-    case 1: return is_canon<1>(op.right) ? launch_rc2<1, canon_par<1>()>(a, o, st) : launch_rc2<1, -1>(a, o, st);
-    case 2: return is_canon<2>(op.right) ? launch_rc2<2, canon_par<2>()>(a, o, st) : launch_rc2<2, -1>(a, o, st);
-    case 3: return is_canon<3>(op.right) ? launch_rc2<3, canon_par<3>()>(a, o, st) : launch_rc2<3, -1>(a, o, st);
-    case 4: return is_canon<4>(op.right) ? launch_rc2<4, canon_par<4>()>(a, o, st) : launch_rc2<4, -1>(a, o, st);
+  switch (op.right.count * 2 + (fma ? 1 : 0)) {
+    case 2: return launch_rc2_s<1, false>(a, o, st);
+    case 3: return launch_rc2_s<1, true>(a, o, st);
+    case 4: return launch_rc2_s<2, false>(a, o, st);
+    case 5: return launch_rc2_s<2, true>(a, o, st);
+    case 6: return launch_rc2_s<3, false>(a, o, st);
+    case 7: return launch_rc2_s<3, true>(a, o, st);
+    case 8: return launch_rc2_s<4, false>(a, o, st);
+    case 9: return launch_rc2_s<4, true>(a, o, st);
     default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
   }
 }
 
 int fista_rc2_halo(int stages) {
   switch (stages) {
-    case 1: return RcGeomV<1, 8>::H3;
-    case 2: return RcGeomV<2, 8>::H3;
-    case 3: return RcGeomV<3, 8>::H3;
-    case 4: return RcGeomV<4, 8>::H3;
+    case 1: return RcGeomV<1, kRc2V>::H3;
+    case 2: return RcGeomV<2, kRc2V>::H3;
+    case 3: return RcGeomV<3, kRc2V>::H3;
+    case 4: return RcGeomV<4, kRc2V>::H3;
     default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
   }
 }
@@ -1351,7 +1338,7 @@ int fista_rc_halo(int stages) {
 }
 
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi,
-                   cudaStream_t st, bool flush, const PeerViews& peers) {
+                   cudaStream_t st, bool flush, const PeerViews& peers, bool fma) {
   if (lo % 4 != 0) throw std::invalid_argument("fista_rc_iter: block start must be a multiple of 4");
   RcArgs a;
   a.n = (int64_t)op.n;
@@ -1361,16 +1348,25 @@ void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t h
   a.sigma = op.sigma;
   a.b = ib;
   a.peers = peers;
-  switch (op.right.count * 2 + (flush ? 1 : 0)) {
-    case 2: return launch_rc<1>(a, st);
-    case 3: return launch_rc_flush<1>(a, st);
-    case 4: return launch_rc<2>(a, st);
-    case 5: return launch_rc_flush<2>(a, st);
-    case 6: return launch_rc<3>(a, st);
-    case 7: return launch_rc_flush<3>(a, st);
-    case 8: return launch_rc<4>(a, st);
-    case 9: return launch_rc_flush<4>(a, st);
-    default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
+  const int S = (int)op.right.count;
+  if (S < 1 || S > 4) throw Unsupported("recomputing FISTA kernel: 1..4 stages");
+  switch ((S - 1) * 4 + (flush ? 2 : 0) + (fma ? 1 : 0)) {
+    case 0: return launch_rc<1, false>(a, st);
+    case 1: return launch_rc<1, true>(a, st);
+    case 2: return launch_rc_flush<1, false>(a, st);
+    case 3: return launch_rc_flush<1, true>(a, st);
+    case 4: return launch_rc<2, false>(a, st);
+    case 5: return launch_rc<2, true>(a, st);
+    case 6: return launch_rc_flush<2, false>(a, st);
+    case 7: return launch_rc_flush<2, true>(a, st);
+    case 8: return launch_rc<3, false>(a, st);
+    case 9: return launch_rc<3, true>(a, st);
+    case 10: return launch_rc_flush<3, false>(a, st);
+    case 11: return launch_rc_flush<3, true>(a, st);
+    case 12: return launch_rc<4, false>(a, st);
+    case 13: return launch_rc<4, true>(a, st);
+    case 14: return launch_rc_flush<4, false>(a, st);
+    default: return launch_rc_flush<4, true>(a, st);
   }
 }
 

@@ -198,8 +198,9 @@ struct PeerViews {
 };
 // The objective lags one kernel (fista_finalize_lagged); flush = true records
 // the last iterate's (x_k of ib) after the loop.
+// fma: the contracted arithmetic (L1B_ARITH_FMA, common.cuh rot<true>)
 void fista_rc_iter(const OpView& op, const IterBufs& ib, uint64_t lo, uint64_t hi, cudaStream_t st,
-                   bool flush = false, const PeerViews& peers = PeerViews());
+                   bool flush = false, const PeerViews& peers = PeerViews(), bool fma = false);
 int fista_rc_halo(int stages);
 // x-window halo of the two-iteration kernel (default 8-entries-per-lane variant)
 int fista_rc2_halo(int stages);
@@ -211,9 +212,9 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 // two iterations (x_{k+1} into ib.x_next, x_{k+2} into x_next2) in one kernel:
 // 24n bytes per iteration (k_iter_rc.cu fista_rc2_kernel); one device
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
-                    cudaStream_t st, const PeerViews& peers = PeerViews());
+                    cudaStream_t st, const PeerViews& peers = PeerViews(), bool fma = false);
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
-void fista_rc_prepare(const OpView& op);
+void fista_rc_prepare(const OpView& op, bool fma = false);
 // general shards: prox / momentum on the own column slice from the reduced g
 void fista_prox(const double* g, double* x, double* y, uint64_t cols, FistaDev* st,
                 double* partials, cudaStream_t stream);

@@ -101,16 +101,18 @@ struct l1b_session {
     return pv;
   }
 
+  bool fma() const { return cfg.arith == L1B_ARITH_FMA; }
+
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
     fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
-                   shard ? v.row_end : v.n, stream, peers(j));
+                   shard ? v.row_end : v.n, stream, peers(j), fma());
   }
 
   void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
     const uint64_t lo = shard ? v.row_begin : 0, hi = shard ? v.row_end : v.n;
     if (recompute)
-      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush, flush ? PeerViews() : peers(j));
+      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush, flush ? PeerViews() : peers(j), fma());
     else
       fista_fused_iter(*v.op, iter_bufs(j), lo, hi, stream);
   }
@@ -320,7 +322,7 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.init_tail = s->single ? v.tail_sq_band : 0.0;  // the init kernel covers rows [0, nr)
   h.lagged = s->recompute ? 1 : 0;
   *s->h_st = h;
-  if (s->recompute) fista_rc_prepare(*v.op);  // module load + grid sizing before t0
+  if (s->recompute) fista_rc_prepare(*v.op, s->fma());  // module load + grid sizing before t0
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
   s->t0 = std::chrono::steady_clock::now();
   // residuals over all (own) rows: rows >= m_active keep r = -b for the whole run
@@ -476,6 +478,8 @@ void validate_cfg(const l1b_solver_cfg* c, uint64_t n) {  // SolverConfig::valid
     throw InvalidArgument("SolverConfig: fixed L must be positive");
   if (c->l_policy != L1B_L_SPECTRUM && c->l_policy != L1B_L_BACKTRACKING)
     throw InvalidArgument("SolverConfig: unknown Lipschitz policy");
+  if (c->arith != L1B_ARITH_EXACT && c->arith != L1B_ARITH_FMA)
+    throw InvalidArgument("SolverConfig: unknown arithmetic mode");
   if (!(c->max_seconds > 0.0)) throw InvalidArgument("SolverConfig: max_seconds must be positive");
 }
 

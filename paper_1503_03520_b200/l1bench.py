@@ -107,6 +107,9 @@ class SolverConfig:  # solvers.hpp:17-41
     seed: int = 0
     block: int = 256  # pcdm: coordinates per block
     op: str = "auto"  # FISTA/ISTA products: "auto" (matrix-free when banded) | "sparse" | "matrix_free"
+    # "exact": the reference's separately rounded a*b+c (bit-identical iterates);
+    # "fma": fused multiply-adds in the large matrix-free FISTA kernels (<= 1e-12)
+    arith: str = "exact"
 
     _IDS = {"ista": N.ISTA, "fista": N.FISTA, "cd": N.CD, "newton_cg": N.NEWTON_CG, "pcdm": N.PCDM}
 
@@ -135,6 +138,10 @@ class SolverConfig:  # solvers.hpp:17-41
         if self.op not in ops:
             raise ValueError(f"SolverConfig: unknown operator path '{self.op}'")
         c.op = ops[self.op]
+        ariths = {"exact": 0, "fma": 1}
+        if self.arith not in ariths:
+            raise ValueError(f"SolverConfig: unknown arithmetic mode '{self.arith}'")
+        c.arith = ariths[self.arith]
         return c
 
 

@@ -105,12 +105,10 @@ def test_rc_session_stepping_matches_solve():
 
 # (the switches are read once per process by the library, so each mode below
 # runs in a subprocess of its own)
-_MODES = {"loop": {}, "pairs": {"L1B_PERSIST": "0"}, "single": {"L1B_PERSIST": "0", "L1B_RC2": "0"},
-          # two-iteration kernel shapes (L1B_RC2_VARIANT): 4 / 6 per lane, 8 without prefetch
-          **{f"pairs_v{v}": {"L1B_PERSIST": "0", "L1B_RC2_VARIANT": str(v)} for v in (1, 2, 3)}}
+_MODES = {"loop": {}, "pairs": {"L1B_PERSIST": "0"}, "single": {"L1B_PERSIST": "0", "L1B_RC2": "0"}}
 
 
-def _mode_run(mode, kw, iters, target=None):
+def _mode_run(mode, kw, iters, target=None, arith="exact"):
     import json
     import subprocess
     import sys
@@ -120,12 +118,13 @@ def _mode_run(mode, kw, iters, target=None):
         "from paper_1503_03520_b200 import l1bench;"
         f"inst = l1bench.build_instance(**{kw!r});"
         "x = np.empty(inst.n);"
-        f"cfg = l1bench.SolverConfig(max_iters={iters}, op='matrix_free'"
+        f"cfg = l1bench.SolverConfig(max_iters={iters}, op='matrix_free', arith={arith!r}"
         + (f", target_objective={target!r}" if target is not None else "") + ");"
         "tr = l1bench.fista_run(inst, cfg, x);"
         "np.save(sys.argv[1], x);"
         "print(json.dumps({'f': list(tr.objectives()), 'it': [int(s.iter) for s in tr.samples],"
-        " 'status': int(tr.status), 'k': int(tr.iterations)}))")
+        " 'nnz': [int(s.nnz) for s in tr.samples], 'status': int(tr.status), 'k': int(tr.iterations),"
+        " 'launches': l1bench.launch_count()}))")
     import tempfile
 
     with tempfile.TemporaryDirectory() as d:
@@ -138,15 +137,14 @@ def _mode_run(mode, kw, iters, target=None):
         return json.loads(p.stdout.strip().splitlines()[-1]), np.load(out)
 
 
-@pytest.mark.parametrize("mode", ["pairs", "pairs_v1", "pairs_v2", "pairs_v3"])
 @pytest.mark.parametrize("n,stages", [(100003, 4), (30001, 3), (20005, 2), (7777, 1)])
-def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages, mode):
-    """fista_rc2_kernel (two iterations per launch, every kernel shape) vs one
-    iteration per launch and vs the oracle: identical x, objectives within 1e-12."""
+def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages):
+    """fista_rc2_kernel (two iterations per launch) vs one iteration per launch
+    and vs the oracle: identical x, objectives within 1e-12."""
     need_cuda()
     kw = dict(n=n, stages=stages, q=1, s_divisor=100, seed=5, theta=TH)
     iters = 41  # odd: the last launch is a single iteration
-    tp, xp = _mode_run(mode, kw, iters)
+    tp, xp = _mode_run("pairs", kw, iters)
     ts, xs = _mode_run("single", kw, iters)
     np.testing.assert_array_equal(xp, xs)
     assert tp["it"] == ts["it"] and tp["k"] == ts["k"] == iters
@@ -154,6 +152,44 @@ def test_two_iteration_kernel_matches_single_and_oracle(oracle, n, stages, mode)
     otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
     np.testing.assert_array_equal(xp, ox)
     assert rel_err(tp["f"], otr["objective"]) < 1e-12
+
+
+# The contracted arithmetic (SolverConfig.arith = "fma", L1B_ARITH_FMA): every
+# a*b + c of the matrix-free FISTA kernels is one fused multiply-add.  Not the
+# reference's bits any more; the bar is the north star's parity contract at
+# 1e-12 (x, objectives) with identical sample iterations and supports.
+@pytest.mark.parametrize("mode", ["pairs", "single"])
+@pytest.mark.parametrize("n,stages", [(100003, 4), (30001, 3), (20005, 2), (7777, 1)])
+def test_fma_kernels_match_oracle(oracle, n, stages, mode):
+    need_cuda()
+    kw = dict(n=n, stages=stages, q=1, s_divisor=100, seed=5, theta=TH)
+    iters = 201  # odd: the two-iteration path ends with a single-iteration launch
+    tf, xf = _mode_run(mode, kw, iters, arith="fma")
+    te, xe = _mode_run(mode, kw, iters, arith="exact")
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+    np.testing.assert_array_equal(xe, ox)  # the exact build: the reference's bits
+    assert not np.array_equal(xf, ox), "fma build produced the exact bits: contraction not active"
+    assert rel_err(xf, ox) < 1e-12
+    assert rel_err(tf["f"], otr["objective"]) < 1e-12
+    assert tf["it"] == [int(i) for i in otr["iter"]] and tf["k"] == iters
+    np.testing.assert_array_equal(np.nonzero(xf)[0], np.nonzero(ox)[0])
+    assert tf["nnz"] == [int(v) for v in otr["nnz"]]
+
+
+def test_fma_kernels_stop_like_the_reference(oracle):
+    """A target between two iterates' objectives stops the fma build on the
+    reference's iteration."""
+    need_cuda()
+    kw = dict(n=30001, stages=4, q=1, s_divisor=50, seed=9, theta=TH)
+    oi = oracle.build_instance(**kw)
+    otr, _ = oracle.fista(oi, max_iters=400)
+    f = otr["objective"]
+    for k in (37, 38):
+        target = float(f[k] + 0.5 * (f[:k].min() - f[k]))
+        tp, xp = _mode_run("pairs", kw, 400, target, arith="fma")
+        otr2, ox2 = oracle.fista(oi, max_iters=400, target=target)
+        assert tp["k"] == int(otr2["iter"][-1]) == k
+        assert rel_err(xp, ox2) < 1e-12
 
 
 def test_two_iteration_kernel_stops_like_the_reference(oracle):
