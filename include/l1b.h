@@ -174,6 +174,22 @@ typedef struct {
 int l1b_problem_info_get(const l1b_problem* p, l1b_problem_info* out);
 int l1b_problem_get_b(const l1b_problem* p, double* b_host);          /* m */
 int l1b_problem_get_sigma(const l1b_problem* p, double* sigma_host);  /* n */
+/* Row-block shards of banded operators keep b also on a window of rows around
+ * their block ([*lo, *hi); the recomputing FISTA kernel rebuilds r there);
+ * b_host (may be NULL) receives hi - lo entries.  *lo == *hi: no window.   */
+int l1b_problem_get_b_window(const l1b_problem* p, uint64_t* lo, uint64_t* hi, double* b_host);
+/* A new right-hand side for the resident operator (the instance metadata --
+ * ||e||, f*, x* -- keeps describing the generated b): b_host holds m entries
+ * (a row-block shard: its own rows, as l1b_problem_get_b returns them, plus
+ * b_win_host with the window of l1b_problem_get_b_window when it has one).
+ * The serving path of bench.py's multi-GPU e2e: operator resident in HBM,
+ * b streamed from pinned host memory.                                       */
+int l1b_problem_set_rhs(l1b_problem* p, const double* b_host, const double* b_win_host);
+/* The sigma entries the problem holds: [*begin, *end) of the global sigma
+ * (a row-block shard keeps its window plus the kernels' halos; a whole
+ * problem all n).  sigma_host (may be NULL) receives end - begin entries.  */
+int l1b_problem_get_sigma_window(const l1b_problem* p, uint64_t* begin, uint64_t* end,
+                                 double* sigma_host);
 int l1b_problem_get_xstar(const l1b_problem* p, uint32_t* support, double* values);
 /* The operator description back (save_instance, serialize.cpp:148-163): stage
  * offsets / angles of the right (right = 1) or left factor (count first, arrays
@@ -210,6 +226,10 @@ int l1b_estimate_gram_lmax(l1b_problem* p, uint64_t iters, uint64_t seed, double
 int l1b_export_csr(const l1b_problem* p, uint64_t* row_ptr, uint32_t* col, double* val);
 int l1b_export_csc(const l1b_problem* p, uint64_t* col_ptr, uint32_t* row, double* val);
 
+/* The Newton-CG Hessian-vector product on device vectors (smoothed_hessvec,
+ * solvers.cpp:188-200; as newton_cg_run's PCG forms it, :536-540):
+ * out = A^T (A v) + tau * d2psi_mu(x) .* v.  Whole problems only.          */
+int l1b_smoothed_hessvec(l1b_problem* p, double mu, const double* d_x, const double* d_v, double* d_out);
 /* tau*||x||_1 + 1/2*||A x - b||^2 (solvers.cpp:145-151). */
 int l1b_objective(l1b_problem* p, const double* d_x, double* f_out);
 
@@ -285,7 +305,26 @@ typedef struct {
   double matvecs_to_target;
   uint64_t n_samples;        /* samples produced (may exceed cap; first cap written) */
   uint64_t iterations;       /* iterations / sweeps / Newton steps executed */
+  uint32_t path;             /* L1B_RAN_* flags: which kernels the solve ran (tests assert them) */
 } l1b_summary;
+
+/* l1b_summary.path */
+enum {
+  L1B_RAN_FISTA_SPARSE = 1u << 0,     /* CSR/CSC SpMV kernel pair (k_spmv.cu) */
+  L1B_RAN_FISTA_MF_PAIR = 1u << 1,    /* two matrix-free product kernels (k_fused.cu) */
+  L1B_RAN_FISTA_STORED = 1u << 2,     /* one matrix-free kernel, stored residuals (k_fused.cu) */
+  L1B_RAN_FISTA_RECOMPUTE = 1u << 3,  /* one iteration per launch, residuals recomputed (k_iter_rc.cu) */
+  L1B_RAN_FISTA_TWO_ITER = 1u << 4,   /* two iterations per launch (fista_rc2v_kernel) */
+  L1B_RAN_FISTA_LOOP = 1u << 5,       /* small instance: chunks of iterations per cooperative launch */
+  L1B_RAN_FMA = 1u << 6,              /* the contracted arithmetic (L1B_ARITH_FMA) was applied */
+  L1B_RAN_PCDM_PAIR = 1u << 7,        /* pair-local CD / PCDM epochs, device coordinate stream */
+  L1B_RAN_PCDM_PLAN = 1u << 8,        /* planned CD / PCDM epochs */
+  L1B_RAN_PCDM_DIRECT = 1u << 9,      /* one-CTA CD / PCDM epochs */
+  L1B_RAN_PCG_PAIR = 1u << 10,        /* pair-local PCG, one cooperative launch per Newton step */
+  L1B_RAN_PCG_LOOP = 1u << 11,        /* CSR/CSC PCG, one cooperative launch per Newton step */
+  L1B_RAN_PCG_KERNELS = 1u << 12,     /* CSR/CSC PCG, four kernels per PCG iteration */
+  L1B_RAN_HOST_LED = 1u << 13         /* FISTA / ISTA with LPolicy::backtracking (host-led trials) */
+};
 
 int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
               l1b_summary* summary, double* x_host, double* d_x);

@@ -187,6 +187,31 @@ void lo_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_
   }
 }
 
+void lo_uniform_stream_window(uint64_t seed, uint64_t count, double lo, double hi, int spectrum,
+                              double shift, uint64_t wlo, uint64_t whi, double* out, double* vmin,
+                              double* vmax) {
+  lo_rng r;
+  lo_rng_seed(&r, seed);
+  double mn = 0.0, mx = 0.0;
+  for (uint64_t i = 0; i < count; ++i) {
+    double v;
+    if (spectrum) {
+      double u;
+      do {
+        u = lo_uniform_in(&r, lo, hi);
+      } while (u <= lo);
+      v = u + shift;
+    } else {
+      v = lo_uniform_in(&r, lo, hi);
+    }
+    if (i == 0 || v < mn) mn = v;
+    if (i == 0 || v > mx) mx = v;
+    if (i >= wlo && i < whi) out[i - wlo] = v;
+  }
+  if (vmin) *vmin = mn;
+  if (vmax) *vmax = mx;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Sparse accumulator sweeps (linops.cpp:113-192)                            */
 

@@ -68,6 +68,16 @@ void lo_permutation_realize(uint64_t n, uint64_t seed, uint32_t* map, uint32_t* 
 void lo_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
                          double* sigma);
 
+/* Streaming windows of the two per-entry generator streams at any length
+ * (C5: 2^32 draws, too long to hold): draws [0, count) of Rng(seed) exactly
+ * as lo_spectrum_uniform (spectrum = 1: reject u <= lo, + shift;
+ * linops.cpp:323-331) or as the l1_subgradient fill before the support signs
+ * (spectrum = 0: lo + (hi - lo) u; instance.cpp:33-35), sequentially; draws
+ * [wlo, whi) are stored into out, min / max over all draws into vmin / vmax. */
+void lo_uniform_stream_window(uint64_t seed, uint64_t count, double lo, double hi, int spectrum,
+                              double shift, uint64_t wlo, uint64_t whi, double* out, double* vmin,
+                              double* vmax);
+
 /* Sparse row / column via the reference's sparse-accumulator sweeps
  * (linops.cpp:113-192, 566-619).  Returns nnz written (sorted ascending,
  * exact zeros dropped).  ws must come from lo_ws_create(max(m, n)).      */

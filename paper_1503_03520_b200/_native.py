@@ -90,7 +90,13 @@ class Summary(C.Structure):
     _fields_ = [("status", C.c_int), ("reached_target", C.c_int), ("final_objective", f64),
                 ("elapsed_s", f64), ("total_matvecs", f64), ("total_pcg_iterations", u64),
                 ("newton_steps", u64), ("time_to_target", f64), ("matvecs_to_target", f64),
-                ("n_samples", u64), ("iterations", u64)]
+                ("n_samples", u64), ("iterations", u64), ("path", u32)]
+
+
+# l1b_summary.path flags (include/l1b.h L1B_RAN_*)
+RAN = {name: 1 << i for i, name in enumerate(
+    ["fista_sparse", "fista_mf_pair", "fista_stored", "fista_recompute", "fista_two_iter", "fista_loop",
+     "fma", "pcdm_pair", "pcdm_plan", "pcdm_direct", "pcg_pair", "pcg_loop", "pcg_kernels", "host_led"])}
 
 
 # every symbol include/l1b.h declares: (name, restype, argtypes)
@@ -114,6 +120,10 @@ SIGNATURES = [
     ("l1b_problem_info_get", C.c_int, [vp, P(ProblemInfo)]),
     ("l1b_problem_get_b", C.c_int, [vp, P(f64)]),
     ("l1b_problem_get_sigma", C.c_int, [vp, P(f64)]),
+    ("l1b_problem_get_sigma_window", C.c_int, [vp, P(u64), P(u64), P(f64)]),
+    ("l1b_problem_get_b_window", C.c_int, [vp, P(u64), P(u64), P(f64)]),
+    ("l1b_problem_set_rhs", C.c_int, [vp, P(f64), P(f64)]),
+    ("l1b_smoothed_hessvec", C.c_int, [vp, f64, vp, vp, vp]),
     ("l1b_problem_set_meta", C.c_int, [vp, f64, f64]),
     ("l1b_problem_get_stages", C.c_int, [vp, C.c_int, P(u32), P(C.c_int32), P(f64)]),
     ("l1b_problem_get_perm", C.c_int, [vp, C.c_int, P(C.c_int), P(u32)]),

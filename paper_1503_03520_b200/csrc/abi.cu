@@ -52,6 +52,19 @@ int sm_count() {
   return sms;
 }
 
+// the device's default stream-ordered pool keeps freed memory cached (no
+// release at synchronisation points): sessions and problems allocate from it
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 int grid_for(uint64_t work, int threads, int max_blocks_per_sm) {
   const uint64_t blocks = (work + threads - 1) / threads;
   const uint64_t cap = (uint64_t)max_blocks_per_sm * sm_count();
@@ -129,19 +142,29 @@ using namespace l1b;
 
 namespace {
 
-// +2 entries of slack: the TMA stages copy 16-byte rounded ranges
+// +2 entries of slack: the TMA stages copy 16-byte rounded ranges.  With a
+// stream the buffer comes from the device's stream-ordered pool (kept cached,
+// keep_pool): creating a problem from host data again (e2e passes, repeated
+// l1b_problem_create) costs no cudaMalloc / page mapping after the first.
 template <class T>
-T* dev_alloc(size_t count, size_t* bytes_acc) {
+T* dev_alloc(size_t count, size_t* bytes_acc, cudaStream_t st = nullptr) {
   T* p = nullptr;
   const size_t bytes = (count + 2) * sizeof(T);
-  L1B_CUDA(cudaMalloc(&p, bytes));
+  if (st) {
+    int dev = 0;
+    L1B_CUDA(cudaGetDevice(&dev));
+    keep_pool(dev);
+    L1B_CUDA(cudaMallocAsync(&p, bytes, st));
+  } else {
+    L1B_CUDA(cudaMalloc(&p, bytes));
+  }
   if (bytes_acc) *bytes_acc += bytes;
   return p;
 }
 
 template <class T>
 T* upload(const T* host, size_t count, cudaStream_t st, size_t* bytes_acc) {
-  T* p = dev_alloc<T>(count, bytes_acc);
+  T* p = dev_alloc<T>(count, bytes_acc, st);
   if (count) L1B_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
   return p;
 }
@@ -173,7 +196,8 @@ struct l1b_problem {
   int world = 1, rank = 0;
   bool sharded = false;  // a row-block shard (l1b_generate with a shard descriptor)
   uint64_t halo = 0;
-  uint64_t sig_begin = 0;  // shards: d_sigma holds sigma[sig_begin, ...)
+  uint64_t sig_begin = 0;  // shards: d_sigma holds sigma[sig_begin, sig_end)
+  uint64_t sig_end = 0;    // 0: the whole problem (sigma[0, n))
   // shards: b on [b_win_lo, b_win_hi) = own rows +- the recomputing kernel's
   // halo (it rebuilds r on the rows around its own block)
   double* d_b_win = nullptr;
@@ -189,7 +213,7 @@ struct l1b_problem {
     for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv,
                     (void*)d_b, (void*)d_b_win, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
                     (void*)csc.idx, (void*)csc.val})
-      if (p) cudaFree(p);
+      if (p) cudaFree(p);  // (pool buffers go back to the pool; the stream is idle)
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
 
@@ -566,7 +590,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   double smax = 0.0, smin = 0.0;
   bool have_sigma = false;
   if (dev_rng && g->spectrum_kind == L1B_SPECTRUM_UNIFORM_Q) {
-    p->d_sigma = dev_alloc<double>(sb - sa, &p->device_bytes);
+    p->d_sigma = dev_alloc<double>(sb - sa, &p->device_bytes, st);
     have_sigma = device_uniform_draws(hostrng::mix_seed(job_seed, 3), n, 0.0, std::pow(10.0, g->q), true,
                                       g->shift, sa, sb, p->d_sigma, &smin, &smax, 0);
     if (!have_sigma) {
@@ -605,6 +629,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   fill_stage_tab(p->view.right, p->r_off, p->r_theta);
   fill_stage_tab(p->view.left, p->l_off, p->l_theta);
   p->sig_begin = sa;
+  p->sig_end = sb;
   p->view.m = m;
   p->view.n = n;
   p->view.sigma = p->d_sigma - sa;  // global indexing inside [sa, sb)
@@ -638,7 +663,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
       }
     }
     if (dev_rng) {
-      d_g = dev_alloc<double>(sb - sa, nullptr);
+      d_g = dev_alloc<double>(sb - sa, nullptr, st);
       device_uniform_draws(hostrng::mix_seed(job_seed, 5), n, -g->fill_bound, g->fill_bound, false, 0.0, sa,
                            sb, d_g, nullptr, nullptr, st);
       uint32_t* d_ws = upload(wsup.data(), wsup.size(), st, nullptr);
@@ -678,7 +703,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   window_stages(p->view.right, false, false, d_g, sa, sb, n, st);
   // e_own = Sigma G^T w, b_own = Sigma G^T x* on [a, b)
   double* d_v = nullptr;
-  double* d_x = dev_alloc<double>(vb - va, nullptr);
+  double* d_x = dev_alloc<double>(vb - va, nullptr, st);
   {
     uint32_t* d_xs = upload(xsup.data(), xsup.size(), st, nullptr);
     double* d_xv = upload(xval.data(), xval.size(), st, nullptr);
@@ -693,7 +718,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
   window_stages(p->view.right, true, true, d_x, va, vb, n, st);
   window_scale_op(d_v + (wa - va), p->d_sigma + (wa - sa), wb - wa, 1, 0.0, st);
   window_scale_op(d_x + (wa - va), p->d_sigma + (wa - sa), wb - wa, 1, 0.0, st);
-  p->d_b = dev_alloc<double>(own, &p->device_bytes);
+  p->d_b = dev_alloc<double>(own, &p->device_bytes, st);
   L1B_CUDA(cudaMemcpyAsync(p->d_b, d_x + (a - va), own * 8, cudaMemcpyDeviceToDevice, st));
   double* d_ss = nullptr;
   L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
@@ -701,7 +726,7 @@ void generate_shard(int device, const l1b_gen_desc* g, const l1b_shard_desc* sh,
     double* d_e = nullptr;
     L1B_CUDA(cudaMalloc(&d_e, (wb - wa) * sizeof(double)));
     L1B_CUDA(cudaMemcpyAsync(d_e, d_v + (wa - va), (wb - wa) * 8, cudaMemcpyDeviceToDevice, st));
-    p->d_b_win = dev_alloc<double>(wb - wa, &p->device_bytes);
+    p->d_b_win = dev_alloc<double>(wb - wa, &p->device_bytes, st);
     L1B_CUDA(cudaMemcpyAsync(p->d_b_win, d_x + (wa - va), (wb - wa) * 8, cudaMemcpyDeviceToDevice, st));
     generator_combine(p->tau, d_e, p->d_b_win, wb - wa, d_ss, st);
     p->b_win_lo = wa;
@@ -831,7 +856,7 @@ std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
   L1B_CUDA(cudaMalloc(&d_e, m * sizeof(double)));
   L1B_CUDA(cudaMalloc(&d_x, n * sizeof(double)));
   L1B_CUDA(cudaMalloc(&d_ss, sizeof(double)));
-  p->d_b = dev_alloc<double>(m, &p->device_bytes);
+  p->d_b = dev_alloc<double>(m, &p->device_bytes, st);
   d_sup = upload(p->xs_sup.data(), s, st, nullptr);
   d_val = upload(p->xs_val.data(), s, st, nullptr);
   sweep_gram_inverse(p->view, d_g, d_g, st);
@@ -992,11 +1017,65 @@ int l1b_problem_get_b(const l1b_problem* p, double* b) {
   });
 }
 
+int l1b_problem_get_b_window(const l1b_problem* p, uint64_t* lo, uint64_t* hi, double* b) {
+  return guard([&] {
+    check_problem(p);
+    if (!lo || !hi) throw InvalidArgument("null argument");
+    *lo = p->b_win_lo;
+    *hi = p->b_win_hi;
+    if (b && p->d_b_win && p->b_win_hi > p->b_win_lo) {
+      L1B_CUDA(cudaMemcpyAsync(b, p->d_b_win, (p->b_win_hi - p->b_win_lo) * sizeof(double),
+                               cudaMemcpyDeviceToHost, p->stream));
+      L1B_CUDA(cudaStreamSynchronize(p->stream));
+    }
+  });
+}
+
+int l1b_problem_set_rhs(l1b_problem* p, const double* b_host, const double* b_win_host) {
+  return guard([&] {
+    check_problem(p);
+    if (!b_host) throw InvalidArgument("null b");
+    cudaStream_t st = p->stream;
+    if (p->sharded && !p->general) {
+      const uint64_t own = p->row_end - p->row_begin;
+      L1B_CUDA(cudaMemcpyAsync(p->d_b, b_host, own * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (p->d_b_win) {
+        if (!b_win_host) throw InvalidArgument("this shard keeps a b window: b_win_host needed");
+        L1B_CUDA(cudaMemcpyAsync(p->d_b_win, b_win_host, (p->b_win_hi - p->b_win_lo) * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
+      }
+      L1B_CUDA(cudaStreamSynchronize(st));  // host buffers are read during the call only
+      return;
+    }
+    L1B_CUDA(cudaMemcpyAsync(p->d_b, b_host, p->m * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (p->general) {
+      L1B_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    band_tail(p);  // (synchronises the stream)
+    if (p->sparse_built)
+      p->tail_sq = p->csr.lines < p->m ? device_sum_sq(p->d_b + p->csr.lines, p->m - p->csr.lines, st) : 0.0;
+  });
+}
+
 int l1b_problem_get_sigma(const l1b_problem* p, double* s) {
   return guard([&] {
     check_whole(p);
     L1B_CUDA(cudaMemcpyAsync(s, p->d_sigma, p->n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     L1B_CUDA(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int l1b_problem_get_sigma_window(const l1b_problem* p, uint64_t* begin, uint64_t* end, double* s) {
+  return guard([&] {
+    if (!p || !begin || !end) throw InvalidArgument("null argument");
+    *begin = p->sig_begin;
+    *end = p->sig_end ? p->sig_end : p->n;
+    if (s) {
+      L1B_CUDA(cudaMemcpyAsync(s, p->d_sigma, (*end - *begin) * sizeof(double), cudaMemcpyDeviceToHost,
+                               p->stream));
+      L1B_CUDA(cudaStreamSynchronize(p->stream));
+    }
   });
 }
 
@@ -1097,7 +1176,7 @@ int l1b_gram_inverse(l1b_problem* p, const double* d_v, double* d_out) {
 namespace {
 const double* gram_diag_device(l1b_problem* p) {
   if (!p->d_gram) {
-    p->d_gram = dev_alloc<double>(p->n, &p->device_bytes);
+    p->d_gram = dev_alloc<double>(p->n, &p->device_bytes, p->stream);
     gram_diagonal(p->view, 0, p->n, p->d_gram, p->stream);
   }
   return p->d_gram;

@@ -72,6 +72,7 @@ struct OpView {
 constexpr int kThreads = 256;
 int sm_count();
 int grid_for(uint64_t work_items, int threads = kThreads, int max_blocks_per_sm = 8);
+void keep_pool(int device);  // default mem pool of `device`: freed memory stays cached
 
 // ---------------------------------------------------------------------------
 // device helpers
@@ -94,7 +95,7 @@ __device__ __forceinline__ void rotate_pair(double& vi, double& vj, double c, do
 // The contracted arithmetic mode (l1b_solver_cfg.arith = L1B_ARITH_FMA): every
 // a*b + c of the hot loop as one fused multiply-add -- one rounding instead of
 // two, so the results are no longer the reference's bits but at least as
-// accurate (parity: <= 1e-12 relative, tests/test_gpu_fma.py).  A rotation
+// accurate (parity: <= 1e-12 relative, tests/test_gpu_rc.py, test_gpu_configs.py).  A rotation
 // costs 2 DMUL + 2 DFMA instead of 4 DMUL + 2 DADD.  F = false is the exact
 // (bit-identical) arithmetic above.
 template <bool F>

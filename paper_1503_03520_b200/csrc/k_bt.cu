@@ -307,6 +307,7 @@ void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sampl
     }
     if (last_sampled != k) sample(k, f, nnz, 0);
     std::memset(sum, 0, sizeof(*sum));
+    sum->path = L1B_RAN_HOST_LED;
     for (size_t q = 0; q < out.size() && samples; ++q)
       if (q < cap) samples[q] = out[q];
     if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, x, n * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -21,6 +21,7 @@
 
 #include <cooperative_groups.h>
 
+#include "guard.hpp"
 #include "solvers.hpp"
 #include "spmv.cuh"
 
@@ -454,6 +455,54 @@ struct PcgPairArgs {
   double* partials;  // >= 3 x grid doubles
 };
 
+// The Hessian-vector product of one pair (a, a + 1) of a single-stage
+// operator (solvers.cpp:536-540 with OperatorSpec::apply / apply_transpose,
+// linops.cpp:422-473): w = G Sigma^T Sigma G^T v, h = w + tau d2psi v.
+// pair = both entries exist (else the lone entry is not rotated).
+__device__ __forceinline__ void pair_hessvec(double v0, double v1, bool pair, double c, double s, double s0,
+                                             double s1, double d0, double d1, double tau, double& h0,
+                                             double& h1) {
+  double u0 = v0, u1 = v1;
+  if (pair) rotate_pair(u0, u1, c, s, true);  // G^T v
+  double w0 = s0 * (s0 * u0), w1 = s1 * (s1 * u1);  // Sigma^T (Sigma G^T v)
+  if (pair) rotate_pair(w0, w1, c, s, false);      // G (...)
+  h0 = w0 + tau * d0 * v0;
+  h1 = w1 + tau * d1 * v1;
+}
+
+// d2psi of the pseudo-Huber term, as the gradient pass forms it (EpiGrad)
+__device__ __forceinline__ double huber_d2(double xj, double mu) {
+  const double q = mu * mu + xj * xj;
+  const double root = sqrt(q);
+  return mu * mu / (q * root);
+}
+
+// l1b_smoothed_hessvec, single-stage operators: one thread per pair
+__global__ void hessvec_pair_kernel(uint64_t n, int off, double c, double s, const double* __restrict__ sigma,
+                                    const double* __restrict__ x, const double* __restrict__ v, double mu,
+                                    double tau, double* __restrict__ out) {
+  const uint64_t U = (n + 2) / 2;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < U;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t a = 2 * (int64_t)u - off;
+    const bool va = a >= 0 && a < (int64_t)n, vb = a + 1 >= 0 && a + 1 < (int64_t)n;
+    const double v0 = va ? v[a] : 0.0, v1 = vb ? v[a + 1] : 0.0;
+    const double d0 = va ? huber_d2(x[a], mu) : 0.0, d1 = vb ? huber_d2(x[a + 1], mu) : 0.0;
+    double h0, h1;
+    pair_hessvec(v0, v1, va && vb, c, s, va ? sigma[a] : 0.0, vb ? sigma[a + 1] : 0.0, d0, d1, tau, h0, h1);
+    if (va) out[a] = h0;
+    if (vb) out[a + 1] = h1;
+  }
+}
+
+// l1b_smoothed_hessvec, other operators: out = A^T (A v) (sweeps) + tau d2psi v
+__global__ void hessvec_diag_kernel(uint64_t n, const double* __restrict__ x, const double* __restrict__ v,
+                                    double mu, double tau, double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] += tau * huber_d2(x[i], mu) * v[i];
+}
+
 template <int P, int BT = kThreads>
 __global__ void __launch_bounds__(BT) pcg_pair_kernel(PcgPairArgs A) {
   namespace cg = cooperative_groups;
@@ -503,14 +552,8 @@ __global__ void __launch_bounds__(BT) pcg_pair_kernel(PcgPairArgs A) {
     double acc[1] = {0.0};
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const bool pair = va[k] && vb[k];
-      double v0 = p[k][0], v1 = p[k][1];
-      if (pair) rotate_pair(v0, v1, c, s, true);  // G^T p
-      const double s0 = c_sig[slot(k, 0)], s1 = c_sig[slot(k, 1)];
-      double w0 = s0 * (s0 * v0), w1 = s1 * (s1 * v1);  // Sigma^T (Sigma G^T p)
-      if (pair) rotate_pair(w0, w1, c, s, false);      // G (...)
-      hp[k][0] = w0 + tau * c_d2[slot(k, 0)] * p[k][0];
-      hp[k][1] = w1 + tau * c_d2[slot(k, 1)] * p[k][1];
+      pair_hessvec(p[k][0], p[k][1], va[k] && vb[k], c, s, c_sig[slot(k, 0)], c_sig[slot(k, 1)],
+                   c_d2[slot(k, 0)], c_d2[slot(k, 1)], tau, hp[k][0], hp[k][1]);
       if (va[k]) acc[0] += p[k][0] * hp[k][0];
       if (vb[k]) acc[0] += p[k][1] * hp[k][1];
     }
@@ -979,6 +1022,7 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
       rr = rr_acc;
     }
     std::memset(sum, 0, sizeof(*sum));
+    sum->path = pair.P ? L1B_RAN_PCG_PAIR : coop_grid > 0 ? L1B_RAN_PCG_LOOP : L1B_RAN_PCG_KERNELS;
     for (size_t q = 0; q < out.size() && samples; ++q)
       if (q < cap) samples[q] = out[q];
     if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, x, n * 8, cudaMemcpyDeviceToHost, st));
@@ -1007,4 +1051,37 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
   fail();
 }
 
+// The Newton-CG Hessian-vector product at x (l1b_smoothed_hessvec): the
+// pair-local arithmetic of pcg_pair_kernel for single-stage operators, the
+// reference's sweeps (+ the same d2psi epilogue) otherwise.
+void smoothed_hessvec(l1b_problem* p, double mu, const double* x, const double* v, double* out) {
+  const ProblemView pv = problem_view(p, false);
+  if (pv.shard) throw Unsupported("smoothed_hessvec: whole problems only");
+  if (!(mu > 0.0)) throw InvalidArgument("pseudo_huber: mu must be positive");
+  const OpView* op = pv.op;
+  cudaStream_t st = pv.stream;
+  if (op->right.count == 1 && op->left.count == 0 && !op->p1 && !op->p2 && pv.m >= pv.n) {
+    hessvec_pair_kernel<<<grid_for((pv.n + 2) / 2), kThreads, 0, st>>>(
+        pv.n, op->right.offset[0], op->right.c[0], op->right.s[0], op->sigma, x, v, mu, pv.tau, out);
+    L1B_LAUNCHED();
+  } else {
+    double* av = nullptr;
+    L1B_CUDA(cudaMallocAsync((void**)&av, pv.m * sizeof(double), st));
+    sweep_apply(*op, v, av, st);
+    sweep_apply_transpose(*op, av, out, st);
+    hessvec_diag_kernel<<<grid_for(pv.n), kThreads, 0, st>>>(pv.n, x, v, mu, pv.tau, out);
+    L1B_LAUNCHED();
+    L1B_CUDA(cudaFreeAsync(av, st));
+  }
+  L1B_CUDA(cudaStreamSynchronize(st));
+}
+
 }  // namespace l1b
+
+extern "C" int l1b_smoothed_hessvec(l1b_problem* p, double mu, const double* d_x, const double* d_v,
+                                    double* d_out) {
+  return l1b::guard([&] {
+    if (!p || !d_x || !d_v || !d_out) throw l1b::InvalidArgument("null argument");
+    l1b::smoothed_hessvec(p, mu, d_x, d_v, d_out);
+  });
+}

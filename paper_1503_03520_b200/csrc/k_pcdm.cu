@@ -1335,6 +1335,7 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, x, n * 8, cudaMemcpyDeviceToDevice, st));
     L1B_CUDA(cudaStreamSynchronize(st));
     std::memset(sum, 0, sizeof(*sum));
+    sum->path = pair_mode > 0 ? L1B_RAN_PCDM_PAIR : plan_k ? L1B_RAN_PCDM_PLAN : L1B_RAN_PCDM_DIRECT;
     sum->status = hs.stop ? hs.status : (time_out ? L1B_TIME_BUDGET : L1B_ITER_BUDGET);
     sum->time_to_target = INFINITY;
     sum->matvecs_to_target = INFINITY;

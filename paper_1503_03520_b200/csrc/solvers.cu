@@ -168,16 +168,6 @@ uint64_t sample_capacity(uint64_t max_iters) {
 
 // Keep freed pool memory cached on the device (release threshold = max), so
 // repeated solves on resident instances do not go back to the driver.
-void keep_pool(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[device] = true;
-}
 
 void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   keep_pool(problem_view(p, false).device);
@@ -428,6 +418,13 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   // final sample when the last iteration was not sampled (solvers.cpp:379)
   if (h.last_sampled != h.k) tr.push_back(FistaSample{h.k, h.f, h.nnz, h.last_ts});
   std::memset(sum, 0, sizeof(*sum));
+  if (uses_loop(s))
+    sum->path = L1B_RAN_FISTA_LOOP | L1B_RAN_FISTA_RECOMPUTE;
+  else if (s->recompute)
+    sum->path = (rc2_enabled() ? L1B_RAN_FISTA_TWO_ITER : 0u) | L1B_RAN_FISTA_RECOMPUTE |
+                (s->fma() ? L1B_RAN_FMA : 0u);
+  else
+    sum->path = s->single ? L1B_RAN_FISTA_STORED : s->fused ? L1B_RAN_FISTA_MF_PAIR : L1B_RAN_FISTA_SPARSE;
   sum->status = status;
   sum->time_to_target = INFINITY;
   sum->matvecs_to_target = INFINITY;

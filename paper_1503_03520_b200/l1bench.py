@@ -169,6 +169,11 @@ class SolverTrace:  # solvers.hpp:54-66
     time_to_target: float = math.inf
     matvecs_to_target: float = math.inf
     iterations: int = 0
+    path: int = 0  # l1b_summary.path: which kernels ran (L1B_RAN_* flags)
+
+    def ran(self, name: str) -> bool:
+        """Did the solve run the kernel family `name` (N.RAN keys, e.g. "pcdm_pair")?"""
+        return bool(self.path & N.RAN[name])
 
     def objectives(self) -> np.ndarray:
         return np.array([s.objective for s in self.samples])
@@ -377,6 +382,30 @@ class ProblemInstance:
         N.check(_lib().l1b_problem_get_sigma(self._h, _ptr(out, _f64p)))
         return out
 
+    def b_window(self):
+        """(lo, b[lo:hi]): a banded shard's b on the rows around its block (empty otherwise)."""
+        a, e = C.c_uint64(), C.c_uint64()
+        N.check(_lib().l1b_problem_get_b_window(self._h, C.byref(a), C.byref(e), None))
+        out = np.empty(e.value - a.value)
+        N.check(_lib().l1b_problem_get_b_window(self._h, C.byref(a), C.byref(e), _ptr(out, _f64p)))
+        return int(a.value), out
+
+    def set_rhs(self, b, b_win=None) -> None:
+        """A new right-hand side for the resident operator (l1b_problem_set_rhs):
+        host float64 arrays (pinned for full PCIe speed) in the layout of
+        ``b`` / ``b_window()``."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        bw = None if b_win is None else np.ascontiguousarray(b_win, dtype=np.float64)
+        N.check(_lib().l1b_problem_set_rhs(self._h, _ptr(b, _f64p), _ptr(bw, _f64p)))
+
+    def sigma_window(self):
+        """(begin, sigma[begin:end]): the sigma entries this problem holds (shards: a window)."""
+        a, e = C.c_uint64(), C.c_uint64()
+        N.check(_lib().l1b_problem_get_sigma_window(self._h, C.byref(a), C.byref(e), None))
+        out = np.empty(e.value - a.value)
+        N.check(_lib().l1b_problem_get_sigma_window(self._h, C.byref(a), C.byref(e), _ptr(out, _f64p)))
+        return int(a.value), out
+
     @property
     def x_star(self) -> SparseSolution:
         s = int(self.info.s)
@@ -445,13 +474,15 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
                    theta: float = 0.6283185307179586, seed: int = 1, job_index: int = 0,
                    fill_bound: float = 0.9, device: int = 0, lazy_sparse: bool = False,
                    solution: str = "uniform", s1_fraction: float = 0.5, value_a: float = -1e4,
-                   value_b: float = 1e-1) -> ProblemInstance:
+                   value_b: float = 1e-1, shard: Optional[tuple] = None) -> ProblemInstance:
     """``build_instance(cfg, enumerate_jobs(cfg)[job_index])`` for a single-job
     ExperimentConfig (bench.cpp:216-316), generated on the GPU.  ``sigma`` gives
     an explicit spectrum (Spectrum::from_values), ``alternating=(odd, even)`` the
     alternating one, otherwise uniform in (0, 10^q] + shift.  ``solution`` is the
     SolutionRule kind (bench.hpp:25-32): "uniform" (default), "spectral"
-    (spectral_sparse_solution, s1_fraction) or "two_value" (value_a, value_b)."""
+    (spectral_sparse_solution, s1_fraction) or "two_value" (value_a, value_b).
+    ``shard=(rank, world)`` builds only that rank's row block of the default
+    even split (banded operators)."""
     sig = None
     g = N.GenDesc()
     g.n, g.m_ratio, g.stages, g.left_stages, g.permute = n, m_ratio, stages, left_stages, int(permute)
@@ -472,7 +503,8 @@ def build_instance(n: int, m_ratio: float = 2.0, stages: int = 1, left_stages: i
         raise ValueError(f"SolutionRule: unknown kind '{solution}'")
     g.solution_kind, g.s1_fraction, g.value_a, g.value_b = kinds[solution], s1_fraction, value_a, value_b
     h = C.c_void_p()
-    N.check(_lib().l1b_generate(device, C.byref(g), None, C.byref(h)))
+    sh = None if shard is None else N.ShardDesc(int(shard[0]), int(shard[1]), 0, 0)
+    N.check(_lib().l1b_generate(device, C.byref(g), None if sh is None else C.byref(sh), C.byref(h)))
     return ProblemInstance(h)
 
 
@@ -593,6 +625,18 @@ def objective(inst: ProblemInstance, x) -> float:
     return float(f.value)
 
 
+def smoothed_hessvec(inst: ProblemInstance, x, mu: float, v):
+    """smoothed_hessvec (solvers.cpp:188-200) as newton_cg_run's PCG forms it
+    (:536-540): A^T A v + tau d2psi_mu(x) v, on device vectors; returns a new
+    CUDA float64 tensor."""
+    import torch
+
+    out = torch.empty(inst.n, dtype=torch.float64, device=x.device)
+    with _Ordered(inst):
+        N.check(_lib().l1b_smoothed_hessvec(inst._h, float(mu), _dptr(x), _dptr(v), _dptr(out)))
+    return out
+
+
 def soft_threshold(v: float, t: float) -> float:  # solvers.cpp:153-157 (host scalar helper)
     if v > t:
         return v - t
@@ -622,6 +666,7 @@ def _trace_from(name: str, samples, k: int, s: N.Summary) -> SolverTrace:
     tr.time_to_target = s.time_to_target
     tr.matvecs_to_target = s.matvecs_to_target
     tr.iterations = int(s.iterations)
+    tr.path = int(s.path)
     return tr
 
 

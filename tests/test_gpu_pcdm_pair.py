@@ -48,6 +48,7 @@ def test_pair_epochs_match_direct_epochs(n, block, solver, epochs):
         kw = dict(max_iters=epochs, seed=3, varpi=4)
     tr_p, x_p = _run(inst, solver, True, **kw)
     tr_d, x_d = _run(inst, solver, False, **kw)
+    assert tr_p.ran("pcdm_pair") and not tr_d.ran("pcdm_pair"), (tr_p.path, tr_d.path)
     np.testing.assert_array_equal(x_p, x_d)
     np.testing.assert_array_equal([s.extra for s in tr_p.samples], [s.extra for s in tr_d.samples])
     np.testing.assert_array_equal([s.nnz for s in tr_p.samples], [s.nnz for s in tr_d.samples])
@@ -68,6 +69,7 @@ def test_pair_pcdm_matches_oracle_c2_shape(oracle):
     inst = l1bench.build_instance(**kw)
     oi = oracle.build_instance(**kw)
     tr, x = _run(inst, "pcdm", True, max_iters=30, block=256, seed=1)
+    assert tr.ran("pcdm_pair"), tr.path
     otr, ox = oracle.pcdm(oi, max_iters=30, block=256, seed=1)
     assert rel_err(x, ox) < 1e-10
     assert rel_err(tr.objectives(), otr["objective"]) < 1e-10
@@ -86,6 +88,7 @@ def test_pair_pcdm_target_stop_matches_direct():
     target = float(f[17] * (1 + 1e-9))  # first met at or before epoch 17
     tr_p, x_p = _run(inst, "pcdm", True, max_iters=40, block=128, seed=9, target_objective=target)
     tr_d, x_d = _run(inst, "pcdm", False, max_iters=40, block=128, seed=9, target_objective=target)
+    assert tr_p.ran("pcdm_pair") and not tr_d.ran("pcdm_pair")
     assert tr_p.status == tr_d.status == l1bench.StopReason.target_reached
     assert tr_p.iterations == tr_d.iterations <= 17
     np.testing.assert_array_equal(x_p, x_d)
@@ -100,5 +103,6 @@ def test_pair_path_not_taken_for_two_stages():
     inst = l1bench.build_instance(n=4096, stages=2, q=1, s_divisor=50, seed=7, theta=TH)
     tr_p, x_p = _run(inst, "pcdm", True, max_iters=5, block=256, seed=3)
     tr_d, x_d = _run(inst, "pcdm", False, max_iters=5, block=256, seed=3)
+    assert not tr_p.ran("pcdm_pair") and tr_p.path == tr_d.path
     np.testing.assert_array_equal(x_p, x_d)
     np.testing.assert_array_equal(tr_p.objectives(), tr_d.objectives())

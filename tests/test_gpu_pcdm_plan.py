@@ -18,16 +18,19 @@ TH = 2 * math.pi / 10
 def _run(inst, solver, planned, **cfg):
     from paper_1503_03520_b200 import l1bench
 
-    old = os.environ.get("L1B_PCDM_PLAN")
-    os.environ["L1B_PCDM_PLAN"] = "1" if planned else "0"
+    env = {"L1B_PCDM_PLAN": "1" if planned else "0", "L1B_PCDM_PAIR": "0"}  # pair-local path off
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         x = np.empty(inst.n)
         tr = l1bench.run_solver(inst, l1bench.SolverConfig(id=solver, **cfg), x)
     finally:
-        if old is None:
-            del os.environ["L1B_PCDM_PLAN"]
-        else:
-            os.environ["L1B_PCDM_PLAN"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    assert tr.ran("pcdm_plan" if planned else "pcdm_direct"), f"path={tr.path:#x}"
     return tr, x
 
 
