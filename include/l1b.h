@@ -431,6 +431,32 @@ int l1b_session_k2(l1b_session* s);
 int l1b_session_finalize(l1b_session* s);
 int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
                     double* x_host);
+/* Serving a resident operator: restart the loop from x_0 = 0 (after
+ * l1b_problem_set_rhs, say) keeping the session's buffers, peer attachments,
+ * communicator and captured graphs; read reports a shard session's trace,
+ * summary and own x like l1b_session_end without ending it.                */
+int l1b_session_restart(l1b_session* s);
+int l1b_session_read(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
+                     double* x_host);
+/* Native shard driver (lagged two-iteration shards, the default protocol of
+ * banded 1..4-stage operators): the per-launch loop of distributed.py --
+ * k1; x halos by NCCL send / recv (or the kernels' peer stores); all-reduce
+ * of the 8 sums; finalize -- issued by the library on the session's stream
+ * with its own NCCL communicator, the steady state replayed from a CUDA
+ * graph of two launches.  This is the "per-iteration NCCL all-reduce of the
+ * partial A^T r" of the north star in its exact sparse form.
+ * NCCL is bound at run time (the process's libnccl.so.2).  unique_id: the
+ * 128-byte ncclUniqueId of l1b_nccl_get_unique_id on rank 0, broadcast by
+ * the caller.  The session's stream must not be the legacy default stream.
+ *   attach -> nccl_start -> nccl_steps(launches) ... -> nccl_finish -> end
+ * k1_ms (optional): events around every k1 instead of the graph; receives
+ * the summed k1 milliseconds of these launches.                            */
+int l1b_nccl_get_unique_id(void* id_out);
+int l1b_nccl_version(int* version);
+int l1b_session_attach_nccl(l1b_session* s, const void* unique_id, int rank, int world);
+int l1b_session_nccl_start(l1b_session* s);
+int l1b_session_nccl_steps(l1b_session* s, uint64_t launches, int use_graph, double* k1_ms);
+int l1b_session_nccl_finish(l1b_session* s);
 /* Kernel launches issued by the library since load (all entry points). */
 uint64_t l1b_launch_count(void);
 

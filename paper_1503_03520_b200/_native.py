@@ -156,6 +156,14 @@ SIGNATURES = [
     ("l1b_session_export_x_ipc", C.c_int, [vp, vp]),
     ("l1b_session_attach_peers_ipc", C.c_int, [vp, vp, u64, vp, u64]),
     ("l1b_session_kernel_mode", C.c_int, [vp, P(C.c_int)]),
+    ("l1b_session_restart", C.c_int, [vp]),
+    ("l1b_session_read", C.c_int, [vp, P(Sample), u64, P(Summary), P(f64)]),
+    ("l1b_nccl_get_unique_id", C.c_int, [vp]),
+    ("l1b_nccl_version", C.c_int, [P(C.c_int)]),
+    ("l1b_session_attach_nccl", C.c_int, [vp, vp, C.c_int, C.c_int]),
+    ("l1b_session_nccl_start", C.c_int, [vp]),
+    ("l1b_session_nccl_steps", C.c_int, [vp, u64, C.c_int, P(f64)]),
+    ("l1b_session_nccl_finish", C.c_int, [vp]),
 ]
 
 

@@ -35,6 +35,9 @@ struct OutOfMemory : std::runtime_error {
 struct Unsupported : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 #define L1B_CUDA(call) ::l1b::cuda_check((call), #call, __FILE__, __LINE__)

@@ -34,6 +34,9 @@ int guard(F&& f) {
   } catch (const CudaError& e) {
     last_error_slot() = e.what();
     return L1B_ECUDA;
+  } catch (const NcclError& e) {
+    last_error_slot() = e.what();
+    return L1B_ENCCL;
   } catch (const Unsupported& e) {
     last_error_slot() = e.what();
     return L1B_EUNSUPPORTED;

@@ -911,15 +911,23 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
   const int W_prev = B == 1 ? 0 : W;
   std::vector<void*> bufs;
-  auto alloc = [&](auto** ptr, size_t bytes) {
-    L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
+  auto alloc = [&](auto** ptr, size_t bytes) {  // out of memory: hand the run to the direct path
+    const cudaError_t e = cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8));
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw Unsupported("pcdm pairs: device memory");
+    }
+    L1B_CUDA(e);
     bufs.push_back((void*)*ptr);
   };
   int rc = 1;
   int* h_flag = nullptr;
   uint64_t* h_starts_pinned = nullptr;
   cudaStream_t gs = nullptr;  // generator stream
-  std::vector<cudaEvent_t> evs;
+  // stream positions relative to S[cur]: [0, gen_end) drawn (or queued on
+  // gs), the chunk starts at pos; pieces = (end, event) of each launch, dropped
+  // (event destroyed) once the chunk walk has moved past them
+  std::vector<std::pair<uint64_t, cudaEvent_t>> pieces;
   try {
     uint32_t* S[2] = {nullptr, nullptr};
     uint16_t* prevd;
@@ -958,12 +966,17 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     auto new_event = [&]() {
       cudaEvent_t e;
       L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      evs.push_back(e);
       return e;
+    };
+    auto drop_pieces = [&](uint64_t upto) {  // events of launches ending at or before upto
+      size_t k = 0;
+      while (k < pieces.size() && pieces[k].first <= upto) cudaEventDestroy(pieces[k++].second);
+      pieces.erase(pieces.begin(), pieces.begin() + k);
     };
     start();  // x = 0, r = -b, epoch-0 sample: the solve's clock starts here
     {
       cudaEvent_t e = new_event();
+      pieces.emplace_back(0, e);
       L1B_CUDA(cudaEventRecord(e, st));
       L1B_CUDA(cudaStreamWaitEvent(gs, e, 0));
     }
@@ -988,11 +1001,8 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     a.st = dst;
     a.trace = trace;
     a.partials = part;
-    // stream positions relative to S[cur]: [0, gen_end) drawn (or queued on
-    // gs), the chunk starts at pos; pieces = (end, event) of each launch
     int cur = 0;
     uint64_t pos = 0, gen_end = 0;
-    std::vector<std::pair<uint64_t, cudaEvent_t>> pieces;
     auto gen_to = [&](uint64_t upto) {
       while (gen_end < upto && gen_end + G <= scap) {
         gen_end += mt_stream_indices(win, G, n, S[cur] + gen_end, words, gs);
@@ -1025,7 +1035,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
         cur ^= 1;
         gen_end -= pos;
         pos = 0;
-        pieces.clear();
+        drop_pieces(~0ull);
         pieces.emplace_back(gen_end, new_event());
         L1B_CUDA(cudaEventRecord(pieces.back().second, st));
       }
@@ -1104,7 +1114,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       } else {
         L1B_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kPairThreads), args, 0, st));
         L1B_LAUNCHED();
-        cd_pair_fold<<<1, kThreads, 0, st>>>(part, (unsigned)grid, E, dst, trace);
+        cd_pair_fold<<<1, kPairThreads, 0, st>>>(part, (unsigned)grid, E, dst, trace);
         L1B_LAUNCHED();
       }
       const uint64_t used = h_starts_pinned[nb];
@@ -1113,6 +1123,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       L1B_CUDA(cudaStreamSynchronize(st));
       if (*h_flag & 4) throw Unsupported("pcdm pairs: event bucket");
       pos += used;  // the draws past the chunk's last block open the next chunk
+      drop_pieces(pos);
       launched += E;
       if (h_st->stop) break;
     }
@@ -1122,7 +1133,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     cudaStreamSynchronize(st);
     if (gs) cudaStreamSynchronize(gs);
     if (gs) cudaStreamDestroy(gs);
-    for (auto e : evs) cudaEventDestroy(e);
+    for (auto& pc : pieces) cudaEventDestroy(pc.second);
     for (void* q : bufs) cudaFree(q);
     if (h_flag) cudaFreeHost(h_flag);
     if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
@@ -1131,7 +1142,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   cudaStreamSynchronize(st);
   if (gs) cudaStreamSynchronize(gs);
   if (gs) cudaStreamDestroy(gs);
-  for (auto e : evs) cudaEventDestroy(e);
+  for (auto& pc : pieces) cudaEventDestroy(pc.second);
   for (void* q : bufs) cudaFree(q);
   if (h_flag) cudaFreeHost(h_flag);
   if (h_starts_pinned) cudaFreeHost(h_starts_pinned);

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "guard.hpp"
+#include "nccl_rt.hpp"
 #include "solvers.hpp"
 
 using namespace l1b;
@@ -89,6 +90,14 @@ struct l1b_session {
   std::vector<void*> ipc_opened;
   std::vector<double*> x_raw;  // cudaMalloc'd x buffers (shards: exportable over IPC)
 
+  // native shard driver (l1b_session_attach_nccl): the library's own NCCL
+  // communicator; graph[q] = two launches starting at launched % 4 == 2q,
+  // captured once and replayed
+  ncclComm_t comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  uint64_t graph_kernels[2] = {0, 0};
+
   PeerViews peers(uint64_t j) const {  // x_{j+1}, x_{j+2} of the neighbours
     PeerViews pv;
     if (!peers_on) return pv;
@@ -138,6 +147,9 @@ struct l1b_session {
   ~l1b_session() {
     cudaSetDevice(v.device);
     if (v.stream) cudaStreamSynchronize(v.stream);
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    if (comm) nccl().CommDestroy(comm);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (double* q : x_raw) cudaFree(q);
     for (void* q : allocs) cudaFreeAsync(q, v.stream);  // back to the stream-ordered pool
@@ -168,6 +180,8 @@ uint64_t sample_capacity(uint64_t max_iters) {
 
 // Keep freed pool memory cached on the device (release threshold = max), so
 // repeated solves on resident instances do not go back to the driver.
+
+void session_reset(l1b_session* s);
 
 void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   keep_pool(problem_view(p, false).device);
@@ -295,6 +309,17 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->trace = (FistaSample*)s->valloc(s->cap * sizeof(FistaSample));
   s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
+  if (s->recompute) fista_rc_prepare(*v.op, s->fma());  // module load + grid sizing before t0
+  session_reset(s);
+}
+
+// x_0 = 0 and the loop state of iteration 0 (begin, and l1b_session_restart)
+void session_reset(l1b_session* s) {
+  const ProblemView& v = s->v;
+  const l1b_solver_cfg* cfg = &s->cfg;
+  cudaStream_t st = v.stream;
+  if (s->single)  // every rotating buffer, halos included (the first launch reads X[3] as x_{-1})
+    for (int q = 0; q < s->nbuf; ++q) L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
   L1B_CUDA(cudaMemsetAsync(s->x, 0, s->nx * sizeof(double), st));
   if (s->accel && !s->single) L1B_CUDA(cudaMemsetAsync(s->y, 0, s->nx * sizeof(double), st));
   FistaDev h;
@@ -312,8 +337,9 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   h.init_tail = s->single ? v.tail_sq_band : 0.0;  // the init kernel covers rows [0, nr)
   h.lagged = s->recompute ? 1 : 0;
   *s->h_st = h;
-  if (s->recompute) fista_rc_prepare(*v.op, s->fma());  // module load + grid sizing before t0
   L1B_CUDA(cudaMemcpyAsync(s->st, s->h_st, sizeof(FistaDev), cudaMemcpyHostToDevice, st));
+  s->launched = 0;
+  s->time_out = false;
   s->t0 = std::chrono::steady_clock::now();
   // residuals over all (own) rows: rows >= m_active keep r = -b for the whole run
   fista_init(s->bufs(), s->nr, st);  // (single: writes r_0 into R[0] and R[2])
@@ -769,6 +795,26 @@ int l1b_session_sync(l1b_session* s, int* stopped, uint64_t* iterations) {
   });
 }
 
+int l1b_session_restart(l1b_session* s) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    if (s->general) throw Unsupported("restart: general shards keep no restartable state");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    session_reset(s);
+  });
+}
+
+int l1b_session_read(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
+                     double* x_host) {
+  return guard([&] {
+    if (!s) throw InvalidArgument("null session");
+    if (!s->shard) throw LogicError("read: single-device sessions report through l1b_session_end");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    l1b_summary tmp;
+    session_finish(s, samples, cap, summary ? summary : &tmp, x_host, nullptr);
+  });
+}
+
 int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summary* summary,
                     double* x_host) {
   const int rc = guard([&] {
@@ -855,6 +901,198 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     cudaEventDestroy(ev[1]);
     cudaFreeHost(h_flags);
     session_finish(&s, samples, cap, summary, x_host, d_x);
+  });
+}
+
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Native shard driver: the loop distributed.py drives from Python
+// (k1 -> halos -> all-reduce -> finalize per launch), issued here on the
+// session's stream with the library's own NCCL communicator and, for the
+// steady state, replayed from a CUDA graph of two launches (x rotates with
+// period 4, a launch advances it by 2), so no host work sits between the
+// kernels of consecutive launches.  Lagged two-iteration shards (the default
+// for banded 1..4-stage operators) only.
+
+namespace {
+
+void check_native(const l1b_session* s) {
+  if (!s) throw InvalidArgument("null session");
+  if (!(s->shard && s->single && s->recompute && s->pairs))
+    throw Unsupported("native shard driver: lagged two-iteration shards only (distributed.py drives the others)");
+}
+
+void check_comm(const l1b_session* s) {
+  check_native(s);
+  if (!s->comm) throw LogicError("no NCCL communicator: call l1b_session_attach_nccl first");
+}
+
+// launch j (iteration j+1, j+2): k1, then the x halos of both new iterates
+// (unless the kernel stored them into the neighbours), all-reduce of the 8
+// sums, finalize (records two iterations, lagged)
+void native_exchange(l1b_session* s, uint64_t j) {
+  const NcclApi& N = nccl();
+  cudaStream_t st = s->v.stream;
+  if (!s->peers_on && s->comm_world > 1) {
+    const size_t h = s->xh, own = s->nx;
+    L1B_NCCL(N.GroupStart());
+    for (int w = 1; w <= 2; ++w) {
+      double* win = s->X[(j + w) % 4];
+      if (s->comm_rank > 0) {
+        L1B_NCCL(N.Send(win + h, h, ncclDouble, s->comm_rank - 1, s->comm, st));
+        L1B_NCCL(N.Recv(win, h, ncclDouble, s->comm_rank - 1, s->comm, st));
+      }
+      if (s->comm_rank < s->comm_world - 1) {
+        L1B_NCCL(N.Send(win + own, h, ncclDouble, s->comm_rank + 1, s->comm, st));
+        L1B_NCCL(N.Recv(win + own + h, h, ncclDouble, s->comm_rank + 1, s->comm, st));
+      }
+    }
+    L1B_NCCL(N.GroupEnd());
+  }
+  L1B_NCCL(N.AllReduce(s->st->scal8, s->st->scal8, 8, ncclDouble, ncclSum, s->comm, st));
+  fista_finalize_launch(s->bufs(), st);
+}
+
+void native_launch(l1b_session* s, cudaEvent_t k1_begin = nullptr, cudaEvent_t k1_end = nullptr) {
+  const uint64_t j = s->launched;
+  if (k1_begin) L1B_CUDA(cudaEventRecord(k1_begin, s->v.stream));
+  s->iterate2(j, s->v.stream);
+  if (k1_end) L1B_CUDA(cudaEventRecord(k1_end, s->v.stream));
+  s->launched += 2;
+  native_exchange(s, j);
+}
+
+void native_reduce_finalize(l1b_session* s) {
+  L1B_NCCL(nccl().AllReduce(s->st->scal, s->st->scal, 4, ncclDouble, ncclSum, s->comm, s->v.stream));
+  fista_finalize_launch(s->bufs(), s->v.stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int l1b_nccl_get_unique_id(void* id_out) {
+  return guard([&] {
+    if (!id_out) throw InvalidArgument("null output");
+    ncclUniqueId id;
+    L1B_NCCL(nccl().GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int l1b_nccl_version(int* version) {
+  return guard([&] {
+    if (!version) throw InvalidArgument("null output");
+    *version = nccl().version;
+  });
+}
+
+int l1b_session_attach_nccl(l1b_session* s, const void* unique_id, int rank, int world) {
+  return guard([&] {
+    check_native(s);
+    if (!unique_id) throw InvalidArgument("null unique id");
+    if (world != s->v.world || rank != s->v.rank)
+      throw InvalidArgument("communicator rank / size differ from the shard's");
+    if (s->comm) throw LogicError("session already has a communicator");
+    if (!s->v.stream) throw InvalidArgument("the native driver needs a non-default stream (graph capture)");
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    const NcclApi& N = nccl();
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    L1B_NCCL(N.CommInitRank(&s->comm, world, id, rank));
+    s->comm_rank = rank;
+    s->comm_world = world;
+    // connect every channel this session uses (all-reduce, neighbour send /
+    // recv) outside of any capture: NCCL sets connections up on first use
+    double* tmp = s->dalloc(2 * s->xh + 8);
+    L1B_CUDA(cudaMemsetAsync(tmp, 0, (2 * s->xh + 8) * 8, s->v.stream));
+    L1B_NCCL(N.AllReduce(tmp, tmp, 8, ncclDouble, ncclSum, s->comm, s->v.stream));
+    if (world > 1) {
+      L1B_NCCL(N.GroupStart());
+      if (rank > 0) {
+        L1B_NCCL(N.Send(tmp + 8, s->xh, ncclDouble, rank - 1, s->comm, s->v.stream));
+        L1B_NCCL(N.Recv(tmp + 8 + s->xh, s->xh, ncclDouble, rank - 1, s->comm, s->v.stream));
+      }
+      if (rank < world - 1) {
+        L1B_NCCL(N.Send(tmp + 8, s->xh, ncclDouble, rank + 1, s->comm, s->v.stream));
+        L1B_NCCL(N.Recv(tmp + 8 + s->xh, s->xh, ncclDouble, rank + 1, s->comm, s->v.stream));
+      }
+      L1B_NCCL(N.GroupEnd());
+    }
+    L1B_CUDA(cudaStreamSynchronize(s->v.stream));
+  });
+}
+
+int l1b_session_nccl_start(l1b_session* s) {
+  return guard([&] {
+    check_comm(s);
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    native_reduce_finalize(s);  // f_0 from the summed ||b_own||^2
+  });
+}
+
+int l1b_session_nccl_steps(l1b_session* s, uint64_t launches, int use_graph, double* k1_ms) {
+  return guard([&] {
+    check_comm(s);
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    cudaStream_t st = s->v.stream;
+    if (k1_ms) {  // events around every k1 (no graph): the per-rank kernel time
+      std::vector<cudaEvent_t> ev(2 * launches);
+      for (auto& e : ev) L1B_CUDA(cudaEventCreate(&e));
+      for (uint64_t i = 0; i < launches; ++i) native_launch(s, ev[2 * i], ev[2 * i + 1]);
+      L1B_CUDA(cudaStreamSynchronize(st));
+      double tot = 0.0;
+      for (uint64_t i = 0; i < launches; ++i) {
+        float a = 0.f;
+        L1B_CUDA(cudaEventElapsedTime(&a, ev[2 * i], ev[2 * i + 1]));
+        tot += a;
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+      *k1_ms = tot;
+      return;
+    }
+    uint64_t i = 0;
+    if (use_graph) {
+      for (; i + 2 <= launches; i += 2) {
+        const int q = (int)((s->launched % 4) / 2);
+        if (!s->graph[q]) {  // capture launches j, j+1 (host bookkeeping rewound afterwards)
+          const uint64_t j0 = s->launched, k0 = g_launch_count.load();
+          cudaGraph_t g = nullptr;
+          L1B_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          try {
+            native_launch(s);
+            native_launch(s);
+          } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            s->launched = j0;
+            throw;
+          }
+          L1B_CUDA(cudaStreamEndCapture(st, &g));
+          s->graph_kernels[q] = g_launch_count.load() - k0;
+          g_launch_count.fetch_sub(s->graph_kernels[q]);  // counted when replayed
+          const cudaError_t e = cudaGraphInstantiate(&s->graph[q], g, 0);
+          cudaGraphDestroy(g);
+          L1B_CUDA(e);
+          s->launched = j0;
+        }
+        L1B_CUDA(cudaGraphLaunch(s->graph[q], st));
+        g_launch_count.fetch_add(s->graph_kernels[q]);
+        s->launched += 4;
+      }
+    }
+    for (; i < launches; ++i) native_launch(s);
+  });
+}
+
+int l1b_session_nccl_finish(l1b_session* s) {
+  return guard([&] {
+    check_comm(s);
+    L1B_CUDA(cudaSetDevice(s->v.device));
+    s->iterate(s->launched, s->v.stream, true);  // flush: ||r||^2 of the last iterate
+    native_reduce_finalize(s);
   });
 }
 

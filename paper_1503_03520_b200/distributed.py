@@ -211,6 +211,48 @@ class CudaShard:
             right, allh[self.rank + 1][1] if right is not None else 0))
         self.peer_halos = left is not None or right is not None
 
+    # -- native driver (l1b_session_attach_nccl ...): the per-launch loop of
+    # fista_iteration issued by the library with its own NCCL communicator,
+    # the steady state replayed from a CUDA graph (lagged two-iteration shards)
+    @property
+    def native_ok(self):
+        return self.single and self.lagged and self.pairs
+
+    def attach_nccl(self, group=None):
+        """ncclUniqueId from rank 0 to every rank (torch.distributed object
+        broadcast: plumbing), then the library's communicator."""
+        import torch.distributed as dist
+
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            N.check(self._lib.l1b_nccl_get_unique_id(uid))
+        obj = [bytes(uid) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        buf = (C.c_char * 128).from_buffer_copy(obj[0])
+        N.check(self._lib.l1b_session_attach_nccl(self.sess._s, buf, self.rank, self.world))
+
+    def native_start(self):
+        N.check(self._lib.l1b_session_nccl_start(self.sess._s))
+
+    def native_steps(self, launches: int, graph: bool = True, timed: bool = False):
+        """`launches` two-iteration launches; timed: events around every k1
+        (no graph), returns their summed milliseconds."""
+        ms = C.c_double(0.0)
+        N.check(self._lib.l1b_session_nccl_steps(self.sess._s, int(launches), 1 if graph else 0,
+                                                 C.byref(ms) if timed else None))
+        self.j += 2 * int(launches)
+        return ms.value if timed else None
+
+    def native_finish(self):
+        N.check(self._lib.l1b_session_nccl_finish(self.sess._s))
+
+    def restart(self):
+        self.sess.restart()
+        self.j = 0
+
+    def read(self, x_out=None):
+        return self.sess.read(x_out)
+
     def prox(self):
         N.check(self._lib.l1b_session_prox(self.sess._s))
 
@@ -363,6 +405,12 @@ def fista_iteration(be, group=None):
 
 
 def bench_main(args, world: int, rank: int, local: int):
+    """C4 row-sharded over the ranks (strong scaling), one JSON line on rank 0
+    with the same keys as the single-GPU line: value (iterations/s, device
+    time, max over ranks), roofline (per-rank k1 launch time from CUDA events,
+    48 bytes per own row per two-iteration launch), e2e (a new b from pinned
+    host memory, the sharded solve, own x back to the host; device time, max
+    over ranks) and cpu_baseline (rank 0, the reference on C4 itself)."""
     import torch
     import torch.distributed as dist
 
@@ -374,14 +422,23 @@ def bench_main(args, world: int, rank: int, local: int):
     os.environ.setdefault("RANK", str(rank))
     os.environ.setdefault("WORLD_SIZE", str(world))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from bench import C4, METRIC, UNIT, ClockSampler, peaks  # noqa: E402
+    from bench import C4, METRIC, UNIT, ClockSampler, peaks, run_reference  # noqa: E402
 
+    # the library's kernels and the collectives on one non-default stream
+    # (graph capture is not allowed on the legacy default stream)
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
     kw = dict(C4)
     kw["n"] = args.n
+    prof = 40  # launches with events around every k1 (roofline), after the timed region
+    e2e_passes = 0 if args.no_e2e else 4
+    launches_run = -(-args.warmup // 2) + -(-args.steps // 2) + prof + 4
+    cfg = l1bench.SolverConfig(max_iters=2 * launches_run, op="matrix_free", arith=args.arith)
     t0 = time.perf_counter()
-    cfg = l1bench.SolverConfig(max_iters=args.warmup + args.steps + 10)
     be = CudaShard(kw, rank, world, local, cfg)
+    torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
+    native = be.native_ok and os.environ.get("L1B_NATIVE_DIST", "1") != "0"
     peer = "off"
     if world > 1 and be.single and be.lagged and os.environ.get("L1B_PEER_HALOS", "1") != "0":
         try:  # halos by the kernels' own stores into the neighbours (cudaIpc, NVLink)
@@ -389,31 +446,85 @@ def bench_main(args, world: int, rank: int, local: int):
             peer = "on"
         except Exception as e:  # reported; the NCCL send / recv exchange stays
             peer = f"unavailable: {e}"
-    start(be)
-    with ClockSampler(local) as clk:
+    if native:
+        be.attach_nccl()
+        be.native_start()
+    else:
+        start(be)
+
+    def run(iters, graph=True):  # >= iters FISTA iterations; returns how many
+        if native:
+            launches = -(-iters // 2)
+            be.native_steps(launches, graph=graph)
+            return 2 * launches
         done = 0
-        while done < args.warmup:
+        while done < iters:
             done += fista_iteration(be)
+        return done
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clk:
+        run(args.warmup)
         torch.cuda.synchronize()
         dist.barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         launches0 = l1bench.launch_count()
-        ev0.record()
-        steps = 0  # iterations in the timed region (two per launch with pairs: K rounded up to even)
-        while steps < args.steps:
-            steps += fista_iteration(be)
-        ev1.record()
+        ev0.record(stream)
+        steps = run(args.steps)  # two iterations per launch: K rounded up to even
+        ev1.record(stream)
         torch.cuda.synchronize()
         launches = l1bench.launch_count() - launches0
         dist.barrier()
-    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_total = float(ms.item())
-    finish_lagged(be)
+        # roofline: the same launches with events around every k1 (no graph)
+        if native:
+            k1_ms = be.native_steps(prof, graph=False, timed=True) / prof
+        else:
+            k1_ms = None
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    if native:
+        be.native_finish()
+    else:
+        finish_lagged(be)
+    torch.cuda.synchronize()
     peer_check = verify_peer_halos(be) if be.peer_halos else None
     stopped, k = be.stopped()
-    tr, _ = be.finish()
+    peak, peak_src = peaks()
+    rf = None
+    if k1_ms is not None:
+        own_bytes = 48 * be.own  # x_k, x_{k-1}, sigma, b read, x_{k+1}, x_{k+2} written
+        per = torch.tensor([own_bytes, k1_ms], dtype=torch.float64, device="cuda")
+        allp = [torch.empty_like(per) for _ in range(world)]
+        dist.all_gather(allp, per)
+        allp = [(float(a[0]), float(a[1])) for a in allp]
+        worst = max(allp, key=lambda a: a[1])
+        agg = sum(a[0] for a in allp) / (max(a[1] for a in allp) * 1e-3) / 1e9
+        rf = {"bound": "hbm", "kernel": "fista_rc2 (two FISTA iterations per launch, matrix-free, "
+                                        "residuals recomputed) on each rank's row block",
+              "achieved": worst[0] / (worst[1] * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+              "frac": worst[0] / (worst[1] * 1e-3) / 1e9 / peak, "peak_source": peak_src,
+              "per_rank": [{"rank": r, "bytes_per_launch": a[0], "launch_ms": a[1],
+                            "achieved": a[0] / (a[1] * 1e-3) / 1e9} for r, a in enumerate(allp)],
+              "aggregate_achieved": agg, "aggregate_peak": world * peak, "aggregate_frac": agg / (world * peak),
+              "aggregate_frac_of_8tbs": agg / (world * 8000.0),
+              "launch_ms_source": f"CUDA events around every k1 of {prof} launches after the timed region "
+                                  "(slowest rank's kernel for achieved/frac)",
+              "traffic": None}
+    e2e_line = None
+    if e2e_passes and native:
+        e2e_line = _e2e_native(be, args, stream, e2e_passes, max_over_ranks)
+    tr = be.read()
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = run_reference(args, warmup=1, steps=2)
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "error": str(e)}
+    dist.barrier()
     if rank == 0:
         info = be.inst.info
         ips = steps / (ms_total / 1000.0)
@@ -424,24 +535,76 @@ def bench_main(args, world: int, rank: int, local: int):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator on device, seed 3)",
             "config": {"workload": f"C4 FISTA n=2^{int(math.log2(info.n))} row-sharded over {world} GPUs "
-                                   f"({be.own} rows/columns per GPU, halo {be.halo})",
-                       "l2": "inputs larger than L2 (no flush needed)",
+                                   f"({be.own} rows/columns per GPU, halo {be.x_halo})",
+                       "l2": "inputs larger than L2 (no flush needed)", "arith": args.arith,
+                       "driver": ("native: k1 -> halos -> NCCL all-reduce -> finalize issued by libl1b with "
+                                  "its own communicator, replayed from a CUDA graph of two launches"
+                                  if native else "python: torch.distributed per launch"),
                        "parallelism": (f"row-block shards x{world}: one matrix-free kernel per two iterations "
-                                       f"(residuals recomputed), NCCL P2P halos of two x vectors ({be.x_halo} "
-                                       f"doubles each per neighbour) + 8-double all-reduce per launch"
+                                       f"(residuals recomputed), halos of two x vectors ({be.x_halo} doubles "
+                                       f"each per neighbour: {'peer stores by the kernel' if be.peer_halos else 'NCCL send/recv'}) "
+                                       f"+ 8-double all-reduce per launch"
                                        if be.single and be.lagged and be.pairs else
-                                       f"row-block shards x{world}: one matrix-free kernel per iteration "
-                                       f"(residuals recomputed), NCCL P2P halo of x ({be.x_halo} doubles per "
-                                       f"neighbour) + 4-double all-reduce" if be.single and be.lagged else
-                                       f"row-block shards x{world}: one matrix-free kernel per iteration, "
-                                       f"NCCL P2P halo of x ({be.x_halo}) and r ({be.r_halo}) doubles per "
-                                       f"neighbour + 4-double all-reduce" if be.single else
-                                       f"row-block shards x{world}: NCCL P2P halo (2 x {be.halo} doubles "
-                                       f"per neighbour per iteration) + 4-double all-reduce")},
+                                       f"row-block shards x{world} (protocol of distributed.py)")},
             "gpu_launches": int(launches), "iterations_done": int(k), "generate_s": gen_s,
+            "final_objective": tr.final_objective,
             "peer_halos": peer, "peer_halo_check": peer_check,
+            "roofline": rf,
             "clocks": clk.summary(),
         }
+        if e2e_line is not None:
+            line["e2e"] = e2e_line
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
         print(json.dumps(line))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _e2e_native(be, args, stream, passes, max_over_ranks):
+    """Serving the resident sharded operator through the public API: every
+    pass uploads this rank's b (own rows + the window the kernel rebuilds r
+    on) from pinned host memory (l1b_problem_set_rhs), restarts the session
+    from x_0 = 0, runs K iterations of the sharded loop and reads the own x
+    back (l1b_session_read).  Device time between events on the library's
+    stream, max over ranks; median of the passes after the first."""
+    import torch
+    import torch.distributed as dist
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = a
+        return t
+
+    b_own = pinned(be.inst.b[:be.own])
+    lo, bw = be.inst.b_window()
+    b_win = pinned(bw)
+    x = torch.empty(be.own, dtype=torch.float64, pin_memory=True)
+    launches = -(-args.steps // 2)
+    times = []
+    for rep in range(passes):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        be.inst.set_rhs(b_own.numpy(), b_win.numpy())
+        be.restart()
+        be.native_start()
+        be.native_steps(launches, graph=True)
+        be.native_finish()
+        tr = be.read(x.numpy())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rep:
+            times.append(max_over_ranks(e0.elapsed_time(e1)))
+    ms = sorted(times)[len(times) // 2]
+    iters = 2 * launches
+    h2d = 8 * (b_own.numel() + b_win.numel())
+    d2h = 8 * be.own + 48 * len(tr.samples)
+    return {"value": iters / (ms * 1e-3), "unit": "iter/s", "h2d_bytes_per_step": h2d / iters,
+            "d2h_bytes_per_step": d2h / iters, "ms": ms, "ms_passes": times,
+            "includes": "per rank: H2D of b (own rows + kernel window) from pinned host memory "
+                        "(l1b_problem_set_rhs), session restart, K sharded FISTA iterations (native driver, "
+                        "NCCL), D2H of the own x and the trace (l1b_session_read); the operator (sigma, "
+                        "stages) stays resident; device time, max over ranks, median of the passes after one "
+                        "warm-up pass"}

@@ -325,7 +325,12 @@ class ProblemInstance:
         self._ext = None
         self.info = N.ProblemInfo()
         N.check(_lib().l1b_problem_info_get(self._h, C.byref(self.info)))
-        self.op = DeviceOperator(self)
+
+    @property
+    def op(self) -> DeviceOperator:
+        # a fresh view per access: a stored one would make instance <-> operator
+        # a reference cycle, and `del inst` would not free the device buffers
+        return DeviceOperator(self)
 
     def __del__(self):
         h, self._h = getattr(self, "_h", None), None
@@ -750,6 +755,17 @@ class Session:
         stopped, k = C.c_int(), C.c_uint64()
         N.check(_lib().l1b_session_sync(self._s, C.byref(stopped), C.byref(k)))
         return bool(stopped.value), int(k.value)
+
+    def restart(self):
+        """x_0 = 0 and iteration 0 again, on the same buffers (serving a new b)."""
+        N.check(_lib().l1b_session_restart(self._s))
+
+    def read(self, x_out: Optional[np.ndarray] = None, cap: int = 1 << 16) -> SolverTrace:
+        """Shard sessions: the trace and own x so far, without ending."""
+        samples = (N.Sample * cap)()
+        summ = N.Summary()
+        N.check(_lib().l1b_session_read(self._s, samples, cap, C.byref(summ), _ptr(x_out, _f64p)))
+        return _trace_from(self._name, samples, min(int(summ.n_samples), cap), summ)
 
     def end(self, x_out: Optional[np.ndarray] = None, cap: int = 1 << 16) -> SolverTrace:
         samples = (N.Sample * cap)()

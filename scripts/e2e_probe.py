@@ -1,4 +1,5 @@
-import sys, time, math
+"""e2e pass breakdown (create / solve / free) and device memory per pass."""
+import sys, time
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 from paper_1503_03520_b200 import l1bench
@@ -14,11 +15,15 @@ def pinned(a):
     return t.numpy()
 psig, pb = pinned(sig), pinned(b)
 px = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
-for label, s_, b_, x_ in [("pageable", sig, b, np.empty(n)), ("pinned", psig, pb, px), ("pinned2", psig, pb, px)]:
+K = int(sys.argv[1]) if len(sys.argv) > 1 else 500
+for rep in range(6):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    p = l1bench.ProblemInstance.from_host(m, n, stages, s_, b_, inst.tau, xs.support, xs.values, device=0)
+    p = l1bench.ProblemInstance.from_host(m, n, stages, psig, pb, inst.tau, xs.support, xs.values, device=0)
     torch.cuda.synchronize(); t1 = time.perf_counter()
-    tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=20), x_)
+    tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=K), px)
     torch.cuda.synchronize(); t2 = time.perf_counter()
-    print(label, "create %.1f ms" % ((t1 - t0) * 1e3), "solve+d2h %.1f ms" % ((t2 - t1) * 1e3), "iters", tr.iterations, "dev %.1f ms" % (tr.elapsed_s * 1e3))
     del p
+    torch.cuda.synchronize(); t3 = time.perf_counter()
+    free, tot = torch.cuda.mem_get_info()
+    print(f"pass {rep}: create {(t1-t0)*1e3:.1f} ms solve+d2h {(t2-t1)*1e3:.1f} ms (device {tr.elapsed_s*1e3:.1f}) "
+          f"free {(t3-t2)*1e3:.1f} ms; total {(t3-t0)*1e3:.1f} ms; device free {free/1e9:.1f} GB", flush=True)
