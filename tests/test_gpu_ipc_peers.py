@@ -47,7 +47,7 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_ipc_peer_halos_two_processes(tmp_path):
+def test_ipc_peer_halos_two_processes(tmp_path, oracle):
     import torch
 
     from gpu_util import need_cuda
@@ -64,3 +64,8 @@ def test_ipc_peer_halos_two_processes(tmp_path):
     np.testing.assert_array_equal(x, x_ref)
     f = parts[0]["f"]
     assert np.max(np.abs(f - tr.objectives()) / np.abs(tr.objectives())) < 1e-12
+    # and the reference's fista_run restated (the oracle), bit for bit
+    otr, ox = oracle.fista(oracle.build_instance(**KW), max_iters=ITERS)
+    np.testing.assert_array_equal(x, ox)
+    of = np.asarray(otr["objective"])
+    assert np.max(np.abs(f - of) / np.abs(of)) < 1e-12

@@ -52,6 +52,20 @@ def _exchange_many(shards, getter):
                 win[own + h:own + 2 * h].copy_(rwin[h:2 * h])
 
 
+def oracle_check(oracle, kw, iters, x, f, exact):
+    """The shards against the reference's fista_run restated (the oracle,
+    pinned bit-exact to the reference in tests/test_oracle.py)."""
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+    if exact:
+        np.testing.assert_array_equal(x, ox)
+    else:
+        assert rel_err(x, ox) < 1e-10
+    np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(ox)[0])
+    of = np.asarray(otr["objective"])
+    assert len(f) == len(of)
+    assert np.max(np.abs(f - of) / np.abs(of)) < 1e-12
+
+
 def _allreduce(shards):
     bufs = [getattr(s, "scal_now", s.scal) for s in shards]  # scal8 after a two-iteration step
     tot = sum(b.clone() for b in bufs)
@@ -61,7 +75,7 @@ def _allreduce(shards):
 
 @pytest.mark.parametrize("world,op", [(2, "sparse"), (3, "sparse"), (2, "matrix_free"), (3, "matrix_free"),
                                      (4, "matrix_free"), (2, "stored"), (3, "stored")])
-def test_shards_reproduce_single_device_fista(world, op):
+def test_shards_reproduce_single_device_fista(world, op, oracle):
     torch = need_cuda()
     from paper_1503_03520_b200 import l1bench
 
@@ -120,6 +134,7 @@ def test_shards_reproduce_single_device_fista(world, op):
         np.testing.assert_array_equal(x, x_ref)
     assert rel_err(x, x_ref) < 1e-12
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
+    oracle_check(oracle, KW, iters, x, outs[0][0].objectives(), exact=op == "matrix_free")
 
 
 def test_shard_rows_match_global_rows():
@@ -151,7 +166,7 @@ KW_PERM = dict(n=4096, stages=2, left_stages=1, permute=True, q=1, s_divisor=100
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_general_shards_reproduce_single_device_fista(world):
+def test_general_shards_reproduce_single_device_fista(world, oracle):
     """Permuted operator with a left stage (not banded): row blocks of A,
     columns of x split; the reduce-scatter of g and the all-gather of x are
     emulated by sums / copies between the shards' buffers."""
@@ -201,10 +216,11 @@ def test_general_shards_reproduce_single_device_fista(world):
     assert x.shape == x_ref.shape
     assert rel_err(x, x_ref) < 1e-12
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(x_ref)[0])
+    oracle_check(oracle, KW_PERM, iters, x, outs[0][0].objectives(), exact=False)
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_peer_halos_reproduce_single_device_fista(world):
+def test_peer_halos_reproduce_single_device_fista(world, oracle):
     """The kernels store the halo entries straight into the neighbours' x
     buffers (l1b_session_attach_peers; same device here, NVLink peers on a
     box): no halo exchange at all, the scalar all-reduce orders the steps."""
@@ -238,3 +254,4 @@ def test_peer_halos_reproduce_single_device_fista(world):
     x = np.concatenate([o[1] for o in outs])
     np.testing.assert_array_equal(x, x_ref)
     assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
+    oracle_check(oracle, KW, iters, x, outs[0][0].objectives(), exact=True)
