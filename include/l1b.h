@@ -81,6 +81,9 @@ int l1b_device_index_stream(int device, uint64_t seed, uint64_t n, const uint64_
 /* Host check of the jump polynomials: raw outputs 2^log2_jump ...
  * 2^log2_jump + count - 1 of std::mt19937_64(seed), reached by jumping. */
 int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, uint64_t* out);
+/* The same through t^(chunk * 79872) mod P: the start of chunk `chunk` of a
+ * coordinate stream (l1b_device_index_stream draws chunks of 312 x 256). */
+int l1b_mt_draws_after_chunk_jump(uint64_t seed, uint64_t chunk, uint64_t count, uint64_t* out);
 /* Returns s through *s_out; support (ascending) and values need capacity s. */
 int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
                                 uint32_t* support_out, double* values_out);

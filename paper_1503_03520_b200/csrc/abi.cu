@@ -412,6 +412,13 @@ int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, u
   });
 }
 
+int l1b_mt_draws_after_chunk_jump(uint64_t seed, uint64_t chunk, uint64_t count, uint64_t* out) {
+  return guard([&] {
+    if (!out && count) throw InvalidArgument("null output");
+    host_draws_after_chunk_jump(seed, chunk, count, out);
+  });
+}
+
 int l1b_device_uniform_draws(int device, uint64_t seed, uint64_t count, double lo, double hi,
                              int spectrum, double shift, uint64_t win_lo, uint64_t win_hi,
                              uint32_t min_log2_chunk, double* d_out, double* vmin, double* vmax,

@@ -21,12 +21,15 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <random>
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "solvers.hpp"
@@ -489,6 +492,33 @@ __global__ void cd_prevd_kernel(const uint32_t* __restrict__ idx, uint64_t L, in
   prevd[q] = d;
 }
 
+// The same look-back from a stable radix sort of (coordinate, position): in
+// sorted order the previous entry with the same key is the previous draw of
+// that coordinate.  key = coordinate, n for the reference's redraw marker.
+__global__ void cd_key_kernel(const uint32_t* __restrict__ idx, uint64_t L, uint32_t n,
+                              uint32_t* __restrict__ key, uint32_t* __restrict__ pos) {
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < L; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = idx[q];
+    key[q] = v == 0xffffffffu ? n : v;
+    pos[q] = (uint32_t)q;
+  }
+}
+
+__global__ void cd_prevd_sorted_kernel(const uint32_t* __restrict__ skey, const uint32_t* __restrict__ spos,
+                                       uint64_t L, uint32_t n, int W, uint16_t* __restrict__ prevd) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < L; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = skey[i], q = spos[i];
+    uint16_t d = 0;
+    if (k == n) {
+      d = kPrevRej;
+    } else if (i > 0 && skey[i - 1] == k) {
+      const uint32_t dist = q - spos[i - 1];
+      if (dist <= (uint32_t)W) d = (uint16_t)dist;
+    }
+    prevd[q] = d;
+  }
+}
+
 // Candidates: the positions whose previous draw of the same coordinate lies
 // within W (or that the reference redraws outright), in stream order, packed
 // (q << 16 | distance).  Tiles of kCandTile positions: count, scan, write.
@@ -550,32 +580,206 @@ __global__ void __launch_bounds__(kThreads) cd_cand_write(const uint16_t* __rest
   }
 }
 
+// ---- the walk to the block starts, on the device --------------------------
+// Block b spans [s_b, s_{b+1}): B kept draws plus the redrawn ones; candidate q
+// (its coordinate's previous draw d back) is redrawn in the block starting at s
+// iff d == kPrevRej or q - d >= s (rng.hpp:37-45 + the distinct-coordinate
+// rule of block PCDM).  The walk is sequential by definition, but through a
+// segment of kSegLen draws starting at S it depends only on the entry phase p =
+// (first block start >= S) - S, which lies in [0, W) since no block is longer
+// than W: F_S(p) = (exit phase, blocks started in the segment).  Every
+// (segment, phase) pair is walked at once (cd_seg_walk_kernel), the F are
+// composed up a binary tree (cd_seg_compose_kernel), each segment finds its
+// entry phase and block offset by descending the tree and re-walks itself to
+// write its block starts (cd_seg_emit_kernel).  No host round trip.
+constexpr uint64_t kSegLen = 4096;
+// one thread per item (these kernels are not grid-stride loops, unlike grid_for's users)
+inline unsigned blocks_for(uint64_t items) { return (unsigned)((items + kThreads - 1) / kThreads); }
+
+// walk from block start s to the first block start >= lim; out[base + t] = the
+// starts with base + t <= out_max (out may be null).  False: a block longer than W.
+// Candidates j0 .. j0 + ns - 1 come from the shared-memory copy sm.
+__device__ __forceinline__ bool walk_blocks(const uint64_t* __restrict__ cand, uint64_t ncand,
+                                            const uint64_t* sm, uint64_t j0, uint64_t ns, uint64_t& j,
+                                            uint64_t& s, uint64_t lim, uint64_t B, uint64_t W, uint32_t& cnt,
+                                            uint64_t* out, uint64_t base, uint64_t out_max) {
+  auto get = [&](uint64_t k) { return k - j0 < ns ? sm[k - j0] : cand[k]; };
+  while (s < lim) {
+    while (j < ncand && (get(j) >> 16) < s) ++j;
+    if (out && base + cnt <= out_max) out[base + cnt] = s;
+    uint64_t e = s + B;
+    while (j < ncand) {
+      const uint64_t c = get(j), q = c >> 16, d = c & 0xffff;
+      if (q >= e) break;
+      if (d == kPrevRej || q - d >= s) ++e;
+      ++j;
+    }
+    if (e - s > W) return false;
+    s = e;
+    ++cnt;
+  }
+  return true;
+}
+
+// a segment's candidates (from its first one on, at most kSegCand) into smem
+constexpr int kSegCand = 1024;
+// (a segment's walks read candidates below S + L + W < S + 2L: up to the first
+// one of segment seg + 2)
+__device__ __forceinline__ uint64_t stage_candidates(const uint64_t* __restrict__ cand, uint64_t ncand,
+                                                     const uint64_t* __restrict__ seg_first, uint64_t seg,
+                                                     uint64_t nseg, uint64_t* sm, int tid, int nthreads) {
+  const uint64_t j0 = seg_first[seg], j1 = seg + 2 < nseg ? seg_first[seg + 2] : ncand;
+  const uint64_t ns = j1 - j0 < (uint64_t)kSegCand ? j1 - j0 : (uint64_t)kSegCand;
+  for (uint64_t t = tid; t < ns; t += nthreads) sm[t] = cand[j0 + t];
+  return ns;
+}
+
+__device__ __forceinline__ uint64_t cand_lower_bound(const uint64_t* __restrict__ cand, uint64_t ncand,
+                                                     uint64_t pos) {
+  uint64_t lo = 0, hi = ncand;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if ((cand[mid] >> 16) < pos) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void cd_seg_first_kernel(const uint64_t* __restrict__ cand, const uint32_t* ncand_p, uint64_t nseg,
+                                    uint64_t* __restrict__ seg_first) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < nseg) seg_first[i] = cand_lower_bound(cand, *ncand_p, i * kSegLen);
+}
+
+// F[seg * W + p] = exit phase | blocks << 32: one CTA per segment, thread p
+// walks from phase p (the segment's candidates staged in shared memory)
+__global__ void cd_seg_walk_kernel(const uint64_t* __restrict__ cand, const uint32_t* ncand_p,
+                                   const uint64_t* __restrict__ seg_first, uint64_t nseg, uint64_t B, uint64_t W,
+                                   uint64_t* __restrict__ F, int* flag) {
+  __shared__ uint64_t sm[kSegCand];
+  const uint64_t seg = blockIdx.x, p = threadIdx.x;
+  const uint64_t ncand = *ncand_p, j0 = seg_first[seg];
+  const uint64_t ns = stage_candidates(cand, ncand, seg_first, seg, nseg, sm, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const uint64_t lim = (seg + 1) * kSegLen;
+  for (uint64_t ph = p; ph < W; ph += blockDim.x) {
+    uint64_t s = seg * kSegLen + ph, j = j0;
+    uint32_t cnt = 0;
+    if (!walk_blocks(cand, ncand, sm, j0, ns, j, s, lim, B, W, cnt, nullptr, 0, 0)) {
+      atomicOr(flag, 16);  // the run is handed over; keep the tree's indices in range
+      F[seg * W + ph] = 0;
+      continue;
+    }
+    F[seg * W + ph] = (s - lim) | ((uint64_t)cnt << 32);
+  }
+}
+
+// parent node i of level l+1 = child 2i, then child 2i + 1 (when it exists).
+// A CTA composes kComposeLevels levels of the subtree over 2^kComposeLevels
+// nodes of level l0 (level by level, barriers between): 3 launches for ~1000
+// segments instead of one per level.
+constexpr int kComposeLevels = 4;
+struct LevelTab {
+  uint64_t off[40], cnt[40];
+};
+__global__ void cd_seg_compose_kernel(uint64_t* __restrict__ lv, LevelTab tab, int l0, int l1, uint64_t W) {
+  for (int l = l0; l < l1; ++l) {
+    const uint64_t n_child = tab.cnt[l], n_par = tab.cnt[l + 1];
+    const uint64_t span = 1ull << (l + 1 - l0);  // parents of this CTA at level l + 1
+    const uint64_t first = (uint64_t)blockIdx.x << (kComposeLevels - (l + 1 - l0));
+    const uint64_t* child = lv + tab.off[l];
+    uint64_t* parent = lv + tab.off[l + 1];
+    const uint64_t count = (kComposeLevels >= (l + 1 - l0) ? (1ull << (kComposeLevels - (l + 1 - l0))) : 1) * W;
+    (void)span;
+    for (uint64_t t = threadIdx.x; t < count; t += blockDim.x) {
+      const uint64_t i = first + t / W, p = t % W;
+      if (i >= n_par) continue;
+      const uint64_t a = child[(2 * i) * W + p];
+      if (2 * i + 1 >= n_child) {
+        parent[i * W + p] = a;
+        continue;
+      }
+      const uint64_t b = child[(2 * i + 1) * W + (a & 0xffffffffull)];
+      parent[i * W + p] = (b & 0xffffffffull) | (((a >> 32) + (b >> 32)) << 32);
+    }
+    __syncthreads();  // (the next level reads this one's nodes, written by this CTA)
+  }
+}
+
+// segment i (one warp each): entry (phase, block offset) from the root down (a
+// right child enters where its left sibling exits), then its block starts into
+// starts[] (entries <= nb; starts[nb] = the end of the chunk's last block)
+__global__ void __launch_bounds__(128) cd_seg_emit_kernel(const uint64_t* __restrict__ cand, const uint32_t* ncand_p,
+                                   const uint64_t* __restrict__ seg_first, const uint64_t* __restrict__ levels,
+                                   const uint64_t* __restrict__ level_off, int nlevels, uint64_t nseg, uint64_t B,
+                                   uint64_t W, uint64_t nb, uint64_t* __restrict__ starts) {
+  __shared__ uint64_t smem[4][kSegCand];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t i = blockIdx.x * 4ull + w;
+  if (i >= nseg) return;
+  const uint64_t ncand = *ncand_p, j0 = seg_first[i];
+  const uint64_t ns = stage_candidates(cand, ncand, seg_first, i, nseg, smem[w], lane, 32);
+  __syncwarp();
+  if (lane) return;
+  uint64_t p = 0, off = 0;
+  for (int l = nlevels - 2; l >= 0; --l) {
+    const uint64_t c = i >> l;
+    if (c & 1) {
+      const uint64_t v = levels[level_off[l] + (c - 1) * W + p];
+      off += v >> 32;
+      p = v & 0xffffffffull;
+    }
+  }
+  if (off > nb) return;
+  uint64_t s = i * kSegLen + p, j = j0;
+  uint32_t cnt = 0;
+  walk_blocks(cand, ncand, smem[w], j0, ns, j, s, (i + 1) * kSegLen, B, W, cnt, starts, off, nb);
+}
+
+// B = 1 (serial CD): no look-back, a block is the rejected raw draws before
+// one kept draw: s_{b+1} = (position of kept draw b) + 1 = b + k + 1, k = the
+// rejected positions before it (~never: p = n / 2^64 per draw)
+__global__ void cd_b1_starts_kernel(const uint64_t* __restrict__ cand, const uint32_t* ncand_p, uint64_t nb,
+                                    uint64_t* __restrict__ starts) {
+  const uint64_t nc = *ncand_p;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= nb; b += (uint64_t)gridDim.x * blockDim.x) {
+    if (b == 0) {
+      starts[0] = 0;
+      continue;
+    }
+    uint64_t k = 0;
+    while (k < nc && (cand[k] >> 16) <= (b - 1) + k) ++k;
+    starts[b] = b + k;
+  }
+}
+
 __global__ void cd_iota_kernel(uint64_t* s, uint64_t count) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
     s[i] = i;
 }
 
+// `lanes` (1 or 32) threads per block b: its draws are [s[b], s[b + 1]); a
+// draw is redrawn iff its previous draw of the same coordinate lies in the block
 __global__ void cd_scatter_kernel(const uint32_t* __restrict__ idx, const uint16_t* __restrict__ prevd,
                                   const uint64_t* __restrict__ s, uint64_t nb, uint64_t per_epoch,
-                                  int off, uint64_t U, uint32_t* cnt, uint32_t* ev, int* flag) {
-  const uint64_t end = s[nb];
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < end;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint16_t d = prevd[q];
-    if (d == kPrevRej) continue;
-    uint64_t lo = 0, hi = nb;  // block b: s[b] <= q < s[b + 1]
-    while (hi - lo > 1) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (s[mid] <= q) lo = mid;
-      else hi = mid;
+                                  int off, uint64_t U, int lanes, uint32_t* cnt, uint32_t* ev, int* flag,
+                                  uint64_t have) {
+  const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / lanes;
+  const int lane = lanes == 1 ? 0 : (threadIdx.x & 31);
+  const uint64_t lim = s[nb] < have ? s[nb] : have;  // (a failed walk is handed over after the launch)
+  for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / lanes; b < nb; b += groups) {
+    const uint64_t s0 = min(s[b], lim), s1 = min(s[b + 1], lim);
+    const uint64_t e = b / per_epoch, bl = b % per_epoch;
+    for (uint64_t q = s0 + lane; q < s1; q += lanes) {
+      const uint16_t d = prevd[q];
+      if (d == kPrevRej) continue;
+      if (d != 0 && (uint64_t)d <= q - s0) continue;  // redrawn
+      const uint64_t i = idx[q] + (uint64_t)off;
+      const uint64_t u = i >> 1;
+      const uint32_t slot = atomicAdd(&cnt[e * U + u], 1u);
+      if (slot < (uint32_t)kEvCap) ev[(e * kEvCap + slot) * U + u] = (uint32_t)(bl << 1) | (uint32_t)(i & 1);
+      else atomicOr(flag, 4);
     }
-    if (d != 0 && (uint64_t)d <= q - s[lo]) continue;  // redrawn
-    const uint64_t e = lo / per_epoch, bl = lo % per_epoch;
-    const uint64_t i = idx[q] + (uint64_t)off;
-    const uint64_t u = i >> 1;
-    const uint32_t slot = atomicAdd(&cnt[e * U + u], 1u);
-    if (slot < (uint32_t)kEvCap) ev[(e * kEvCap + slot) * U + u] = (uint32_t)(bl << 1) | (uint32_t)(i & 1);
-    else atomicOr(flag, 4);
   }
 }
 
@@ -589,33 +793,50 @@ struct CdPairArgs {
   const double* cval;
   double *x, *r;
   const uint32_t *cnt, *ev;
+  const unsigned long long* mask;  // event masks (MW > 0)
   uint64_t epochs;  // of this launch
   CdDev* st;
   CdSample* trace;
-  double* partials;  // 2 x grid x 5
+  double* partials;  // (SYNC: 2, else epochs) x warps x 5
 };
 
-// the objective of an epoch from the blocks' partials (fixed order: every
-// caller folds identically) and cd_stats_kernel's bookkeeping
-__device__ __forceinline__ void epoch_objective(const double* part, unsigned nblocks, double tau, double& f,
-                                                double& nnz, double& applied, double& colops) {
+// the objective of an epoch from the blocks' partials, folded by ONE warp in a
+// fixed order (lane-strided sums, then a shuffle tree; lane 0's result): every
+// caller -- the SYNC epoch kernel's warp 0, the fold kernel's warp per epoch --
+// reduces identically, so a run with a target records the same bits as one
+// without.  Returns f, nnz, applied, colops in every lane.
+template <bool CG = true>
+__device__ __forceinline__ void epoch_objective_warp(const double* part, unsigned nblocks, double tau,
+                                                     double& f, double& nnz, double& applied,
+                                                     double& colops) {
+  const int lane = threadIdx.x & 31;
   double tot[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (unsigned q = threadIdx.x; q < nblocks; q += blockDim.x) {
+  for (unsigned q0 = lane; q0 < nblocks; q0 += 128) {  // rows q0, q0 + 32, ..: loads first, sums in order
+    double v[4][5];
 #pragma unroll
-    for (int w = 0; w < 5; ++w) tot[w] += __ldcg(&part[(size_t)q * 5 + w]);
-  }
-  block_sum<5>(tot);
-  __shared__ double bc[5];
-  if (threadIdx.x == 0) {
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-    for (int w = 0; w < 5; ++w) bc[w] = tot[w];
+      for (int w = 0; w < 5; ++w) {
+        const double* a = &part[(size_t)(q0 + 32 * j) * 5 + w];
+        v[j][w] = q0 + 32 * j < nblocks ? (CG ? __ldcg(a) : *a) : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (q0 + 32 * j < nblocks)
+#pragma unroll
+        for (int w = 0; w < 5; ++w) tot[w] += v[j][w];
   }
-  __syncthreads();
-  f = tau * bc[0] + 0.5 * bc[2];
-  nnz = bc[1];
-  applied = bc[3];
-  colops = bc[4];
-  __syncthreads();
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int w = 0; w < 5; ++w) tot[w] += __shfl_down_sync(0xffffffffu, tot[w], o);
+  }
+#pragma unroll
+  for (int w = 0; w < 5; ++w) tot[w] = __shfl_sync(0xffffffffu, tot[w], 0);
+  f = tau * tot[0] + 0.5 * tot[2];
+  nnz = tot[1];
+  applied = tot[3];
+  colops = tot[4];
 }
 
 // stop: 0 = go on, 1 = target, 2 = non-finite, 3 = epoch budget
@@ -634,29 +855,102 @@ __device__ __forceinline__ void epoch_record(CdDev* st, CdSample* trace, uint64_
   }
 }
 
-// !SYNC launches: the samples of its epochs, in order (one CTA)
+// !SYNC launches: the samples of its epochs, in order -- a warp folds each
+// epoch and writes its sample (all SMs); the last CTA to finish (threadfence +
+// ticket) finds the first stopping epoch and writes the loop state.  The sample
+// count of epoch ep is n_samples + ep: a record loop has no other state.
+constexpr int kFoldMax = 256;  // epochs per launch (the chunk's E <= this)
 __global__ void cd_pair_fold(const double* partials, unsigned nblocks, uint64_t epochs, CdDev* st,
-                             CdSample* trace) {
+                             CdSample* trace, double* vals, unsigned* ticket) {
   if (*(volatile int*)&st->stop) return;
-  const uint64_t epoch0 = st->epoch, max_epochs = st->max_epochs;
-  const double tau = st->tau;
-  for (uint64_t ep = 0; ep < epochs; ++ep) {
+  const uint64_t ep = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t epoch0 = st->epoch, max_epochs = st->max_epochs, cap = st->cap, ns0 = st->n_samples;
+  if (ep < epochs) {
     double f, nnz, applied, colops;
-    epoch_objective(partials + (size_t)ep * nblocks * 5, nblocks, tau, f, nnz, applied, colops);
-    const uint64_t epoch = epoch0 + ep + 1;
-    const int stop = !isfinite(f) ? 2 : epoch >= max_epochs ? 3 : 0;
-    if (threadIdx.x == 0) epoch_record(st, trace, epoch, f, nnz, applied, colops, stop);
-    if (stop) break;
+    epoch_objective_warp<false>(partials + (size_t)ep * nblocks * 5, nblocks, st->tau, f, nnz, applied, colops);
+    if ((threadIdx.x & 31) == 0) {
+      vals[ep * 4 + 0] = f;
+      vals[ep * 4 + 1] = nnz;
+      vals[ep * 4 + 2] = applied;
+      vals[ep * 4 + 3] = colops;
+      const uint64_t slot = ns0 + ep;  // (samples after a stopping epoch lie past n_samples: never read)
+      if (slot < cap) trace[slot] = CdSample{epoch0 + ep + 1, f, nnz, applied, colops, global_timer_ns()};
+    }
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the first epoch that stops the run: non-finite objective or the epoch budget
+  __shared__ unsigned long long first;
+  if (threadIdx.x == 0) first = epochs;
+  __syncthreads();
+  for (uint64_t e = threadIdx.x; e < epochs; e += blockDim.x) {
+    const double f = __ldcg(&vals[e * 4]);
+    if (!isfinite(f) || epoch0 + e + 1 >= max_epochs) atomicMin(&first, (unsigned long long)e);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint64_t lastep = first < epochs ? first : epochs - 1;
+  const double f = __ldcg(&vals[lastep * 4]);
+  st->n_samples = ns0 + lastep + 1;
+  st->epoch = epoch0 + lastep + 1;
+  st->applied = (unsigned long long)__ldcg(&vals[lastep * 4 + 2]);
+  st->colops = (unsigned long long)__ldcg(&vals[lastep * 4 + 3]);
+  st->f = f;
+  st->last_ts = global_timer_ns();
+  if (first < epochs) {
+    st->stop = 1;
+    st->status = !isfinite(f) ? -1 : 1;
+  }
+  *ticket = 0;  // ready for the next launch
+}
+
+constexpr int kPairThreads = 128;  // more SMs, one warp per sub-partition (the epoch is a latency chain)
+
+// Event masks (the default when an epoch has at most 64 MW blocks, C2: 128):
+// bit bl of mask[e][member][bl >> 6][u] = member `member` of pair u steps in
+// block bl of epoch e.  Ascending set bits are the pair's events in block
+// order: no per-pair sort, no event list.  MW = 0: the event lists (cnt / ev).
+__global__ void cd_mask_scatter_kernel(const uint32_t* __restrict__ idx, const uint16_t* __restrict__ prevd,
+                                       const uint64_t* __restrict__ s, uint64_t nb, uint64_t per_epoch,
+                                       int off, uint64_t U, int MW, unsigned long long* __restrict__ mask,
+                                       uint64_t have) {
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t lim = s[nb] < have ? s[nb] : have;  // (a failed walk is handed over after the launch)
+  for (uint64_t b = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; b < nb; b += warps) {
+    const uint64_t s0 = min(s[b], lim), s1 = min(s[b + 1], lim);
+    const uint64_t e = b / per_epoch, bl = b % per_epoch;
+    for (uint64_t q = s0 + lane; q < s1; q += 32) {
+      const uint16_t d = prevd[q];
+      if (d == kPrevRej) continue;
+      if (d != 0 && (uint64_t)d <= q - s0) continue;  // redrawn
+      const uint64_t i = idx[q] + (uint64_t)off;
+      const uint64_t u = i >> 1, mem = i & 1;
+      atomicOr(&mask[((e * 2 + mem) * MW + (bl >> 6)) * U + u], 1ull << (bl & 63));
+    }
   }
 }
 
+// sum of 5 doubles over the warp, lane 0 (fixed order)
+__device__ __forceinline__ void warp_sum5(double* v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int w = 0; w < 5; ++w) v[w] += __shfl_down_sync(0xffffffffu, v[w], o);
+}
+
 // SYNC: a grid barrier per epoch, the objective and the stop test in the
-// kernel (runs with a target).  !SYNC: epochs back to back, each block's
-// partials kept per epoch; cd_pair_fold records the samples afterwards (no
-// target: only the epoch budget or a non-finite objective stops a run, and the
-// budget is the launch's epoch count).
-constexpr int kPairThreads = 128;  // more SMs, one warp per sub-partition (the epoch is a latency chain)
-template <int P, bool SYNC>
+// kernel (runs with a target).  !SYNC: epochs back to back, each WARP's
+// partials kept per epoch (no block barrier: warps run their epochs
+// independently); cd_pair_fold records the samples afterwards (no target: only
+// the epoch budget or a non-finite objective stops a run, and the budget is
+// the launch's epoch count).
+template <int P, bool SYNC, int MW>
 __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
   namespace cg = cooperative_groups;
   CdDev* st = A.st;
@@ -668,6 +962,7 @@ __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
   const int64_t n = (int64_t)A.n;
   const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const unsigned nwarps = (unsigned)(T >> 5), gwarp = (unsigned)(g0 >> 5);
   const double c = A.c, s = A.s;
   // per pair: members e = 0, 1 (coordinates a + e), column entries (row member, value)
   double x[P][2], r[P][2], sig[P][2], bb[P][2], li[P][2], cv[P][2][2];
@@ -704,12 +999,118 @@ __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
       }
     }
   }
+  // the step's scale beta L_i and threshold tau / (beta L_i) (solvers.cpp:457-458),
+  // the same operations on the same operands as every step recomputes them
+  double sc[P][2], th[P][2];
+#pragma unroll
+  for (int k = 0; k < P; ++k)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      sc[k][e] = beta * li[k][e];
+      th[k][e] = tau / sc[k][e];
+    }
   // rows [n, m) stay 0 - b (empty rows): their ||r||^2 share, once
   double tail = 0.0;
   for (uint64_t i = (uint64_t)n + g0; i < A.m; i += T) tail += A.r[i] * A.r[i];
-  // the bucket count and first kPre events of the next epoch are loaded one
-  // epoch ahead (independent of the running epoch)
+  double acc[5];  // ||x||_1, nnz, ||r||^2, applied, colops of the running epoch
+  // one block of pair k: the members in `in` step against the block's residual
+  // rows, then the rows take r + sum_c delta_c A(rho, c) in ascending column order
+  auto block_step = [&](int k, int in) {
+    const double r0 = r[k][0], r1 = r[k][1];
+    double d[2] = {0.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (!((in >> e) & 1) || li[k][e] == 0.0) continue;  // zero columns are skipped (solvers.cpp:455)
+      double gi = 0.0;
+      for (int q = 0; q < nc[k][e]; ++q) gi += cv[k][e][q] * (cr[k][e][q] ? r1 : r0);
+      acc[4] += 1.0;
+      const double xi = x[k][e];
+      const double xn = soft_threshold(xi - gi / sc[k][e], th[k][e]);
+      d[e] = xn - xi;
+      if (d[e] != 0.0) {
+        x[k][e] = xn;
+        acc[3] += 1.0;
+        acc[4] += 1.0;
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      double v = f ? r1 : r0;
+      bool any = false;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (d[e] == 0.0) continue;
+        for (int q = 0; q < nc[k][e]; ++q)
+          if (cr[k][e][q] == f) {
+            v += d[e] * cv[k][e][q];
+            any = true;
+          }
+      }
+      if (any) r[k][f] = v;
+    }
+  };
+  // one member e alone in its block (the common case: a block holds B of n
+  // coordinates): block_step(k, 1 << e) with the member picked by selects, so a
+  // warp runs one FP64 division per event instead of both members' code
+  auto one_step = [&](int k, int e) {
+    const double lie = e ? li[k][1] : li[k][0];
+    if (lie == 0.0) return;  // zero columns are skipped (solvers.cpp:455)
+    const double r0 = r[k][0], r1 = r[k][1];
+    const int nce = e ? nc[k][1] : nc[k][0];
+    const int c0 = e ? cr[k][1][0] : cr[k][0][0], c1 = e ? cr[k][1][1] : cr[k][0][1];
+    const double v0 = e ? cv[k][1][0] : cv[k][0][0], v1 = e ? cv[k][1][1] : cv[k][0][1];
+    double gi = 0.0;
+    if (nce > 0) gi += v0 * (c0 ? r1 : r0);
+    if (nce > 1) gi += v1 * (c1 ? r1 : r0);
+    acc[4] += 1.0;
+    const double xi = e ? x[k][1] : x[k][0];
+    const double xn = soft_threshold(xi - gi / (e ? sc[k][1] : sc[k][0]), e ? th[k][1] : th[k][0]);
+    const double d = xn - xi;
+    if (d == 0.0) return;
+    if (e) x[k][1] = xn;
+    else x[k][0] = xn;
+    acc[3] += 1.0;
+    acc[4] += 1.0;
+    double w0 = r0, w1 = r1;
+    bool a0 = false, a1 = false;
+    if (nce > 0) {
+      if (c0) { w1 += d * v0; a1 = true; } else { w0 += d * v0; a0 = true; }
+    }
+    if (nce > 1) {
+      if (c1) { w1 += d * v1; a1 = true; } else { w0 += d * v1; a0 = true; }
+    }
+    if (a0) r[k][0] = w0;
+    if (a1) r[k][1] = w1;
+  };
+  auto step = [&](int k, int in) {
+    if (in == 3) block_step(k, 3);
+    else one_step(k, in >> 1);
+  };
+  // MW > 0: the masks are loaded two epochs ahead; MW == 0: the bucket count
+  // and first kPre events one epoch ahead
   constexpr int kPre = 4;
+  constexpr int NM = MW > 0 ? 2 * MW : 1;
+  // mask mode: a 3-epoch ring in shared memory filled by cp.async two epochs
+  // ahead (no registers held by pending loads)
+  __shared__ __align__(16) unsigned long long mring[MW > 0 ? 3 : 1][kPairThreads][MW > 0 ? P * NM : 1];
+  auto issue_masks = [&](uint64_t ep) {
+    if constexpr (MW > 0) {
+      if (ep < A.epochs) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          if (!live[k]) continue;
+          const uint64_t u = g0 + (uint64_t)k * T;
+#pragma unroll
+          for (int w = 0; w < NM; ++w) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&mring[ep % 3][threadIdx.x][k * NM + w]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+                         "l"(&A.mask[(ep * NM + w) * A.U + u]));
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;");
+    }
+  };
   uint32_t pc[P], pk[P][kPre];
   auto prefetch = [&](uint64_t ep) {
 #pragma unroll
@@ -722,70 +1123,67 @@ __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
       for (int j = 0; j < kPre; ++j) pk[k][j] = __ldcg(&A.ev[(ep * kEvCap + j) * A.U + u]);
     }
   };
-  prefetch(0);
+  if constexpr (MW > 0) {
+    issue_masks(0);
+    issue_masks(1);
+  } else {
+    prefetch(0);
+  }
   for (uint64_t ep = 0; ep < A.epochs; ++ep) {
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // ||x||_1, nnz, ||r||^2, applied, colops
+#pragma unroll
+    for (int w = 0; w < 5; ++w) acc[w] = 0.0;
+    unsigned long long cur_m[P][NM];
     uint32_t cur_c[P], cur_k[P][kPre];
+    if constexpr (MW > 0) {
+      issue_masks(ep + 2);
+      asm volatile("cp.async.wait_group 2;" ::: "memory");  // epoch ep's group has landed
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      cur_c[k] = pc[k];
+      for (int k = 0; k < P; ++k)
 #pragma unroll
-      for (int j = 0; j < kPre; ++j) cur_k[k][j] = pk[k][j];
+        for (int w = 0; w < NM; ++w) cur_m[k][w] = live[k] ? mring[ep % 3][threadIdx.x][k * NM + w] : 0ull;
+    } else {
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        cur_c[k] = pc[k];
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) cur_k[k][j] = pk[k][j];
+      }
+      prefetch(ep + 1);
     }
-    prefetch(ep + 1);
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       if (!live[k]) continue;
-      const uint64_t u = g0 + (uint64_t)k * T;
-      const int cnt = min((int)cur_c[k], kEvCap);
-      uint32_t key[kEvCap];
-      for (int j = 0; j < cnt; ++j) {
-        const uint32_t v = j < kPre ? cur_k[k][j] : __ldcg(&A.ev[(ep * kEvCap + j) * A.U + u]);
-        int q = j;  // insertion sort: ascending (block, member)
-        while (q > 0 && key[q - 1] > v) {
-          key[q] = key[q - 1];
-          --q;
-        }
-        key[q] = v;
-      }
-      int j = 0;
-      while (j < cnt) {
-        const uint32_t bl = key[j] >> 1;
-        int in = 0;  // bit e: member e steps in this block
-        while (j < cnt && (key[j] >> 1) == bl) in |= 1 << (key[j++] & 1);
-        const double r0 = r[k][0], r1 = r[k][1];  // the block's residual
-        double d[2] = {0.0, 0.0};
+      if constexpr (MW > 0) {
+        // member masks m0 = cur_m[k][0 .. MW), m1 = cur_m[k][MW .. 2 MW): set
+        // bits of their union in ascending order = the pair's blocks
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (!((in >> e) & 1) || li[k][e] == 0.0) continue;  // zero columns are skipped (solvers.cpp:455)
-          double gi = 0.0;
-          for (int q = 0; q < nc[k][e]; ++q) gi += cv[k][e][q] * (cr[k][e][q] ? r1 : r0);
-          acc[4] += 1.0;
-          const double scale = beta * li[k][e];
-          const double xi = x[k][e];
-          const double xn = soft_threshold(xi - gi / scale, tau / scale);
-          d[e] = xn - xi;
-          if (d[e] != 0.0) {
-            x[k][e] = xn;
-            acc[3] += 1.0;
-            acc[4] += 1.0;
+        for (int w = 0; w < MW; ++w) {
+          unsigned long long m0 = cur_m[k][w], m1 = cur_m[k][MW + w], both = m0 | m1;
+          while (both) {
+            const unsigned long long bit = both & (~both + 1ull);
+            both ^= bit;
+            step(k, ((m0 & bit) ? 1 : 0) | ((m1 & bit) ? 2 : 0));
           }
         }
-        // rows: r + sum over the pair's columns (ascending) with a step of delta_c A(rho, c)
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          double v = f ? r1 : r0;
-          bool any = false;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            if (d[e] == 0.0) continue;
-            for (int q = 0; q < nc[k][e]; ++q)
-              if (cr[k][e][q] == f) {
-                v += d[e] * cv[k][e][q];
-                any = true;
-              }
+      } else {
+        const uint64_t u = g0 + (uint64_t)k * T;
+        const int cnt = min((int)cur_c[k], kEvCap);
+        uint32_t key[kEvCap];
+        for (int j = 0; j < cnt; ++j) {
+          const uint32_t v = j < kPre ? cur_k[k][j] : __ldcg(&A.ev[(ep * kEvCap + j) * A.U + u]);
+          int q = j;  // insertion sort: ascending (block, member)
+          while (q > 0 && key[q - 1] > v) {
+            key[q] = key[q - 1];
+            --q;
           }
-          if (any) r[k][f] = v;
+          key[q] = v;
+        }
+        int j = 0;
+        while (j < cnt) {
+          const uint32_t bl = key[j] >> 1;
+          int in = 0;  // bit e: member e steps in this block
+          while (j < cnt && (key[j] >> 1) == bl) in |= 1 << (key[j++] & 1);
+          step(k, in);
         }
       }
       // refresh r = A x - b on the pair's rows (solvers.cpp:472-474: apply, then - b)
@@ -803,16 +1201,28 @@ __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
       }
     }
     acc[2] += tail;
-    block_sum<5>(acc);
-    double* part = A.partials + (size_t)(SYNC ? (ep & 1) : ep) * gridDim.x * 5;
-    if (threadIdx.x == 0) {
+    warp_sum5(acc);
+    double* part = A.partials + (size_t)(SYNC ? (ep & 1) : ep) * nwarps * 5;
+    if ((threadIdx.x & 31) == 0) {
 #pragma unroll
-      for (int q = 0; q < 5; ++q) part[(size_t)blockIdx.x * 5 + q] = acc[q];
+      for (int q = 0; q < 5; ++q) part[(size_t)gwarp * 5 + q] = acc[q];
     }
     if constexpr (!SYNC) continue;
     cg::this_grid().sync();
-    double f, nnz, applied, colops;
-    epoch_objective(part, gridDim.x, tau, f, nnz, applied, colops);
+    __shared__ double fo[4];
+    if (threadIdx.x < 32) {
+      double f, nnz, applied, colops;
+      epoch_objective_warp(part, nwarps, tau, f, nnz, applied, colops);
+      if (threadIdx.x == 0) {
+        fo[0] = f;
+        fo[1] = nnz;
+        fo[2] = applied;
+        fo[3] = colops;
+      }
+    }
+    __syncthreads();
+    const double f = fo[0], nnz = fo[1], applied = fo[2], colops = fo[3];
+    __syncthreads();
     const uint64_t epoch = epoch0 + ep + 1;
     const int stop = !isfinite(f) ? 2 : (has_target && f <= target) ? 1 : epoch >= max_epochs ? 3 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) epoch_record(st, A.trace, epoch, f, nnz, applied, colops, stop);
@@ -829,13 +1239,13 @@ __global__ void __launch_bounds__(kPairThreads) cd_pair_kernel(CdPairArgs A) {
   }
 }
 
-template <int P>
+template <int P, int MW>
 int cd_pair_capacity() {
   static const int cap = [] {
     int per_sm = 0, per_sm2 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P, true>, kPairThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cd_pair_kernel<P, true, MW>, kPairThreads, 0) !=
             cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, cd_pair_kernel<P, false>, kPairThreads, 0) !=
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, cd_pair_kernel<P, false, MW>, kPairThreads, 0) !=
             cudaSuccess) {
       cudaGetLastError();
       return 0;
@@ -843,6 +1253,17 @@ int cd_pair_capacity() {
     return std::min(per_sm, per_sm2) * sm_count();
   }();
   return cap;
+}
+
+template <int MW>
+void pick_pair_kernel(bool sync, const std::function<void(int, int, const void*)>& try_p) {
+  auto fn = [&](auto pc) -> const void* {
+    constexpr int Pk = decltype(pc)::value;
+    return sync ? (const void*)cd_pair_kernel<Pk, true, MW> : (const void*)cd_pair_kernel<Pk, false, MW>;
+  };
+  try_p(1, cd_pair_capacity<1, MW>(), fn(std::integral_constant<int, 1>()));
+  try_p(2, cd_pair_capacity<2, MW>(), fn(std::integral_constant<int, 2>()));
+  if constexpr (MW == 0) try_p(4, cd_pair_capacity<4, MW>(), fn(std::integral_constant<int, 4>()));
 }
 
 uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {  // rng.hpp:37-45
@@ -860,6 +1281,30 @@ double cd_damping(uint64_t omega, uint64_t varpi, uint64_t n) {  // solvers.cpp:
                    static_cast<double>(n - 1);
 }
 
+
+// Page-locked host staging kept per thread and grown on demand: a solve does
+// not pay cudaMallocHost (milliseconds for megabytes) after the first.
+template <class T>
+T* pinned_scratch(int slot, size_t count) {
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  thread_local Buf bufs[4];
+  Buf& b = bufs[slot];
+  const size_t want = std::max<size_t>(count * sizeof(T), 64);
+  if (b.bytes < want) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    L1B_CUDA(cudaMallocHost(&b.p, want + want / 2));
+    b.bytes = want + want / 2;
+  }
+  return static_cast<T*>(b.p);
+}
 
 // The pair-local path (see cd_pair_kernel): 1 = ran (state in x / r / dst),
 // 0 = not applicable, -1 = handed over mid-run (the caller restarts on the
@@ -888,16 +1333,24 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     }
   };
   // with a target the objective is tested every epoch inside the kernel (grid
-  // barrier); without one the epochs run back to back
+  // barrier); without one the epochs run back to back.  Epochs of at most 256
+  // blocks take event masks (MW words per member), longer ones event lists.
   const bool sync = cfg->has_target != 0;
-  try_p(1, cd_pair_capacity<1>(), sync ? (const void*)cd_pair_kernel<1, true> : (const void*)cd_pair_kernel<1, false>);
-  try_p(2, cd_pair_capacity<2>(), sync ? (const void*)cd_pair_kernel<2, true> : (const void*)cd_pair_kernel<2, false>);
-  try_p(4, cd_pair_capacity<4>(), sync ? (const void*)cd_pair_kernel<4, true> : (const void*)cd_pair_kernel<4, false>);
+  const char* mask_env = getenv("L1B_PCDM_MASK");  // 0: event lists even for short epochs (A/B)
+  int mw = (per_epoch <= 128 && !(mask_env && mask_env[0] == '0')) ? 2 : 0;
+  if (mw) pick_pair_kernel<2>(sync, try_p);
+  if (!P) {  // (mask kernels take at most 2 pairs per thread)
+    mw = 0;
+    pick_pair_kernel<0>(sync, try_p);
+  }
   if (!P) return 0;
+  const uint64_t nwarps = (uint64_t)grid * (kPairThreads / 32);
   cudaStream_t st = v.stream;
-  // chunks of ~2^19 draws: the stream for the next chunk is drawn (side stream,
-  // one SM) while the current chunk's walk and epochs run
-  const uint64_t E_max = std::max<uint64_t>(1, std::min<uint64_t>(cfg->max_iters, (1ull << 19) / (per_epoch * B)));
+  // chunks of up to ~2^22 draws (C2's 100 epochs: one chunk): the stream for the
+  // next chunk is drawn (side stream, jump-started chunks on all SMs) while the
+  // current chunk's walk and epochs run
+  const uint64_t E_max = std::max<uint64_t>(
+      1, std::min<uint64_t>(std::min<uint64_t>(cfg->max_iters, kFoldMax), (1ull << 22) / (per_epoch * B)));
   auto margin = [&](uint64_t T) { return T * B / n + 4096; };  // ~2x the expected redraws (B / 2n per draw)
   const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));  // one chunk
   const uint64_t G = cap_raw / 2;  // draws per generator launch
@@ -911,14 +1364,27 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
   const int W_prev = B == 1 ? 0 : W;
   std::vector<void*> bufs;
-  auto alloc = [&](auto** ptr, size_t bytes) {  // out of memory: hand the run to the direct path
-    const cudaError_t e = cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8));
+  cudaStream_t st0 = v.stream;
+  keep_pool(v.device);
+  // stream-ordered pool (kept cached): no cudaMalloc after the first solve;
+  // out of memory hands the run to the direct path
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    const cudaError_t e = cudaMallocAsync((void**)ptr, std::max<size_t>(bytes, 8), st0);
     if (e == cudaErrorMemoryAllocation) {
       cudaGetLastError();
       throw Unsupported("pcdm pairs: device memory");
     }
     L1B_CUDA(e);
     bufs.push_back((void*)*ptr);
+  };
+  // L1B_PCDM_TRACE=1: host-side phase times on stderr
+  const bool tracing = getenv("L1B_PCDM_TRACE") != nullptr;
+  auto tprev = std::chrono::steady_clock::now();
+  auto ptrace = [&](const char* what) {
+    if (!tracing) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pcdm pairs] %-20s %8.1f us\n", what, std::chrono::duration<double, std::micro>(now - tprev).count());
+    tprev = now;
   };
   int rc = 1;
   int* h_flag = nullptr;
@@ -939,7 +1405,6 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     uint64_t* cand;
     void* scan_tmp;
     size_t scan_bytes = 0;
-    std::vector<uint64_t> h_cand;
     alloc(&S[0], (scap + 312) * 4);  // + one generator round of slack
     alloc(&prevd, (cap_raw + 312) * 2);
     alloc(&sarr, (E_max * per_epoch + 1) * 8);
@@ -948,14 +1413,39 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     alloc(&win, 312 * 8);
     alloc(&words, (G + 312) * 8);
     alloc(&flag, 16);
-    alloc(&part, (size_t)(sync ? 2 : E_max) * grid * 5 * 8);
+    alloc(&part, (size_t)(sync ? 2 : E_max) * nwarps * 5 * 8);
+    double* fvals = nullptr;
+    alloc(&fvals, (size_t)E_max * 4 * 8 + 16);
+    unsigned* fticket = reinterpret_cast<unsigned*>(fvals + E_max * 4);
+    L1B_CUDA(cudaMemsetAsync(fticket, 0, 8, st0));
+    unsigned long long* mask = nullptr;
+    if (mw) alloc(&mask, (size_t)E_max * 2 * mw * U * 8);
     const uint64_t max_tiles = (cap_raw + 312 + kCandTile - 1) / kCandTile;
     alloc(&tile_cnt, (max_tiles + 1) * 4);
     alloc(&cand, (cap_raw + 312) * 8);
     L1B_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, tile_cnt, tile_cnt, (int)(max_tiles + 1), st));
-    alloc(&scan_tmp, scan_bytes);
-    L1B_CUDA(cudaMallocHost(&h_starts_pinned, (E_max * per_epoch + 1) * 8));
-    L1B_CUDA(cudaMallocHost(&h_flag, 16));
+    // look-back by a stable sort of (coordinate, position) (blocks of B > 1)
+    const int key_bits = 64 - __builtin_clzll((unsigned long long)n);  // keys 0 .. n
+    uint32_t *key = nullptr, *pos_in = nullptr, *skey = nullptr, *spos = nullptr;
+    size_t sort_bytes = 0;
+    if (W_prev > 0) {
+      alloc(&key, (cap_raw + 312) * 4);
+      alloc(&pos_in, (cap_raw + 312) * 4);
+      alloc(&skey, (cap_raw + 312) * 4);
+      alloc(&spos, (cap_raw + 312) * 4);
+      L1B_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, skey, pos_in, spos,
+                                               (int)(cap_raw + 312), 0, key_bits, st));
+    }
+    alloc(&scan_tmp, std::max(scan_bytes, sort_bytes));
+    h_starts_pinned = pinned_scratch<uint64_t>(0, 64);  // [0]: the chunk's end, [1..]: level offsets
+    h_flag = pinned_scratch<int>(1, 4);
+    uint64_t* h_lvoff = h_starts_pinned + 1;
+    // the device walk: segment heads, the phase maps of every tree level
+    const uint64_t max_seg = (cap_raw + 312 + kSegLen - 1) / kSegLen;
+    uint64_t *seg_first = nullptr, *seg_lv = nullptr, *lvoff = nullptr;
+    alloc(&seg_first, max_seg * 8);
+    alloc(&seg_lv, (2 * max_seg + 64) * (uint64_t)W * 8);
+    alloc(&lvoff, 64 * 8);
     L1B_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
     {
       uint64_t w[312];
@@ -973,6 +1463,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       while (k < pieces.size() && pieces[k].first <= upto) cudaEventDestroy(pieces[k++].second);
       pieces.erase(pieces.begin(), pieces.begin() + k);
     };
+    ptrace("set up");
     start();  // x = 0, r = -b, epoch-0 sample: the solve's clock starts here
     {
       cudaEvent_t e = new_event();
@@ -998,6 +1489,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     a.r = r;
     a.cnt = cnt;
     a.ev = ev;
+    a.mask = mask;
     a.st = dst;
     a.trace = trace;
     a.partials = part;
@@ -1041,14 +1533,29 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       }
       uint32_t* idx = S[cur] + pos;
       uint64_t have = 0;
+      // draws the rest of the run can consume (blocks + expected redraws, x2 margin)
+      const uint64_t rest = (cfg->max_iters - launched) * per_epoch * B;
+      const uint64_t total_bound = pos + rest + margin(rest);
       for (;;) {
         if (need > cap_raw) throw Unsupported("pcdm pairs: chunk buffer");
-        gen_to(pos + need + G);  // this chunk's draws and one launch ahead
+        // this chunk's draws, and one launch ahead while the run can still use it
+        gen_to(std::max(pos + need, std::min(pos + need + G, total_bound)));
         wait_for(pos + need);
         have = need;
-        cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
-            idx, have, W_prev, prevd);
-        L1B_LAUNCHED();
+        if (W_prev > 0) {
+          cd_key_kernel<<<grid_for(have), kThreads, 0, st>>>(idx, have, (uint32_t)n, key, pos_in);
+          L1B_LAUNCHED();
+          size_t sb = sort_bytes;
+          L1B_CUDA(cub::DeviceRadixSort::SortPairs(scan_tmp, sb, key, skey, pos_in, spos, (int)have, 0, key_bits,
+                                                   st));
+          cd_prevd_sorted_kernel<<<grid_for(have), kThreads, 0, st>>>(skey, spos, have, (uint32_t)n, W_prev,
+                                                                      prevd);
+          L1B_LAUNCHED();
+        } else {
+          cd_prevd_kernel<<<(unsigned)((have + kThreads - 1) / kThreads), kThreads, (W + kThreads) * 4, st>>>(
+              idx, have, W_prev, prevd);
+          L1B_LAUNCHED();
+        }
         const uint64_t tiles = (have + kCandTile - 1) / kCandTile;
         cd_cand_count<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt);
         L1B_LAUNCHED();
@@ -1057,54 +1564,84 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
         L1B_CUDA(cub::DeviceScan::ExclusiveSum(scan_tmp, tb, tile_cnt, tile_cnt, (int)(tiles + 1), st));
         cd_cand_write<<<(unsigned)tiles, kThreads, 0, st>>>(prevd, have, tile_cnt, cand);
         L1B_LAUNCHED();
-        uint32_t ncand = 0;
-        L1B_CUDA(cudaMemcpyAsync(h_flag, tile_cnt + tiles, 4, cudaMemcpyDeviceToHost, st));
-        L1B_CUDA(cudaStreamSynchronize(st));
-        ncand = (uint32_t)h_flag[0];
-        h_cand.resize(ncand);
-        if (ncand)
-          L1B_CUDA(cudaMemcpyAsync(h_cand.data(), cand, (size_t)ncand * 8, cudaMemcpyDeviceToHost, st));
-        L1B_CUDA(cudaStreamSynchronize(st));
-        // block starts: a draw is redrawn iff its previous draw lies inside its block
-        if (B == 1 && ncand == 0) {  // serial CD without a rejected draw: block b starts at b
-          if (nb + 1 > have) {
-            need = have + have / 2;
-            continue;
-          }
-          cd_iota_kernel<<<grid_for(nb + 1), kThreads, 0, st>>>(sarr, nb + 1);
+        // block starts on the device (no host round trip); a stream too short
+        // for nb blocks leaves starts[nb] at ~0 and hands the run over below
+        const uint64_t nseg = (have + kSegLen - 1) / kSegLen;
+        const uint32_t* ncand_d = tile_cnt + tiles;
+        L1B_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+        L1B_CUDA(cudaMemsetAsync(sarr + nb, 0xff, 8, st));
+        if (B == 1) {
+          cd_b1_starts_kernel<<<grid_for(nb + 1), kThreads, 0, st>>>(cand, ncand_d, nb, sarr);
           L1B_LAUNCHED();
-          h_starts_pinned[nb] = nb;
           break;
         }
-        bool short_stream = false;
-        uint64_t sb = 0, j = 0;
-        for (uint64_t blk = 0; blk < nb; ++blk) {
-          h_starts_pinned[blk] = sb;
-          uint64_t e = sb + B;
-          while (j < ncand && (h_cand[j] >> 16) < e) {
-            const uint64_t q = h_cand[j] >> 16, d = h_cand[j] & 0xffff;
-            if (d == kPrevRej || q - d >= sb) ++e;
-            ++j;
+        cd_seg_first_kernel<<<blocks_for(nseg), kThreads, 0, st>>>(cand, ncand_d, nseg, seg_first);
+        L1B_LAUNCHED();
+        cd_seg_walk_kernel<<<(unsigned)nseg, (unsigned)std::min(1024, (W + 31) / 32 * 32), 0, st>>>(cand, ncand_d, seg_first,
+                                                                                      nseg, B, W, seg_lv, flag);
+        L1B_LAUNCHED();
+        int nlevels = 1;
+        {
+          LevelTab tab;
+          uint64_t n_l = nseg, o = 0;
+          tab.off[0] = 0;
+          tab.cnt[0] = nseg;
+          h_lvoff[0] = 0;
+          while (n_l > 1) {  // level sizes and offsets
+            o += n_l * W;
+            n_l = (n_l + 1) / 2;
+            if (nlevels >= 40) throw Unsupported("pcdm pairs: walk tree depth");
+            tab.off[nlevels] = o;
+            tab.cnt[nlevels] = n_l;
+            h_lvoff[nlevels++] = o;
           }
-          if (e - sb > (uint64_t)W) throw Unsupported("pcdm pairs: block longer than the look-back");
-          if (e > have) {
-            short_stream = true;
-            break;
+          for (int l0 = 0; l0 + 1 < nlevels; l0 += kComposeLevels) {
+            const int l1 = std::min(nlevels - 1, l0 + kComposeLevels);
+            const uint64_t groups = (tab.cnt[l0] + (1ull << kComposeLevels) - 1) >> kComposeLevels;
+            cd_seg_compose_kernel<<<(unsigned)groups, 512, 0, st>>>(seg_lv, tab, l0, l1, W);
+            L1B_LAUNCHED();
           }
-          sb = e;
+          L1B_CUDA(cudaMemcpyAsync(lvoff, h_lvoff, nlevels * 8, cudaMemcpyHostToDevice, st));
         }
-        if (short_stream) {  // more redraws than the margin: wait for more draws and walk again
-          need = have + have / 2;
-          continue;
+        cd_seg_emit_kernel<<<(unsigned)((nseg + 3) / 4), 128, 0, st>>>(cand, ncand_d, seg_first, seg_lv, lvoff,
+                                                                     nlevels, nseg, B, W, nb, sarr);
+        L1B_LAUNCHED();
+        ptrace("walk queued");
+        if (getenv("L1B_PCDM_WALK_CHECK")) {  // the device walk against the sequential one (tests)
+          uint32_t nc = 0;
+          L1B_CUDA(cudaMemcpyAsync(&nc, ncand_d, 4, cudaMemcpyDeviceToHost, st));
+          L1B_CUDA(cudaStreamSynchronize(st));
+          std::vector<uint64_t> hc(nc), dev(nb + 1);
+          if (nc) L1B_CUDA(cudaMemcpy(hc.data(), cand, (size_t)nc * 8, cudaMemcpyDeviceToHost));
+          L1B_CUDA(cudaMemcpy(dev.data(), sarr, (nb + 1) * 8, cudaMemcpyDeviceToHost));
+          uint64_t sb = 0, j = 0;
+          for (uint64_t blk = 0; blk <= nb; ++blk) {
+            if (dev[blk] != sb) {
+              fprintf(stderr, "[pcdm pairs] walk mismatch at block %llu: device %llu, host %llu\n",
+                      (unsigned long long)blk, (unsigned long long)dev[blk], (unsigned long long)sb);
+              throw std::runtime_error("pcdm pairs: device walk differs from the sequential walk");
+            }
+            uint64_t e = sb + B;
+            while (j < nc && (hc[j] >> 16) < e) {
+              const uint64_t q = hc[j] >> 16, d = hc[j] & 0xffff;
+              if (d == kPrevRej || q - d >= sb) ++e;
+              ++j;
+            }
+            sb = e;
+          }
         }
-        h_starts_pinned[nb] = sb;
-        L1B_CUDA(cudaMemcpyAsync(sarr, h_starts_pinned, (nb + 1) * 8, cudaMemcpyHostToDevice, st));
         break;
       }
-      L1B_CUDA(cudaMemsetAsync(flag, 0, 4, st));
-      L1B_CUDA(cudaMemsetAsync(cnt, 0, E * U * 4, st));
-      cd_scatter_kernel<<<grid_for(T), kThreads, 0, st>>>(idx, prevd, sarr, nb, per_epoch, a.off, U, cnt, ev,
-                                                        flag);
+      if (mw) {
+        L1B_CUDA(cudaMemsetAsync(mask, 0, (size_t)E * 2 * mw * U * 8, st));
+        cd_mask_scatter_kernel<<<grid_for(nb * 32), kThreads, 0, st>>>(idx, prevd, sarr, nb, per_epoch, a.off, U,
+                                                                      mw, mask, have);
+      } else {
+        L1B_CUDA(cudaMemsetAsync(cnt, 0, E * U * 4, st));
+        const int lanes = B >= 32 ? 32 : 1;  // per block
+        cd_scatter_kernel<<<grid_for(nb * lanes), kThreads, 0, st>>>(idx, prevd, sarr, nb, per_epoch, a.off, U,
+                                                                    lanes, cnt, ev, flag, have);
+      }
       L1B_LAUNCHED();
       a.epochs = E;
       void* args[] = {&a};
@@ -1114,14 +1651,19 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       } else {
         L1B_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kPairThreads), args, 0, st));
         L1B_LAUNCHED();
-        cd_pair_fold<<<1, kPairThreads, 0, st>>>(part, (unsigned)grid, E, dst, trace);
+        cd_pair_fold<<<(unsigned)((E + 3) / 4), 128, 0, st>>>(part, (unsigned)nwarps, E, dst, trace, fvals,
+                                                             fticket);
         L1B_LAUNCHED();
       }
-      const uint64_t used = h_starts_pinned[nb];
       L1B_CUDA(cudaMemcpyAsync(h_flag, flag, 4, cudaMemcpyDeviceToHost, st));
+      L1B_CUDA(cudaMemcpyAsync(h_starts_pinned, sarr + nb, 8, cudaMemcpyDeviceToHost, st));
       L1B_CUDA(cudaMemcpyAsync(h_st, dst, sizeof(CdDev), cudaMemcpyDeviceToHost, st));
       L1B_CUDA(cudaStreamSynchronize(st));
+      ptrace("epochs done");
+      const uint64_t used = h_starts_pinned[0];
       if (*h_flag & 4) throw Unsupported("pcdm pairs: event bucket");
+      if (*h_flag & 16) throw Unsupported("pcdm pairs: block longer than the look-back");
+      if (used > have) throw Unsupported("pcdm pairs: stream shorter than the chunk's blocks");
       pos += used;  // the draws past the chunk's last block open the next chunk
       drop_pieces(pos);
       launched += E;
@@ -1134,18 +1676,14 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
     if (gs) cudaStreamSynchronize(gs);
     if (gs) cudaStreamDestroy(gs);
     for (auto& pc : pieces) cudaEventDestroy(pc.second);
-    for (void* q : bufs) cudaFree(q);
-    if (h_flag) cudaFreeHost(h_flag);
-    if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
+    for (void* q : bufs) cudaFreeAsync(q, st0);
     throw;
   }
   cudaStreamSynchronize(st);
   if (gs) cudaStreamSynchronize(gs);
   if (gs) cudaStreamDestroy(gs);
   for (auto& pc : pieces) cudaEventDestroy(pc.second);
-  for (void* q : bufs) cudaFree(q);
-  if (h_flag) cudaFreeHost(h_flag);
-  if (h_starts_pinned) cudaFreeHost(h_starts_pinned);
+  for (void* q : bufs) cudaFreeAsync(q, st0);
   return rc;
 }
 }  // namespace
@@ -1182,19 +1720,19 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
   const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(16, (1ull << 26) / std::max<uint64_t>(1, per_epoch * B)));
   const uint64_t tcap = std::min<uint64_t>(cfg->max_iters + 2, 1ull << 22);
   std::vector<void*> bufs;
-  auto alloc = [&](auto** ptr, size_t bytes) {
-    L1B_CUDA(cudaMalloc((void**)ptr, std::max<size_t>(bytes, 8)));
+  keep_pool(v.device);
+  auto alloc = [&](auto** ptr, size_t bytes) {  // stream-ordered pool, kept cached
+    L1B_CUDA(cudaMallocAsync((void**)ptr, std::max<size_t>(bytes, 8), st));
     bufs.push_back((void*)*ptr);
   };
   uint32_t* h_coords = nullptr;  // two chunk buffers: generate one while the other uploads
   CdDev* h_st = nullptr;
   cudaEvent_t uploaded[2] = {nullptr, nullptr};
-  try {
-    alloc(&x, n * 8);
-    alloc(&r, v.m * 8);
+  // the direct path's buffers (host draws, planned or direct epochs): only when
+  // the pair-local path does not run
+  auto alloc_direct = [&]() {
     alloc(&delta, n * 8);
     alloc(&stamp, n * 4);
-    alloc(&partials, (size_t)spmv_grid_max() * 4 * 8);
     alloc(&d_coords, 2 * chunk * per_epoch * B * 4);
     if (plan_k) {
       const uint64_t S = chunk * per_epoch * B, K = (uint64_t)plan_k;
@@ -1208,10 +1746,15 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       alloc(&plan.rc, K * K * S * 4);
       alloc(&plan.rv, K * K * S * 8);
     }
+    h_coords = pinned_scratch<uint32_t>(3, 2 * chunk * per_epoch * B);
+    for (auto& e : uploaded) L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  };
+  try {
+    alloc(&x, n * 8);
+    alloc(&r, v.m * 8);
+    alloc(&partials, (size_t)spmv_grid_max() * 4 * 8);
     alloc(&dst, sizeof(CdDev));
     alloc(&trace, tcap * sizeof(CdSample));
-    L1B_CUDA(cudaMallocHost(&h_coords, 2 * chunk * per_epoch * B * 4));
-    for (auto& e : uploaded) L1B_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     L1B_CUDA(cudaMallocHost(&h_st, sizeof(CdDev)));
     CdDev h;
     std::memset(&h, 0, sizeof(h));
@@ -1226,7 +1769,7 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     // path when the pair-local one hands over)
     auto init_state = [&]() {
       L1B_CUDA(cudaMemsetAsync(x, 0, n * 8, st));
-      L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
+      if (stamp) L1B_CUDA(cudaMemsetAsync(stamp, 0, n * 4, st));
       *h_st = h;
       L1B_CUDA(cudaMemcpyAsync(dst, h_st, sizeof(CdDev), cudaMemcpyHostToDevice, st));
       cd_init_residual<<<grid_for(v.m), kThreads, 0, st>>>(v.b, r, v.m, dst, partials);
@@ -1246,6 +1789,7 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
                                       time_out);
     if (pair_mode <= 0) {  // not applicable, or handed over (a bucket / the look-back overflowed)
       L1B_CUDA(cudaStreamSynchronize(st));
+      alloc_direct();
       launched = 0;
       time_out = false;
       start();
@@ -1384,18 +1928,17 @@ void run_pcdm(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     }
   } catch (...) {
     cudaStreamSynchronize(st);
-    for (void* q : bufs) cudaFree(q);
-    if (h_coords) cudaFreeHost(h_coords);
+    for (void* q : bufs) cudaFreeAsync(q, st);
     if (h_st) cudaFreeHost(h_st);
     for (auto e : uploaded)
       if (e) cudaEventDestroy(e);
     throw;
   }
+  for (void* q : bufs) cudaFreeAsync(q, st);
   cudaStreamSynchronize(st);
-  for (void* q : bufs) cudaFree(q);
-  cudaFreeHost(h_coords);
   cudaFreeHost(h_st);
-  for (auto e : uploaded) cudaEventDestroy(e);
+  for (auto e : uploaded)
+    if (e) cudaEventDestroy(e);
 }
 
 }  // namespace l1b

@@ -28,9 +28,19 @@
 //     tempers, converts exactly like uniform_in and stores the draws that fall
 //     in the requested window (coalesced), reducing min / max over all draws.
 //
+// The coordinate streams of CD / PCDM (uniform_index, mt_stream_indices) are
+// cut the same way into chunks of J = 312 x 256 draws, but every chunk starts
+// from the SAME base: window c = sum_j p^(c)_j W_j with p^(c) = t^(c J) mod P
+// (host: one carry-less multiplication mod P per chunk, cached per process),
+// so all chunk starts come from one kernel (mt_jump_many_kernel: CTAs split
+// the coefficients of every jump, regenerate the base words their slice
+// needs, and XOR their partial windows together).
+//
 // The spectrum's rejection (u <= lo, i.e. a raw draw with (x >> 11) == 0,
 // probability 2^-53 per draw) would shift every later position: it is
 // detected and reported, and the caller falls back to the sequential stream.
+#include <immintrin.h>
+
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -204,6 +214,98 @@ const Poly& pow2_poly(int e) {
   return cache.emplace(e, cur).first->second;
 }
 
+// a * b mod P (deg a, deg b < DEG): carry-less products word by word, then the
+// bit-serial reduction of Reducer
+__attribute__((target("pclmul,sse2"))) void clmul_acc_hw(const uint64_t* a, const uint64_t* b, uint64_t* prod) {
+  for (int i = 0; i < PW; ++i) {
+    if (!a[i]) continue;
+    const __m128i ai = _mm_set_epi64x(0, (long long)a[i]);
+    for (int j = 0; j < PW; ++j) {
+      if (!b[j]) continue;
+      const __m128i r = _mm_clmulepi64_si128(ai, _mm_set_epi64x(0, (long long)b[j]), 0x00);
+      prod[i + j] ^= (uint64_t)_mm_cvtsi128_si64(r);
+      prod[i + j + 1] ^= (uint64_t)_mm_cvtsi128_si64(_mm_unpackhi_epi64(r, r));
+    }
+  }
+}
+
+void clmul_acc_sw(const uint64_t* a, const uint64_t* b, uint64_t* prod) {
+  for (int i = 0; i < PW; ++i) {
+    if (!a[i]) continue;
+    for (int j = 0; j < PW; ++j) {
+      const uint64_t y = b[j];
+      if (!y) continue;
+      uint64_t lo = 0, hi = 0;
+      for (int k = 0; k < 64; ++k)
+        if ((a[i] >> k) & 1ull) {
+          lo ^= y << k;
+          if (k) hi ^= y >> (64 - k);
+        }
+      prod[i + j] ^= lo;
+      prod[i + j + 1] ^= hi;
+    }
+  }
+}
+
+Poly mulmod(const Poly& a, const Poly& b) {
+  static const bool hw = __builtin_cpu_supports("pclmul");
+  Poly prod(2 * PW + 4, 0);
+  if (hw)
+    clmul_acc_hw(a.data(), b.data(), prod.data());
+  else
+    clmul_acc_sw(a.data(), b.data(), prod.data());
+  reducer().reduce(prod);
+  prod.resize(PW);
+  return prod;
+}
+
+// t^J mod P for any J (square-and-multiply over the cached t^(2^e))
+Poly pow_t(uint64_t J) {
+  Poly r(PW, 0);
+  r[0] = 1;  // t^0
+  for (int e = 0; J >> e; ++e)
+    if ((J >> e) & 1ull) r = mulmod(r, pow2_poly(e));
+  return r;
+}
+
+// t^(c J) mod P for c = 0 .. C-1, uploaded to the device (cached per device
+// and J, grown on demand: one multiplication mod P per new chunk, once per
+// process)
+struct JumpTable {
+  uint64_t J = 0;
+  std::vector<Poly> host;  // host[c] = t^(c J)
+  uint64_t* dev = nullptr;
+  uint64_t dev_count = 0;
+};
+
+const uint64_t* jump_table(uint64_t J, uint64_t C, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, uint64_t>, JumpTable> tabs;
+  int dev = 0;
+  L1B_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  JumpTable& t = tabs[{dev, J}];
+  if (t.host.empty()) {
+    t.J = J;
+    Poly one(PW, 0);
+    one[0] = 1;
+    t.host.push_back(one);
+  }
+  if (t.dev_count >= C) return t.dev;
+  const Poly step = pow_t(J);
+  while (t.host.size() < C) t.host.push_back(mulmod(t.host.back(), step));
+  uint64_t* d = nullptr;
+  L1B_CUDA(cudaMalloc(&d, C * PW * 8));  // process-lifetime table (a few hundred KB)
+  std::vector<uint64_t> flat(C * PW);
+  for (uint64_t c = 0; c < C; ++c) std::memcpy(flat.data() + c * PW, t.host[c].data(), PW * 8);
+  L1B_CUDA(cudaMemcpyAsync(d, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, st));
+  L1B_CUDA(cudaStreamSynchronize(st));
+  if (t.dev) cudaFree(t.dev);
+  t.dev = d;
+  t.dev_count = C;
+  return t.dev;
+}
+
 // ---------------------------------------------------------------------------
 // device: jump tree
 //
@@ -348,11 +450,19 @@ __global__ void __launch_bounds__(DRAW_THREADS) mt_draw_kernel(const uint64_t* _
 // neighbour published at the previous barrier.  The untempered words go to
 // global memory; mt_temper_kernel (all SMs) tempers and reduces them after.
 constexpr int IDX_THREADS = 160;
-__global__ void __launch_bounds__(IDX_THREADS) mt_words_kernel(uint64_t* window, uint64_t count,
-                                                               uint64_t* __restrict__ words) {
+// CTA c continues from window win_in[c] for min(J, count - c J) words (a
+// multiple of 2 MID) into words[c J ...]; the last CTA leaves its final window
+// in win_out (one CTA = the sequential stream)
+__global__ void __launch_bounds__(IDX_THREADS) mt_words_kernel(const uint64_t* __restrict__ win_in, uint64_t J,
+                                                               uint64_t count, uint64_t* __restrict__ words,
+                                                               uint64_t* __restrict__ win_out) {
   __shared__ uint64_t pub[2][2][MID];   // [buffer][A | B][column]
   const int tid = threadIdx.x;
   const bool rec = tid < MID - 1;       // columns 0..154 (thread 0 also 155)
+  const uint64_t c = blockIdx.x, base0 = c * J;
+  const uint64_t len = min(J, count - base0);
+  const uint64_t* window = win_in + c * NW;
+  words += base0;
   uint64_t A = 0, B = 0, A2 = 0, B2 = 0;  // A2 / B2: column 155 (thread 0)
   if (rec) {
     A = window[tid];
@@ -368,7 +478,7 @@ __global__ void __launch_bounds__(IDX_THREADS) mt_words_kernel(uint64_t* window,
   }
   __syncthreads();
   int p = 0;
-  for (uint64_t base = 0; base < count; base += 2 * MID) {
+  for (uint64_t base = 0; base < len; base += 2 * MID) {
     if (rec) {
       const uint64_t NA = pub[p][0][tid + 1], NB = pub[p][1][tid + 1];
       const uint64_t ya = next_word(A, NA, B);   // step t
@@ -393,16 +503,64 @@ __global__ void __launch_bounds__(IDX_THREADS) mt_words_kernel(uint64_t* window,
     p ^= 1;
     __syncthreads();
   }
+  if (c + 1 != gridDim.x) return;
   if (rec) {
-    window[tid] = A;
-    window[MID + tid] = B;
+    win_out[tid] = A;
+    win_out[MID + tid] = B;
   }
   if (tid == 0) {
-    window[MID - 1] = A2;
-    window[2 * MID - 1] = B2;
+    win_out[MID - 1] = A2;
+    win_out[2 * MID - 1] = B2;
   }
 }
 
+// windows[c] ^= sum over the set coefficients j of t^(c J) mod P in slice
+// blockIdx.x of x[j .. j + 312) (windows[c] zeroed before; chunk c = blockIdx.y
+// + 1).  Every thread walks the same coefficient bits (uniform branches);
+// thread k accumulates output word k.
+constexpr int JM_SLICE = 39;  // polynomial words per CTA (8 slices)
+constexpr int JM_SLICES = (PW + JM_SLICE - 1) / JM_SLICE;
+constexpr int JM_THREADS = 320;
+__global__ void __launch_bounds__(JM_THREADS) mt_jump_many_kernel(const uint64_t* __restrict__ window,
+                                                                  const uint64_t* __restrict__ polys,
+                                                                  uint64_t* __restrict__ windows) {
+  __shared__ uint64_t xs[JM_SLICE * 64 + NW];
+  __shared__ uint64_t ring[1024];
+  __shared__ uint64_t pw[JM_SLICE];
+  const uint64_t c = blockIdx.y + 1;
+  const int w0 = blockIdx.x * JM_SLICE, w1 = min(PW, w0 + JM_SLICE);
+  const int j0 = w0 * 64, jn = min(SEQ, w1 * 64 + NW) - j0;
+  // x[j0 .. j0 + jn) of the base stream, regenerated here from the window (the
+  // recurrence through a 1024-word ring, 156 words per step): no separate
+  // sequential launch ahead of the jump
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) {
+    const uint64_t v = window[i];
+    ring[i] = v;
+    if (i >= j0 && i < j0 + jn) xs[i - j0] = v;
+  }
+  for (int i = threadIdx.x; i < w1 - w0; i += blockDim.x) pw[i] = polys[c * PW + w0 + i];
+  __syncthreads();
+  for (int base = 0; base + NW < j0 + jn; base += MID) {
+    const int k = base + threadIdx.x;  // x[k + 312] from x[k], x[k + 1], x[k + 156]
+    if (threadIdx.x < MID && k + NW < j0 + jn) {
+      const uint64_t v = next_word(ring[k & 1023], ring[(k + 1) & 1023], ring[(k + MID) & 1023]);
+      ring[(k + NW) & 1023] = v;
+      if (k + NW >= j0) xs[k + NW - j0] = v;
+    }
+    __syncthreads();
+  }
+  const int k = threadIdx.x;
+  if (k >= NW) return;
+  uint64_t acc = 0;
+  for (int w = 0; w < w1 - w0; ++w) {
+    const uint64_t bits = pw[w];  // the same for every thread: uniform predicates
+    const uint64_t* xb = xs + (w << 6) + k;
+#pragma unroll
+    for (int b = 0; b < 64; ++b)
+      if ((bits >> b) & 1ull) acc ^= xb[b];
+  }
+  if (acc) atomicXor((unsigned long long*)&windows[c * NW + k], (unsigned long long)acc);
+}
 
 template <bool POW2>
 __global__ void mt_temper_kernel(const uint64_t* __restrict__ words, uint64_t count, uint64_t n, uint64_t lim,
@@ -539,21 +697,66 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 
 void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312); }
 
+// Chunks of kIdxChunk draws (a multiple of 312) start from windows jumped
+// ahead by t^(c J) mod P, all from the same base sequence: one sequential
+// generation of 19937 words, one jump kernel for every chunk, one CTA per chunk
+// for the recurrence, then the tempering over all SMs.  Short streams (one
+// chunk) run the recurrence directly.
+constexpr uint64_t kIdxChunk = 312 * 256;
+
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            uint64_t* d_words, cudaStream_t st) {
-  count = (count + 2 * mt::MID - 1) / (2 * mt::MID) * (2 * mt::MID);
+  using namespace mt;
+  count = (count + 2 * MID - 1) / (2 * MID) * (2 * MID);
   if (count == 0) return 0;
   const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
   uint64_t* words = d_words;
   if (!words) L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
-  mt::mt_words_kernel<<<1, mt::IDX_THREADS, 0, st>>>(d_window, count, words);
-  L1B_LAUNCHED();
+  const uint64_t C = (count + kIdxChunk - 1) / kIdxChunk;
+  if (C == 1) {
+    mt_words_kernel<<<1, IDX_THREADS, 0, st>>>(d_window, count, count, words, d_window);
+    L1B_LAUNCHED();
+  } else {
+    const uint64_t* polys = jump_table(kIdxChunk, C, st);
+    uint64_t* wins = nullptr;
+    L1B_CUDA(cudaMallocAsync(&wins, C * NW * 8, st));
+    L1B_CUDA(cudaMemcpyAsync(wins, d_window, NW * 8, cudaMemcpyDeviceToDevice, st));
+    L1B_CUDA(cudaMemsetAsync(wins + NW, 0, (C - 1) * NW * 8, st));
+    mt_jump_many_kernel<<<dim3(JM_SLICES, (unsigned)(C - 1)), JM_THREADS, 0, st>>>(d_window, polys, wins);
+    L1B_LAUNCHED();
+    mt_words_kernel<<<(unsigned)C, IDX_THREADS, 0, st>>>(wins, kIdxChunk, count, words, d_window);
+    L1B_LAUNCHED();
+    L1B_CUDA(cudaFreeAsync(wins, st));
+  }
   const int grid = grid_for(count);
   if ((n & (n - 1)) == 0) mt::mt_temper_kernel<true><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
   else mt::mt_temper_kernel<false><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
   L1B_LAUNCHED();
   if (!d_words) L1B_CUDA(cudaFreeAsync(words, st));
   return count;
+}
+
+// host restatement of the chunked jump (tests): raw outputs c J .. c J + count - 1
+// of std::mt19937_64(seed) through t^(c J) mod P, J = the index-stream chunk
+void host_draws_after_chunk_jump(uint64_t seed, uint64_t c, uint64_t count, uint64_t* out) {
+  using namespace mt;
+  std::vector<uint64_t> x(SEQ + 1);
+  seed_window(seed, x.data());
+  if (c) {
+    const Poly p = pow_t(kIdxChunk * c);
+    for (int k = 0; k < DEG; ++k) x[k + NW] = next_word(x[k], x[k + 1], x[k + MID]);
+    uint64_t w[NW] = {};
+    for (int j = 0; j < DEG; ++j)
+      if ((p[j >> 6] >> (j & 63)) & 1ull)
+        for (int i = 0; i < NW; ++i) w[i] ^= x[j + i];
+    std::copy(w, w + NW, x.begin());
+  }
+  std::vector<uint64_t> r(x.begin(), x.begin() + NW);
+  r.resize(NW + count + 1);
+  for (uint64_t k = 0; k < count; ++k) {
+    r[k + NW] = next_word(r[k], r[k + 1], r[k + MID]);
+    out[k] = temper(r[k + NW]);
+  }
 }
 
 }  // namespace l1b

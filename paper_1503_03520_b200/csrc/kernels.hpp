@@ -45,12 +45,18 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 // d_out[q] = index of draw q, 0xffffffff where the reference would redraw.
 // Draws count rounded up to a multiple of 312 (returned; d_out must hold them).
 // d_words: scratch of as many 64-bit words (null: allocated on the stream).
+// Streams longer than one chunk (312 x 256 draws) run in parallel chunks
+// started by jump-ahead (k_rng.cu).
 void mt_seed_state(uint64_t seed, uint64_t* w312);
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            uint64_t* d_words, cudaStream_t st);
 // host: raw 64-bit outputs 2^log2_jump .. 2^log2_jump + count - 1 of
 // std::mt19937_64(seed) through the jump polynomial (log2_jump < 0: no jump)
 void host_draws_after_jump(uint64_t seed, int log2_jump, uint64_t count, uint64_t* out);
+// host: raw outputs c J .. c J + count - 1 through t^(c J) mod P, J = the
+// coordinate-stream chunk (the start of chunk c in mt_stream_indices)
+void host_draws_after_chunk_jump(uint64_t seed, uint64_t c, uint64_t count, uint64_t* out);
+constexpr uint64_t kIdxChunkDraws = 312 * 256;
 
 // ---- k_bt.cu ----------------------------------------------------------------
 // estimate_gram_lmax (linops.cpp:757-778) with the matrix-free products (syncs)

@@ -151,7 +151,9 @@ def test_shards_device_rng_reproduce_global_instance():
 
 
 @pytest.mark.parametrize("n,pieces", [(32768, [100_000]), (1_000_003, [1, 311, 313, 40_000, 3]),
-                                      (4096, [312] * 7), ((1 << 31), [5000])])
+                                      (4096, [312] * 7), ((1 << 31), [5000]),
+                                      # several jump-started chunks of 312 x 256 draws per piece
+                                      (32768, [3_300_000]), (1_000_003, [200_000, 500_001, 79_872, 90_000])])
 def test_coordinate_index_stream_bit_exact(oracle, n, pieces):
     """The pair-local CD / PCDM coordinate stream (mt_stream_indices, continued
     over several launches) against std::mt19937_64 reduced like uniform_index:

@@ -41,3 +41,24 @@ def test_mix_seeded_generator_streams(oracle):
             oracle.lib.lo_rng_next(ctypes.byref(r))
         want = np.array([oracle.lib.lo_rng_next(ctypes.byref(r)) for _ in range(400)], dtype=np.uint64)
         np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("seed,chunk", [(1, 1), (7, 2), (2**64 - 3, 5)])
+def test_chunk_jump_lands_on_sequential_stream(oracle, seed, chunk):
+    """The coordinate-stream chunks (mt_stream_indices): chunk c starts at
+    t^(c J) mod P, J = 312 x 256, by one carry-less multiplication mod P per
+    chunk -- the same stream position as stepping c J draws."""
+    from paper_1503_03520_b200 import _native as N
+
+    lib = N.load()
+    J = 312 * 256
+    count = 700
+    got = np.empty(count, dtype=np.uint64)
+    N.check(lib.l1b_mt_draws_after_chunk_jump(seed, chunk, count,
+                                              got.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    r = oracle.rng(seed)
+    nxt = oracle.lib.lo_rng_next
+    for _ in range(chunk * J):
+        nxt(ctypes.byref(r))
+    want = np.array([nxt(ctypes.byref(r)) for _ in range(count)], dtype=np.uint64)
+    np.testing.assert_array_equal(got, want)
