@@ -442,6 +442,7 @@ class Reference:
         L.ref_build_instance.restype = C.c_void_p
         L.ref_build_instance2.argtypes = L.ref_build_instance.argtypes + [C.c_int, f64, f64, f64]
         L.ref_build_instance2.restype = C.c_void_p
+        L.ref_next_spectrum_alternating.argtypes = [C.c_int, f64, f64]
         L.ref_save_instance.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_save_instance.restype = C.c_int
         L.ref_load_instance.argtypes = [C.c_char_p]
@@ -483,8 +484,10 @@ class Reference:
     def build_instance(self, n, m_ratio=2.0, stages=1, left_stages=0, permute=False, q=1,
                        shift=0.1, s_divisor=128, gamma=10.0, tau=1.0, theta=2 * math.pi / 10,
                        seed=1, sigma=None, solution="uniform", s1_fraction=0.5, value_a=-1e4,
-                       value_b=1e-1):
+                       value_b=1e-1, alternating=None):
         sig = None if sigma is None else np.ascontiguousarray(sigma, dtype=np.float64)
+        if alternating is not None:  # SpectrumRule::Kind::alternating (odd_value, even_value)
+            self.lib.ref_next_spectrum_alternating(1, float(alternating[0]), float(alternating[1]))
         h = self.lib.ref_build_instance2(n, m_ratio, stages, left_stages, int(permute), q, shift,
                                          s_divisor, gamma, tau, theta, seed, _ptr(sig, f64),
                                          self.SOLUTION_KINDS[solution], s1_fraction, value_a, value_b)

@@ -103,6 +103,16 @@ void* ref_build_instance(uint64_t n, double m_ratio, uint64_t stages, uint64_t l
                              tau, theta, seed, sigma_explicit, 0, 0.5, -1e4, 1e-1);
 }
 
+// SpectrumRule::Kind::alternating (bench.hpp:16-23, bench.cpp:278) for the next
+// ref_build_instance2 call: the odd / even values (on = 0: uniform_q again)
+static thread_local int g_alt_on = 0;
+static thread_local double g_alt_odd = 0.1, g_alt_even = 100.0;
+void ref_next_spectrum_alternating(int on, double odd_value, double even_value) {
+  g_alt_on = on;
+  g_alt_odd = odd_value;
+  g_alt_even = even_value;
+}
+
 // + SolutionRule (bench.hpp:25-32): kind 0 uniform, 1 spectral, 2 two_value
 void* ref_build_instance2(uint64_t n, double m_ratio, uint64_t stages, uint64_t left_stages,
                           int permute, int q, double shift, uint64_t s_divisor, double gamma,
@@ -122,6 +132,12 @@ void* ref_build_instance2(uint64_t n, double m_ratio, uint64_t stages, uint64_t 
     cfg.m_ratio = m_ratio;
     cfg.spectrum.q_list = {q};
     cfg.spectrum.shift = shift;
+    if (g_alt_on) {
+      cfg.spectrum.kind = SpectrumRule::Kind::alternating;
+      cfg.spectrum.odd_value = g_alt_odd;
+      cfg.spectrum.even_value = g_alt_even;
+      g_alt_on = 0;
+    }
     cfg.theta_list = {theta};
     cfg.stage_counts = {static_cast<std::size_t>(stages)};
     cfg.left_stage_count = static_cast<std::size_t>(left_stages);

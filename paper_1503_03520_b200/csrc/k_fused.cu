@@ -626,25 +626,10 @@ void launch_iter_v(const IterArgs& a, cudaStream_t st) {
   L1B_LAUNCHED();
 }
 
-// pipeline depth x min CTAs/SM; L1B_ITER_VARIANT overrides the default (tuning runs)
-int iter_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("L1B_ITER_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
+// pipeline depth 2 x 2 CTAs/SM (measured best of 3/4/5 x 1..4)
 template <int S>
 void launch_iter(const IterArgs& a, cudaStream_t st) {
-  switch (iter_variant()) {
-    case 1: return launch_iter_v<S, 1, 4>(a, st);
-    case 2: return launch_iter_v<S, 1, 3>(a, st);
-    case 3: return launch_iter_v<S, 3, 1>(a, st);
-    case 4: return launch_iter_v<S, 1, 2>(a, st);
-    default: return launch_iter_v<S, 2, 2>(a, st);
-  }
+  launch_iter_v<S, 2, 2>(a, st);
 }
 
 }  // namespace

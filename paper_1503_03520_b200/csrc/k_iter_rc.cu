@@ -41,10 +41,9 @@
 //                        default, V = 8: 24n bytes per iteration)
 //   fista_rc_persistent  up to a chunk of iterations in one cooperative
 //                        launch (small instances, n <= 2^20)
-//   fista_pair_cluster / fista_pair_small
-//                        single-stage instances (n <= 16384 / 4096): pair-local
-//                        products, state in registers, an 8-CTA cluster or one
-//                        CTA for the whole chunk
+//   fista_pair_cluster   single-stage instances (n <= 16384): pair-local
+//                        products, state in registers, an 8-CTA cluster for
+//                        the whole chunk
 #include "common.cuh"
 #include "fista.cuh"
 #include "kernels.hpp"
@@ -836,116 +835,10 @@ __device__ __forceinline__ void pair_residual(double x0, double x1, bool pair, d
   r1 = s1 * x1 - b1;
 }
 
-template <int P>
-__global__ void __launch_bounds__(kPairThreads, 1) fista_pair_small(RcPArgs Pa, int off) {
-  __shared__ FistaDev sst;
-  extern __shared__ double cs[];
-  const RcArgs& A = Pa.a;
-  const int64_t n = A.n;
-  const int t = threadIdx.x, T = blockDim.x;
-  const double c = A.right.c[0], s = A.right.s[0];
-  double* c_sig = cs;
-  double* c_b = cs + 2 * P * T;
-  auto slot = [&](int k, int e) { return (2 * k + e) * T + t; };
-  if (t == 0) sst = *A.b.st;
-  int64_t a[P];
-  bool va[P], vb[P];
-  double xk[P][2], xm[P][2], rk[P][2], rm[P][2];
-  const uint64_t j0 = Pa.j0;
-  const double* X0 = Pa.X[j0 % 4];
-  const double* X1 = Pa.X[(j0 + 3) % 4];
-#pragma unroll
-  for (int k = 0; k < P; ++k) {
-    a[k] = 2 * (int64_t)(t + k * T) - off;
-    va[k] = a[k] >= 0 && a[k] < n;
-    vb[k] = a[k] + 1 >= 0 && a[k] + 1 < n;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const bool v = e == 0 ? va[k] : vb[k];
-      const int64_t i = a[k] + e;
-      c_sig[slot(k, e)] = v ? A.sigma[i] : 0.0;
-      c_b[slot(k, e)] = v ? A.b.b[i] : 0.0;
-      xk[k][e] = v ? X0[i] : 0.0;
-      xm[k][e] = v ? X1[i] : 0.0;
-    }
-    const bool pair = va[k] && vb[k];
-    const double s0 = c_sig[slot(k, 0)], s1 = c_sig[slot(k, 1)];
-    const double b0 = c_b[slot(k, 0)], b1 = c_b[slot(k, 1)];
-    pair_residual(xk[k][0], xk[k][1], pair, c, s, s0, s1, b0, b1, rk[k][0], rk[k][1]);
-    pair_residual(xm[k][0], xm[k][1], pair, c, s, s0, s1, b0, b1, rm[k][0], rm[k][1]);
-  }
-  __syncthreads();
-  uint64_t done = 0;
-  for (; done < Pa.iters; ++done) {
-    if (sst.stop) break;  // uniform: read after the last barrier
-    const double beta = sst.beta_y;
-    const double inv_l = 1.0 / sst.lval;
-    const double thr = sst.tau * inv_l;
-    double l1 = 0.0, rr = 0.0;
-    unsigned nz = 0, mism = 0;
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const bool pair = va[k] && vb[k];
-      const double s0 = c_sig[slot(k, 0)], s1 = c_sig[slot(k, 1)];
-      if (va[k]) rr += rk[k][0] * rk[k][0];  // ||r_k||^2: x_k's objective, recorded one step late
-      if (vb[k]) rr += rk[k][1] * rk[k][1];
-      double g0 = s0 * ((1.0 + beta) * rk[k][0] - beta * rm[k][0]);  // sigma r_y
-      double g1 = s1 * ((1.0 + beta) * rk[k][1] - beta * rm[k][1]);
-      if (pair) rotate_pair(g0, g1, c, s, false);  // G (.) = A^T r_y
-      double tr[2];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool v = e == 0 ? va[k] : vb[k];
-        const double y = xk[k][e] + beta * (xk[k][e] - xm[k][e]);
-        const double v_ = shrink(y - inv_l * (e == 0 ? g0 : g1), thr);
-        tr[e] = v ? v_ : 0.0;
-        if (v) {
-          l1 += fabs(v_);
-          nz += v_ != 0.0;
-          mism += v_ != y;
-        }
-      }
-      double n0, n1;
-      pair_residual(tr[0], tr[1], pair, c, s, s0, s1, c_b[slot(k, 0)], c_b[slot(k, 1)], n0, n1);
-      xm[k][0] = xk[k][0];
-      xm[k][1] = xk[k][1];
-      xk[k][0] = tr[0];
-      xk[k][1] = tr[1];
-      rm[k][0] = rk[k][0];
-      rm[k][1] = rk[k][1];
-      rk[k][0] = n0;
-      rk[k][1] = n1;
-    }
-    double sums[4] = {l1, (double)nz, (double)mism, rr};
-    block_sum<4>(sums);
-    if (t == 0) {
-      sst.scal[0] = sums[0];
-      sst.scal[1] = sums[1];
-      sst.scal[2] = sums[2];
-      sst.scal[3] = sums[3];
-      fista_finalize_lagged(&sst, A.b.trace, false);
-    }
-    __syncthreads();
-  }
-  // the two newest iterates back to their rotating buffers
-  double* Xk = Pa.X[(j0 + done) % 4];
-  double* Xm = Pa.X[(j0 + done + 3) % 4];
-#pragma unroll
-  for (int k = 0; k < P; ++k) {
-    if (va[k]) {
-      Xk[a[k]] = xk[k][0];
-      Xm[a[k]] = xm[k][0];
-    }
-    if (vb[k]) {
-      Xk[a[k] + 1] = xk[k][1];
-      Xm[a[k] + 1] = xm[k][1];
-    }
-  }
-  if (t == 0) *A.b.st = sst;
-}
-
-// The same pair-local iteration on a cluster of kClusterCtas CTAs (one per SM):
-// FP64 work and the per-thread pair count shrink 8x.  The reduction goes
+// Single-stage instances, pair-local: with one Givens stage every product acts
+// on disjoint pairs, so a thread keeps its pairs' x_k, x_{k-1}, r_k, r_{k-1}
+// in registers for a whole chunk of iterations, on a cluster of kClusterCtas
+// CTAs (one per SM).  The reduction goes
 // through distributed shared memory with ONE cluster barrier per iteration:
 // every CTA stores its four block sums into every CTA (double-buffered by
 // iteration parity), and after the barrier each CTA folds the eight partials
@@ -1106,17 +999,9 @@ void launch_pair_cluster_p(const RcPArgs& p, int threads, int off, cudaStream_t 
   L1B_LAUNCHED();
 }
 
-template <int P>
-void launch_pair_small_p(const RcPArgs& p, int threads, int off, cudaStream_t st) {
-  const int bytes = 4 * P * threads * (int)sizeof(double);
-  L1B_CUDA(cudaFuncSetAttribute(fista_pair_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  fista_pair_small<P><<<1, threads, bytes, st>>>(p, off);
-  L1B_LAUNCHED();
-}
-
 // single-stage instances: a cluster of 8 CTAs for at most 2 x 8 x 512 pairs
-// (n <= 16384), else one CTA for at most 4 x 512 pairs; offset 1 needs n / 2 + 1
-// pairs.  L1B_PAIR_SMALL=0 keeps the window kernel, =1 the one-CTA kernel.
+// (n <= 16384); offset 1 needs n / 2 + 1 pairs.  L1B_PAIR_SMALL=0 keeps the
+// window kernel (the cross-check).
 bool launch_pair_small(const RcPArgs& p, const StageTab& right, cudaStream_t st) {
   const char* e = getenv("L1B_PAIR_SMALL");
   if (e && e[0] == '0') return false;
@@ -1124,23 +1009,12 @@ bool launch_pair_small(const RcPArgs& p, const StageTab& right, cudaStream_t st)
   const int off = right.offset[0];
   const uint64_t n = (uint64_t)p.a.n;
   const uint64_t units = off ? n / 2 + 1 : (n + 1) / 2;
-  if (!(e && e[0] == '1')) {
-    for (int P : {1, 2}) {
-      const uint64_t thr = (units + (uint64_t)P * kClusterCtas - 1) / ((uint64_t)P * kClusterCtas);
-      if (thr > (uint64_t)kPairThreads) continue;
-      const int threads = (int)std::max<uint64_t>(32, (thr + 31) / 32 * 32);
-      if (P == 1) launch_pair_cluster_p<1>(p, threads, off, st);
-      if (P == 2) launch_pair_cluster_p<2>(p, threads, off, st);
-      return true;
-    }
-  }
-  for (int P : {1, 2, 4}) {
-    const uint64_t thr = (units + P - 1) / P;
+  for (int P : {1, 2}) {
+    const uint64_t thr = (units + (uint64_t)P * kClusterCtas - 1) / ((uint64_t)P * kClusterCtas);
     if (thr > (uint64_t)kPairThreads) continue;
-    const int threads = (int)((thr + 31) / 32 * 32);
-    if (P == 1) launch_pair_small_p<1>(p, threads, off, st);
-    if (P == 2) launch_pair_small_p<2>(p, threads, off, st);
-    if (P == 4) launch_pair_small_p<4>(p, threads, off, st);
+    const int threads = (int)std::max<uint64_t>(32, (thr + 31) / 32 * 32);
+    if (P == 1) launch_pair_cluster_p<1>(p, threads, off, st);
+    if (P == 2) launch_pair_cluster_p<2>(p, threads, off, st);
     return true;
   }
   return false;

@@ -692,13 +692,10 @@ PairPlan pcg_pair_plan(const ProblemView& v) {
     }
   };
   // four pairs per thread: 512-thread CTAs (one per SM, fewer partials per
-  // barrier; C3 42.3 -> 39.7 ms) unless L1B_PCG_BT=256
-  const char* eb = getenv("L1B_PCG_BT");
-  const bool wide = !(eb && atoi(eb) == 256);
+  // barrier; C3 42.3 -> 39.7 ms against 256-thread CTAs)
   try_p(1, pair_capacity<1>());
   try_p(2, pair_capacity<2>());
-  if (wide) try_p(4, pair_capacity<4, 512>(), 512);
-  try_p(4, pair_capacity<4>());
+  try_p(4, pair_capacity<4, 512>(), 512);
   try_p(8, pair_capacity<8>());
   return pl;
 }
@@ -714,10 +711,8 @@ int pcg_loop_grid() {
       return 0;
     }
     // all co-resident CTAs (measured at C3: 1/2/4/8 per SM -> 49/31/27/27 us per
-    // PCG iteration); L1B_PCG_BPS caps it for experiments
-    const char* e = getenv("L1B_PCG_BPS");
-    const int bps = e ? std::min(per_sm, std::max(1, atoi(e))) : per_sm;
-    return std::min(bps * sm_count(), spmv_grid_max());
+    // PCG iteration)
+    return std::min(per_sm * sm_count(), spmv_grid_max());
   }();
   return cap;
 }

@@ -1336,8 +1336,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   // barrier); without one the epochs run back to back.  Epochs of at most 256
   // blocks take event masks (MW words per member), longer ones event lists.
   const bool sync = cfg->has_target != 0;
-  const char* mask_env = getenv("L1B_PCDM_MASK");  // 0: event lists even for short epochs (A/B)
-  int mw = (per_epoch <= 128 && !(mask_env && mask_env[0] == '0')) ? 2 : 0;
+  int mw = per_epoch <= 128 ? 2 : 0;
   if (mw) pick_pair_kernel<2>(sync, try_p);
   if (!P) {  // (mask kernels take at most 2 pairs per thread)
     mw = 0;

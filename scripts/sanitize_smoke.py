@@ -9,6 +9,7 @@ import torch
 ROOT = os.path.join(os.path.dirname(__file__), "..")
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
 from paper_1503_03520_b200 import l1bench  # noqa: E402
 
 TH = 2 * math.pi / 10
@@ -34,11 +35,20 @@ for kw in [dict(n=1000, stages=4, q=1, s_divisor=50, seed=3), dict(n=101, stages
     torch.cuda.synchronize()
 # emulated shards (matrix-free single kernel + CSR/CSC)
 import test_gpu_shards as T  # noqa: E402
+from pyoracle import Oracle  # noqa: E402  (the shard tests' checker)
 
+ORC = Oracle()
 T.KW = dict(n=4096, stages=4, q=1, s_divisor=100, seed=3, theta=TH)
 for op in ("matrix_free", "sparse"):
-    T.test_shards_reproduce_single_device_fista(2, op)
+    T.test_shards_reproduce_single_device_fista(2, op, ORC)
 T.KW_PERM = dict(n=1024, stages=2, left_stages=1, permute=True, q=1, s_divisor=50, seed=6, theta=TH)
-T.test_general_shards_reproduce_single_device_fista(2)
+T.test_general_shards_reproduce_single_device_fista(2, ORC)
+# the C2 path at a small size: jump-started coordinate stream, sorted look-back,
+# device walk over several segments, event masks, the cp.async epoch kernel,
+# fold; serial CD (B = 1); with a target (cooperative epochs)
+c2 = l1bench.build_instance(n=8192, stages=1, q=1, s_divisor=100, seed=1, theta=TH)
+l1bench.pcdm_run(c2, l1bench.SolverConfig(max_iters=30, block=256, seed=1))
+l1bench.coordinate_descent_run(c2, l1bench.SolverConfig(max_iters=5, seed=1))
+l1bench.pcdm_run(c2, l1bench.SolverConfig(max_iters=10, block=256, seed=1, target_objective=1.0))
 torch.cuda.synchronize()
 print("sanitize smoke done")

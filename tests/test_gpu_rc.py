@@ -244,10 +244,9 @@ def _pair_instance(oracle, n, off, q, seed):
 @pytest.mark.parametrize("n,off", [(4096, 0), (4095, 1), (2047, 0), (1000, 1), (513, 0), (6, 1), (3, 0),
                                    (12001, 1), (16384, 0)])
 def test_pair_small_kernel_bit_identical(oracle, n, off):
-    """The pair-local kernels for single-stage instances -- the 8-CTA cluster
-    (default, n <= 16384) and the one-CTA kernel (L1B_PAIR_SMALL=1, n <= 4096)
-    -- against the oracle and the window kernel (L1B_PAIR_SMALL=0): identical
-    iterates, samples, stop."""
+    """The pair-local kernel for single-stage instances (an 8-CTA cluster, the
+    default for n <= 16384) against the oracle and the window kernel
+    (L1B_PAIR_SMALL=0): identical iterates, samples, stop."""
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
@@ -259,7 +258,7 @@ def test_pair_small_kernel_bit_identical(oracle, n, off):
     np.testing.assert_array_equal(x, ox)
     np.testing.assert_array_equal(tr.iters(), otr["iter"])
     assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
-    for mode in ("0", "1") if n <= 4096 else ("0",):
+    for mode in ("0",):
         tw, xw = _solve(inst, iters, rc=True, env={"L1B_PAIR_SMALL": mode})
         np.testing.assert_array_equal(x, xw)
         np.testing.assert_array_equal(tr.iters(), tw.iters())

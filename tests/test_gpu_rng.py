@@ -176,3 +176,22 @@ def test_coordinate_index_stream_bit_exact(oracle, n, pieces):
     lim = np.uint64((1 << 64) - 1 - ((1 << 64) - 1) % n)
     want = np.where(raw >= lim, np.uint64(0xFFFFFFFF), raw % np.uint64(n)).astype(np.uint32)
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("kw", [dict(n=3001, stages=3, alternating=(2.0, 0.5), s_divisor=30, seed=8),
+                                dict(n=4096, stages=1, alternating=(0.1, 100.0), s_divisor=64, seed=5),
+                                dict(n=70001, stages=4, alternating=(3.0, 0.25), s_divisor=100, seed=2)])
+def test_alternating_spectrum_matches_reference(reference, kw):
+    """SpectrumRule::Kind::alternating (Spectrum::alternating, linops.cpp:332-335)
+    built on the device against the reference's own build_instance (the
+    unmodified reference library): sigma, b and x* bit for bit."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(kw, theta=2 * math.pi / 10)
+    dev = l1bench.build_instance(**kw)
+    ref = reference.build_instance(**kw)
+    np.testing.assert_array_equal(dev.sigma(), ref.sigma())
+    np.testing.assert_array_equal(dev.b, ref.b())
+    np.testing.assert_array_equal(dev.x_star.support, ref.x_star()[0])
+    np.testing.assert_array_equal(dev.x_star.values, ref.x_star()[1])
