@@ -212,7 +212,7 @@ struct l1b_problem {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv,
                     (void*)d_b, (void*)d_b_win, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
-                    (void*)csc.idx, (void*)csc.val})
+                    (void*)csc.idx, (void*)csc.val, (void*)csr.tile_rng, (void*)csc.tile_rng})
       if (p) cudaFree(p);  // (pool buffers go back to the pool; the stream is idle)
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
@@ -227,6 +227,8 @@ struct l1b_problem {
     c.val = csr.val;
     c.lanes = 32;
     c.tile_nnz_max = csr.tile_nnz_max;
+    c.tile_rng = csr.tile_rng;
+    c.x_len = csr.x_len;
     return c;
   }
   Csr cols() const {
@@ -239,6 +241,8 @@ struct l1b_problem {
     c.val = csc.val;
     c.lanes = 32;
     c.tile_nnz_max = csc.tile_nnz_max;
+    c.tile_rng = csc.tile_rng;
+    c.x_len = csc.x_len;
     return c;
   }
 };

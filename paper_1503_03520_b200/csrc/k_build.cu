@@ -202,6 +202,33 @@ __global__ void tile_max_kernel(const uint64_t* offs, uint64_t lines, uint64_t t
   if (mx) atomicMax(out, mx);
 }
 
+// min / max stored index of each 256-line tile (one warp per tile)
+template <typename PtrT>
+__global__ void tile_range_kernel(const PtrT* __restrict__ ptr, const uint32_t* __restrict__ idx, uint64_t lines,
+                                  uint32_t* __restrict__ rng, unsigned* max_idx) {
+  const uint64_t ntiles = (lines + 255) / 256;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+       t += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint64_t a = ptr[t * 256], b = ptr[min(t * 256 + 256, lines)];
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint64_t q = a + lane; q < b; q += 32) {
+      const uint32_t v = idx[q];
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+    for (int o = 16; o; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      rng[2 * t] = lo;
+      rng[2 * t + 1] = hi;
+      if (b > a) atomicMax(max_idx, hi);
+    }
+  }
+}
+
 __global__ void widen_u32(const uint32_t* in, uint64_t* out, uint64_t n) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
        t += (uint64_t)gridDim.x * blockDim.x)
@@ -277,6 +304,7 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
     unsigned long long last;
     unsigned int max_len;
     int overflow;
+    unsigned int max_idx;
   }* scratch = nullptr;
   L1B_CUDA(cudaMallocAsync(&counts, (nlines + 1) * sizeof(uint32_t), st));
   L1B_CUDA(cudaMallocAsync(&offs, (nlines + 1) * sizeof(uint64_t), st));
@@ -345,12 +373,28 @@ void build_lines(const OpView& op, bool rows, uint64_t first, uint64_t nlines, u
     tile_max_kernel<<<grid_for((keep + 255) / 256), kThreads, 0, st>>>(offs, keep, 256, &scratch->last);
     L1B_LAUNCHED();
   }
+  if (keep > 0) {  // per-tile index ranges (x staged with the tile)
+    const uint64_t ntiles = (keep + 255) / 256;
+    if (cudaMalloc(&out->tile_rng, ntiles * 2 * sizeof(uint32_t)) != cudaSuccess) {
+      cudaGetLastError();
+      out->tile_rng = nullptr;  // the SpMV then gathers x from global memory
+    } else if (out->ptr32) {
+      tile_range_kernel<uint32_t><<<grid_for(ntiles * 32), kThreads, 0, st>>>((const uint32_t*)out->ptr, out->idx,
+                                                                              keep, out->tile_rng, &scratch->max_idx);
+      L1B_LAUNCHED();
+    } else {
+      tile_range_kernel<uint64_t><<<grid_for(ntiles * 32), kThreads, 0, st>>>((const uint64_t*)out->ptr, out->idx,
+                                                                              keep, out->tile_rng, &scratch->max_idx);
+      L1B_LAUNCHED();
+    }
+  }
   L1B_CUDA(cudaMemcpyAsync(&h, scratch, sizeof(Scratch), cudaMemcpyDeviceToHost, st));
   L1B_CUDA(cudaFreeAsync(counts, st));
   L1B_CUDA(cudaFreeAsync(offs, st));
   L1B_CUDA(cudaFreeAsync(scratch, st));
   L1B_CUDA(cudaStreamSynchronize(st));
   out->tile_nnz_max = h.last;
+  out->x_len = total ? (uint64_t)h.max_idx + 1 : 0;
 }
 
 void gram_diagonal(const OpView& op, uint64_t first, uint64_t ncols, double* d, cudaStream_t st) {

@@ -21,6 +21,8 @@ struct LinesOut {
   void* ptr = nullptr;   // (lines + 1) x u32 or u64 (+16 B of slack for the bulk copies)
   uint32_t* idx = nullptr;
   double* val = nullptr;
+  uint32_t* tile_rng = nullptr;  // per 256-line tile: min, max index (the SpMV stages x[min..max])
+  uint64_t x_len = 0;            // largest index + 1: entries of x the products read
 };
 // Lines [first, first + nlines) of A (rows) or A^T (columns = CSC of A).
 // Indices are stored minus idx_base (wrapping), i.e. local to a window; only
@@ -106,6 +108,8 @@ struct Csr {  // CSR of A (rows) or of A^T (= CSC of A)
   const double* val = nullptr;
   int lanes = 32;  // lines per warp tile (fallback kernel)
   uint64_t tile_nnz_max = ~0ull;  // max nonzeros of a 256-line tile (TMA kernel when <= 2048)
+  const uint32_t* tile_rng = nullptr;  // per 256-line tile: min, max index (null: not staged)
+  uint64_t x_len = 0;                  // x entries the products may read (staging never reads past)
 };
 
 // y[0, lines) = M x

@@ -110,6 +110,10 @@ constexpr int kTileNnz = 2048;    // nonzero capacity of one tile
 constexpr int kStages = L1B_SPMV_STAGES;
 constexpr int kVecTma = L1B_SPMV_VEC;
 
+// x window staged with each tile when the tile's index range fits (banded
+// operators: 256 + 2 x bandwidth entries): the gathers then hit shared memory
+constexpr int kTileX = 320;
+
 template <typename PtrT, int NV>
 struct TmaLayout {
   static constexpr size_t r16(size_t b) { return (b + 15) / 16 * 16; }
@@ -117,7 +121,8 @@ struct TmaLayout {
   static constexpr size_t idx_bytes = (kTileNnz + 8) * 4;
   static constexpr size_t ptr_bytes = r16((kTileLines + 1 + 16 / sizeof(PtrT)) * sizeof(PtrT));
   static constexpr size_t vec_bytes = kVecTma ? kTileLines * 8 : 0;
-  static constexpr size_t stage_bytes = vals_bytes + idx_bytes + ptr_bytes + NV * vec_bytes;
+  static constexpr size_t x_bytes = kTileX * 8;
+  static constexpr size_t stage_bytes = vals_bytes + idx_bytes + ptr_bytes + NV * vec_bytes + x_bytes;
   static constexpr size_t prod_off = kStages * stage_bytes;
   static constexpr size_t prod_bytes = r16((kTileNnz + kTileNnz / 16 + 2) * 8);
   static constexpr size_t bars_off = prod_off + prod_bytes;
@@ -130,11 +135,13 @@ __global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const
                                                                const double* __restrict__ val,
                                                                const double* __restrict__ x,
                                                                uint64_t nlines, Epi epi,
-                                                               int vec_tma) {
+                                                               int vec_tma, const uint32_t* __restrict__ tile_rng,
+                                                               uint64_t x_len) {
   if (epi.skip()) return;
   epi.start();
   using L = TmaLayout<PtrT, Epi::kVec>;
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t x_lo[kStages];  // first staged x index of each slot (~0: not staged)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
   double* prod = reinterpret_cast<double*>(smem + L::prod_off);
   const int t = threadIdx.x;
@@ -164,7 +171,21 @@ __global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const
     const PtrT ia = p0 & ~(PtrT)3, ib = (p1 + 3) & ~(PtrT)3;
     const uint32_t val_b = (uint32_t)(vb - va) * 8u, idx_b = (uint32_t)(ib - ia) * 4u;
     const uint32_t nv = vec_tma ? (uint32_t)(nl & ~1ull) : 0u;
-    mbar_arrive_expect_tx(&bars[k % kStages], ptr_b + val_b + idx_b + Epi::kVec * nv * 8u);
+    // x[lo .. hi] for this tile's gathers (16-byte aligned superset) when it fits
+    uint32_t x_b = 0;
+    uint64_t xl = ~0ull;
+    if (tile_rng) {
+      const uint64_t tix = blockIdx.x + k * gridDim.x;
+      const uint64_t lo = tile_rng[2 * tix] & ~1ull, hi = tile_rng[2 * tix + 1];
+      const uint64_t cnt = (hi - lo + 2) & ~1ull;  // even: 16-byte bulk copies
+      if (hi >= lo && cnt <= (uint64_t)kTileX && lo + cnt <= x_len) {  // never past x's end
+        xl = lo;
+        x_b = (uint32_t)(cnt * 8);
+      }
+    }
+    x_lo[k % kStages] = xl;
+    mbar_arrive_expect_tx(&bars[k % kStages], ptr_b + val_b + idx_b + Epi::kVec * nv * 8u + x_b);
+    if (x_b) bulk_g2s(s_vec + Epi::kVec * (L::vec_bytes / 8), x + xl, x_b, &bars[k % kStages]);
     bulk_g2s(s_ptr, ptr + r0, ptr_b, &bars[k % kStages]);
     if (val_b) bulk_g2s_evict_first(s_val, val + va, val_b, &bars[k % kStages], pol);
     if (idx_b) bulk_g2s_evict_first(s_idx, idx + ia, idx_b, &bars[k % kStages], pol);
@@ -208,6 +229,8 @@ __global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const
     mbar_wait(&bars[k % kStages], (uint32_t)((k / kStages) & 1));
     const PtrT p0 = s_ptr[0], p1 = s_ptr[nl];
     const PtrT va = p0 & ~(PtrT)1, ia = p0 & ~(PtrT)3;
+    const uint64_t xl = x_lo[k % kStages];
+    const double* s_x = s_vec + Epi::kVec * (L::vec_bytes / 8) - (xl == ~0ull ? 0 : xl);
     // products: 8 independent gathers per thread
     for (PtrT q0 = p0 + t; q0 < p1; q0 += kThreads * kUnroll) {
       double vv[kUnroll];
@@ -220,10 +243,18 @@ __global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const
           ii[u] = s_idx[q - ia];
         }
       }
+      if (xl != ~0ull) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const PtrT q = q0 + kThreads * u;
-        if (q < p1) prod[pad((int)(q - p0))] = vv[u] * __ldg(x + ii[u]);
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + kThreads * u;
+          if (q < p1) prod[pad((int)(q - p0))] = vv[u] * s_x[ii[u]];
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const PtrT q = q0 + kThreads * u;
+          if (q < p1) prod[pad((int)(q - p0))] = vv[u] * __ldg(x + ii[u]);
+        }
       }
     }
     __syncthreads();
@@ -264,10 +295,12 @@ inline void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t
     int vec_tma = kVecTma;
     for (int v = 0; v < Epi::kVec; ++v)
       if (reinterpret_cast<uintptr_t>(epi.vec(v)) % 16) vec_tma = 0;
+    // x staging needs 16-byte aligned x (odd windows gather from global memory)
+    const uint32_t* rng = reinterpret_cast<uintptr_t>(x) % 16 ? nullptr : M.tile_rng;
     const uint64_t tiles = (M.lines + kTileLines - 1) / kTileLines;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
     spmv_tma_kernel<PtrT, Epi><<<grid, kThreads, L::total, st>>>(
-        (const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi, vec_tma);
+        (const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi, vec_tma, rng, M.x_len);
     L1B_LAUNCHED();
     return;
   }
