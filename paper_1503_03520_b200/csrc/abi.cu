@@ -210,10 +210,16 @@ struct l1b_problem {
   ~l1b_problem() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv,
-                    (void*)d_b, (void*)d_b_win, (void*)d_gram, csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr,
-                    (void*)csc.idx, (void*)csc.val, (void*)csr.tile_rng, (void*)csc.tile_rng})
-      if (p) cudaFree(p);  // (pool buffers go back to the pool; the stream is idle)
+    // stream-ordered pool buffers go back to the (retained) pool: cudaFree on
+    // them would hand the pages back to the driver and the next problem of the
+    // same size would map them again (the e2e passes varied 0.38 - 0.6 s)
+    for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv, (void*)d_b,
+                    (void*)d_b_win, (void*)d_gram})
+      if (p) cudaFreeAsync(p, stream);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : {csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr, (void*)csc.idx, (void*)csc.val,
+                    (void*)csr.tile_rng, (void*)csc.tile_rng})
+      if (p) cudaFree(p);  // (the CSR/CSC copy: plain allocations)
     if (stream && own_stream) cudaStreamDestroy(stream);
   }
 
@@ -924,6 +930,7 @@ extern "C" {
 
 // build_instance (bench.cpp:253-316) + generate_instance (instance.cpp:53-89).
 int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard, l1b_problem** out) {
+  NvtxRange nvtx("l1b_generate");
   return guard([&] {
     if (!g || !out) throw InvalidArgument("null argument");
     *out = nullptr;
@@ -944,6 +951,7 @@ int l1b_generate(int device, const l1b_gen_desc* g, const l1b_shard_desc* shard,
 int l1b_problem_create(int device, const l1b_operator_desc* op, double tau, const double* b_host,
                        const uint32_t* xs_support, const double* xs_values, uint64_t s,
                        l1b_problem** out) {
+  NvtxRange nvtx("l1b_problem_create");
   return guard([&] {
     if (!op || !out || !b_host || !op->sigma) throw InvalidArgument("null argument");
     *out = nullptr;
@@ -1143,6 +1151,7 @@ int l1b_problem_set_stream(l1b_problem* p, void* stream) {
 }
 
 int l1b_apply(l1b_problem* p, int path, const double* d_x, double* d_y) {
+  NvtxRange nvtx("l1b_apply");
   return guard([&] {
     check_whole(p);
     if (path == L1B_PATH_SWEEP) {

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -37,6 +38,15 @@ struct Unsupported : std::runtime_error {
 };
 struct NcclError : std::runtime_error {
   using std::runtime_error::runtime_error;
+};
+
+// NVTX range around a C-ABI entry point (header-only NVTX 3: a no-op unless a
+// tool such as nsys / ncu --nvtx attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -685,6 +686,7 @@ int l1b_session_finalize(l1b_session* s) {
 }
 
 int l1b_session_step(l1b_session* s, uint64_t iters) {
+  NvtxRange nvtx("l1b_session_step");
   return guard([&] {
     if (!s) throw InvalidArgument("null session");
     if (s->shard) throw LogicError("shard sessions are stepped by the caller (k1 / k2 / finalize)");
@@ -829,6 +831,7 @@ int l1b_session_end(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
 
 int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
               l1b_summary* summary, double* x_host, double* d_x) {
+  NvtxRange nvtx("l1b_solve");
   return guard([&] {
     if (!p || !summary) throw InvalidArgument("null argument");
     ProblemView v = problem_view(p, false);
@@ -850,6 +853,15 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     }
     // host-side setup before session_begin: the device clock of the trace
     // starts in its init kernel
+    // L1B_SOLVE_TRACE=1: host-side phase times on stderr
+    const bool tracing = getenv("L1B_SOLVE_TRACE") != nullptr;
+    auto tp = std::chrono::steady_clock::now();
+    auto ptrace = [&](const char* what) {
+      if (!tracing) return;
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[l1b_solve] %-16s %9.1f us\n", what, std::chrono::duration<double, std::micro>(now - tp).count());
+      tp = now;
+    };
     int* h_flags = nullptr;
     L1B_CUDA(cudaMallocHost(&h_flags, 2 * sizeof(int)));
     l1b_session s;
@@ -859,6 +871,7 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       cudaFreeHost(h_flags);
       throw;
     }
+    ptrace("session begun");
     cudaStream_t st = v.stream;
     cudaEvent_t ev[2];
     L1B_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -891,6 +904,7 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
         chunk = std::min<uint64_t>(chunk * 2, 64);
       }
       L1B_CUDA(cudaStreamSynchronize(st));
+      ptrace("iterations done");
     } catch (...) {
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
@@ -901,6 +915,7 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     cudaEventDestroy(ev[1]);
     cudaFreeHost(h_flags);
     session_finish(&s, samples, cap, summary, x_host, d_x);
+    ptrace("finished");
   });
 }
 
@@ -1034,6 +1049,7 @@ int l1b_session_nccl_start(l1b_session* s) {
 }
 
 int l1b_session_nccl_steps(l1b_session* s, uint64_t launches, int use_graph, double* k1_ms) {
+  NvtxRange nvtx("l1b_session_nccl_steps");
   return guard([&] {
     check_comm(s);
     L1B_CUDA(cudaSetDevice(s->v.device));
