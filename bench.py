@@ -105,8 +105,6 @@ class ClockSampler:
 # matrix-free kernels by l1b_session_kernel_mode: (bytes per launch / n, iterations
 # per launch, name); every array at its stored width, each element once
 MF_KERNELS = {
-    6: (56, 3, "fista_rc3 (three FISTA iterations per launch, matrix-free, residuals recomputed): "
-               "x_k, x_{k-1}, sigma, b read, x_{k+1}, x_{k+2}, x_{k+3} written"),
     4: (48, 2, "fista_rc2 (two FISTA iterations per launch, matrix-free, residuals recomputed): "
                "x_k, x_{k-1}, sigma, b read, x_{k+1}, x_{k+2} written"),
     3: (40, 1, "fista_rc (one FISTA iteration, matrix-free, residuals recomputed): x_k, x_{k-1}, "
@@ -165,7 +163,7 @@ def roofline(path, t, info, peak, peak_src):
     b1, b2, ipl = kernel_bytes(path, n, m_act, nnz, ptr_bytes, t.get("kmode"))
     if path == "matrix_free":
         names = (MF_KERNELS[t["kmode"]][2], "-")
-        key1 = {6: "rc3", 4: "rc2", 3: "k1", 2: "stored"}[t["kmode"]]
+        key1 = {4: "rc2", 3: "k1", 2: "stored"}[t["kmode"]]
     else:
         names = ("fista_k1 (A^T r_y + prox/momentum, CSC)", "fista_k2 (A x - b + residual momentum, CSR)")
         key1 = "k1"

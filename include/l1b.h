@@ -326,8 +326,7 @@ enum {
   L1B_RAN_PCG_PAIR = 1u << 10,        /* pair-local PCG, one cooperative launch per Newton step */
   L1B_RAN_PCG_LOOP = 1u << 11,        /* CSR/CSC PCG, one cooperative launch per Newton step */
   L1B_RAN_PCG_KERNELS = 1u << 12,     /* CSR/CSC PCG, four kernels per PCG iteration */
-  L1B_RAN_HOST_LED = 1u << 13,        /* FISTA / ISTA with LPolicy::backtracking (host-led trials) */
-  L1B_RAN_FISTA_THREE_ITER = 1u << 14 /* three iterations per launch (fista_rc3v_kernel) */
+  L1B_RAN_HOST_LED = 1u << 13         /* FISTA / ISTA with LPolicy::backtracking (host-led trials) */
 };
 
 int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
@@ -420,16 +419,14 @@ int l1b_session_prox(l1b_session* s);
 /* Which FISTA kernels a session runs (bench roofline bookkeeping):
  * bytes per iteration 288n-class CSR/CSC pair, 96n matrix-free pair, 64n
  * stored-residual single kernel, 40n recomputing kernel, 24n two-iteration
- * recomputing kernel, 56n/3 three-iteration recomputing kernel (one device),
- * general-shard CSR/CSC.                                                    */
+ * recomputing kernel (one device), general-shard CSR/CSC.                   */
 enum {
   L1B_KMODE_SPARSE = 0,
   L1B_KMODE_MATRIX_FREE_PAIR = 1,
   L1B_KMODE_STORED_RESIDUAL = 2,
   L1B_KMODE_RECOMPUTE = 3,
   L1B_KMODE_RECOMPUTE_TWO = 4,
-  L1B_KMODE_GENERAL_SHARD = 5,
-  L1B_KMODE_RECOMPUTE_THREE = 6
+  L1B_KMODE_GENERAL_SHARD = 5
 };
 int l1b_session_kernel_mode(l1b_session* s, int* mode);
 int l1b_session_k1(l1b_session* s);

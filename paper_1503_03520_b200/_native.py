@@ -56,7 +56,7 @@ class ProblemInfo(C.Structure):
 
 # l1b_session_kernel_mode (include/l1b.h)
 KMODE_SPARSE, KMODE_MATRIX_FREE_PAIR, KMODE_STORED_RESIDUAL = 0, 1, 2
-KMODE_RECOMPUTE, KMODE_RECOMPUTE_TWO, KMODE_GENERAL_SHARD, KMODE_RECOMPUTE_THREE = 3, 4, 5, 6
+KMODE_RECOMPUTE, KMODE_RECOMPUTE_TWO, KMODE_GENERAL_SHARD = 3, 4, 5
 
 
 class ShardBuffers(C.Structure):
@@ -96,8 +96,7 @@ class Summary(C.Structure):
 # l1b_summary.path flags (include/l1b.h L1B_RAN_*)
 RAN = {name: 1 << i for i, name in enumerate(
     ["fista_sparse", "fista_mf_pair", "fista_stored", "fista_recompute", "fista_two_iter", "fista_loop",
-     "fma", "pcdm_pair", "pcdm_plan", "pcdm_direct", "pcg_pair", "pcg_loop", "pcg_kernels", "host_led",
-     "fista_three_iter"])}
+     "fma", "pcdm_pair", "pcdm_plan", "pcdm_direct", "pcg_pair", "pcg_loop", "pcg_kernels", "host_led"])}
 
 
 # every symbol include/l1b.h declares: (name, restype, argtypes)

@@ -115,37 +115,4 @@ __device__ inline void fista_finalize_lagged2(FistaDev* st, FistaSample* trace) 
   st->pend_valid = 1;
 }
 
-// Lagged bookkeeping after a three-iteration kernel (iterations j+1 .. j+3):
-// records iteration j (stashed sums + ||r_j||^2), then j+1 and j+2 (their sums
-// and residuals are in scal12), each unless the previous record stopped the
-// loop; then the momentum for the next kernel and x_{j+3}'s sums are stashed.
-// Same values and order of checks as three fista_finalize_lagged calls.
-__device__ inline void fista_finalize_lagged3(FistaDev* st, FistaSample* trace) {
-  const double* q = st->scal12;
-  const uint64_t ts = global_timer_ns();
-  if (st->pend_valid) {
-    const double f = st->tau * st->pend[0] + 0.5 * (q[0] + st->tail_sq);
-    st->pend_valid = 0;
-    fista_record(st, trace, st->k + 1, f, st->pend[1], st->pend[2] == 0.0, st->pend_ts);
-    if (st->stop) return;
-  }
-  double t_next, beta;
-  for (int it = 0; it < 2; ++it) {  // x_{j+1}, x_{j+2}: sums at q[1 + 4 it], ||r|| at q[4 + 4 it]
-    fista_momentum(st, &t_next, &beta);  // the step the kernel used for the next iterate
-    st->beta_y = beta;
-    if (st->accel) st->t = t_next;
-    const double f = st->tau * q[1 + 4 * it] + 0.5 * (q[4 + 4 * it] + st->tail_sq);
-    fista_record(st, trace, st->k + 1, f, q[2 + 4 * it], q[3 + 4 * it] == 0.0, ts);
-    if (st->stop) return;
-  }
-  fista_momentum(st, &t_next, &beta);
-  st->beta_y = beta;
-  if (st->accel) st->t = t_next;
-  st->pend[0] = q[9];
-  st->pend[1] = q[10];
-  st->pend[2] = q[11];
-  st->pend_ts = ts;
-  st->pend_valid = 1;
-}
-
 }  // namespace l1b

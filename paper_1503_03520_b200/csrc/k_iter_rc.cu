@@ -616,201 +616,6 @@ __global__ void __launch_bounds__(kRcThreads, MB) fista_rc2v_kernel(RcArgs A, Rc
   }
 }
 
-// THREE FISTA iterations per launch (temporal blocking one step deeper): a
-// launch reads x_k, x_{k-1}, sigma, b once and writes x_{k+1}, x_{k+2},
-// x_{k+3}: 56n bytes per three iterations (18.7n per iteration against 24n).
-// Seven chain runs (six in series: the halo is 6S), the same operations per
-// iteration as the two-iteration kernel, so the same iterates.
-template <int S, int V>
-struct RcGeom3V {
-  static constexpr int W = 32 * V;
-  static constexpr int H3 = (6 * S + V - 1) / V * V;
-  static constexpr int OWN = W - 2 * H3;
-};
-
-struct Acc3 {
-  double rr[3] = {0.0, 0.0, 0.0};  // ||r_k||^2, ||r_{k+1}||^2, ||r_{k+2}||^2
-  double l1[3] = {0.0, 0.0, 0.0};  // ||x_{k+1}||_1, ||x_{k+2}||_1, ||x_{k+3}||_1
-  unsigned nz[3] = {0, 0, 0}, mis[3] = {0, 0, 0};
-};
-
-struct Rc3Out {
-  double *x1, *x2, *x3;
-};
-
-template <int S, bool FAST, int PAR, int V, bool F>
-__device__ __forceinline__ void segment3v(const RcArgs& A, const Rc3Out& O, const SegV<V>& d, int64_t w0,
-                                          int lane, bool lane_own, double beta_a, double beta_b, double beta_c,
-                                          double inv_l, double thr, Acc3& acc) {
-  using G = RcGeom3V<S, V>;
-  const int64_t n = A.n;
-  const int64_t e0 = w0 + V * lane;
-  bool mine[V];
-  if (FAST) {
-#pragma unroll
-    for (int i = 0; i < V; ++i) mine[i] = lane_own;
-  } else {
-    const int64_t own_lo = w0 + G::H3, own_hi = min(own_lo + G::OWN, A.hi);
-#pragma unroll
-    for (int i = 0; i < V; ++i) mine[i] = e0 + i >= own_lo && e0 + i < own_hi;
-  }
-  // iteration 1: r_k, r_{k-1} rebuilt from x_k, x_{k-1}
-  double t[2][V];
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    t[0][i] = d.xk[i];
-    t[1][i] = d.xm[i];
-  }
-  wchainv<S, true, FAST, 2, PAR, V, F>(t, e0, n, A.right);
-  double rprev[V], g[1][V], rr = 0.0;  // rprev: r_k, then r_{k+1}
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    rprev[i] = mul_sub<F>(d.sg[i], t[0][i], d.bb[i]);
-    if (mine[i]) rr = F ? __fma_rn(rprev[i], rprev[i], rr) : rr + rprev[i] * rprev[i];
-    const double rm = mul_sub<F>(d.sg[i], t[1][i], d.bb[i]);
-    g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_a, rprev[i], beta_a * rm);
-  }
-  acc.rr[0] += rr;
-  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
-  double xa[V], xb[V];  // x_{k+1}, then x_{k+2} (xb); the older one for the momentum
-  {
-    double l1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const double y = F ? __fma_rn(beta_a, d.xk[i] - d.xm[i], d.xk[i]) : d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
-      double v = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
-      l1 += mine[i] ? fabs(v) : 0.0;
-      acc.nz[0] += (unsigned)(mine[i] & (v != 0.0));
-      acc.mis[0] += (unsigned)(mine[i] & (v != y));
-      if (!FAST && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
-      xa[i] = v;
-    }
-    acc.l1[0] += l1;
-  }
-  store_ownv<FAST, V>(O.x1, e0, mine, lane_own, xa);
-  // iteration 2: r_{k+1} from x_{k+1}; momentum with x_k
-  {
-    double t1[1][V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) t1[0][i] = xa[i];
-    wchainv<S, true, FAST, 1, PAR, V, F>(t1, e0, n, A.right);
-    double rr1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const double r1 = mul_sub<F>(d.sg[i], t1[0][i], d.bb[i]);
-      if (mine[i]) rr1 = F ? __fma_rn(r1, r1, rr1) : rr1 + r1 * r1;
-      g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_b, r1, beta_b * rprev[i]);
-      rprev[i] = r1;
-    }
-    acc.rr[1] += rr1;
-  }
-  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
-  {
-    double l1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const double y = F ? __fma_rn(beta_b, xa[i] - d.xk[i], xa[i]) : xa[i] + beta_b * (xa[i] - d.xk[i]);
-      double v = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
-      l1 += mine[i] ? fabs(v) : 0.0;
-      acc.nz[1] += (unsigned)(mine[i] & (v != 0.0));
-      acc.mis[1] += (unsigned)(mine[i] & (v != y));
-      if (!FAST && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
-      xb[i] = v;
-    }
-    acc.l1[1] += l1;
-  }
-  store_ownv<FAST, V>(O.x2, e0, mine, lane_own, xb);
-  // iteration 3: r_{k+2} from x_{k+2}; momentum with x_{k+1}
-  {
-    double t2[1][V];
-#pragma unroll
-    for (int i = 0; i < V; ++i) t2[0][i] = xb[i];
-    wchainv<S, true, FAST, 1, PAR, V, F>(t2, e0, n, A.right);
-    double rr2 = 0.0;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const double r2 = mul_sub<F>(d.sg[i], t2[0][i], d.bb[i]);
-      if (mine[i]) rr2 = F ? __fma_rn(r2, r2, rr2) : rr2 + r2 * r2;
-      g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_c, r2, beta_c * rprev[i]);
-    }
-    acc.rr[2] += rr2;
-  }
-  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
-  {
-    double x3[V], l1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const double y = F ? __fma_rn(beta_c, xb[i] - xa[i], xb[i]) : xb[i] + beta_c * (xb[i] - xa[i]);
-      x3[i] = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
-      l1 += mine[i] ? fabs(x3[i]) : 0.0;
-      acc.nz[2] += (unsigned)(mine[i] & (x3[i] != 0.0));
-      acc.mis[2] += (unsigned)(mine[i] & (x3[i] != y));
-    }
-    acc.l1[2] += l1;
-    store_ownv<FAST, V>(O.x3, e0, mine, lane_own, x3);
-  }
-}
-
-template <int S, int MB, int PAR, int V, bool PF, bool F>
-__global__ void __launch_bounds__(kRcThreads, MB) fista_rc3v_kernel(RcArgs A, Rc3Out O) {
-  using G = RcGeom3V<S, V>;
-  FistaDev* st = A.b.st;
-  if (*(volatile int*)&st->stop) return;
-  const double beta_a = st->beta_y;
-  // the next two steps of the t-sequence (solvers.cpp:349-350)
-  double beta_b, beta_c;
-  {
-    const double t1 = st->t;
-    const double t2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t1 * t1));
-    const double t3 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t2 * t2));
-    beta_b = st->accel ? (t1 - 1.0) / t2 : 0.0;
-    beta_c = st->accel ? (t2 - 1.0) / t3 : 0.0;
-  }
-  const double inv_l = 1.0 / st->lval;
-  const double thr = st->tau * inv_l;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool lane_own = V * lane >= G::H3 && V * lane < G::H3 + G::OWN;
-  const int64_t n = A.n, lo = A.lo, hi = A.hi;
-  const int64_t lim_lo = max((int64_t)0, lo - G::H3), lim_hi = min(n, hi + G::H3);
-  const int64_t nseg = (hi - lo + G::OWN - 1) / G::OWN;
-  const int64_t stride = (int64_t)gridDim.x * kRcWarps;
-  Acc3 acc;
-  auto w0_of = [&](int64_t q) { return lo + q * G::OWN - G::H3; };
-  auto full_of = [&](int64_t w0) { return w0 >= lim_lo && w0 + G::W <= lim_hi; };
-  const int64_t base = lo - G::H3;
-  const int64_t w_min = max((int64_t)2, lim_lo), w_max = min(lim_hi, n - 1) - G::W;
-  const int64_t q_lo = w_min <= base ? 0 : (w_min - base + G::OWN - 1) / G::OWN;
-  const int64_t q_hi = w_max < base ? 0 : min((w_max - base) / G::OWN + 1, (hi - lo) / G::OWN);
-  SegV<V> sa, sb;
-  int64_t q = (int64_t)blockIdx.x * kRcWarps + warp;
-  if (q < nseg) load_segv<V>(A, w0_of(q) + V * lane, full_of(w0_of(q)), lim_lo, lim_hi, sa);
-  for (; q < nseg; q += stride) {
-    if (PF && q + stride < nseg) {
-      const int64_t w1 = w0_of(q + stride);
-      load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sb);
-    }
-    if (q >= q_lo && q < q_hi)
-      segment3v<S, true, PAR, V, F>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, beta_c, inv_l, thr, acc);
-    else
-      segment3v<S, false, PAR, V, F>(A, O, sa, w0_of(q), lane, lane_own, beta_a, beta_b, beta_c, inv_l, thr, acc);
-    if (PF) {
-      sa = sb;
-    } else if (q + stride < nseg) {
-      const int64_t w1 = w0_of(q + stride);
-      load_segv<V>(A, w1 + V * lane, full_of(w1), lim_lo, lim_hi, sa);
-    }
-  }
-  double sums[12] = {acc.rr[0], acc.l1[0], (double)acc.nz[0], (double)acc.mis[0],
-                     acc.rr[1], acc.l1[1], (double)acc.nz[1], (double)acc.mis[1],
-                     acc.rr[2], acc.l1[2], (double)acc.nz[2], (double)acc.mis[2]};
-  double tot[12];
-  if (grid_sum<12>(sums, A.b.partials, &st->ticket[0], tot) && threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < 12; ++k) st->scal12[k] = tot[k];
-    fista_finalize_lagged3(st, A.b.trace);
-  }
-}
-
 // Small instances (C1: n = 2^12, a few warps of work per iteration): the
 // per-kernel cost is launch + grid-reduction latency, not bandwidth.  One
 // cooperative launch then runs up to `iters` iterations back to back, with
@@ -1256,17 +1061,6 @@ void launch_rc2(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
   L1B_LAUNCHED();
 }
 
-template <int S, int PAR, bool F>
-void launch_rc3(const RcArgs& a, const Rc3Out& o, cudaStream_t st) {
-  using G = RcGeom3V<S, kRc2V>;
-  const int grid_cap = grid_cap_of<fista_rc3v_kernel<S, 1, PAR, kRc2V, true, F>>();
-  const int64_t nseg = (a.hi - a.lo + G::OWN - 1) / G::OWN;
-  const int64_t blocks = (nseg + kRcWarps - 1) / kRcWarps;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, grid_cap));
-  fista_rc3v_kernel<S, 1, PAR, kRc2V, true, F><<<grid, kRcThreads, 0, st>>>(a, o);
-  L1B_LAUNCHED();
-}
-
 // offsets (S-1-s) % 2, the generator's alternating stages (bench.cpp:270)
 template <int S>
 constexpr int canon_par() {
@@ -1302,22 +1096,14 @@ void launch_rc2_s(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
 }  // namespace
 
 template <int S, bool F>
-void launch_rc3_s(const RcArgs& a, const Rc3Out& o, cudaStream_t st) {
-  if (is_canon<S>(a.right)) return launch_rc3<S, canon_par<S>(), F>(a, o, st);
-  launch_rc3<S, -1, F>(a, o, st);
-}
-
-template <int S, bool F>
 void prepare_s(const StageTab& t) {
   if (is_canon<S>(t)) {
     grid_cap_of<fista_rc_kernel<S, 2, false, canon_par<S>(), F>>();
     grid_cap_of<fista_rc2v_kernel<S, 1, canon_par<S>(), kRc2V, true, F>>();
-    grid_cap_of<fista_rc3v_kernel<S, 1, canon_par<S>(), kRc2V, true, F>>();
     if (!F) grid_cap_of<fista_rc_persistent<S, canon_par<S>()>>();
   } else {
     grid_cap_of<fista_rc_kernel<S, 2, false, -1, F>>();
     grid_cap_of<fista_rc2v_kernel<S, 1, -1, kRc2V, true, F>>();
-    grid_cap_of<fista_rc3v_kernel<S, 1, -1, kRc2V, true, F>>();
     if (!F) grid_cap_of<fista_rc_persistent<S, -1>>();
   }
   grid_cap_of<fista_rc_kernel<S, 2, true, -1, F>>();
@@ -1401,30 +1187,6 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
     case 7: return launch_rc2_s<3, true>(a, o, st);
     case 8: return launch_rc2_s<4, false>(a, o, st);
     case 9: return launch_rc2_s<4, true>(a, o, st);
-    default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
-  }
-}
-
-void fista_rc_iter3(const OpView& op, const IterBufs& ib, double* x_next2, double* x_next3, uint64_t n,
-                    cudaStream_t st, bool fma) {
-  RcArgs a;
-  a.n = (int64_t)op.n;
-  a.lo = 0;
-  a.hi = (int64_t)n;
-  a.right = op.right;
-  a.sigma = op.sigma;
-  a.b = ib;
-  a.peers = PeerViews();
-  const Rc3Out o{ib.x_next, x_next2, x_next3};
-  switch (op.right.count * 2 + (fma ? 1 : 0)) {
-    case 2: return launch_rc3_s<1, false>(a, o, st);
-    case 3: return launch_rc3_s<1, true>(a, o, st);
-    case 4: return launch_rc3_s<2, false>(a, o, st);
-    case 5: return launch_rc3_s<2, true>(a, o, st);
-    case 6: return launch_rc3_s<3, false>(a, o, st);
-    case 7: return launch_rc3_s<3, true>(a, o, st);
-    case 8: return launch_rc3_s<4, false>(a, o, st);
-    case 9: return launch_rc3_s<4, true>(a, o, st);
     default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
   }
 }

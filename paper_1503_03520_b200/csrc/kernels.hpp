@@ -146,8 +146,6 @@ struct FistaDev {
   // (l1, nnz, mism) of x_{k+2}
   double scal8[8];
   int pair_pending;  // shards: the last kernel ran two iterations (finalize: lagged2)
-  // three-iteration kernel: the same four sums for x_{k+1}, x_{k+2}, x_{k+3}
-  double scal12[12];
 };
 
 struct FistaBufs {
@@ -225,11 +223,6 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 // 24n bytes per iteration (k_iter_rc.cu fista_rc2_kernel); one device
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
                     cudaStream_t st, const PeerViews& peers = PeerViews(), bool fma = false);
-// THREE iterations j+1 .. j+3 per launch (one device): x_{j+1} into ib.x_next,
-// x_{j+2}, x_{j+3} into x_next2, x_next3 (global-index views); lagged record of
-// three iterations (fista_finalize_lagged3)
-void fista_rc_iter3(const OpView& op, const IterBufs& ib, double* x_next2, double* x_next3, uint64_t n,
-                    cudaStream_t st, bool fma = false);
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op, bool fma = false);
 // general shards: prox / momentum on the own column slice from the reduced g

@@ -45,13 +45,8 @@ struct l1b_session {
   bool general = false;    // general row-block shard: reduce-scatter g, all-gather x (distributed.py)
   double *g_full = nullptr, *x_full = nullptr;  // n_pad = world * col_slice entries each
   uint64_t n_pad = 0, col_off = 0;              // own slice: [col_off, col_off + nx)
-  double* X[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  // x rotation period: 4 for the recomputing kernels (two-iteration launches),
-  // 5 on one device with three-iteration launches (a launch reads x_{j-1}, x_j
-  // and writes x_{j+1} .. x_{j+3}; a stop decided for any recorded iteration
-  // still finds its iterate)
-  int nbuf = 3;
-  bool triples = false;  // one device: three iterations per launch (fista_rc3v_kernel)
+  double* X[4] = {nullptr, nullptr, nullptr, nullptr};
+  int nbuf = 3;  // x rotation period: 4 for the recomputing kernels (two-iteration launches)
   double* R[3] = {nullptr, nullptr, nullptr};
   uint64_t xh = 0, rh = 0;  // single-kernel windows: x / r halo widths (shards: H / 2H)
   uint64_t nx = 0, nr = 0, halo = 0;  // own columns / own rows / window overhang
@@ -120,13 +115,8 @@ struct l1b_session {
 
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
-    fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % (uint64_t)nbuf] + (int64_t)xh - lo, (uint64_t)lo,
+    fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
                    shard ? v.row_end : v.n, stream, peers(j), fma());
-  }
-
-  void iterate3(uint64_t j, cudaStream_t stream) const {  // one device: launches j, j+1, j+2
-    const uint64_t P = (uint64_t)nbuf;
-    fista_rc_iter3(*v.op, iter_bufs(j), X[(j + 2) % P], X[(j + 3) % P], v.n, stream, fma());
   }
 
   void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
@@ -182,8 +172,6 @@ struct l1b_session {
 namespace {
 
 bool rc2_enabled();  // L1B_RC2 switch (below)
-bool rc3_enabled();  // L1B_RC3 switch (below)
-bool uses_loop_n(uint64_t n);
 
 uint64_t sample_capacity(uint64_t max_iters) {
   uint64_t c = std::min<uint64_t>(max_iters, 1000) + 2;
@@ -244,8 +232,6 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
     s->rh = s->shard && !s->recompute ? 2 * H : 0;
     s->halo = s->xh;
     s->nbuf = s->recompute ? 4 : 3;
-    s->triples = s->recompute && !s->shard && rc2_enabled() && rc3_enabled() && !uses_loop_n(v.n);
-    if (s->triples) s->nbuf = 5;
     for (int q = 0; q < s->nbuf; ++q) {
       if (s->shard && s->recompute) {  // plain allocations: exportable to peer processes (IPC)
         double* p = nullptr;
@@ -384,25 +370,11 @@ bool rc2_enabled() {
   return on != 0;
 }
 
-// Large single-device instances run three iterations per launch (56n bytes
-// per three iterations, 18.7n per iteration); L1B_RC3=0 keeps two.
-bool rc3_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("L1B_RC3");
-    on = !(e && e[0] == '0');
-  }
-  return on != 0;
-}
-
-// `iters` single-device recomputing iterations as three-iteration launches
-// (two-iteration ones without triples; a two- or one-iteration launch for the
-// remainder); returns false when the session is not one
+// `iters` single-device recomputing iterations as two-iteration launches (+ one
+// single launch for an odd count); returns false when the session is not one
 bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
   if (!(s->recompute && !s->shard && rc2_enabled())) return false;
   uint64_t i = 0;
-  if (s->triples)
-    for (; i + 3 <= iters; i += 3) s->iterate3(s->launched + i, st);
   for (; i + 2 <= iters; i += 2) s->iterate2(s->launched + i, st);
   if (i < iters) s->iterate(s->launched + i, st);
   return true;
@@ -411,8 +383,9 @@ bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
 // small single-device recomputing sessions step through fista_rc_loop (one
 // launch per chunk; also for single iterations, so that every iteration of a
 // session reduces its sums in the same order)
-bool uses_loop_n(uint64_t n) { return n <= kPersistMaxN && persist_enabled(); }
-bool uses_loop(const l1b_session* s) { return s->recompute && !s->shard && uses_loop_n(s->v.n); }
+bool uses_loop(const l1b_session* s) {
+  return s->recompute && !s->shard && s->v.n <= kPersistMaxN && persist_enabled();
+}
 
 void session_step(l1b_session* s, uint64_t iters) {
   const FistaBufs b = s->bufs();
@@ -475,8 +448,8 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   if (uses_loop(s))
     sum->path = L1B_RAN_FISTA_LOOP | L1B_RAN_FISTA_RECOMPUTE;
   else if (s->recompute)
-    sum->path = (rc2_enabled() ? L1B_RAN_FISTA_TWO_ITER : 0u) | (s->triples ? L1B_RAN_FISTA_THREE_ITER : 0u) |
-                L1B_RAN_FISTA_RECOMPUTE | (s->fma() ? L1B_RAN_FMA : 0u);
+    sum->path = (rc2_enabled() ? L1B_RAN_FISTA_TWO_ITER : 0u) | L1B_RAN_FISTA_RECOMPUTE |
+                (s->fma() ? L1B_RAN_FMA : 0u);
   else
     sum->path = s->single ? L1B_RAN_FISTA_STORED : s->fused ? L1B_RAN_FISTA_MF_PAIR : L1B_RAN_FISTA_SPARSE;
   sum->status = status;
@@ -569,7 +542,7 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
     out->own = s->nx;
     out->halo = s->halo;
     out->single = s->single ? 1 : 0;
-    for (int q = 0; q < 4; ++q) out->x_bufs[q] = s->X[q];  // (shards rotate through 4)
+    for (int q = 0; q < 4; ++q) out->x_bufs[q] = s->X[q];
     for (int q = 0; q < 3; ++q) out->r_bufs[q] = s->R[q];
     out->x_nbufs = s->nbuf;
     out->x_halo = s->xh;
@@ -592,7 +565,6 @@ int l1b_session_kernel_mode(l1b_session* s, int* mode) {
     *mode = s->general ? L1B_KMODE_GENERAL_SHARD
             : !s->single ? (s->fused ? L1B_KMODE_MATRIX_FREE_PAIR : L1B_KMODE_SPARSE)
             : !s->recompute ? L1B_KMODE_STORED_RESIDUAL
-            : s->triples ? L1B_KMODE_RECOMPUTE_THREE
             : (!s->shard && rc2_enabled()) ? L1B_KMODE_RECOMPUTE_TWO
                                            : L1B_KMODE_RECOMPUTE;
   });
@@ -754,34 +726,25 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
       ms_out[1] = k2;
       return;
     }
-    // three- / two-iteration launches, timed each -- where session_step uses them too
+    // two-iteration launches, timed each -- where session_step uses them too
     if (s->recompute && !s->shard && rc2_enabled()) {
       uint64_t i = 0;
-      std::vector<uint64_t> starts;
-      while (i < iters) {
-        starts.push_back(i);
+      for (; i < iters; i += 2) {
         L1B_CUDA(cudaEventRecord(ev[3 * i], st));
-        uint64_t step = 1;
-        if (s->triples && i + 3 <= iters) {
-          s->iterate3(s->launched + i, st);
-          step = 3;
-        } else if (i + 2 <= iters) {
+        if (i + 2 <= iters)
           s->iterate2(s->launched + i, st);
-          step = 2;
-        } else {
+        else
           s->iterate(s->launched + i, st);
-        }
         L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
         L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
-        i += step;
       }
       s->launched += iters;
       L1B_CUDA(cudaStreamSynchronize(st));
       double k1 = 0.0, k2 = 0.0;  // k2: the empty second slot, as in single-kernel mode
-      for (uint64_t q : starts) {
+      for (i = 0; i < iters; i += 2) {
         float a = 0.f, c = 0.f;
-        L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * q], ev[3 * q + 1]));
-        L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * q + 1], ev[3 * q + 2]));
+        L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+        L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));
         k1 += a;
         k2 += c;
       }
