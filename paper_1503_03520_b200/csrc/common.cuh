@@ -68,6 +68,7 @@ struct StageTab {
   int offset[kMaxStages];
   double c[kMaxStages];  // cos(theta) from the host libm (linops.cpp:84-85)
   double s[kMaxStages];
+  double t[kMaxStages];  // tan(theta / 2) = s / (1 + c): the lifting form of the contracted kernels
 };
 
 struct OpView {
@@ -117,14 +118,23 @@ __device__ __forceinline__ void rot(double& vi, double& vj, double c, double s, 
     rotate_pair(vi, vj, c, s, transposed);
     return;
   }
-  const double a = vi, b = vj;
-  if (transposed) {
-    vi = __fma_rn(c, a, s * b);
-    vj = __fma_rn(c, b, -(s * a));
+  // contracted arithmetic: the rotation as three shears (lifting,
+  // R(theta) = L(-t) U(s) L(-t), t = tan(theta / 2)): three dependent FMAs
+  // instead of two products and two FMAs.  `c` carries t here (the callers
+  // pass StageTab::t in this mode).
+  const double t = c;
+  double a = vi, b = vj;
+  if (transposed) {  // R(-theta)
+    a = __fma_rn(t, b, a);
+    b = __fma_rn(-s, a, b);
+    a = __fma_rn(t, b, a);
   } else {
-    vi = __fma_rn(c, a, -(s * b));
-    vj = __fma_rn(s, a, c * b);
+    a = __fma_rn(-t, b, a);
+    b = __fma_rn(s, a, b);
+    a = __fma_rn(-t, b, a);
   }
+  vi = a;
+  vj = b;
 }
 // a * b - c
 template <bool F>

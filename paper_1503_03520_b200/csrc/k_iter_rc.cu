@@ -158,7 +158,7 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
   for (int k = 0; k < S; ++k) {
     const int s = TR ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
     const int o = tab.offset[s];
-    const double c = tab.c[s], sn = tab.s[s];
+    const double c = F ? tab.t[s] : tab.c[s], sn = tab.s[s];  // (F: the lifting form)
     const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
     if (par == 0) {
       const bool p0 = INTERIOR || (e0 >= o && e0 + 1 < n);
@@ -370,7 +370,7 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
   for (int k = 0; k < S; ++k) {
     const int s = TR ? k : S - 1 - k;
     const int o = tab.offset[s];
-    const double c = tab.c[s], sn = tab.s[s];
+    const double c = F ? tab.t[s] : tab.c[s], sn = tab.s[s];  // (F: the lifting form)
     const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
     if (par == 0) {
 #pragma unroll
