@@ -181,8 +181,8 @@ def roofline(path, t, info, peak, peak_src):
             traffic = None
     long_ms = (t["k1_ms_long"] * ipl if dom[3] != "k2" else t["k2_ms_long"])
     if path == "matrix_free" and t.get("kmode") == 4:
-        limiter = ("HBM streaming: ncu shows DRAM 6.42 GB per launch (1.00x algorithmic), the FP64 pipe 59.5 % "
-                   "busy (profiles/r2_ncu_full_fista_rc2v_fma.txt)" if t.get("arith") == "fma" else
+        limiter = ("HBM streaming: ncu shows DRAM 6.42 GB per launch (1.00x algorithmic), the FP64 pipe 52.9 % "
+                   "busy with the lifting rotations (profiles/r2_ncu_full_fista_rc2v_lift.txt)" if t.get("arith") == "fma" else
                    "FP64 issue (separately rounded a*b+c): ncu shows the FP64 pipe at 76.5 % of peak and DRAM "
                    "at ~71 % (profiles/r1_ncu_full_fista_rc2v.txt)")
     else:
