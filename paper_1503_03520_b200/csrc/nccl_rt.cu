@@ -52,6 +52,7 @@ const NcclApi& nccl() {
       bind(h, "ncclGroupStart", api.GroupStart);
       bind(h, "ncclGroupEnd", api.GroupEnd);
       bind(h, "ncclGetErrorString", api.GetErrorString);
+      bind(h, "ncclCommGetAsyncError", api.CommGetAsyncError);
       api.GetVersion(&api.version);
     } catch (const std::exception& e) {
       err = e.what();
@@ -65,6 +66,15 @@ void nccl_check(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return;
   const NcclApi& n = nccl();
   throw NcclError(std::string(what) + ": " + n.GetErrorString(r));
+}
+
+void nccl_check_async(ncclComm_t comm) {
+  if (!comm) return;
+  const NcclApi& n = nccl();
+  ncclResult_t async = ncclSuccess;
+  nccl_check(n.CommGetAsyncError(comm, &async), "ncclCommGetAsyncError");
+  if (async != ncclSuccess && async != ncclInProgress)
+    throw NcclError(std::string("NCCL communicator failed: ") + n.GetErrorString(async));
 }
 
 }  // namespace l1b

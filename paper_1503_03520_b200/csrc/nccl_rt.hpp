@@ -27,6 +27,7 @@ struct NcclApi {
   decltype(&ncclGroupStart) GroupStart;
   decltype(&ncclGroupEnd) GroupEnd;
   decltype(&ncclGetErrorString) GetErrorString;
+  decltype(&ncclCommGetAsyncError) CommGetAsyncError;
   int version = 0;
   std::string path;
 };
@@ -34,6 +35,9 @@ struct NcclApi {
 // the process's NCCL (throws NcclError when none can be loaded)
 const NcclApi& nccl();
 void nccl_check(ncclResult_t r, const char* what);
+// a communicator's asynchronous error (a failed peer, a network error), polled
+// between launches of the native driver: throws NcclError when set
+void nccl_check_async(ncclComm_t comm);
 #define L1B_NCCL(call) ::l1b::nccl_check((call), #call)
 
 }  // namespace l1b

@@ -1100,6 +1100,7 @@ int l1b_session_nccl_steps(l1b_session* s, uint64_t launches, int use_graph, dou
       }
     }
     for (; i < launches; ++i) native_launch(s);
+    nccl_check_async(s->comm);  // a peer's failure surfaces here, not as a hang later
   });
 }
 
@@ -1109,6 +1110,7 @@ int l1b_session_nccl_finish(l1b_session* s) {
     L1B_CUDA(cudaSetDevice(s->v.device));
     s->iterate(s->launched, s->v.stream, true);  // flush: ||r||^2 of the last iterate
     native_reduce_finalize(s);
+    nccl_check_async(s->comm);
   });
 }
 
