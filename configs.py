@@ -151,7 +151,7 @@ def run_cpu(name, c):
 C5 = dict(n=1 << 32, stages=4, q=0, s_divisor=10000, seed=4, theta=THETA)
 
 
-def run_c5(ranks, iters, world=8):
+def run_c5(ranks, iters, world=8, arith="fma"):
     """Per-rank shards of C5 on the one GPU (see the module docstring)."""
     import gc
 
@@ -162,11 +162,11 @@ def run_c5(ranks, iters, world=8):
 
     out = {"config": "c5", "desc": "FISTA, n=2^32 x m=2^33, 4 stages, q=0, s=n/10000, seed 4; "
                                    f"rank shards of the {world}-way row split, one at a time on one GPU",
-           "world": world, "iterations_timed": iters, "ranks": []}
+           "world": world, "iterations_timed": iters, "arith": arith, "ranks": []}
     for r in ranks:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sh = CudaShard(C5, r, world, 0, l1bench.SolverConfig(max_iters=iters + 8, op="matrix_free"))
+        sh = CudaShard(C5, r, world, 0, l1bench.SolverConfig(max_iters=iters + 8, op="matrix_free", arith=arith))
         torch.cuda.synchronize()
         gen_s = time.perf_counter() - t0
         assert sh.single and sh.pairs, "C5 shards run the two-iteration kernel"
