@@ -124,13 +124,23 @@ struct TmaLayout {
   static constexpr size_t x_bytes = kTileX * 8;
   static constexpr size_t stage_bytes = vals_bytes + idx_bytes + ptr_bytes + NV * vec_bytes + x_bytes;
   static constexpr size_t prod_off = kStages * stage_bytes;
-  static constexpr size_t prod_bytes = r16((kTileNnz + kTileNnz / 16 + 2) * 8);
+  static constexpr size_t prod_bytes = r16((size_t)(kThreads / 32) * (256 + 256 / 16 + 2) * 8);
   static constexpr size_t bars_off = prod_off + prod_bytes;
-  static constexpr size_t total = bars_off + kStages * 8;
+  static constexpr size_t total = bars_off + 2 * kStages * 8;  // full + empty barriers
 };
 
+// Warp-specialised: warps 0-7 consume, warp 8 (one lane) produces.  Consumer
+// warp w owns lines [32w, 32w + 32) of every tile, and their nonzeros are one
+// contiguous range, so the warp computes exactly the products its own lines
+// sum: a __syncwarp separates the two phases, no block barrier per tile.  A
+// slot is handed back to the producer through its "empty" mbarrier (one
+// arrival per consumer warp); "full" completes on the TMA bytes.
+constexpr int kSpmvThreads = kThreads + 32;
+constexpr int kWarpProd = 256;                              // products per warp chunk
+constexpr int kWarpProdPad = kWarpProd + kWarpProd / 16 + 2;  // + the bank-conflict padding
+
 template <typename PtrT, class Epi>
-__global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const PtrT* __restrict__ ptr,
+__global__ void __launch_bounds__(kSpmvThreads, L1B_SPMV_MINB) spmv_tma_kernel(const PtrT* __restrict__ ptr,
                                                                const uint32_t* __restrict__ idx,
                                                                const double* __restrict__ val,
                                                                const double* __restrict__ x,
@@ -142,136 +152,159 @@ __global__ void __launch_bounds__(kThreads, L1B_SPMV_MINB) spmv_tma_kernel(const
   using L = TmaLayout<PtrT, Epi::kVec>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t x_lo[kStages];  // first staged x index of each slot (~0: not staged)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bars_off);
+  uint64_t* empty = full + kStages;
   double* prod = reinterpret_cast<double*>(smem + L::prod_off);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  constexpr int kConsumers = kThreads / 32;
   const uint64_t ntiles = (nlines + kTileLines - 1) / kTileLines;
   const uint64_t mine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   constexpr int E = 16 / sizeof(PtrT);
 
-  uint64_t pol = 0;
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
     fence_mbar_init();
-    pol = l2_evict_first_policy();
   }
   __syncthreads();
 
-  // producer: stream tile #k of this CTA into its ring slot
-  auto issue = [&](uint64_t k, PtrT p0, PtrT p1) {
-    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
-    const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
-    unsigned char* base = smem + (k % kStages) * L::stage_bytes;
-    double* s_val = reinterpret_cast<double*>(base);
-    uint32_t* s_idx = reinterpret_cast<uint32_t*>(base + L::vals_bytes);
-    PtrT* s_ptr = reinterpret_cast<PtrT*>(base + L::vals_bytes + L::idx_bytes);
-    double* s_vec = reinterpret_cast<double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
-    const uint32_t ptr_b = (uint32_t)(((nl + 1 + E - 1) / E) * 16);
-    const PtrT va = p0 & ~(PtrT)1, vb = (p1 + 1) & ~(PtrT)1;
-    const PtrT ia = p0 & ~(PtrT)3, ib = (p1 + 3) & ~(PtrT)3;
-    const uint32_t val_b = (uint32_t)(vb - va) * 8u, idx_b = (uint32_t)(ib - ia) * 4u;
-    const uint32_t nv = vec_tma ? (uint32_t)(nl & ~1ull) : 0u;
-    // x[lo .. hi] for this tile's gathers (16-byte aligned superset) when it fits
-    uint32_t x_b = 0;
-    uint64_t xl = ~0ull;
-    if (tile_rng) {
-      const uint64_t tix = blockIdx.x + k * gridDim.x;
-      const uint64_t lo = tile_rng[2 * tix] & ~1ull, hi = tile_rng[2 * tix + 1];
-      const uint64_t cnt = (hi - lo + 2) & ~1ull;  // even: 16-byte bulk copies
-      if (hi >= lo && cnt <= (uint64_t)kTileX && lo + cnt <= x_len) {  // never past x's end
-        xl = lo;
-        x_b = (uint32_t)(cnt * 8);
+  if (warp == kConsumers) {
+    // ---- producer: stream tile k of this CTA into slot k % kStages ---------
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      PtrT b0 = 0, b1 = 0;  // row-pointer bounds of the next tile (prefetched)
+      uint32_t g0 = 1, g1 = 0;  // its index range (tile_rng)
+      auto prefetch = [&](uint64_t k) {
+        const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+        const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
+        b0 = __ldg(ptr + r0);
+        b1 = __ldg(ptr + r0 + nl);
+        if (tile_rng) {
+          const uint64_t tix = blockIdx.x + k * gridDim.x;
+          g0 = __ldg(tile_rng + 2 * tix);
+          g1 = __ldg(tile_rng + 2 * tix + 1);
+        }
+      };
+      if (mine) prefetch(0);
+      for (uint64_t k = 0; k < mine; ++k) {
+        const int slot = (int)(k % kStages);
+        if (k >= (uint64_t)kStages) {
+          mbar_wait(&empty[slot], (uint32_t)(((k / kStages) - 1) & 1));  // tile k - kStages consumed
+          fence_proxy_async();  // the consumers' generic reads before the bulk writes
+        }
+        const PtrT p0 = b0, p1 = b1;
+        const uint32_t lo_i = g0, hi_i = g1;
+        const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+        const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
+        if (k + 1 < mine) prefetch(k + 1);
+        unsigned char* base = smem + slot * L::stage_bytes;
+        double* s_val = reinterpret_cast<double*>(base);
+        uint32_t* s_idx = reinterpret_cast<uint32_t*>(base + L::vals_bytes);
+        PtrT* s_ptr = reinterpret_cast<PtrT*>(base + L::vals_bytes + L::idx_bytes);
+        double* s_vec = reinterpret_cast<double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
+        const uint32_t ptr_b = (uint32_t)(((nl + 1 + E - 1) / E) * 16);
+        const PtrT va = p0 & ~(PtrT)1, vb = (p1 + 1) & ~(PtrT)1;
+        const PtrT ia = p0 & ~(PtrT)3, ib = (p1 + 3) & ~(PtrT)3;
+        const uint32_t val_b = (uint32_t)(vb - va) * 8u, idx_b = (uint32_t)(ib - ia) * 4u;
+        const uint32_t nv = vec_tma ? (uint32_t)(nl & ~1ull) : 0u;
+        uint32_t x_b = 0;
+        uint64_t xl = ~0ull;
+        if (tile_rng) {  // x[lo .. hi] for this tile's gathers, when it fits and stays inside x
+          const uint64_t lo = lo_i & ~1ull, hi = hi_i;
+          const uint64_t cnt = (hi - lo + 2) & ~1ull;
+          if (hi >= lo && cnt <= (uint64_t)kTileX && lo + cnt <= x_len) {
+            xl = lo;
+            x_b = (uint32_t)(cnt * 8);
+          }
+        }
+        x_lo[slot] = xl;
+        mbar_arrive_expect_tx(&full[slot], ptr_b + val_b + idx_b + Epi::kVec * nv * 8u + x_b);
+        bulk_g2s(s_ptr, ptr + r0, ptr_b, &full[slot]);
+        if (val_b) bulk_g2s_evict_first(s_val, val + va, val_b, &full[slot], pol);
+        if (idx_b) bulk_g2s_evict_first(s_idx, idx + ia, idx_b, &full[slot], pol);
+        if (nv) {
+#pragma unroll
+          for (int v = 0; v < Epi::kVec; ++v)
+            bulk_g2s(s_vec + v * kTileLines, epi.vec(v) + r0, nv * 8u, &full[slot]);
+        }
+        if (x_b) bulk_g2s(s_vec + Epi::kVec * (L::vec_bytes / 8), x + xl, x_b, &full[slot]);
       }
     }
-    x_lo[k % kStages] = xl;
-    mbar_arrive_expect_tx(&bars[k % kStages], ptr_b + val_b + idx_b + Epi::kVec * nv * 8u + x_b);
-    if (x_b) bulk_g2s(s_vec + Epi::kVec * (L::vec_bytes / 8), x + xl, x_b, &bars[k % kStages]);
-    bulk_g2s(s_ptr, ptr + r0, ptr_b, &bars[k % kStages]);
-    if (val_b) bulk_g2s_evict_first(s_val, val + va, val_b, &bars[k % kStages], pol);
-    if (idx_b) bulk_g2s_evict_first(s_idx, idx + ia, idx_b, &bars[k % kStages], pol);
-    if (nv) {
+  } else {
+    // ---- consumers ---------------------------------------------------------
+    const int lw0 = warp * 32;
+    for (uint64_t k = 0; k < mine; ++k) {
+      const int slot = (int)(k % kStages);
+      const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
+      const int nl = (int)min((uint64_t)kTileLines, nlines - r0);
+      unsigned char* base = smem + slot * L::stage_bytes;
+      const double* s_val = reinterpret_cast<const double*>(base);
+      const uint32_t* s_idx = reinterpret_cast<const uint32_t*>(base + L::vals_bytes);
+      const PtrT* s_ptr = reinterpret_cast<const PtrT*>(base + L::vals_bytes + L::idx_bytes);
+      const double* s_vec =
+          reinterpret_cast<const double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
+      mbar_wait(&full[slot], (uint32_t)((k / kStages) & 1));
+      if (lw0 < nl) {
+        const PtrT p0 = s_ptr[0];
+        const PtrT va = p0 & ~(PtrT)1, ia = p0 & ~(PtrT)3;
+        (void)p0;
+        const uint64_t xl = x_lo[slot];
+        const double* s_x = s_vec + Epi::kVec * (L::vec_bytes / 8) - (xl == ~0ull ? 0 : xl);
+        const PtrT q_lo = s_ptr[lw0], q_hi = s_ptr[min(lw0 + 32, nl)];
+        const int line = lw0 + lane;
+        const PtrT la = line < nl ? s_ptr[line] : q_hi, le = line < nl ? s_ptr[line + 1] : q_hi;
+        double* wp = prod + warp * kWarpProdPad;  // this warp's product region (no other warp touches it)
+        double sum = 0.0;
+        // the warp's products in chunks of kWarpProd: gathers, then every lane
+        // adds its line's share in ascending index order (the same order as one
+        // pass over the whole line)
+        for (PtrT c0 = q_lo; c0 < q_hi; c0 += kWarpProd) {
+          const PtrT c1 = min((PtrT)(c0 + kWarpProd), q_hi);
+          for (PtrT q0 = c0 + lane; q0 < c1; q0 += 32 * kUnroll) {
+            double vv[kUnroll];
+            uint32_t ii[kUnroll];
 #pragma unroll
-      for (int v = 0; v < Epi::kVec; ++v)
-        bulk_g2s(s_vec + v * kTileLines, epi.vec(v) + r0, nv * 8u, &bars[k % kStages]);
-    }
-  };
-  auto bounds = [&](uint64_t k, PtrT* p0, PtrT* p1) {
-    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
-    const uint64_t nl = min((uint64_t)kTileLines, nlines - r0);
-    *p0 = __ldg(ptr + r0);
-    *p1 = __ldg(ptr + r0 + nl);
-  };
-
-  PtrT nx0 = 0, nx1 = 0;  // row-pointer bounds of the next tile to issue (prefetched)
-  if (t == 0) {
-    for (uint64_t k = 0; k + 1 < (uint64_t)kStages && k < mine; ++k) {
-      PtrT a, b;
-      bounds(k, &a, &b);
-      issue(k, a, b);
-    }
-    if (kStages - 1 < mine) bounds(kStages - 1, &nx0, &nx1);
-  }
-
-  for (uint64_t k = 0; k < mine; ++k) {
-    if (t == 0 && k + kStages - 1 < mine) {
-      fence_proxy_async();  // the slot was last read by generic loads in iteration k-1
-      issue(k + kStages - 1, nx0, nx1);
-      if (k + kStages < mine) bounds(k + kStages, &nx0, &nx1);
-    }
-    const uint64_t r0 = (blockIdx.x + k * gridDim.x) * (uint64_t)kTileLines;
-    const int nl = (int)min((uint64_t)kTileLines, nlines - r0);
-    unsigned char* base = smem + (k % kStages) * L::stage_bytes;
-    const double* s_val = reinterpret_cast<const double*>(base);
-    const uint32_t* s_idx = reinterpret_cast<const uint32_t*>(base + L::vals_bytes);
-    const PtrT* s_ptr = reinterpret_cast<const PtrT*>(base + L::vals_bytes + L::idx_bytes);
-    const double* s_vec =
-        reinterpret_cast<const double*>(base + L::vals_bytes + L::idx_bytes + L::ptr_bytes);
-    mbar_wait(&bars[k % kStages], (uint32_t)((k / kStages) & 1));
-    const PtrT p0 = s_ptr[0], p1 = s_ptr[nl];
-    const PtrT va = p0 & ~(PtrT)1, ia = p0 & ~(PtrT)3;
-    const uint64_t xl = x_lo[k % kStages];
-    const double* s_x = s_vec + Epi::kVec * (L::vec_bytes / 8) - (xl == ~0ull ? 0 : xl);
-    // products: 8 independent gathers per thread
-    for (PtrT q0 = p0 + t; q0 < p1; q0 += kThreads * kUnroll) {
-      double vv[kUnroll];
-      uint32_t ii[kUnroll];
+            for (int u = 0; u < kUnroll; ++u) {
+              const PtrT q = q0 + 32 * u;
+              if (q < c1) {
+                vv[u] = s_val[q - va];
+                ii[u] = s_idx[q - ia];
+              }
+            }
+            if (xl != ~0ull) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const PtrT q = q0 + kThreads * u;
-        if (q < p1) {
-          vv[u] = s_val[q - va];
-          ii[u] = s_idx[q - ia];
+              for (int u = 0; u < kUnroll; ++u) {
+                const PtrT q = q0 + 32 * u;
+                if (q < c1) wp[pad((int)(q - c0))] = vv[u] * s_x[ii[u]];
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                const PtrT q = q0 + 32 * u;
+                if (q < c1) wp[pad((int)(q - c0))] = vv[u] * __ldg(x + ii[u]);
+              }
+            }
+          }
+          __syncwarp();
+          const PtrT a = max(la, c0), e = min(le, c1);
+          for (PtrT q = a; q < e; ++q) sum += wp[pad((int)(q - c0))];
+          __syncwarp();  // (the next chunk reuses the region)
+        }
+        if (line < nl) {
+          double pv[Epi::kVec > 0 ? Epi::kVec : 1];
+          if (vec_tma && line < (nl & ~1)) {
+#pragma unroll
+            for (int v = 0; v < Epi::kVec; ++v) pv[v] = s_vec[v * kTileLines + line];
+          } else {
+            load_vecs(epi, r0 + line, pv);
+          }
+          epi.line(r0 + line, sum, pv);
         }
       }
-      if (xl != ~0ull) {
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const PtrT q = q0 + kThreads * u;
-          if (q < p1) prod[pad((int)(q - p0))] = vv[u] * s_x[ii[u]];
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const PtrT q = q0 + kThreads * u;
-          if (q < p1) prod[pad((int)(q - p0))] = vv[u] * __ldg(x + ii[u]);
-        }
-      }
+      if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    __syncthreads();
-    if (t < nl) {
-      const PtrT a = s_ptr[t], e = s_ptr[t + 1];
-      double sum = 0.0;
-      for (PtrT q = a; q < e; ++q) sum += prod[pad((int)(q - p0))];
-      double pv[Epi::kVec > 0 ? Epi::kVec : 1];
-      if (vec_tma && t < (nl & ~1)) {
-#pragma unroll
-        for (int v = 0; v < Epi::kVec; ++v) pv[v] = s_vec[v * kTileLines + t];
-      } else {
-        load_vecs(epi, r0 + t, pv);
-      }
-      epi.line(r0 + t, sum, pv);
-    }
-    __syncthreads();
   }
   epi.finish();
 }
@@ -289,7 +322,7 @@ inline void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::total));
       int per_sm = 0;
       L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_tma_kernel<PtrT, Epi>,
-                                                            kThreads, L::total));
+                                                            kSpmvThreads, L::total));
       grid_cap = std::max(1, per_sm) * sm_count();
     }
     int vec_tma = kVecTma;
@@ -299,7 +332,7 @@ inline void launch_p(const Csr& M, const double* x, const Epi& epi, cudaStream_t
     const uint32_t* rng = reinterpret_cast<uintptr_t>(x) % 16 ? nullptr : M.tile_rng;
     const uint64_t tiles = (M.lines + kTileLines - 1) / kTileLines;
     const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)grid_cap));
-    spmv_tma_kernel<PtrT, Epi><<<grid, kThreads, L::total, st>>>(
+    spmv_tma_kernel<PtrT, Epi><<<grid, kSpmvThreads, L::total, st>>>(
         (const PtrT*)M.ptr, M.idx, M.val, x, M.lines, epi, vec_tma, rng, M.x_len);
     L1B_LAUNCHED();
     return;
