@@ -255,7 +255,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=C4["n"],
+    ap.add_argument("--n", "--columns", dest="n", type=int, default=C4["n"],
                     help="global n, row-sharded across ranks when N > 1 (default C4: 2^27)")
     ap.add_argument("--arith", default="fma", choices=["fma", "exact"],
                     help="headline arithmetic of the matrix-free FISTA kernels")
