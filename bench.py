@@ -423,7 +423,8 @@ def e2e(inst, steps, device, serving=False):
         resident = l1bench.ProblemInstance.from_host(m, n, stages, g["sigma"], g["b"], tau, g["xs"].support,
                                                      g["xs"].values, device=device)
     times = []
-    for rep in range(4):  # pass 0 warms up (first-use pool growth / allocations); 1-3 are timed
+    passes = 6 if steps <= 100 else 4  # short passes are noisier: median of five, else of three
+    for rep in range(passes):  # pass 0 warms up (first-use pool growth / allocations); the rest are timed
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if serving:
@@ -438,7 +439,7 @@ def e2e(inst, steps, device, serving=False):
             times.append(time.perf_counter() - t0)
         del p
     del resident
-    t = sorted(times)[len(times) // 2]  # median of three
+    t = sorted(times)[len(times) // 2]  # median
     h2d = 8 * m + (0 if serving else 8 * n + 12 * len(g["xs"].support))
     d2h = 8 * n + 48 * len(tr.samples)
     return {"value": steps / t, "unit": UNIT, "steps": steps, "h2d_bytes_per_step": h2d / steps,
@@ -447,7 +448,7 @@ def e2e(inst, steps, device, serving=False):
                          if serving else
                          "H2D of sigma/b/x* from pinned host buffers (l1b_problem_create), ") +
                         "K FISTA iterations (l1b_solve, matrix-free path), D2H of x and trace; wall clock, "
-                        "median of three identical passes after one warm-up pass"}
+                        f"median of {passes - 1} identical passes after one warm-up pass"}
 
 
 if __name__ == "__main__":
