@@ -87,6 +87,11 @@ int l1b_mt_draws_after_chunk_jump(uint64_t seed, uint64_t chunk, uint64_t count,
 /* Returns s through *s_out; support (ascending) and values need capacity s. */
 int l1b_uniform_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
                                 uint32_t* support_out, double* values_out);
+/* The same on the device (k_solution.cu: Floyd's sampling from the draws
+ * alone -- first occurrences by a stable sort, chains by relaxation); the
+ * host replay when a draw the reference redraws occurs (*on_device = 0).   */
+int l1b_device_uniform_sparse_solution(int device, uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
+                                       uint32_t* support_out, double* values_out, int* on_device);
 
 /* ------------------------------------------------------------------------ */
 /* Problem = device-resident instance: operator (sweep description + CSR/CSC

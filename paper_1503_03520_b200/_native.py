@@ -113,6 +113,7 @@ SIGNATURES = [
     ("l1b_mt_draws_after_jump", C.c_int, [u64, u32, u64, P(u64)]),
     ("l1b_mt_draws_after_chunk_jump", C.c_int, [u64, u64, u64, P(u64)]),
     ("l1b_uniform_sparse_solution", C.c_int, [u64, u64, f64, u64, P(u32), P(f64)]),
+    ("l1b_device_uniform_sparse_solution", C.c_int, [C.c_int, u64, u64, f64, u64, P(u32), P(f64), P(C.c_int)]),
     ("l1b_generate", C.c_int, [C.c_int, P(GenDesc), P(ShardDesc), P(vp)]),
     ("l1b_problem_create", C.c_int, [C.c_int, P(OperatorDesc), f64, P(f64), P(u32), P(f64), u64,
                                      P(vp)]),

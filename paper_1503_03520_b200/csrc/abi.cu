@@ -423,6 +423,26 @@ int l1b_mt_draws_after_jump(uint64_t seed, uint32_t log2_jump, uint64_t count, u
   });
 }
 
+int l1b_device_uniform_sparse_solution(int device, uint64_t n, uint64_t s, double gamma, uint64_t rng_seed,
+                                       uint32_t* support_out, double* values_out, int* on_device) {
+  return guard([&] {
+    if (s > n) throw InvalidArgument("uniform_sparse_solution: s must not exceed n");
+    if (!(gamma > 0.0)) throw InvalidArgument("uniform_sparse_solution: gamma must be positive");
+    if (s && (!support_out || !values_out)) throw InvalidArgument("null output");
+    L1B_CUDA(cudaSetDevice(device));
+    std::vector<uint32_t> sup;
+    std::vector<double> val;
+    const bool dev = device_sparse_solution(n, s, gamma, rng_seed, sup, val, nullptr);
+    if (!dev) {  // (a redraw: the sequential stream)
+      hostrng::Rng r(rng_seed);
+      hostrng::sparse_solution(n, s, gamma, r, sup, val);
+    }
+    if (on_device) *on_device = dev ? 1 : 0;
+    std::copy(sup.begin(), sup.end(), support_out);
+    std::copy(val.begin(), val.end(), values_out);
+  });
+}
+
 int l1b_mt_draws_after_chunk_jump(uint64_t seed, uint64_t chunk, uint64_t count, uint64_t* out) {
   return guard([&] {
     if (!out && count) throw InvalidArgument("null output");
@@ -515,13 +535,21 @@ void planted_solution(const l1b_gen_desc* g, uint64_t n, uint64_t job_seed, cons
   const uint64_t s = std::max<uint64_t>(1, n / g->s_divisor);
   switch (g->solution_kind) {
     case L1B_SOLUTION_UNIFORM: {
+      // on the device (k_solution.cu) like the sigma / fill streams; the host
+      // replay when a draw the reference redraws occurs
+      if (device_rng_for(n) && device_sparse_solution(n, s, g->gamma, hostrng::mix_seed(job_seed, 4), p->xs_sup,
+                                                      p->xs_val, p->stream))
+        return;
       hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
       hostrng::sparse_solution(n, s, g->gamma, r, p->xs_sup, p->xs_val);
       return;
     }
     case L1B_SOLUTION_TWO_VALUE: {
-      hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
-      hostrng::sparse_solution(n, s, 1.0, r, p->xs_sup, p->xs_val);
+      if (!(device_rng_for(n) && device_sparse_solution(n, s, 1.0, hostrng::mix_seed(job_seed, 4), p->xs_sup,
+                                                         p->xs_val, p->stream))) {
+        hostrng::Rng r(hostrng::mix_seed(job_seed, 4));
+        hostrng::sparse_solution(n, s, 1.0, r, p->xs_sup, p->xs_val);
+      }
       const size_t half = p->xs_val.size() / 2;
       for (size_t k = 0; k < p->xs_val.size(); ++k) p->xs_val[k] = k < half ? g->value_a : g->value_b;
       return;

@@ -704,14 +704,11 @@ void mt_seed_state(uint64_t seed, uint64_t* w312) { mt::seed_window(seed, w312);
 // chunk) run the recurrence directly.
 constexpr uint64_t kIdxChunk = 312 * 256;
 
-uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
-                           uint64_t* d_words, cudaStream_t st) {
+namespace {
+// the untempered words of draws [0, count) of the stream continued from
+// d_window (count a multiple of 312; d_window advanced past them)
+void mt_stream_words(uint64_t* d_window, uint64_t count, uint64_t* words, cudaStream_t st) {
   using namespace mt;
-  count = (count + 2 * MID - 1) / (2 * MID) * (2 * MID);
-  if (count == 0) return 0;
-  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
-  uint64_t* words = d_words;
-  if (!words) L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
   const uint64_t C = (count + kIdxChunk - 1) / kIdxChunk;
   if (C == 1) {
     mt_words_kernel<<<1, IDX_THREADS, 0, st>>>(d_window, count, count, words, d_window);
@@ -728,6 +725,33 @@ uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint3
     L1B_LAUNCHED();
     L1B_CUDA(cudaFreeAsync(wins, st));
   }
+}
+
+__global__ void mt_temper_raw_kernel(uint64_t* words, uint64_t count) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    words[k] = mt::temper(words[k]);
+}
+}  // namespace
+
+uint64_t mt_stream_raw(uint64_t* d_window, uint64_t count, uint64_t* d_out, cudaStream_t st) {
+  count = (count + 2 * mt::MID - 1) / (2 * mt::MID) * (2 * mt::MID);
+  if (count == 0) return 0;
+  mt_stream_words(d_window, count, d_out, st);
+  mt_temper_raw_kernel<<<grid_for(count), kThreads, 0, st>>>(d_out, count);
+  L1B_LAUNCHED();
+  return count;
+}
+
+uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
+                           uint64_t* d_words, cudaStream_t st) {
+  using namespace mt;
+  count = (count + 2 * MID - 1) / (2 * MID) * (2 * MID);
+  if (count == 0) return 0;
+  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  uint64_t* words = d_words;
+  if (!words) L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
+  mt_stream_words(d_window, count, words, st);
   const int grid = grid_for(count);
   if ((n & (n - 1)) == 0) mt::mt_temper_kernel<true><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);
   else mt::mt_temper_kernel<false><<<grid, kThreads, 0, st>>>(words, count, n, lim, d_out);

@@ -52,6 +52,14 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 void mt_seed_state(uint64_t seed, uint64_t* w312);
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            uint64_t* d_words, cudaStream_t st);
+// the raw 64-bit outputs of the same continued stream (count rounded up to 312)
+uint64_t mt_stream_raw(uint64_t* d_window, uint64_t count, uint64_t* d_out, cudaStream_t st);
+// ---- k_solution.cu ------------------------------------------------------------
+// uniform_sparse_solution (solution.cpp:47-75) from Rng(seed) on the device:
+// the support ascending and the values; false when a draw the reference
+// would redraw occurs (the caller replays the stream on the host).  Syncs.
+bool device_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t seed, std::vector<uint32_t>& sup,
+                            std::vector<double>& val, cudaStream_t st);
 // host: raw 64-bit outputs 2^log2_jump .. 2^log2_jump + count - 1 of
 // std::mt19937_64(seed) through the jump polynomial (log2_jump < 0: no jump)
 void host_draws_after_jump(uint64_t seed, int log2_jump, uint64_t count, uint64_t* out);

@@ -195,3 +195,31 @@ def test_alternating_spectrum_matches_reference(reference, kw):
     np.testing.assert_array_equal(dev.b, ref.b())
     np.testing.assert_array_equal(dev.x_star.support, ref.x_star()[0])
     np.testing.assert_array_equal(dev.x_star.values, ref.x_star()[1])
+
+
+@pytest.mark.parametrize("n,s,seed", [(1000, 1000, 1), (1000, 1, 2), (4096, 40, 3), (1 << 15, 327, 4),
+                                      (5000, 4000, 9), ((1 << 20) + 7, 10_000, 5), (1 << 27, 134_217, None),
+                                      (1 << 32, 429_496, None)])
+def test_device_floyd_sampling_matches_reference(oracle, n, s, seed):
+    """uniform_sparse_solution (solution.cpp:47-75) on the device against the
+    oracle's sequential Floyd sampling on the same stream: support and values
+    bit for bit (C4's and C5's own seeds and sizes included; s = n chooses all)."""
+    need_cuda()
+    from paper_1503_03520_b200 import _native as N
+
+    if seed is None:  # the generator's seed for x* of C4 / C5: mix_seed(job seed, 4)
+        seed = oracle.mix_seed(oracle.mix_seed(3 if n == 1 << 27 else 4, 0), 4)
+    sup = np.empty(s, dtype=np.uint32)
+    val = np.empty(s)
+    on_dev = ctypes.c_int()
+    N.check(N.load().l1b_device_uniform_sparse_solution(
+        0, n, s, 10.0, seed, sup.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+        val.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(on_dev)))
+    assert on_dev.value == 1
+    rng = oracle.rng(seed)
+    osup = np.empty(s, dtype=np.uint32)
+    oval = np.empty(s)
+    oracle.lib.lo_uniform_sparse_solution(n, s, 10.0, ctypes.byref(rng), osup.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                          oval.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    np.testing.assert_array_equal(sup, osup)
+    np.testing.assert_array_equal(val, oval)
