@@ -55,6 +55,10 @@ const char* l1b_last_error(void);
  * uniform_sparse_solution (solution.cpp:47-75).                             */
 uint64_t l1b_mix_seed(uint64_t seed, uint64_t salt);
 int l1b_realize_permutation(uint64_t n, uint64_t seed, uint32_t* map_out);
+/* The same on the device (k_solution.cu: the Fisher-Yates result from its
+ * draws alone -- targets sorted, value chains by pointer jumping); the host
+ * replay after a redrawn index (*on_device = 0).  n <= 2^32.               */
+int l1b_device_realize_permutation(int device, uint64_t n, uint64_t seed, uint32_t* map_out, int* on_device);
 int l1b_realize_spectrum_uniform(uint64_t n, double lo, double hi, double shift, uint64_t seed,
                                  double* sigma_out);
 /* Device realisation of the per-entry streams (Spectrum::uniform,

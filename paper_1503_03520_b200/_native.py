@@ -106,6 +106,7 @@ SIGNATURES = [
     ("l1b_launch_count", u64, []),
     ("l1b_mix_seed", u64, [u64, u64]),
     ("l1b_realize_permutation", C.c_int, [u64, u64, P(u32)]),
+    ("l1b_device_realize_permutation", C.c_int, [C.c_int, u64, u64, P(u32), P(C.c_int)]),
     ("l1b_realize_spectrum_uniform", C.c_int, [u64, f64, f64, f64, u64, P(f64)]),
     ("l1b_device_uniform_draws", C.c_int, [C.c_int, u64, u64, f64, f64, C.c_int, f64, u64, u64, u32,
                                            vp, P(f64), P(f64), P(C.c_int)]),

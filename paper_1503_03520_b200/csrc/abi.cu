@@ -443,6 +443,16 @@ int l1b_device_uniform_sparse_solution(int device, uint64_t n, uint64_t s, doubl
   });
 }
 
+int l1b_device_realize_permutation(int device, uint64_t n, uint64_t seed, uint32_t* map_out, int* on_device) {
+  return guard([&] {
+    if (!map_out && n) throw InvalidArgument("null output");
+    L1B_CUDA(cudaSetDevice(device));
+    const bool dev = device_permutation(n, seed, map_out, nullptr);
+    if (!dev) hostrng::permutation(n, seed, map_out);
+    if (on_device) *on_device = dev ? 1 : 0;
+  });
+}
+
 int l1b_mt_draws_after_chunk_jump(uint64_t seed, uint64_t chunk, uint64_t count, uint64_t* out) {
   return guard([&] {
     if (!out && count) throw InvalidArgument("null output");
@@ -843,8 +853,12 @@ std::unique_ptr<l1b_problem> generate_whole(int device, const l1b_gen_desc* g) {
     if (g->permute) {
       p1.resize(m);
       p2.resize(m);
-      pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
-      pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
+      // Fisher-Yates on the device from its draws alone (k_solution.cu); the host
+      // replay below n = 2^16 or after a redrawn index
+      const bool d1 = dev_rng && device_permutation(m, hostrng::mix_seed(job_seed, 1), p1.data(), nullptr);
+      const bool d2 = dev_rng && device_permutation(m, hostrng::mix_seed(job_seed, 2), p2.data(), nullptr);
+      if (!d1) pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 1), p1.data()); });
+      if (!d2) pool.emplace_back([&] { hostrng::permutation(m, hostrng::mix_seed(job_seed, 2), p2.data()); });
     }
     if (!d_sig) {
       sigma.resize(n);

@@ -60,6 +60,9 @@ uint64_t mt_stream_raw(uint64_t* d_window, uint64_t count, uint64_t* d_out, cuda
 // would redraw occurs (the caller replays the stream on the host).  Syncs.
 bool device_sparse_solution(uint64_t n, uint64_t s, double gamma, uint64_t seed, std::vector<uint32_t>& sup,
                             std::vector<double>& val, cudaStream_t st);
+// Permutation::realize (linops.cpp:224-239) from Rng(seed) on the device into
+// host_map (m entries); false on a draw the reference redraws.  Syncs.
+bool device_permutation(uint64_t m, uint64_t seed, uint32_t* host_map, cudaStream_t st);
 // host: raw 64-bit outputs 2^log2_jump .. 2^log2_jump + count - 1 of
 // std::mt19937_64(seed) through the jump polynomial (log2_jump < 0: no jump)
 void host_draws_after_jump(uint64_t seed, int log2_jump, uint64_t count, uint64_t* out);

@@ -223,3 +223,24 @@ def test_device_floyd_sampling_matches_reference(oracle, n, s, seed):
                                           oval.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     np.testing.assert_array_equal(sup, osup)
     np.testing.assert_array_equal(val, oval)
+
+
+@pytest.mark.parametrize("n,seed", [(2, 1), (3, 2), (17, 3), (1000, 4), (1 << 16, 5), (1_000_003, 6),
+                                    (1 << 24, 7)])
+def test_device_permutation_matches_reference(oracle, n, seed):
+    """Permutation::realize (linops.cpp:224-239, Fisher-Yates with
+    uniform_index) on the device against the oracle's sequential shuffle on the
+    same stream, bit for bit."""
+    need_cuda()
+    from paper_1503_03520_b200 import _native as N
+
+    got = np.empty(n, dtype=np.uint32)
+    on_dev = ctypes.c_int()
+    N.check(N.load().l1b_device_realize_permutation(0, n, seed, got.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                                     ctypes.byref(on_dev)))
+    assert on_dev.value == 1
+    want = np.empty(n, dtype=np.uint32)
+    inv = np.empty(n, dtype=np.uint32)
+    oracle.lib.lo_permutation_realize(n, seed, want.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                      inv.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)))
+    np.testing.assert_array_equal(got, want)
