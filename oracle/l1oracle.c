@@ -67,6 +67,23 @@ double lo_normal(lo_rng* r) {
 /* rng.hpp:32-34 */
 double lo_uniform_in(lo_rng* r, double lo, double hi) { return lo + (hi - lo) * lo_uniform_unit(r); }
 
+/* Test hook (not in the reference): lowers the rejection limit of the CD /
+ * PCDM coordinate draws by UINT64_MAX >> s, as L1B_TEST_INDEX_REJECT does in
+ * the library, so the redraw paths meet the oracle.  0 = the reference's. */
+static int g_index_reject = 0;
+void lo_set_index_reject(int s) { g_index_reject = s; }
+
+static uint64_t lo_coord_index(lo_rng* r, uint64_t n) {
+  uint64_t top = UINT64_MAX;
+  if (g_index_reject >= 1 && g_index_reject <= 63) top -= UINT64_MAX >> g_index_reject;
+  const uint64_t limit = top - top % n;
+  uint64_t x;
+  do {
+    x = lo_rng_next(r);
+  } while (x >= limit);
+  return x % n;
+}
+
 /* rng.hpp:37-45 */
 uint64_t lo_uniform_index(lo_rng* r, uint64_t n) {
   if (n == 0) abort();
@@ -806,7 +823,7 @@ lo_summary lo_cd(const lo_op* A, double tau, const double* b, const lo_cfg* cfg,
     uint64_t applied = 0;
     double col_ops = 0.0;
     for (uint64_t u = 0; u < n; ++u) {
-      const uint64_t i = lo_uniform_index(&rng, n);
+      const uint64_t i = lo_coord_index(&rng, n);
       const double li = lips[i];
       if (li == 0.0) continue;
       double gi = 0.0;
@@ -887,7 +904,7 @@ lo_summary lo_pcdm(const lo_op* A, double tau, const double* b, const lo_cfg* cf
       for (uint64_t t = 0; t < B; ++t) {
         uint64_t i;
         do {
-          i = lo_uniform_index(&rng, n);
+          i = lo_coord_index(&rng, n);
         } while (stamp[i] == cur);
         stamp[i] = cur;
         blk[t] = (uint32_t)i;

@@ -38,6 +38,7 @@ uint64_t lo_mix_seed(uint64_t seed, uint64_t salt);
 double lo_uniform_unit(lo_rng* r);
 double lo_uniform_in(lo_rng* r, double lo, double hi);
 uint64_t lo_uniform_index(lo_rng* r, uint64_t n);
+void lo_set_index_reject(int s); /* test hook: CD / PCDM redraws with probability ~2^-s */
 
 /* ---- Operator A = P1 * Gtilde * P2 * Sigma * G^T (linops.hpp:159-206) ----
  * Only paired stages (RotationStage::Kind::paired) are restated.           */

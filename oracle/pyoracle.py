@@ -203,6 +203,7 @@ class Oracle:
         L.lo_soft_threshold.restype = f64
         L.lo_cd_damping.argtypes = [u64, u64, u64]
         L.lo_cd_damping.restype = f64
+        L.lo_set_index_reject.argtypes = [C.c_int]
         L.lo_objective.argtypes = [P(LoOp), f64, P(f64), P(f64)]
         L.lo_objective.restype = f64
 
@@ -376,6 +377,11 @@ class Oracle:
 
     def newton_cg(self, inst, **kw):
         return self._run(self.lib.lo_newton_cg, inst, self.cfg(**kw))
+
+    def set_index_reject(self, s):
+        """Test hook: CD / PCDM coordinate draws redrawn with probability
+        ~2^-s (0 = the reference's limit); mirrors L1B_TEST_INDEX_REJECT."""
+        self.lib.lo_set_index_reject(int(s))
 
     def cd(self, inst, csc=None, csr=None, **kw):
         csc = csc or self.csc(inst.op)

@@ -1267,7 +1267,7 @@ void pick_pair_kernel(bool sync, const std::function<void(int, int, const void*)
 }
 
 uint64_t uniform_index(std::mt19937_64& g, uint64_t n) {  // rng.hpp:37-45
-  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  const uint64_t lim = coord_index_limit(n);
   uint64_t x;
   do {
     x = g();
@@ -1350,7 +1350,13 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   // current chunk's walk and epochs run
   const uint64_t E_max = std::max<uint64_t>(
       1, std::min<uint64_t>(std::min<uint64_t>(cfg->max_iters, kFoldMax), (1ull << 22) / (per_epoch * B)));
-  auto margin = [&](uint64_t T) { return T * B / n + 4096; };  // ~2x the expected redraws (B / 2n per draw)
+  // rejected raw draws per kept one: < n / 2^64 with the reference's limit,
+  // ~2^-s under the L1B_TEST_INDEX_REJECT hook
+  const double p_rej = (double)(UINT64_MAX - coord_index_limit(n)) * 0x1p-64;
+  const double rej = p_rej / (1.0 - p_rej);
+  auto margin = [&](uint64_t T) {  // ~2x the expected redraws (B / 2n per draw, plus rejections)
+    return T * B / n + (uint64_t)(2.0 * rej * (double)T) + 4096;
+  };
   const uint64_t cap_raw = 2 * (E_max * per_epoch * B + margin(E_max * per_epoch * B));  // one chunk
   const uint64_t G = cap_raw / 2;  // draws per generator launch
   // stream buffer: the whole run when it fits in 2^25 draws, else rewound
@@ -1360,7 +1366,7 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
   // length (a longer block hands the run to the direct path)
   // (B = 1, serial CD: a block never redraws; no look-back, only rejected raw
   // draws become candidates)
-  const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)));
+  const int W = (int)(B + 64 + 4 * ((B * B + 2 * n - 1) / (2 * n)) + (uint64_t)(4.0 * rej * (double)B));
   const int W_prev = B == 1 ? 0 : W;
   std::vector<void*> bufs;
   cudaStream_t st0 = v.stream;
@@ -1668,8 +1674,9 @@ int pair_epochs(const ProblemView& v, const l1b_solver_cfg* cfg, uint64_t B, uin
       launched += E;
       if (h_st->stop) break;
     }
-  } catch (const Unsupported&) {
+  } catch (const Unsupported& e) {
     rc = -1;
+    if (tracing) fprintf(stderr, "[pcdm pairs] declined: %s\n", e.what());
   } catch (...) {
     cudaStreamSynchronize(st);
     if (gs) cudaStreamSynchronize(gs);

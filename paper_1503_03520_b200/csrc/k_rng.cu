@@ -743,12 +743,21 @@ uint64_t mt_stream_raw(uint64_t* d_window, uint64_t count, uint64_t* d_out, cuda
   return count;
 }
 
+uint64_t coord_index_limit(uint64_t n) {
+  uint64_t top = UINT64_MAX;
+  if (const char* e = getenv("L1B_TEST_INDEX_REJECT")) {
+    const int s = atoi(e);
+    if (s >= 1 && s <= 63) top -= UINT64_MAX >> s;
+  }
+  return top - top % n;
+}
+
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            uint64_t* d_words, cudaStream_t st) {
   using namespace mt;
   count = (count + 2 * MID - 1) / (2 * MID) * (2 * MID);
   if (count == 0) return 0;
-  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
+  const uint64_t lim = coord_index_limit(n);
   uint64_t* words = d_words;
   if (!words) L1B_CUDA(cudaMallocAsync(&words, count * 8, st));
   mt_stream_words(d_window, count, words, st);

@@ -50,6 +50,12 @@ bool device_uniform_draws(uint64_t seed, uint64_t count, double lo, double hi, b
 // Streams longer than one chunk (312 x 256 draws) run in parallel chunks
 // started by jump-ahead (k_rng.cu).
 void mt_seed_state(uint64_t seed, uint64_t* w312);
+// The rejection limit of the CD / PCDM coordinate draws: UINT64_MAX -
+// UINT64_MAX % n (rng.hpp:37-45).  Test hook: L1B_TEST_INDEX_REJECT=s lowers
+// it by UINT64_MAX >> s (a draw is redrawn with probability ~2^-s), so the
+// redraw paths, hit once per ~2^64/n draws otherwise, run under parity tests
+// (oracle: lo_set_index_reject).  Read per call.
+uint64_t coord_index_limit(uint64_t n);
 uint64_t mt_stream_indices(uint64_t* d_window, uint64_t count, uint64_t n, uint32_t* d_out,
                            uint64_t* d_words, cudaStream_t st);
 // the raw 64-bit outputs of the same continued stream (count rounded up to 312)

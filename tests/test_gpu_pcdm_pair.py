@@ -106,3 +106,42 @@ def test_pair_path_not_taken_for_two_stages():
     assert not tr_p.ran("pcdm_pair") and tr_p.path == tr_d.path
     np.testing.assert_array_equal(x_p, x_d)
     np.testing.assert_array_equal(tr_p.objectives(), tr_d.objectives())
+
+
+@pytest.mark.parametrize("n,block,solver,epochs,shift", [(1000, 1, "cd", 6, 3), (4097, 1, "cd", 4, 1),
+                                                         (4096, 256, "pcdm", 10, 3), (3001, 512, "pcdm", 6, 2),
+                                                         (65536, 1024, "pcdm", 3, 4), (8192, 256, "pcdm", 150, 5)])
+def test_redrawn_draws_match_direct_and_oracle(oracle, n, block, solver, epochs, shift):
+    """Draws the reference rejects (x >= UINT64_MAX - UINT64_MAX % n) come once
+    per ~2^64/n draws, so the walk's redraw handling (B = 1: blocks extended by
+    rejected draws, cd_b1_starts_kernel; B > 1: kPrevRej candidates) never meets
+    a real stream.  L1B_TEST_INDEX_REJECT=s (and the oracle's
+    lo_set_index_reject) lower the limit so ~2^-s of the draws are redrawn:
+    the pair path, the direct path and the oracle must still agree."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(n=n, stages=1, q=1, s_divisor=50, seed=7, theta=TH)
+    inst = l1bench.build_instance(**kw)
+    cfg = dict(max_iters=epochs, seed=3, varpi=4) if solver == "cd" else dict(max_iters=epochs, block=block, seed=3)
+    tr_0, x_0 = _run(inst, solver, True, **cfg)
+    os.environ["L1B_TEST_INDEX_REJECT"] = str(shift)
+    oracle.set_index_reject(shift)
+    try:
+        tr_p, x_p = _run(inst, solver, True, **cfg)
+        tr_d, x_d = _run(inst, solver, False, **cfg)
+        oi = oracle.build_instance(**kw)
+        if solver == "cd":
+            otr, ox = oracle.cd(oi, **cfg)
+        else:
+            otr, ox = oracle.pcdm(oi, **cfg)
+    finally:
+        del os.environ["L1B_TEST_INDEX_REJECT"]
+        oracle.set_index_reject(0)
+    assert tr_p.ran("pcdm_pair") and not tr_d.ran("pcdm_pair"), (tr_p.path, tr_d.path)
+    assert not np.array_equal(x_0, x_p)  # the hook moved the stream
+    np.testing.assert_array_equal(x_p, x_d)
+    np.testing.assert_array_equal([s.extra for s in tr_p.samples], [s.extra for s in tr_d.samples])
+    np.testing.assert_array_equal([s.extra for s in tr_p.samples], otr["extra"])
+    assert rel_err(x_p, ox) < 1e-10
+    assert rel_err(tr_p.objectives(), otr["objective"]) < 1e-10
