@@ -149,11 +149,59 @@ def time_path(inst, op, args, prof_iters=100, arith="exact"):
     ms_total = ev0.elapsed_time(ev1)
     kms_long = sess.profile(prof_iters)
     kmode = sess.kernel_mode()
+    tile = sess.tile_geometry() if kmode == 6 else None
     sess.end()
-    return {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
-            "k1_ms": kms[0] / args.steps, "k2_ms": kms[1] / args.steps, "launches": int(launches),
-            "k1_ms_long": kms_long[0] / prof_iters, "k2_ms_long": kms_long[1] / prof_iters,
-            "kmode": kmode, "arith": arith}
+    out = {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
+           "k1_ms": kms[0] / args.steps, "k2_ms": kms[1] / args.steps, "launches": int(launches),
+           "k1_ms_long": kms_long[0] / prof_iters, "k2_ms_long": kms_long[1] / prof_iters,
+           "kmode": kmode, "arith": arith}
+    if tile:  # profile(): ms[0] = the tile launches, ms[1] = the remainder's launches
+        k = tile[0]
+        out.update(tile=tile, tile_ms=kms[0] / (args.steps // k), tile_ms_long=kms_long[0] / (prof_iters // k),
+                   tile_launches=args.steps // k)
+    return out
+
+
+# FP64 flops per entry and iteration of the matrix-free FISTA step with S
+# stages (fma = 2): the chains G^T x and G u, 3 per entry and stage each
+# (lifting: 3 fma per pair; exact: 4 mul + 2 add per pair), plus r = sigma t - b
+# (2), ||r||^2 (2), u = sigma ((1+beta) r - beta r') (4), y (3), y - g / L (2),
+# the shrink (1) and ||x||_1 (1)
+def flops_per_entry(stages):
+    return 6 * stages + 15
+
+
+def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
+    """The tile kernel (K iterations per launch) is bound by the FP64 pipe and
+    its issue latency, not by HBM: the roofline is FP64 flops per launch over
+    the measured fma throughput; the HBM side is reported beside it."""
+    n = int(info.n)
+    k, span, valid = t["tile"]
+    flops = flops_per_entry(stages) * n * k
+    byts = 48.0 * n * span / valid  # x_k, x_{k-1}, sigma, b read and two x written, tiles overlapping by span - valid
+    ms, ms_long = t["tile_ms"], t["tile_ms_long"]
+    achieved = flops / (ms * 1e-3) / 1e12
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("matrix_free:tile" + (":fma" if t.get("arith") == "fma" else ""))
+        except Exception:
+            traffic = None
+    return {"bound": "fp64", "kernel": f"fista_tb ({k} FISTA iterations per launch on chip-resident tiles of "
+                                       f"{span} entries, {valid} kept; matrix-free, residuals carried)",
+            "achieved": achieved, "peak": fp64_peak, "peak_source": fp64_src, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak, "flops_per_launch": flops, "flops_per_entry_iteration": flops_per_entry(stages),
+            "iterations_per_launch": k, "launch_ms": ms,
+            "launch_ms_source": "CUDA events around every launch of the timed region",
+            "launch_ms_long_run": ms_long, "achieved_long_run": flops / (ms_long * 1e-3) / 1e12,
+            "traffic": traffic,
+            "limiter": ("FP64 pipe and issue latency: ncu shows the FP64 pipe 51.5 % busy, 1.95 IPC, DRAM 11.8 % "
+                        "(profiles/r2_ncu_full_fista_tb.txt); the pipe also executes the shrink's compares and "
+                        "the halo entries' work (own 240 of 256 per warp window, kept 1712 of 1920 per tile)"),
+            "hbm": {"achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
+                    "frac": byts / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": byts},
+            "hbm_gbs_ax_atr": byts / (ms * 1e-3) / 1e9}
 
 
 def roofline(path, t, info, peak, peak_src):
@@ -303,16 +351,25 @@ def main():
     inst = l1bench.build_instance(device=local, lazy_sparse=True, **kw)
     gen_s = time.perf_counter() - t0
     peak, peak_src = peaks()
+    fp64_peak = l1bench.fp64_peak(local)
+    fp64_src = ("measured on this GPU by l1b_fp64_peak (independent fma chains, all SMs, best of 3); "
+                "nominal 148 SMs x 64 lanes x 2 x 1.965 GHz = 37.2")
+
+    def mf_roofline(t):
+        if t["kmode"] == 6:
+            return roofline_tile(t, info, kw["stages"], fp64_peak, fp64_src, peak, peak_src)
+        return roofline("matrix_free", t, info, peak, peak_src)
+
     with ClockSampler(local) as clk:
         fused = time_path(inst, "matrix_free", args, arith=args.arith)
     info = inst.info  # builds nothing; CSR/CSC come with the first sparse use below
-    rf = roofline("matrix_free", fused, info, peak, peak_src)
+    rf = mf_roofline(fused)
     # the other arithmetic mode on the same instance (exact = the reference's bits)
     other = "exact" if args.arith == "fma" else "fma"
     with ClockSampler(local) as clk_other:
         alt = time_path(inst, "matrix_free", args, arith=other)
     alt_line = {"arith": other, "value": alt["ips"], "ms_per_step": alt["ms_step"],
-                "roofline": roofline("matrix_free", alt, info, peak, peak_src), "clocks": clk_other.summary()}
+                "roofline": mf_roofline(alt), "clocks": clk_other.summary()}
     # e2e before the CSR/CSC copy exists (37 GB of device memory at C4)
     e2e_line = e2e_more = None
     if not args.no_e2e:
@@ -340,10 +397,13 @@ def main():
         "config": {"workload": f"C4 FISTA: n=2^{int(math.log2(info.n))} cols x m=2^{int(math.log2(info.m))} rows, "
                                f"4 stages, nnz={info.nnz}, q=1, s=n/1000, tau=1, seed 3",
                    "l2": "inputs larger than L2 (no flush needed)", "parallelism": "single GPU",
-                   "path": ("matrix-free, residuals recomputed from x (Givens stages in registers + "
-                            "warp shuffles, 256-bit loads); " +
-                            ("two FISTA iterations per launch, 24n bytes/iteration" if fused["kmode"] == 4
-                             else "one FISTA iteration per launch") +
+                   "path": ("matrix-free (Givens stages in registers + warp shuffles, 256-bit loads); " +
+                            (f"{fused['tile'][0]} FISTA iterations per launch on tiles held on chip (x halos "
+                             f"exchanged between warps in shared memory, r_k carried between iterations): "
+                             f"{48.0 * fused['tile'][1] / fused['tile'][2] / fused['tile'][0]:.2f}n bytes/iteration"
+                             if fused["kmode"] == 6 else
+                             "two FISTA iterations per launch, residuals recomputed, 24n bytes/iteration"
+                             if fused["kmode"] == 4 else "one FISTA iteration per launch") +
                             ("; fused multiply-adds (arith='fma'): iterates within 1e-12 of the reference's "
                              "fista_run, same supports (tests/test_gpu_rc.py, tests/test_gpu_configs.py)"
                              if args.arith == "fma" else

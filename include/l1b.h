@@ -335,7 +335,8 @@ enum {
   L1B_RAN_PCG_PAIR = 1u << 10,        /* pair-local PCG, one cooperative launch per Newton step */
   L1B_RAN_PCG_LOOP = 1u << 11,        /* CSR/CSC PCG, one cooperative launch per Newton step */
   L1B_RAN_PCG_KERNELS = 1u << 12,     /* CSR/CSC PCG, four kernels per PCG iteration */
-  L1B_RAN_HOST_LED = 1u << 13         /* FISTA / ISTA with LPolicy::backtracking (host-led trials) */
+  L1B_RAN_HOST_LED = 1u << 13,        /* FISTA / ISTA with LPolicy::backtracking (host-led trials) */
+  L1B_RAN_FISTA_TILE = 1u << 14       /* K iterations per launch on chip-resident tiles (fista_tb_kernel) */
 };
 
 int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
@@ -435,9 +436,19 @@ enum {
   L1B_KMODE_STORED_RESIDUAL = 2,
   L1B_KMODE_RECOMPUTE = 3,
   L1B_KMODE_RECOMPUTE_TWO = 4,
-  L1B_KMODE_GENERAL_SHARD = 5
+  L1B_KMODE_GENERAL_SHARD = 5,
+  L1B_KMODE_RECOMPUTE_TILE = 6  /* K iterations per launch (fista_tb_kernel); l1b_session_tile_iters gives K */
 };
 int l1b_session_kernel_mode(l1b_session* s, int* mode);
+/* L1B_KMODE_RECOMPUTE_TILE sessions: iterations per launch, entries per tile
+ * (span) and entries a tile keeps (valid = span - 2 x the halo erosion of
+ * those iterations): HBM bytes per launch = 48 n span / valid.  Other
+ * sessions: all three 0.  (No reference counterpart: measurement only.) */
+int l1b_session_tile_geometry(l1b_session* s, int* iters, int64_t* span, int64_t* valid);
+/* Dense FP64 fma throughput of `device` in TFLOP/s (a probe kernel of
+ * independent fma chains; measurement only, no reference counterpart): the
+ * denominator of the FP64-bound kernels' roofline in bench.py. */
+int l1b_fp64_peak(int device, double* tflops);
 int l1b_session_k1(l1b_session* s);
 int l1b_session_k2(l1b_session* s);
 int l1b_session_finalize(l1b_session* s);

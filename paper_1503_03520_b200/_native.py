@@ -57,6 +57,7 @@ class ProblemInfo(C.Structure):
 # l1b_session_kernel_mode (include/l1b.h)
 KMODE_SPARSE, KMODE_MATRIX_FREE_PAIR, KMODE_STORED_RESIDUAL = 0, 1, 2
 KMODE_RECOMPUTE, KMODE_RECOMPUTE_TWO, KMODE_GENERAL_SHARD = 3, 4, 5
+KMODE_RECOMPUTE_TILE = 6
 
 
 class ShardBuffers(C.Structure):
@@ -96,7 +97,8 @@ class Summary(C.Structure):
 # l1b_summary.path flags (include/l1b.h L1B_RAN_*)
 RAN = {name: 1 << i for i, name in enumerate(
     ["fista_sparse", "fista_mf_pair", "fista_stored", "fista_recompute", "fista_two_iter", "fista_loop",
-     "fma", "pcdm_pair", "pcdm_plan", "pcdm_direct", "pcg_pair", "pcg_loop", "pcg_kernels", "host_led"])}
+     "fma", "pcdm_pair", "pcdm_plan", "pcdm_direct", "pcg_pair", "pcg_loop", "pcg_kernels", "host_led",
+     "fista_tile"])}
 
 
 # every symbol include/l1b.h declares: (name, restype, argtypes)
@@ -159,6 +161,8 @@ SIGNATURES = [
     ("l1b_session_export_x_ipc", C.c_int, [vp, vp]),
     ("l1b_session_attach_peers_ipc", C.c_int, [vp, vp, u64, vp, u64]),
     ("l1b_session_kernel_mode", C.c_int, [vp, P(C.c_int)]),
+    ("l1b_session_tile_geometry", C.c_int, [vp, P(C.c_int), P(C.c_int64), P(C.c_int64)]),
+    ("l1b_fp64_peak", C.c_int, [C.c_int, P(f64)]),
     ("l1b_session_restart", C.c_int, [vp]),
     ("l1b_session_read", C.c_int, [vp, P(Sample), u64, P(Summary), P(f64)]),
     ("l1b_nccl_get_unique_id", C.c_int, [vp]),

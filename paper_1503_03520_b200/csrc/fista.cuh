@@ -115,4 +115,37 @@ __device__ inline void fista_finalize_lagged2(FistaDev* st, FistaSample* trace) 
   st->pend_valid = 1;
 }
 
+// Lagged bookkeeping after a K-iteration tile kernel (iterations j+1 .. j+K
+// from x_j, x_{j-1}): q[4i .. 4i+3] = l1, nnz, mismatches of x_{j+i+1} and
+// ||r_{j+i}||^2.  Records iteration j (stashed sums + ||r_j||^2), then j+1 ..
+// j+K-1 (each from the previous x's sums and the next r), committing one step
+// of the t-sequence after each; x_{j+K}'s sums are stashed.  Same values and
+// order of checks as K fista_finalize_lagged calls (K = 2: lagged2).
+__device__ inline void fista_finalize_laggedk(FistaDev* st, FistaSample* trace, const double* q, int K) {
+  const uint64_t ts = global_timer_ns();
+  if (st->pend_valid) {
+    const double f = st->tau * st->pend[0] + 0.5 * (q[3] + st->tail_sq);
+    st->pend_valid = 0;
+    fista_record(st, trace, st->k + 1, f, st->pend[1], st->pend[2] == 0.0, st->pend_ts);
+    if (st->stop) return;
+  }
+  double t_next, beta;
+  for (int i = 0; i + 1 < K; ++i) {
+    fista_momentum(st, &t_next, &beta);
+    st->beta_y = beta;
+    if (st->accel) st->t = t_next;
+    const double f = st->tau * q[4 * i] + 0.5 * (q[4 * (i + 1) + 3] + st->tail_sq);
+    fista_record(st, trace, st->k + 1, f, q[4 * i + 1], q[4 * i + 2] == 0.0, ts);
+    if (st->stop) return;
+  }
+  fista_momentum(st, &t_next, &beta);
+  st->beta_y = beta;
+  if (st->accel) st->t = t_next;
+  st->pend[0] = q[4 * (K - 1)];
+  st->pend[1] = q[4 * (K - 1) + 1];
+  st->pend[2] = q[4 * (K - 1) + 2];
+  st->pend_ts = ts;
+  st->pend_valid = 1;
+}
+
 }  // namespace l1b

@@ -51,6 +51,10 @@
 #include <cooperative_groups.h>
 #include <cstdlib>
 
+#ifndef TB_WARPS
+#define TB_WARPS 8
+#endif
+
 namespace l1b {
 namespace {
 
@@ -1087,10 +1091,306 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
   launch_rc_v<S, 2, true, -1, F>(a, st);  // once per solve: the generic stage table
 }
 
+// ---------------------------------------------------------------------------
+// K iterations per launch: tiles of the line advanced K iterations on chip.
+//
+// A CTA of kTbWarps warps takes a tile of SPAN = kTbWarps * OWN consecutive
+// entries; warp w holds the window [s0 + w OWN - H, s0 + (w+1) OWN + H) in
+// registers (8 entries per lane: lane 0 / 31 are the halos, lanes 1..30 own),
+// sigma and b of the window in shared memory.  One iteration:
+//   r_k = sigma .* (G^T x_k) - b on the window (r_{k-1} is the previous
+//   iteration's r_k, kept in registers: two chain runs per iteration, against
+//   the two-iteration kernel's 2.5), u = sigma .* ((1+beta) r_k - beta r_{k-1}),
+//   g = G u, x_{k+1} on the own lanes; then every warp hands its first / last
+//   8 own entries to its neighbours through shared memory (one block barrier).
+// The tile's two outermost halos are never refreshed: their wrong values creep
+// inwards by 2S entries per iteration, so only the middle VALID = SPAN - 2E
+// entries (E >= 2S (K-1)) of a tile are kept; consecutive tiles overlap by 2E.
+// HBM: x_k, x_{k-1}, sigma, b read once and two x written per K iterations,
+// 48n (1 + 2E / VALID) bytes per launch -- the FP64 pipe bounds the kernel.
+// Per entry the operations are segment2v's: identical iterates.  CTAs are
+// persistent (one per SM), tiles strided by the grid; the per-iteration sums
+// are accumulated per warp in shared memory and folded in a fixed order.
+constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
+constexpr int kTbCtas = 512 / kTbThreads;  // resident CTAs per SM (128 registers per thread)
+template <int S>
+struct TbGeom {
+  static constexpr int W = 32 * kTbV;
+  static constexpr int H = kTbV;  // one lane per side; >= 2S for S <= 4
+  static constexpr int OWN = W - 2 * H;
+  static constexpr int SPAN = kTbWarps * OWN;
+  static_assert(2 * S <= H, "halo narrower than two chain runs");
+};
+constexpr int tb_erosion(int S, int K) { return (2 * S * (K - 1) + 7) / 8 * 8; }
+
+struct TbArgs {
+  int64_t n;
+  StageTab right;
+  const double* sigma;
+  const double* b;
+  const double* x_k;
+  const double* x_km1;
+  double* out1;  // x_{k+K-1}
+  double* out2;  // x_{k+K}
+  FistaDev* st;
+  FistaSample* trace;
+  double* partials;  // gridDim.x * 4K per-CTA sums, then the 4K totals
+  int64_t valid, ntiles;
+  int K, E, replay;
+};
+
+struct TbSmem {
+  double2 sb[kTbWarps][kTbV][32];  // (sigma, b) by [warp][entry][lane]: one 128-bit load, conflict-free
+  double xch[2][2][kTbWarps][kTbV];  // [iteration parity][first / last own lane][warp][entry]
+  double lane_acc[kTbKMax][2][kTbWarps][32];  // per lane and iteration: ||x_{k+1}||_1, ||r_k||^2
+  double cnt[kTbWarps][kTbKMax][2];           // per warp and iteration: nnz, mismatches
+  double beta[kTbKMax];
+  double inv_l, thr;
+  int last;
+};
+
+// One iteration on the warp's window.  xc = x_k (window, halos current);
+// xo = x_{k-1} on entry (own lanes), x_{k+1} on exit; rp = r_{k-1} on entry,
+// r_k on exit (both valid on the own entries +- S).
+template <int S, int PAR, bool F, bool INTERIOR, bool FIRST>
+__device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int64_t e0, int lane,
+                                        int warp, bool lane_valid, const double (&xc)[kTbV],
+                                        double (&xo)[kTbV], double (&rp)[kTbV], unsigned& nx) {
+  constexpr int V = kTbV;
+  constexpr int KC = FIRST ? 2 : 1;
+  const int64_t n = A.n;
+  const double bt = sm.beta[it], bt1 = 1.0 + bt;
+  double t[KC][V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    t[0][i] = xc[i];
+    if (FIRST) t[KC - 1][i] = xo[i];
+  }
+  wchainv<S, true, INTERIOR, KC, PAR, V, F>(t, e0, n, A.right);
+  double g[1][V], rr = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const double2 q = sm.sb[warp][i][lane];
+    const double sg = q.x, bb = q.y;
+    const double rk = mul_sub<F>(sg, t[0][i], bb);
+    rr = F ? __fma_rn(rk, rk, rr) : rr + rk * rk;
+    const double rm = FIRST ? mul_sub<F>(sg, t[KC - 1][i], bb) : rp[i];
+    g[0][i] = sg * mul_sub<F>(bt1, rk, bt * rm);
+    rp[i] = rk;
+  }
+  wchainv<S, false, INTERIOR, 1, PAR, V, F>(g, e0, n, A.right);
+  const double inv_l = sm.inv_l, thr = sm.thr;
+  double l1 = 0.0;
+  unsigned nz = 0, mis = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const double y = F ? __fma_rn(bt, xc[i] - xo[i], xc[i]) : xc[i] + bt * (xc[i] - xo[i]);
+    // soft_threshold (shrink()) with its two compares reused for nnz: above
+    // thr z - thr > 0 and below -thr z + thr < 0 exactly (a difference of
+    // distinct doubles never rounds to zero), so v != 0 iff one of them holds
+    const double z = F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i];
+    const bool hi = z > thr, lo = z < -thr;
+    double v = hi ? z - thr : (lo ? z + thr : 0.0);
+    l1 += fabs(v);
+    nz += (unsigned)(hi | lo);
+    mis += (unsigned)(v != y);
+    if (!INTERIOR && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
+    xo[i] = v;
+  }
+  const int K = A.K;
+  double* dst = it == K - 1 ? A.out2 : (it == K - 2 && !A.replay) ? A.out1 : nullptr;
+  if (dst && lane_valid) {
+    if (INTERIOR || e0 + V <= n) {
+      const double a[4] = {xo[0], xo[1], xo[2], xo[3]}, c[4] = {xo[4], xo[5], xo[6], xo[7]};
+      st4(dst + e0, a);
+      st4(dst + e0 + 4, c);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i)
+        if (e0 + i < n) dst[e0 + i] = xo[i];
+    }
+  }
+  if (lane_valid) {
+    sm.lane_acc[it][0][warp][lane] += l1;
+    sm.lane_acc[it][1][warp][lane] += rr;
+  }
+  nz = __reduce_add_sync(kFull, lane_valid ? nz : 0u);
+  mis = __reduce_add_sync(kFull, lane_valid ? mis : 0u);
+  if (lane == 0) {
+    sm.cnt[warp][it][0] += (double)nz;
+    sm.cnt[warp][it][1] += (double)mis;
+  }
+  if (it + 1 < K) {
+    // halo exchange for the next iteration (slot parity alternates: one
+    // block barrier per exchange)
+    const int p = nx & 1;
+    ++nx;
+    if (lane == 1) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) sm.xch[p][0][warp][i] = xo[i];
+    } else if (lane == 30) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) sm.xch[p][1][warp][i] = xo[i];
+    }
+    __syncthreads();
+    if (lane == 0 && warp > 0) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][1][warp - 1][i];
+    } else if (lane == 31 && warp + 1 < kTbWarps) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][0][warp + 1][i];
+    }
+  }
+}
+
+template <int S, int PAR, bool F, bool INTERIOR>
+__device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0, int lane, int warp,
+                                        unsigned& nx) {
+  using G = TbGeom<S>;
+  constexpr int V = kTbV;
+  const int64_t n = A.n;
+  const int64_t w0 = t0 - A.E + (int64_t)warp * G::OWN - G::H;
+  const int64_t e0 = w0 + V * lane;
+  // validity is per lane: t0, VALID, E, OWN and H are multiples of 8, so a
+  // tile's kept range starts and ends on lane boundaries; entries past n are
+  // zero in every array and contribute nothing to the sums
+  const bool lane_valid = lane >= 1 && lane <= 30 && e0 >= t0 && e0 + V <= t0 + A.valid && e0 < n;
+  double xa[V], xb[V], rp[V];  // x_k / x_{k-1} ping-pong: no register copies between iterations
+  {
+    double sg[V], bb[V];
+    if (w0 >= 0 && w0 + G::W <= n) {
+      ldv<V>(A.x_k + e0, xa);
+      ldv<V>(A.x_km1 + e0, xb);
+      ldv<V>(A.sigma + e0, sg);
+      ldv<V>(A.b + e0, bb);
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const bool in = e0 + i >= 0 && e0 + i < n;
+        xa[i] = in ? A.x_k[e0 + i] : 0.0;
+        xb[i] = in ? A.x_km1[e0 + i] : 0.0;
+        sg[i] = in ? A.sigma[e0 + i] : 0.0;
+        bb[i] = in ? A.b[e0 + i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(sg[i], bb[i]);
+  }
+  __syncwarp();
+  const int K = A.K;
+  tb_step<S, PAR, F, INTERIOR, true>(A, sm, 0, e0, lane, warp, lane_valid, xa, xb, rp, nx);  // x_{k+1} in xb
+  int it = 1;
+  for (; it + 1 < K; it += 2) {
+    tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
+    tb_step<S, PAR, F, INTERIOR, false>(A, sm, it + 1, e0, lane, warp, lane_valid, xa, xb, rp, nx);
+  }
+  if (it < K) tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
+}
+
+template <int S, int PAR, bool F>
+__global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A) {
+  using G = TbGeom<S>;
+  extern __shared__ __align__(16) unsigned char tb_raw[];
+  TbSmem& sm = *reinterpret_cast<TbSmem*>(tb_raw);
+  FistaDev* st = A.st;
+  if (!A.replay && *(volatile int*)&st->stop) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int K = A.K;
+  if (threadIdx.x == 0) {
+    // beta of each iteration: beta_y, then the t-sequence (fista_momentum)
+    double t = A.replay ? st->snap_t : st->t;
+    sm.beta[0] = A.replay ? st->snap_beta : st->beta_y;
+    if (!A.replay && blockIdx.x == 0) {
+      st->snap_t = st->t;
+      st->snap_beta = st->beta_y;
+    }
+    for (int i = 1; i < K; ++i) {
+      const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+      sm.beta[i] = st->accel ? (t - 1.0) / tn : 0.0;
+      t = tn;
+    }
+    sm.inv_l = 1.0 / st->lval;
+    sm.thr = st->tau * sm.inv_l;
+  }
+  for (int q = threadIdx.x; q < kTbKMax * 2 * kTbWarps * 32; q += kTbThreads) (&sm.lane_acc[0][0][0][0])[q] = 0.0;
+  for (int q = threadIdx.x; q < kTbWarps * kTbKMax * 2; q += kTbThreads) (&sm.cnt[0][0][0])[q] = 0.0;
+  __syncthreads();
+  unsigned nx = 0;  // exchanges so far (the same count in every warp)
+  for (int64_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const int64_t t0 = tile * A.valid;
+    const int64_t s_lo = t0 - A.E - G::H, s_hi = t0 - A.E + G::SPAN + G::H;
+    if (s_lo >= 2 && s_hi <= A.n - 1)
+      tb_tile<S, PAR, F, true>(A, sm, t0, lane, warp, nx);
+    else
+      tb_tile<S, PAR, F, false>(A, sm, t0, lane, warp, nx);
+  }
+  __syncthreads();
+  double* part = A.partials;
+  for (int q = threadIdx.x; q < 4 * K; q += kTbThreads) {  // fixed order: warps, then lanes
+    const int i = q >> 2, c = q & 3;
+    double s = 0.0;
+    if (c == 1 || c == 2) {
+      for (int w = 0; w < kTbWarps; ++w) s += sm.cnt[w][i][c - 1];
+    } else {
+      for (int w = 0; w < kTbWarps; ++w)
+        for (int l = 0; l < 32; ++l) s += sm.lane_acc[i][c == 0 ? 0 : 1][w][l];
+    }
+    part[(size_t)blockIdx.x * 4 * K + q] = s;
+  }
+  if (A.replay) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sm.last = atomicAdd(&st->ticket[0], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!sm.last) return;
+  __threadfence();
+  double* tot = part + (size_t)gridDim.x * 4 * K;
+  for (int q = threadIdx.x; q < 4 * K; q += kTbThreads) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&part[(size_t)b * 4 * K + q]);
+    tot[q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->ticket[0] = 0u;
+    fista_finalize_laggedk(st, A.trace, tot, K);
+  }
+}
+
+template <int S, int PAR, bool F>
+int tb_grid_cap() {
+  static const int cap = [] {
+    L1B_CUDA(cudaFuncSetAttribute(fista_tb_kernel<S, PAR, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(TbSmem)));
+    int per_sm = 0;
+    L1B_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_tb_kernel<S, PAR, F>, kTbThreads,
+                                                           sizeof(TbSmem)));
+    return std::max(1, per_sm) * sm_count();
+  }();
+  return cap;
+}
+
+template <int S, int PAR, bool F>
+void launch_tb(TbArgs a, cudaStream_t st) {
+  using G = TbGeom<S>;
+  a.E = tb_erosion(S, a.K);
+  a.valid = G::SPAN - 2 * a.E;
+  a.ntiles = (a.n + a.valid - 1) / a.valid;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, tb_grid_cap<S, PAR, F>()));
+  fista_tb_kernel<S, PAR, F><<<grid, kTbThreads, sizeof(TbSmem), st>>>(a);
+  L1B_LAUNCHED();
+}
+
 template <int S, bool F>
 void launch_rc2_s(const RcArgs& a, const Rc2Out& o, cudaStream_t st) {
   if (is_canon<S>(a.right)) return launch_rc2<S, canon_par<S>(), F>(a, o, st);
   launch_rc2<S, -1, F>(a, o, st);
+}
+
+template <int S, bool F>
+void launch_tb_s(const TbArgs& a, cudaStream_t st) {
+  if (is_canon<S>(a.right)) return launch_tb<S, canon_par<S>(), F>(a, st);
+  launch_tb<S, -1, F>(a, st);
 }
 
 }  // namespace
@@ -1107,6 +1407,10 @@ void prepare_s(const StageTab& t) {
     if (!F) grid_cap_of<fista_rc_persistent<S, -1>>();
   }
   grid_cap_of<fista_rc_kernel<S, 2, true, -1, F>>();
+  if (is_canon<S>(t))
+    tb_grid_cap<S, canon_par<S>(), F>();
+  else
+    tb_grid_cap<S, -1, F>();
 }
 
 void fista_rc_prepare(const OpView& op, bool fma) {
@@ -1189,6 +1493,61 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
     case 9: return launch_rc2_s<4, true>(a, o, st);
     default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
   }
+}
+
+void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* out2, int K, bool replay,
+                    double* tb, cudaStream_t st, bool fma) {
+  if (K < 1 || K > kTbKMax) throw std::invalid_argument("fista_rc_iterk: K out of range");
+  TbArgs a;
+  a.n = (int64_t)op.n;
+  a.right = op.right;
+  a.sigma = op.sigma;
+  a.b = ib.b;
+  a.x_k = ib.x_k;
+  a.x_km1 = ib.x_km1;
+  a.out1 = out1;
+  a.out2 = out2;
+  a.st = ib.st;
+  a.trace = ib.trace;
+  a.partials = tb;
+  a.K = K;
+  a.replay = replay ? 1 : 0;
+  switch (op.right.count * 2 + (fma ? 1 : 0)) {
+    case 2: return launch_tb_s<1, false>(a, st);
+    case 3: return launch_tb_s<1, true>(a, st);
+    case 4: return launch_tb_s<2, false>(a, st);
+    case 5: return launch_tb_s<2, true>(a, st);
+    case 6: return launch_tb_s<3, false>(a, st);
+    case 7: return launch_tb_s<3, true>(a, st);
+    case 8: return launch_tb_s<4, false>(a, st);
+    case 9: return launch_tb_s<4, true>(a, st);
+    default: throw Unsupported("recomputing FISTA kernel: 1..4 stages");
+  }
+}
+
+void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid) {
+  *span = TbGeom<4>::SPAN;  // (the tile shape does not depend on S)
+  *valid = *span - 2 * tb_erosion(stages, K);
+}
+
+uint64_t fista_tb_scratch() { return (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax; }
+
+// the tile kernel above 2^20 entries (smaller instances run whole chunks of
+// iterations in one cooperative launch); L1B_TB=0 switches it off
+// (read per session: tests switch it; L1B_TB=2 takes the tile kernel at any n)
+bool tb_enabled(uint64_t n, int stages) {
+  const char* e = getenv("L1B_TB");
+  if (stages < 1 || stages > 4 || (e && e[0] == '0')) return false;
+  return (e && e[0] == '2') || n > (1ull << 20);  // (<= 2^20: fista_rc_loop)
+}
+
+// iterations per tile launch (L1B_TB_K, read per session): K = 2 (mod 4)
+// keeps the x rotation of the two-iteration kernel (a launch from x_j writes
+// X[(j+K-1) % 4], X[(j+K) % 4], never its inputs X[j % 4], X[(j-1) % 4])
+int tb_iters() {
+  const char* e = getenv("L1B_TB_K");
+  const int k = e ? atoi(e) : 14;  // (C4: 14 -> 2119 iter/s, 10 -> 2112, 6 -> less)
+  return (k < 2 || k > kTbKMax || k % 4 != 2) ? 14 : k;
 }
 
 int fista_rc2_halo(int stages) {

@@ -163,6 +163,9 @@ struct FistaDev {
   // (l1, nnz, mism) of x_{k+2}
   double scal8[8];
   int pair_pending;  // shards: the last kernel ran two iterations (finalize: lagged2)
+  // tile kernel (K iterations per launch): t and beta_y as the last launch
+  // found them -- a stop inside a launch replays it from there (fista_rc_iterk)
+  double snap_t, snap_beta;
 };
 
 struct FistaBufs {
@@ -240,6 +243,22 @@ void fista_rc_loop(const OpView& op, const IterBufs& ib, double* const X[4], uin
 // 24n bytes per iteration (k_iter_rc.cu fista_rc2_kernel); one device
 void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint64_t lo, uint64_t hi,
                     cudaStream_t st, const PeerViews& peers = PeerViews(), bool fma = false);
+// K iterations in one launch (k_iter_rc.cu fista_tb_kernel: tiles of 16 warps
+// advance K iterations with their x halos exchanged in shared memory):
+// x_{k+K-1} into out1, x_{k+K} into out2; K in [2, kTbKMax].  tb = device
+// scratch of fista_tb_scratch(K) doubles.  replay: the same iterations from
+// the launch's snapshot of t / beta_y without any bookkeeping, only out2
+// written (a stop inside the launch: x of the stopping iteration).  One device.
+constexpr int kTbKMax = 14;
+void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* out2, int K, bool replay,
+                    double* tb, cudaStream_t st, bool fma);
+uint64_t fista_tb_scratch();
+void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid);
+// k_probe.cu: dense FP64 fma throughput of this GPU (TFLOP/s, best of 3 timed runs)
+double fp64_peak_tflops(int device);
+// n from which the tile kernel runs (L1B_TB=0: never; L1B_TB_K: iterations per launch)
+bool tb_enabled(uint64_t n, int stages);
+int tb_iters();
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op, bool fma = false);
 // general shards: prox / momentum on the own column slice from the reduced g

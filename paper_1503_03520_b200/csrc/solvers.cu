@@ -113,6 +113,19 @@ struct l1b_session {
 
   bool fma() const { return cfg.arith == L1B_ARITH_FMA; }
 
+  // tile kernel (K iterations per launch, one device): tbk = K (0: off),
+  // tb = its per-CTA sums, tb_starts = j of every launch (a stop inside one is
+  // replayed from its inputs, which no later launch overwrites)
+  int tbk = 0;
+  double* tb = nullptr;
+  std::vector<uint64_t> tb_starts;
+
+  void iteratek(uint64_t j, cudaStream_t stream) {
+    const int K = tbk;
+    fista_rc_iterk(*v.op, iter_bufs(j), X[(j + K - 1) % 4], X[(j + K) % 4], K, false, tb, stream, fma());
+    tb_starts.push_back(j);
+  }
+
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
     fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
@@ -310,6 +323,10 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->trace = (FistaSample*)s->valloc(s->cap * sizeof(FistaSample));
   s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
+  if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count)) {
+    s->tbk = tb_iters();
+    s->tb = s->dalloc(fista_tb_scratch());
+  }
   if (s->recompute) fista_rc_prepare(*v.op, s->fma());  // module load + grid sizing before t0
   session_reset(s);
 }
@@ -319,6 +336,7 @@ void session_reset(l1b_session* s) {
   const ProblemView& v = s->v;
   const l1b_solver_cfg* cfg = &s->cfg;
   cudaStream_t st = v.stream;
+  s->tb_starts.clear();
   if (s->single)  // every rotating buffer, halos included (the first launch reads X[3] as x_{-1})
     for (int q = 0; q < s->nbuf; ++q) L1B_CUDA(cudaMemsetAsync(s->X[q], 0, (s->nx + 2 * s->xh) * 8, st));
   L1B_CUDA(cudaMemsetAsync(s->x, 0, s->nx * sizeof(double), st));
@@ -375,6 +393,8 @@ bool rc2_enabled() {
 bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
   if (!(s->recompute && !s->shard && rc2_enabled())) return false;
   uint64_t i = 0;
+  if (s->tbk)
+    for (; i + (uint64_t)s->tbk <= iters; i += (uint64_t)s->tbk) s->iteratek(s->launched + i, st);
   for (; i + 2 <= iters; i += 2) s->iterate2(s->launched + i, st);
   if (i < iters) s->iterate(s->launched + i, st);
   return true;
@@ -384,7 +404,7 @@ bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
 // launch per chunk; also for single iterations, so that every iteration of a
 // session reduces its sums in the same order)
 bool uses_loop(const l1b_session* s) {
-  return s->recompute && !s->shard && s->v.n <= kPersistMaxN && persist_enabled();
+  return s->recompute && !s->shard && !s->tbk && s->v.n <= kPersistMaxN && persist_enabled();
 }
 
 void session_step(l1b_session* s, uint64_t iters) {
@@ -439,6 +459,18 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
     L1B_CUDA(cudaMemcpyAsync(tr.data(), s->trace, kept * sizeof(FistaSample),
                              cudaMemcpyDeviceToHost, st));
   const double* xf = s->single ? s->X[h.k % (uint64_t)s->nbuf] + s->xh : s->x;  // x after the last executed iteration
+  // a tile launch stores only its last two iterates: a stop before those is
+  // replayed from the launch's inputs (same operations: the same x)
+  for (auto it = s->tb_starts.rbegin(); it != s->tb_starts.rend(); ++it) {
+    const uint64_t j = *it;
+    if (h.k <= j) continue;
+    if (h.k + 1 < j + (uint64_t)s->tbk) {
+      double* dst = s->X[(j + 1) % 4];
+      fista_rc_iterk(*s->v.op, s->iter_bufs(j), nullptr, dst, (int)(h.k - j), true, s->tb, st, s->fma());
+      xf = dst;
+    }
+    break;
+  }
   if (x_host) L1B_CUDA(cudaMemcpyAsync(x_host, xf, s->nx * 8, cudaMemcpyDeviceToHost, st));
   if (d_x) L1B_CUDA(cudaMemcpyAsync(d_x, xf, s->nx * 8, cudaMemcpyDeviceToDevice, st));
   L1B_CUDA(cudaStreamSynchronize(st));
@@ -449,7 +481,7 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
     sum->path = L1B_RAN_FISTA_LOOP | L1B_RAN_FISTA_RECOMPUTE;
   else if (s->recompute)
     sum->path = (rc2_enabled() ? L1B_RAN_FISTA_TWO_ITER : 0u) | L1B_RAN_FISTA_RECOMPUTE |
-                (s->fma() ? L1B_RAN_FMA : 0u);
+                (s->tb_starts.empty() ? 0u : L1B_RAN_FISTA_TILE) | (s->fma() ? L1B_RAN_FMA : 0u);
   else
     sum->path = s->single ? L1B_RAN_FISTA_STORED : s->fused ? L1B_RAN_FISTA_MF_PAIR : L1B_RAN_FISTA_SPARSE;
   sum->status = status;
@@ -559,12 +591,29 @@ int l1b_session_buffers(l1b_session* s, l1b_shard_buffers* out) {
   });
 }
 
+int l1b_fp64_peak(int device, double* tflops) {
+  return guard([&] {
+    if (!tflops) throw InvalidArgument("null argument");
+    *tflops = fp64_peak_tflops(device);
+  });
+}
+
+int l1b_session_tile_geometry(l1b_session* s, int* iters, int64_t* span, int64_t* valid) {
+  return guard([&] {
+    if (!s || !iters || !span || !valid) throw InvalidArgument("null argument");
+    *iters = s->tbk;
+    *span = *valid = 0;
+    if (s->tbk) fista_tb_geometry((int)s->v.op->right.count, s->tbk, span, valid);
+  });
+}
+
 int l1b_session_kernel_mode(l1b_session* s, int* mode) {
   return guard([&] {
     if (!s || !mode) throw InvalidArgument("null argument");
     *mode = s->general ? L1B_KMODE_GENERAL_SHARD
             : !s->single ? (s->fused ? L1B_KMODE_MATRIX_FREE_PAIR : L1B_KMODE_SPARSE)
             : !s->recompute ? L1B_KMODE_STORED_RESIDUAL
+            : s->tbk ? L1B_KMODE_RECOMPUTE_TILE
             : (!s->shard && rc2_enabled()) ? L1B_KMODE_RECOMPUTE_TWO
                                            : L1B_KMODE_RECOMPUTE;
   });
@@ -726,22 +775,30 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
       ms_out[1] = k2;
       return;
     }
-    // two-iteration launches, timed each -- where session_step uses them too
+    // tile / two-iteration launches, timed each -- where session_step uses them too
     if (s->recompute && !s->shard && rc2_enabled()) {
+      const uint64_t K = s->tbk ? (uint64_t)s->tbk : 2;
       uint64_t i = 0;
-      for (; i < iters; i += 2) {
+      // (tile sessions: ms_out[0] = the tile launches, ms_out[1] = the
+      // remainder's two-iteration / single launches)
+      for (; i < iters; i += K) {
         L1B_CUDA(cudaEventRecord(ev[3 * i], st));
-        if (i + 2 <= iters)
+        if (i + K <= iters && s->tbk)
+          s->iteratek(s->launched + i, st);
+        else if (i + K <= iters)
           s->iterate2(s->launched + i, st);
-        else
-          s->iterate(s->launched + i, st);
         L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
+        if (i + K > iters) {  // the remainder: two-iteration launches (+ one single)
+          uint64_t r = i;
+          for (; r + 2 <= iters; r += 2) s->iterate2(s->launched + r, st);
+          if (r < iters) s->iterate(s->launched + r, st);
+        }
         L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
       }
       s->launched += iters;
       L1B_CUDA(cudaStreamSynchronize(st));
       double k1 = 0.0, k2 = 0.0;  // k2: the empty second slot, as in single-kernel mode
-      for (i = 0; i < iters; i += 2) {
+      for (i = 0; i < iters; i += K) {
         float a = 0.f, c = 0.f;
         L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
         L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));

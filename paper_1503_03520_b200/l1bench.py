@@ -727,6 +727,13 @@ def known_solver(ident: str) -> bool:  # solvers.cpp:570-572 (+ pcdm)
     return ident in SolverConfig._IDS
 
 
+def fp64_peak(device: int = 0) -> float:
+    """Dense FP64 fma throughput of the GPU in TFLOP/s (l1b_fp64_peak)."""
+    v = C.c_double()
+    N.check(_lib().l1b_fp64_peak(int(device), C.byref(v)))
+    return float(v.value)
+
+
 class Session:
     """Stepping handle over the device-resident FISTA/ISTA loop (bench.py)."""
 
@@ -750,6 +757,13 @@ class Session:
         m = C.c_int()
         N.check(_lib().l1b_session_kernel_mode(self._s, C.byref(m)))
         return int(m.value)
+
+    def tile_geometry(self):
+        """(iterations per launch, entries per tile, entries kept per tile) of a
+        tile-kernel session (N.KMODE_RECOMPUTE_TILE); zeros otherwise."""
+        k, span, valid = C.c_int(), C.c_int64(), C.c_int64()
+        N.check(_lib().l1b_session_tile_geometry(self._s, C.byref(k), C.byref(span), C.byref(valid)))
+        return int(k.value), int(span.value), int(valid.value)
 
     def sync(self):
         stopped, k = C.c_int(), C.c_uint64()

@@ -1,0 +1,136 @@
+"""The tile kernel (k_iter_rc.cu fista_tb_kernel: K FISTA iterations per
+launch, 16-warp tiles with their x halos exchanged in shared memory, the
+eroded tile ends recomputed by the neighbouring tiles) against the
+two-iteration kernel (L1B_TB=0) and the oracle's restatement of fista_run
+(solvers.cpp:290-380): iterates bit-identical in both arithmetic modes,
+objectives within 1e-12, the same stop; a stop inside a launch is replayed
+from the launch's inputs."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from gpu_util import need_cuda, rel_err
+
+pytestmark = pytest.mark.gpu
+
+TH = 2 * math.pi / 10
+
+
+def _solve(inst, tile, k=None, **cfg):
+    """tile: None = the default choice for the size, True = forced (L1B_TB=2,
+    any n), False = off (L1B_TB=0)."""
+    from paper_1503_03520_b200 import l1bench
+
+    env = {"L1B_TB": {None: "1", True: "2", False: "0"}[tile]}
+    if k is not None:
+        env["L1B_TB_K"] = str(k)
+    old = {key: os.environ.get(key) for key in env}
+    os.environ.update(env)
+    try:
+        x = np.empty(inst.n)
+        tr = l1bench.fista_run(inst, l1bench.SolverConfig(op="matrix_free", **cfg), x)
+    finally:
+        for key, v in old.items():
+            if v is None:
+                del os.environ[key]
+            else:
+                os.environ[key] = v
+    return tr, x
+
+
+@pytest.mark.parametrize("n,stages,k", [(100003, 4, 10), (50001, 3, 14), (20005, 2, 6), (7777, 1, 10),
+                                        (3001, 4, 14), (449, 4, 10), (300007, 4, 2)])
+def test_tile_matches_oracle_and_two_iteration_kernel(oracle, n, stages, k):
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(n=n, stages=stages, q=1, s_divisor=100, seed=5, theta=TH)
+    inst = l1bench.build_instance(**kw)
+    oi = oracle.build_instance(**kw)
+    iters = 63  # K-launches, then two-iteration launches and a single one
+    tr, x = _solve(inst, True, k, max_iters=iters)
+    assert tr.ran("fista_tile"), tr.path
+    otr, ox = oracle.fista(oi, max_iters=iters)
+    assert tr.iterations == iters and tr.status == l1bench.StopReason.iter_budget
+    np.testing.assert_array_equal(x, ox)
+    assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
+    np.testing.assert_array_equal(tr.iters(), otr["iter"])
+    np.testing.assert_array_equal([s.nnz for s in tr.samples], otr["nnz"])
+    tr2, x2 = _solve(inst, False, max_iters=iters)
+    assert not tr2.ran("fista_tile")
+    np.testing.assert_array_equal(x, x2)
+    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
+
+
+@pytest.mark.parametrize("n,stages", [(1 << 20 | 4099, 4), (1 << 21, 3)])
+def test_tile_default_at_large_n_fma(n, stages):
+    """Above 2^20 the tile kernel is the default; the contracted arithmetic
+    gives the two-iteration kernel's bits too (same operations per entry)."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    inst = l1bench.build_instance(n=n, stages=stages, q=1, s_divisor=1000, seed=3, theta=TH)
+    tr, x = _solve(inst, None, max_iters=40, arith="fma")
+    assert tr.ran("fista_tile") and tr.ran("fma"), tr.path
+    tr2, x2 = _solve(inst, False, max_iters=40, arith="fma")
+    assert not tr2.ran("fista_tile")
+    np.testing.assert_array_equal(x, x2)
+    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
+    assert tr.iterations == tr2.iterations == 40
+
+
+@pytest.mark.parametrize("stop_at", [11, 12, 13, 17, 18, 19, 20])
+def test_stop_inside_a_tile_launch_is_replayed(stop_at):
+    """A target met at iteration stop_at: launches of K = 10 cover 1-10,
+    11-20, ...; only the last two iterates of a launch are stored, so stops at
+    11..18 are replayed from x_10, x_9.  Same stop, iterations, status and x
+    as the two-iteration kernel."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    inst = l1bench.build_instance(n=200003, stages=4, q=1, s_divisor=100, seed=2, theta=TH)
+    full, _ = _solve(inst, False, max_iters=40)
+    f = full.objectives()
+    it = list(full.iters())
+    target = float(f[it.index(stop_at)] * (1 + 1e-9))
+    assert all(v > target for v in f[:it.index(stop_at)])  # first met at stop_at
+    tr, x = _solve(inst, True, 10, max_iters=40, target_objective=target)
+    tr2, x2 = _solve(inst, False, max_iters=40, target_objective=target)
+    assert tr.ran("fista_tile")
+    assert tr.status == tr2.status == l1bench.StopReason.target_reached
+    assert tr.iterations == tr2.iterations == stop_at
+    np.testing.assert_array_equal(x, x2)
+    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
+
+
+def test_tile_session_steps_and_profile():
+    """Session.step in odd chunks (K-launches + remainders) and profile
+    (timed K-launches) give the one-call solve's iterates."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    inst = l1bench.build_instance(n=(1 << 20) + 12345, stages=4, q=1, s_divisor=1000, seed=3, theta=TH)
+    old = os.environ.get("L1B_TB")
+    os.environ["L1B_TB"] = "1"
+    try:
+        cfg = l1bench.SolverConfig(max_iters=57, op="matrix_free")
+        s = l1bench.Session(inst, cfg)
+        assert s.kernel_mode() == 6
+        k, span, valid = s.tile_geometry()
+        assert k == 14 and span % 240 == 0 and valid == span - 2 * 104
+        s.step(3)
+        s.profile(30)
+        s.step(24)
+        x = np.empty(inst.n)
+        tr = s.end(x)
+    finally:
+        if old is None:
+            del os.environ["L1B_TB"]
+        else:
+            os.environ["L1B_TB"] = old
+    tr2, x2 = _solve(inst, False, max_iters=57)
+    np.testing.assert_array_equal(x, x2)
+    assert tr.iterations == 57
+    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
