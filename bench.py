@@ -178,7 +178,9 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
     n = int(info.n)
     k, span, valid = t["tile"]
     flops = flops_per_entry(stages) * n * k
-    byts = 48.0 * n * span / valid  # x_k, x_{k-1}, sigma, b read and two x written, tiles overlapping by span - valid
+    # x_k, x_{k-1}, sigma, b read once and two x written per launch (the tiles' overlapping
+    # reads, (span - valid) / valid of the four inputs, hit L2: ncu DRAM bytes = 1.00 x 48n)
+    byts = 48.0 * n
     ms, ms_long = t["tile_ms"], t["tile_ms_long"]
     achieved = flops / (ms * 1e-3) / 1e12
     traffic = None
@@ -400,12 +402,14 @@ def main():
                    "path": ("matrix-free (Givens stages in registers + warp shuffles, 256-bit loads); " +
                             (f"{fused['tile'][0]} FISTA iterations per launch on tiles held on chip (x halos "
                              f"exchanged between warps in shared memory, r_k carried between iterations): "
-                             f"{48.0 * fused['tile'][1] / fused['tile'][2] / fused['tile'][0]:.2f}n bytes/iteration"
+                             f"{48.0 / fused['tile'][0]:.2f}n bytes/iteration"
                              if fused["kmode"] == 6 else
                              "two FISTA iterations per launch, residuals recomputed, 24n bytes/iteration"
                              if fused["kmode"] == 4 else "one FISTA iteration per launch") +
-                            ("; fused multiply-adds (arith='fma'): iterates within 1e-12 of the reference's "
-                             "fista_run, same supports (tests/test_gpu_rc.py, tests/test_gpu_configs.py)"
+                            ("; fused multiply-adds (arith='fma'; the tile kernel rotates in the scaled form, "
+                             "prod cos carried by sigma): iterates within 1e-12 of the reference's "
+                             "fista_run, same supports (tests/test_gpu_tile.py, tests/test_gpu_rc.py, "
+                             "tests/test_gpu_configs.py)"
                              if args.arith == "fma" else
                              "; iterates bit-identical to the reference's fista_run")),
                    "arith": args.arith},

@@ -265,6 +265,14 @@ void fill_stage_tab(StageTab& tab, const std::vector<int32_t>& off, const std::v
     tab.s[k] = std::sin(th[k]);
     tab.t[k] = tab.s[k] / (1.0 + tab.c[k]);
   }
+  tab.cprod = 1.0;
+  tab.scaled_ok = 1;
+  for (size_t k = 0; k < off.size(); ++k) {
+    if (std::fabs(tab.c[k]) < 0.25) tab.scaled_ok = 0;
+    tab.tn[k] = tab.scaled_ok ? tab.s[k] / tab.c[k] : 0.0;
+    tab.ic[k] = tab.scaled_ok ? 1.0 / tab.c[k] : 1.0;
+    tab.cprod *= tab.c[k];
+  }
 }
 
 std::vector<uint32_t> inverse_map(const uint32_t* map, uint64_t m) {

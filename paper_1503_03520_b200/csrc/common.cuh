@@ -69,6 +69,14 @@ struct StageTab {
   double c[kMaxStages];  // cos(theta) from the host libm (linops.cpp:84-85)
   double s[kMaxStages];
   double t[kMaxStages];  // tan(theta / 2) = s / (1 + c): the lifting form of the contracted kernels
+  // the scaled form of the tile kernel (contracted arithmetic): a stage is
+  // cos(theta) * [[1, -tan], [tan, 1]] on every pair, so G = (prod cos) * M
+  // with M two independent fmas per pair; entries a stage leaves unpaired
+  // take 1 / cos(theta) instead
+  double tn[kMaxStages];  // tan(theta)
+  double ic[kMaxStages];  // 1 / cos(theta)
+  double cprod = 1.0;     // prod cos(theta)
+  int scaled_ok = 0;      // every |cos(theta)| >= 1/4: the scaled form is well conditioned
 };
 
 struct OpView {
@@ -136,6 +144,19 @@ __device__ __forceinline__ void rot(double& vi, double& vj, double c, double s, 
   vi = a;
   vj = b;
 }
+// The scaled form of a rotation (contracted arithmetic, tile kernel):
+// [[1, -tn], [tn, 1]] (transposed: tn -> -tn), two independent fmas; the
+// factor cos(theta) is carried by the caller (StageTab::cprod).
+__device__ __forceinline__ void rot_scaled(double& vi, double& vj, double tn, bool transposed) {
+  const double a = vi, b = vj;
+  if (transposed) {
+    vi = __fma_rn(tn, b, a);
+    vj = __fma_rn(-tn, a, b);
+  } else {
+    vi = __fma_rn(-tn, b, a);
+    vj = __fma_rn(tn, a, b);
+  }
+}
 // a * b - c
 template <bool F>
 __device__ __forceinline__ double mul_sub(double a, double b, double c) {
@@ -147,6 +168,30 @@ __device__ __forceinline__ double soft_threshold(double v, double t) {
   if (v > t) return v - t;
   if (v < -t) return v + t;
   return 0.0;
+}
+
+// soft_threshold on the bit patterns: |z| > t as an unsigned compare of the
+// magnitude bits (t >= 0, z not NaN), then z - copysign(t, z) outside the band
+// and z - z = +0 inside it -- the values of soft_threshold() bit for bit, with
+// one FP64 instruction instead of two sums and the compares.  nz = (result != 0).
+__device__ __forceinline__ double soft_threshold_bits(double z, double t, bool& nz) {
+  // (on the 32-bit halves: a 64-bit mask of the sign would be turned back
+  // into an FP64 |z|)
+  const unsigned zh = (unsigned)__double2hiint(z), zl = (unsigned)__double2loint(z);
+  const unsigned th = (unsigned)__double2hiint(t), tl = (unsigned)__double2loint(t);
+  const unsigned ah = zh & 0x7fffffffu;
+  nz = (((unsigned long long)ah << 32) | zl) > (((unsigned long long)th << 32) | tl);
+  const unsigned sh = nz ? (th | (zh & 0x80000000u)) : zh, sl = nz ? tl : zl;
+  return z - __hiloint2double((int)sh, (int)sl);
+}
+// bits of a that differ from b's, or-ed into acc (acc != 0 <=> some a != b so far)
+__device__ __forceinline__ unsigned differing_bits(unsigned acc, double a, double b) {
+  return acc | ((unsigned)__double2hiint(a) ^ (unsigned)__double2hiint(b)) |
+         ((unsigned)__double2loint(a) ^ (unsigned)__double2loint(b));
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // ---- TMA bulk copies + mbarriers (PTX; sm_90+ / sm_100a) -------------------

@@ -367,50 +367,97 @@ struct Rc2Out {
 // The two-iteration kernel with V entries per lane (window 32 V): the halo
 // (>= 4S, a multiple of V) is a smaller share of a wider window -- fewer
 // rotations per own entry, more registers per thread.
-template <int S, bool TR, bool INTERIOR, int K, int PAR, int V, bool F>
+template <int S, bool TR, bool INTERIOR, int K, int PAR, int V, bool F, bool SC = false, bool SYM = false>
 __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n,
                                         const StageTab& tab) {
+  // SC (with F): the scaled form -- every pair takes [[1, -tan], [tan, 1]] and
+  // the caller carries prod cos(theta); an entry a stage leaves unpaired (the
+  // ends of [0, n)) takes 1 / cos(theta).  Otherwise F: lifting, !F: exact.
+  static_assert(!SC || F, "the scaled form belongs to the contracted arithmetic");
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int s = TR ? k : S - 1 - k;
     const int o = tab.offset[s];
-    const double c = F ? tab.t[s] : tab.c[s], sn = tab.s[s];  // (F: the lifting form)
+    const double c = SC ? tab.tn[s] : F ? tab.t[s] : tab.c[s];  // (F: the lifting form)
+    const double sn = SC ? tab.ic[s] : tab.s[s];
     const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
     if (par == 0) {
 #pragma unroll
       for (int p = 0; p < V; p += 2) {
         const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
 #pragma unroll
-        for (int q = 0; q < K; ++q)
-          if (ok) rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
+        for (int q = 0; q < K; ++q) {
+          if (SC) {
+            if (ok) rot_scaled(v[q][p], v[q][p + 1], c, TR);
+            else v[q][p] *= sn, v[q][p + 1] *= sn;
+          } else if (ok) {
+            rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
+          }
+        }
       }
     } else {
-      // the pair straddling lanes l, l+1 is rotated once, by lane l, which
-      // hands the right output back (one rotation fewer per lane and odd stage
-      // than rotating it on both sides)
-      double right[K], back[K];
+      if (SYM && (SC || !F)) {
+        // the pair straddling lanes l, l+1: each output of a rotation is a
+        // function of the pair alone, so lane l forms the left output from its
+        // neighbour's first entry and lane l+1 the right output from its
+        // neighbour's last one -- the same operations as rotating the pair on
+        // one lane (the same bits), one shuffle deep instead of shuffle ->
+        // rotation -> shuffle back
+        const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
+        const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
 #pragma unroll
-      for (int q = 0; q < K; ++q) right[q] = __shfl_down_sync(kFull, v[q][0], 1);
-      const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
-      const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
+        for (int q = 0; q < K; ++q) {
+          const double right = __shfl_down_sync(kFull, v[q][0], 1);
+          const double left = __shfl_up_sync(kFull, v[q][V - 1], 1);
+          const double a = v[q][V - 1], b = v[q][0];
+          if (SC) {
+            v[q][V - 1] = pr ? __fma_rn(TR ? c : -c, right, a) : a * sn;
+            v[q][0] = pl ? __fma_rn(TR ? -c : c, left, b) : b * sn;
+          } else {  // rotate_pair's two outputs (linops.cpp:20-30)
+            if (pr) v[q][V - 1] = TR ? c * a + sn * right : c * a - sn * right;
+            if (pl) v[q][0] = TR ? -sn * left + c * b : sn * left + c * b;
+          }
+        }
+      } else {
+        // (lifting form) the pair straddling lanes l, l+1 is rotated once, by lane l, which
+        // hands the right output back (one rotation fewer per lane and odd stage
+        // than rotating it on both sides)
+        double right[K], back[K];
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
-        double a = v[q][V - 1], b = right[q];
-        if (pr) rot<F>(a, b, c, sn, TR);
-        v[q][V - 1] = a;
-        back[q] = b;
-      }
+        for (int q = 0; q < K; ++q) right[q] = __shfl_down_sync(kFull, v[q][0], 1);
+        const bool pr = INTERIOR || (e0 + V - 1 >= o && e0 + V < n);
+        const bool pl = INTERIOR || (e0 - 1 >= o && e0 < n);
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
-        const double b = __shfl_up_sync(kFull, back[q], 1);
-        if (pl) v[q][0] = b;
+        for (int q = 0; q < K; ++q) {
+          double a = v[q][V - 1], b = right[q];
+          if (SC) {
+            if (pr) rot_scaled(a, b, c, TR);
+            else a *= sn;
+          } else if (pr) {
+            rot<F>(a, b, c, sn, TR);
+          }
+          v[q][V - 1] = a;
+          back[q] = b;
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const double b = __shfl_up_sync(kFull, back[q], 1);
+          if (pl) v[q][0] = b;
+          else if (SC) v[q][0] *= sn;
+        }
       }
 #pragma unroll
       for (int p = 1; p + 1 < V; p += 2) {
         const bool ok = INTERIOR || (e0 + p >= o && e0 + p + 1 < n);
 #pragma unroll
-        for (int q = 0; q < K; ++q)
-          if (ok) rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
+        for (int q = 0; q < K; ++q) {
+          if (SC) {
+            if (ok) rot_scaled(v[q][p], v[q][p + 1], c, TR);
+            else v[q][p] *= sn, v[q][p + 1] *= sn;
+          } else if (ok) {
+            rot<F>(v[q][p], v[q][p + 1], c, sn, TR);
+          }
+        }
       }
     }
   }
@@ -1112,6 +1159,25 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
 // persistent (one per SM), tiles strided by the grid; the per-iteration sums
 // are accumulated per warp in shared memory and folded in a fixed order.
 constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
+#ifndef TB_SCALED
+#define TB_SCALED 1  // contracted arithmetic: rotations in the scaled form (0: lifting, as in the two-iteration kernel)
+#endif
+#ifndef TB_ISHRINK
+#define TB_ISHRINK 1  // shrink and its counters on the bit patterns
+#endif
+#ifndef TB_PREFETCH
+#define TB_PREFETCH 1  // L2 prefetch of the CTA's next tile
+#endif
+#ifndef TB_SPLIT
+#define TB_SPLIT 0  // 1: split-phase halo exchange on a tile mbarrier (arrive before the bookkeeping, wait after it)
+#endif
+#ifndef TB_NSYNC
+#define TB_NSYNC 0  // 1: halo exchange between neighbouring warps on mbarriers instead of one block barrier per iteration (measured slower: 2120 vs 2477 iter/s)
+#endif
+#ifndef TB_SYM
+#define TB_SYM 1  // exact arithmetic: each lane forms its own output of a straddling pair (one shuffle deep; +0.5 %; the scaled form measured 1 % slower that way)
+#endif
+constexpr bool kTbScaled = TB_SCALED != 0, kTbSym = TB_SYM != 0, kTbSymF = TB_SYM == 2;
 constexpr int kTbCtas = 512 / kTbThreads;  // resident CTAs per SM (128 registers per thread)
 template <int S>
 struct TbGeom {
@@ -1142,17 +1208,21 @@ struct TbArgs {
 struct TbSmem {
   double2 sb[kTbWarps][kTbV][32];  // (sigma, b) by [warp][entry][lane]: one 128-bit load, conflict-free
   double xch[2][2][kTbWarps][kTbV];  // [iteration parity][first / last own lane][warp][entry]
-  double lane_acc[kTbKMax][2][kTbWarps][32];  // per lane and iteration: ||x_{k+1}||_1, ||r_k||^2
+  double2 lane_acc[kTbKMax][kTbWarps][32];  // per lane and iteration: (||x_{k+1}||_1, ||r_k||^2), one 128-bit access
   double cnt[kTbWarps][kTbKMax][2];           // per warp and iteration: nnz, mismatches
   double beta[kTbKMax];
   double inv_l, thr;
+  uint64_t nbar[2][2][kTbWarps];  // [slot][first / last own lane][producing warp]: "halo stored" (TB_NSYNC)
+  uint64_t xbar[2];               // [slot]: every warp's halos stored (TB_SPLIT)
   int last;
 };
 
 // One iteration on the warp's window.  xc = x_k (window, halos current);
 // xo = x_{k-1} on entry (own lanes), x_{k+1} on exit; rp = r_{k-1} on entry,
 // r_k on exit (both valid on the own entries +- S).
-template <int S, int PAR, bool F, bool INTERIOR, bool FIRST>
+// STORE: 0 = an iteration that stores no iterate (it < K - 2), -1 = decided
+// from it (the first and the last iterations of a tile).
+template <int S, int PAR, bool F, bool INTERIOR, bool FIRST, int STORE = -1>
 __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int64_t e0, int lane,
                                         int warp, bool lane_valid, const double (&xc)[kTbV],
                                         double (&xo)[kTbV], double (&rp)[kTbV], unsigned& nx) {
@@ -1166,7 +1236,7 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     t[0][i] = xc[i];
     if (FIRST) t[KC - 1][i] = xo[i];
   }
-  wchainv<S, true, INTERIOR, KC, PAR, V, F>(t, e0, n, A.right);
+  wchainv<S, true, INTERIOR, KC, PAR, V, F, F && kTbScaled, F ? kTbSymF : kTbSym>(t, e0, n, A.right);
   double g[1][V], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -1178,28 +1248,55 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     g[0][i] = sg * mul_sub<F>(bt1, rk, bt * rm);
     rp[i] = rk;
   }
-  wchainv<S, false, INTERIOR, 1, PAR, V, F>(g, e0, n, A.right);
+  wchainv<S, false, INTERIOR, 1, PAR, V, F, F && kTbScaled, F ? kTbSymF : kTbSym>(g, e0, n, A.right);
   const double inv_l = sm.inv_l, thr = sm.thr;
   double l1 = 0.0;
   unsigned nz = 0, mis = 0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const double y = F ? __fma_rn(bt, xc[i] - xo[i], xc[i]) : xc[i] + bt * (xc[i] - xo[i]);
+    const double z = F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i];
+#if TB_ISHRINK
+    // soft_threshold and (trial != y) on the bit patterns (neither x nor y is
+    // ever -0: a difference of equal doubles is +0, and so is +0 + -0): five
+    // FP64 instructions of the shrink and its counters become integer ones
+    bool nzp;
+    double v = soft_threshold_bits(z, thr, nzp);
+    l1 += fabs(v);
+    nz += nzp ? 1u : 0u;
+    mis = differing_bits(mis, v, y);  // (only mis != 0 matters: the fixed-point check)
+#else
     // soft_threshold (shrink()) with its two compares reused for nnz: above
     // thr z - thr > 0 and below -thr z + thr < 0 exactly (a difference of
     // distinct doubles never rounds to zero), so v != 0 iff one of them holds
-    const double z = F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i];
     const bool hi = z > thr, lo = z < -thr;
     double v = hi ? z - thr : (lo ? z + thr : 0.0);
     l1 += fabs(v);
     nz += (unsigned)(hi | lo);
     mis += (unsigned)(v != y);
+#endif
     if (!INTERIOR && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
     xo[i] = v;
   }
   const int K = A.K;
-  double* dst = it == K - 1 ? A.out2 : (it == K - 2 && !A.replay) ? A.out1 : nullptr;
-  if (dst && lane_valid) {
+#if TB_SPLIT
+  // split-phase exchange: the halos are stored and the tile's mbarrier is
+  // arrived at (one lane per warp, after __syncwarp) before the iteration's
+  // bookkeeping, which overlaps the other warps' arrival; the wait follows it
+  const int xp = nx & 1;
+  const unsigned xph = (nx >> 1) & 1;
+  if (it + 1 < K) {
+    if (lane == 1 || lane == 30) {
+      double* d = &sm.xch[xp][lane == 30 ? 1 : 0][warp][0];
+#pragma unroll
+      for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(d + i) = make_double2(xo[i], xo[i + 1]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.xbar[xp]);
+  }
+#endif
+  double* dst = STORE == 0 ? nullptr : it == K - 1 ? A.out2 : (it == K - 2 && !A.replay) ? A.out1 : nullptr;
+  if (STORE != 0 && dst && lane_valid) {
     if (INTERIOR || e0 + V <= n) {
       const double a[4] = {xo[0], xo[1], xo[2], xo[3]}, c[4] = {xo[4], xo[5], xo[6], xo[7]};
       st4(dst + e0, a);
@@ -1211,28 +1308,62 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     }
   }
   if (lane_valid) {
-    sm.lane_acc[it][0][warp][lane] += l1;
-    sm.lane_acc[it][1][warp][lane] += rr;
+    double2 acc = sm.lane_acc[it][warp][lane];
+    acc.x += l1;
+    acc.y += rr;
+    sm.lane_acc[it][warp][lane] = acc;
   }
   nz = __reduce_add_sync(kFull, lane_valid ? nz : 0u);
+#if TB_ISHRINK
+  mis = __any_sync(kFull, lane_valid && mis != 0u) ? 1u : 0u;
+#else
   mis = __reduce_add_sync(kFull, lane_valid ? mis : 0u);
+#endif
   if (lane == 0) {
     sm.cnt[warp][it][0] += (double)nz;
     sm.cnt[warp][it][1] += (double)mis;
   }
+#if TB_SPLIT
+  if (it + 1 < K) {
+    ++nx;
+    mbar_wait(&sm.xbar[xp], xph);
+    if ((lane == 0 && warp > 0) || (lane == 31 && warp + 1 < kTbWarps)) {
+      const double* q = lane == 0 ? &sm.xch[xp][1][warp - 1][0] : &sm.xch[xp][0][warp + 1][0];
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const double2 w = *reinterpret_cast<const double2*>(q + i);
+        xo[i] = w.x, xo[i + 1] = w.y;
+      }
+    }
+    return;
+  }
+#endif
   if (it + 1 < K) {
     // halo exchange for the next iteration (slot parity alternates: one
     // block barrier per exchange)
     const int p = nx & 1;
+#if TB_NSYNC
+    // each warp waits for its two neighbours only (an mbarrier per warp,
+    // side and slot, completed by the storing lane: release / acquire), so
+    // the warps of a tile drift up to one iteration apart instead of meeting
+    // at a block barrier.  Slot s is stored again two exchanges later, after
+    // this warp has consumed the neighbour's next halo, which the neighbour
+    // stored after reading slot s: one phase in flight per barrier.
+    const unsigned ph = (nx >> 1) & 1;
     ++nx;
     if (lane == 1) {
 #pragma unroll
       for (int i = 0; i < V; ++i) sm.xch[p][0][warp][i] = xo[i];
+      mbar_arrive(&sm.nbar[p][0][warp]);
     } else if (lane == 30) {
 #pragma unroll
       for (int i = 0; i < V; ++i) sm.xch[p][1][warp][i] = xo[i];
+      mbar_arrive(&sm.nbar[p][1][warp]);
     }
-    __syncthreads();
+    __syncwarp();
+    // (the whole warp waits: no divergent spin loop)
+    if (warp > 0) mbar_wait(&sm.nbar[p][1][warp - 1], ph);
+    if (warp + 1 < kTbWarps) mbar_wait(&sm.nbar[p][0][warp + 1], ph);
     if (lane == 0 && warp > 0) {
 #pragma unroll
       for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][1][warp - 1][i];
@@ -1240,6 +1371,24 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
 #pragma unroll
       for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][0][warp + 1][i];
     }
+#else
+    ++nx;
+    // (one store / load sequence for both sides: the side picks the address)
+    if (lane == 1 || lane == 30) {
+      double* d = &sm.xch[p][lane == 30 ? 1 : 0][warp][0];
+#pragma unroll
+      for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(d + i) = make_double2(xo[i], xo[i + 1]);
+    }
+    __syncthreads();
+    if ((lane == 0 && warp > 0) || (lane == 31 && warp + 1 < kTbWarps)) {
+      const double* q = lane == 0 ? &sm.xch[p][1][warp - 1][0] : &sm.xch[p][0][warp + 1][0];
+#pragma unroll
+      for (int i = 0; i < V; i += 2) {
+        const double2 w = *reinterpret_cast<const double2*>(q + i);
+        xo[i] = w.x, xo[i + 1] = w.y;
+      }
+    }
+#endif
   }
 }
 
@@ -1273,18 +1422,41 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
         bb[i] = in ? A.b[e0 + i] : 0.0;
       }
     }
+    // (scaled form: sigma carries prod cos(theta) of the chain it multiplies --
+    // r = (sigma C) (M^T x) - b and u = (sigma C) w, so G u = M (sigma C w))
+    const double cs = F && kTbScaled ? A.right.cprod : 1.0;
 #pragma unroll
-    for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(sg[i], bb[i]);
+    for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(F && kTbScaled ? sg[i] * cs : sg[i], bb[i]);
   }
+#if TB_PREFETCH
+  {
+    // this CTA's next tile: its four input lines pulled into L2 now, K
+    // iterations before they are loaded (64 B per lane and array)
+    const int64_t en = e0 + (int64_t)gridDim.x * A.valid;
+    if (en >= 0 && en + V <= n) {
+      prefetch_l2(A.x_k + en);
+      prefetch_l2(A.x_km1 + en);
+      prefetch_l2(A.sigma + en);
+      prefetch_l2(A.b + en);
+    }
+  }
+#endif
   __syncwarp();
   const int K = A.K;
   tb_step<S, PAR, F, INTERIOR, true>(A, sm, 0, e0, lane, warp, lane_valid, xa, xb, rp, nx);  // x_{k+1} in xb
+  // iterations 1 .. K-3 store nothing (their instantiation carries no store
+  // logic); the last two (and whatever a replay's K leaves) decide from `it`
   int it = 1;
-  for (; it + 1 < K; it += 2) {
-    tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
-    tb_step<S, PAR, F, INTERIOR, false>(A, sm, it + 1, e0, lane, warp, lane_valid, xa, xb, rp, nx);
+  for (; it + 3 < K; it += 2) {
+    tb_step<S, PAR, F, INTERIOR, false, 0>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
+    tb_step<S, PAR, F, INTERIOR, false, 0>(A, sm, it + 1, e0, lane, warp, lane_valid, xa, xb, rp, nx);
   }
-  if (it < K) tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
+  for (; it < K; ++it) {
+    if (it & 1)
+      tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xb, xa, rp, nx);
+    else
+      tb_step<S, PAR, F, INTERIOR, false>(A, sm, it, e0, lane, warp, lane_valid, xa, xb, rp, nx);
+  }
 }
 
 template <int S, int PAR, bool F>
@@ -1311,8 +1483,17 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
     }
     sm.inv_l = 1.0 / st->lval;
     sm.thr = st->tau * sm.inv_l;
+#if TB_NSYNC
+    for (int q = 0; q < 4 * kTbWarps; ++q) mbar_init(&sm.nbar[0][0][0] + q, 1);
+    fence_mbar_init();
+#endif
+#if TB_SPLIT
+    mbar_init(&sm.xbar[0], kTbWarps);
+    mbar_init(&sm.xbar[1], kTbWarps);
+    fence_mbar_init();
+#endif
   }
-  for (int q = threadIdx.x; q < kTbKMax * 2 * kTbWarps * 32; q += kTbThreads) (&sm.lane_acc[0][0][0][0])[q] = 0.0;
+  for (int q = threadIdx.x; q < kTbKMax * 2 * kTbWarps * 32; q += kTbThreads) (&sm.lane_acc[0][0][0].x)[q] = 0.0;
   for (int q = threadIdx.x; q < kTbWarps * kTbKMax * 2; q += kTbThreads) (&sm.cnt[0][0][0])[q] = 0.0;
   __syncthreads();
   unsigned nx = 0;  // exchanges so far (the same count in every warp)
@@ -1333,7 +1514,7 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
       for (int w = 0; w < kTbWarps; ++w) s += sm.cnt[w][i][c - 1];
     } else {
       for (int w = 0; w < kTbWarps; ++w)
-        for (int l = 0; l < 32; ++l) s += sm.lane_acc[i][c == 0 ? 0 : 1][w][l];
+        for (int l = 0; l < 32; ++l) s += c == 0 ? sm.lane_acc[i][w][l].x : sm.lane_acc[i][w][l].y;
     }
     part[(size_t)blockIdx.x * 4 * K + q] = s;
   }
@@ -1540,6 +1721,8 @@ bool tb_enabled(uint64_t n, int stages) {
   if (stages < 1 || stages > 4 || (e && e[0] == '0')) return false;
   return (e && e[0] == '2') || n > (1ull << 20);  // (<= 2^20: fista_rc_loop)
 }
+
+bool tb_arith_ok(const StageTab& t) { return !kTbScaled || t.scaled_ok != 0; }
 
 // iterations per tile launch (L1B_TB_K, read per session): K = 2 (mod 4)
 // keeps the x rotation of the two-iteration kernel (a launch from x_j writes

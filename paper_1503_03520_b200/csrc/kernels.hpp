@@ -249,7 +249,10 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
 // scratch of fista_tb_scratch(K) doubles.  replay: the same iterations from
 // the launch's snapshot of t / beta_y without any bookkeeping, only out2
 // written (a stop inside the launch: x of the stopping iteration).  One device.
-constexpr int kTbKMax = 14;
+#ifndef TB_KMAX
+#define TB_KMAX 14
+#endif
+constexpr int kTbKMax = TB_KMAX;
 void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* out2, int K, bool replay,
                     double* tb, cudaStream_t st, bool fma);
 uint64_t fista_tb_scratch();
@@ -258,6 +261,7 @@ void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid);
 double fp64_peak_tflops(int device);
 // n from which the tile kernel runs (L1B_TB=0: never; L1B_TB_K: iterations per launch)
 bool tb_enabled(uint64_t n, int stages);
+bool tb_arith_ok(const StageTab& t);  // contracted arithmetic: the tile kernel's rotation form applies
 int tb_iters();
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op, bool fma = false);

@@ -323,7 +323,10 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->trace = (FistaSample*)s->valloc(s->cap * sizeof(FistaSample));
   s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
   L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
-  if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count)) {
+  // (contracted arithmetic: the tile kernel rotates in the scaled form, which
+  // needs |cos(theta)| >= 1/4 in every stage; else the two-iteration kernel)
+  if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count) &&
+      (!s->fma() || tb_arith_ok(v.op->right))) {
     s->tbk = tb_iters();
     s->tb = s->dalloc(fista_tb_scratch());
   }

@@ -38,7 +38,12 @@ def _check(d):
         assert k in d, k
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] > 0
     r = d["roofline"]
-    assert r["bound"] == "hbm" and r["achieved"] > 0 and r["peak"] > 0 and r["unit"] == "GB/s"
+    # (the tile kernel, n > 2^20 on one GPU, is bound by the FP64 pipe and says so;
+    # its HBM side rides along in r["hbm"])
+    assert r["achieved"] > 0 and r["peak"] > 0
+    assert (r["bound"], r["unit"]) in (("hbm", "GB/s"), ("fp64", "TFLOP/s"))
+    if r["bound"] == "fp64":
+        assert r["hbm"]["unit"] == "GB/s" and r["hbm"]["achieved"] > 0 and r["hbm"]["peak"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
 
