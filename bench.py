@@ -198,9 +198,11 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
             "launch_ms_source": "CUDA events around every launch of the timed region",
             "launch_ms_long_run": ms_long, "achieved_long_run": flops / (ms_long * 1e-3) / 1e12,
             "traffic": traffic,
-            "limiter": ("FP64 pipe and issue latency: ncu shows the FP64 pipe 51.5 % busy, 1.95 IPC, DRAM 11.8 % "
-                        "(profiles/r2_ncu_full_fista_tb.txt); the pipe also executes the shrink's compares and "
-                        "the halo entries' work (own 240 of 256 per warp window, kept 1712 of 1920 per tile)"),
+            "limiter": ("instruction issue at IPC 2.06 (issue slots 51.6 % busy, FP64 pipe 44.8 %): per iteration a "
+                        "thread issues ~315 instructions for its 8 entries, 148 of them FP64; stalls: fixed-latency "
+                        "dependencies, shuffle / shared-memory latency, the block barrier of the halo exchange "
+                        "(profiles/r2_ncu_full_fista_tb3.txt, fma build); DRAM 6.43 GB per launch = 1.00 x 48n; the "
+                        "pipe also carries the halo entries' work (own 240 of 256 per warp window, kept 1712 of 1920 per tile)"),
             "hbm": {"achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
                     "frac": byts / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": byts},
             "hbm_gbs_ax_atr": byts / (ms * 1e-3) / 1e9}
@@ -375,11 +377,13 @@ def main():
     # e2e before the CSR/CSC copy exists (37 GB of device memory at C4)
     e2e_line = e2e_more = None
     if not args.no_e2e:
-        e2e_line = e2e(inst, args.steps, local)
-        e2e_more = {"serving_resident_operator": e2e(inst, args.steps, local, serving=True)}
+        other = "exact" if args.arith == "fma" else "fma"
+        e2e_line = e2e(inst, args.steps, local, arith=args.arith)
+        e2e_more = {"serving_resident_operator": e2e(inst, args.steps, local, serving=True, arith=args.arith),
+                    f"arith_{other}": e2e(inst, args.steps, local, arith=other)}
         if args.steps != C4_ITERS:  # the C4 run's own length beside the requested K
-            e2e_more[f"k{C4_ITERS}"] = e2e(inst, C4_ITERS, local)
-            e2e_more[f"k{C4_ITERS}_serving"] = e2e(inst, C4_ITERS, local, serving=True)
+            e2e_more[f"k{C4_ITERS}"] = e2e(inst, C4_ITERS, local, arith=args.arith)
+            e2e_more[f"k{C4_ITERS}_serving"] = e2e(inst, C4_ITERS, local, serving=True, arith=args.arith)
     if args.no_sparse:
         print(json.dumps({"metric": METRIC, "value": fused["ips"], "ms_per_step": fused["ms_step"],
                           "arith": args.arith, "roofline": rf, "clocks": clk.summary(),
@@ -463,12 +467,14 @@ def small_configs():
     return out
 
 
-def e2e(inst, steps, device, serving=False):
+def e2e(inst, steps, device, serving=False, arith="fma"):
     """Same metric through the public API from HOST buffers, every pass:
     upload sigma, b, x* (from_host -> l1b_problem_create), run K iterations
     (l1b_solve, default operator path) and copy x back -- all inside the timed
     region.  serving=True: the operator (sigma, stages) stays resident and a
-    pass uploads only b (l1b_problem_set_rhs) before the solve."""
+    pass uploads only b (l1b_problem_set_rhs) before the solve.  arith: the
+    l1b_solver_cfg.arith of the solve (the headline's; the other mode rides
+    along in e2e_more)."""
     import torch
 
     from paper_1503_03520_b200 import l1bench
@@ -497,7 +503,7 @@ def e2e(inst, steps, device, serving=False):
         else:
             p = l1bench.ProblemInstance.from_host(m, n, stages, g["sigma"], g["b"], tau, g["xs"].support,
                                                   g["xs"].values, device=device)
-        tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=steps), x)
+        tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=steps, arith=arith), x)
         torch.cuda.synchronize()
         if rep:
             times.append(time.perf_counter() - t0)
@@ -506,7 +512,7 @@ def e2e(inst, steps, device, serving=False):
     t = sorted(times)[len(times) // 2]  # median
     h2d = 8 * m + (0 if serving else 8 * n + 12 * len(g["xs"].support))
     d2h = 8 * n + 48 * len(tr.samples)
-    return {"value": steps / t, "unit": UNIT, "steps": steps, "h2d_bytes_per_step": h2d / steps,
+    return {"value": steps / t, "unit": UNIT, "steps": steps, "arith": arith, "h2d_bytes_per_step": h2d / steps,
             "d2h_bytes_per_step": d2h / steps, "seconds": t, "seconds_passes": times,
             "includes": ("H2D of b from pinned host memory into the resident operator (l1b_problem_set_rhs), "
                          if serving else

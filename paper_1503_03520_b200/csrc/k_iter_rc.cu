@@ -1168,6 +1168,9 @@ constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
 #ifndef TB_PREFETCH
 #define TB_PREFETCH 1  // L2 prefetch of the CTA's next tile
 #endif
+#ifndef TB_GACC
+#define TB_GACC 0  // 1: per-lane accumulators in global memory (frees 56 KB of shared memory per CTA)
+#endif
 #ifndef TB_SPLIT
 #define TB_SPLIT 0  // 1: split-phase halo exchange on a tile mbarrier (arrive before the bookkeeping, wait after it)
 #endif
@@ -1178,7 +1181,10 @@ constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
 #define TB_SYM 1  // exact arithmetic: each lane forms its own output of a straddling pair (one shuffle deep; +0.5 %; the scaled form measured 1 % slower that way)
 #endif
 constexpr bool kTbScaled = TB_SCALED != 0, kTbSym = TB_SYM != 0, kTbSymF = TB_SYM == 2;
-constexpr int kTbCtas = 512 / kTbThreads;  // resident CTAs per SM (128 registers per thread)
+#ifndef TB_CTAS
+#define TB_CTAS (512 / (32 * TB_WARPS))
+#endif
+constexpr int kTbCtas = TB_CTAS;  // resident CTAs per SM (default: 128 registers per thread)
 template <int S>
 struct TbGeom {
   static constexpr int W = 32 * kTbV;
@@ -1201,6 +1207,7 @@ struct TbArgs {
   FistaDev* st;
   FistaSample* trace;
   double* partials;  // gridDim.x * 4K per-CTA sums, then the 4K totals
+  double2* lacc;     // TB_GACC: the per-lane (l1, ||r||^2) accumulators [CTA][iteration][thread] in global memory
   int64_t valid, ntiles;
   int K, E, replay;
 };
@@ -1208,7 +1215,9 @@ struct TbArgs {
 struct TbSmem {
   double2 sb[kTbWarps][kTbV][32];  // (sigma, b) by [warp][entry][lane]: one 128-bit load, conflict-free
   double xch[2][2][kTbWarps][kTbV];  // [iteration parity][first / last own lane][warp][entry]
+#if !TB_GACC
   double2 lane_acc[kTbKMax][kTbWarps][32];  // per lane and iteration: (||x_{k+1}||_1, ||r_k||^2), one 128-bit access
+#endif
   double cnt[kTbWarps][kTbKMax][2];           // per warp and iteration: nnz, mismatches
   double beta[kTbKMax];
   double inv_l, thr;
@@ -1308,10 +1317,18 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     }
   }
   if (lane_valid) {
+#if TB_GACC
+    double2* slot = A.lacc + ((size_t)blockIdx.x * kTbKMax + it) * kTbThreads + threadIdx.x;
+    double2 acc = *slot;
+    acc.x += l1;
+    acc.y += rr;
+    *slot = acc;
+#else
     double2 acc = sm.lane_acc[it][warp][lane];
     acc.x += l1;
     acc.y += rr;
     sm.lane_acc[it][warp][lane] = acc;
+#endif
   }
   nz = __reduce_add_sync(kFull, lane_valid ? nz : 0u);
 #if TB_ISHRINK
@@ -1493,7 +1510,12 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
     fence_mbar_init();
 #endif
   }
+#if TB_GACC
+  for (int i = 0; i < kTbKMax; ++i)  // (each thread its own slots)
+    A.lacc[((size_t)blockIdx.x * kTbKMax + i) * kTbThreads + threadIdx.x] = make_double2(0.0, 0.0);
+#else
   for (int q = threadIdx.x; q < kTbKMax * 2 * kTbWarps * 32; q += kTbThreads) (&sm.lane_acc[0][0][0].x)[q] = 0.0;
+#endif
   for (int q = threadIdx.x; q < kTbWarps * kTbKMax * 2; q += kTbThreads) (&sm.cnt[0][0][0])[q] = 0.0;
   __syncthreads();
   unsigned nx = 0;  // exchanges so far (the same count in every warp)
@@ -1514,7 +1536,14 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
       for (int w = 0; w < kTbWarps; ++w) s += sm.cnt[w][i][c - 1];
     } else {
       for (int w = 0; w < kTbWarps; ++w)
-        for (int l = 0; l < 32; ++l) s += c == 0 ? sm.lane_acc[i][w][l].x : sm.lane_acc[i][w][l].y;
+        for (int l = 0; l < 32; ++l) {
+#if TB_GACC
+          const double2 a = A.lacc[((size_t)blockIdx.x * kTbKMax + i) * kTbThreads + w * 32 + l];
+#else
+          const double2 a = sm.lane_acc[i][w][l];
+#endif
+          s += c == 0 ? a.x : a.y;
+        }
     }
     part[(size_t)blockIdx.x * 4 * K + q] = s;
   }
@@ -1691,6 +1720,7 @@ void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* 
   a.st = ib.st;
   a.trace = ib.trace;
   a.partials = tb;
+  a.lacc = reinterpret_cast<double2*>(tb + (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax);
   a.K = K;
   a.replay = replay ? 1 : 0;
   switch (op.right.count * 2 + (fma ? 1 : 0)) {
@@ -1711,7 +1741,10 @@ void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid) {
   *valid = *span - 2 * tb_erosion(stages, K);
 }
 
-uint64_t fista_tb_scratch() { return (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax; }
+uint64_t fista_tb_scratch() {
+  const uint64_t partials = (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax;
+  return partials + (TB_GACC ? (uint64_t)4 * sm_count() * kTbKMax * kTbThreads * 2 : 0);
+}
 
 // the tile kernel above 2^20 entries (smaller instances run whole chunks of
 // iterations in one cooperative launch); L1B_TB=0 switches it off

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "guard.hpp"
@@ -31,6 +32,39 @@ void run_newton_cg(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* sample
 void run_fista_backtracking(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, uint64_t cap,
                             l1b_summary* summary, double* x_host, double* d_x);
 }  // namespace l1b
+
+// Small page-locked blocks (the stop flags and the state read back at the end
+// of a solve), cached for the process: cudaMallocHost / cudaFreeHost are
+// heavyweight driver calls (page locking, device-wide synchronisation) that a
+// solve should not pay on every call.
+constexpr size_t kPinnedBlock = 4096;
+struct PinnedCache {
+  std::mutex m;
+  std::vector<void*> free_;
+  void* get() {
+    {
+      std::lock_guard<std::mutex> g(m);
+      if (!free_.empty()) {
+        void* p = free_.back();
+        free_.pop_back();
+        return p;
+      }
+    }
+    void* p = nullptr;
+    L1B_CUDA(cudaMallocHost(&p, kPinnedBlock));
+    return p;
+  }
+  void put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(m);
+    free_.push_back(p);
+  }
+};
+PinnedCache& pinned_cache() {
+  static PinnedCache* c = new PinnedCache();  // (never destroyed: no driver calls at exit)
+  return *c;
+}
+void pinned_release(void* p) { pinned_cache().put(p); }
 
 struct l1b_session {
   l1b_problem* prob = nullptr;
@@ -114,16 +148,22 @@ struct l1b_session {
   bool fma() const { return cfg.arith == L1B_ARITH_FMA; }
 
   // tile kernel (K iterations per launch, one device): tbk = K (0: off),
-  // tb = its per-CTA sums, tb_starts = j of every launch (a stop inside one is
+  // tb = its per-CTA sums, tb_starts = (j, K) of every launch (a stop inside one is
   // replayed from its inputs, which no later launch overwrites)
   int tbk = 0;
   double* tb = nullptr;
-  std::vector<uint64_t> tb_starts;
+  std::vector<std::pair<uint64_t, int>> tb_starts;
 
-  void iteratek(uint64_t j, cudaStream_t stream) {
-    const int K = tbk;
+  void iteratek(uint64_t j, cudaStream_t stream, int K = 0) {
+    if (K == 0) K = tbk;
     fista_rc_iterk(*v.op, iter_bufs(j), X[(j + K - 1) % 4], X[(j + K) % 4], K, false, tb, stream, fma());
-    tb_starts.push_back(j);
+    tb_starts.emplace_back(j, K);
+  }
+  // the longest tile launch a remainder of r iterations takes (K = 2 mod 4
+  // keeps the rotation of the x buffers; below 6 the two-iteration kernel)
+  static int tile_remainder(uint64_t r) {
+    if (r < 6) return 0;
+    return (int)(r - (r + 2) % 4);
   }
 
   void iterate2(uint64_t j, cudaStream_t stream) const {
@@ -168,7 +208,7 @@ struct l1b_session {
     for (double* q : x_raw) cudaFree(q);
     for (void* q : allocs) cudaFreeAsync(q, v.stream);  // back to the stream-ordered pool
     if (v.stream) cudaStreamSynchronize(v.stream);
-    if (h_st) cudaFreeHost(h_st);
+    if (h_st) pinned_release(h_st);
   }
   std::vector<void*> allocs;
   // stream-ordered allocations from the device pool (kept cached between
@@ -322,7 +362,8 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->cap = sample_capacity(cfg->max_iters);
   s->trace = (FistaSample*)s->valloc(s->cap * sizeof(FistaSample));
   s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
-  L1B_CUDA(cudaMallocHost(&s->h_st, sizeof(FistaDev)));
+  static_assert(sizeof(FistaDev) <= kPinnedBlock, "FistaDev outgrew the pinned block");
+  s->h_st = (FistaDev*)pinned_cache().get();
   // (contracted arithmetic: the tile kernel rotates in the scaled form, which
   // needs |cos(theta)| >= 1/4 in every stage; else the two-iteration kernel)
   if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count) &&
@@ -382,6 +423,7 @@ bool persist_enabled() {
 
 // Large single-device instances run two iterations per launch (24n instead
 // of 40n bytes per iteration); L1B_RC2=0 keeps one per launch.
+
 bool rc2_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -396,8 +438,13 @@ bool rc2_enabled() {
 bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
   if (!(s->recompute && !s->shard && rc2_enabled())) return false;
   uint64_t i = 0;
-  if (s->tbk)
+  if (s->tbk) {
     for (; i + (uint64_t)s->tbk <= iters; i += (uint64_t)s->tbk) s->iteratek(s->launched + i, st);
+    if (const int kr = l1b_session::tile_remainder(iters - i)) {  // one shorter tile launch
+      s->iteratek(s->launched + i, st, kr);
+      i += (uint64_t)kr;
+    }
+  }
   for (; i + 2 <= iters; i += 2) s->iterate2(s->launched + i, st);
   if (i < iters) s->iterate(s->launched + i, st);
   return true;
@@ -465,9 +512,9 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
   // a tile launch stores only its last two iterates: a stop before those is
   // replayed from the launch's inputs (same operations: the same x)
   for (auto it = s->tb_starts.rbegin(); it != s->tb_starts.rend(); ++it) {
-    const uint64_t j = *it;
+    const uint64_t j = it->first;
     if (h.k <= j) continue;
-    if (h.k + 1 < j + (uint64_t)s->tbk) {
+    if (h.k + 1 < j + (uint64_t)it->second) {
       double* dst = s->X[(j + 1) % 4];
       fista_rc_iterk(*s->v.op, s->iter_bufs(j), nullptr, dst, (int)(h.k - j), true, s->tb, st, s->fma());
       xf = dst;
@@ -791,8 +838,13 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
         else if (i + K <= iters)
           s->iterate2(s->launched + i, st);
         L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
-        if (i + K > iters) {  // the remainder: two-iteration launches (+ one single)
+        if (i + K > iters) {  // the remainder: a shorter tile launch, two-iteration launches (+ one single)
           uint64_t r = i;
+          if (s->tbk)
+            if (const int kr = l1b_session::tile_remainder(iters - r)) {
+              s->iteratek(s->launched + r, st, kr);
+              r += (uint64_t)kr;
+            }
           for (; r + 2 <= iters; r += 2) s->iterate2(s->launched + r, st);
           if (r < iters) s->iterate(s->launched + r, st);
         }
@@ -923,12 +975,12 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
       tp = now;
     };
     int* h_flags = nullptr;
-    L1B_CUDA(cudaMallocHost(&h_flags, 2 * sizeof(int)));
+    h_flags = (int*)pinned_cache().get();
     l1b_session s;
     try {
       session_begin(p, cfg, &s);
     } catch (...) {
-      cudaFreeHost(h_flags);
+      pinned_cache().put(h_flags);
       throw;
     }
     ptrace("session begun");
@@ -940,7 +992,9 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
     int slot = 0;
     // small instances run whole chunks in one launch (fista_rc_loop): start at
     // the full chunk, each launch costs a reload of the instance
-    uint64_t chunk = uses_loop(&s) ? 64 : 4;
+    // (tile sessions: chunks of whole K-iteration launches)
+    const uint64_t tk = (uint64_t)s.tbk;
+    uint64_t chunk = uses_loop(&s) ? 64 : tk ? tk : 4;
     try {
       while (s.launched < cfg->max_iters) {
         // loop-head time check (solvers.cpp:314), at chunk granularity
@@ -961,19 +1015,19 @@ int l1b_solve(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_sample* samples, ui
           pending[slot] = false;
           if (h_flags[slot]) break;
         }
-        chunk = std::min<uint64_t>(chunk * 2, 64);
+        chunk = std::min<uint64_t>(chunk * 2, tk ? 4 * tk : 64);
       }
       L1B_CUDA(cudaStreamSynchronize(st));
       ptrace("iterations done");
     } catch (...) {
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
-      cudaFreeHost(h_flags);
+      pinned_cache().put(h_flags);
       throw;
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
-    cudaFreeHost(h_flags);
+    pinned_cache().put(h_flags);
     session_finish(&s, samples, cap, summary, x_host, d_x);
     ptrace("finished");
   });

@@ -6,6 +6,7 @@ from paper_1503_03520_b200 import l1bench
 from bench import C4
 torch.cuda.set_device(0)
 inst = l1bench.build_instance(device=0, lazy_sparse=True, **C4)
+ARITH = sys.argv[2] if len(sys.argv) > 2 else "fma"
 sig, b, xs = inst.sigma(), inst.b, inst.x_star
 m, n = inst.m, inst.n
 stages = [((4 - 1 - i) % 2, C4["theta"]) for i in range(4)]
@@ -20,7 +21,7 @@ for rep in range(6):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     p = l1bench.ProblemInstance.from_host(m, n, stages, psig, pb, inst.tau, xs.support, xs.values, device=0)
     torch.cuda.synchronize(); t1 = time.perf_counter()
-    tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=K), px)
+    tr = l1bench.fista_run(p, l1bench.SolverConfig(max_iters=K, arith=ARITH), px)
     torch.cuda.synchronize(); t2 = time.perf_counter()
     del p
     torch.cuda.synchronize(); t3 = time.perf_counter()

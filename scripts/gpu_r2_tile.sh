@@ -13,3 +13,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:fist
   python scripts/tile_one.py fma > gpurun_out/ncu_tb.log 2>&1; echo "exit $?" >> gpurun_out/ncu_tb.log
 ncu -i gpurun_out/r2_fista_tb.ncu-rep --page details > gpurun_out/r2_ncu_full_fista_tb.txt 2>&1
 ncu -i gpurun_out/r2_fista_tb.ncu-rep --page source --csv > gpurun_out/r2_fista_tb_source.csv 2>&1
+L1B_SOLVE_TRACE=1 timeout 600 python scripts/e2e_probe.py 500 fma > gpurun_out/e2e_probe.log 2>&1
