@@ -574,6 +574,8 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const double y = F ? __fma_rn(beta_a, d.xk[i] - d.xm[i], d.xk[i]) : d.xk[i] + beta_a * (d.xk[i] - d.xm[i]);
+    // (the FP64 compares of shrink() here; the tile kernel takes the same values from the
+    // bit patterns, soft_threshold_bits -- measured neutral in this kernel: 1996 vs 2002 iter/s)
     double v = shrink(F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i], thr);
     l1 += mine[i] ? fabs(v) : 0.0;
     acc.nza += (unsigned)(mine[i] & (v != 0.0));
@@ -1159,32 +1161,12 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
 // persistent (one per SM), tiles strided by the grid; the per-iteration sums
 // are accumulated per warp in shared memory and folded in a fixed order.
 constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
-#ifndef TB_SCALED
-#define TB_SCALED 1  // contracted arithmetic: rotations in the scaled form (0: lifting, as in the two-iteration kernel)
-#endif
-#ifndef TB_ISHRINK
-#define TB_ISHRINK 1  // shrink and its counters on the bit patterns
-#endif
-#ifndef TB_PREFETCH
-#define TB_PREFETCH 1  // L2 prefetch of the CTA's next tile
-#endif
-#ifndef TB_GACC
-#define TB_GACC 0  // 1: per-lane accumulators in global memory (frees 56 KB of shared memory per CTA)
-#endif
-#ifndef TB_SPLIT
-#define TB_SPLIT 0  // 1: split-phase halo exchange on a tile mbarrier (arrive before the bookkeeping, wait after it)
-#endif
-#ifndef TB_NSYNC
-#define TB_NSYNC 0  // 1: halo exchange between neighbouring warps on mbarriers instead of one block barrier per iteration (measured slower: 2120 vs 2477 iter/s)
-#endif
-#ifndef TB_SYM
-#define TB_SYM 1  // exact arithmetic: each lane forms its own output of a straddling pair (one shuffle deep; +0.5 %; the scaled form measured 1 % slower that way)
-#endif
-constexpr bool kTbScaled = TB_SCALED != 0, kTbSym = TB_SYM != 0, kTbSymF = TB_SYM == 2;
-#ifndef TB_CTAS
-#define TB_CTAS (512 / (32 * TB_WARPS))
-#endif
-constexpr int kTbCtas = TB_CTAS;  // resident CTAs per SM (default: 128 registers per thread)
+// contracted arithmetic: rotations in the scaled form (the two-iteration
+// kernel keeps the lifting form).  Exact arithmetic: each lane forms its own
+// output of a straddling pair (one shuffle deep, +0.5 %; the scaled form
+// measured 1 % slower that way and shuffles the rotated value back instead).
+constexpr bool kTbScaled = true, kTbSym = true, kTbSymF = false;
+constexpr int kTbCtas = 512 / kTbThreads;  // resident CTAs per SM (128 registers per thread)
 template <int S>
 struct TbGeom {
   static constexpr int W = 32 * kTbV;
@@ -1207,7 +1189,6 @@ struct TbArgs {
   FistaDev* st;
   FistaSample* trace;
   double* partials;  // gridDim.x * 4K per-CTA sums, then the 4K totals
-  double2* lacc;     // TB_GACC: the per-lane (l1, ||r||^2) accumulators [CTA][iteration][thread] in global memory
   int64_t valid, ntiles;
   int K, E, replay;
 };
@@ -1215,14 +1196,10 @@ struct TbArgs {
 struct TbSmem {
   double2 sb[kTbWarps][kTbV][32];  // (sigma, b) by [warp][entry][lane]: one 128-bit load, conflict-free
   double xch[2][2][kTbWarps][kTbV];  // [iteration parity][first / last own lane][warp][entry]
-#if !TB_GACC
   double2 lane_acc[kTbKMax][kTbWarps][32];  // per lane and iteration: (||x_{k+1}||_1, ||r_k||^2), one 128-bit access
-#endif
   double cnt[kTbWarps][kTbKMax][2];           // per warp and iteration: nnz, mismatches
   double beta[kTbKMax];
   double inv_l, thr;
-  uint64_t nbar[2][2][kTbWarps];  // [slot][first / last own lane][producing warp]: "halo stored" (TB_NSYNC)
-  uint64_t xbar[2];               // [slot]: every warp's halos stored (TB_SPLIT)
   int last;
 };
 
@@ -1265,7 +1242,6 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
   for (int i = 0; i < V; ++i) {
     const double y = F ? __fma_rn(bt, xc[i] - xo[i], xc[i]) : xc[i] + bt * (xc[i] - xo[i]);
     const double z = F ? __fma_rn(-inv_l, g[0][i], y) : y - inv_l * g[0][i];
-#if TB_ISHRINK
     // soft_threshold and (trial != y) on the bit patterns (neither x nor y is
     // ever -0: a difference of equal doubles is +0, and so is +0 + -0): five
     // FP64 instructions of the shrink and its counters become integer ones
@@ -1274,36 +1250,10 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     l1 += fabs(v);
     nz += nzp ? 1u : 0u;
     mis = differing_bits(mis, v, y);  // (only mis != 0 matters: the fixed-point check)
-#else
-    // soft_threshold (shrink()) with its two compares reused for nnz: above
-    // thr z - thr > 0 and below -thr z + thr < 0 exactly (a difference of
-    // distinct doubles never rounds to zero), so v != 0 iff one of them holds
-    const bool hi = z > thr, lo = z < -thr;
-    double v = hi ? z - thr : (lo ? z + thr : 0.0);
-    l1 += fabs(v);
-    nz += (unsigned)(hi | lo);
-    mis += (unsigned)(v != y);
-#endif
     if (!INTERIOR && (e0 + i < 0 || e0 + i >= n)) v = 0.0;
     xo[i] = v;
   }
   const int K = A.K;
-#if TB_SPLIT
-  // split-phase exchange: the halos are stored and the tile's mbarrier is
-  // arrived at (one lane per warp, after __syncwarp) before the iteration's
-  // bookkeeping, which overlaps the other warps' arrival; the wait follows it
-  const int xp = nx & 1;
-  const unsigned xph = (nx >> 1) & 1;
-  if (it + 1 < K) {
-    if (lane == 1 || lane == 30) {
-      double* d = &sm.xch[xp][lane == 30 ? 1 : 0][warp][0];
-#pragma unroll
-      for (int i = 0; i < V; i += 2) *reinterpret_cast<double2*>(d + i) = make_double2(xo[i], xo[i + 1]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.xbar[xp]);
-  }
-#endif
   double* dst = STORE == 0 ? nullptr : it == K - 1 ? A.out2 : (it == K - 2 && !A.replay) ? A.out1 : nullptr;
   if (STORE != 0 && dst && lane_valid) {
     if (INTERIOR || e0 + V <= n) {
@@ -1317,78 +1267,21 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
     }
   }
   if (lane_valid) {
-#if TB_GACC
-    double2* slot = A.lacc + ((size_t)blockIdx.x * kTbKMax + it) * kTbThreads + threadIdx.x;
-    double2 acc = *slot;
-    acc.x += l1;
-    acc.y += rr;
-    *slot = acc;
-#else
     double2 acc = sm.lane_acc[it][warp][lane];
     acc.x += l1;
     acc.y += rr;
     sm.lane_acc[it][warp][lane] = acc;
-#endif
   }
   nz = __reduce_add_sync(kFull, lane_valid ? nz : 0u);
-#if TB_ISHRINK
   mis = __any_sync(kFull, lane_valid && mis != 0u) ? 1u : 0u;
-#else
-  mis = __reduce_add_sync(kFull, lane_valid ? mis : 0u);
-#endif
   if (lane == 0) {
     sm.cnt[warp][it][0] += (double)nz;
     sm.cnt[warp][it][1] += (double)mis;
   }
-#if TB_SPLIT
-  if (it + 1 < K) {
-    ++nx;
-    mbar_wait(&sm.xbar[xp], xph);
-    if ((lane == 0 && warp > 0) || (lane == 31 && warp + 1 < kTbWarps)) {
-      const double* q = lane == 0 ? &sm.xch[xp][1][warp - 1][0] : &sm.xch[xp][0][warp + 1][0];
-#pragma unroll
-      for (int i = 0; i < V; i += 2) {
-        const double2 w = *reinterpret_cast<const double2*>(q + i);
-        xo[i] = w.x, xo[i + 1] = w.y;
-      }
-    }
-    return;
-  }
-#endif
   if (it + 1 < K) {
     // halo exchange for the next iteration (slot parity alternates: one
     // block barrier per exchange)
     const int p = nx & 1;
-#if TB_NSYNC
-    // each warp waits for its two neighbours only (an mbarrier per warp,
-    // side and slot, completed by the storing lane: release / acquire), so
-    // the warps of a tile drift up to one iteration apart instead of meeting
-    // at a block barrier.  Slot s is stored again two exchanges later, after
-    // this warp has consumed the neighbour's next halo, which the neighbour
-    // stored after reading slot s: one phase in flight per barrier.
-    const unsigned ph = (nx >> 1) & 1;
-    ++nx;
-    if (lane == 1) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) sm.xch[p][0][warp][i] = xo[i];
-      mbar_arrive(&sm.nbar[p][0][warp]);
-    } else if (lane == 30) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) sm.xch[p][1][warp][i] = xo[i];
-      mbar_arrive(&sm.nbar[p][1][warp]);
-    }
-    __syncwarp();
-    // (the whole warp waits: no divergent spin loop)
-    if (warp > 0) mbar_wait(&sm.nbar[p][1][warp - 1], ph);
-    if (warp + 1 < kTbWarps) mbar_wait(&sm.nbar[p][0][warp + 1], ph);
-    if (lane == 0 && warp > 0) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][1][warp - 1][i];
-    } else if (lane == 31 && warp + 1 < kTbWarps) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) xo[i] = sm.xch[p][0][warp + 1][i];
-    }
-#else
     ++nx;
     // (one store / load sequence for both sides: the side picks the address)
     if (lane == 1 || lane == 30) {
@@ -1405,7 +1298,6 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
         xo[i] = w.x, xo[i + 1] = w.y;
       }
     }
-#endif
   }
 }
 
@@ -1445,7 +1337,6 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
 #pragma unroll
     for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(F && kTbScaled ? sg[i] * cs : sg[i], bb[i]);
   }
-#if TB_PREFETCH
   {
     // this CTA's next tile: its four input lines pulled into L2 now, K
     // iterations before they are loaded (64 B per lane and array)
@@ -1457,7 +1348,6 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
       prefetch_l2(A.b + en);
     }
   }
-#endif
   __syncwarp();
   const int K = A.K;
   tb_step<S, PAR, F, INTERIOR, true>(A, sm, 0, e0, lane, warp, lane_valid, xa, xb, rp, nx);  // x_{k+1} in xb
@@ -1500,22 +1390,8 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
     }
     sm.inv_l = 1.0 / st->lval;
     sm.thr = st->tau * sm.inv_l;
-#if TB_NSYNC
-    for (int q = 0; q < 4 * kTbWarps; ++q) mbar_init(&sm.nbar[0][0][0] + q, 1);
-    fence_mbar_init();
-#endif
-#if TB_SPLIT
-    mbar_init(&sm.xbar[0], kTbWarps);
-    mbar_init(&sm.xbar[1], kTbWarps);
-    fence_mbar_init();
-#endif
   }
-#if TB_GACC
-  for (int i = 0; i < kTbKMax; ++i)  // (each thread its own slots)
-    A.lacc[((size_t)blockIdx.x * kTbKMax + i) * kTbThreads + threadIdx.x] = make_double2(0.0, 0.0);
-#else
   for (int q = threadIdx.x; q < kTbKMax * 2 * kTbWarps * 32; q += kTbThreads) (&sm.lane_acc[0][0][0].x)[q] = 0.0;
-#endif
   for (int q = threadIdx.x; q < kTbWarps * kTbKMax * 2; q += kTbThreads) (&sm.cnt[0][0][0])[q] = 0.0;
   __syncthreads();
   unsigned nx = 0;  // exchanges so far (the same count in every warp)
@@ -1537,11 +1413,7 @@ __global__ void __launch_bounds__(kTbThreads, kTbCtas) fista_tb_kernel(TbArgs A)
     } else {
       for (int w = 0; w < kTbWarps; ++w)
         for (int l = 0; l < 32; ++l) {
-#if TB_GACC
-          const double2 a = A.lacc[((size_t)blockIdx.x * kTbKMax + i) * kTbThreads + w * 32 + l];
-#else
           const double2 a = sm.lane_acc[i][w][l];
-#endif
           s += c == 0 ? a.x : a.y;
         }
     }
@@ -1720,7 +1592,6 @@ void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* 
   a.st = ib.st;
   a.trace = ib.trace;
   a.partials = tb;
-  a.lacc = reinterpret_cast<double2*>(tb + (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax);
   a.K = K;
   a.replay = replay ? 1 : 0;
   switch (op.right.count * 2 + (fma ? 1 : 0)) {
@@ -1741,10 +1612,7 @@ void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid) {
   *valid = *span - 2 * tb_erosion(stages, K);
 }
 
-uint64_t fista_tb_scratch() {
-  const uint64_t partials = (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax;
-  return partials + (TB_GACC ? (uint64_t)4 * sm_count() * kTbKMax * kTbThreads * 2 : 0);
-}
+uint64_t fista_tb_scratch() { return (uint64_t)(4 * sm_count() + 1) * 4 * kTbKMax; }
 
 // the tile kernel above 2^20 entries (smaller instances run whole chunks of
 // iterations in one cooperative launch); L1B_TB=0 switches it off

@@ -249,10 +249,7 @@ void fista_rc_iter2(const OpView& op, const IterBufs& ib, double* x_next2, uint6
 // scratch of fista_tb_scratch(K) doubles.  replay: the same iterations from
 // the launch's snapshot of t / beta_y without any bookkeeping, only out2
 // written (a stop inside the launch: x of the stopping iteration).  One device.
-#ifndef TB_KMAX
-#define TB_KMAX 14
-#endif
-constexpr int kTbKMax = TB_KMAX;
+constexpr int kTbKMax = 14;
 void fista_rc_iterk(const OpView& op, const IterBufs& ib, double* out1, double* out2, int K, bool replay,
                     double* tb, cudaStream_t st, bool fma);
 uint64_t fista_tb_scratch();
