@@ -1160,13 +1160,16 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
 // Per entry the operations are segment2v's: identical iterates.  CTAs are
 // persistent (one per SM), tiles strided by the grid; the per-iteration sums
 // are accumulated per warp in shared memory and folded in a fixed order.
-constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = 8;
+#ifndef TB_V
+#define TB_V 8  // entries per lane
+#endif
+constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = TB_V;
 // contracted arithmetic: rotations in the scaled form (the two-iteration
 // kernel keeps the lifting form).  Exact arithmetic: each lane forms its own
 // output of a straddling pair (one shuffle deep, +0.5 %; the scaled form
 // measured 1 % slower that way and shuffles the rotated value back instead).
 constexpr bool kTbScaled = true, kTbSym = true, kTbSymF = false;
-constexpr int kTbCtas = 512 / kTbThreads;  // resident CTAs per SM (128 registers per thread)
+constexpr int kTbCtas = (kTbV <= 8 ? 512 : 256) / kTbThreads;  // resident CTAs per SM (128 registers per thread at 8 entries per lane)
 template <int S>
 struct TbGeom {
   static constexpr int W = 32 * kTbV;
@@ -1175,7 +1178,7 @@ struct TbGeom {
   static constexpr int SPAN = kTbWarps * OWN;
   static_assert(2 * S <= H, "halo narrower than two chain runs");
 };
-constexpr int tb_erosion(int S, int K) { return (2 * S * (K - 1) + 7) / 8 * 8; }
+constexpr int tb_erosion(int S, int K) { return (2 * S * (K - 1) + kTbV - 1) / kTbV * kTbV; }
 
 struct TbArgs {
   int64_t n;
@@ -1257,9 +1260,11 @@ __device__ __forceinline__ void tb_step(const TbArgs& A, TbSmem& sm, int it, int
   double* dst = STORE == 0 ? nullptr : it == K - 1 ? A.out2 : (it == K - 2 && !A.replay) ? A.out1 : nullptr;
   if (STORE != 0 && dst && lane_valid) {
     if (INTERIOR || e0 + V <= n) {
-      const double a[4] = {xo[0], xo[1], xo[2], xo[3]}, c[4] = {xo[4], xo[5], xo[6], xo[7]};
-      st4(dst + e0, a);
-      st4(dst + e0 + 4, c);
+#pragma unroll
+      for (int j = 0; j < V; j += 4) {
+        const double a[4] = {xo[j], xo[j + 1], xo[j + 2], xo[j + 3]};
+        st4(dst + e0 + j, a);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < V; ++i)
@@ -1309,7 +1314,7 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
   const int64_t n = A.n;
   const int64_t w0 = t0 - A.E + (int64_t)warp * G::OWN - G::H;
   const int64_t e0 = w0 + V * lane;
-  // validity is per lane: t0, VALID, E, OWN and H are multiples of 8, so a
+  // validity is per lane: t0, VALID, E, OWN and H are multiples of V, so a
   // tile's kept range starts and ends on lane boundaries; entries past n are
   // zero in every array and contribute nothing to the sums
   const bool lane_valid = lane >= 1 && lane <= 30 && e0 >= t0 && e0 + V <= t0 + A.valid && e0 < n;
@@ -1342,10 +1347,13 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
     // iterations before they are loaded (64 B per lane and array)
     const int64_t en = e0 + (int64_t)gridDim.x * A.valid;
     if (en >= 0 && en + V <= n) {
-      prefetch_l2(A.x_k + en);
-      prefetch_l2(A.x_km1 + en);
-      prefetch_l2(A.sigma + en);
-      prefetch_l2(A.b + en);
+#pragma unroll
+      for (int j = 0; j < V; j += 8) {
+        prefetch_l2(A.x_k + en + j);
+        prefetch_l2(A.x_km1 + en + j);
+        prefetch_l2(A.sigma + en + j);
+        prefetch_l2(A.b + en + j);
+      }
     }
   }
   __syncwarp();

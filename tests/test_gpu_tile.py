@@ -184,3 +184,57 @@ def test_tile_session_steps_and_profile():
     np.testing.assert_array_equal(x, x2)
     assert tr.iterations == 57
     assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
+
+
+@pytest.mark.parametrize("iters", [24, 27, 34, 41])
+def test_remainder_runs_as_a_shorter_tile_launch(oracle, iters):
+    """K = 14: 24 = 14 + 10, 27 = 14 + 10 + 2 + 1, 34 = 2 x 14 + 6, 41 = 2 x 14 + 10 + 2 + 1 --
+    the remainder takes one shorter tile launch (K = 2 mod 4), then two-iteration
+    and single launches: the oracle's iterates bit for bit, and a target met
+    inside the shorter launch is replayed from that launch's own inputs."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(n=150001, stages=4, q=1, s_divisor=100, seed=7, theta=TH)
+    inst = l1bench.build_instance(**kw)
+    tr, x = _solve(inst, True, 14, max_iters=iters)
+    assert tr.ran("fista_tile") and tr.iterations == iters
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+    np.testing.assert_array_equal(x, ox)
+    assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
+    # a stop three iterations before the end: inside the last tile launch or after it
+    f, it = tr.objectives(), list(tr.iters())
+    stop_at = iters - 3
+    target = float(f[it.index(stop_at)] * (1 + 1e-9))
+    if all(v > target for v in f[:it.index(stop_at)]):
+        tr1, x1 = _solve(inst, True, 14, max_iters=iters, target_objective=target)
+        tr2, x2 = _solve(inst, False, max_iters=iters, target_objective=target)
+        assert tr1.iterations == tr2.iterations == stop_at
+        assert tr1.status == tr2.status == l1bench.StopReason.target_reached
+        np.testing.assert_array_equal(x1, x2)
+
+
+def test_ista_on_tiles(oracle):
+    """ISTA (no momentum: beta = 0 in every iteration of a launch) through the
+    tile kernel: the oracle's ista iterates bit for bit."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    kw = dict(n=60013, stages=3, q=1, s_divisor=100, seed=9, theta=TH)
+    inst = l1bench.build_instance(**kw)
+    env = {"L1B_TB": "2", "L1B_TB_K": "10"}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        x = np.empty(inst.n)
+        tr = l1bench.ista_run(inst, l1bench.SolverConfig(op="matrix_free", max_iters=37), x)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    assert tr.ran("fista_tile"), tr.path
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=37, accelerated=False)
+    np.testing.assert_array_equal(x, ox)
+    assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
