@@ -203,6 +203,10 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
                         "dependencies, shuffle / shared-memory latency, the block barrier of the halo exchange "
                         "(profiles/r2_ncu_full_fista_tb3.txt, fma build); DRAM 6.43 GB per launch = 1.00 x 48n; the "
                         "pipe also carries the halo entries' work (own 240 of 256 per warp window, kept 1712 of 1920 per tile)"),
+            "note": ("temporal blocking took the HBM bytes out of the iteration (48n bytes per 14 iterations instead "
+                     "of per 2): this kernel is not HBM-bound, so its roofline is the FP64 one and roofline.hbm only "
+                     "records how little of the memory system it needs; the HBM-bound two-iteration kernel (L1B_TB=0, "
+                     "the sharded runs) reaches 0.93-1.00 of the measured copy bandwidth at 1870-2000 iter/s"),
             "hbm": {"achieved": byts / (ms * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
                     "frac": byts / (ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_launch": byts},
             "hbm_gbs_ax_atr": byts / (ms * 1e-3) / 1e9}

@@ -21,6 +21,7 @@ These run minutes of single-threaded reference CPU work (C4: ~20 GB of host
 memory); the GPU box has the cores and memory for them."""
 import ctypes
 import math
+import os
 import threading
 
 import numpy as np
@@ -169,24 +170,40 @@ def test_c4_generator_bit_exact(c4):
 
 
 def test_c4_first_iterations_match_fista_run(c4):
+    """C4 itself (n = 2^27) against the reference's own fista_run, 16
+    iterations: the tile kernel (one launch of 14 iterations, then a
+    two-iteration launch) and the two-iteration kernel alone (L1B_TB=0), each
+    in the exact arithmetic (the reference's bits) and in the contracted one
+    (<= 1e-12, same support)."""
     from paper_1503_03520_b200 import l1bench
 
     inst, ri = c4
-    iters = 4
+    iters = 16
     rtr, rx = ri.solve("fista", max_iters=iters)
-    x = np.empty(inst.n)
-    tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters), x)
-    assert tr.ran("fista_two_iter") and not tr.ran("fma"), f"path={tr.path:#x}"
-    np.testing.assert_array_equal(x, rx)
-    np.testing.assert_array_equal(tr.iters(), rtr["iter"])
-    np.testing.assert_array_equal([s.nnz for s in tr.samples], rtr["nnz"])
-    assert rel_err(tr.objectives(), rtr["objective"]) < 1e-12
-    xf = np.empty(inst.n)
-    tf = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, arith="fma"), xf)
-    assert tf.ran("fista_two_iter") and tf.ran("fma"), f"path={tf.path:#x}"
-    assert rel_err(xf, rx) < 1e-12
-    assert rel_err(tf.objectives(), rtr["objective"]) < 1e-12
-    np.testing.assert_array_equal(np.nonzero(xf)[0], np.nonzero(rx)[0])
+
+    def run(tile, arith):
+        old = os.environ.get("L1B_TB")
+        os.environ["L1B_TB"] = "1" if tile else "0"
+        try:
+            x = np.empty(inst.n)
+            tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, arith=arith), x)
+        finally:
+            if old is None:
+                del os.environ["L1B_TB"]
+            else:
+                os.environ["L1B_TB"] = old
+        assert tr.ran("fista_tile") == tile and tr.ran("fista_two_iter"), f"path={tr.path:#x}"
+        assert tr.ran("fma") == (arith == "fma"), f"path={tr.path:#x}"
+        np.testing.assert_array_equal(tr.iters(), rtr["iter"])
+        assert rel_err(tr.objectives(), rtr["objective"]) < 1e-12
+        np.testing.assert_array_equal([s.nnz for s in tr.samples], rtr["nnz"])
+        return x
+
+    for tile in (True, False):
+        np.testing.assert_array_equal(run(tile, "exact"), rx)
+        xf = run(tile, "fma")
+        assert rel_err(xf, rx) < 1e-12
+        np.testing.assert_array_equal(np.nonzero(xf)[0], np.nonzero(rx)[0])
 
 
 # ---------------------------------------------------------------- C5 ------
