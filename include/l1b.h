@@ -295,6 +295,8 @@ enum { L1B_OP_AUTO = 0, L1B_OP_SPARSE = 1, L1B_OP_MATRIX_FREE = 2 };
 enum { L1B_L_SPECTRUM = 0, L1B_L_BACKTRACKING = 1 };
 enum { L1B_ARITH_EXACT = 0, L1B_ARITH_FMA = 1 };
 
+/* SolverConfig's defaults (solvers.hpp:19-38); arith = L1B_ARITH_EXACT unless the
+   environment says L1B_ARITH=fma (for callers without a field for it: the drop-in) */
 void l1b_solver_cfg_default(l1b_solver_cfg* cfg);
 
 /* TraceSample (solvers.hpp:45-52) */

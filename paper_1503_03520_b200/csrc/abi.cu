@@ -1368,6 +1368,11 @@ void l1b_solver_cfg_default(l1b_solver_cfg* c) {
   c->varpi = 1;
   c->block = 256;
   c->op = L1B_OP_AUTO;
+  // L1B_ARITH=fma: the contracted arithmetic as the default of callers that
+  // have no field for it (the reference-side drop-in maps l1bench::SolverConfig,
+  // which knows no arithmetic mode, onto these defaults)
+  const char* e = getenv("L1B_ARITH");
+  c->arith = (e && (std::strcmp(e, "fma") == 0 || std::strcmp(e, "1") == 0)) ? L1B_ARITH_FMA : L1B_ARITH_EXACT;
 }
 
 }  // extern "C"

@@ -80,3 +80,27 @@ def test_invalid_arguments_map_to_value_error():
         l1bench.SolverConfig(id="bogus").to_c()
     with pytest.raises(ValueError):
         l1bench.build_instance(1)  # ExperimentConfig: dimensions must be at least 2
+
+
+def test_solver_cfg_default_takes_the_arithmetic_from_the_environment():
+    """l1b_solver_cfg_default (SolverConfig's defaults, solvers.hpp:19-38): the
+    reference's bits unless L1B_ARITH=fma -- the switch of callers without a
+    field for the mode (the reference-side drop-in)."""
+    from paper_1503_03520_b200 import _native as N
+
+    lib = N.load()
+    old = os.environ.pop("L1B_ARITH", None)
+    try:
+        c = N.SolverCfg()
+        lib.l1b_solver_cfg_default(ctypes.byref(c))
+        assert c.arith == 0 and c.max_iters == 100000 and c.block == 256
+        os.environ["L1B_ARITH"] = "fma"
+        lib.l1b_solver_cfg_default(ctypes.byref(c))
+        assert c.arith == 1
+        os.environ["L1B_ARITH"] = "exact"
+        lib.l1b_solver_cfg_default(ctypes.byref(c))
+        assert c.arith == 0
+    finally:
+        os.environ.pop("L1B_ARITH", None)
+        if old is not None:
+            os.environ["L1B_ARITH"] = old
