@@ -285,10 +285,12 @@ typedef struct {
                           reference's bits; L1B_ARITH_FMA: the matrix-free FISTA kernels of
                           instances with n > 2^20 contract a*b+c into one fused multiply-add
                           (one rounding: <= 1e-12 relative to the reference, not bit-exact).
-                          The tile kernel (single device) rotates in the scaled form there --
-                          cos(theta) [[1, -tan], [tan, 1]] with prod cos carried by sigma; it
-                          needs |cos(theta)| >= 1/4 in every stage, else the two-iteration
-                          kernel's lifting form runs.  Other paths ignore it */
+                          The tile and two-iteration kernels rotate in the scaled form there --
+                          cos(theta) [[1, -tan], [tan, 1]] with prod cos carried by sigma (the
+                          same operations per entry in both: a sharded run gives the single
+                          device's bits); it needs |cos(theta)| >= 1/4 in every stage, else the
+                          request is declined (exact arithmetic, L1B_RAN_FMA not set).  Other
+                          paths ignore it */
 } l1b_solver_cfg;
 
 enum { L1B_OP_AUTO = 0, L1B_OP_SPARSE = 1, L1B_OP_MATRIX_FREE = 2 };

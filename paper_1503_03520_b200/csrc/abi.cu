@@ -184,6 +184,7 @@ struct l1b_problem {
   uint32_t *d_p1 = nullptr, *d_p2 = nullptr, *d_p1inv = nullptr, *d_p2inv = nullptr;
   double* d_b = nullptr;
   double* d_gram = nullptr;
+  double* d_sigma_c = nullptr;  // sigma * prod cos(theta): the contracted arithmetic's scaled rotations (lazily built)
   std::vector<uint32_t> xs_sup;
   std::vector<double> xs_val;
   double noise_norm = 0.0, cert_kappa = 1.0, lmax = 0.0;
@@ -214,7 +215,7 @@ struct l1b_problem {
     // them would hand the pages back to the driver and the next problem of the
     // same size would map them again (the e2e passes varied 0.38 - 0.6 s)
     for (void* p : {(void*)d_sigma, (void*)d_p1, (void*)d_p2, (void*)d_p1inv, (void*)d_p2inv, (void*)d_b,
-                    (void*)d_b_win, (void*)d_gram})
+                    (void*)d_b_win, (void*)d_gram, (void*)d_sigma_c})
       if (p) cudaFreeAsync(p, stream);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : {csr.ptr, (void*)csr.idx, (void*)csr.val, csc.ptr, (void*)csc.idx, (void*)csc.val,
@@ -1417,4 +1418,17 @@ ProblemView problem_view(l1b_problem* p, bool need_sparse) {
   return v;
 }
 const double* problem_gram(l1b_problem* p) { return gram_diag_device(p); }
+
+// sigma * prod cos(theta_s) over the right stages, indexed like view.sigma
+// (global index; a shard: its window): the sigma of the contracted kernels,
+// whose rotations run in the scaled form (StageTab::cprod, k_iter_rc.cu)
+const double* problem_sigma_scaled(l1b_problem* p) {
+  const uint64_t lo = p->sig_end ? p->sig_begin : 0, hi = p->sig_end ? p->sig_end : p->n;
+  if (!p->d_sigma_c) {
+    L1B_CUDA(cudaSetDevice(p->device));
+    p->d_sigma_c = dev_alloc<double>(hi - lo, &p->device_bytes, p->stream);
+    scale_copy(p->d_sigma, p->view.right.cprod, p->d_sigma_c, hi - lo, p->stream);
+  }
+  return p->d_sigma_c - lo;
+}
 }  // namespace l1b

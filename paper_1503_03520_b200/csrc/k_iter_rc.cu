@@ -559,7 +559,9 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
     t[0][i] = d.xk[i];
     t[1][i] = d.xm[i];
   }
-  wchainv<S, true, FAST, 2, PAR, V, F>(t, e0, n, A.right);
+  // (F: the scaled form, A.sigma = sigma * prod cos(theta) -- the tile kernel's
+  // operations entry for entry, so the two kernels agree bit for bit)
+  wchainv<S, true, FAST, 2, PAR, V, F, F>(t, e0, n, A.right);
   double rk[V], g[1][V], rr = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -569,7 +571,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
     g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_a, rk[i], beta_a * rm);
   }
   acc.rr0 += rr;
-  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
+  wchainv<S, false, FAST, 1, PAR, V, F, F>(g, e0, n, A.right);
   double x1[1][V], l1 = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -589,7 +591,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
   double t1[1][V];
 #pragma unroll
   for (int i = 0; i < V; ++i) t1[0][i] = x1[0][i];
-  wchainv<S, true, FAST, 1, PAR, V, F>(t1, e0, n, A.right);
+  wchainv<S, true, FAST, 1, PAR, V, F, F>(t1, e0, n, A.right);
   double rr1 = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -598,7 +600,7 @@ __device__ __forceinline__ void segment2v(const RcArgs& A, const Rc2Out& O, cons
     g[0][i] = d.sg[i] * mul_sub<F>(1.0 + beta_b, r1, beta_b * rk[i]);
   }
   acc.rr1 += rr1;
-  wchainv<S, false, FAST, 1, PAR, V, F>(g, e0, n, A.right);
+  wchainv<S, false, FAST, 1, PAR, V, F, F>(g, e0, n, A.right);
   double x2[V], l1b = 0.0;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
@@ -1336,11 +1338,11 @@ __device__ __forceinline__ void tb_tile(const TbArgs& A, TbSmem& sm, int64_t t0,
         bb[i] = in ? A.b[e0 + i] : 0.0;
       }
     }
-    // (scaled form: sigma carries prod cos(theta) of the chain it multiplies --
-    // r = (sigma C) (M^T x) - b and u = (sigma C) w, so G u = M (sigma C w))
-    const double cs = F && kTbScaled ? A.right.cprod : 1.0;
+    // (contracted arithmetic: A.sigma is sigma * prod cos(theta), the factor
+    // the scaled rotations leave out -- r = (sigma C) (M^T x) - b and
+    // u = (sigma C) w, so G u = M (sigma C w); problem_sigma_scaled)
 #pragma unroll
-    for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(F && kTbScaled ? sg[i] * cs : sg[i], bb[i]);
+    for (int i = 0; i < V; ++i) sm.sb[warp][i][lane] = make_double2(sg[i], bb[i]);
   }
   {
     // this CTA's next tile: its four input lines pulled into L2 now, K
@@ -1630,8 +1632,6 @@ bool tb_enabled(uint64_t n, int stages) {
   if (stages < 1 || stages > 4 || (e && e[0] == '0')) return false;
   return (e && e[0] == '2') || n > (1ull << 20);  // (<= 2^20: fista_rc_loop)
 }
-
-bool tb_arith_ok(const StageTab& t) { return !kTbScaled || t.scaled_ok != 0; }
 
 // iterations per tile launch (L1B_TB_K, read per session): K = 2 (mod 4)
 // keeps the x rotation of the two-iteration kernel (a launch from x_j writes

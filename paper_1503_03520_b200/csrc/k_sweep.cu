@@ -363,6 +363,19 @@ void window_stages(const StageTab& tab, bool forward, bool transposed, double* v
   }
 }
 
+namespace {
+__global__ void scale_copy_kernel(const double* __restrict__ in, double a, double* __restrict__ out, uint64_t len) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] * a;
+}
+}  // namespace
+
+void scale_copy(const double* in, double a, double* out, uint64_t len, cudaStream_t st) {
+  if (!len) return;
+  scale_copy_kernel<<<grid_for(len), kThreads, 0, st>>>(in, a, out, len);
+  L1B_LAUNCHED();
+}
+
 void window_scale_op(double* v, const double* sig, uint64_t len, int mode, double tau,
                      cudaStream_t st) {
   if (!len) return;

@@ -112,6 +112,8 @@ void certificate(const double* r, const double* xd, double tau, uint64_t n, doub
 void window_stages(const StageTab& tab, bool forward, bool transposed, double* v, uint64_t ws,
                    uint64_t we, uint64_t dim, cudaStream_t st);
 // mode 0: v /= sig^2, 1: v = sig * v, 2: v *= tau
+// out[i] = in[i] * a
+void scale_copy(const double* in, double a, double* out, uint64_t len, cudaStream_t st);
 void window_scale_op(double* v, const double* sig, uint64_t len, int mode, double tau,
                      cudaStream_t st);
 
@@ -258,7 +260,6 @@ void fista_tb_geometry(int stages, int K, int64_t* span, int64_t* valid);
 double fp64_peak_tflops(int device);
 // n from which the tile kernel runs (L1B_TB=0: never; L1B_TB_K: iterations per launch)
 bool tb_enabled(uint64_t n, int stages);
-bool tb_arith_ok(const StageTab& t);  // contracted arithmetic: the tile kernel's rotation form applies
 int tb_iters();
 // loads the recomputing kernels and sizes their grids (outside the timed loop)
 void fista_rc_prepare(const OpView& op, bool fma = false);

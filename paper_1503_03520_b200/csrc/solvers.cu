@@ -145,7 +145,13 @@ struct l1b_session {
     return pv;
   }
 
-  bool fma() const { return cfg.arith == L1B_ARITH_FMA; }
+  // contracted arithmetic: honoured where every rotation stage has
+  // |cos(theta)| >= 1/4 (the scaled form of the two-iteration and tile
+  // kernels, StageTab::scaled_ok); steeper stages keep the exact arithmetic.
+  // opf = the operator with sigma * prod cos(theta) as its sigma (those kernels' view)
+  bool fma() const { return cfg.arith == L1B_ARITH_FMA && v.op->right.scaled_ok != 0; }
+  OpView opf;
+  const OpView& op2() const { return fma() ? opf : *v.op; }
 
   // tile kernel (K iterations per launch, one device): tbk = K (0: off),
   // tb = its per-CTA sums, tb_starts = (j, K) of every launch (a stop inside one is
@@ -156,7 +162,7 @@ struct l1b_session {
 
   void iteratek(uint64_t j, cudaStream_t stream, int K = 0) {
     if (K == 0) K = tbk;
-    fista_rc_iterk(*v.op, iter_bufs(j), X[(j + K - 1) % 4], X[(j + K) % 4], K, false, tb, stream, fma());
+    fista_rc_iterk(op2(), iter_bufs(j), X[(j + K - 1) % 4], X[(j + K) % 4], K, false, tb, stream, fma());
     tb_starts.emplace_back(j, K);
   }
   // the longest tile launch a remainder of r iterations takes (K = 2 mod 4
@@ -168,7 +174,7 @@ struct l1b_session {
 
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
-    fista_rc_iter2(*v.op, iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
+    fista_rc_iter2(op2(), iter_bufs(j), X[(j + 2) % 4] + (int64_t)xh - lo, (uint64_t)lo,
                    shard ? v.row_end : v.n, stream, peers(j), fma());
   }
 
@@ -364,12 +370,13 @@ void session_begin(l1b_problem* p, const l1b_solver_cfg* cfg, l1b_session* s) {
   s->st = (FistaDev*)s->valloc(sizeof(FistaDev));
   static_assert(sizeof(FistaDev) <= kPinnedBlock, "FistaDev outgrew the pinned block");
   s->h_st = (FistaDev*)pinned_cache().get();
-  // (contracted arithmetic: the tile kernel rotates in the scaled form, which
-  // needs |cos(theta)| >= 1/4 in every stage; else the two-iteration kernel)
-  if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count) &&
-      (!s->fma() || tb_arith_ok(v.op->right))) {
+  if (s->recompute && !s->shard && rc2_enabled() && tb_enabled(v.n, (int)v.op->right.count)) {
     s->tbk = tb_iters();
     s->tb = s->dalloc(fista_tb_scratch());
+  }
+  if (s->recompute && s->fma()) {  // sigma * prod cos(theta), built once per problem
+    s->opf = *v.op;
+    s->opf.sigma = problem_sigma_scaled(p);
   }
   if (s->recompute) fista_rc_prepare(*v.op, s->fma());  // module load + grid sizing before t0
   session_reset(s);
@@ -516,7 +523,7 @@ void session_finish(l1b_session* s, l1b_sample* samples, uint64_t cap, l1b_summa
     if (h.k <= j) continue;
     if (h.k + 1 < j + (uint64_t)it->second) {
       double* dst = s->X[(j + 1) % 4];
-      fista_rc_iterk(*s->v.op, s->iter_bufs(j), nullptr, dst, (int)(h.k - j), true, s->tb, st, s->fma());
+      fista_rc_iterk(s->op2(), s->iter_bufs(j), nullptr, dst, (int)(h.k - j), true, s->tb, st, s->fma());
       xf = dst;
     }
     break;

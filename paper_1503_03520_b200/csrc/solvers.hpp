@@ -38,5 +38,6 @@ struct ProblemView {
 
 ProblemView problem_view(l1b_problem* p, bool need_sparse = true);
 const double* problem_gram(l1b_problem* p);  // lazily built diag(A^T A)
+const double* problem_sigma_scaled(l1b_problem* p);  // lazily built sigma * prod cos(theta) (contracted arithmetic)
 
 }  // namespace l1b

@@ -67,10 +67,10 @@ def test_tile_matches_oracle_and_two_iteration_kernel(oracle, n, stages, k):
 @pytest.mark.parametrize("n,stages", [(1 << 20 | 4099, 4), (1 << 21, 3)])
 def test_tile_default_at_large_n_fma(oracle, n, stages):
     """Above 2^20 the tile kernel is the default.  In the contracted arithmetic
-    it rotates in the scaled form (two independent fmas per pair, prod cos
-    carried by sigma), the two-iteration kernel in the lifting form: both within
-    1e-12 of the oracle's fista_run restatement and of each other, same
-    supports."""
+    both it and the two-iteration kernel rotate in the scaled form (two
+    independent fmas per pair, prod cos carried by sigma) with the same
+    operations per entry: bit-identical to each other, within 1e-12 of the
+    oracle's fista_run restatement, same supports."""
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
@@ -79,15 +79,16 @@ def test_tile_default_at_large_n_fma(oracle, n, stages):
     tr, x = _solve(inst, None, max_iters=40, arith="fma")
     assert tr.ran("fista_tile") and tr.ran("fma"), tr.path
     tr2, x2 = _solve(inst, False, max_iters=40, arith="fma")
-    assert not tr2.ran("fista_tile")
+    assert not tr2.ran("fista_tile") and tr2.ran("fma")
+    np.testing.assert_array_equal(x, x2)
+    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-13
     otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=40)
-    scale = np.max(np.abs(ox))
-    assert np.max(np.abs(x - ox)) < 1e-12 * scale and np.max(np.abs(x - x2)) < 1e-12 * scale
+    assert np.max(np.abs(x - ox)) < 1e-12 * np.max(np.abs(ox))
     np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(ox)[0])
     assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
-    assert rel_err(tr.objectives(), tr2.objectives()) < 1e-12
     np.testing.assert_array_equal([s.nnz for s in tr.samples], otr["nnz"])
     assert tr.iterations == tr2.iterations == 40
+
 
 
 @pytest.mark.parametrize("n,stages,k", [(100003, 4, 10), (50001, 3, 14), (20005, 2, 6), (7777, 1, 10),
@@ -113,22 +114,23 @@ def test_tile_fma_scaled_rotations_match_oracle(oracle, n, stages, k):
     np.testing.assert_array_equal([s.nnz for s in tr.samples], otr["nnz"])
 
 
-def test_tile_fma_declines_steep_rotations(oracle):
-    """|cos(theta)| < 1/4: the scaled form is not used -- the contracted
-    arithmetic keeps the two-iteration kernel (lifting form); the exact
-    arithmetic still runs on tiles."""
+def test_steep_rotations_keep_the_exact_arithmetic(oracle):
+    """|cos(theta)| < 1/4: the scaled form of the contracted arithmetic is not
+    used -- arith = "fma" is declined (flag not set) and the exact kernels run:
+    the oracle's iterates bit for bit."""
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
     kw = dict(n=(1 << 20) + 4099, stages=4, q=1, s_divisor=1000, seed=5, theta=0.47 * math.pi)
     inst = l1bench.build_instance(**kw)
     tr, x = _solve(inst, None, max_iters=41, arith="fma")
-    assert tr.ran("fma") and not tr.ran("fista_tile"), tr.path
+    assert tr.ran("fista_tile") and not tr.ran("fma"), tr.path
     otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=41)
-    assert np.max(np.abs(x - ox)) < 1e-12 * np.max(np.abs(ox))
-    tr, x = _solve(inst, None, max_iters=41)
-    assert tr.ran("fista_tile")
     np.testing.assert_array_equal(x, ox)
+    tr2, x2 = _solve(inst, False, max_iters=41, arith="fma")
+    assert not tr2.ran("fista_tile") and not tr2.ran("fma")
+    np.testing.assert_array_equal(x2, ox)
+
 
 
 @pytest.mark.parametrize("stop_at", [11, 12, 13, 17, 18, 19, 20])
