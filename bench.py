@@ -164,7 +164,7 @@ def time_path(inst, op, args, prof_iters=100, arith="exact"):
 
 # FP64 flops per entry and iteration of the matrix-free FISTA step with S
 # stages (fma = 2): the chains G^T x and G u, 3 per entry and stage each
-# (lifting: 3 fma per pair; exact: 4 mul + 2 add per pair), plus r = sigma t - b
+# (the reference's rotation: 4 mul + 2 add per pair), plus r = sigma t - b
 # (2), ||r||^2 (2), u = sigma ((1+beta) r - beta r') (4), y (3), y - g / L (2),
 # the shrink (1) and ||x||_1 (1)
 def flops_per_entry(stages):
@@ -237,8 +237,8 @@ def roofline(path, t, info, peak, peak_src):
             traffic = None
     long_ms = (t["k1_ms_long"] * ipl if dom[3] != "k2" else t["k2_ms_long"])
     if path == "matrix_free" and t.get("kmode") == 4:
-        limiter = ("HBM streaming: ncu shows DRAM 6.42 GB per launch (1.00x algorithmic), the FP64 pipe 52.9 % "
-                   "busy with the lifting rotations (profiles/r2_ncu_full_fista_rc2v_lift.txt)" if t.get("arith") == "fma" else
+        limiter = ("HBM streaming: ncu shows DRAM 6.44 GB per launch (1.00x algorithmic) at 80.5 % of its peak, the "
+                   "FP64 pipe 45.7 % busy with the scaled rotations (profiles/r2_ncu_full_fista_rc2v_scaled.txt)" if t.get("arith") == "fma" else
                    "FP64 issue (separately rounded a*b+c): ncu shows the FP64 pipe at 76.5 % of peak and DRAM "
                    "at ~71 % (profiles/r1_ncu_full_fista_rc2v.txt)")
     else:
