@@ -240,3 +240,34 @@ def test_ista_on_tiles(oracle):
     otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=37, accelerated=False)
     np.testing.assert_array_equal(x, ox)
     assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
+
+
+def test_tile_random_shapes_and_angles(oracle):
+    """Seeded sweep over sizes (ends of [0, n) anywhere inside a tile, n odd and
+    even, smaller than one tile and several tiles long), stage counts, launch
+    lengths and rotation angles (including ones the scaled form declines): the
+    exact arithmetic gives the oracle's bits, the contracted one stays within
+    1e-12 with the same support, and says whether it was applied."""
+    need_cuda()
+    from paper_1503_03520_b200 import l1bench
+
+    rng = np.random.default_rng(20261021)
+    for case in range(14):
+        n = int(rng.integers(300, 9000))
+        stages = int(rng.integers(1, 5))
+        k = int(rng.choice([2, 6, 10, 14]))
+        theta = float(rng.choice([0.3, TH, 1.0, 1.2, 1.4, -0.8, 2.2]))
+        iters = int(rng.integers(k + 1, 3 * k + 6))
+        kw = dict(n=n, stages=stages, q=1, s_divisor=50, seed=100 + case, theta=theta)
+        inst = l1bench.build_instance(**kw)
+        otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+        tr, x = _solve(inst, True, k, max_iters=iters)
+        assert tr.ran("fista_tile"), (kw, k, iters)
+        np.testing.assert_array_equal(x, ox, err_msg=f"{kw} k={k} iters={iters}")
+        assert rel_err(tr.objectives(), otr["objective"]) < 1e-12
+        trf, xf = _solve(inst, True, k, max_iters=iters, arith="fma")
+        assert trf.ran("fista_tile")
+        assert trf.ran("fma") == (abs(math.cos(theta)) >= 0.25), (kw, trf.path)
+        assert np.max(np.abs(xf - ox)) <= 1e-12 * max(np.max(np.abs(ox)), 1e-300), (kw, k, iters)
+        np.testing.assert_array_equal(np.nonzero(xf)[0], np.nonzero(ox)[0])
+        assert rel_err(trf.objectives(), otr["objective"]) < 1e-12
