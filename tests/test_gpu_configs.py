@@ -170,45 +170,61 @@ def test_c4_generator_bit_exact(c4):
 
 
 def test_c4_first_iterations_match_fista_run(c4):
-    """C4 itself (n = 2^27) against the reference's own fista_run, 16
-    iterations: the tile kernel (one launch of 14 iterations, then a
-    two-iteration launch) and the two-iteration kernel alone (L1B_TB=0), each
-    in the exact arithmetic (the reference's bits) and in the contracted one
-    (<= 1e-12, same support)."""
+    """C4 itself (n = 2^27) against the reference's own fista_run, 8
+    iterations (~50 s of reference CPU time): the tile kernel (one launch of 6
+    iterations on chip-resident tiles, then a two-iteration launch) and the
+    two-iteration kernel alone (L1B_TB=0), each in the exact arithmetic (the
+    reference's bits) and in the contracted one (<= 1e-12, same support); then,
+    without the reference, the default 14-iteration tile launch against the
+    two-iteration kernel over 16 iterations, bit for bit in both arithmetics."""
     from paper_1503_03520_b200 import l1bench
 
     inst, ri = c4
-    iters = 16
-    rtr, rx = ri.solve("fista", max_iters=iters)
 
-    def run(tile, arith):
-        old = os.environ.get("L1B_TB")
-        os.environ["L1B_TB"] = "1" if tile else "0"
+    def run(tile, arith, iters, k=None):
+        env = {"L1B_TB": "1" if tile else "0"}
+        if k:
+            env["L1B_TB_K"] = str(k)
+        old = {key: os.environ.get(key) for key in env}
+        os.environ.update(env)
         try:
             x = np.empty(inst.n)
             tr = l1bench.fista_run(inst, l1bench.SolverConfig(max_iters=iters, arith=arith), x)
         finally:
-            if old is None:
-                del os.environ["L1B_TB"]
-            else:
-                os.environ["L1B_TB"] = old
+            for key, v in old.items():
+                if v is None:
+                    del os.environ[key]
+                else:
+                    os.environ[key] = v
         assert tr.ran("fista_tile") == tile and tr.ran("fista_two_iter"), f"path={tr.path:#x}"
         assert tr.ran("fma") == (arith == "fma"), f"path={tr.path:#x}"
-        np.testing.assert_array_equal(tr.iters(), rtr["iter"])
-        assert rel_err(tr.objectives(), rtr["objective"]) < 1e-12
-        np.testing.assert_array_equal([s.nnz for s in tr.samples], rtr["nnz"])
-        return x
+        return tr, x
 
+    iters = 8
+    rtr, rx = ri.solve("fista", max_iters=iters)
     xfs = []
     for tile in (True, False):
-        np.testing.assert_array_equal(run(tile, "exact"), rx)
-        xf = run(tile, "fma")
-        assert rel_err(xf, rx) < 1e-12
-        np.testing.assert_array_equal(np.nonzero(xf)[0], np.nonzero(rx)[0])
-        xfs.append(xf)
+        for arith in ("exact", "fma"):
+            tr, x = run(tile, arith, iters, k=6)
+            np.testing.assert_array_equal(tr.iters(), rtr["iter"])
+            assert rel_err(tr.objectives(), rtr["objective"]) < 1e-12
+            np.testing.assert_array_equal([s.nnz for s in tr.samples], rtr["nnz"])
+            if arith == "exact":
+                np.testing.assert_array_equal(x, rx)
+            else:
+                assert rel_err(x, rx) < 1e-12
+                np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(rx)[0])
+                xfs.append(x)
     # (the same operations per entry in both kernels: the contracted arithmetic too is
     # independent of the launch shape -- and of the row split, which runs the second kernel)
     np.testing.assert_array_equal(xfs[0], xfs[1])
+    del xfs, rx
+    for arith in ("exact", "fma"):
+        tr1, x1 = run(True, arith, 16)
+        tr2, x2 = run(False, arith, 16)
+        np.testing.assert_array_equal(x1, x2)
+        assert rel_err(tr1.objectives(), tr2.objectives()) < 1e-13
+        np.testing.assert_array_equal([s.nnz for s in tr1.samples], [s.nnz for s in tr2.samples])
 
 
 # ---------------------------------------------------------------- C5 ------
