@@ -255,3 +255,48 @@ def test_peer_halos_reproduce_single_device_fista(world, oracle):
     np.testing.assert_array_equal(x, x_ref)
     assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
     oracle_check(oracle, KW, iters, x, outs[0][0].objectives(), exact=True)
+
+
+def test_shards_in_contracted_arithmetic_give_the_tile_kernels_bits(oracle):
+    """n > 2^20, arith = fma: the single device runs the tile kernel (14
+    iterations per launch), the two emulated ranks the two-iteration kernel on
+    their row blocks -- both in the scaled form with the same operations per
+    entry, so the row split changes no bit; within 1e-12 of the oracle."""
+    torch = need_cuda()
+    from paper_1503_03520_b200 import l1bench
+    from paper_1503_03520_b200.distributed import CudaShard
+
+    kw = dict(n=(1 << 20) + 4096, stages=4, q=1, s_divisor=1000, seed=3, theta=2 * math.pi / 10)
+    iters = 30
+    cfg = l1bench.SolverConfig(max_iters=iters, op="matrix_free", arith="fma")
+    inst = l1bench.build_instance(**kw)
+    x_ref = np.empty(inst.n)
+    tr = l1bench.fista_run(inst, cfg, x_ref)
+    assert tr.ran("fista_tile") and tr.ran("fma"), tr.path
+    shards = [CudaShard(kw, r, 2, 0, cfg) for r in range(2)]
+    assert shards[0].single and shards[0].lagged and shards[0].pairs
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    _exchange_many(shards, lambda s: s.initial_halos())
+    for _ in range(iters // 2):  # two iterations per k1
+        for s in shards:
+            s.k1()
+        _exchange_many(shards, lambda s: s.next_halos())
+        _allreduce(shards)
+        for s in shards:
+            s.finalize()
+    for s in shards:
+        s.flush()
+    _allreduce(shards)
+    for s in shards:
+        s.finalize()
+    torch.cuda.synchronize()
+    outs = [s.finish() for s in shards]
+    assert outs[0][0].iterations == iters
+    x = np.concatenate([o[1] for o in outs])
+    np.testing.assert_array_equal(x, x_ref)
+    assert rel_err(outs[0][0].objectives(), tr.objectives()) < 1e-12
+    otr, ox = oracle.fista(oracle.build_instance(**kw), max_iters=iters)
+    assert rel_err(x, ox) < 1e-12
+    np.testing.assert_array_equal(np.nonzero(x)[0], np.nonzero(ox)[0])
