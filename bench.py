@@ -150,15 +150,18 @@ def time_path(inst, op, args, prof_iters=100, arith="exact"):
     kms_long = sess.profile(prof_iters)
     kmode = sess.kernel_mode()
     tile = sess.tile_geometry() if kmode == 6 else None
+    plan, plan_long = (sess.tile_plan(args.steps), sess.tile_plan(prof_iters)) if tile else ([], [])
+    if tile and not (plan and plan_long):  # fewer than 6 iterations: no tile launch ran
+        tile = None
+        kmode = 4
     sess.end()
     out = {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
            "k1_ms": kms[0] / args.steps, "k2_ms": kms[1] / args.steps, "launches": int(launches),
            "k1_ms_long": kms_long[0] / prof_iters, "k2_ms_long": kms_long[1] / prof_iters,
            "kmode": kmode, "arith": arith}
-    if tile:  # profile(): ms[0] = the tile launches, ms[1] = the remainder's launches
-        k = tile[0]
-        out.update(tile=tile, tile_ms=kms[0] / (args.steps // k), tile_ms_long=kms_long[0] / (prof_iters // k),
-                   tile_launches=args.steps // k)
+    if tile:  # profile(): ms[0] = the tile launches, ms[1] = what is left after them
+        out.update(tile=tile, tile_plan=plan, tile_plan_long=plan_long,
+                   tile_ms=kms[0] / len(plan), tile_ms_long=kms_long[0] / len(plan_long), tile_launches=len(plan))
     return out
 
 
@@ -176,7 +179,9 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
     its issue latency, not by HBM: the roofline is FP64 flops per launch over
     the measured fma throughput; the HBM side is reported beside it."""
     n = int(info.n)
-    k, span, valid = t["tile"]
+    kmax, span, valid = t["tile"]
+    plan = t["tile_plan"]
+    k = sum(plan) / len(plan)  # iterations per launch of the timed region (20 = 10 + 10; 500 = 35 x 14 + 10)
     flops = flops_per_entry(stages) * n * k
     # x_k, x_{k-1}, sigma, b read once and two x written per launch (the tiles' overlapping
     # reads, (span - valid) / valid of the four inputs, hit L2: ncu DRAM bytes = 1.00 x 48n)
@@ -190,8 +195,9 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
             traffic = json.load(open(tf)).get("matrix_free:tile" + (":fma" if t.get("arith") == "fma" else ""))
         except Exception:
             traffic = None
-    return {"bound": "fp64", "kernel": f"fista_tb ({k} FISTA iterations per launch on chip-resident tiles of "
+    return {"bound": "fp64", "kernel": f"fista_tb ({kmax} FISTA iterations per launch on chip-resident tiles of "
                                        f"{span} entries, {valid} kept; matrix-free, residuals carried)",
+            "launches": plan if len(plan) <= 8 else f"{plan.count(kmax)} x {kmax} + {[q for q in plan if q != kmax]}",
             "achieved": achieved, "peak": fp64_peak, "peak_source": fp64_src, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak, "flops_per_launch": flops, "flops_per_entry_iteration": flops_per_entry(stages),
             "iterations_per_launch": k, "launch_ms": ms,
@@ -408,9 +414,10 @@ def main():
                                f"4 stages, nnz={info.nnz}, q=1, s=n/1000, tau=1, seed 3",
                    "l2": "inputs larger than L2 (no flush needed)", "parallelism": "single GPU",
                    "path": ("matrix-free (Givens stages in registers + warp shuffles, 256-bit loads); " +
-                            (f"{fused['tile'][0]} FISTA iterations per launch on tiles held on chip (x halos "
+                            (f"{sum(fused['tile_plan']) / len(fused['tile_plan']):g} FISTA iterations per launch "
+                             f"(launches of up to {fused['tile'][0]}) on tiles held on chip (x halos "
                              f"exchanged between warps in shared memory, r_k carried between iterations): "
-                             f"{48.0 / fused['tile'][0]:.2f}n bytes/iteration"
+                             f"{48.0 * len(fused['tile_plan']) / sum(fused['tile_plan']):.2f}n bytes/iteration"
                              if fused["kmode"] == 6 else
                              "two FISTA iterations per launch, residuals recomputed, 24n bytes/iteration"
                              if fused["kmode"] == 4 else "one FISTA iteration per launch") +

@@ -452,6 +452,11 @@ int l1b_session_kernel_mode(l1b_session* s, int* mode);
  * those iterations): HBM bytes per launch = 48 n span / valid.  Other
  * sessions: all three 0.  (No reference counterpart: measurement only.) */
 int l1b_session_tile_geometry(l1b_session* s, int* iters, int64_t* span, int64_t* valid);
+/* The tile launches l1b_session_step / _profile take for `iters` iterations
+ * (each K = 2 mod 4 and at most the session's K, spread evenly: 20 = 10 + 10;
+ * fewer than 6 left over go to two-iteration / single launches): up to `cap`
+ * launch lengths into ks, their number into *count.  (Measurement only.) */
+int l1b_session_tile_plan(l1b_session* s, uint64_t iters, int* ks, int cap, int* count);
 /* Dense FP64 fma throughput of `device` in TFLOP/s (a probe kernel of
  * independent fma chains; measurement only, no reference counterpart): the
  * denominator of the FP64-bound kernels' roofline in bench.py. */

@@ -165,11 +165,26 @@ struct l1b_session {
     fista_rc_iterk(op2(), iter_bufs(j), X[(j + K - 1) % 4], X[(j + K) % 4], K, false, tb, stream, fma());
     tb_starts.emplace_back(j, K);
   }
-  // the longest tile launch a remainder of r iterations takes (K = 2 mod 4
-  // keeps the rotation of the x buffers; below 6 the two-iteration kernel)
-  static int tile_remainder(uint64_t r) {
-    if (r < 6) return 0;
-    return (int)(r - (r + 2) % 4);
+  // The tile launches `iters` iterations take (each K = 2 mod 4, 6 <= K <=
+  // tbk: the rotation of the x buffers; what is left, < 6 iterations, goes to
+  // two-iteration / single launches).  A remainder of 6 or more gets its own
+  // launch and the iterations are spread evenly (20 = 10 + 10, not 14 + 6: a
+  // launch costs a tile start, and a short one keeps less of its tiles).
+  std::vector<int> tile_plan(uint64_t iters) const {
+    std::vector<int> ks;
+    if (!tbk) return ks;
+    const uint64_t kmax = (uint64_t)tbk, kmin = std::min<uint64_t>(6, kmax);  // (K = 2: tests)
+    uint64_t l = iters / kmax + (iters % kmax >= kmin ? 1 : 0), r = iters;
+    for (; l > 0 && r >= kmin; --l) {
+      uint64_t k = std::min((r + l - 1) / l, kmax);
+      const uint64_t down = (k + 2) % 4;  // to the next value = 2 mod 4 below
+      k = k > down ? k - down : kmin;
+      k = std::max(k, kmin);
+      if (k > r) break;
+      ks.push_back((int)k);
+      r -= k;
+    }
+    return ks;
   }
 
   void iterate2(uint64_t j, cudaStream_t stream) const {
@@ -445,12 +460,9 @@ bool rc2_enabled() {
 bool step_pairs(l1b_session* s, uint64_t iters, cudaStream_t st) {
   if (!(s->recompute && !s->shard && rc2_enabled())) return false;
   uint64_t i = 0;
-  if (s->tbk) {
-    for (; i + (uint64_t)s->tbk <= iters; i += (uint64_t)s->tbk) s->iteratek(s->launched + i, st);
-    if (const int kr = l1b_session::tile_remainder(iters - i)) {  // one shorter tile launch
-      s->iteratek(s->launched + i, st, kr);
-      i += (uint64_t)kr;
-    }
+  for (const int k : s->tile_plan(iters)) {
+    s->iteratek(s->launched + i, st, k);
+    i += (uint64_t)k;
   }
   for (; i + 2 <= iters; i += 2) s->iterate2(s->launched + i, st);
   if (i < iters) s->iterate(s->launched + i, st);
@@ -664,6 +676,15 @@ int l1b_session_tile_geometry(l1b_session* s, int* iters, int64_t* span, int64_t
   });
 }
 
+int l1b_session_tile_plan(l1b_session* s, uint64_t iters, int* ks, int cap, int* count) {
+  return guard([&] {
+    if (!s || !count || (cap > 0 && !ks)) throw InvalidArgument("null argument");
+    const std::vector<int> plan = s->tile_plan(iters);
+    *count = (int)plan.size();
+    for (int i = 0; i < cap && i < (int)plan.size(); ++i) ks[i] = plan[(size_t)i];
+  });
+}
+
 int l1b_session_kernel_mode(l1b_session* s, int* mode) {
   return guard([&] {
     if (!s || !mode) throw InvalidArgument("null argument");
@@ -834,38 +855,41 @@ int l1b_session_profile(l1b_session* s, uint64_t iters, double* ms_out, int n_ms
     }
     // tile / two-iteration launches, timed each -- where session_step uses them too
     if (s->recompute && !s->shard && rc2_enabled()) {
-      const uint64_t K = s->tbk ? (uint64_t)s->tbk : 2;
+      // ms_out[0] = the tile launches (tile sessions; else the two-iteration
+      // launches), ms_out[1] = what is left after them (two-iteration / single
+      // launches; empty for sessions without tiles and an even count)
+      const std::vector<int> plan = s->tile_plan(iters);
       uint64_t i = 0;
-      // (tile sessions: ms_out[0] = the tile launches, ms_out[1] = the
-      // remainder's two-iteration / single launches)
-      for (; i < iters; i += K) {
-        L1B_CUDA(cudaEventRecord(ev[3 * i], st));
-        if (i + K <= iters && s->tbk)
-          s->iteratek(s->launched + i, st);
-        else if (i + K <= iters)
-          s->iterate2(s->launched + i, st);
-        L1B_CUDA(cudaEventRecord(ev[3 * i + 1], st));
-        if (i + K > iters) {  // the remainder: a shorter tile launch, two-iteration launches (+ one single)
-          uint64_t r = i;
-          if (s->tbk)
-            if (const int kr = l1b_session::tile_remainder(iters - r)) {
-              s->iteratek(s->launched + r, st, kr);
-              r += (uint64_t)kr;
-            }
-          for (; r + 2 <= iters; r += 2) s->iterate2(s->launched + r, st);
-          if (r < iters) s->iterate(s->launched + r, st);
-        }
-        L1B_CUDA(cudaEventRecord(ev[3 * i + 2], st));
+      size_t e = 0;
+      auto rec = [&] { L1B_CUDA(cudaEventRecord(ev[e++], st)); };
+      std::vector<std::pair<size_t, int>> spans;  // (first event, slot)
+      for (const int k : plan) {
+        spans.emplace_back(e, 0);
+        rec();
+        s->iteratek(s->launched + i, st, k);
+        rec();
+        i += (uint64_t)k;
+      }
+      const int rest_slot = s->tbk ? 1 : 0;
+      for (; i + 2 <= iters; i += 2) {
+        spans.emplace_back(e, rest_slot);
+        rec();
+        s->iterate2(s->launched + i, st);
+        rec();
+      }
+      if (i < iters) {
+        spans.emplace_back(e, 1);
+        rec();
+        s->iterate(s->launched + i, st);
+        rec();
       }
       s->launched += iters;
       L1B_CUDA(cudaStreamSynchronize(st));
-      double k1 = 0.0, k2 = 0.0;  // k2: the empty second slot, as in single-kernel mode
-      for (i = 0; i < iters; i += K) {
-        float a = 0.f, c = 0.f;
-        L1B_CUDA(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
-        L1B_CUDA(cudaEventElapsedTime(&c, ev[3 * i + 1], ev[3 * i + 2]));
-        k1 += a;
-        k2 += c;
+      double k1 = 0.0, k2 = 0.0;
+      for (const auto& sp : spans) {
+        float a = 0.f;
+        L1B_CUDA(cudaEventElapsedTime(&a, ev[sp.first], ev[sp.first + 1]));
+        (sp.second ? k2 : k1) += a;
       }
       for (auto& e : ev) cudaEventDestroy(e);
       ms_out[0] = k1;

@@ -765,6 +765,13 @@ class Session:
         N.check(_lib().l1b_session_tile_geometry(self._s, C.byref(k), C.byref(span), C.byref(valid)))
         return int(k.value), int(span.value), int(valid.value)
 
+    def tile_plan(self, iters: int):
+        """Lengths of the tile launches step(iters) / profile(iters) take."""
+        cap = max(1, int(iters) // 6 + 1)
+        ks, cnt = (C.c_int * cap)(), C.c_int()
+        N.check(_lib().l1b_session_tile_plan(self._s, int(iters), ks, cap, C.byref(cnt)))
+        return [int(ks[i]) for i in range(min(cap, cnt.value))]
+
     def sync(self):
         stopped, k = C.c_int(), C.c_uint64()
         N.check(_lib().l1b_session_sync(self._s, C.byref(stopped), C.byref(k)))

@@ -172,6 +172,10 @@ def test_tile_session_steps_and_profile():
         assert s.kernel_mode() == 6
         k, span, valid = s.tile_geometry()
         assert k == 14 and span % 240 == 0 and valid == span - 2 * 104
+        # launches spread evenly, each K = 2 mod 4; fewer than 6 left over: two-iteration / single launches
+        assert s.tile_plan(20) == [10, 10] and sorted(s.tile_plan(500)) == [10] + [14] * 35
+        assert s.tile_plan(29) == [14, 14] and sorted(s.tile_plan(34)) == [10, 10, 14] and s.tile_plan(27) == [14, 10]
+        assert s.tile_plan(5) == [] and s.tile_plan(6) == [6] and s.tile_plan(14) == [14]
         s.step(3)
         s.profile(30)
         s.step(24)
@@ -190,10 +194,11 @@ def test_tile_session_steps_and_profile():
 
 @pytest.mark.parametrize("iters", [24, 27, 34, 41])
 def test_remainder_runs_as_a_shorter_tile_launch(oracle, iters):
-    """K = 14: 24 = 14 + 10, 27 = 14 + 10 + 2 + 1, 34 = 2 x 14 + 6, 41 = 2 x 14 + 10 + 2 + 1 --
-    the remainder takes one shorter tile launch (K = 2 mod 4), then two-iteration
-    and single launches: the oracle's iterates bit for bit, and a target met
-    inside the shorter launch is replayed from that launch's own inputs."""
+    """K = 14: 24 = 10 + 14, 27 = 14 + 10 + 2 + 1, 34 = 10 + 10 + 14, 41 = 14 + 14 + 10 + 2 + 1 --
+    a remainder of 6 or more takes its own tile launch (K = 2 mod 4, the
+    iterations spread evenly), the rest two-iteration and single launches: the
+    oracle's iterates bit for bit, and a target met inside a shorter launch is
+    replayed from that launch's own inputs."""
     need_cuda()
     from paper_1503_03520_b200 import l1bench
 
