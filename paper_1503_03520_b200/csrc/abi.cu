@@ -264,7 +264,6 @@ void fill_stage_tab(StageTab& tab, const std::vector<int32_t>& off, const std::v
     tab.offset[k] = off[k];
     tab.c[k] = std::cos(th[k]);
     tab.s[k] = std::sin(th[k]);
-    tab.t[k] = tab.s[k] / (1.0 + tab.c[k]);
   }
   tab.cprod = 1.0;
   tab.scaled_ok = 1;

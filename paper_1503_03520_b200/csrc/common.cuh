@@ -68,8 +68,7 @@ struct StageTab {
   int offset[kMaxStages];
   double c[kMaxStages];  // cos(theta) from the host libm (linops.cpp:84-85)
   double s[kMaxStages];
-  double t[kMaxStages];  // tan(theta / 2) = s / (1 + c): the lifting form of the contracted kernels
-  // the scaled form of the tile kernel (contracted arithmetic): a stage is
+  // the scaled form of the contracted arithmetic: a stage is
   // cos(theta) * [[1, -tan], [tan, 1]] on every pair, so G = (prod cos) * M
   // with M two independent fmas per pair; entries a stage leaves unpaired
   // take 1 / cos(theta) instead
@@ -117,34 +116,15 @@ __device__ __forceinline__ void rotate_pair(double& vi, double& vj, double c, do
 // The contracted arithmetic mode (l1b_solver_cfg.arith = L1B_ARITH_FMA): every
 // a*b + c of the hot loop as one fused multiply-add -- one rounding instead of
 // two, so the results are no longer the reference's bits but at least as
-// accurate (parity: <= 1e-12 relative, tests/test_gpu_rc.py, test_gpu_configs.py).  A rotation
-// costs 2 DMUL + 2 DFMA instead of 4 DMUL + 2 DADD.  F = false is the exact
-// (bit-identical) arithmetic above.
+// accurate (parity: <= 1e-12 relative, tests/test_gpu_rc.py, test_gpu_configs.py) --
+// and every rotation in the scaled form below.  rot<false> is the exact
+// (bit-identical) rotate_pair; rot<true> exists for the call sites' dead
+// branches only (they take rot_scaled).
 template <bool F>
 __device__ __forceinline__ void rot(double& vi, double& vj, double c, double s, bool transposed) {
-  if (!F) {
-    rotate_pair(vi, vj, c, s, transposed);
-    return;
-  }
-  // contracted arithmetic: the rotation as three shears (lifting,
-  // R(theta) = L(-t) U(s) L(-t), t = tan(theta / 2)): three dependent FMAs
-  // instead of two products and two FMAs.  `c` carries t here (the callers
-  // pass StageTab::t in this mode).
-  const double t = c;
-  double a = vi, b = vj;
-  if (transposed) {  // R(-theta)
-    a = __fma_rn(t, b, a);
-    b = __fma_rn(-s, a, b);
-    a = __fma_rn(t, b, a);
-  } else {
-    a = __fma_rn(-t, b, a);
-    b = __fma_rn(s, a, b);
-    a = __fma_rn(-t, b, a);
-  }
-  vi = a;
-  vj = b;
+  rotate_pair(vi, vj, c, s, transposed);
 }
-// The scaled form of a rotation (contracted arithmetic, tile kernel):
+// The scaled form of a rotation (contracted arithmetic):
 // [[1, -tn], [tn, 1]] (transposed: tn -> -tn), two independent fmas; the
 // factor cos(theta) is carried by the caller (StageTab::cprod).
 __device__ __forceinline__ void rot_scaled(double& vi, double& vj, double tn, bool transposed) {

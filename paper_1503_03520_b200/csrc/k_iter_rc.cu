@@ -158,19 +158,30 @@ __device__ __forceinline__ void load_seg(const RcArgs& A, int64_t e, bool full, 
 template <int S, bool TR, bool INTERIOR, int K, int PAR, bool F = false>
 __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
                                        const StageTab& tab) {
+  // F: the scaled form of the contracted arithmetic (rot_scaled; the caller's
+  // sigma carries prod cos(theta), entries a stage leaves unpaired take
+  // 1 / cos(theta)) -- wchainv's operations at 4 entries per lane
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int s = TR ? k : S - 1 - k;  // A x: forward, transposed; A^T: reverse, plain
     const int o = tab.offset[s];
-    const double c = F ? tab.t[s] : tab.c[s], sn = tab.s[s];  // (F: the lifting form)
+    const double c = F ? tab.tn[s] : tab.c[s], sn = F ? tab.ic[s] : tab.s[s];
     const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
+    auto pair = [&](double& a, double& b, bool ok) {
+      if (F) {
+        if (ok) rot_scaled(a, b, c, TR);
+        else a *= sn, b *= sn;
+      } else if (ok) {
+        rotate_pair(a, b, c, sn, TR);
+      }
+    };
     if (par == 0) {
       const bool p0 = INTERIOR || (e0 >= o && e0 + 1 < n);
       const bool p2 = INTERIOR || (e0 + 2 >= o && e0 + 3 < n);
 #pragma unroll
       for (int q = 0; q < K; ++q) {
-        if (p0) rot<F>(v[q][0], v[q][1], c, sn, TR);
-        if (p2) rot<F>(v[q][2], v[q][3], c, sn, TR);
+        pair(v[q][0], v[q][1], p0);
+        pair(v[q][2], v[q][3], p2);
       }
     } else {
       // the pair straddling lanes l, l+1 is rotated once, by lane l, which
@@ -184,7 +195,12 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         double a = v[q][3], b = right[q];
-        if (p3) rot<F>(a, b, c, sn, TR);
+        if (F) {
+          if (p3) rot_scaled(a, b, c, TR);
+          else a *= sn;
+        } else if (p3) {
+          rotate_pair(a, b, c, sn, TR);
+        }
         v[q][3] = a;
         back[q] = b;
       }
@@ -192,10 +208,10 @@ __device__ __forceinline__ void wchain(double (&v)[K][4], int64_t e0, int64_t n,
       for (int q = 0; q < K; ++q) {
         const double b = __shfl_up_sync(kFull, back[q], 1);  // lane-1's right output
         if (pm) v[q][0] = b;
+        else if (F) v[q][0] *= sn;
       }
 #pragma unroll
-      for (int q = 0; q < K; ++q)
-        if (p1) rot<F>(v[q][1], v[q][2], c, sn, TR);
+      for (int q = 0; q < K; ++q) pair(v[q][1], v[q][2], p1);
     }
   }
 }
@@ -370,15 +386,15 @@ struct Rc2Out {
 template <int S, bool TR, bool INTERIOR, int K, int PAR, int V, bool F, bool SC = false, bool SYM = false>
 __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n,
                                         const StageTab& tab) {
-  // SC (with F): the scaled form -- every pair takes [[1, -tan], [tan, 1]] and
-  // the caller carries prod cos(theta); an entry a stage leaves unpaired (the
-  // ends of [0, n)) takes 1 / cos(theta).  Otherwise F: lifting, !F: exact.
-  static_assert(!SC || F, "the scaled form belongs to the contracted arithmetic");
+  // SC (= F): the scaled form of the contracted arithmetic -- every pair takes
+  // [[1, -tan], [tan, 1]] and the caller's sigma carries prod cos(theta); an
+  // entry a stage leaves unpaired (the ends of [0, n)) takes 1 / cos(theta).
+  static_assert(SC == F, "contracted arithmetic <=> scaled form");
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     const int s = TR ? k : S - 1 - k;
     const int o = tab.offset[s];
-    const double c = SC ? tab.tn[s] : F ? tab.t[s] : tab.c[s];  // (F: the lifting form)
+    const double c = SC ? tab.tn[s] : tab.c[s];
     const double sn = SC ? tab.ic[s] : tab.s[s];
     const int par = PAR >= 0 ? (PAR >> s) & 1 : (o & 1);
     if (par == 0) {
@@ -419,7 +435,7 @@ __device__ __forceinline__ void wchainv(double (&v)[K][V], int64_t e0, int64_t n
           }
         }
       } else {
-        // (lifting form) the pair straddling lanes l, l+1 is rotated once, by lane l, which
+        // the pair straddling lanes l, l+1 is rotated once, by lane l, which
         // hands the right output back (one rotation fewer per lane and odd stage
         // than rotating it on both sides)
         double right[K], back[K];

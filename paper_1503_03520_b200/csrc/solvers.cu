@@ -148,7 +148,7 @@ struct l1b_session {
   // contracted arithmetic: honoured where every rotation stage has
   // |cos(theta)| >= 1/4 (the scaled form of the two-iteration and tile
   // kernels, StageTab::scaled_ok); steeper stages keep the exact arithmetic.
-  // opf = the operator with sigma * prod cos(theta) as its sigma (those kernels' view)
+  // opf = the operator with sigma * prod cos(theta) as its sigma (the contracted kernels' view)
   bool fma() const { return cfg.arith == L1B_ARITH_FMA && v.op->right.scaled_ok != 0; }
   OpView opf;
   const OpView& op2() const { return fma() ? opf : *v.op; }
@@ -196,7 +196,7 @@ struct l1b_session {
   void iterate(uint64_t j, cudaStream_t stream, bool flush = false) const {
     const uint64_t lo = shard ? v.row_begin : 0, hi = shard ? v.row_end : v.n;
     if (recompute)
-      fista_rc_iter(*v.op, iter_bufs(j), lo, hi, stream, flush, flush ? PeerViews() : peers(j), fma());
+      fista_rc_iter(op2(), iter_bufs(j), lo, hi, stream, flush, flush ? PeerViews() : peers(j), fma());
     else
       fista_fused_iter(*v.op, iter_bufs(j), lo, hi, stream);
   }
