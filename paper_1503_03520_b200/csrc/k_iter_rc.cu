@@ -1182,10 +1182,10 @@ void launch_rc_flush(const RcArgs& a, cudaStream_t st) {
 #define TB_V 8  // entries per lane
 #endif
 constexpr int kTbWarps = TB_WARPS, kTbThreads = 32 * kTbWarps, kTbV = TB_V;
-// contracted arithmetic: rotations in the scaled form (the two-iteration
-// kernel keeps the lifting form).  Exact arithmetic: each lane forms its own
-// output of a straddling pair (one shuffle deep, +0.5 %; the scaled form
-// measured 1 % slower that way and shuffles the rotated value back instead).
+// contracted arithmetic: rotations in the scaled form, as in the other two
+// kernels.  Exact arithmetic: each lane forms its own output of a straddling
+// pair (one shuffle deep, +0.5 %; the scaled form measured 1 % slower that way
+// and shuffles the rotated value back instead).
 constexpr bool kTbScaled = true, kTbSym = true, kTbSymF = false;
 constexpr int kTbCtas = (kTbV <= 8 ? 512 : 256) / kTbThreads;  // resident CTAs per SM (128 registers per thread at 8 entries per lane)
 template <int S>
