@@ -204,10 +204,10 @@ def roofline_tile(t, info, stages, fp64_peak, fp64_src, hbm_peak, hbm_src):
             "launch_ms_source": "CUDA events around every launch of the timed region",
             "launch_ms_long_run": ms_long, "achieved_long_run": flops / (ms_long * 1e-3) / 1e12,
             "traffic": traffic,
-            "limiter": ("instruction issue at IPC 2.06 (issue slots 51.6 % busy, FP64 pipe 44.8 %): per iteration a "
+            "limiter": ("instruction issue at IPC 2.05 (issue slots 51.3 % busy, FP64 pipe 44.5 %): per iteration a "
                         "thread issues ~315 instructions for its 8 entries, 148 of them FP64; stalls: fixed-latency "
                         "dependencies, shuffle / shared-memory latency, the block barrier of the halo exchange "
-                        "(profiles/r2_ncu_full_fista_tb3.txt, fma build); DRAM 6.43 GB per launch = 1.00 x 48n; the "
+                        "(profiles/r2_ncu_full_fista_tb3.txt, fma build); DRAM 6.44 GB per launch = 1.00 x 48n; the "
                         "pipe also carries the halo entries' work (own 240 of 256 per warp window, kept 1712 of 1920 per tile)"),
             "note": ("temporal blocking took the HBM bytes out of the iteration (48n bytes per 14 iterations instead "
                      "of per 2): this kernel is not HBM-bound, so its roofline is the FP64 one and roofline.hbm only "
