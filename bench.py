@@ -151,9 +151,11 @@ def time_path(inst, op, args, prof_iters=100, arith="exact"):
     kmode = sess.kernel_mode()
     tile = sess.tile_geometry() if kmode == 6 else None
     plan, plan_long = (sess.tile_plan(args.steps), sess.tile_plan(prof_iters)) if tile else ([], [])
-    if tile and not (plan and plan_long):  # fewer than 6 iterations: no tile launch ran
+    if tile and not (plan and plan_long):  # fewer than 6 timed iterations: two-iteration launches only
         tile = None
         kmode = 4
+        kms = [kms[1], 0.0]  # (a tile session files those launches in the second slot)
+        kms_long = [kms[0] * prof_iters / args.steps, 0.0]
     sess.end()
     out = {"ms_step": ms_total / args.steps, "ips": 1000.0 * args.steps / ms_total,
            "k1_ms": kms[0] / args.steps, "k2_ms": kms[1] / args.steps, "launches": int(launches),
