@@ -457,6 +457,8 @@ int l1b_session_tile_geometry(l1b_session* s, int* iters, int64_t* span, int64_t
  * fewer than 6 left over go to two-iteration / single launches): up to `cap`
  * launch lengths into ks, their number into *count.  (Measurement only.) */
 int l1b_session_tile_plan(l1b_session* s, uint64_t iters, int* ks, int cap, int* count);
+/* The same plan without a session, for K = kmax iterations per launch (host arithmetic only). */
+int l1b_tile_plan(int kmax, uint64_t iters, int* ks, int cap, int* count);
 /* Dense FP64 fma throughput of `device` in TFLOP/s (a probe kernel of
  * independent fma chains; measurement only, no reference counterpart): the
  * denominator of the FP64-bound kernels' roofline in bench.py. */

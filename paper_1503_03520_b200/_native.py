@@ -163,6 +163,7 @@ SIGNATURES = [
     ("l1b_session_kernel_mode", C.c_int, [vp, P(C.c_int)]),
     ("l1b_session_tile_geometry", C.c_int, [vp, P(C.c_int), P(C.c_int64), P(C.c_int64)]),
     ("l1b_session_tile_plan", C.c_int, [vp, C.c_uint64, P(C.c_int), C.c_int, P(C.c_int)]),
+    ("l1b_tile_plan", C.c_int, [C.c_int, C.c_uint64, P(C.c_int), C.c_int, P(C.c_int)]),
     ("l1b_fp64_peak", C.c_int, [C.c_int, P(f64)]),
     ("l1b_session_restart", C.c_int, [vp]),
     ("l1b_session_read", C.c_int, [vp, P(Sample), u64, P(Summary), P(f64)]),

@@ -66,6 +66,24 @@ PinnedCache& pinned_cache() {
 }
 void pinned_release(void* p) { pinned_cache().put(p); }
 
+// (see l1b_session::tile_plan) kmax = the session's iterations per tile launch, 0: no tiles
+static std::vector<int> plan_tile_launches(int kmax_, uint64_t iters) {
+  std::vector<int> ks;
+  if (kmax_ <= 0) return ks;
+  const uint64_t kmax = (uint64_t)kmax_, kmin = std::min<uint64_t>(6, kmax);  // (K = 2: tests)
+  uint64_t l = iters / kmax + (iters % kmax >= kmin ? 1 : 0), r = iters;
+  for (; l > 0 && r >= kmin; --l) {
+    uint64_t k = std::min((r + l - 1) / l, kmax);
+    const uint64_t down = (k + 2) % 4;  // to the next value = 2 mod 4 below
+    k = k > down ? k - down : kmin;
+    k = std::max(k, kmin);
+    if (k > r) break;
+    ks.push_back((int)k);
+    r -= k;
+  }
+  return ks;
+}
+
 struct l1b_session {
   l1b_problem* prob = nullptr;
   ProblemView v;
@@ -170,22 +188,7 @@ struct l1b_session {
   // two-iteration / single launches).  A remainder of 6 or more gets its own
   // launch and the iterations are spread evenly (20 = 10 + 10, not 14 + 6: a
   // launch costs a tile start, and a short one keeps less of its tiles).
-  std::vector<int> tile_plan(uint64_t iters) const {
-    std::vector<int> ks;
-    if (!tbk) return ks;
-    const uint64_t kmax = (uint64_t)tbk, kmin = std::min<uint64_t>(6, kmax);  // (K = 2: tests)
-    uint64_t l = iters / kmax + (iters % kmax >= kmin ? 1 : 0), r = iters;
-    for (; l > 0 && r >= kmin; --l) {
-      uint64_t k = std::min((r + l - 1) / l, kmax);
-      const uint64_t down = (k + 2) % 4;  // to the next value = 2 mod 4 below
-      k = k > down ? k - down : kmin;
-      k = std::max(k, kmin);
-      if (k > r) break;
-      ks.push_back((int)k);
-      r -= k;
-    }
-    return ks;
-  }
+  std::vector<int> tile_plan(uint64_t iters) const { return plan_tile_launches(tbk, iters); }
 
   void iterate2(uint64_t j, cudaStream_t stream) const {
     const int64_t lo = shard ? (int64_t)v.row_begin : 0;
@@ -680,6 +683,16 @@ int l1b_session_tile_plan(l1b_session* s, uint64_t iters, int* ks, int cap, int*
   return guard([&] {
     if (!s || !count || (cap > 0 && !ks)) throw InvalidArgument("null argument");
     const std::vector<int> plan = s->tile_plan(iters);
+    *count = (int)plan.size();
+    for (int i = 0; i < cap && i < (int)plan.size(); ++i) ks[i] = plan[(size_t)i];
+  });
+}
+
+int l1b_tile_plan(int kmax, uint64_t iters, int* ks, int cap, int* count) {
+  return guard([&] {
+    if (!count || (cap > 0 && !ks)) throw InvalidArgument("null argument");
+    if (kmax < 0 || (kmax > 0 && kmax % 4 != 2)) throw InvalidArgument("tile plan: K must be 2 mod 4");
+    const std::vector<int> plan = plan_tile_launches(kmax, iters);
     *count = (int)plan.size();
     for (int i = 0; i < cap && i < (int)plan.size(); ++i) ks[i] = plan[(size_t)i];
   });

@@ -104,3 +104,47 @@ def test_solver_cfg_default_takes_the_arithmetic_from_the_environment():
         os.environ.pop("L1B_ARITH", None)
         if old is not None:
             os.environ["L1B_ARITH"] = old
+
+
+def _plan_mirror(kmax, iters):
+    ks, kmin = [], min(6, kmax)
+    launches, r = iters // kmax + (1 if iters % kmax >= kmin else 0), iters
+    while launches > 0 and r >= kmin:
+        k = min((r + launches - 1) // launches, kmax)
+        down = (k + 2) % 4
+        k = max(k - down if k > down else kmin, kmin)
+        if k > r:
+            break
+        ks.append(k)
+        r -= k
+        launches -= 1
+    return ks
+
+
+def test_tile_launch_plan():
+    """l1b_tile_plan: the tile launches a step of `iters` iterations takes --
+    every launch K = 2 mod 4 (the rotation of the four x buffers) and at most
+    kmax, fewer than 6 iterations (kmax for K = 2) left to the two-iteration /
+    single launches, the iterations spread evenly over the launches."""
+    from paper_1503_03520_b200 import _native as N
+
+    lib = N.load()
+
+    def plan(kmax, iters):
+        cap = iters // 2 + 2
+        ks, cnt = (ctypes.c_int * cap)(), ctypes.c_int()
+        assert lib.l1b_tile_plan(kmax, iters, ks, cap, ctypes.byref(cnt)) == 0
+        return [ks[i] for i in range(cnt.value)]
+
+    assert plan(14, 20) == [10, 10] and plan(14, 29) == [14, 14] and plan(14, 5) == []
+    assert sorted(plan(14, 500)) == [10] + [14] * 35 and plan(0, 100) == []
+    for kmax in (2, 6, 10, 14):
+        for iters in list(range(0, 130)) + [499, 500, 501, 1000, 12345]:
+            p = plan(kmax, iters)
+            assert p == _plan_mirror(kmax, iters), (kmax, iters)
+            assert all(k % 4 == 2 and min(6, kmax) <= k <= kmax for k in p)
+            assert 0 <= iters - sum(p) < min(6, kmax) + (4 if kmax > 6 else 0) or not p
+            if p:
+                assert max(p) - min(p) <= 4 or kmax == 14  # spread evenly
+    out = ctypes.c_int()
+    assert lib.l1b_tile_plan(12, 100, None, 0, ctypes.byref(out)) != 0  # K must be 2 mod 4
